@@ -1,0 +1,125 @@
+/*
+ * fs.h — C ABI of the B200-native damped-Fisher Cholesky solve.
+ *
+ * Solves (S^T S + lam I) x = v for a wide score matrix S (n x m, one sample per
+ * row, row-major, leading dimension ldS >= m) by the paper's Algorithm 1:
+ *   W = S S^T + lam I  ->  L = chol(W)  ->  z = L^-T L^-1 (S v)  ->  x = (v - S^T z) / lam
+ *
+ * Every pointer argument named S, v, x, W, L, u, z, y, r is a DEVICE pointer;
+ * every call is ordered on the given CUDA stream (cudaStream_t passed as void*,
+ * NULL = legacy default stream).  No call allocates device memory except
+ * fs_ctx_create.  Plain C types only: no torch, no C++ in the signatures.
+ *
+ * This ABI replaces the numpy/scipy calls of the reference package
+ * (/root/reference/pkg/src/fisher_solve/, cited per entry point below).  The
+ * Python mirror of the reference's public API (solve_chol, solve_svd_eigh,
+ * solve_svd_direct, gram, residual, ...) lives in paper_2310_17556_b200/ and
+ * binds these symbols with ctypes; see INTEGRATION.md.
+ */
+#ifndef FS_H_
+#define FS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FS_OK = 0,
+  FS_EINVAL = 1,      /* bad argument -> Python ValueError (core.py:99-119)            */
+  FS_NOT_PD = 2,      /* Cholesky breakdown -> FactorizationError(pivot) (solvers.py:82-87) */
+  FS_ECUDA = 3,       /* CUDA runtime/driver error                                      */
+  FS_ENOMEM = 4,      /* problem larger than the context was created for               */
+  FS_EUNSUPPORTED = 5 /* e.g. precision mode not available for this dtype              */
+} fs_status;
+
+typedef enum { FS_F32 = 0, FS_F64 = 1 } fs_dtype;
+
+/* How the Gram product S S^T is computed (the only dense contraction). */
+typedef enum {
+  FS_PREC_FP64 = 0,   /* exact-product fp64 FMA (the reference's arithmetic)            */
+  FS_PREC_TF32X3 = 1, /* fp32 input, tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, fp64 drain */
+  FS_PREC_AUTO = 2    /* FP64 for fp64 input, TF32X3 for fp32 input                     */
+} fs_precision;
+
+/* Host-supplied sum-all-reduce over ranks of `count` doubles in device memory,
+ * in place, ordered on `stream`.  NULL = single rank.  Returns 0 on success. */
+typedef int (*fs_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
+
+typedef struct fs_ctx fs_ctx;
+
+/* Version string "fisher-b200 <semver> sm_100a". */
+const char* fs_version(void);
+
+/* Create a context on `device` able to solve problems with n <= n_max and
+ * local column count m <= m_max.  Owns every device workspace (Gram partials,
+ * W/L, GEMV partials, status word).  Replaces nothing in the reference (numpy
+ * allocates per call); it is the B200 analogue of CholWorkspace (solvers.py:57-71). */
+int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max);
+void fs_ctx_destroy(fs_ctx* ctx);
+const char* fs_last_error(const fs_ctx* ctx);
+/* Bytes of device workspace a context for (n, m) owns (feeds WorkspaceMeter, core.py:63-96). */
+size_t fs_workspace_bytes(int64_t n, int64_t m);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t fs_launch_count(const fs_ctx* ctx);
+
+/* ---- stage entry points (parity tests, ncu isolation, multi-rank drivers) ---- */
+
+/* Gram: packed-lower G[i(i+1)/2 + j] = sum_k S[i,k] S[j,k] (+ lam on i == j), fp64.
+ * Replaces core.py:284-289 (numpy A @ A.T -> dsyrk, symmetrize, diagonal shift). */
+int fs_gram_packed(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+                   int64_t ldS, double lam, double* G_packed, void* stream);
+
+/* Row GEMV: u[i] = sum_k S[i,k] w[k], fp64 accumulation, w of type `wdtype`.
+ * Replaces solvers.py:110 (t1 = A @ b) and core.py:297 (A @ x). */
+int fs_gemv_rows(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                 const void* w, int wdtype, double* u, void* stream);
+
+/* Unpack a packed lower Gram into a full row-major n x n matrix (upper zeroed). */
+int fs_unpack_lower(fs_ctx* ctx, const double* G_packed, int64_t n, double add_diag, double* W,
+                    int64_t ldW, void* stream);
+
+/* In-place lower Cholesky of W (row-major, lower triangle read, upper left zero).
+ * Synchronizes `stream`.  On breakdown returns FS_NOT_PD and *pivot = 0-based index
+ * of the first non-positive/NaN pivot (LAPACK info-1).  Replaces solvers.py:74-90 (dpotrf). */
+int fs_potrf(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, int64_t* pivot, void* stream);
+/* Asynchronous variant: leaves the status word on the device (read via fs_status_read). */
+int fs_potrf_async(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, void* stream);
+/* Synchronizes `stream` and returns the device status: 0 ok, else pivot+1. */
+int64_t fs_status_read(fs_ctx* ctx, void* stream);
+
+/* In place: z <- L^-T L^-1 z.  Replaces solvers.py:111 and :114 (two dtrtrs). */
+int fs_trsv_pair(fs_ctx* ctx, const double* L, int64_t n, int64_t ldL, double* z, void* stream);
+
+/* Column GEMV + epilogue: x[k] = (x_prev[k] if accumulate) + (v[k] - sum_i z[i] S[i,k]) / lam.
+ * Replaces solvers.py:122-126 (w = t3 @ A; x = (b - w)/lam) and the refinement x += d (:188). */
+int fs_gemv_cols_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                       const double* z, const void* v, int vdtype, double lam, int accumulate,
+                       double* x, void* stream);
+
+/* Residual tail: r[k] = sum_i y[i] S[i,k] + lam x[k] - v[k] (y = S x), and
+ * sums[0] += ||r||^2, sums[1] += ||v||^2 (deterministic, fp64).  r may be NULL.
+ * Replaces core.py:297 ((A@x)@A + lam*x) and core.py:319-321 (norms). */
+int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                     const double* y, const double* x, const void* v, int vdtype, double lam,
+                     double* r, double* sums, void* stream);
+
+/* ---- one-shot solve (the drop-in for solvers.py:151-206) ----
+ * S, v: device, this rank's column shard.  x: device fp64 out (length m).
+ * allreduce: NULL for one rank, else called on [G_packed | u], y and the norm pair.
+ * flags: bit0 = compute residual diagnostics, bit1 = allow the reference's one-step
+ * refinement (solvers.py:183-194) when rel_residual > refine_above.
+ * out_res: host double[2] = {abs_residual, rel_residual} (if bit0).  Synchronizes. */
+#define FS_FLAG_RESIDUAL 1
+#define FS_FLAG_REFINE 2
+int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+                  int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
+                  void* allreduce_user, int flags, double refine_above, int64_t* pivot,
+                  double* out_res, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FS_H_ */

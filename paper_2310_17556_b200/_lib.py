@@ -1,0 +1,129 @@
+"""ctypes binding of libfisher_b200.so (the C ABI declared in include/fs.h).
+
+There is no CPU fallback: importing the solver entry points without the built
+library, or calling them without a CUDA device, raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfisher_b200.so")
+
+FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED = range(6)
+FS_F32, FS_F64 = 0, 1
+FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO = 0, 1, 2
+FS_FLAG_RESIDUAL, FS_FLAG_REFINE = 1, 2
+
+_c_int64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _c_int64, _vp, _vp)
+
+# name -> (restype, argtypes); must match include/fs.h exactly
+SIGNATURES = {
+    "fs_version": (ctypes.c_char_p, []),
+    "fs_ctx_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, _c_int64, _c_int64]),
+    "fs_ctx_destroy": (None, [_vp]),
+    "fs_last_error": (ctypes.c_char_p, [_vp]),
+    "fs_workspace_bytes": (ctypes.c_size_t, [_c_int64, _c_int64]),
+    "fs_launch_count": (_c_int64, [_vp]),
+    "fs_gram_packed": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64,
+                                      ctypes.c_double, _vp, _vp]),
+    "fs_gemv_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, ctypes.c_int,
+                                    _vp, _vp]),
+    "fs_unpack_lower": (ctypes.c_int, [_vp, _vp, _c_int64, ctypes.c_double, _vp, _c_int64, _vp]),
+    "fs_potrf": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, ctypes.POINTER(_c_int64), _vp]),
+    "fs_potrf_async": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp]),
+    "fs_status_read": (_c_int64, [_vp, _vp]),
+    "fs_trsv_pair": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp, _vp]),
+    "fs_gemv_cols_solve": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _vp,
+                                          ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp, _vp]),
+    "fs_residual_cols": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _vp, _vp,
+                                        ctypes.c_int, ctypes.c_double, _vp, _vp, _vp]),
+    "fs_chol_solve": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
+                                     ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,
+                                     ctypes.POINTER(_c_int64), _dp, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA extension is missing or unusable; there is deliberately no fallback."""
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the ctypes library with typed signatures."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeLibraryError(
+                f"{path} is missing: build it with `python -m paper_2310_17556_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+class Context:
+    """Owns one fs_ctx (device workspaces) sized for n <= n_max, m <= m_max."""
+
+    def __init__(self, device: int, n_max: int, m_max: int):
+        self.lib = load()
+        self.device = int(device)
+        self.n_max = int(n_max)
+        self.m_max = int(m_max)
+        h = _vp()
+        rc = self.lib.fs_ctx_create(ctypes.byref(h), self.device, self.n_max, self.m_max)
+        if rc != FS_OK:
+            raise NativeLibraryError(f"fs_ctx_create failed with status {rc} (n_max={n_max}, m_max={m_max})")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.fs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_error(self) -> str:
+        return (self.lib.fs_last_error(self.handle) or b"").decode()
+
+    def launches(self) -> int:
+        return int(self.lib.fs_launch_count(self.handle))
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context_for(device: int, n: int, m: int) -> Context:
+    """Return a cached context on `device` large enough for (n, m); grows geometrically."""
+    ctx = _contexts.get(device)
+    if ctx is None or ctx.n_max < n or ctx.m_max < m:
+        n_max = max(n, ctx.n_max if ctx else 0)
+        m_max = max(m, ctx.m_max if ctx else 0)
+        if ctx is not None:
+            ctx.close()
+        ctx = Context(device, n_max, m_max)
+        _contexts[device] = ctx
+    return ctx
+
+
+def release_contexts():
+    for ctx in list(_contexts.values()):
+        ctx.close()
+    _contexts.clear()

@@ -1,0 +1,317 @@
+"""Core types of the damped Fisher system, mirroring fisher_solve.core on B200.
+
+Mirrors /root/reference/pkg/src/fisher_solve/core.py (same names, argument meaning
+and errors).  Differences that make it B200-native:
+
+* ``ScoreMatrix`` keeps the scores resident on a CUDA device (``.tensor``), in the
+  caller's precision when that is float32/float64 (the reference always widens to
+  float64, core.py:108-119; ints/bools still widen to float64).  ``.data`` returns a
+  read-only host copy for code written against the reference.
+* ``gram`` and ``residual`` run on the GPU through the C ABI (include/fs.h); there
+  is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+EPS = float(np.finfo(np.float64).eps)   # core.py:16
+
+
+class ScalarKind(enum.Enum):             # core.py:22-24
+    REAL64 = "real64"
+    REAL32 = "real32"
+    COMPLEX128 = "complex128"
+
+
+class Method(enum.Enum):                 # core.py:27-35
+    CHOL = "chol"
+    SVD_EIGH = "eigh"
+    SVD_DIRECT = "svd"
+    NAIVE = "naive"
+    RVB = "rvb"
+    CG = "cg"
+
+
+class Variant(enum.Enum):                # core.py:38-48
+    PLAIN = "plain"
+    HERMITIAN = "hermitian"
+    REALPART = "realpart"
+
+
+class FactorizationError(RuntimeError):  # core.py:51-60
+    """A factorization broke down; ``pivot`` is the 0-based failing leading minor."""
+
+    def __init__(self, message: str, pivot: int | None = None):
+        super().__init__(message)
+        self.pivot = pivot
+
+
+class WorkspaceMeter:                    # core.py:63-96
+    """Integer bookkeeping of scalar slots a solver allocates (device slots here)."""
+
+    __slots__ = ("current_slots", "peak_slots")
+
+    def __init__(self):
+        self.current_slots = 0
+        self.peak_slots = 0
+
+    def alloc(self, slots: int) -> None:
+        self.current_slots += int(slots)
+        if self.current_slots > self.peak_slots:
+            self.peak_slots = self.current_slots
+
+    def free(self, slots: int) -> None:
+        self.current_slots -= int(slots)
+
+    def peak_bytes(self, itemsize: int = 8) -> int:
+        return self.peak_slots * int(itemsize)
+
+
+def default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _coerce_damping(lam) -> float:       # core.py:99-105
+    if isinstance(lam, bool) or not isinstance(lam, (int, float, np.integer, np.floating)):
+        raise ValueError(f"damping must be a real scalar, got {type(lam).__name__}")
+    lam = float(lam)
+    if not np.isfinite(lam) or lam <= 0.0:
+        raise ValueError(f"damping must be finite and > 0, got {lam}")
+    return lam
+
+
+def _to_device_tensor(a, name: str, device) -> torch.Tensor:
+    """Coerce to a contiguous float32/float64 CUDA tensor and validate finiteness (core.py:108-119)."""
+    if isinstance(a, torch.Tensor):
+        t = a
+        if t.is_complex():
+            raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+    else:
+        arr = np.asarray(a)
+        if np.iscomplexobj(arr):
+            raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
+        if not (np.issubdtype(arr.dtype, np.number) or arr.dtype == np.bool_):
+            raise ValueError(f"{name} must be numeric, got dtype {arr.dtype}")
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+    dev = device if device is not None else (t.device if t.is_cuda else default_device())
+    t = t.to(dev, non_blocking=True).contiguous()
+    if t.numel() and not bool(torch.isfinite(t).all()):
+        raise ValueError(f"{name} must contain only finite entries")
+    return t
+
+
+class ScoreMatrix:
+    """Dense n-by-m score matrix, one sample per row, resident on a CUDA device (core.py:122-162)."""
+
+    def __init__(self, data, device=None):
+        src = data
+        t = _to_device_tensor(data, "score matrix", device)
+        if t.dim() != 2:
+            raise ValueError(f"score matrix must be 2-D, got shape {tuple(t.shape)}")
+        if t.shape[0] < 1 or t.shape[1] < 1:
+            raise ValueError(f"score matrix needs at least one row and column, got {tuple(t.shape)}")
+        if isinstance(src, torch.Tensor) and src.is_cuda and t.data_ptr() == src.data_ptr():
+            t = t.clone()  # freezing must not alias the caller's tensor (core.py:139-140)
+        self._t = t
+        self._host = None
+        # numpy in -> numpy out (drop-in semantics); CUDA tensor in -> CUDA tensor out
+        self.host_origin = not (isinstance(src, torch.Tensor) and src.is_cuda)
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        return self._t
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            h = self._t.cpu().numpy()
+            h.flags.writeable = False
+            self._host = h
+        return self._host
+
+    @property
+    def n(self) -> int:
+        return int(self._t.shape[0])
+
+    @property
+    def m(self) -> int:
+        return int(self._t.shape[1])
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.n, self.m)
+
+    @property
+    def is_complex(self) -> bool:
+        return False
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self._t.dtype
+
+    @property
+    def scalar_kind(self) -> ScalarKind:
+        return ScalarKind.REAL64 if self._t.dtype == torch.float64 else ScalarKind.REAL32
+
+
+class DampedSystem:
+    """The system (S^T S + lam I) x = v (core.py:165-203); v lives beside S in S's dtype."""
+
+    def __init__(self, S: ScoreMatrix, lam, v):
+        if not isinstance(S, ScoreMatrix):
+            S = ScoreMatrix(S)
+        self.S = S
+        self.lam = _coerce_damping(lam)
+        if isinstance(v, torch.Tensor) and v.is_complex() or (not isinstance(v, torch.Tensor) and np.iscomplexobj(np.asarray(v))):
+            raise ValueError("real score matrix with complex right-hand side")
+        t = _to_device_tensor(v, "right-hand side", S.tensor.device)
+        if t.dim() != 1:
+            raise ValueError(f"right-hand side must be 1-D, got shape {tuple(t.shape)}")
+        if t.shape[0] != S.m:
+            raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
+        if isinstance(v, torch.Tensor) and v.is_cuda and t.data_ptr() == v.data_ptr():
+            t = t.clone()
+        self._v = t.to(S.dtype)
+        self._host_v = None
+
+    @property
+    def v_tensor(self) -> torch.Tensor:
+        return self._v
+
+    @property
+    def v(self) -> np.ndarray:
+        if self._host_v is None:
+            h = self._v.cpu().numpy()
+            h.flags.writeable = False
+            self._host_v = h
+        return self._host_v
+
+    @property
+    def n(self) -> int:
+        return self.S.n
+
+    @property
+    def m(self) -> int:
+        return self.S.m
+
+
+@dataclass(frozen=True)
+class Solution:                          # core.py:206-223
+    x: object          # numpy float64 (host systems) or a CUDA float64 tensor (device systems)
+    method: Method
+    abs_residual: float
+    rel_residual: float
+    wall_seconds: float
+    iterations: int | None = None
+    converged: bool = True
+    precision: str = "fp64"
+
+
+def _dt(t: torch.Tensor) -> int:
+    return _lib.FS_F64 if t.dtype == torch.float64 else _lib.FS_F32
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check(ctx, rc: int, what: str):
+    if rc == _lib.FS_OK:
+        return
+    msg = f"{what}: {ctx.last_error()} (status {rc})"
+    if rc in (_lib.FS_EINVAL, _lib.FS_EUNSUPPORTED):
+        raise ValueError(msg)
+    raise _lib.NativeLibraryError(msg)
+
+
+PRECISIONS = {"fp64": _lib.FS_PREC_FP64, "tf32x3": _lib.FS_PREC_TF32X3, "auto": _lib.FS_PREC_AUTO}
+
+
+def resolve_precision(precision: str, dtype: torch.dtype) -> str:
+    if precision not in PRECISIONS:
+        raise ValueError(f"unknown precision {precision!r}; expected one of {sorted(PRECISIONS)}")
+    if precision == "auto":
+        return "tf32x3" if dtype == torch.float32 else "fp64"
+    if precision == "tf32x3" and dtype != torch.float32:
+        raise ValueError("precision 'tf32x3' needs float32 scores")
+    return precision
+
+
+def gram_packed(S: ScoreMatrix, lam: float, precision: str = "auto") -> torch.Tensor:
+    """Packed lower W = S S^T + lam I on the device (fp64, length n(n+1)/2)."""
+    t = S.tensor
+    n, m = S.n, S.m
+    prec = resolve_precision(precision, t.dtype)
+    ctx = _lib.context_for(t.device.index, n, m)
+    out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
+    rc = ctx.lib.fs_gram_packed(ctx.handle, _dt(t), PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0),
+                                float(lam), out.data_ptr(), _stream(t.device))
+    _check(ctx, rc, "fs_gram_packed")
+    return out
+
+
+def gram(S: ScoreMatrix, lam: float, meter: WorkspaceMeter | None = None, precision: str = "auto") -> np.ndarray:
+    """Damped Gram matrix W = S S^T + lam I, n-by-n, exactly symmetric (core.py:270-290)."""
+    lam = _coerce_damping(lam)
+    n = S.n
+    if meter is not None:
+        meter.alloc(n * (n + 1) // 2)
+    packed = gram_packed(S, lam, precision).cpu().numpy()
+    W = np.zeros((n, n))
+    W[np.tril_indices(n)] = packed
+    W = W + np.tril(W, -1).T   # mirror: exactly symmetric by construction
+    if meter is not None:
+        meter.alloc(n * n)
+        meter.free(n * (n + 1) // 2)
+    return W
+
+
+def residual_device(system: DampedSystem, x: torch.Tensor) -> tuple[float, float]:
+    """||(S^T S + lam I) x - v|| and its relative value, fp64 on the device (core.py:307-322)."""
+    S = system.S.tensor
+    n, m = system.n, system.m
+    ctx = _lib.context_for(S.device.index, n, m)
+    st = _stream(S.device)
+    y = torch.empty(n, dtype=torch.float64, device=S.device)
+    sums = torch.empty(2, dtype=torch.float64, device=S.device)
+    rc = ctx.lib.fs_gemv_rows(ctx.handle, _dt(S), S.data_ptr(), n, m, S.stride(0), x.data_ptr(), _lib.FS_F64,
+                              y.data_ptr(), st)
+    _check(ctx, rc, "fs_gemv_rows")
+    v = system.v_tensor
+    rc = ctx.lib.fs_residual_cols(ctx.handle, _dt(S), S.data_ptr(), n, m, S.stride(0), y.data_ptr(), x.data_ptr(),
+                                  v.data_ptr(), _dt(v), system.lam, None, sums.data_ptr(), st)
+    _check(ctx, rc, "fs_residual_cols")
+    rr, vv = sums.cpu().tolist()
+    abs_res = float(np.sqrt(rr))
+    return abs_res, abs_res / max(float(np.sqrt(vv)), EPS)
+
+
+def residual(system: DampedSystem, x, variant: Variant = Variant.PLAIN) -> tuple[float, float]:
+    """Absolute and relative residual of x (core.py:307-322), evaluated on the GPU."""
+    if not isinstance(variant, Variant):
+        raise ValueError(f"unknown operator variant: {variant!r}")
+    if variant is not Variant.PLAIN:
+        raise ValueError("the B200 path implements the PLAIN (real) operator only")
+    if isinstance(x, torch.Tensor):
+        xt = x.to(system.S.tensor.device, torch.float64).contiguous()
+    else:
+        xa = np.asarray(x)
+        if xa.ndim != 1 or xa.shape[0] != system.m:
+            raise ValueError(f"solution vector has shape {xa.shape}, expected ({system.m},)")
+        xt = torch.from_numpy(np.ascontiguousarray(xa, dtype=np.float64)).to(system.S.tensor.device)
+    if xt.dim() != 1 or xt.shape[0] != system.m:
+        raise ValueError(f"solution vector has shape {tuple(xt.shape)}, expected ({system.m},)")
+    return residual_device(system, xt)

@@ -1,0 +1,375 @@
+// api.cu — the extern "C" boundary declared in include/fs.h.
+//
+// The one-shot fs_chol_solve is the drop-in for _solve_chol_impl (solvers.py:151-194):
+//   gram (core.py:270-290) -> potrf (solvers.py:74-90) -> _chol_apply (solvers.py:101-127)
+//   -> first-pass residual (solvers.py:160-170) -> optional one-step refinement (:183-194).
+// Stream-ordered; one host synchronisation at the end to read the pivot/status word and
+// the residual norms.  Multi-rank: the caller's allreduce sums [G_packed | u], y and the
+// norm pair; everything else is rank-local (column-sharded S, v, x).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/fs.h"
+#include "kernels.h"
+
+struct fs_ctx {
+  int device = 0;
+  int num_sms = 148;
+  int64_t n_max = 0, m_max = 0;
+  double* d_packed = nullptr;   // n(n+1)/2 packed Gram | n u   (the all-reduce buffer)
+  double* d_W = nullptr;        // n x n, becomes L in place
+  double* d_z = nullptr;        // n
+  double* d_y = nullptr;        // n
+  double* d_partials = nullptr; // row-GEMV chunk partials
+  double* d_block_sums = nullptr;
+  double* d_sums = nullptr;     // 4
+  double* d_r = nullptr;        // m (negated residual, refinement right-hand side)
+  double* d_syrk_ws = nullptr;
+  int64_t* d_status = nullptr;
+  int64_t* h_status = nullptr;  // pinned
+  double* h_sums = nullptr;     // pinned
+  size_t ws_bytes = 0;
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+const double kEps = 2.220446049250313e-16;  // core.py:16
+
+size_t packed_len(int64_t n) { return (size_t)(n * (n + 1) / 2 + n); }
+
+struct Sizes {
+  size_t packed, W, vec, partials, block_sums, r, syrk;
+};
+
+Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
+  Sizes s;
+  s.packed = packed_len(n) * sizeof(double);
+  s.W = (size_t)n * n * sizeof(double);
+  s.vec = (size_t)n * sizeof(double);
+  s.partials = (size_t)fs::gemv_rows_chunks(m, true) * n * sizeof(double);
+  s.block_sums = (size_t)fs::residual_cols_blocks(m, true) * 2 * sizeof(double);
+  s.r = (size_t)m * sizeof(double);
+  s.syrk = std::max(fs::syrk_simt_workspace_bytes(n, m, num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
+  return s;
+}
+
+int fail(fs_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(fs_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, FS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define FS_CK(expr, where)                          \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, where); \
+  } while (0)
+
+int check_shape(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS) {
+  if (!ctx) return FS_EINVAL;
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(ctx, FS_EINVAL, "dtype must be FS_F32 or FS_F64");
+  if (!S) return fail(ctx, FS_EINVAL, "S is NULL");
+  if (n < 1 || m < 1) return fail(ctx, FS_EINVAL, "score matrix needs at least one row and column");
+  if (ldS < m) return fail(ctx, FS_EINVAL, "ldS must be >= m");
+  if (n > ctx->n_max || m > ctx->m_max) return fail(ctx, FS_ENOMEM, "problem exceeds the context's n_max/m_max");
+  return FS_OK;
+}
+
+int check_lam(fs_ctx* ctx, double lam) {
+  if (!(lam > 0.0) || !isfinite(lam)) return fail(ctx, FS_EINVAL, "damping must be finite and > 0");
+  return FS_OK;
+}
+
+int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t ldS, int* use_tc) {
+  *use_tc = 0;
+  if (precision == FS_PREC_FP64) return FS_OK;
+  if (precision == FS_PREC_TF32X3 || precision == FS_PREC_AUTO) {
+    if (dtype != FS_F32) {
+      if (precision == FS_PREC_AUTO) return FS_OK;
+      return fail(ctx, FS_EUNSUPPORTED, "TF32X3 precision needs fp32 scores");
+    }
+    if (!fs::syrk_tc_supported(S, ldS)) {
+      if (precision == FS_PREC_AUTO) return FS_OK;
+      return fail(ctx, FS_EINVAL, "TF32X3 needs a 16-byte aligned S with ldS*4 % 16 == 0");
+    }
+    *use_tc = 1;
+    return FS_OK;
+  }
+  return fail(ctx, FS_EINVAL, "unknown precision mode");
+}
+
+int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+              int64_t ldS, double lam, double* Gp, cudaStream_t st) {
+  int use_tc = 0;
+  int rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc);
+  if (rc) return rc;
+  int l = 0;
+  cudaError_t e = use_tc ? fs::syrk_tc((const float*)S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l)
+                         : fs::syrk_simt(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gram");
+  return FS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fs_version(void) { return "fisher-b200 0.1.0 sm_100a"; }
+
+size_t fs_workspace_bytes(int64_t n, int64_t m) {
+  Sizes s = sizes_for(n, m, 148);
+  return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + s.r + s.syrk +
+         sizeof(int64_t);
+}
+
+int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
+  if (!out || n_max < 1 || m_max < 1) return FS_EINVAL;
+  *out = nullptr;
+  fs_ctx* ctx = new fs_ctx();
+  ctx->device = device;
+  ctx->n_max = n_max;
+  ctx->m_max = m_max;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete ctx; return FS_ECUDA; }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  if (sms > 0) ctx->num_sms = sms;
+  Sizes s = sizes_for(n_max, m_max, ctx->num_sms);
+  bool ok = true;
+  auto A = [&](void** p, size_t b) { if (ok && cudaMalloc(p, std::max<size_t>(b, 16)) != cudaSuccess) ok = false; };
+  A((void**)&ctx->d_packed, s.packed);
+  A((void**)&ctx->d_W, s.W);
+  A((void**)&ctx->d_z, s.vec);
+  A((void**)&ctx->d_y, s.vec);
+  A((void**)&ctx->d_partials, s.partials);
+  A((void**)&ctx->d_block_sums, s.block_sums);
+  A((void**)&ctx->d_sums, 4 * sizeof(double));
+  A((void**)&ctx->d_r, s.r);
+  A((void**)&ctx->d_syrk_ws, s.syrk);
+  A((void**)&ctx->d_status, sizeof(int64_t));
+  if (ok && cudaMallocHost((void**)&ctx->h_status, sizeof(int64_t)) != cudaSuccess) ok = false;
+  if (ok && cudaMallocHost((void**)&ctx->h_sums, 4 * sizeof(double)) != cudaSuccess) ok = false;
+  if (!ok) {
+    cudaGetLastError();
+    fs_ctx_destroy(ctx);
+    return FS_ENOMEM;
+  }
+  ctx->ws_bytes = fs_workspace_bytes(n_max, m_max);
+  cudaMemset(ctx->d_status, 0, sizeof(int64_t));
+  *out = ctx;
+  return FS_OK;
+}
+
+void fs_ctx_destroy(fs_ctx* ctx) {
+  if (!ctx) return;
+  cudaFree(ctx->d_packed); cudaFree(ctx->d_W); cudaFree(ctx->d_z); cudaFree(ctx->d_y);
+  cudaFree(ctx->d_partials); cudaFree(ctx->d_block_sums); cudaFree(ctx->d_sums);
+  cudaFree(ctx->d_r); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
+  if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
+  delete ctx;
+}
+
+const char* fs_last_error(const fs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t fs_launch_count(const fs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fs_gram_packed(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+                   int64_t ldS, double lam, double* G_packed, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if (!(lam >= 0.0) || !isfinite(lam)) return fail(ctx, FS_EINVAL, "diagonal shift must be finite and >= 0");
+  if (!G_packed) return fail(ctx, FS_EINVAL, "G_packed is NULL");
+  return gram_impl(ctx, dtype, precision, S, n, m, ldS, lam, G_packed, (cudaStream_t)stream);
+}
+
+int fs_gemv_rows(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                 const void* w, int wdtype, double* u, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if (!w || !u) return fail(ctx, FS_EINVAL, "NULL vector");
+  int l = 0;
+  cudaError_t e = fs::gemv_rows(dtype == FS_F64, S, n, m, ldS, w, wdtype == FS_F64, ctx->d_partials, u,
+                                (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_rows");
+  return FS_OK;
+}
+
+int fs_unpack_lower(fs_ctx* ctx, const double* G_packed, int64_t n, double add_diag, double* W,
+                    int64_t ldW, void* stream) {
+  if (!ctx || !G_packed || !W || n < 1 || ldW < n) return fail(ctx, FS_EINVAL, "bad unpack arguments");
+  int l = 0;
+  cudaError_t e = fs::unpack_lower(G_packed, n, add_diag, W, ldW, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "unpack_lower");
+  return FS_OK;
+}
+
+int fs_potrf_async(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, void* stream) {
+  if (!ctx || !W || n < 1 || ldW < n) return fail(ctx, FS_EINVAL, "bad potrf arguments");
+  if (n > ctx->n_max) return fail(ctx, FS_ENOMEM, "n exceeds n_max");
+  cudaStream_t st = (cudaStream_t)stream;
+  FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
+  int l = 0;
+  cudaError_t e = fs::potrf_lower(W, n, ldW, ctx->d_status, st, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "potrf");
+  return FS_OK;
+}
+
+int64_t fs_status_read(fs_ctx* ctx, void* stream) {
+  if (!ctx) return -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st) != cudaSuccess) return -1;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+  return *ctx->h_status;
+}
+
+int fs_potrf(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, int64_t* pivot, void* stream) {
+  int rc = fs_potrf_async(ctx, W, n, ldW, stream);
+  if (rc) return rc;
+  const int64_t s = fs_status_read(ctx, stream);
+  if (s < 0) return fail(ctx, FS_ECUDA, "potrf status read failed");
+  if (pivot) *pivot = s > 0 ? s - 1 : -1;
+  if (s > 0) return fail(ctx, FS_NOT_PD, "Gram matrix is not positive definite");
+  return FS_OK;
+}
+
+int fs_trsv_pair(fs_ctx* ctx, const double* L, int64_t n, int64_t ldL, double* z, void* stream) {
+  if (!ctx || !L || !z || n < 1 || ldL < n) return fail(ctx, FS_EINVAL, "bad trsv arguments");
+  int l = 0;
+  cudaError_t e = fs::trsv_pair(L, n, ldL, z, nullptr, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
+  return FS_OK;
+}
+
+int fs_gemv_cols_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                       const double* z, const void* v, int vdtype, double lam, int accumulate,
+                       double* x, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if ((rc = check_lam(ctx, lam))) return rc;
+  if (!z || !v || !x) return fail(ctx, FS_EINVAL, "NULL vector");
+  int l = 0;
+  cudaError_t e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, z, v, vdtype == FS_F64, lam,
+                                      accumulate != 0, x, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve");
+  return FS_OK;
+}
+
+int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
+                     const double* y, const double* x, const void* v, int vdtype, double lam,
+                     double* r, double* sums, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if (!y || !x || !v || !sums) return fail(ctx, FS_EINVAL, "NULL vector");
+  int l = 0;
+  cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, y, x, v, vdtype == FS_F64, lam, r,
+                                    ctx->d_block_sums, sums, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
+  return FS_OK;
+}
+
+int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+                  int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
+                  void* allreduce_user, int flags, double refine_above, int64_t* pivot,
+                  double* out_res, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if ((rc = check_lam(ctx, lam))) return rc;
+  if (!v || !x) return fail(ctx, FS_EINVAL, "NULL vector");
+  if (pivot) *pivot = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int vdt = dtype;  // v has the dtype of S
+  double* u = ctx->d_packed + n * (n + 1) / 2;
+  // 1. partial Gram (no shift) and u = S v, packed for one all-reduce
+  if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
+  if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+  if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
+    return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
+  // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
+  if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
+  if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
+  FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
+  {
+    int l = 0;
+    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_z, ctx->d_status, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
+  }
+  // 3. x = (v - S^T z) / lam on the local shard
+  if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
+  const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
+  const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
+  double abs_res = NAN, rel_res = NAN;
+  for (int pass = 0; want_res && pass < 2; ++pass) {
+    // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
+    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
+    if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of y failed");
+    {
+      int l = 0;
+      cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
+                                        want_refine && pass == 0 ? ctx->d_r : nullptr, ctx->d_block_sums,
+                                        ctx->d_sums, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
+    }
+    if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
+    FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
+    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+    if (*ctx->h_status != 0) break;
+    abs_res = sqrt(ctx->h_sums[0]);
+    rel_res = abs_res / std::max(sqrt(ctx->h_sums[1]), kEps);
+    if (pass == 1 || !want_refine || !(rel_res > refine_above)) break;
+    // one correction pass with the same factor (solvers.py:183-194): d = chol_apply(-r)
+    // residual_cols stored r = (S^T y + lam x) - v; refinement right-hand side is -r
+    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream))) return rc;
+    if (allreduce && allreduce(ctx->d_z, n, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
+    {
+      int l = 0;
+      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_z, ctx->d_status, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
+    }
+    // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
+    {
+      int l = 0;
+      cudaError_t e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, ctx->d_z, ctx->d_r, true, -lam,
+                                          true, x, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve (refine)");
+    }
+  }
+  if (!want_res) {
+    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+  }
+  if (*ctx->h_status != 0) {
+    if (pivot) *pivot = *ctx->h_status - 1;
+    return fail(ctx, FS_NOT_PD, "Gram matrix is not positive definite at pivot " + std::to_string(*ctx->h_status - 1));
+  }
+  if (out_res) { out_res[0] = abs_res; out_res[1] = rel_res; }
+  return FS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+// gemv.cu — HBM-bound streaming passes over the score matrix S (n x m, row-major).
+//
+//   gemv_rows        u = S w            (solvers.py:110 "A @ b", core.py:297 "A @ x")
+//   gemv_cols_solve  x = (v - S^T z)/λ  (solvers.py:122-126, fused epilogue; refinement :188)
+//   residual_cols    r = S^T y + λx - v, ||r||², ||v||²   (core.py:297, :319-321)
+//
+// Roofline: each pass reads S once (n·m·s bytes) plus O(m) vectors; the kernels are
+// sized to keep ~32–64 KB of loads in flight per SM (Little's law at ~6.5 TB/s) and
+// use 16-byte L1::no_allocate / L2::evict_first loads.  All reductions are fixed-order
+// (per-chunk partials reduced in chunk order) so results are bit-reproducible.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fs {
+namespace {
+
+constexpr int kRowThreads = 256;   // 8 warps
+constexpr int kRowUnroll = 8;      // vectors per lane per row
+constexpr int kColThreads = 256;
+
+template <typename TS> struct VecOf;
+template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
+template <> struct VecOf<double> { using V = double2; static constexpr int N = 2; };
+
+template <typename T> FS_DEVINL void vec_to_array(const float4& v, T* a) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
+template <typename T> FS_DEVINL void vec_to_array(const double2& v, T* a) { a[0] = v.x; a[1] = v.y; }
+
+template <typename TS>
+constexpr int row_chunk_cols() { return kWarp * VecOf<TS>::N * kRowUnroll; }
+
+// One CTA = one column chunk of width CW; warp w handles rows w, w+8, ...
+// Products: fp32 x fp32 are formed in fp32 and summed per lane (32 terms) before the
+// fp64 warp reduction; any fp64 operand forces exact fp64 products.
+template <typename TS, typename TW, bool kVec>
+__global__ void __launch_bounds__(kRowThreads)
+gemv_rows_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
+                 const TW* __restrict__ w, double* __restrict__ partials) {
+  using VT = typename VecOf<TS>::V;
+  constexpr int VN = VecOf<TS>::N;
+  constexpr int CW = row_chunk_cols<TS>();
+  constexpr bool kF32 = sizeof(TS) == 4 && sizeof(TW) == 4;
+  using Acc = typename std::conditional<kF32, float, double>::type;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * CW;
+  Acc wr[kRowUnroll][VN];
+#pragma unroll
+  for (int u = 0; u < kRowUnroll; ++u)
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      int64_t c = c0 + (int64_t)(u * kWarp + lane) * VN + e;
+      wr[u][e] = c < m ? (Acc)w[c] : (Acc)0;
+    }
+  const bool full = c0 + CW <= m;
+  for (int64_t i = warp; i < n; i += kRowThreads / kWarp) {
+    const TS* row = S + i * ldS + c0;
+    Acc acc = 0;
+    if (kVec && full) {
+      VT buf[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u)
+        buf[u] = ld_stream(reinterpret_cast<const VT*>(row + (u * kWarp + lane) * VN));
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        TS a[VN];
+        vec_to_array(buf[u], a);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc = fma((Acc)a[e], wr[u][e], acc);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          int64_t c = (int64_t)(u * kWarp + lane) * VN + e;
+          if (c0 + c < m) acc = fma((Acc)ld_stream(row + c), wr[u][e], acc);
+        }
+    }
+    double s = warp_sum((double)acc);
+    if (lane == 0) partials[(int64_t)blockIdx.x * n + i] = s;
+  }
+}
+
+// out[i] = sum_{c=0..C-1} partials[c*n + i], fixed order.
+__global__ void reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_t n,
+                                     double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t c = 0; c < chunks; ++c) s += partials[c * n + i];
+  out[i] = s;
+}
+
+// One thread owns VN consecutive columns and walks all n rows.
+template <typename TS, typename TV, bool kVec>
+__global__ void __launch_bounds__(kColThreads)
+gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
+                       const double* __restrict__ z, const TV* __restrict__ v, double lam,
+                       int accumulate, double* __restrict__ x) {
+  using VT = typename VecOf<TS>::V;
+  constexpr int VN = VecOf<TS>::N;
+  constexpr int kZ = 2048;
+  constexpr int kInner = 16;  // fp32 partial sums span 16 rows before folding into fp64
+  using Zt = TS;              // fp32 mode multiplies in fp32 (z rounded once), fp64 mode exact
+  __shared__ Zt zs[kZ];
+  const int64_t col = ((int64_t)blockIdx.x * kColThreads + threadIdx.x) * VN;
+  double acc[VN];
+#pragma unroll
+  for (int e = 0; e < VN; ++e) acc[e] = 0.0;
+  const bool full = kVec && (col + VN <= m);
+  for (int64_t r0 = 0; r0 < n; r0 += kZ) {
+    const int rows = (int)(n - r0 < kZ ? n - r0 : kZ);
+    __syncthreads();
+    for (int t = threadIdx.x; t < rows; t += kColThreads) zs[t] = (Zt)z[r0 + t];
+    __syncthreads();
+    if (col >= m) continue;
+    const TS* base = S + r0 * ldS + col;
+    for (int i0 = 0; i0 < rows; i0 += kInner) {
+      TS part[VN];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) part[e] = 0;
+      const int cnt = min(kInner, rows - i0);
+      if (full && cnt == kInner) {
+        VT buf[kInner];
+#pragma unroll
+        for (int k = 0; k < kInner; ++k)
+          buf[k] = ld_stream(reinterpret_cast<const VT*>(base + (int64_t)(i0 + k) * ldS));
+#pragma unroll
+        for (int k = 0; k < kInner; ++k) {
+          TS a[VN];
+          vec_to_array(buf[k], a);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) part[e] = fma(zs[i0 + k], a[e], part[e]);
+        }
+      } else {
+        for (int k = 0; k < cnt; ++k)
+#pragma unroll
+          for (int e = 0; e < VN; ++e)
+            if (col + e < m) part[e] = fma(zs[i0 + k], ld_stream(base + (int64_t)(i0 + k) * ldS + e), part[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[e] += (double)part[e];
+    }
+  }
+  if (col >= m) return;
+#pragma unroll
+  for (int e = 0; e < VN; ++e) {
+    const int64_t c = col + e;
+    if (c < m) {
+      double xv = ((double)v[c] - acc[e]) / lam;  // true IEEE division (x = v/λ exactly for S = 0)
+      if (accumulate) xv = x[c] + xv;
+      x[c] = xv;
+    }
+  }
+}
+
+// r = S^T y + λx - v with exact fp64 products; per-block ||r||², ||v||² partials.
+template <typename TS, typename TV, bool kVec>
+__global__ void __launch_bounds__(kColThreads)
+residual_cols_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
+                     const double* __restrict__ y, const double* __restrict__ x,
+                     const TV* __restrict__ v, double lam, double* __restrict__ r,
+                     double* __restrict__ block_sums) {
+  using VT = typename VecOf<TS>::V;
+  constexpr int VN = VecOf<TS>::N;
+  constexpr int kZ = 2048;
+  constexpr int kInner = 16;
+  __shared__ double ys[kZ];
+  __shared__ double red[2][kColThreads / kWarp];
+  const int64_t col = ((int64_t)blockIdx.x * kColThreads + threadIdx.x) * VN;
+  double acc[VN];
+#pragma unroll
+  for (int e = 0; e < VN; ++e) acc[e] = 0.0;
+  const bool full = kVec && (col + VN <= m);
+  for (int64_t r0 = 0; r0 < n; r0 += kZ) {
+    const int rows = (int)(n - r0 < kZ ? n - r0 : kZ);
+    __syncthreads();
+    for (int t = threadIdx.x; t < rows; t += kColThreads) ys[t] = y[r0 + t];
+    __syncthreads();
+    if (col >= m) continue;
+    const TS* base = S + r0 * ldS + col;
+    for (int i0 = 0; i0 < rows; i0 += kInner) {
+      const int cnt = min(kInner, rows - i0);
+      if (full && cnt == kInner) {
+        VT buf[kInner];
+#pragma unroll
+        for (int k = 0; k < kInner; ++k)
+          buf[k] = ld_stream(reinterpret_cast<const VT*>(base + (int64_t)(i0 + k) * ldS));
+#pragma unroll
+        for (int k = 0; k < kInner; ++k) {
+          TS a[VN];
+          vec_to_array(buf[k], a);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) acc[e] = fma(ys[i0 + k], (double)a[e], acc[e]);
+        }
+      } else {
+        for (int k = 0; k < cnt; ++k)
+#pragma unroll
+          for (int e = 0; e < VN; ++e)
+            if (col + e < m) acc[e] = fma(ys[i0 + k], (double)ld_stream(base + (int64_t)(i0 + k) * ldS + e), acc[e]);
+      }
+    }
+  }
+  double rr = 0.0, vv = 0.0;
+  if (col < m) {
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      const int64_t c = col + e;
+      if (c < m) {
+        const double vc = (double)v[c];
+        const double rc = (acc[e] + lam * x[c]) - vc;  // ((A@x)@A + lam*x) - v, core.py:297/:319
+        if (r) r[c] = rc;
+        rr += rc * rc;
+        vv += vc * vc;
+      }
+    }
+  }
+  rr = warp_sum(rr);
+  vv = warp_sum(vv);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { red[0][warp] = rr; red[1][warp] = vv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kColThreads / kWarp; ++w) { a += red[0][w]; b += red[1][w]; }
+    block_sums[2 * blockIdx.x] = a;
+    block_sums[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void reduce_pairs_kernel(const double* __restrict__ block_sums, int64_t blocks,
+                                    double* __restrict__ sums) {
+  // one warp, fixed order: lane l sums blocks l, l+32, ...; then a fixed shuffle tree
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < blocks; i += 32) {
+    a += block_sums[2 * i];
+    b += block_sums[2 * i + 1];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (threadIdx.x == 0) { sums[0] = a; sums[1] = b; }
+}
+
+inline bool aligned16(const void* p, int64_t ld, int es) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * es) % 16 == 0);
+}
+
+template <typename TS>
+cudaError_t gemv_rows_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const void* w, bool w_f64,
+                        double* partials, double* u, cudaStream_t st, int* launches) {
+  constexpr int CW = row_chunk_cols<TS>();
+  const int64_t chunks = (m + CW - 1) / CW;
+  const bool vec = aligned16(S, ldS, sizeof(TS));
+  dim3 grid((unsigned)chunks);
+  if (w_f64) {
+    if (vec) gemv_rows_kernel<TS, double, true><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const double*)w, partials);
+    else gemv_rows_kernel<TS, double, false><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const double*)w, partials);
+  } else {
+    if (vec) gemv_rows_kernel<TS, float, true><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
+    else gemv_rows_kernel<TS, float, false><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
+  }
+  reduce_chunks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, chunks, n, u);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+template <typename TS>
+cudaError_t gemv_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const double* z,
+                        const void* v, bool v_f64, double lam, bool accumulate, double* x,
+                        cudaStream_t st, int* launches) {
+  constexpr int VN = VecOf<TS>::N;
+  const int64_t blocks = (m + (int64_t)kColThreads * VN - 1) / ((int64_t)kColThreads * VN);
+  const bool vec = aligned16(S, ldS, sizeof(TS));
+  dim3 grid((unsigned)blocks);
+  const int acc = accumulate ? 1 : 0;
+#define FS_COLS(TV, VEC) gemv_cols_solve_kernel<TS, TV, VEC><<<grid, kColThreads, 0, st>>>(S, n, m, ldS, z, (const TV*)v, lam, acc, x)
+  if (v_f64) { if (vec) FS_COLS(double, true); else FS_COLS(double, false); }
+  else { if (vec) FS_COLS(float, true); else FS_COLS(float, false); }
+#undef FS_COLS
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+template <typename TS>
+cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const double* y,
+                            const double* x, const void* v, bool v_f64, double lam, double* r,
+                            double* block_sums, double* sums, cudaStream_t st, int* launches) {
+  constexpr int VN = VecOf<TS>::N;
+  const int64_t blocks = (m + (int64_t)kColThreads * VN - 1) / ((int64_t)kColThreads * VN);
+  const bool vec = aligned16(S, ldS, sizeof(TS));
+  dim3 grid((unsigned)blocks);
+#define FS_RES(TV, VEC) residual_cols_kernel<TS, TV, VEC><<<grid, kColThreads, 0, st>>>(S, n, m, ldS, y, x, (const TV*)v, lam, r, block_sums)
+  if (v_f64) { if (vec) FS_RES(double, true); else FS_RES(double, false); }
+  else { if (vec) FS_RES(float, true); else FS_RES(float, false); }
+#undef FS_RES
+  reduce_pairs_kernel<<<1, 32, 0, st>>>(block_sums, blocks, sums);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int64_t gemv_rows_chunks(int64_t m, bool s_is_f64) {
+  const int64_t cw = s_is_f64 ? row_chunk_cols<double>() : row_chunk_cols<float>();
+  return (m + cw - 1) / cw;
+}
+
+int64_t residual_cols_blocks(int64_t m, bool s_is_f64) {
+  const int64_t w = (int64_t)kColThreads * (s_is_f64 ? 2 : 4);
+  return (m + w - 1) / w;
+}
+
+cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
+                      bool w_f64, double* partials, double* u, cudaStream_t st, int* launches) {
+  if (s_f64) return gemv_rows_t<double>((const double*)S, n, m, ldS, w, w_f64, partials, u, st, launches);
+  return gemv_rows_t<float>((const float*)S, n, m, ldS, w, w_f64, partials, u, st, launches);
+}
+
+cudaError_t gemv_cols_solve(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,
+                            const double* z, const void* v, bool v_f64, double lam, bool accumulate,
+                            double* x, cudaStream_t st, int* launches) {
+  if (s_f64) return gemv_cols_t<double>((const double*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, st, launches);
+  return gemv_cols_t<float>((const float*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, st, launches);
+}
+
+cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,
+                          const double* y, const double* x, const void* v, bool v_f64, double lam,
+                          double* r, double* block_sums, double* sums, cudaStream_t st,
+                          int* launches) {
+  if (s_f64) return residual_cols_t<double>((const double*)S, n, m, ldS, y, x, v, v_f64, lam, r, block_sums, sums, st, launches);
+  return residual_cols_t<float>((const float*)S, n, m, ldS, y, x, v, v_f64, lam, r, block_sums, sums, st, launches);
+}
+
+}  // namespace fs

@@ -1,0 +1,41 @@
+// kernels.h — host-side launchers of the fisher-b200 CUDA kernels (internal, C++).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fs {
+
+// ---- gemv.cu (HBM-bound streaming passes over S) ----
+// Number of column chunks the row-GEMV splits m into (partials buffer = chunks * n doubles).
+int64_t gemv_rows_chunks(int64_t m, bool s_is_f64);
+cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
+                      bool w_f64, double* partials, double* u, cudaStream_t st, int* launches);
+cudaError_t gemv_cols_solve(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,
+                            const double* z, const void* v, bool v_f64, double lam, bool accumulate,
+                            double* x, cudaStream_t st, int* launches);
+int64_t residual_cols_blocks(int64_t m, bool s_is_f64);
+cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,
+                          const double* y, const double* x, const void* v, bool v_f64, double lam,
+                          double* r, double* block_sums, double* sums, cudaStream_t st,
+                          int* launches);
+
+// ---- syrk_simt.cu (exact-product fp64 Gram, any dtype) ----
+size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms);
+cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam,
+                      double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);
+
+// ---- syrk_tc.cu (tcgen05 3xTF32 Gram, fp32 input) ----
+size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);
+bool syrk_tc_supported(const void* S, int64_t ldS);
+cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam,
+                    double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);
+
+// ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
+cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
+                         cudaStream_t st, int* launches);
+cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, cudaStream_t st,
+                        int* launches);
+cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, double* z, const int64_t* d_status,
+                      cudaStream_t st, int* launches);
+
+}  // namespace fs

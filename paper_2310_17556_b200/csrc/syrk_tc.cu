@@ -1,0 +1,326 @@
+// syrk_tc.cu — Gram W = S S^T (+λI) for fp32 scores on the 5th-gen tensor cores.
+//
+// Replaces core.py:284 (numpy A @ A.T -> OpenBLAS dsyrk) for FS_PREC_TF32X3.
+//
+// Precision mode "3xTF32": every fp32 element x is split on the fly into
+//   hi = rna_tf32(x)  (11 significant bits, exact in tf32)   lo = x - hi  (exact in fp32)
+// and each K-step issues three tcgen05.mma.kind::tf32:  hi*hi^T + hi*lo^T + lo*hi^T
+// (the dropped lo*lo^T term is <= 2^-22 relative and unbiased in sign off the diagonal).
+// fp32 accumulation in TMEM is limited to D K-blocks (16 columns each) per chunk; every
+// chunk is drained by the epilogue warps into an fp64 running sum, so the long m-axis
+// contraction is effectively fp64-accumulated (deterministic: fixed chunk boundaries and a
+// fixed-order reduction over split-K partials).
+//
+// Layout / pipeline (one CTA per SM, 384 threads):
+//   warp 0      TMA producer: S tiles (128 rows x 16 fp32, SWIZZLE_64B) -> raw ring (4 stages)
+//   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=128*NB, K=8 per MMA)
+//   warps 4-7   converters: raw -> (hi in place, lo to the lo ring), fence.proxy.async
+//   warps 8-11  epilogue: tcgen05.ld (32x32b) -> fp64 partial tile in global (L2) memory
+// Work decomposition: lower block tiles (I, J0..J0+NB-1) of 128-row blocks; split-K over
+// P CTAs per tile with K-blocks interleaved (kb = q, q+P, ...) so every CTA streams the
+// same region of S at the same time (S read once from HBM, reused from L2).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace fs {
+namespace {
+
+constexpr int kNB = 2;                    // 128-row blocks per B tile -> N = 256
+constexpr int kM = 128;
+constexpr int kN = 128 * kNB;
+constexpr int kBK = 16;                   // fp32 columns per stage (64 B rows, SWIZZLE_64B)
+constexpr int kStages = 4;
+constexpr int kBoxBytes = 128 * kBK * 4;  // one 128-row box = 8 KB
+constexpr int kStageBytes = (kNB + 1) * kBoxBytes;
+constexpr int kThreads = 384;
+constexpr int kTmemCols = 2 * kN;         // double-buffered fp32 accumulator
+constexpr int kDrainBlocks = 1024;        // K-blocks per fp32 chunk (16384 columns)
+constexpr uint32_t kIdesc = ptx::idesc_tf32(kM, kN);
+constexpr size_t kSmemBytes = 2 * (size_t)kStages * kStageBytes + 1024 + 256;
+
+struct Plan {
+  int nb, tiles, P, grid, KB, D;
+  bool direct;
+};
+
+FS_DEVINL void tile_of(int t, int nb, int& I, int& J0) {
+  int acc = 0;
+  for (int i = 0; i < nb; ++i) {
+    const int cnt = i / kNB + 1;
+    if (t < acc + cnt) { I = i; J0 = (t - acc) * kNB; return; }
+    acc += cnt;
+  }
+  I = nb - 1; J0 = 0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int nb, int tiles, int P, int KB,
+               int D, double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* raw = smem;
+  uint8_t* lo = smem + (size_t)kStages * kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * (size_t)kStages * kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + kStages;
+  uint64_t* empty = bars + 2 * kStages;
+  uint64_t* tfull = bars + 3 * kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&conv[s], 128);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 128);
+    }
+    ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tmap);
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int units = tiles * P;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      int s = 0; uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int t = u / P, q = u % P;
+        int I, J0; tile_of(t, nb, I, J0);
+        const bool a_in_b = I >= J0 && I < J0 + kNB;
+        const uint32_t bytes = (kNB + (a_in_b ? 0 : 1)) * kBoxBytes;
+        const int nk = (KB - q + P - 1) / P;
+        for (int k = 0; k < nk; ++k) {
+          const int col = (q + k * P) * kBK;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], bytes);
+          uint8_t* st = raw + (size_t)s * kStageBytes;
+#pragma unroll
+          for (int j = 0; j < kNB; ++j) ptx::tma_load_2d(st + j * kBoxBytes, &tmap, &full[s], col, (J0 + j) * 128);
+          if (!a_in_b) ptx::tma_load_2d(st + kNB * kBoxBytes, &tmap, &full[s], col, I * 128);
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      int s = 0; uint32_t ph = 0; uint32_t chunk = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int t = u / P, q = u % P;
+        int I, J0; tile_of(t, nb, I, J0);
+        const bool a_in_b = I >= J0 && I < J0 + kNB;
+        const int a_off = a_in_b ? (I - J0) * kBoxBytes : kNB * kBoxBytes;
+        const int nk = (KB - q + P - 1) / P;
+        uint32_t dacc = 0;
+        for (int k = 0; k < nk; ++k) {
+          const int kin = k % D;
+          if (kin == 0) {
+            const uint32_t b = chunk & 1;
+            ptx::mbar_wait(&tempty[b], ((chunk >> 1) & 1) ^ 1);
+            ptx::tc_fence_after();
+            dacc = tmem + b * kN;
+          }
+          ptx::mbar_wait(&conv[s], ph);
+          ptx::tc_fence_after();
+          const uint32_t rs = ptx::smem_u32(raw + (size_t)s * kStageBytes);
+          const uint32_t ls = ptx::smem_u32(lo + (size_t)s * kStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint64_t a_hi = ptx::desc_kmajor_sw64(rs + a_off + off);
+            const uint64_t a_lo = ptx::desc_kmajor_sw64(ls + a_off + off);
+            const uint64_t b_hi = ptx::desc_kmajor_sw64(rs + off);
+            const uint64_t b_lo = ptx::desc_kmajor_sw64(ls + off);
+            ptx::mma_tf32(dacc, a_hi, b_hi, kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_tf32(dacc, a_hi, b_lo, kIdesc, 1u);
+            ptx::mma_tf32(dacc, a_lo, b_hi, kIdesc, 1u);
+          }
+          ptx::mma_commit(&empty[s]);
+          if (kin == D - 1 || k == nk - 1) {
+            ptx::mma_commit(&tfull[chunk & 1]);
+            ++chunk;
+          }
+          if (++s == kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ======================= converters =======================
+    const int ct = threadIdx.x - 128;
+    int s = 0; uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u / P, q = u % P;
+      int I, J0; tile_of(t, nb, I, J0);
+      const bool a_in_b = I >= J0 && I < J0 + kNB;
+      const int nvec = (kNB + (a_in_b ? 0 : 1)) * (kBoxBytes / 16);
+      const int nk = (KB - q + P - 1) / P;
+      for (int k = 0; k < nk; ++k) {
+        ptx::mbar_wait(&full[s], ph);
+        float4* r4 = reinterpret_cast<float4*>(raw + (size_t)s * kStageBytes);
+        float4* l4 = reinterpret_cast<float4*>(lo + (size_t)s * kStageBytes);
+#pragma unroll 4
+        for (int i = ct; i < nvec; i += 128) {
+          const float4 x = r4[i];
+          float4 h, l;
+          h.x = ptx::tf32_rna(x.x); h.y = ptx::tf32_rna(x.y); h.z = ptx::tf32_rna(x.z); h.w = ptx::tf32_rna(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          r4[i] = h;
+          l4[i] = l;
+        }
+        ptx::fence_async_smem();
+        ptx::mbar_arrive(&conv[s]);
+        if (++s == kStages) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ======================= epilogue =======================
+    const int r = threadIdx.x - 256;               // accumulator row == TMEM lane
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    uint32_t chunk = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u / P, q = u % P;
+      int I, J0; tile_of(t, nb, I, J0);
+      const int nk = (KB - q + P - 1) / P;
+      const int nch = (nk + D - 1) / D;
+      double* acc = direct ? accbuf + (size_t)blockIdx.x * kM * kN : accbuf + (size_t)u * kM * kN;
+      for (int j = 0; j < nch; ++j) {
+        const uint32_t b = chunk & 1;
+        ptx::mbar_wait(&tfull[b], (chunk >> 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int cb = 0; cb < kN / 32; ++cb) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + b * kN + cb * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const size_t idx = (size_t)(cb * 32 + e) * kM + r;
+            const double x = (double)__uint_as_float(v[e]);
+            acc[idx] = (j == 0) ? x : acc[idx] + x;
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[b]);
+        ++chunk;
+      }
+      if (direct) {
+        const int64_t gi = (int64_t)I * 128 + r;
+        if (gi < n) {
+          for (int c = 0; c < kN; ++c) {
+            const int64_t gj = (int64_t)J0 * 128 + c;
+            if (gj > gi) break;
+            Gp[gi * (gi + 1) / 2 + gj] = acc[(size_t)c * kM + r] + (gi == gj ? lam : 0.0);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+}
+
+// Fixed-order sum of the P split-K partial tiles -> packed lower Gram (+λ on the diagonal).
+__global__ void syrk_tc_reduce(const double* __restrict__ ws, int nb, int P, int64_t n, double lam,
+                               double* __restrict__ Gp) {
+  int I, J0;
+  tile_of(blockIdx.x, nb, I, J0);
+  for (int e = threadIdx.x; e < kM * kN; e += blockDim.x) {
+    const int c = e / kM, r = e % kM;
+    const int64_t gi = (int64_t)I * 128 + r, gj = (int64_t)J0 * 128 + c;
+    if (gi >= n || gj > gi) continue;
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += ws[((size_t)blockIdx.x * P + q) * kM * kN + e];
+    Gp[gi * (gi + 1) / 2 + gj] = s + (gi == gj ? lam : 0.0);
+  }
+}
+
+Plan make_plan(int64_t n, int64_t m, int num_sms) {
+  Plan p;
+  p.nb = (int)((n + 127) / 128);
+  p.tiles = 0;
+  for (int i = 0; i < p.nb; ++i) p.tiles += i / kNB + 1;
+  p.KB = (int)((m + kBK - 1) / kBK);
+  p.P = p.tiles >= num_sms ? 1 : std::max(1, std::min(num_sms / p.tiles, p.KB));
+  const int units = p.tiles * p.P;
+  p.grid = std::min(units, num_sms);
+  p.D = kDrainBlocks;
+  p.direct = p.P == 1;
+  return p;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool syrk_tc_supported(const void* S, int64_t ldS) {
+  return (reinterpret_cast<uintptr_t>(S) % 16 == 0) && ((ldS * 4) % 16 == 0);
+}
+
+size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
+  Plan p = make_plan(n, m, num_sms);
+  const size_t slots = p.direct ? (size_t)p.grid : (size_t)p.tiles * p.P;
+  return slots * kM * kN * sizeof(double);
+}
+
+cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam, double* G_packed, double* ws,
+                    int num_sms, cudaStream_t st, int* launches) {
+  EncodeTiledFn encode = get_encode();
+  if (!encode) return cudaErrorNotSupported;
+  Plan p = make_plan(n, m, num_sms);
+  CUtensorMap tmap;
+  const cuuint64_t gdim[2] = {(cuuint64_t)m, (cuuint64_t)n};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ldS * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, 128u};
+  const cuuint32_t estride[2] = {1u, 1u};
+  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(S), gdim, gstride, box, estride,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  syrk_tc_kernel<<<p.grid, kThreads, kSmemBytes, st>>>(tmap, n, p.nb, p.tiles, p.P, p.KB, p.D, ws, G_packed, lam,
+                                                       p.direct ? 1 : 0);
+  if (launches) *launches += 1;
+  if (!p.direct) {
+    syrk_tc_reduce<<<p.tiles, 256, 0, st>>>(ws, p.nb, p.P, n, lam, G_packed);
+    if (launches) *launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fs

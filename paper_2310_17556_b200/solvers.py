@@ -1,0 +1,164 @@
+"""Solver entry points of the damped Fisher system on B200 (mirror of fisher_solve.solvers).
+
+``solve_chol`` is the hot path (solvers.py:151-206 of the reference): one call into
+``fs_chol_solve`` of libfisher_b200.so runs Gram (tcgen05 SYRK) -> potrf -> TRSV pair
+-> fused (v - S^T z)/lam epilogue -> fp64 residual diagnostics -> optional one-step
+refinement, ordered on the current CUDA stream with a single host synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from time import perf_counter
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import (
+    EPS,
+    DampedSystem,
+    FactorizationError,
+    Method,
+    ScoreMatrix,
+    Solution,
+    Variant,
+    WorkspaceMeter,
+    PRECISIONS,
+    _check,
+    _dt,
+    _stream,
+    resolve_precision,
+)
+
+DEFAULT_NAIVE_CAP = 4096            # solvers.py:38
+DEFAULT_SIGMA_FLOOR = 1e-12         # solvers.py:39
+REFINE_ABOVE_REL = 1e-10            # solvers.py:43 (_REFINE_ABOVE_REL)
+
+
+def fp32_residual_bound(sigma2_max_over_lam: float) -> float:
+    """Stated tolerance of the fp32 (tf32x3) mode: 4 u32 sigma_max^2 / lam."""
+    return 4.0 * 2.0 ** -24 * sigma2_max_over_lam
+
+
+@dataclass(frozen=True)
+class CholWorkspace:
+    """Lower Cholesky factor of the damped Gram matrix (solvers.py:57-71), device resident."""
+
+    L: torch.Tensor   # n x n float64 CUDA tensor, upper triangle exactly zero
+
+    @property
+    def n(self) -> int:
+        return int(self.L.shape[0])
+
+    def solve_gram(self, b) -> np.ndarray:
+        """Solve (L L^T) y = b by forward then back substitution on the GPU."""
+        bt = torch.as_tensor(np.asarray(b, dtype=np.float64) if not isinstance(b, torch.Tensor) else b,
+                             dtype=torch.float64).to(self.L.device).clone()
+        ctx = _lib.context_for(self.L.device.index, self.n, 1)
+        rc = ctx.lib.fs_trsv_pair(ctx.handle, self.L.data_ptr(), self.n, self.L.stride(0), bt.data_ptr(),
+                                  _stream(self.L.device))
+        _check(ctx, rc, "fs_trsv_pair")
+        return bt.cpu().numpy() if not isinstance(b, torch.Tensor) else bt
+
+
+def cholesky_lower_device(W: torch.Tensor) -> torch.Tensor:
+    """In-place-safe lower Cholesky on the GPU with the reference's pivot contract (solvers.py:74-90)."""
+    n = int(W.shape[0])
+    L = W.to(torch.float64).contiguous().clone()
+    L = torch.tril(L)  # the kernel reads the lower triangle and keeps the upper exactly zero
+    ctx = _lib.context_for(L.device.index, n, 1)
+    piv = ctypes.c_int64(-1)
+    rc = ctx.lib.fs_potrf(ctx.handle, L.data_ptr(), n, L.stride(0), ctypes.byref(piv), _stream(L.device))
+    if rc == _lib.FS_NOT_PD:
+        raise FactorizationError(
+            f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",
+            pivot=int(piv.value))
+    _check(ctx, rc, "fs_potrf")
+    return L
+
+
+def _cholesky_lower(W) -> np.ndarray:
+    """Host-array convenience mirror of solvers.py:74-90 (runs on the GPU)."""
+    from .core import default_device
+    Wt = torch.as_tensor(np.asarray(W, dtype=np.float64)).to(default_device())
+    return cholesky_lower_device(Wt).cpu().numpy()
+
+
+def _meter_slots(n: int, m: int) -> int:
+    lib = _lib.load()
+    return int(lib.fs_workspace_bytes(n, m)) // 8
+
+
+def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
+               refine: str | bool = "auto", diagnostics: bool = True) -> Solution:
+    """Solve (S^T S + lam I) x = v through the n-by-n Gram factorization (solvers.py:197-206).
+
+    precision: "fp64" (exact fp64 products, the reference's arithmetic), "tf32x3" (fp32 scores,
+    tcgen05 3xTF32 Gram with fp64 drains) or "auto" (by the scores' dtype).
+    refine: "auto" applies the reference's one-step refinement rule (rel_residual > 1e-10,
+    solvers.py:171-194) in fp64 mode and no refinement in tf32x3 mode, whose stated bound is
+    4 u32 sigma_max^2/lam; True forces the reference rule, False disables it.
+    diagnostics: compute abs/rel residual on the GPU (two extra passes over S), as the
+    reference does inside solve_chol (solvers.py:160-170).
+    """
+    if system.S.is_complex:
+        raise ValueError("solve_chol handles real scores; use solve_chol_hermitian")
+    t0 = perf_counter()
+    S = system.S.tensor
+    v = system.v_tensor
+    n, m = system.n, system.m
+    prec = resolve_precision(precision, S.dtype)
+    if refine == "auto":
+        do_refine = prec == "fp64"
+    else:
+        do_refine = bool(refine)
+    if do_refine and not diagnostics:
+        raise ValueError("refinement needs the residual diagnostics")
+    ctx = _lib.context_for(S.device.index, n, m)
+    if meter is not None:
+        meter.alloc(_meter_slots(n, m) + m)
+    x = torch.empty(m, dtype=torch.float64, device=S.device)
+    piv = ctypes.c_int64(-1)
+    res = (ctypes.c_double * 2)(float("nan"), float("nan"))
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (_lib.FS_FLAG_REFINE if do_refine else 0)
+    rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
+                               v.data_ptr(), system.lam, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
+                               REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(S.device))
+    if meter is not None:
+        meter.free(_meter_slots(n, m))
+    if rc == _lib.FS_NOT_PD:
+        raise FactorizationError(
+            f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",
+            pivot=int(piv.value))
+    _check(ctx, rc, "fs_chol_solve")
+    xo = x.cpu().numpy() if system.S.host_origin else x
+    return Solution(x=xo, method=Method.CHOL, abs_residual=float(res[0]), rel_residual=float(res[1]),
+                    wall_seconds=perf_counter() - t0, precision=prec)
+
+
+def _not_yet(name: str):
+    raise NotImplementedError(
+        f"{name}: the GPU route is scheduled after the chol hot path (SURVEY §8f-2); "
+        "there is deliberately no CPU fallback in this package")
+
+
+def solve_chol_hermitian(system, meter=None):
+    """solvers.py:209-213 — complex variants are SURVEY §8f row 3 (not in this build)."""
+    _not_yet("solve_chol_hermitian")
+
+
+def solve_realpart(system, meter=None):
+    """solvers.py:216-240 — complex variants are SURVEY §8f row 3 (not in this build)."""
+    _not_yet("solve_realpart")
+
+
+def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOOR) -> Solution:
+    """solvers.py:347-354 comparison route."""
+    _not_yet("solve_svd_eigh")
+
+
+def solve_svd_direct(system: DampedSystem) -> Solution:
+    """solvers.py:357-364 comparison route."""
+    _not_yet("solve_svd_direct")
