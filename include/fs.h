@@ -60,8 +60,9 @@ const char* fs_version(void);
 int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max);
 void fs_ctx_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);
-/* Bytes of device workspace a context for (n, m) owns (feeds WorkspaceMeter, core.py:63-96). */
-size_t fs_workspace_bytes(int64_t n, int64_t m);
+/* Device bytes one solve of (n, m) in (dtype, precision) touches besides S, v, x
+ * (feeds WorkspaceMeter, core.py:63-96; a context may own more to serve any smaller problem). */
+size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t fs_launch_count(const fs_ctx* ctx);
 

@@ -28,7 +28,7 @@ SIGNATURES = {
     "fs_ctx_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, _c_int64, _c_int64]),
     "fs_ctx_destroy": (None, [_vp]),
     "fs_last_error": (ctypes.c_char_p, [_vp]),
-    "fs_workspace_bytes": (ctypes.c_size_t, [_c_int64, _c_int64]),
+    "fs_workspace_bytes": (ctypes.c_size_t, [_c_int64, _c_int64, ctypes.c_int, ctypes.c_int]),
     "fs_launch_count": (_c_int64, [_vp]),
     "fs_gram_packed": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64,
                                       ctypes.c_double, _vp, _vp]),

@@ -89,8 +89,12 @@ def _coerce_damping(lam) -> float:       # core.py:99-105
     return lam
 
 
-def _to_device_tensor(a, name: str, device) -> torch.Tensor:
-    """Coerce to a contiguous float32/float64 CUDA tensor and validate finiteness (core.py:108-119)."""
+def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.Tensor:
+    """Coerce to a float32/float64 CUDA tensor and validate finiteness (core.py:108-119).
+
+    2-D inputs get unit column stride and 16-byte aligned rows (padded leading dimension);
+    ``force_copy`` guarantees the result does not alias ``a`` (the reference freezes a copy).
+    """
     if isinstance(a, torch.Tensor):
         t = a
         if t.is_complex():
@@ -107,7 +111,18 @@ def _to_device_tensor(a, name: str, device) -> torch.Tensor:
             arr = arr.astype(np.float64)
         t = torch.from_numpy(np.ascontiguousarray(arr))
     dev = device if device is not None else (t.device if t.is_cuda else default_device())
-    t = t.to(dev, non_blocking=True).contiguous()
+    if t.dim() == 2 and t.shape[1] > 0:
+        # rows start on 16-byte boundaries (TMA / vector-load requirement); pad columns are never read
+        per16 = 16 // t.element_size()
+        ld = -(-t.shape[1] // per16) * per16
+        if force_copy or not (t.is_cuda and t.device == dev and t.stride(1) == 1 and t.stride(0) % per16 == 0
+                              and t.data_ptr() % 16 == 0):
+            buf = torch.empty((t.shape[0], ld), dtype=t.dtype, device=dev)
+            t = buf[:, : t.shape[1]].copy_(t, non_blocking=True)
+    else:
+        t = t.to(dev, non_blocking=True).contiguous()
+        if force_copy and isinstance(a, torch.Tensor) and t.data_ptr() == a.data_ptr():
+            t = t.clone()
     if t.numel() and not bool(torch.isfinite(t).all()):
         raise ValueError(f"{name} must contain only finite entries")
     return t
@@ -118,13 +133,12 @@ class ScoreMatrix:
 
     def __init__(self, data, device=None):
         src = data
-        t = _to_device_tensor(data, "score matrix", device)
+        aliasable = isinstance(src, torch.Tensor) and src.is_cuda
+        t = _to_device_tensor(data, "score matrix", device, force_copy=aliasable)
         if t.dim() != 2:
             raise ValueError(f"score matrix must be 2-D, got shape {tuple(t.shape)}")
         if t.shape[0] < 1 or t.shape[1] < 1:
             raise ValueError(f"score matrix needs at least one row and column, got {tuple(t.shape)}")
-        if isinstance(src, torch.Tensor) and src.is_cuda and t.data_ptr() == src.data_ptr():
-            t = t.clone()  # freezing must not alias the caller's tensor (core.py:139-140)
         self._t = t
         self._host = None
         # numpy in -> numpy out (drop-in semantics); CUDA tensor in -> CUDA tensor out
@@ -177,13 +191,12 @@ class DampedSystem:
         self.lam = _coerce_damping(lam)
         if isinstance(v, torch.Tensor) and v.is_complex() or (not isinstance(v, torch.Tensor) and np.iscomplexobj(np.asarray(v))):
             raise ValueError("real score matrix with complex right-hand side")
-        t = _to_device_tensor(v, "right-hand side", S.tensor.device)
+        t = _to_device_tensor(v, "right-hand side", S.tensor.device,
+                              force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
         if t.dim() != 1:
             raise ValueError(f"right-hand side must be 1-D, got shape {tuple(t.shape)}")
         if t.shape[0] != S.m:
             raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
-        if isinstance(v, torch.Tensor) and v.is_cuda and t.data_ptr() == v.data_ptr():
-            t = t.clone()
         self._v = t.to(S.dtype)
         self._host_v = None
 

@@ -29,7 +29,8 @@ struct fs_ctx {
   double* d_partials = nullptr; // row-GEMV chunk partials
   double* d_block_sums = nullptr;
   double* d_sums = nullptr;     // 4
-  double* d_r = nullptr;        // m (negated residual, refinement right-hand side)
+  double* d_r = nullptr;        // m (residual vector, refinement right-hand side)
+  double* d_v64 = nullptr;      // m (fp64 copy of an fp32 v in fp64 precision mode)
   double* d_syrk_ws = nullptr;
   int64_t* d_status = nullptr;
   int64_t* h_status = nullptr;  // pinned
@@ -128,9 +129,12 @@ extern "C" {
 
 const char* fs_version(void) { return "fisher-b200 0.1.0 sm_100a"; }
 
-size_t fs_workspace_bytes(int64_t n, int64_t m) {
+size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision) {
+  // device bytes one solve of (n, m) touches besides S, v and x (feeds WorkspaceMeter)
   Sizes s = sizes_for(n, m, 148);
-  return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + s.r + s.syrk +
+  const bool tc = dtype == FS_F32 && precision != FS_PREC_FP64;
+  const size_t gram = tc ? fs::syrk_tc_plan_bytes(n, m, 148) : fs::syrk_simt_plan_bytes(n, m, 148);
+  return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + 2 * s.r + gram +
          sizeof(int64_t);
 }
 
@@ -157,6 +161,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
   A((void**)&ctx->d_block_sums, s.block_sums);
   A((void**)&ctx->d_sums, 4 * sizeof(double));
   A((void**)&ctx->d_r, s.r);
+  A((void**)&ctx->d_v64, s.r);
   A((void**)&ctx->d_syrk_ws, s.syrk);
   A((void**)&ctx->d_status, sizeof(int64_t));
   if (ok && cudaMallocHost((void**)&ctx->h_status, sizeof(int64_t)) != cudaSuccess) ok = false;
@@ -166,7 +171,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
     fs_ctx_destroy(ctx);
     return FS_ENOMEM;
   }
-  ctx->ws_bytes = fs_workspace_bytes(n_max, m_max);
+  ctx->ws_bytes = s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + s.r + s.syrk;
   cudaMemset(ctx->d_status, 0, sizeof(int64_t));
   *out = ctx;
   return FS_OK;
@@ -176,7 +181,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   if (!ctx) return;
   cudaFree(ctx->d_packed); cudaFree(ctx->d_W); cudaFree(ctx->d_z); cudaFree(ctx->d_y);
   cudaFree(ctx->d_partials); cudaFree(ctx->d_block_sums); cudaFree(ctx->d_sums);
-  cudaFree(ctx->d_r); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
+  cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
   delete ctx;
@@ -296,7 +301,20 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   if (!v || !x) return fail(ctx, FS_EINVAL, "NULL vector");
   if (pivot) *pivot = -1;
   cudaStream_t st = (cudaStream_t)stream;
-  const int vdt = dtype;  // v has the dtype of S
+  int vdt = dtype;  // v has the dtype of S
+  {
+    // fp64 precision mode on fp32 scores: widen v once so every GEMV product is exact fp64
+    int use_tc = 0;
+    if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+    if (dtype == FS_F32 && !use_tc) {
+      int l = 0;
+      cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "widen v");
+      v = ctx->d_v64;
+      vdt = FS_F64;
+    }
+  }
   double* u = ctx->d_packed + n * (n + 1) / 2;
   // 1. partial Gram (no shift) and u = S v, packed for one all-reduce
   if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;

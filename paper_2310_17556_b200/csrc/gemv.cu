@@ -101,7 +101,9 @@ gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t l
   constexpr int VN = VecOf<TS>::N;
   constexpr int kZ = 2048;
   constexpr int kInner = 16;  // fp32 partial sums span 16 rows before folding into fp64
-  using Zt = TS;              // fp32 mode multiplies in fp32 (z rounded once), fp64 mode exact
+  // fp32 S with an fp32 right-hand side multiplies in fp32 (z rounded once); an fp64 right-hand
+  // side (fp64 precision mode) makes every product and sum exact fp64
+  using Zt = typename std::conditional<sizeof(TS) == 8 || sizeof(TV) == 8, double, float>::type;
   __shared__ Zt zs[kZ];
   const int64_t col = ((int64_t)blockIdx.x * kColThreads + threadIdx.x) * VN;
   double acc[VN];
@@ -116,7 +118,7 @@ gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t l
     if (col >= m) continue;
     const TS* base = S + r0 * ldS + col;
     for (int i0 = 0; i0 < rows; i0 += kInner) {
-      TS part[VN];
+      Zt part[VN];
 #pragma unroll
       for (int e = 0; e < VN; ++e) part[e] = 0;
       const int cnt = min(kInner, rows - i0);
@@ -130,13 +132,13 @@ gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t l
           TS a[VN];
           vec_to_array(buf[k], a);
 #pragma unroll
-          for (int e = 0; e < VN; ++e) part[e] = fma(zs[i0 + k], a[e], part[e]);
+          for (int e = 0; e < VN; ++e) part[e] = fma(zs[i0 + k], (Zt)a[e], part[e]);
         }
       } else {
         for (int k = 0; k < cnt; ++k)
 #pragma unroll
           for (int e = 0; e < VN; ++e)
-            if (col + e < m) part[e] = fma(zs[i0 + k], ld_stream(base + (int64_t)(i0 + k) * ldS + e), part[e]);
+            if (col + e < m) part[e] = fma(zs[i0 + k], (Zt)ld_stream(base + (int64_t)(i0 + k) * ldS + e), part[e]);
       }
 #pragma unroll
       for (int e = 0; e < VN; ++e) acc[e] += (double)part[e];
@@ -241,6 +243,11 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ block_sums, int64
   if (threadIdx.x == 0) { sums[0] = a; sums[1] = b; }
 }
 
+__global__ void widen_kernel(const float* __restrict__ in, int64_t m, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (double)in[i];
+}
+
 inline bool aligned16(const void* p, int64_t ld, int es) {
   return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * es) % 16 == 0);
 }
@@ -299,6 +306,12 @@ cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, cons
 }
 
 }  // namespace
+
+cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches) {
+  widen_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(in, m, out);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
 
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64) {
   const int64_t cw = s_is_f64 ? row_chunk_cols<double>() : row_chunk_cols<float>();

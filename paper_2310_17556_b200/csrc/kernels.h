@@ -6,6 +6,7 @@
 namespace fs {
 
 // ---- gemv.cu (HBM-bound streaming passes over S) ----
+cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches);
 // Number of column chunks the row-GEMV splits m into (partials buffer = chunks * n doubles).
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64);
 cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
@@ -20,12 +21,14 @@ cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64
                           int* launches);
 
 // ---- syrk_simt.cu (exact-product fp64 Gram, any dtype) ----
-size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms);
+size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms);  // bound for any smaller problem
+size_t syrk_simt_plan_bytes(int64_t n, int64_t m, int num_sms);       // exact for (n, m)
 cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam,
                       double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);
 
 // ---- syrk_tc.cu (tcgen05 3xTF32 Gram, fp32 input) ----
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);
+size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms);
 bool syrk_tc_supported(const void* S, int64_t ldS);
 cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam,
                     double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);

@@ -118,11 +118,18 @@ void plan(int64_t n, int64_t m, int num_sms, int64_t& tiles, int& splits, int64_
 
 }  // namespace
 
-size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms) {
+size_t syrk_simt_plan_bytes(int64_t n, int64_t m, int num_sms) {
   int64_t tiles, kchunk;
   int splits;
   plan(n, m, num_sms, tiles, splits, kchunk);
   return splits > 1 ? (size_t)splits * tiles * kTile * kTile * sizeof(double) : 0;
+}
+
+size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms) {
+  // splits > 1 only when tiles < 4*num_sms, and then splits*tiles <= 4*num_sms + tiles
+  // < 8*num_sms: a bound that holds for every (n, m), so one context serves smaller problems
+  (void)n; (void)m;
+  return (size_t)8 * num_sms * kTile * kTile * sizeof(double);
 }
 
 cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam,

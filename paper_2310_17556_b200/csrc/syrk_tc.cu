@@ -38,9 +38,15 @@ constexpr int kBK = 16;                   // fp32 columns per stage (64 B rows, 
 constexpr int kStages = 4;
 constexpr int kBoxBytes = 128 * kBK * 4;  // one 128-row box = 8 KB
 constexpr int kStageBytes = (kNB + 1) * kBoxBytes;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kTmemCols = 2 * kN;         // double-buffered fp32 accumulator
-constexpr int kDrainBlocks = 1024;        // K-blocks per fp32 chunk (16384 columns)
+// The tensor core's fp32 accumulation truncates (round-toward-zero-like): the bias grows with
+// the number of MMAs summed into one accumulator (~2^-25 relative per MMA, measured).  Chunks of
+// kDrainBlocks K-blocks (6 MMAs each) are therefore drained into round-to-nearest fp32 register
+// sums, which are flushed into fp64 every kFlushChunks chunks.
+constexpr int kDrainBlocks = 4;
+constexpr int kFlushChunks = 32;
+constexpr int kRegsProducer = 56, kRegsConverter = 64, kRegsEpilogue = 192;
 constexpr uint32_t kIdesc = ptx::idesc_tf32(kM, kN);
 constexpr size_t kSmemBytes = 2 * (size_t)kStages * kStageBytes + 1024 + 256;
 
@@ -83,7 +89,7 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int nb, int 
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 128);
+      ptx::mbar_init(&tempty[b], 256);
     }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmap);
@@ -94,8 +100,11 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int nb, int 
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int units = tiles * P;
+  const int wg = warp >> 2;
 
-  if (warp == 0) {
+  if (wg == 0) {
+   ptx::setmaxnreg_dec<kRegsProducer>();
+   if (warp == 0) {
     // ======================= TMA producer =======================
     if (lane == 0) {
       int s = 0; uint32_t ph = 0;
@@ -160,8 +169,10 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int nb, int 
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+   }
+  } else if (wg == 1) {
     // ======================= converters =======================
+    ptx::setmaxnreg_dec<kRegsConverter>();
     const int ct = threadIdx.x - 128;
     int s = 0; uint32_t ph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -188,44 +199,58 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, int64_t n, int nb, int 
         if (++s == kStages) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 8) {
-    // ======================= epilogue =======================
-    const int r = threadIdx.x - 256;               // accumulator row == TMEM lane
-    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  } else {
+    // ======================= epilogue (8 warps) =======================
+    ptx::setmaxnreg_inc<kRegsEpilogue>();
+    // warp -> TMEM lane quarter (warp & 3) and column half ((warp - 8) >> 2); thread -> one row
+    const int sub = warp & 3, half = (warp - 8) >> 2;
+    const int r = 32 * sub + lane;
+    const uint32_t lane_base = (uint32_t)(32 * sub) << 16;
+    float acc[kN / 2];
     uint32_t chunk = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int t = u / P, q = u % P;
       int I, J0; tile_of(t, nb, I, J0);
       const int nk = (KB - q + P - 1) / P;
       const int nch = (nk + D - 1) / D;
-      double* acc = direct ? accbuf + (size_t)blockIdx.x * kM * kN : accbuf + (size_t)u * kM * kN;
+      double* sc = direct ? accbuf + (size_t)blockIdx.x * kM * kN : accbuf + (size_t)u * kM * kN;
+      bool first_flush = true;
       for (int j = 0; j < nch; ++j) {
         const uint32_t b = chunk & 1;
         ptx::mbar_wait(&tfull[b], (chunk >> 1) & 1);
         ptx::tc_fence_after();
-#pragma unroll 1
-        for (int cb = 0; cb < kN / 32; ++cb) {
+        const bool fresh = (j % kFlushChunks) == 0;
+#pragma unroll
+        for (int cb = 0; cb < kN / 64; ++cb) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(tmem + lane_base + b * kN + cb * 32, v);
+          ptx::tmem_ld_32x32b_x32(tmem + lane_base + b * kN + half * (kN / 2) + cb * 32, v);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const size_t idx = (size_t)(cb * 32 + e) * kM + r;
-            const double x = (double)__uint_as_float(v[e]);
-            acc[idx] = (j == 0) ? x : acc[idx] + x;
+            const float x = __uint_as_float(v[e]);
+            acc[cb * 32 + e] = fresh ? x : acc[cb * 32 + e] + x;
           }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[b]);
         ++chunk;
+        if ((j + 1) % kFlushChunks == 0 || j == nch - 1) {
+#pragma unroll
+          for (int e = 0; e < kN / 2; ++e) {
+            const size_t idx = (size_t)(half * (kN / 2) + e) * kM + r;
+            sc[idx] = first_flush ? (double)acc[e] : sc[idx] + (double)acc[e];
+          }
+          first_flush = false;
+        }
       }
       if (direct) {
         const int64_t gi = (int64_t)I * 128 + r;
         if (gi < n) {
-          for (int c = 0; c < kN; ++c) {
+          for (int e = 0; e < kN / 2; ++e) {
+            const int c = half * (kN / 2) + e;
             const int64_t gj = (int64_t)J0 * 128 + c;
             if (gj > gi) break;
-            Gp[gi * (gi + 1) / 2 + gj] = acc[(size_t)c * kM + r] + (gi == gj ? lam : 0.0);
+            Gp[gi * (gi + 1) / 2 + gj] = sc[(size_t)c * kM + r] + (gi == gj ? lam : 0.0);
           }
         }
       }
@@ -257,7 +282,7 @@ Plan make_plan(int64_t n, int64_t m, int num_sms) {
   p.tiles = 0;
   for (int i = 0; i < p.nb; ++i) p.tiles += i / kNB + 1;
   p.KB = (int)((m + kBK - 1) / kBK);
-  p.P = p.tiles >= num_sms ? 1 : std::max(1, std::min(num_sms / p.tiles, p.KB));
+  p.P = p.tiles >= num_sms ? 1 : std::max(1, std::min(num_sms / p.tiles, p.KB / 16));  // >= 16 K-blocks per unit
   const int units = p.tiles * p.P;
   p.grid = std::min(units, num_sms);
   p.D = kDrainBlocks;
@@ -283,14 +308,20 @@ EncodeTiledFn get_encode() {
 
 }  // namespace
 
+size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms) {
+  Plan p = make_plan(n, m, num_sms);
+  return (size_t)(p.direct ? p.grid : p.tiles * p.P) * kM * kN * sizeof(double);
+}
+
 bool syrk_tc_supported(const void* S, int64_t ldS) {
   return (reinterpret_cast<uintptr_t>(S) % 16 == 0) && ((ldS * 4) % 16 == 0);
 }
 
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
-  Plan p = make_plan(n, m, num_sms);
-  const size_t slots = p.direct ? (size_t)p.grid : (size_t)p.tiles * p.P;
-  return slots * kM * kN * sizeof(double);
+  // one fp64 partial tile per unit (split-K) or per resident CTA (direct): never more than
+  // num_sms slots for ANY (n, m), so a context sized once serves every smaller problem
+  (void)n; (void)m;
+  return (size_t)num_sms * kM * kN * sizeof(double);
 }
 
 cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam, double* G_packed, double* ws,

@@ -45,6 +45,12 @@ FS_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_
       : "memory");
 }
 
+// ---------------- register reallocation (warpgroup-wide) ----------------
+template <uint32_t kRegs>
+FS_DEV void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+template <uint32_t kRegs>
+FS_DEV void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs)); }
+
 // ---------------- tcgen05 / TMEM ----------------
 template <uint32_t kCols>
 FS_DEV void tmem_alloc(uint32_t* dst_smem) {

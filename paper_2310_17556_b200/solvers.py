@@ -86,9 +86,9 @@ def _cholesky_lower(W) -> np.ndarray:
     return cholesky_lower_device(Wt).cpu().numpy()
 
 
-def _meter_slots(n: int, m: int) -> int:
+def _meter_slots(n: int, m: int, dtype: int, precision: int) -> int:
     lib = _lib.load()
-    return int(lib.fs_workspace_bytes(n, m)) // 8
+    return int(lib.fs_workspace_bytes(n, m, dtype, precision)) // 8
 
 
 def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
@@ -118,7 +118,7 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
         raise ValueError("refinement needs the residual diagnostics")
     ctx = _lib.context_for(S.device.index, n, m)
     if meter is not None:
-        meter.alloc(_meter_slots(n, m) + m)
+        meter.alloc(_meter_slots(n, m, _dt(S), PRECISIONS[prec]) + m)
     x = torch.empty(m, dtype=torch.float64, device=S.device)
     piv = ctypes.c_int64(-1)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
@@ -127,7 +127,7 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
                                v.data_ptr(), system.lam, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
                                REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(S.device))
     if meter is not None:
-        meter.free(_meter_slots(n, m))
+        meter.free(_meter_slots(n, m, _dt(S), PRECISIONS[prec]))
     if rc == _lib.FS_NOT_PD:
         raise FactorizationError(
             f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",

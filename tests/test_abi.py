@@ -46,8 +46,8 @@ def test_version_and_workspace_query_without_gpu():
     from paper_2310_17556_b200 import _lib
     lib = _lib.load()
     assert lib.fs_version().decode().startswith("fisher-b200")
-    small = lib.fs_workspace_bytes(64, 4096)
-    big = lib.fs_workspace_bytes(1024, 1000000)
+    small = lib.fs_workspace_bytes(64, 4096, _lib.FS_F64, _lib.FS_PREC_FP64)
+    big = lib.fs_workspace_bytes(1024, 1000000, _lib.FS_F32, _lib.FS_PREC_TF32X3)
     assert 0 < small < big
     # workspace is O(n^2 + n m / chunk + m): far below the n*m*8 bytes of S itself
     assert big < 1024 * 1000000 * 8
