@@ -66,6 +66,19 @@ size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t fs_launch_count(const fs_ctx* ctx);
 
+/* Stage timing of fs_chol_solve with CUDA events on the solve stream (no extra syncs).
+ * fs_profile_read fills ms[stage] for the most recent solve, stages in this order: */
+#define FS_PROF_GRAM 0       /* S S^T (tcgen05 / fp64 SYRK + split-K reduce)   */
+#define FS_PROF_GEMV_SV 1    /* u = S v                                         */
+#define FS_PROF_ALLREDUCE 2  /* caller's all-reduce of [W | u] (0 for one rank) */
+#define FS_PROF_POTRF 3      /* unpack + lam + Cholesky                         */
+#define FS_PROF_TRSV 4       /* z = L^-T L^-1 u                                 */
+#define FS_PROF_GEMV_STZ 5   /* x = (v - S^T z) / lam                           */
+#define FS_PROF_RESIDUAL 6   /* y = S x, r = S^T y + lam x - v, norms (+ refinement) */
+#define FS_PROF_STAGES 7
+int fs_profile_enable(fs_ctx* ctx, int on);
+int fs_profile_read(fs_ctx* ctx, double* ms, int count);
+
 /* ---- stage entry points (parity tests, ncu isolation, multi-rank drivers) ---- */
 
 /* Gram: packed-lower G[i(i+1)/2 + j] = sum_k S[i,k] S[j,k] (+ lam on i == j), fp64.

@@ -16,6 +16,7 @@ FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED = range(6)
 FS_F32, FS_F64 = 0, 1
 FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO = 0, 1, 2
 FS_FLAG_RESIDUAL, FS_FLAG_REFINE = 1, 2
+PROF_STAGES = ("gram", "gemv_sv", "allreduce", "potrf", "trsv", "gemv_stz", "residual")
 
 _c_int64 = ctypes.c_int64
 _vp = ctypes.c_void_p
@@ -30,6 +31,8 @@ SIGNATURES = {
     "fs_last_error": (ctypes.c_char_p, [_vp]),
     "fs_workspace_bytes": (ctypes.c_size_t, [_c_int64, _c_int64, ctypes.c_int, ctypes.c_int]),
     "fs_launch_count": (_c_int64, [_vp]),
+    "fs_profile_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "fs_profile_read": (ctypes.c_int, [_vp, _dp, ctypes.c_int]),
     "fs_gram_packed": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64,
                                       ctypes.c_double, _vp, _vp]),
     "fs_gemv_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, ctypes.c_int,
@@ -105,6 +108,14 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.fs_launch_count(self.handle))
+
+    def profile(self, on: bool = True) -> None:
+        self.lib.fs_profile_enable(self.handle, 1 if on else 0)
+
+    def stage_ms(self) -> dict:
+        buf = (ctypes.c_double * len(PROF_STAGES))()
+        self.lib.fs_profile_read(self.handle, buf, len(PROF_STAGES))
+        return dict(zip(PROF_STAGES, list(buf)))
 
 
 _contexts: dict[int, Context] = {}

@@ -38,7 +38,21 @@ struct fs_ctx {
   size_t ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
+  // stage timing (fs_profile_enable): events recorded on the solve stream at stage boundaries
+  bool prof_on = false;
+  cudaEvent_t ev[FS_PROF_STAGES + 1] = {};
+  int ev_used[FS_PROF_STAGES + 1] = {};
+  double prof_ms[FS_PROF_STAGES] = {};
 };
+
+namespace {
+inline void prof_mark(fs_ctx* ctx, int slot, cudaStream_t st) {
+  if (ctx->prof_on && ctx->ev[slot]) {
+    cudaEventRecord(ctx->ev[slot], st);
+    ctx->ev_used[slot] = 1;
+  }
+}
+}  // namespace
 
 namespace {
 
@@ -171,6 +185,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
     fs_ctx_destroy(ctx);
     return FS_ENOMEM;
   }
+  for (int i = 0; i <= FS_PROF_STAGES; ++i) cudaEventCreate(&ctx->ev[i]);
   ctx->ws_bytes = s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + s.r + s.syrk;
   cudaMemset(ctx->d_status, 0, sizeof(int64_t));
   *out = ctx;
@@ -184,12 +199,26 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
+  for (int i = 0; i <= FS_PROF_STAGES; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   delete ctx;
 }
 
 const char* fs_last_error(const fs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t fs_launch_count(const fs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fs_profile_enable(fs_ctx* ctx, int on) {
+  if (!ctx) return FS_EINVAL;
+  ctx->prof_on = on != 0;
+  return FS_OK;
+}
+
+int fs_profile_read(fs_ctx* ctx, double* ms, int count) {
+  if (!ctx || !ms || count < 1) return FS_EINVAL;
+  for (int i = 0; i < count && i < FS_PROF_STAGES; ++i) ms[i] = ctx->prof_ms[i];
+  return FS_OK;
+}
 
 int fs_gram_packed(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
                    int64_t ldS, double lam, double* G_packed, void* stream) {
@@ -316,14 +345,20 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     }
   }
   double* u = ctx->d_packed + n * (n + 1) / 2;
+  for (int i = 0; i <= FS_PROF_STAGES; ++i) ctx->ev_used[i] = 0;
+  prof_mark(ctx, 0, st);
   // 1. partial Gram (no shift) and u = S v, packed for one all-reduce
   if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
+  prof_mark(ctx, FS_PROF_GRAM + 1, st);
   if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+  prof_mark(ctx, FS_PROF_GEMV_SV + 1, st);
   if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
     return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
+  prof_mark(ctx, FS_PROF_ALLREDUCE + 1, st);
   // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
   if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
   if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
+  prof_mark(ctx, FS_PROF_POTRF + 1, st);
   FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
   {
     int l = 0;
@@ -331,8 +366,10 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     ctx->launches += l;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
+  prof_mark(ctx, FS_PROF_TRSV + 1, st);
   // 3. x = (v - S^T z) / lam on the local shard
   if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
+  prof_mark(ctx, FS_PROF_GEMV_STZ + 1, st);
   const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
   const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
   double abs_res = NAN, rel_res = NAN;
@@ -351,6 +388,7 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     }
     if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
       return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
+    prof_mark(ctx, FS_PROF_RESIDUAL + 1, st);
     FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
@@ -381,6 +419,19 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   if (!want_res) {
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
+  }
+  if (ctx->prof_on) {
+    // stage k spans the last recorded boundary before it to its own boundary (refinement
+    // passes, when taken, are folded into the residual stage)
+    int prev = 0;
+    for (int k = 0; k < FS_PROF_STAGES; ++k) {
+      ctx->prof_ms[k] = 0.0;
+      if (ctx->ev_used[k + 1]) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev[prev], ctx->ev[k + 1]) == cudaSuccess) ctx->prof_ms[k] = ms;
+        prev = k + 1;
+      }
+    }
   }
   if (*ctx->h_status != 0) {
     if (pivot) *pivot = *ctx->h_status - 1;
