@@ -45,6 +45,13 @@ FS_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_
       : "memory");
 }
 
+// L2-only prefetch of a 2-D tile (no shared memory, no completion tracking).
+FS_DEV void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // ---------------- register reallocation (warpgroup-wide) ----------------
 template <uint32_t kRegs>
 FS_DEV void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs)); }
@@ -102,6 +109,19 @@ FS_DEV uint64_t desc_kmajor_sw64(uint32_t smem_addr) {
   d |= (uint64_t)(512 >> 4) << 32;                    // stride byte offset: 8 rows * 64 B
   d |= (uint64_t)1 << 46;                             // descriptor version (sm_100)
   d |= (uint64_t)4 << 61;                             // layout: SWIZZLE_64B
+  return d;
+}
+
+// K-major descriptor for a swizzled layout whose rows are kRowBytes (64 -> SW64, 128 -> SW128).
+template <int kRowBytes>
+FS_DEV uint64_t desc_kmajor(uint32_t smem_addr) {
+  static_assert(kRowBytes == 64 || kRowBytes == 128, "64 B or 128 B rows");
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);               // start address
+  d |= (uint64_t)1 << 16;                                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((8 * kRowBytes) >> 4) << 32;               // SBO: one 8-row swizzle atom
+  d |= (uint64_t)1 << 46;                                    // descriptor version (sm_100)
+  d |= (uint64_t)(kRowBytes == 128 ? 2 : 4) << 61;           // SWIZZLE_128B : SWIZZLE_64B
   return d;
 }
 
