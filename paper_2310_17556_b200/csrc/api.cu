@@ -32,6 +32,7 @@ struct fs_ctx {
   double* d_r = nullptr;        // m (residual vector, refinement right-hand side)
   double* d_v64 = nullptr;      // m (fp64 copy of an fp32 v in fp64 precision mode)
   double* d_syrk_ws = nullptr;
+  double* d_potrf = nullptr;    // inverted diagonal blocks (Linv) + double-buffered panels
   int64_t* d_status = nullptr;
   int64_t* h_status = nullptr;  // pinned
   double* h_sums = nullptr;     // pinned
@@ -61,7 +62,7 @@ const double kEps = 2.220446049250313e-16;  // core.py:16
 size_t packed_len(int64_t n) { return (size_t)(n * (n + 1) / 2 + n); }
 
 struct Sizes {
-  size_t packed, W, vec, partials, block_sums, r, syrk;
+  size_t packed, W, vec, partials, block_sums, r, syrk, potrf;
 };
 
 Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
@@ -73,6 +74,7 @@ Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
   s.block_sums = (size_t)fs::residual_cols_blocks(m, true) * 2 * sizeof(double);
   s.r = (size_t)m * sizeof(double);
   s.syrk = std::max(fs::syrk_simt_workspace_bytes(n, m, num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
+  s.potrf = (size_t)fs::potrf_scratch_doubles(n) * sizeof(double);
   return s;
 }
 
@@ -148,7 +150,7 @@ size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision) {
   Sizes s = sizes_for(n, m, 148);
   const bool tc = dtype == FS_F32 && precision != FS_PREC_FP64;
   const size_t gram = tc ? fs::syrk_tc_plan_bytes(n, m, 148) : fs::syrk_simt_plan_bytes(n, m, 148);
-  return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + 2 * s.r + gram +
+  return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + 2 * s.r + gram + s.potrf +
          sizeof(int64_t);
 }
 
@@ -177,6 +179,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
   A((void**)&ctx->d_r, s.r);
   A((void**)&ctx->d_v64, s.r);
   A((void**)&ctx->d_syrk_ws, s.syrk);
+  A((void**)&ctx->d_potrf, s.potrf);
   A((void**)&ctx->d_status, sizeof(int64_t));
   if (ok && cudaMallocHost((void**)&ctx->h_status, sizeof(int64_t)) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&ctx->h_sums, 4 * sizeof(double)) != cudaSuccess) ok = false;
@@ -197,6 +200,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_packed); cudaFree(ctx->d_W); cudaFree(ctx->d_z); cudaFree(ctx->d_y);
   cudaFree(ctx->d_partials); cudaFree(ctx->d_block_sums); cudaFree(ctx->d_sums);
   cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
+  cudaFree(ctx->d_potrf);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
   for (int i = 0; i <= FS_PROF_STAGES; ++i)
@@ -258,7 +262,7 @@ int fs_potrf_async(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
   int l = 0;
-  cudaError_t e = fs::potrf_lower(W, n, ldW, ctx->d_status, st, &l);
+  cudaError_t e = fs::potrf_lower(W, n, ldW, ctx->d_status, ctx->d_potrf, st, &l);
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "potrf");
   return FS_OK;
@@ -284,8 +288,10 @@ int fs_potrf(fs_ctx* ctx, double* W, int64_t n, int64_t ldW, int64_t* pivot, voi
 
 int fs_trsv_pair(fs_ctx* ctx, const double* L, int64_t n, int64_t ldL, double* z, void* stream) {
   if (!ctx || !L || !z || n < 1 || ldL < n) return fail(ctx, FS_EINVAL, "bad trsv arguments");
+  if (n > ctx->n_max) return fail(ctx, FS_ENOMEM, "n exceeds n_max");
   int l = 0;
-  cudaError_t e = fs::trsv_pair(L, n, ldL, z, nullptr, (cudaStream_t)stream, &l);
+  cudaError_t e = fs::invert_diag_blocks(L, n, ldL, ctx->d_potrf, (cudaStream_t)stream, &l);
+  if (e == cudaSuccess) e = fs::trsv_pair(L, n, ldL, ctx->d_potrf, z, nullptr, (cudaStream_t)stream, &l);
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   return FS_OK;
@@ -362,7 +368,7 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
   {
     int l = 0;
-    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_z, ctx->d_status, st, &l);
+    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
     ctx->launches += l;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
@@ -403,7 +409,7 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
       return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
     {
       int l = 0;
-      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_z, ctx->d_status, st, &l);
+      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
       ctx->launches += l;
       if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
     }

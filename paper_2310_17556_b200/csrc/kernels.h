@@ -36,9 +36,14 @@ cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double la
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
                          cudaStream_t st, int* launches);
-cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, cudaStream_t st,
-                        int* launches);
-cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, double* z, const int64_t* d_status,
-                      cudaStream_t st, int* launches);
+// scratch = potrf_scratch_doubles(n) doubles; on return it starts with the inverted 64x64
+// diagonal blocks of L (Linv), which trsv_pair consumes
+int64_t potrf_scratch_doubles(int64_t n);
+cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch,
+                        cudaStream_t st, int* launches);
+cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* scratch, cudaStream_t st,
+                               int* launches);
+cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
+                      const int64_t* d_status, cudaStream_t st, int* launches);
 
 }  // namespace fs
