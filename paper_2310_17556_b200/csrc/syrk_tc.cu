@@ -1,10 +1,10 @@
-// syrk_tc.cu — Gram W = S S^T (+λI) for fp32 scores on the 5th-gen tensor cores.
+// syrk_tc.cu — Gram W = S S^T (+λI) for fp32 scores on the 5th-gen tensor cores, CTA pairs.
 //
 // Replaces core.py:284 (numpy A @ A.T -> OpenBLAS dsyrk) for FS_PREC_TF32X3.
 //
 // Precision mode "3xTF32": every fp32 element x is split on the fly into
 //   hi = rna_tf32(x)  (11 significant bits, exact in tf32)   lo = x - hi  (exact in fp32)
-// and each K-step issues three tcgen05.mma.kind::tf32:  hi*hi^T + hi*lo^T + lo*hi^T
+// and each K-step issues three tcgen05.mma.kind::tf32:  lo*hi^T + hi*lo^T + hi*hi^T
 // (the dropped lo*lo^T term is <= 2^-22 relative and unbiased in sign off the diagonal).
 // The tensor core's fp32 accumulation truncates (round-toward-zero-like; measured ~2^-25
 // relative per MMA into one accumulator), so the TMEM accumulator is drained every
@@ -12,15 +12,22 @@
 // flushed into fp64 every kFlushChunks drains.  Deterministic: fixed chunk boundaries and a
 // fixed-order fp64 reduction over split-K partials.
 //
-// Layout / pipeline (one CTA per SM, 512 threads, setmaxnreg-rebalanced):
-//   warp 0      TMA producer: S boxes (128 rows x kBK fp32, swizzled) -> raw ring
-//               + L2 bulk prefetch of 1 KB row spans 32 K-blocks ahead (DRAM sees long bursts)
-//   warp 1      TMEM allocator + single-thread MMA issuer (M=128, N=256, K=8 per MMA)
-//   warps 4-7   converters: raw -> hi in place, lo -> lo ring, fence.proxy.async
-//   warps 8-15  epilogue: tcgen05.ld (32x32b) -> fp32 RN sums -> fp64 partial tile (L2)
-// Work decomposition: lower block tiles (I, J0..J0+1) of 128-row blocks; split-K over
-// P CTAs per tile, each a contiguous K range, so the CTAs of all tiles with the same split
-// index walk the same columns of S together (S read ~once from HBM, reused from L2).
+// Work decomposition: 128-row blocks; a PAIR TILE is rows {2p, 2p+1} x cols {2q, 2q+1}
+// (q <= p), computed by a cluster of two CTAs with tcgen05.mma.cta_group::2 (M=256, N=256):
+// CTA c holds A = row block 2p+c and the B half = row block 2q+c in its own smem and owns the
+// 128 x 256 accumulator of its row block in its own TMEM.  On diagonal pair tiles A == B, so
+// each CTA loads a single box.  Per K-column every CTA loads 2 boxes (1 on the diagonal) instead
+// of the 3 of a single-CTA 128x256 tile, and the tensor core reads half of B from each SM.
+// Split-K over P clusters per pair tile, contiguous K ranges (S streamed ~once from HBM).
+//
+// Roles per CTA (512 threads, setmaxnreg-rebalanced):
+//   warp 0      TMA producer (own boxes, own barrier) + L2 bulk prefetch of 1 KB row spans ahead
+//   warp 1      TMEM allocator (cta_group::2, both CTAs); MMA issuer in the leader CTA only
+//   warps 4-7   converters: raw -> hi in place, lo -> lo ring; release-arrive on the LEADER's
+//               conv barrier (mapa), so the leader's MMA sees both CTAs' operands converted
+//   warps 8-15  epilogue: tcgen05.ld own TMEM -> fp32 RN sums -> fp64 partials; release-arrive
+//               on the leader's tempty barrier
+// MMA completion is tcgen05.commit.cta_group::2 ... multicast::cluster to both CTAs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdlib.h>
@@ -34,41 +41,35 @@
 namespace fs {
 namespace {
 
-constexpr int kNB = 2;                    // 128-row blocks per B tile -> N = 256
-constexpr int kM = 128;
-constexpr int kN = 128 * kNB;
-#ifndef FS_SYRK_BK
-#define FS_SYRK_BK 32
-#endif
-constexpr int kBK = FS_SYRK_BK;           // fp32 columns per K-block (rows of 4*kBK bytes, swizzled)
+constexpr int kBlk = 128;                 // rows per block / per CTA operand box
+constexpr int kN = 256;                   // MMA N (two B halves of 128 rows)
+constexpr int kBK = 32;                   // fp32 columns per K-block (128 B rows, SWIZZLE_128B)
 constexpr int kRowBytes = 4 * kBK;
-constexpr int kRaw = kBK == 16 ? 6 : 3;   // raw (TMA destination, hi in place) ring depth
-constexpr int kLo = kBK == 16 ? 2 : 1;    // lo ring depth
-constexpr int kBoxBytes = 128 * kBK * 4;  // one 128-row box = 8 KB
-constexpr int kStageBytes = (kNB + 1) * kBoxBytes;
+constexpr int kRaw = 4;                   // raw ring (TMA destination, hi in place)
+constexpr int kLo = 2;                    // lo ring
+constexpr int kBoxBytes = kBlk * kRowBytes;   // 16 KB
+constexpr int kStageBytes = 2 * kBoxBytes;    // A box + B box
 constexpr int kThreads = 512;
 constexpr int kTmemCols = 2 * kN;         // double-buffered fp32 accumulator
-constexpr int kDrainBlocks = 64 / kBK;     // 4 x 16 or 2 x 32 columns: 24 MMAs per drain
+constexpr int kDrainBlocks = 2;           // 2 x 32 columns = 24 MMAs per drained chunk
 constexpr int kFlushChunks = 64;
-constexpr int kPfSpan = 1024 / kRowBytes; // K-blocks per L2 prefetch span (1 KB per row)
-constexpr int kPfAhead = 2;               // spans prefetched ahead of the TMA loads
+constexpr int kPfSpan = 256 / kBK;        // K-blocks per L2 prefetch span (1 KB per row)
+constexpr int kPfAhead = 2;               // spans kept in flight ahead of the TMA loads
 constexpr int kRegsProducer = 56, kRegsConverter = 64, kRegsEpilogue = 192;
-constexpr uint32_t kIdesc = ptx::idesc_tf32(kM, kN);
+constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 constexpr size_t kSmemBytes = (size_t)(kRaw + kLo) * kStageBytes + 1024 + 512;
 
 struct Plan {
-  int nb, tiles, P, grid, KB, KC, D;
+  int nb, np, tiles, P, clusters, KB, KC, D;
   bool direct;
 };
 
-FS_DEVINL void tile_of(int t, int nb, int& I, int& J0) {
-  int acc = 0;
-  for (int i = 0; i < nb; ++i) {
-    const int cnt = i / kNB + 1;
-    if (t < acc + cnt) { I = i; J0 = (t - acc) * kNB; return; }
-    acc += cnt;
-  }
-  I = nb - 1; J0 = 0;
+FS_DEVINL void pair_of(int t, int& p, int& q) {  // lower pair tiles (p >= q), row-major
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  p = i;
+  q = t - i * (i + 1) / 2;
 }
 
 struct Ring {  // stage index + mbarrier phase of a circular buffer
@@ -77,42 +78,44 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
   FS_DEVINL void next(int depth) { if (++s == depth) { s = 0; ph ^= 1; } }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap pmap, int64_t n,
-               int nb, int tiles, int P, int KB, int KC, int D, double* __restrict__ accbuf,
-               double* __restrict__ Gp, double lam, int direct, int dbg) {
+               int tiles, int P, int KB, int KC, int D, double* __restrict__ accbuf, double* __restrict__ Gp,
+               double lam, int direct, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw = smem;
   uint8_t* lo = smem + (size_t)kRaw * kStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(kRaw + kLo) * kStageBytes);
-  uint64_t* full = bars;                 // TMA -> converters        [kRaw]
-  uint64_t* conv = full + kRaw;          // converters -> MMA        [kRaw]
-  uint64_t* empty = conv + kRaw;         // MMA -> TMA (raw free)    [kRaw]
-  uint64_t* lo_free = empty + kRaw;      // MMA -> converters        [kLo]
-  uint64_t* tfull = lo_free + kLo;       // MMA -> epilogue          [2]
-  uint64_t* tempty = tfull + 2;          // epilogue -> MMA          [2]
+  uint64_t* full = bars;                 // local TMA -> local converters           [kRaw]
+  uint64_t* conv = full + kRaw;          // both CTAs' converters -> leader MMA     [kRaw]
+  uint64_t* empty = conv + kRaw;         // MMA (multicast) -> each producer        [kRaw]
+  uint64_t* lo_free = empty + kRaw;      // MMA (multicast) -> each converter group [kLo]
+  uint64_t* tfull = lo_free + kLo;       // MMA (multicast) -> each epilogue        [2]
+  uint64_t* tempty = tfull + 2;          // both CTAs' epilogues -> leader MMA      [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = ptx::cluster_ctarank();   // 0 = leader
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRaw; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&conv[s], 128);
+      ptx::mbar_init(&conv[s], 2 * 128);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kLo; ++s) ptx::mbar_init(&lo_free[s], 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 256);
+      ptx::mbar_init(&tempty[b], 2 * 256);
     }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmap);
     ptx::tma_prefetch_desc(&pmap);
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc2<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();                   // barriers initialised and TMEM allocated in both CTAs
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int units = tiles * P;
@@ -121,24 +124,23 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
   if (wg == 0) {
     ptx::setmaxnreg_dec<kRegsProducer>();
     if (warp == 0 && lane == 0) {
-      // ======================= TMA producer =======================
+      // ======================= TMA producer (each CTA: its own boxes) =======================
       Ring rr;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
-        int I, J0; tile_of(t, nb, I, J0);
-        const bool a_in_b = I >= J0 && I < J0 + kNB;
-        const uint32_t bytes = (kNB + (a_in_b ? 0 : 1)) * kBoxBytes;
-        const int kb0 = q * KC, nk = min(KC, KB - kb0);   // contiguous K range of this split
+        int pp, qq; pair_of(t, pp, qq);
+        const int rowA = (2 * pp + (int)crank) * kBlk, rowB = (2 * qq + (int)crank) * kBlk;
+        const bool diag = pp == qq;                       // A == B: one box
+        const uint32_t bytes = (diag ? 1 : 2) * kBoxBytes;
+        const int kb0 = q * KC, nk = min(KC, KB - kb0);
         for (int k = 0; k < nk; ++k) {
           if (!(dbg & 32) && k % kPfSpan == 0) {
-            // keep kPfAhead spans of every operand row block in flight to L2
             for (int a = (k == 0 ? 0 : kPfAhead); a <= kPfAhead; ++a) {
               const int pk = k + a * kPfSpan;
               if (pk >= nk) break;
               const int pcol = (kb0 + pk) * kBK;
-#pragma unroll
-              for (int j = 0; j < kNB; ++j) ptx::tma_prefetch_l2_2d(&pmap, pcol, (J0 + j) * 128);
-              if (!a_in_b) ptx::tma_prefetch_l2_2d(&pmap, pcol, I * 128);
+              ptx::tma_prefetch_l2_2d(&pmap, pcol, rowA);
+              if (!diag) ptx::tma_prefetch_l2_2d(&pmap, pcol, rowB);
             }
           }
           ptx::mbar_wait(&empty[rr.s], rr.ph ^ 1);
@@ -146,21 +148,19 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
           ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
           uint8_t* st = raw + (size_t)rr.s * kStageBytes;
           const int col = (kb0 + k) * kBK;
-#pragma unroll
-          for (int j = 0; j < kNB; ++j) ptx::tma_load_2d(st + j * kBoxBytes, &tmap, &full[rr.s], col, (J0 + j) * 128);
-          if (!a_in_b) ptx::tma_load_2d(st + kNB * kBoxBytes, &tmap, &full[rr.s], col, I * 128);
+          ptx::tma_load_2d(st, &tmap, &full[rr.s], col, rowA);
+          if (!diag) ptx::tma_load_2d(st + kBoxBytes, &tmap, &full[rr.s], col, rowB);
           rr.next(kRaw);
         }
       }
-    } else if (warp == 1 && lane == 0) {
-      // ======================= MMA issuer =======================
+    } else if (warp == 1 && lane == 0 && crank == 0) {
+      // ======================= MMA issuer (leader CTA) =======================
       Ring rr, lr;
       uint32_t chunk = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
-        int I, J0; tile_of(t, nb, I, J0);
-        const bool a_in_b = I >= J0 && I < J0 + kNB;
-        const int a_off = a_in_b ? (I - J0) * kBoxBytes : kNB * kBoxBytes;
+        int pp, qq; pair_of(t, pp, qq);
+        const int b_off = (pp == qq) ? 0 : kBoxBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         uint32_t dacc = 0;
         for (int k = 0; k < nk; ++k) {
@@ -178,18 +178,18 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < (dbg & 4 ? 0 : kBK / 8); ++kk) {
             const uint32_t off = kk * 32;
-            const uint64_t a_hi = ptx::desc_kmajor<kRowBytes>(rs + a_off + off);
-            const uint64_t a_lo = ptx::desc_kmajor<kRowBytes>(ls + a_off + off);
-            const uint64_t b_hi = ptx::desc_kmajor<kRowBytes>(rs + off);
-            const uint64_t b_lo = ptx::desc_kmajor<kRowBytes>(ls + off);
-            ptx::mma_tf32(dacc, a_lo, b_hi, kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
-            ptx::mma_tf32(dacc, a_hi, b_lo, kIdesc, 1u);
-            ptx::mma_tf32(dacc, a_hi, b_hi, kIdesc, 1u);
+            const uint64_t a_hi = ptx::desc_kmajor<kRowBytes>(rs + off);
+            const uint64_t a_lo = ptx::desc_kmajor<kRowBytes>(ls + off);
+            const uint64_t b_hi = ptx::desc_kmajor<kRowBytes>(rs + b_off + off);
+            const uint64_t b_lo = ptx::desc_kmajor<kRowBytes>(ls + b_off + off);
+            ptx::mma2_tf32(dacc, a_lo, b_hi, kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma2_tf32(dacc, a_hi, b_lo, kIdesc, 1u);
+            ptx::mma2_tf32(dacc, a_hi, b_hi, kIdesc, 1u);
           }
-          ptx::mma_commit(&empty[rr.s]);
-          ptx::mma_commit(&lo_free[lr.s]);
+          ptx::mma2_commit_mc(&empty[rr.s], 0x3);
+          ptx::mma2_commit_mc(&lo_free[lr.s], 0x3);
           if (kin == D - 1 || k == nk - 1) {
-            ptx::mma_commit(&tfull[chunk & 1]);
+            ptx::mma2_commit_mc(&tfull[chunk & 1], 0x3);
             ++chunk;
           }
           rr.next(kRaw);
@@ -198,15 +198,15 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
       }
     }
   } else if (wg == 1) {
-    // ======================= converters =======================
+    // ======================= converters (each CTA: its own smem) =======================
     ptx::setmaxnreg_dec<kRegsConverter>();
     const int ct = threadIdx.x - 128;
+    const uint32_t conv0 = ptx::mapa(ptx::smem_u32(conv), 0);   // leader's conv[0]
     Ring rr, lr;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = cluster; u < units; u += nclusters) {
       const int t = u / P, q = u % P;
-      int I, J0; tile_of(t, nb, I, J0);
-      const bool a_in_b = I >= J0 && I < J0 + kNB;
-      const int nvec = (kNB + (a_in_b ? 0 : 1)) * (kBoxBytes / 16);
+      int pp, qq; pair_of(t, pp, qq);
+      const int nvec = ((pp == qq) ? 1 : 2) * (kBoxBytes / 16);
       const int kb0 = q * KC, nk = min(KC, KB - kb0);
       for (int k = 0; k < nk; ++k) {
         ptx::mbar_wait(&full[rr.s], rr.ph);
@@ -220,32 +220,33 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
             float4 h, l;
             h.x = ptx::tf32_rna(x.x); h.y = ptx::tf32_rna(x.y); h.z = ptx::tf32_rna(x.z); h.w = ptx::tf32_rna(x.w);
             l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+            if (dbg & 64) { l = make_float4(0.f, 0.f, 0.f, 0.f); h = x; }   // probe: raw operand, no lo
             r4[i] = h;
             l4[i] = l;
           }
           ptx::fence_async_smem();
         }
-        ptx::mbar_arrive(&conv[rr.s]);
+        ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
         rr.next(kRaw);
         lr.next(kLo);
       }
     }
   } else {
-    // ======================= epilogue (8 warps) =======================
+    // ======================= epilogue (8 warps, own TMEM) =======================
     ptx::setmaxnreg_inc<kRegsEpilogue>();
-    // warp -> TMEM lane quarter (warp & 3) and column half ((warp - 8) >> 2); thread -> one row
     const int sub = warp & 3, half = (warp - 8) >> 2;
-    const int r = 32 * sub + lane;
+    const int r = 32 * sub + lane;                       // row within this CTA's 128-row block
     const uint32_t lane_base = (uint32_t)(32 * sub) << 16;
+    const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(tempty), 0);
     float acc[kN / 2];
     uint32_t chunk = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = cluster; u < units; u += nclusters) {
       const int t = u / P, q = u % P;
-      int I, J0; tile_of(t, nb, I, J0);
+      int pp, qq; pair_of(t, pp, qq);
       const int kb0 = q * KC, nk = min(KC, KB - kb0);
       const int nch = (nk + D - 1) / D;
-      double* __restrict__ sc = (direct ? accbuf + (size_t)blockIdx.x * kM * kN : accbuf + (size_t)u * kM * kN) +
-                                (size_t)half * (kN / 2) * kM + r;   // column-major [c][r], this thread's row
+      const size_t slot = direct ? (size_t)blockIdx.x : ((size_t)u * 2 + crank);
+      double* __restrict__ sc = accbuf + slot * kBlk * kN + (size_t)half * (kN / 2) * kBlk + r;  // [c][r]
       bool first_flush = true;
       for (int j = 0; j < nch; ++j) {
         const uint32_t b = chunk & 1;
@@ -264,67 +265,67 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
           }
         }
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&tempty[b]);
+        ptx::mbar_arrive_cluster(tempty0 + b * 8);
         ++chunk;
         if (!(dbg & 8) && ((j + 1) % kFlushChunks == 0 || j == nch - 1)) {
-          // fp64 flush, 16 independent loads in flight per group
 #pragma unroll
           for (int g = 0; g < kN / 2; g += 16) {
             double old[16];
             if (!first_flush) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) old[e] = sc[(size_t)(g + e) * kM];
+              for (int e = 0; e < 16; ++e) old[e] = sc[(size_t)(g + e) * kBlk];
             }
 #pragma unroll
-            for (int e = 0; e < 16; ++e) sc[(size_t)(g + e) * kM] = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
+            for (int e = 0; e < 16; ++e) sc[(size_t)(g + e) * kBlk] = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
           }
           first_flush = false;
         }
       }
       if (direct) {
-        const int64_t gi = (int64_t)I * 128 + r;
+        const int64_t gi = (int64_t)(2 * pp + crank) * kBlk + r;
         if (gi < n) {
           for (int e = 0; e < kN / 2; ++e) {
             const int c = half * (kN / 2) + e;
-            const int64_t gj = (int64_t)J0 * 128 + c;
+            const int64_t gj = (int64_t)(2 * qq) * kBlk + c;
             if (gj > gi) break;
-            Gp[gi * (gi + 1) / 2 + gj] = sc[(size_t)e * kM] + (gi == gj ? lam : 0.0);
+            Gp[gi * (gi + 1) / 2 + gj] = sc[(size_t)e * kBlk] + (gi == gj ? lam : 0.0);
           }
         }
       }
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+  ptx::cluster_sync();                   // both CTAs done with TMEM and with each other's barriers
+  if (warp == 1) ptx::tmem_dealloc2<kTmemCols>(tmem);
 }
 
 // Fixed-order sum of the P split-K partial tiles -> packed lower Gram (+λ on the diagonal).
-__global__ void syrk_tc_reduce(const double* __restrict__ ws, int nb, int P, int64_t n, double lam,
-                               double* __restrict__ Gp) {
-  int I, J0;
-  tile_of(blockIdx.x, nb, I, J0);
-  for (int e = threadIdx.x; e < kM * kN; e += blockDim.x) {
-    const int c = e / kM, r = e % kM;
-    const int64_t gi = (int64_t)I * 128 + r, gj = (int64_t)J0 * 128 + c;
+// Block (t, c): pair tile t, CTA half c (row block 2p+c).
+__global__ void syrk_tc_reduce(const double* __restrict__ ws, int P, int64_t n, double lam, double* __restrict__ Gp) {
+  int pp, qq;
+  pair_of(blockIdx.x >> 1, pp, qq);
+  const int c = blockIdx.x & 1;
+  for (int e = threadIdx.x; e < kBlk * kN; e += blockDim.x) {
+    const int col = e / kBlk, r = e % kBlk;
+    const int64_t gi = (int64_t)(2 * pp + c) * kBlk + r, gj = (int64_t)(2 * qq) * kBlk + col;
     if (gi >= n || gj > gi) continue;
     double s = 0.0;
-    for (int q = 0; q < P; ++q) s += ws[((size_t)blockIdx.x * P + q) * kM * kN + e];
+    for (int q = 0; q < P; ++q) s += ws[(((size_t)(blockIdx.x >> 1) * P + q) * 2 + c) * kBlk * kN + e];
     Gp[gi * (gi + 1) / 2 + gj] = s + (gi == gj ? lam : 0.0);
   }
 }
 
 Plan make_plan(int64_t n, int64_t m, int num_sms) {
   Plan p;
-  p.nb = (int)((n + 127) / 128);
-  p.tiles = 0;
-  for (int i = 0; i < p.nb; ++i) p.tiles += i / kNB + 1;
+  p.nb = (int)((n + kBlk - 1) / kBlk);
+  p.np = (p.nb + 1) / 2;
+  p.tiles = p.np * (p.np + 1) / 2;
   p.KB = (int)((m + kBK - 1) / kBK);
-  p.P = p.tiles >= num_sms ? 1 : std::max(1, std::min(num_sms / p.tiles, p.KB / 16));  // >= 16 K-blocks per unit
+  const int max_clusters = num_sms / 2;
+  p.P = p.tiles >= max_clusters ? 1 : std::max(1, std::min(max_clusters / p.tiles, p.KB / 8));
   p.KC = (p.KB + p.P - 1) / p.P;          // K-blocks per split, contiguous in m
   p.P = (p.KB + p.KC - 1) / p.KC;          // every split non-empty
-  const int units = p.tiles * p.P;
-  p.grid = std::min(units, num_sms);
+  p.clusters = std::min(p.tiles * p.P, max_clusters);
   p.D = kDrainBlocks;
   p.direct = p.P == 1;
   return p;
@@ -350,7 +351,7 @@ EncodeTiledFn get_encode() {
 
 size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms) {
   Plan p = make_plan(n, m, num_sms);
-  return (size_t)(p.direct ? p.grid : p.tiles * p.P) * kM * kN * sizeof(double);
+  return (size_t)(p.direct ? 2 * p.clusters : 2 * p.tiles * p.P) * kBlk * kN * sizeof(double);
 }
 
 bool syrk_tc_supported(const void* S, int64_t ldS) {
@@ -358,10 +359,10 @@ bool syrk_tc_supported(const void* S, int64_t ldS) {
 }
 
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
-  // one fp64 partial tile per unit (split-K) or per resident CTA (direct): never more than
-  // num_sms slots for ANY (n, m), so a context sized once serves every smaller problem
+  // one fp64 128x256 partial per CTA of a split-K unit (<= num_sms CTAs) or per resident CTA
+  // (direct): never more than num_sms slots for ANY (n, m)
   (void)n; (void)m;
-  return (size_t)num_sms * kM * kN * sizeof(double);
+  return (size_t)num_sms * kBlk * kN * sizeof(double);
 }
 
 cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam, double* G_packed, double* ws,
@@ -372,11 +373,11 @@ cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double la
   CUtensorMap tmap, pmap;
   const cuuint64_t gdim[2] = {(cuuint64_t)m, (cuuint64_t)n};
   const cuuint64_t gstride[1] = {(cuuint64_t)ldS * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kBK, 128u};
-  const cuuint32_t pbox[2] = {(cuuint32_t)(kBK * kPfSpan), 128u};   // 1 KB x 128 rows prefetch box
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBlk};
+  const cuuint32_t pbox[2] = {(cuuint32_t)(kBK * kPfSpan), (cuuint32_t)kBlk};
   const cuuint32_t estride[2] = {1u, 1u};
   CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(S), gdim, gstride, box, estride,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, kBK == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   cr = encode(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(S), gdim, gstride, pbox, estride,
@@ -390,11 +391,11 @@ cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double la
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
-  syrk_tc_kernel<<<p.grid, kThreads, kSmemBytes, st>>>(tmap, pmap, n, p.nb, p.tiles, p.P, p.KB, p.KC, p.D, ws,
-                                                       G_packed, lam, p.direct ? 1 : 0, dbg);
+  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(tmap, pmap, n, p.tiles, p.P, p.KB, p.KC, p.D, ws,
+                                                               G_packed, lam, p.direct ? 1 : 0, dbg);
   if (launches) *launches += 1;
   if (!p.direct) {
-    syrk_tc_reduce<<<p.tiles, 256, 0, st>>>(ws, p.nb, p.P, n, lam, G_packed);
+    syrk_tc_reduce<<<2 * p.tiles, 256, 0, st>>>(ws, p.P, n, lam, G_packed);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
