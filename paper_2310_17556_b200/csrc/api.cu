@@ -17,6 +17,7 @@
 
 #include "../../include/fs.h"
 #include "kernels.h"
+#include "tiles.cuh"
 
 struct fs_ctx {
   int device = 0;
@@ -39,18 +40,23 @@ struct fs_ctx {
   size_t ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
-  // stage timing (fs_profile_enable): events recorded on the solve stream at stage boundaries
+  uint8_t* d_St = nullptr;      // tiled fp32 copy of S for the tensor-core Gram (lazy, tiles.cuh)
+  size_t St_bytes = 0;
+  // stage timing (fs_profile_enable): events recorded on the solve stream after each stage,
+  // in chronological order; stage time = gap to the previous mark
+  static constexpr int kMaxMarks = 24;
   bool prof_on = false;
-  cudaEvent_t ev[FS_PROF_STAGES + 1] = {};
-  int ev_used[FS_PROF_STAGES + 1] = {};
+  cudaEvent_t ev[kMaxMarks] = {};
+  int ev_stage[kMaxMarks] = {};
+  int n_marks = 0;
   double prof_ms[FS_PROF_STAGES] = {};
 };
 
 namespace {
-inline void prof_mark(fs_ctx* ctx, int slot, cudaStream_t st) {
-  if (ctx->prof_on && ctx->ev[slot]) {
-    cudaEventRecord(ctx->ev[slot], st);
-    ctx->ev_used[slot] = 1;
+inline void prof_mark(fs_ctx* ctx, int stage, cudaStream_t st) {
+  if (ctx->prof_on && ctx->n_marks < fs_ctx::kMaxMarks && ctx->ev[ctx->n_marks]) {
+    cudaEventRecord(ctx->ev[ctx->n_marks], st);
+    ctx->ev_stage[ctx->n_marks++] = stage;
   }
 }
 }  // namespace
@@ -116,26 +122,49 @@ int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int6
       if (precision == FS_PREC_AUTO) return FS_OK;
       return fail(ctx, FS_EUNSUPPORTED, "TF32X3 precision needs fp32 scores");
     }
-    if (!fs::syrk_tc_supported(S, ldS)) {
-      if (precision == FS_PREC_AUTO) return FS_OK;
-      return fail(ctx, FS_EINVAL, "TF32X3 needs a 16-byte aligned S with ldS*4 % 16 == 0");
-    }
     *use_tc = 1;
     return FS_OK;
   }
   return fail(ctx, FS_EINVAL, "unknown precision mode");
 }
 
+// The tiled copy S_t is sized for the context's (n_max, m_max) and allocated on the first
+// TF32X3 use (fp64-only users never pay for it).
+int ensure_tiles(fs_ctx* ctx) {
+  const size_t need = fs::tiles_bytes(ctx->n_max, ctx->m_max);
+  if (ctx->St_bytes >= need) return FS_OK;
+  if (ctx->d_St) cudaFree(ctx->d_St);
+  ctx->d_St = nullptr;
+  ctx->St_bytes = 0;
+  if (cudaMalloc((void**)&ctx->d_St, need) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, FS_ENOMEM, "cannot allocate the tiled copy of S for TF32X3");
+  }
+  ctx->St_bytes = need;
+  return FS_OK;
+}
+
+// Gram stage.  TF32X3: retile S into S_t (optionally fused with u = S w), then the CTA-pair
+// tcgen05 SYRK on S_t.  FP64: exact-product SIMT SYRK on S.
 int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
-              int64_t ldS, double lam, double* Gp, cudaStream_t st) {
+              int64_t ldS, double lam, double* Gp, cudaStream_t st, const float* w32 = nullptr,
+              double* u = nullptr) {
   int use_tc = 0;
   int rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc);
   if (rc) return rc;
   int l = 0;
-  cudaError_t e = use_tc ? fs::syrk_tc((const float*)S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l)
-                         : fs::syrk_simt(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  cudaError_t e;
+  if (use_tc) {
+    if ((rc = ensure_tiles(ctx))) return rc;
+    e = fs::gemv_rows_retile((const float*)S, n, m, ldS, w32, ctx->d_partials, u, ctx->d_St, st, &l);
+    if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
+    if (e == cudaSuccess) e = fs::syrk_tc(ctx->d_St, n, m, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  } else {
+    e = fs::syrk_simt(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  }
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gram");
+  prof_mark(ctx, FS_PROF_GRAM, st);
   return FS_OK;
 }
 
@@ -188,7 +217,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
     fs_ctx_destroy(ctx);
     return FS_ENOMEM;
   }
-  for (int i = 0; i <= FS_PROF_STAGES; ++i) cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; i < fs_ctx::kMaxMarks; ++i) cudaEventCreate(&ctx->ev[i]);
   ctx->ws_bytes = s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + s.r + s.syrk;
   cudaMemset(ctx->d_status, 0, sizeof(int64_t));
   *out = ctx;
@@ -203,8 +232,9 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_potrf);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
-  for (int i = 0; i <= FS_PROF_STAGES; ++i)
+  for (int i = 0; i < fs_ctx::kMaxMarks; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->d_St) cudaFree(ctx->d_St);
   delete ctx;
 }
 
@@ -351,20 +381,28 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     }
   }
   double* u = ctx->d_packed + n * (n + 1) / 2;
-  for (int i = 0; i <= FS_PROF_STAGES; ++i) ctx->ev_used[i] = 0;
-  prof_mark(ctx, 0, st);
-  // 1. partial Gram (no shift) and u = S v, packed for one all-reduce
-  if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
-  prof_mark(ctx, FS_PROF_GRAM + 1, st);
-  if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
-  prof_mark(ctx, FS_PROF_GEMV_SV + 1, st);
+  ctx->n_marks = 0;
+  prof_mark(ctx, -1, st);
+  // 1. partial Gram (no shift) and u = S v, packed for one all-reduce (TF32X3: one fused
+  //    streaming pass computes u and writes the tiled copy the tensor-core SYRK reads)
+  {
+    int use_tc = 0;
+    if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+    if (use_tc && vdt == FS_F32) {
+      if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st, (const float*)v, u))) return rc;
+    } else {
+      if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
+      if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+      prof_mark(ctx, FS_PROF_GEMV_SV, st);
+    }
+  }
   if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
     return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
-  prof_mark(ctx, FS_PROF_ALLREDUCE + 1, st);
+  prof_mark(ctx, FS_PROF_ALLREDUCE, st);
   // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
   if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
   if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
-  prof_mark(ctx, FS_PROF_POTRF + 1, st);
+  prof_mark(ctx, FS_PROF_POTRF, st);
   FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
   {
     int l = 0;
@@ -372,10 +410,10 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     ctx->launches += l;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
-  prof_mark(ctx, FS_PROF_TRSV + 1, st);
+  prof_mark(ctx, FS_PROF_TRSV, st);
   // 3. x = (v - S^T z) / lam on the local shard
   if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
-  prof_mark(ctx, FS_PROF_GEMV_STZ + 1, st);
+  prof_mark(ctx, FS_PROF_GEMV_STZ, st);
   const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
   const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
   double abs_res = NAN, rel_res = NAN;
@@ -394,7 +432,7 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     }
     if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
       return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
-    prof_mark(ctx, FS_PROF_RESIDUAL + 1, st);
+    prof_mark(ctx, FS_PROF_RESIDUAL, st);
     FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
@@ -427,16 +465,13 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     FS_CK(cudaStreamSynchronize(st), "sync");
   }
   if (ctx->prof_on) {
-    // stage k spans the last recorded boundary before it to its own boundary (refinement
-    // passes, when taken, are folded into the residual stage)
-    int prev = 0;
-    for (int k = 0; k < FS_PROF_STAGES; ++k) {
-      ctx->prof_ms[k] = 0.0;
-      if (ctx->ev_used[k + 1]) {
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ctx->ev[prev], ctx->ev[k + 1]) == cudaSuccess) ctx->prof_ms[k] = ms;
-        prev = k + 1;
-      }
+    // each mark closes the stage it names (refinement passes fold into their stages)
+    for (int k = 0; k < FS_PROF_STAGES; ++k) ctx->prof_ms[k] = 0.0;
+    for (int i = 1; i < ctx->n_marks; ++i) {
+      float ms = 0.f;
+      const int sidx = ctx->ev_stage[i];
+      if (sidx >= 0 && sidx < FS_PROF_STAGES && cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]) == cudaSuccess)
+        ctx->prof_ms[sidx] += ms;
     }
   }
   if (*ctx->h_status != 0) {

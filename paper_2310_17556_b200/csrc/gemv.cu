@@ -10,6 +10,7 @@
 // (per-chunk partials reduced in chunk order) so results are bit-reproducible.
 #include "common.cuh"
 #include "kernels.h"
+#include "tiles.cuh"
 
 namespace fs {
 namespace {
@@ -78,6 +79,69 @@ gemv_rows_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
     }
     double s = warp_sum((double)acc);
     if (lane == 0) partials[(int64_t)blockIdx.x * n + i] = s;
+  }
+}
+
+// fp32 u = S w that also writes the tiled copy S_t (tiles.cuh) of the CTA's column chunk:
+// each lane's float4 is exactly one 16-byte chunk of one tile row, so every warp store is
+// four full 128-byte tile rows.  Columns in [m, KB*32) and rows in [n, nb*128) are zeroed.
+__global__ void __launch_bounds__(kRowThreads)
+gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
+                        const float* __restrict__ w, double* __restrict__ partials, uint8_t* __restrict__ St,
+                        int has_w, int vec_ok) {
+  constexpr int VN = 4;
+  constexpr int CW = row_chunk_cols<float>();            // 1024 columns = 32 K-blocks
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * CW;
+  const int64_t nb = tiles_nb(n), KB = tiles_kb(m);
+  float wr[kRowUnroll][VN];
+#pragma unroll
+  for (int u = 0; u < kRowUnroll; ++u)
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      const int64_t c = c0 + (int64_t)(u * kWarp + lane) * VN + e;
+      wr[u][e] = (has_w && c < m) ? w[c] : 0.f;
+    }
+  const bool full = vec_ok && c0 + CW <= m;
+  const int chunk = lane & 7;
+  for (int64_t i = warp; i < nb * kTileRows; i += kRowThreads / kWarp) {
+    float4 buf[kRowUnroll];
+    if (i < n) {
+      const float* row = S + i * ldS + c0;
+      if (full) {
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) buf[u] = ld_stream(reinterpret_cast<const float4*>(row + (u * kWarp + lane) * VN));
+      } else {
+#pragma unroll
+        for (int u = 0; u < kRowUnroll; ++u) {
+          float a[VN];
+#pragma unroll
+          for (int e = 0; e < VN; ++e) {
+            const int64_t c = (int64_t)(u * kWarp + lane) * VN + e;
+            a[e] = (c0 + c < m) ? __ldg(row + c) : 0.f;
+          }
+          buf[u] = make_float4(a[0], a[1], a[2], a[3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) buf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kRowUnroll; ++u) {
+      const int64_t kb = (c0 >> 5) + u * 4 + (lane >> 3);
+      if (kb < KB) *reinterpret_cast<float4*>(St + tile_chunk_offset(nb, kb, i, chunk)) = buf[u];
+    }
+    if (i < n && has_w) {
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        acc = fmaf(buf[u].x, wr[u][0], acc); acc = fmaf(buf[u].y, wr[u][1], acc);
+        acc = fmaf(buf[u].z, wr[u][2], acc); acc = fmaf(buf[u].w, wr[u][3], acc);
+      }
+      const double s = warp_sum((double)acc);
+      if (lane == 0) partials[(int64_t)blockIdx.x * n + i] = s;
+    }
   }
 }
 
@@ -310,6 +374,21 @@ cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, cons
 cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches) {
   widen_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(in, m, out);
   if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                             double* u, uint8_t* St, cudaStream_t st, int* launches) {
+  constexpr int CW = row_chunk_cols<float>();
+  const int64_t chunks = (m + CW - 1) / CW;
+  const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
+  gemv_rows_retile_kernel<<<(unsigned)chunks, kRowThreads, 0, st>>>(S, n, m, ldS, w, partials, St, w != nullptr,
+                                                                     vec_ok);
+  if (launches) *launches += 1;
+  if (w) {
+    reduce_chunks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, chunks, n, u);
+    if (launches) *launches += 1;
+  }
   return cudaGetLastError();
 }
 

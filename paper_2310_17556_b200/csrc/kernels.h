@@ -7,6 +7,9 @@ namespace fs {
 
 // ---- gemv.cu (HBM-bound streaming passes over S) ----
 cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches);
+// fp32 u = S w (w may be NULL: retile only) that also writes the tiled copy S_t (tiles.cuh)
+cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                             double* u, uint8_t* St, cudaStream_t st, int* launches);
 // Number of column chunks the row-GEMV splits m into (partials buffer = chunks * n doubles).
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64);
 cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
@@ -29,9 +32,9 @@ cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
 // ---- syrk_tc.cu (tcgen05 3xTF32 Gram, fp32 input) ----
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);
 size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms);
-bool syrk_tc_supported(const void* S, int64_t ldS);
-cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam,
-                    double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);
+// St: the tiled copy written by gemv_rows_retile
+cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
+                    cudaStream_t st, int* launches);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,

@@ -2,10 +2,11 @@
 //
 // Replaces core.py:284 (numpy A @ A.T -> OpenBLAS dsyrk) for FS_PREC_TF32X3.
 //
-// Precision mode "3xTF32": every fp32 element x is split on the fly into
-//   hi = rna_tf32(x)  (11 significant bits, exact in tf32)   lo = x - hi  (exact in fp32)
-// and each K-step issues three tcgen05.mma.kind::tf32:  lo*hi^T + hi*lo^T + hi*hi^T
-// (the dropped lo*lo^T term is <= 2^-22 relative and unbiased in sign off the diagonal).
+// Precision mode "3xTF32": every fp32 element x is split into hi = trunc_tf32(x) (the tensor
+// core truncates raw fp32 operands to tf32 itself, tools/probe_tf32.py) and lo = x - hi (exact
+// in fp32, written by the converter warps), and each K-step issues three
+// tcgen05.mma.kind::tf32:  lo*hi^T + hi*lo^T + hi*hi^T.  The dropped lo*lo^T term is
+// <= 2^-20 relative; off the diagonal it is sign-random, on the diagonal a ~3e-7 bias.
 // The tensor core's fp32 accumulation truncates (round-toward-zero-like; measured ~2^-25
 // relative per MMA into one accumulator), so the TMEM accumulator is drained every
 // kDrainBlocks K-blocks (24 MMAs) into round-to-nearest fp32 register sums, which are
@@ -21,9 +22,10 @@
 // Split-K over P clusters per pair tile, contiguous K ranges (S streamed ~once from HBM).
 //
 // Roles per CTA (512 threads, setmaxnreg-rebalanced):
-//   warp 0      TMA producer (own boxes, own barrier) + L2 bulk prefetch of 1 KB row spans ahead
+//   warp 0      producer: 1-D bulk copies of its own pre-swizzled 16 KB S_t tiles (tiles.cuh),
+//               own barrier, + L2 bulk prefetch kPfDist K-blocks ahead
 //   warp 1      TMEM allocator (cta_group::2, both CTAs); MMA issuer in the leader CTA only
-//   warps 4-7   converters: raw -> hi in place, lo -> lo ring; release-arrive on the LEADER's
+//   warps 4-7   converters: raw -> lo ring (integer mask + FADD); release-arrive on the LEADER's
 //               conv barrier (mapa), so the leader's MMA sees both CTAs' operands converted
 //   warps 8-15  epilogue: tcgen05.ld own TMEM -> fp32 RN sums -> fp64 partials; release-arrive
 //               on the leader's tempty barrier
@@ -37,25 +39,25 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tiles.cuh"
 
 namespace fs {
 namespace {
 
 constexpr int kBlk = 128;                 // rows per block / per CTA operand box
 constexpr int kN = 256;                   // MMA N (two B halves of 128 rows)
-constexpr int kBK = 32;                   // fp32 columns per K-block (128 B rows, SWIZZLE_128B)
+constexpr int kBK = kTileCols;            // fp32 columns per K-block (128 B rows, SWIZZLE_128B)
 constexpr int kRowBytes = 4 * kBK;
-constexpr int kRaw = 4;                   // raw ring (TMA destination, hi in place)
-constexpr int kLo = 2;                    // lo ring
+constexpr int kRaw = 4;                   // raw ring (TMA destination, read by MMA as hi)
+constexpr int kLo = 3;                    // lo ring (>= 3: the lo slot loop MMA->converter->MMA must not throttle)
 constexpr int kBoxBytes = kBlk * kRowBytes;   // 16 KB
 constexpr int kStageBytes = 2 * kBoxBytes;    // A box + B box
 constexpr int kThreads = 512;
 constexpr int kTmemCols = 2 * kN;         // double-buffered fp32 accumulator
 constexpr int kDrainBlocks = 2;           // 2 x 32 columns = 24 MMAs per drained chunk
 constexpr int kFlushChunks = 64;
-constexpr int kPfSpan = 256 / kBK;        // K-blocks per L2 prefetch span (1 KB per row)
-constexpr int kPfAhead = 2;               // spans kept in flight ahead of the TMA loads
-constexpr int kRegsProducer = 56, kRegsConverter = 64, kRegsEpilogue = 192;
+constexpr int kPfDist = 8;                // K-blocks between an L2 prefetch and its bulk load
+constexpr int kRegsProducer = 56, kRegsConverter = 80, kRegsEpilogue = 184;
 constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 constexpr size_t kSmemBytes = (size_t)(kRaw + kLo) * kStageBytes + 1024 + 512;
 
@@ -79,9 +81,8 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap pmap, int64_t n,
-               int tiles, int P, int KB, int KC, int D, double* __restrict__ accbuf, double* __restrict__ Gp,
-               double lam, int direct, int dbg) {
+syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, int P, int KB, int KC, int D,
+               double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw = smem;
@@ -101,17 +102,15 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRaw; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&conv[s], 2 * 128);
+      ptx::mbar_init(&conv[s], 2);                 // one elected arrive per CTA
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kLo; ++s) ptx::mbar_init(&lo_free[s], 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 2 * 256);
+      ptx::mbar_init(&tempty[b], 2);                // one elected arrive per CTA
     }
     ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tmap);
-    ptx::tma_prefetch_desc(&pmap);
   }
   if (warp == 1) ptx::tmem_alloc2<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
@@ -124,32 +123,28 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
   if (wg == 0) {
     ptx::setmaxnreg_dec<kRegsProducer>();
     if (warp == 0 && lane == 0) {
-      // ======================= TMA producer (each CTA: its own boxes) =======================
+      // ============ bulk-copy producer (each CTA: its own pre-swizzled S_t tiles) ============
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
         int pp, qq; pair_of(t, pp, qq);
-        const int rowA = (2 * pp + (int)crank) * kBlk, rowB = (2 * qq + (int)crank) * kBlk;
-        const bool diag = pp == qq;                       // A == B: one box
+        const int blkA = 2 * pp + (int)crank, blkB = 2 * qq + (int)crank;
+        const bool diag = pp == qq;                       // A == B: one tile
         const uint32_t bytes = (diag ? 1 : 2) * kBoxBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         for (int k = 0; k < nk; ++k) {
-          if (!(dbg & 32) && k % kPfSpan == 0) {
-            for (int a = (k == 0 ? 0 : kPfAhead); a <= kPfAhead; ++a) {
-              const int pk = k + a * kPfSpan;
-              if (pk >= nk) break;
-              const int pcol = (kb0 + pk) * kBK;
-              ptx::tma_prefetch_l2_2d(&pmap, pcol, rowA);
-              if (!diag) ptx::tma_prefetch_l2_2d(&pmap, pcol, rowB);
-            }
+          const size_t krow = (size_t)(kb0 + k) * nbt;
+          if (!(dbg & 32) && k + kPfDist < nk) {
+            const size_t pk = (size_t)(kb0 + k + kPfDist) * nbt;
+            ptx::bulk_prefetch_l2(St + (pk + blkA) * kTileBytes, kTileBytes);
+            if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kTileBytes, kTileBytes);
           }
           ptx::mbar_wait(&empty[rr.s], rr.ph ^ 1);
           if (dbg & 1) { ptx::mbar_arrive(&full[rr.s]); rr.next(kRaw); continue; }
           ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
           uint8_t* st = raw + (size_t)rr.s * kStageBytes;
-          const int col = (kb0 + k) * kBK;
-          ptx::tma_load_2d(st, &tmap, &full[rr.s], col, rowA);
-          if (!diag) ptx::tma_load_2d(st + kBoxBytes, &tmap, &full[rr.s], col, rowB);
+          ptx::bulk_load(st, St + (krow + blkA) * kTileBytes, kTileBytes, &full[rr.s]);
+          if (!diag) ptx::bulk_load(st + kBoxBytes, St + (krow + blkB) * kTileBytes, kTileBytes, &full[rr.s]);
           rr.next(kRaw);
         }
       }
@@ -212,21 +207,24 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
         ptx::mbar_wait(&full[rr.s], rr.ph);
         ptx::mbar_wait(&lo_free[lr.s], lr.ph ^ 1);
         if (!(dbg & 2)) {
-          float4* r4 = reinterpret_cast<float4*>(raw + (size_t)rr.s * kStageBytes);
+          // the tensor core truncates fp32 operands to tf32 (measured: tools/probe_tf32.py), so the
+          // raw tile already IS hi = trunc(x); only lo = x - trunc(x) (exact in fp32) is written
+          const uint4* r4 = reinterpret_cast<const uint4*>(raw + (size_t)rr.s * kStageBytes);
           float4* l4 = reinterpret_cast<float4*>(lo + (size_t)lr.s * kStageBytes);
-#pragma unroll 4
+#pragma unroll 8
           for (int i = ct; i < nvec; i += 128) {
-            const float4 x = r4[i];
-            float4 h, l;
-            h.x = ptx::tf32_rna(x.x); h.y = ptx::tf32_rna(x.y); h.z = ptx::tf32_rna(x.z); h.w = ptx::tf32_rna(x.w);
-            l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-            if (dbg & 64) { l = make_float4(0.f, 0.f, 0.f, 0.f); h = x; }   // probe: raw operand, no lo
-            r4[i] = h;
+            const uint4 x = r4[i];
+            float4 l;
+            l.x = __uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u);
+            l.y = __uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u);
+            l.z = __uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u);
+            l.w = __uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u);
             l4[i] = l;
           }
           ptx::fence_async_smem();
         }
-        ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
+        ptx::named_bar_sync(1, 128);                 // all converter writes of this stage done
+        if (ct == 0) ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
         rr.next(kRaw);
         lr.next(kLo);
       }
@@ -265,7 +263,8 @@ syrk_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
           }
         }
         ptx::tc_fence_before();
-        ptx::mbar_arrive_cluster(tempty0 + b * 8);
+        ptx::named_bar_sync(2, 256);                 // all epilogue TMEM reads of this chunk done
+        if (threadIdx.x == 256) ptx::mbar_arrive_cluster(tempty0 + b * 8);
         ++chunk;
         if (!(dbg & 8) && ((j + 1) % kFlushChunks == 0 || j == nch - 1)) {
 #pragma unroll
@@ -331,22 +330,6 @@ Plan make_plan(int64_t n, int64_t m, int num_sms) {
   return p;
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
 }  // namespace
 
 size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms) {
@@ -365,25 +348,9 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
   return (size_t)num_sms * kBlk * kN * sizeof(double);
 }
 
-cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double lam, double* G_packed, double* ws,
-                    int num_sms, cudaStream_t st, int* launches) {
-  EncodeTiledFn encode = get_encode();
-  if (!encode) return cudaErrorNotSupported;
+cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
+                    cudaStream_t st, int* launches) {
   Plan p = make_plan(n, m, num_sms);
-  CUtensorMap tmap, pmap;
-  const cuuint64_t gdim[2] = {(cuuint64_t)m, (cuuint64_t)n};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ldS * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBlk};
-  const cuuint32_t pbox[2] = {(cuuint32_t)(kBK * kPfSpan), (cuuint32_t)kBlk};
-  const cuuint32_t estride[2] = {1u, 1u};
-  CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(S), gdim, gstride, box, estride,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  cr = encode(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(S), gdim, gstride, pbox, estride,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -391,8 +358,8 @@ cudaError_t syrk_tc(const float* S, int64_t n, int64_t m, int64_t ldS, double la
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
-  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(tmap, pmap, n, p.tiles, p.P, p.KB, p.KC, p.D, ws,
-                                                               G_packed, lam, p.direct ? 1 : 0, dbg);
+  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(St, n, (int)tiles_nb(n), p.tiles, p.P, p.KB, p.KC, p.D,
+                                                               ws, G_packed, lam, p.direct ? 1 : 0, dbg);
   if (launches) *launches += 1;
   if (!p.direct) {
     syrk_tc_reduce<<<2 * p.tiles, 256, 0, st>>>(ws, p.P, n, lam, G_packed);

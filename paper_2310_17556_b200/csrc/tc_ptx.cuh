@@ -47,9 +47,16 @@ FS_DEV uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
 FS_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// release-arrive on an mbarrier given by its shared::cluster address (local or peer CTA)
+// arrive on an mbarrier given by its shared::cluster address (local or peer CTA); default
+// (release, cta) semantics as CUTLASS's ClusterBarrier::arrive(cta_id) — a cluster-scope
+// release here costs ~2x the whole pipeline step
 FS_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// named barrier among `count` threads (id 0 is __syncthreads)
+FS_DEV void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // ---------------- TMA ----------------
@@ -63,6 +70,18 @@ FS_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// 1-D bulk copy global -> shared (contiguous `bytes`, multiple of 16), completes on `bar`.
+FS_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+FS_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
 }
 
 // L2-only prefetch of a 2-D tile (no shared memory, no completion tracking).
