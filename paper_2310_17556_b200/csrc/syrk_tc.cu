@@ -74,6 +74,14 @@ FS_DEVINL void pair_of(int t, int& p, int& q) {  // lower pair tiles (p >= q), r
   q = t - i * (i + 1) / 2;
 }
 
+// lo = x - trunc_tf32(x) (exact in fp32), itself rounded to nearest tf32 (add half an ulp of
+// the kept 10-bit mantissa, then mask) so that the tensor core's own truncation of the lo
+// operand cannot bias the hi*lo terms.  Integer ops only (no cvt).
+FS_DEVINL float tf32_lo(uint32_t xb) {
+  const float lo = __uint_as_float(xb) - __uint_as_float(xb & 0xFFFFE000u);
+  return __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
+}
+
 struct Ring {  // stage index + mbarrier phase of a circular buffer
   int s = 0;
   uint32_t ph = 0;
@@ -170,16 +178,23 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
           ptx::tc_fence_after();
           const uint32_t rs = ptx::smem_u32(raw + (size_t)rr.s * kStageBytes);
           const uint32_t ls = ptx::smem_u32(lo + (size_t)lr.s * kStageBytes);
+          // small correction products first (while this chunk's accumulator is still small, the
+          // tensor core's truncating accumulation loses least), then the four hi*hi products
+          if (!(dbg & 4)) {
 #pragma unroll
-          for (int kk = 0; kk < (dbg & 4 ? 0 : kBK / 8); ++kk) {
-            const uint32_t off = kk * 32;
-            const uint64_t a_hi = ptx::desc_kmajor<kRowBytes>(rs + off);
-            const uint64_t a_lo = ptx::desc_kmajor<kRowBytes>(ls + off);
-            const uint64_t b_hi = ptx::desc_kmajor<kRowBytes>(rs + b_off + off);
-            const uint64_t b_lo = ptx::desc_kmajor<kRowBytes>(ls + b_off + off);
-            ptx::mma2_tf32(dacc, a_lo, b_hi, kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
-            ptx::mma2_tf32(dacc, a_hi, b_lo, kIdesc, 1u);
-            ptx::mma2_tf32(dacc, a_hi, b_hi, kIdesc, 1u);
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint32_t off = kk * 32;
+              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(ls + off), ptx::desc_kmajor<kRowBytes>(rs + b_off + off),
+                             kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
+              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(rs + off), ptx::desc_kmajor<kRowBytes>(ls + b_off + off),
+                             kIdesc, 1u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint32_t off = kk * 32;
+              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(rs + off), ptx::desc_kmajor<kRowBytes>(rs + b_off + off),
+                             kIdesc, 1u);
+            }
           }
           ptx::mma2_commit_mc(&empty[rr.s], 0x3);
           ptx::mma2_commit_mc(&lo_free[lr.s], 0x3);
@@ -215,10 +230,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
           for (int i = ct; i < nvec; i += 128) {
             const uint4 x = r4[i];
             float4 l;
-            l.x = __uint_as_float(x.x) - __uint_as_float(x.x & 0xFFFFE000u);
-            l.y = __uint_as_float(x.y) - __uint_as_float(x.y & 0xFFFFE000u);
-            l.z = __uint_as_float(x.z) - __uint_as_float(x.z & 0xFFFFE000u);
-            l.w = __uint_as_float(x.w) - __uint_as_float(x.w & 0xFFFFE000u);
+            l.x = tf32_lo(x.x); l.y = tf32_lo(x.y); l.z = tf32_lo(x.z); l.w = tf32_lo(x.w);
             l4[i] = l;
           }
           ptx::fence_async_smem();
