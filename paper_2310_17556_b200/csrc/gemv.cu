@@ -145,14 +145,30 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
   }
 }
 
-// out[i] = sum_{c=0..C-1} partials[c*n + i], fixed order.
-__global__ void reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_t n,
-                                     double* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double s = 0.0;
-  for (int64_t c = 0; c < chunks; ++c) s += partials[c * n + i];
-  out[i] = s;
+// out[i] = sum_{c=0..C-1} partials[c*n + i], fixed order: block = 32 rows; warp w sums the
+// chunks c = w, w+8, ... (coalesced 256-byte rows), then the 8 warp sums in warp order.
+constexpr int kRedRows = 32, kRedWarps = 8;
+__global__ void __launch_bounds__(kRedRows * kRedWarps)
+reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_t n, double* __restrict__ out) {
+  __shared__ double part[kRedWarps][kRedRows];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kRedRows + lane;
+  double s0 = 0.0, s1 = 0.0;
+  if (i < n) {
+    int64_t c = w;
+    for (; c + kRedWarps < chunks; c += 2 * kRedWarps) {
+      s0 += partials[c * n + i];
+      s1 += partials[(c + kRedWarps) * n + i];
+    }
+    if (c < chunks) s0 += partials[c * n + i];
+  }
+  part[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && i < n) {
+    double s = 0.0;
+    for (int k = 0; k < kRedWarps; ++k) s += part[k][lane];
+    out[i] = s;
+  }
 }
 
 // One thread owns VN consecutive columns and walks all n rows.
@@ -330,7 +346,7 @@ cudaError_t gemv_rows_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const vo
     if (vec) gemv_rows_kernel<TS, float, true><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
     else gemv_rows_kernel<TS, float, false><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
   }
-  reduce_chunks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, chunks, n, u);
+  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n, u);
   if (launches) *launches += 2;
   return cudaGetLastError();
 }
@@ -386,7 +402,7 @@ cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, 
                                                                      vec_ok);
   if (launches) *launches += 1;
   if (w) {
-    reduce_chunks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(partials, chunks, n, u);
+    reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n, u);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();

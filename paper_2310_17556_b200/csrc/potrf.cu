@@ -81,64 +81,93 @@ __device__ void invert_64(const double (*L)[kLd], double (*X)[kLd], double (*T)[
   __syncthreads();
 }
 
-// In-place Cholesky of the identity-padded 64x64 block A (smem, lower) by all 256 threads with
-// ONE barrier per column: step j updates A[r][c] -= A[r][j] A[c][j] / A[j][j] (unscaled pivot
-// column, never rewritten inside the step), and a final pass scales L[r][c] = A[r][c]/sqrt(d_c).
-// Sets *fail to the first bad local pivot (or -1).
+// In-place Cholesky of the identity-padded 64x64 block A (smem, lower) by 256 threads.
+// Thread (r = tid/4, q = tid%4) keeps its row's 16 elements A[r][q + 4cc] in REGISTERS for the
+// whole factorisation (smem round trips through an aliased array serialise at ~50 cycles each).
+// Step j: the pivot column j lives in a double-buffered smem vector col[] written by its owners
+// at the end of step j-1, together with 1/d_j computed (one __drcp_rn) by the thread that
+// finalised A[j][j]; one barrier per column.  Unscaled update A[r][c] -= A[r][j] A[c][j] / d_j;
+// a final pass scales L[r][c] = A[r][c] * rsqrt(d_c).  Sets *fail (first bad pivot or -1).
 __device__ void factor_block(double (*A)[kLd], int b, int* fail) {
+  __shared__ double col[2][kNB];
+  __shared__ double dinv[2];
+  __shared__ double dval[kNB];
   const int tid = threadIdx.x, r = tid >> 2, q = tid & 3;
-  if (tid == 0) *fail = -1;
+  double a[kNB / 4];
+#pragma unroll
+  for (int cc = 0; cc < kNB / 4; ++cc) a[cc] = A[r][q + 4 * cc];
+  if (q == 0) col[0][r] = A[r][0];
+  if (tid == 0) {
+    *fail = -1;
+    dinv[0] = __drcp_rn(A[0][0]);
+  }
 #pragma unroll 1
   for (int j = 0; j < b; ++j) {
     __syncthreads();
-    const double d = A[j][j];
-    if (!(d > 0.0)) {                 // every thread sees the same d: uniform exit
+    const int buf = j & 1;
+    const double d = col[buf][j];
+    if (!(d > 0.0)) {                  // uniform: every thread reads the same pivot
       if (tid == 0) *fail = j;
       __syncthreads();
       return;
     }
-    if (r > j) {
-      const double s = A[r][j] / d;
+    if (tid == 0) dval[j] = d;
+    const double s = (r > j) ? col[buf][r] * dinv[buf] : 0.0;
+    double cj[kNB / 4];
 #pragma unroll
-      for (int cc = 0; cc < kNB / 4; ++cc) {
-        const int c = q + 4 * cc;
-        if (c > j && c <= r) A[r][c] = fma(-s, A[c][j], A[r][c]);
+    for (int cc = 0; cc < kNB / 4; ++cc) cj[cc] = col[buf][q + 4 * cc];
+#pragma unroll
+    for (int cc = 0; cc < kNB / 4; ++cc) {
+      const int c = q + 4 * cc;
+      if (r > j && c > j && c <= r) a[cc] = fma(-s, cj[cc], a[cc]);
+      // publish column j+1 (final after this update) and its pivot reciprocal; predicated
+      // stores with a compile-time register index keep a[] out of local memory
+      if (c == j + 1 && j + 1 < b) {
+        col[buf ^ 1][r] = a[cc];
+        if (r == j + 1) dinv[buf ^ 1] = __drcp_rn(a[cc]);
       }
     }
   }
-  __shared__ double sq[kNB];
   __syncthreads();
-  if (tid < kNB) sq[tid] = (tid < b) ? sqrt(A[tid][tid]) : 1.0;
-  __syncthreads();
-  // scale: L[c][c] = sqrt(d_c), L[r][c] = A[r][c] / sqrt(d_c)
-  for (int e = tid; e < kNB * kNB; e += kThreads) {
-    const int rr = e >> 6, c = e & 63;
-    if (c < b && rr >= c) A[rr][c] = (rr == c) ? sq[c] : A[rr][c] / sq[c];
-  }
-  __syncthreads();
-  for (int e = tid; e < kNB * kNB; e += kThreads) {   // restore identity padding of the diagonal
-    const int rr = e >> 6, c = e & 63;
-    if (rr >= b && rr == c) A[rr][c] = 1.0;
+  // scale: L[r][c] = A[r][c] * rsqrt(d_c) (diagonal: d_c * rsqrt(d_c) = sqrt(d_c))
+#pragma unroll
+  for (int cc = 0; cc < kNB / 4; ++cc) {
+    const int c = q + 4 * cc;
+    double v = (c <= r) ? a[cc] : 0.0;
+    if (c < b && c <= r) v *= rsqrt(dval[c]);
+    if (r >= b || c >= b) v = (r == c) ? 1.0 : 0.0;   // identity padding
+    A[r][c] = v;
   }
   __syncthreads();
 }
 
-// X <- X L^-T (each of the 64 rows of X solved against the lower 64x64 L; 4 threads per row).
+// X <- X L^-T: each of the 64 rows of X solved against the lower 64x64 L (rdiag = 1/L_jj).
+// Thread (r, q) handles columns p = q + 4cc of row r.  Step j issues its 32 smem loads up
+// front (X[r][.] and L[j][.], all independent), four predicated FMA chains, a 4-lane shuffle
+// reduction, and the owner lane stores x_j: one store per step, so nothing serialises on
+// smem aliasing.  No block barriers (a row lives in one warp).
 __device__ void trsm_rows(const double (*L)[kLd], const double* rdiag, double (*X)[kLd]) {
-  const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int tid = threadIdx.x, r = tid >> 2, q = tid & 3;
 #pragma unroll 1
   for (int j = 0; j < kNB; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-    int p = q;
-    for (; p + 4 < j; p += 8) {
-      s0 = fma(X[r][p], L[j][p], s0);
-      s1 = fma(X[r][p + 4], L[j][p + 4], s1);
+    double xv[kNB / 4], lj[kNB / 4];
+#pragma unroll
+    for (int cc = 0; cc < kNB / 4; ++cc) {
+      xv[cc] = X[r][q + 4 * cc];
+      lj[cc] = L[j][q + 4 * cc];
     }
-    if (p < j) s0 = fma(X[r][p], L[j][p], s0);
-    s0 += s1;
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
-    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
-    if (q == 0) X[r][j] = (X[r][j] - s0) * rdiag[j];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < kNB / 4; cc += 4) {
+      if (q + 4 * cc < j) s0 = fma(xv[cc], lj[cc], s0);
+      if (q + 4 * (cc + 1) < j) s1 = fma(xv[cc + 1], lj[cc + 1], s1);
+      if (q + 4 * (cc + 2) < j) s2 = fma(xv[cc + 2], lj[cc + 2], s2);
+      if (q + 4 * (cc + 3) < j) s3 = fma(xv[cc + 3], lj[cc + 3], s3);
+    }
+    double sum = (s0 + s1) + (s2 + s3);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (q == (j & 3)) X[r][j] = (X[r][j] - sum) * rdiag[j];
     __syncwarp();
   }
 }

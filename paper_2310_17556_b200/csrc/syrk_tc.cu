@@ -312,16 +312,19 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
 
 // Fixed-order sum of the P split-K partial tiles -> packed lower Gram (+λ on the diagonal).
 // Block (t, c): pair tile t, CTA half c (row block 2p+c).
+constexpr int kRedSplit = 16;   // blocks per (pair tile, CTA half): 2048 elements each
 __global__ void syrk_tc_reduce(const double* __restrict__ ws, int P, int64_t n, double lam, double* __restrict__ Gp) {
+  const int tc = blockIdx.x / kRedSplit, part = blockIdx.x % kRedSplit;
   int pp, qq;
-  pair_of(blockIdx.x >> 1, pp, qq);
-  const int c = blockIdx.x & 1;
-  for (int e = threadIdx.x; e < kBlk * kN; e += blockDim.x) {
+  pair_of(tc >> 1, pp, qq);
+  const int c = tc & 1;
+  constexpr int kPer = kBlk * kN / kRedSplit;
+  for (int e = part * kPer + threadIdx.x; e < (part + 1) * kPer; e += blockDim.x) {
     const int col = e / kBlk, r = e % kBlk;
     const int64_t gi = (int64_t)(2 * pp + c) * kBlk + r, gj = (int64_t)(2 * qq) * kBlk + col;
     if (gi >= n || gj > gi) continue;
     double s = 0.0;
-    for (int q = 0; q < P; ++q) s += ws[(((size_t)(blockIdx.x >> 1) * P + q) * 2 + c) * kBlk * kN + e];
+    for (int q = 0; q < P; ++q) s += ws[(((size_t)(tc >> 1) * P + q) * 2 + c) * kBlk * kN + e];
     Gp[gi * (gi + 1) / 2 + gj] = s + (gi == gj ? lam : 0.0);
   }
 }
@@ -374,7 +377,7 @@ cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double*
                                                                ws, G_packed, lam, p.direct ? 1 : 0, dbg);
   if (launches) *launches += 1;
   if (!p.direct) {
-    syrk_tc_reduce<<<2 * p.tiles, 256, 0, st>>>(ws, p.P, n, lam, G_packed);
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.P, n, lam, G_packed);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
