@@ -128,45 +128,85 @@ def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.T
     return t
 
 
+def _coerce_host(a, name: str) -> np.ndarray:
+    """numpy side of core.py:108-119: numeric dtype -> C-contiguous float32/float64 (no copy when it
+    already is one).  Finiteness is checked on the device during the upload (fs_chol_solve_host)."""
+    arr = np.asarray(a)
+    if np.iscomplexobj(arr):
+        raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
+    if not (np.issubdtype(arr.dtype, np.number) or arr.dtype == np.bool_):
+        raise ValueError(f"{name} must be numeric, got dtype {arr.dtype}")
+    if arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
+    return np.ascontiguousarray(arr)
+
+
 class ScoreMatrix:
-    """Dense n-by-m score matrix, one sample per row, resident on a CUDA device (core.py:122-162)."""
+    """Dense n-by-m score matrix, one sample per row (core.py:122-162).
+
+    A CUDA tensor is copied once onto an aligned device buffer and validated immediately.  A host
+    array (numpy, lists) stays on the host until first use: solve_chol streams it to the GPU in
+    row chunks overlapped with the Gram (fs_chol_solve_host) and checks finiteness there, so a
+    non-finite entry raises the reference's ValueError from that first call.  The host array is
+    read at that point, not copied at construction.
+    """
 
     def __init__(self, data, device=None):
         src = data
-        aliasable = isinstance(src, torch.Tensor) and src.is_cuda
-        t = _to_device_tensor(data, "score matrix", device, force_copy=aliasable)
-        if t.dim() != 2:
-            raise ValueError(f"score matrix must be 2-D, got shape {tuple(t.shape)}")
-        if t.shape[0] < 1 or t.shape[1] < 1:
-            raise ValueError(f"score matrix needs at least one row and column, got {tuple(t.shape)}")
-        self._t = t
         self._host = None
+        self._t = None
+        self._device = device
+        if isinstance(src, torch.Tensor):
+            t = _to_device_tensor(data, "score matrix", device, force_copy=src.is_cuda)
+            shape = tuple(t.shape)
+            self._t = t
+        else:
+            arr = _coerce_host(data, "score matrix")
+            shape = arr.shape
+            self._src = arr
+        if len(shape) != 2:
+            raise ValueError(f"score matrix must be 2-D, got shape {shape}")
+        if shape[0] < 1 or shape[1] < 1:
+            raise ValueError(f"score matrix needs at least one row and column, got {shape}")
+        self._shape = (int(shape[0]), int(shape[1]))
         # numpy in -> numpy out (drop-in semantics); CUDA tensor in -> CUDA tensor out
         self.host_origin = not (isinstance(src, torch.Tensor) and src.is_cuda)
 
     @property
+    def is_uploaded(self) -> bool:
+        return self._t is not None
+
+    @property
+    def host_array(self) -> np.ndarray | None:
+        """The C-contiguous host array of a host-origin matrix that has not been uploaded yet."""
+        return None if self._t is not None else self._src
+
+    @property
     def tensor(self) -> torch.Tensor:
+        if self._t is None:
+            self._t = _to_device_tensor(self._src, "score matrix", self._device)
+            self._src = None
         return self._t
 
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            h = self._t.cpu().numpy()
+            h = self._src.view() if self._t is None else self._t.cpu().numpy()
             h.flags.writeable = False
             self._host = h
         return self._host
 
     @property
     def n(self) -> int:
-        return int(self._t.shape[0])
+        return self._shape[0]
 
     @property
     def m(self) -> int:
-        return int(self._t.shape[1])
+        return self._shape[1]
 
     @property
     def shape(self) -> tuple[int, int]:
-        return (self.n, self.m)
+        return self._shape
 
     @property
     def is_complex(self) -> bool:
@@ -174,11 +214,19 @@ class ScoreMatrix:
 
     @property
     def dtype(self) -> torch.dtype:
-        return self._t.dtype
+        if self._t is not None:
+            return self._t.dtype
+        return torch.float32 if self._src.dtype == np.float32 else torch.float64
+
+    @property
+    def device(self) -> torch.device:
+        if self._t is not None:
+            return self._t.device
+        return self._device if self._device is not None else default_device()
 
     @property
     def scalar_kind(self) -> ScalarKind:
-        return ScalarKind.REAL64 if self._t.dtype == torch.float64 else ScalarKind.REAL32
+        return ScalarKind.REAL64 if self.dtype == torch.float64 else ScalarKind.REAL32
 
 
 class DampedSystem:
@@ -191,6 +239,20 @@ class DampedSystem:
         self.lam = _coerce_damping(lam)
         if isinstance(v, torch.Tensor) and v.is_complex() or (not isinstance(v, torch.Tensor) and np.iscomplexobj(np.asarray(v))):
             raise ValueError("real score matrix with complex right-hand side")
+        self._v = None
+        self._vh = None
+        self._host_v = None
+        if not S.is_uploaded and not (isinstance(v, torch.Tensor) and v.is_cuda):
+            # host system: v stays on the host beside S (validated here, it is small)
+            vh = _coerce_host(v.numpy() if isinstance(v, torch.Tensor) else v, "right-hand side")
+            if vh.ndim != 1:
+                raise ValueError(f"right-hand side must be 1-D, got shape {vh.shape}")
+            if vh.shape[0] != S.m:
+                raise ValueError(f"right-hand side length {vh.shape[0]} does not match parameter count {S.m}")
+            if not np.isfinite(vh).all():
+                raise ValueError("right-hand side must contain only finite entries")
+            self._vh = np.ascontiguousarray(vh, dtype=np.float32 if S.dtype == torch.float32 else np.float64)
+            return
         t = _to_device_tensor(v, "right-hand side", S.tensor.device,
                               force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
         if t.dim() != 1:
@@ -198,16 +260,22 @@ class DampedSystem:
         if t.shape[0] != S.m:
             raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
         self._v = t.to(S.dtype)
-        self._host_v = None
+
+    @property
+    def host_v(self) -> np.ndarray | None:
+        """v on the host (S's dtype) while the system has not been uploaded."""
+        return self._vh if self._v is None else None
 
     @property
     def v_tensor(self) -> torch.Tensor:
+        if self._v is None:
+            self._v = torch.from_numpy(self._vh).to(self.S.tensor.device)
         return self._v
 
     @property
     def v(self) -> np.ndarray:
         if self._host_v is None:
-            h = self._v.cpu().numpy()
+            h = self._vh.view() if self._v is None else self._v.cpu().numpy()
             h.flags.writeable = False
             self._host_v = h
         return self._host_v

@@ -42,6 +42,18 @@ struct fs_ctx {
   std::string err;
   uint8_t* d_St = nullptr;      // tiled fp32 copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
+  // host-buffer entry (fs_chol_solve_host): device copies of S, v, x, an upload stream and
+  // one event per uploaded row chunk (all lazy)
+  void* d_Sin = nullptr;
+  size_t Sin_bytes = 0;
+  double* d_vin = nullptr;      // m_max doubles (holds v in its own dtype)
+  double* d_xin = nullptr;      // m_max doubles
+  int* d_flag = nullptr;        // non-finite input flag
+  int* h_flag = nullptr;        // pinned
+  cudaStream_t up_st = nullptr;
+  static constexpr int kMaxChunks = 64;
+  cudaEvent_t ev_chunk[kMaxChunks] = {};
+  cudaEvent_t ev_free = nullptr;
   // stage timing (fs_profile_enable): events recorded on the solve stream after each stage,
   // in chronological order; stage time = gap to the previous mark
   static constexpr int kMaxMarks = 24;
@@ -170,6 +182,101 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
 
 }  // namespace
 
+// Everything after the Gram/u stage of _solve_chol_impl: all-reduce, potrf, _chol_apply,
+// residual, optional refinement, status + norms read-back (one host synchronisation per pass).
+static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
+               double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
+               double refine_above, int64_t* pivot, double* out_res, cudaStream_t st) {
+  int rc = FS_OK;
+  void* stream = (void*)st;
+  double* u = ctx->d_packed + n * (n + 1) / 2;
+  if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
+    return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
+  prof_mark(ctx, FS_PROF_ALLREDUCE, st);
+  // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
+  if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
+  if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
+  prof_mark(ctx, FS_PROF_POTRF, st);
+  FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
+  {
+    int l = 0;
+    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
+  }
+  prof_mark(ctx, FS_PROF_TRSV, st);
+  // 3. x = (v - S^T z) / lam on the local shard
+  if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
+  prof_mark(ctx, FS_PROF_GEMV_STZ, st);
+  const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
+  const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
+  double abs_res = NAN, rel_res = NAN;
+  for (int pass = 0; want_res && pass < 2; ++pass) {
+    // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
+    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
+    if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of y failed");
+    {
+      int l = 0;
+      cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
+                                        want_refine && pass == 0 ? ctx->d_r : nullptr, ctx->d_block_sums,
+                                        ctx->d_sums, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
+    }
+    if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
+    prof_mark(ctx, FS_PROF_RESIDUAL, st);
+    FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
+    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+    if (*ctx->h_status != 0) break;
+    abs_res = sqrt(ctx->h_sums[0]);
+    rel_res = abs_res / std::max(sqrt(ctx->h_sums[1]), kEps);
+    if (pass == 1 || !want_refine || !(rel_res > refine_above)) break;
+    // one correction pass with the same factor (solvers.py:183-194): d = chol_apply(-r)
+    // residual_cols stored r = (S^T y + lam x) - v; refinement right-hand side is -r
+    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream))) return rc;
+    if (allreduce && allreduce(ctx->d_z, n, allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
+    {
+      int l = 0;
+      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
+    }
+    // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
+    {
+      int l = 0;
+      cudaError_t e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, ctx->d_z, ctx->d_r, true, -lam,
+                                          true, x, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve (refine)");
+    }
+  }
+  if (!want_res) {
+    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+  }
+  if (ctx->prof_on) {
+    // each mark closes the stage it names (refinement passes fold into their stages)
+    for (int k = 0; k < FS_PROF_STAGES; ++k) ctx->prof_ms[k] = 0.0;
+    for (int i = 1; i < ctx->n_marks; ++i) {
+      float ms = 0.f;
+      const int sidx = ctx->ev_stage[i];
+      if (sidx >= 0 && sidx < FS_PROF_STAGES && cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]) == cudaSuccess)
+        ctx->prof_ms[sidx] += ms;
+    }
+  }
+  if (*ctx->h_status != 0) {
+    if (pivot) *pivot = *ctx->h_status - 1;
+    return fail(ctx, FS_NOT_PD, "Gram matrix is not positive definite at pivot " + std::to_string(*ctx->h_status - 1));
+  }
+  if (out_res) { out_res[0] = abs_res; out_res[1] = rel_res; }
+  return FS_OK;
+}
+
+
 extern "C" {
 
 const char* fs_version(void) { return "fisher-b200 0.1.0 sm_100a"; }
@@ -235,6 +342,15 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   for (int i = 0; i < fs_ctx::kMaxMarks; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->d_St) cudaFree(ctx->d_St);
+  if (ctx->d_Sin) cudaFree(ctx->d_Sin);
+  if (ctx->d_vin) cudaFree(ctx->d_vin);
+  if (ctx->d_xin) cudaFree(ctx->d_xin);
+  if (ctx->d_flag) cudaFree(ctx->d_flag);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  for (int i = 0; i < fs_ctx::kMaxChunks; ++i)
+    if (ctx->ev_chunk[i]) cudaEventDestroy(ctx->ev_chunk[i]);
+  if (ctx->ev_free) cudaEventDestroy(ctx->ev_free);
+  if (ctx->up_st) cudaStreamDestroy(ctx->up_st);
   delete ctx;
 }
 
@@ -396,90 +512,110 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
       prof_mark(ctx, FS_PROF_GEMV_SV, st);
     }
   }
-  if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
-    return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
-  prof_mark(ctx, FS_PROF_ALLREDUCE, st);
-  // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
-  if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
-  if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
-  prof_mark(ctx, FS_PROF_POTRF, st);
-  FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
-  {
-    int l = 0;
-    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
+  return solve_tail(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
+                    out_res, st);
+}
+
+int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host, int64_t n, int64_t m,
+                       int64_t ldS, const void* v_host, double lam, double* x_host, fs_allreduce_fn allreduce,
+                       void* allreduce_user, int flags, double refine_above, int64_t* pivot,
+                       double* out_res, void* stream) {
+  int rc = check_shape(ctx, dtype, S_host, n, m, ldS);
+  if (rc) return rc;
+  if ((rc = check_lam(ctx, lam))) return rc;
+  if (!v_host || !x_host) return fail(ctx, FS_EINVAL, "NULL vector");
+  if (pivot) *pivot = -1;
+  int use_tc = 0;
+  if ((rc = resolve_precision(ctx, dtype, precision, S_host, ldS, &use_tc))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t elem = dtype == FS_F64 ? 8 : 4;
+  const int64_t per16 = 16 / (int64_t)elem;
+  const int64_t ldd = (m + per16 - 1) / per16 * per16;   // device rows start on 16-byte boundaries
+  const size_t need = (size_t)n * ldd * elem;
+  // ---- lazy resources ----
+  if (ctx->Sin_bytes < need) {
+    if (ctx->d_Sin) { cudaStreamSynchronize(st); cudaFree(ctx->d_Sin); }
+    ctx->d_Sin = nullptr;
+    ctx->Sin_bytes = 0;
+    if (cudaMalloc(&ctx->d_Sin, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, FS_ENOMEM, "cannot allocate the device copy of S");
+    }
+    ctx->Sin_bytes = need;
+  }
+  if (!ctx->d_vin) {
+    bool ok = cudaMalloc((void**)&ctx->d_vin, ctx->m_max * sizeof(double)) == cudaSuccess &&
+              cudaMalloc((void**)&ctx->d_xin, ctx->m_max * sizeof(double)) == cudaSuccess &&
+              cudaMalloc((void**)&ctx->d_flag, sizeof(int)) == cudaSuccess &&
+              cudaMallocHost((void**)&ctx->h_flag, sizeof(int)) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ctx->up_st, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_free, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < fs_ctx::kMaxChunks; ++i)
+      ok = cudaEventCreateWithFlags(&ctx->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      cudaGetLastError();
+      return fail(ctx, FS_ENOMEM, "cannot allocate the host-entry buffers");
+    }
+  }
+  if (use_tc && (rc = ensure_tiles(ctx))) return rc;
+  ctx->n_marks = 0;
+  prof_mark(ctx, -1, st);
+  FS_CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st), "flag reset");
+  FS_CK(cudaMemcpyAsync(ctx->d_vin, v_host, m * elem, cudaMemcpyHostToDevice, st), "v h2d");
+  int l = 0;
+  FS_CK(fs::check_finite(ctx->d_vin, dtype == FS_F64, 1, m, m, ctx->d_flag, ctx->num_sms, st, &l), "check v");
+  // the upload stream must not overwrite d_Sin while earlier work on `st` still reads it
+  FS_CK(cudaEventRecord(ctx->ev_free, st), "event");
+  FS_CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_free, 0), "event wait");
+  const int64_t hpitch = ldS * (int64_t)elem, dpitch = ldd * (int64_t)elem;
+  auto upload = [&](int64_t r0, int64_t r1, int ev) -> cudaError_t {
+    const char* src = (const char*)S_host + r0 * hpitch;
+    char* dst = (char*)ctx->d_Sin + r0 * dpitch;
+    cudaError_t e = (hpitch == dpitch)
+                        ? cudaMemcpyAsync(dst, src, (size_t)(r1 - r0) * hpitch, cudaMemcpyHostToDevice, ctx->up_st)
+                        : cudaMemcpy2DAsync(dst, dpitch, src, hpitch, m * elem, r1 - r0, cudaMemcpyHostToDevice,
+                                            ctx->up_st);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[ev], ctx->up_st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_chunk[ev], 0);
+    return e;
+  };
+  const void* S = ctx->d_Sin;
+  const void* v = ctx->d_vin;
+  double* x = ctx->d_xin;
+  if (use_tc) {
+    // per 256-row pair chunk: upload -> (retile + u rows + non-finite check) -> SYRK pair row
+    double* u = ctx->d_packed + n * (n + 1) / 2;
+    const int np = (int)((n + 2 * fs::kTileRows - 1) / (2 * fs::kTileRows));
+    for (int p = 0; p < np; ++p) {
+      const int64_t r0 = (int64_t)p * 2 * fs::kTileRows;
+      const int64_t r1 = std::min<int64_t>(n, r0 + 2 * fs::kTileRows);
+      FS_CK(upload(r0, r1, p % fs_ctx::kMaxChunks), "S h2d");
+      FS_CK(fs::gemv_rows_retile((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, u, ctx->d_St, st, &l,
+                                 r0, r1, ctx->d_flag),
+            "retile");
+      FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, p, p + 1),
+            "syrk_tc");
+    }
     ctx->launches += l;
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
+    prof_mark(ctx, FS_PROF_GRAM, st);
+    rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
+                    pivot, out_res, st);
+  } else {
+    FS_CK(upload(0, n, 0), "S h2d");
+    FS_CK(fs::check_finite(S, dtype == FS_F64, n, m, ldd, ctx->d_flag, ctx->num_sms, st, &l), "check S");
+    ctx->launches += l;
+    rc = fs_chol_solve(ctx, dtype, precision, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
+                       refine_above, pivot, out_res, stream);
   }
-  prof_mark(ctx, FS_PROF_TRSV, st);
-  // 3. x = (v - S^T z) / lam on the local shard
-  if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
-  prof_mark(ctx, FS_PROF_GEMV_STZ, st);
-  const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
-  const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
-  double abs_res = NAN, rel_res = NAN;
-  for (int pass = 0; want_res && pass < 2; ++pass) {
-    // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
-    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
-    if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
-      return fail(ctx, FS_ECUDA, "allreduce of y failed");
-    {
-      int l = 0;
-      cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
-                                        want_refine && pass == 0 ? ctx->d_r : nullptr, ctx->d_block_sums,
-                                        ctx->d_sums, st, &l);
-      ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
-    }
-    if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
-      return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
-    prof_mark(ctx, FS_PROF_RESIDUAL, st);
-    FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
-    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
-    FS_CK(cudaStreamSynchronize(st), "sync");
-    if (*ctx->h_status != 0) break;
-    abs_res = sqrt(ctx->h_sums[0]);
-    rel_res = abs_res / std::max(sqrt(ctx->h_sums[1]), kEps);
-    if (pass == 1 || !want_refine || !(rel_res > refine_above)) break;
-    // one correction pass with the same factor (solvers.py:183-194): d = chol_apply(-r)
-    // residual_cols stored r = (S^T y + lam x) - v; refinement right-hand side is -r
-    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream))) return rc;
-    if (allreduce && allreduce(ctx->d_z, n, allreduce_user, stream) != 0)
-      return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
-    {
-      int l = 0;
-      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
-      ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
-    }
-    // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
-    {
-      int l = 0;
-      cudaError_t e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, ctx->d_z, ctx->d_r, true, -lam,
-                                          true, x, st, &l);
-      ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve (refine)");
-    }
+  if (rc != FS_OK && rc != FS_NOT_PD) return rc;
+  FS_CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
+  if (rc == FS_OK) FS_CK(cudaMemcpyAsync(x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, st), "x d2h");
+  FS_CK(cudaStreamSynchronize(st), "sync");
+  if (*ctx->h_flag) {
+    if (pivot) *pivot = -1;
+    return fail(ctx, FS_EINVAL, "score matrix and right-hand side must contain only finite entries");
   }
-  if (!want_res) {
-    FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
-    FS_CK(cudaStreamSynchronize(st), "sync");
-  }
-  if (ctx->prof_on) {
-    // each mark closes the stage it names (refinement passes fold into their stages)
-    for (int k = 0; k < FS_PROF_STAGES; ++k) ctx->prof_ms[k] = 0.0;
-    for (int i = 1; i < ctx->n_marks; ++i) {
-      float ms = 0.f;
-      const int sidx = ctx->ev_stage[i];
-      if (sidx >= 0 && sidx < FS_PROF_STAGES && cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]) == cudaSuccess)
-        ctx->prof_ms[sidx] += ms;
-    }
-  }
-  if (*ctx->h_status != 0) {
-    if (pivot) *pivot = *ctx->h_status - 1;
-    return fail(ctx, FS_NOT_PD, "Gram matrix is not positive definite at pivot " + std::to_string(*ctx->h_status - 1));
-  }
-  if (out_res) { out_res[0] = abs_res; out_res[1] = rel_res; }
-  return FS_OK;
+  return rc;
 }
 
 }  // extern "C"

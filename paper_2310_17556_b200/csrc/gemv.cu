@@ -88,7 +88,7 @@ gemv_rows_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 __global__ void __launch_bounds__(kRowThreads)
 gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
                         const float* __restrict__ w, double* __restrict__ partials, uint8_t* __restrict__ St,
-                        int has_w, int vec_ok) {
+                        int has_w, int vec_ok, int64_t r0, int64_t r1, int64_t rz, int* __restrict__ nonfinite) {
   constexpr int VN = 4;
   constexpr int CW = row_chunk_cols<float>();            // 1024 columns = 32 K-blocks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -104,9 +104,11 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
     }
   const bool full = vec_ok && c0 + CW <= m;
   const int chunk = lane & 7;
-  for (int64_t i = warp; i < nb * kTileRows; i += kRowThreads / kWarp) {
+  // rows [r0, r1) are read from S; rows [r1, rz) are zero padding of the tiled copy
+  bool bad = false;
+  for (int64_t i = r0 + warp; i < rz; i += kRowThreads / kWarp) {
     float4 buf[kRowUnroll];
-    if (i < n) {
+    if (i < r1) {
       const float* row = S + i * ldS + c0;
       if (full) {
 #pragma unroll
@@ -131,8 +133,9 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
     for (int u = 0; u < kRowUnroll; ++u) {
       const int64_t kb = (c0 >> 5) + u * 4 + (lane >> 3);
       if (kb < KB) *reinterpret_cast<float4*>(St + tile_chunk_offset(nb, kb, i, chunk)) = buf[u];
+      bad |= !(isfinite(buf[u].x) && isfinite(buf[u].y) && isfinite(buf[u].z) && isfinite(buf[u].w));
     }
-    if (i < n && has_w) {
+    if (i < r1 && has_w) {
       float acc = 0.f;
 #pragma unroll
       for (int u = 0; u < kRowUnroll; ++u) {
@@ -143,13 +146,15 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
       if (lane == 0) partials[(int64_t)blockIdx.x * n + i] = s;
     }
   }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
 }
 
 // out[i] = sum_{c=0..C-1} partials[c*n + i], fixed order: block = 32 rows; warp w sums the
 // chunks c = w, w+8, ... (coalesced 256-byte rows), then the 8 warp sums in warp order.
 constexpr int kRedRows = 32, kRedWarps = 8;
 __global__ void __launch_bounds__(kRedRows * kRedWarps)
-reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_t n, double* __restrict__ out) {
+reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_t n, int64_t stride,
+                     double* __restrict__ out) {
   __shared__ double part[kRedWarps][kRedRows];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * kRedRows + lane;
@@ -157,10 +162,10 @@ reduce_chunks_kernel(const double* __restrict__ partials, int64_t chunks, int64_
   if (i < n) {
     int64_t c = w;
     for (; c + kRedWarps < chunks; c += 2 * kRedWarps) {
-      s0 += partials[c * n + i];
-      s1 += partials[(c + kRedWarps) * n + i];
+      s0 += partials[c * stride + i];
+      s1 += partials[(c + kRedWarps) * stride + i];
     }
-    if (c < chunks) s0 += partials[c * n + i];
+    if (c < chunks) s0 += partials[c * stride + i];
   }
   part[w][lane] = s0 + s1;
   __syncthreads();
@@ -323,6 +328,19 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ block_sums, int64
   if (threadIdx.x == 0) { sums[0] = a; sums[1] = b; }
 }
 
+// flag |= 1 if any of the rows x cols entries (leading dimension ld) is not finite
+template <typename T>
+__global__ void check_finite_kernel(const T* __restrict__ a, int64_t rows, int64_t cols, int64_t ld,
+                                    int* __restrict__ flag) {
+  bool bad = false;
+  const int64_t total = rows * cols;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / cols, c = k - r * cols;
+    bad |= !isfinite(a[r * ld + c]);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void widen_kernel(const float* __restrict__ in, int64_t m, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) out[i] = (double)in[i];
@@ -346,7 +364,8 @@ cudaError_t gemv_rows_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const vo
     if (vec) gemv_rows_kernel<TS, float, true><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
     else gemv_rows_kernel<TS, float, false><<<grid, kRowThreads, 0, st>>>(S, n, m, ldS, (const float*)w, partials);
   }
-  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n, u);
+  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n, n,
+                                                                                                 u);
   if (launches) *launches += 2;
   return cudaGetLastError();
 }
@@ -387,6 +406,15 @@ cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, cons
 
 }  // namespace
 
+cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
+                         cudaStream_t st, int* launches) {
+  const unsigned grid = (unsigned)(num_sms * 8);
+  if (is64) check_finite_kernel<double><<<grid, 256, 0, st>>>((const double*)a, rows, cols, ld, flag);
+  else check_finite_kernel<float><<<grid, 256, 0, st>>>((const float*)a, rows, cols, ld, flag);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches) {
   widen_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(in, m, out);
   if (launches) *launches += 1;
@@ -394,15 +422,19 @@ cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, 
 }
 
 cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
-                             double* u, uint8_t* St, cudaStream_t st, int* launches) {
+                             double* u, uint8_t* St, cudaStream_t st, int* launches, int64_t r0, int64_t r1,
+                             int* nonfinite) {
   constexpr int CW = row_chunk_cols<float>();
   const int64_t chunks = (m + CW - 1) / CW;
   const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
+  if (r1 < 0) r1 = n;
+  const int64_t rz = (r1 == n) ? tiles_nb(n) * kTileRows : r1;   // the last rows also zero the padding
   gemv_rows_retile_kernel<<<(unsigned)chunks, kRowThreads, 0, st>>>(S, n, m, ldS, w, partials, St, w != nullptr,
-                                                                     vec_ok);
+                                                                     vec_ok, r0, r1, rz, nonfinite);
   if (launches) *launches += 1;
-  if (w) {
-    reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n, u);
+  if (w && r1 > r0) {
+    reduce_chunks_kernel<<<(unsigned)((r1 - r0 + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(
+        partials + r0, chunks, r1 - r0, n, u + r0);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();

@@ -6,10 +6,15 @@
 namespace fs {
 
 // ---- gemv.cu (HBM-bound streaming passes over S) ----
+cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
+                         cudaStream_t st, int* launches);
 cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches);
 // fp32 u = S w (w may be NULL: retile only) that also writes the tiled copy S_t (tiles.cuh)
+// rows [r0, r1) only (r1 < 0: all; when r1 == n the tiled copy's zero padding rows are written
+// too); nonfinite (may be NULL) is OR-ed with 1 if any element read is not finite
 cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
-                             double* u, uint8_t* St, cudaStream_t st, int* launches);
+                             double* u, uint8_t* St, cudaStream_t st, int* launches, int64_t r0 = 0, int64_t r1 = -1,
+                             int* nonfinite = nullptr);
 // Number of column chunks the row-GEMV splits m into (partials buffer = chunks * n doubles).
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64);
 cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
@@ -33,8 +38,9 @@ cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);
 size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms);
 // St: the tiled copy written by gemv_rows_retile
+// pair rows [prow0, prow1) of the lower Gram (pair row p = 128-row blocks 2p, 2p+1); -1 = all
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
-                    cudaStream_t st, int* launches);
+                    cudaStream_t st, int* launches, int prow0 = 0, int prow1 = -1);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,

@@ -62,7 +62,7 @@ constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 constexpr size_t kSmemBytes = (size_t)(kRaw + kLo) * kStageBytes + 1024 + 512;
 
 struct Plan {
-  int nb, np, tiles, P, clusters, KB, KC, D;
+  int nb, np, tile0, tiles, P, clusters, KB, KC, D;
   bool direct;
 };
 
@@ -89,7 +89,7 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, int P, int KB, int KC, int D,
+syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
                double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -135,7 +135,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
-        int pp, qq; pair_of(t, pp, qq);
+        int pp, qq; pair_of(tile0 + t, pp, qq);
         const int blkA = 2 * pp + (int)crank, blkB = 2 * qq + (int)crank;
         const bool diag = pp == qq;                       // A == B: one tile
         const uint32_t bytes = (diag ? 1 : 2) * kBoxBytes;
@@ -162,7 +162,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
       uint32_t chunk = 0;
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
-        int pp, qq; pair_of(t, pp, qq);
+        int pp, qq; pair_of(tile0 + t, pp, qq);
         const int b_off = (pp == qq) ? 0 : kBoxBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         uint32_t dacc = 0;
@@ -215,7 +215,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
     Ring rr, lr;
     for (int u = cluster; u < units; u += nclusters) {
       const int t = u / P, q = u % P;
-      int pp, qq; pair_of(t, pp, qq);
+      int pp, qq; pair_of(tile0 + t, pp, qq);
       const int nvec = ((pp == qq) ? 1 : 2) * (kBoxBytes / 16);
       const int kb0 = q * KC, nk = min(KC, KB - kb0);
       for (int k = 0; k < nk; ++k) {
@@ -252,7 +252,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
     uint32_t chunk = 0;
     for (int u = cluster; u < units; u += nclusters) {
       const int t = u / P, q = u % P;
-      int pp, qq; pair_of(t, pp, qq);
+      int pp, qq; pair_of(tile0 + t, pp, qq);
       const int kb0 = q * KC, nk = min(KC, KB - kb0);
       const int nch = (nk + D - 1) / D;
       const size_t slot = direct ? (size_t)blockIdx.x : ((size_t)u * 2 + crank);
@@ -313,10 +313,11 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tiles, in
 // Fixed-order sum of the P split-K partial tiles -> packed lower Gram (+λ on the diagonal).
 // Block (t, c): pair tile t, CTA half c (row block 2p+c).
 constexpr int kRedSplit = 16;   // blocks per (pair tile, CTA half): 2048 elements each
-__global__ void syrk_tc_reduce(const double* __restrict__ ws, int P, int64_t n, double lam, double* __restrict__ Gp) {
+__global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, int64_t n, double lam,
+                               double* __restrict__ Gp) {
   const int tc = blockIdx.x / kRedSplit, part = blockIdx.x % kRedSplit;
   int pp, qq;
-  pair_of(tc >> 1, pp, qq);
+  pair_of(tile0 + (tc >> 1), pp, qq);
   const int c = tc & 1;
   constexpr int kPer = kBlk * kN / kRedSplit;
   for (int e = part * kPer + threadIdx.x; e < (part + 1) * kPer; e += blockDim.x) {
@@ -329,11 +330,13 @@ __global__ void syrk_tc_reduce(const double* __restrict__ ws, int P, int64_t n, 
   }
 }
 
-Plan make_plan(int64_t n, int64_t m, int num_sms) {
+Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1) {
   Plan p;
   p.nb = (int)((n + kBlk - 1) / kBlk);
   p.np = (p.nb + 1) / 2;
-  p.tiles = p.np * (p.np + 1) / 2;
+  if (prow1 < 0 || prow1 > p.np) prow1 = p.np;
+  p.tile0 = prow0 * (prow0 + 1) / 2;
+  p.tiles = prow1 * (prow1 + 1) / 2 - p.tile0;
   p.KB = (int)((m + kBK - 1) / kBK);
   const int max_clusters = num_sms / 2;
   p.P = p.tiles >= max_clusters ? 1 : std::max(1, std::min(max_clusters / p.tiles, p.KB / 8));
@@ -364,8 +367,9 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
 }
 
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
-                    cudaStream_t st, int* launches) {
-  Plan p = make_plan(n, m, num_sms);
+                    cudaStream_t st, int* launches, int prow0, int prow1) {
+  Plan p = make_plan(n, m, num_sms, prow0, prow1);
+  if (p.tiles <= 0) return cudaSuccess;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -373,11 +377,12 @@ cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double*
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
-  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(St, n, (int)tiles_nb(n), p.tiles, p.P, p.KB, p.KC, p.D,
+  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC,
+                                                               p.D,
                                                                ws, G_packed, lam, p.direct ? 1 : 0, dbg);
   if (launches) *launches += 1;
   if (!p.direct) {
-    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.P, n, lam, G_packed);
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();

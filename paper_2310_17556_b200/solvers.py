@@ -106,34 +106,48 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
     if system.S.is_complex:
         raise ValueError("solve_chol handles real scores; use solve_chol_hermitian")
     t0 = perf_counter()
-    S = system.S.tensor
-    v = system.v_tensor
     n, m = system.n, system.m
-    prec = resolve_precision(precision, S.dtype)
+    prec = resolve_precision(precision, system.S.dtype)
     if refine == "auto":
         do_refine = prec == "fp64"
     else:
         do_refine = bool(refine)
     if do_refine and not diagnostics:
         raise ValueError("refinement needs the residual diagnostics")
-    ctx = _lib.context_for(S.device.index, n, m)
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (_lib.FS_FLAG_REFINE if do_refine else 0)
+    dt = _lib.FS_F32 if system.S.dtype == torch.float32 else _lib.FS_F64
+    device = system.S.device
+    ctx = _lib.context_for(device.index, n, m)
+    slots = _meter_slots(n, m, dt, PRECISIONS[prec])
     if meter is not None:
-        meter.alloc(_meter_slots(n, m, _dt(S), PRECISIONS[prec]) + m)
-    x = torch.empty(m, dtype=torch.float64, device=S.device)
+        meter.alloc(slots + m)
     piv = ctypes.c_int64(-1)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
-    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (_lib.FS_FLAG_REFINE if do_refine else 0)
-    rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
-                               v.data_ptr(), system.lam, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
-                               REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(S.device))
+    Sh, vh = system.S.host_array, system.host_v
+    if Sh is not None and vh is not None:
+        # host system: one call streams S in row chunks overlapped with the Gram, returns x on the host
+        x = np.empty(m, dtype=np.float64)
+        rc = ctx.lib.fs_chol_solve_host(ctx.handle, dt, PRECISIONS[prec], Sh.ctypes.data, n, m,
+                                        Sh.strides[0] // Sh.itemsize, vh.ctypes.data, system.lam, x.ctypes.data,
+                                        _lib.ALLREDUCE_FN(), None, flags, REFINE_ABOVE_REL, ctypes.byref(piv), res,
+                                        _stream(device))
+        what = "fs_chol_solve_host"
+    else:
+        S = system.S.tensor
+        v = system.v_tensor
+        x = torch.empty(m, dtype=torch.float64, device=S.device)
+        rc = ctx.lib.fs_chol_solve(ctx.handle, dt, PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
+                                   v.data_ptr(), system.lam, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
+                                   REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(S.device))
+        what = "fs_chol_solve"
     if meter is not None:
-        meter.free(_meter_slots(n, m, _dt(S), PRECISIONS[prec]))
+        meter.free(slots)
     if rc == _lib.FS_NOT_PD:
         raise FactorizationError(
             f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",
             pivot=int(piv.value))
-    _check(ctx, rc, "fs_chol_solve")
-    xo = x.cpu().numpy() if system.S.host_origin else x
+    _check(ctx, rc, what)
+    xo = x.cpu().numpy() if (system.S.host_origin and isinstance(x, torch.Tensor)) else x
     return Solution(x=xo, method=Method.CHOL, abs_residual=float(res[0]), rel_residual=float(res[1]),
                     wall_seconds=perf_counter() - t0, precision=prec)
 

@@ -427,3 +427,85 @@ def test_headline_shape_tf32x3_vs_fp64_mode(fsb):
     assert sol.rel_residual <= 4 * U32 * sig2 / lam, sol.rel_residual
     assert sol64.rel_residual <= max(1e-8, 8 * U64 * sig2 / lam) * 10
     del W
+
+
+# ---------------------------------------------------------------- host-buffer entry (fs_chol_solve_host)
+
+@pytest.mark.parametrize("n,m", [(1, 7), (65, 1001), (300, 10000), (513, 4099), (1024, 65536)])
+def test_host_entry_matches_device_entry(fsb, n, m):
+    """numpy in -> the chunked upload/Gram pipeline; CUDA tensor in -> the device entry.  fp64 mode
+    runs the identical kernels (bit-identical); tf32x3 splits the SYRK per 256-row chunk, so only
+    the fp64 drain order differs."""
+    S, v, lam = O.generate_problem(11, n, m, 1e-3)
+    dev = torch.device("cuda", 0)
+    for dt, prec in ((np.float64, "fp64"), (np.float32, "tf32x3"), (np.float32, "fp64")):
+        Sh, vh = S.astype(dt), v.astype(dt)
+        host = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=prec)
+        assert isinstance(host.x, np.ndarray)
+        d = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(Sh).to(dev)), lam,
+                                            torch.from_numpy(vh).to(dev)), precision=prec)
+        xd = d.x.cpu().numpy()
+        if prec == "fp64":
+            assert np.array_equal(host.x, xd), (dt, O.rel_err(host.x, xd))
+            assert host.rel_residual == d.rel_residual
+        else:
+            assert O.rel_err(host.x, xd) <= 1e-7, O.rel_err(host.x, xd)
+            ref = O.solve_chol(Sh.astype(np.float64), vh.astype(np.float64), lam)
+            assert O.rel_err(host.x, ref.x) <= 1e-6
+
+
+@pytest.mark.parametrize("where", ["first", "last_row", "last_col", "inf"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_host_entry_rejects_non_finite_scores(fsb, where, dt):
+    S, v, lam = O.generate_problem(12, 300, 2003, 1e-3)
+    S = S.astype(dt)
+    i, j = {"first": (0, 0), "last_row": (299, 1000), "last_col": (150, 2002), "inf": (257, 5)}[where]
+    S[i, j] = np.inf if where == "inf" else np.nan
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v.astype(dt))
+    with pytest.raises(ValueError, match="finite"):
+        fsb.solve_chol(system)
+    # the context stays usable
+    S[i, j] = 0.0
+    sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v.astype(dt)))
+    assert np.isfinite(sol.x).all()
+
+
+def test_host_entry_rejects_non_finite_rhs(fsb):
+    S, v, lam = O.generate_problem(13, 10, 100, 1e-3)
+    v[3] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_entry_abi_pitched_rows(fsb, pinned):
+    """fs_chol_solve_host with ldS > m (pitched host rows), pinned and pageable host memory."""
+    from paper_2310_17556_b200 import _lib
+    lib = _lib.load()
+    n, m, ld = 260, 3001, 3008 + 5
+    S, v, lam = O.generate_problem(14, n, m, 1e-3)
+    buf = torch.zeros((n, ld), dtype=torch.float32, pin_memory=pinned)
+    buf[:, :m] = torch.from_numpy(S.astype(np.float32))
+    buf[:, m:] = float("nan")                      # pitch padding is never read
+    v32 = v.astype(np.float32)
+    x = np.empty(m)
+    ctx = _lib.Context(0, n, m)
+    piv = ctypes.c_int64(0)
+    res = (ctypes.c_double * 2)()
+    for prec in (_lib.FS_PREC_TF32X3, _lib.FS_PREC_FP64):
+        rc = lib.fs_chol_solve_host(ctx.handle, _lib.FS_F32, prec, buf.data_ptr(), n, m, ld, v32.ctypes.data, lam,
+                                    x.ctypes.data, _lib.ALLREDUCE_FN(), None, _lib.FS_FLAG_RESIDUAL, 1e-10,
+                                    ctypes.byref(piv), res, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0, ctx.last_error()
+        ref = O.solve_chol(S.astype(np.float32).astype(np.float64), v32.astype(np.float64), lam)
+        assert O.rel_err(x, ref.x) <= (1e-6 if prec == _lib.FS_PREC_TF32X3 else 1e-10)
+        assert res[1] == res[1] and piv.value == -1
+    # argument errors: ldS < m, lam <= 0
+    assert lib.fs_chol_solve_host(ctx.handle, _lib.FS_F32, _lib.FS_PREC_AUTO, buf.data_ptr(), n, m, m - 1,
+                                  v32.ctypes.data, lam, x.ctypes.data, _lib.ALLREDUCE_FN(), None, 0, 1e-10,
+                                  ctypes.byref(piv), res, 0) == _lib.FS_EINVAL
+    assert lib.fs_chol_solve_host(ctx.handle, _lib.FS_F32, _lib.FS_PREC_AUTO, buf.data_ptr(), n, m, ld,
+                                  v32.ctypes.data, -1.0, x.ctypes.data, _lib.ALLREDUCE_FN(), None, 0, 1e-10,
+                                  ctypes.byref(piv), res, 0) == _lib.FS_EINVAL
+    ctx.close()
+
