@@ -136,9 +136,9 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
 /* ---- one-shot solve from HOST buffers (the same call with S, v, x in host memory) ----
  * What a numpy caller of solvers.py:197 solve_chol(system) hands over: S (n x m, leading
  * dimension ldS, row-major), v (length m, S's dtype) and x (fp64 out) in host memory —
- * page-locked for full overlap.  S is uploaded in 256-row chunks on a second stream; the Gram
- * and u = S v of each chunk run while the next one is in flight, so the H2D transfer hides
- * all but the last chunk's Gram.  Non-finite entries in S or v are detected on the device
+ * page-locked for full overlap.  S is uploaded in column chunks (>= 32 MB, at most 16; 2-D
+ * copies of all rows) on a second stream; the Gram and u = S v of each chunk's K range run
+ * while the next chunk is in flight, so the transfer hides all but the last chunk's share.  Non-finite entries in S or v are detected on the device
  * and return FS_EINVAL (core.py:108-119 rejects them).  Synchronizes. */
 int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host, int64_t n, int64_t m,
                        int64_t ldS, const void* v_host, double lam, double* x_host, fs_allreduce_fn allreduce,

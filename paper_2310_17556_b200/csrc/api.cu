@@ -568,12 +568,13 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
   FS_CK(cudaEventRecord(ctx->ev_free, st), "event");
   FS_CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_free, 0), "event wait");
   const int64_t hpitch = ldS * (int64_t)elem, dpitch = ldd * (int64_t)elem;
-  auto upload = [&](int64_t r0, int64_t r1, int ev) -> cudaError_t {
-    const char* src = (const char*)S_host + r0 * hpitch;
-    char* dst = (char*)ctx->d_Sin + r0 * dpitch;
-    cudaError_t e = (hpitch == dpitch)
-                        ? cudaMemcpyAsync(dst, src, (size_t)(r1 - r0) * hpitch, cudaMemcpyHostToDevice, ctx->up_st)
-                        : cudaMemcpy2DAsync(dst, dpitch, src, hpitch, m * elem, r1 - r0, cudaMemcpyHostToDevice,
+  // upload columns [c0, c1) of every row (2-D copy: n segments of (c1-c0) elements)
+  auto upload = [&](int64_t c0, int64_t c1, int ev) -> cudaError_t {
+    const char* src = (const char*)S_host + c0 * (int64_t)elem;
+    char* dst = (char*)ctx->d_Sin + c0 * (int64_t)elem;
+    cudaError_t e = (c0 == 0 && c1 == m && hpitch == dpitch)
+                        ? cudaMemcpyAsync(dst, src, (size_t)n * hpitch, cudaMemcpyHostToDevice, ctx->up_st)
+                        : cudaMemcpy2DAsync(dst, dpitch, src, hpitch, (c1 - c0) * elem, n, cudaMemcpyHostToDevice,
                                             ctx->up_st);
     if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_chunk[ev], ctx->up_st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_chunk[ev], 0);
@@ -583,25 +584,32 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
   const void* v = ctx->d_vin;
   double* x = ctx->d_xin;
   if (use_tc) {
-    // per 256-row pair chunk: upload -> (retile + u rows + non-finite check) -> SYRK pair row
+    // K-chunks of >= 32 MB (at most 16): upload columns [c0, c1) of all rows -> retile them (+ u
+    // partials + finiteness) -> SYRK over their K-blocks, accumulated into the packed Gram.  The
+    // transfer of chunk c+1 overlaps the kernels of chunk c; only the last chunk's share is exposed.
     double* u = ctx->d_packed + n * (n + 1) / 2;
-    const int np = (int)((n + 2 * fs::kTileRows - 1) / (2 * fs::kTileRows));
-    for (int p = 0; p < np; ++p) {
-      const int64_t r0 = (int64_t)p * 2 * fs::kTileRows;
-      const int64_t r1 = std::min<int64_t>(n, r0 + 2 * fs::kTileRows);
-      FS_CK(upload(r0, r1, p % fs_ctx::kMaxChunks), "S h2d");
-      FS_CK(fs::gemv_rows_retile((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, u, ctx->d_St, st, &l,
-                                 r0, r1, ctx->d_flag),
+    const int64_t CW = fs::gemv_rows_chunk_cols();
+    const int64_t by_bytes = ((int64_t)(32 << 20) / (n * (int64_t)elem) + CW - 1) / CW * CW;
+    const int64_t by_count = (m + 16 * CW - 1) / (16 * CW) * CW;
+    const int64_t W = std::max<int64_t>(CW, std::max(by_bytes, by_count));
+    int c = 0;
+    for (int64_t c0 = 0; c0 < m; c0 += W, ++c) {
+      const int64_t c1 = std::min(m, c0 + W);
+      FS_CK(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
+      FS_CK(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
+                            ctx->d_flag, st, &l),
             "retile");
-      FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, p, p + 1),
+      FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
+                        (int)(c0 / fs::kTileCols), (int)((c1 + fs::kTileCols - 1) / fs::kTileCols), c > 0),
             "syrk_tc");
     }
+    FS_CK(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
     ctx->launches += l;
     prof_mark(ctx, FS_PROF_GRAM, st);
     rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
                     pivot, out_res, st);
   } else {
-    FS_CK(upload(0, n, 0), "S h2d");
+    FS_CK(upload(0, m, 0), "S h2d");
     FS_CK(fs::check_finite(S, dtype == FS_F64, n, m, ldd, ctx->d_flag, ctx->num_sms, st, &l), "check S");
     ctx->launches += l;
     rc = fs_chol_solve(ctx, dtype, precision, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,

@@ -88,11 +88,13 @@ gemv_rows_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 __global__ void __launch_bounds__(kRowThreads)
 gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
                         const float* __restrict__ w, double* __restrict__ partials, uint8_t* __restrict__ St,
-                        int has_w, int vec_ok, int64_t r0, int64_t r1, int64_t rz, int* __restrict__ nonfinite) {
+                        int has_w, int vec_ok, int64_t r0, int64_t r1, int64_t rz, int* __restrict__ nonfinite,
+                        int64_t cb0) {
   constexpr int VN = 4;
   constexpr int CW = row_chunk_cols<float>();            // 1024 columns = 32 K-blocks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * CW;
+  const int64_t cb = cb0 + blockIdx.x;                   // global column chunk
+  const int64_t c0 = cb * CW;
   const int64_t nb = tiles_nb(n), KB = tiles_kb(m);
   float wr[kRowUnroll][VN];
 #pragma unroll
@@ -143,7 +145,7 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
         acc = fmaf(buf[u].z, wr[u][2], acc); acc = fmaf(buf[u].w, wr[u][3], acc);
       }
       const double s = warp_sum((double)acc);
-      if (lane == 0) partials[(int64_t)blockIdx.x * n + i] = s;
+      if (lane == 0) partials[cb * n + i] = s;
     }
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
@@ -430,7 +432,7 @@ cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, 
   if (r1 < 0) r1 = n;
   const int64_t rz = (r1 == n) ? tiles_nb(n) * kTileRows : r1;   // the last rows also zero the padding
   gemv_rows_retile_kernel<<<(unsigned)chunks, kRowThreads, 0, st>>>(S, n, m, ldS, w, partials, St, w != nullptr,
-                                                                     vec_ok, r0, r1, rz, nonfinite);
+                                                                     vec_ok, r0, r1, rz, nonfinite, 0);
   if (launches) *launches += 1;
   if (w && r1 > r0) {
     reduce_chunks_kernel<<<(unsigned)((r1 - r0 + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(
@@ -439,6 +441,31 @@ cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, 
   }
   return cudaGetLastError();
 }
+
+cudaError_t retile_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                        uint8_t* St, int64_t c0, int64_t c1, int* nonfinite, cudaStream_t st, int* launches) {
+  constexpr int CW = row_chunk_cols<float>();
+  if (c0 % CW) return cudaErrorInvalidValue;
+  const int64_t cb0 = c0 / CW, cb1 = (c1 + CW - 1) / CW;
+  if (cb1 <= cb0) return cudaSuccess;
+  const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
+  gemv_rows_retile_kernel<<<(unsigned)(cb1 - cb0), kRowThreads, 0, st>>>(
+      S, n, m, ldS, w, partials, St, w != nullptr, vec_ok, 0, n, tiles_nb(n) * kTileRows, nonfinite, cb0);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_row_partials(const double* partials, int64_t n, int64_t m, double* u, cudaStream_t st,
+                                int* launches) {
+  constexpr int CW = row_chunk_cols<float>();
+  const int64_t chunks = (m + CW - 1) / CW;
+  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(partials, chunks, n,
+                                                                                                 n, u);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+int64_t gemv_rows_chunk_cols() { return row_chunk_cols<float>(); }
 
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64) {
   const int64_t cw = s_is_f64 ? row_chunk_cols<double>() : row_chunk_cols<float>();

@@ -15,6 +15,13 @@ cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, 
 cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
                              double* u, uint8_t* St, cudaStream_t st, int* launches, int64_t r0 = 0, int64_t r1 = -1,
                              int* nonfinite = nullptr);
+// column range [c0, c1) of all rows (c0 a multiple of gemv_rows_chunk_cols()): tiled copy + the
+// u-partials of its column chunks; no reduction (reduce_row_partials finishes u)
+cudaError_t retile_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                        uint8_t* St, int64_t c0, int64_t c1, int* nonfinite, cudaStream_t st, int* launches);
+cudaError_t reduce_row_partials(const double* partials, int64_t n, int64_t m, double* u, cudaStream_t st,
+                                int* launches);
+int64_t gemv_rows_chunk_cols();
 // Number of column chunks the row-GEMV splits m into (partials buffer = chunks * n doubles).
 int64_t gemv_rows_chunks(int64_t m, bool s_is_f64);
 cudaError_t gemv_rows(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const void* w,
@@ -38,9 +45,11 @@ cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);
 size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms);
 // St: the tiled copy written by gemv_rows_retile
-// pair rows [prow0, prow1) of the lower Gram (pair row p = 128-row blocks 2p, 2p+1); -1 = all
+// pair rows [prow0, prow1) of the lower Gram (pair row p = 128-row blocks 2p, 2p+1) over the
+// K-blocks [kb_begin, kb_end) of S_t (-1 = all); accum != 0 adds into G_packed instead of storing
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
-                    cudaStream_t st, int* launches, int prow0 = 0, int prow1 = -1);
+                    cudaStream_t st, int* launches, int prow0 = 0, int prow1 = -1, int kb_begin = 0, int kb_end = -1,
+                    int accum = 0);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,

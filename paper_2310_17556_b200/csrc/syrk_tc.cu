@@ -62,7 +62,7 @@ constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 constexpr size_t kSmemBytes = (size_t)(kRaw + kLo) * kStageBytes + 1024 + 512;
 
 struct Plan {
-  int nb, np, tile0, tiles, P, clusters, KB, KC, D;
+  int nb, np, tile0, tiles, P, clusters, KB, KC, D, kb_base;
   bool direct;
 };
 
@@ -90,7 +90,8 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
-               double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg) {
+               double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg, int kb_base,
+               int accum) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw = smem;
@@ -141,9 +142,9 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         const uint32_t bytes = (diag ? 1 : 2) * kBoxBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         for (int k = 0; k < nk; ++k) {
-          const size_t krow = (size_t)(kb0 + k) * nbt;
+          const size_t krow = (size_t)(kb_base + kb0 + k) * nbt;
           if (!(dbg & 32) && k + kPfDist < nk) {
-            const size_t pk = (size_t)(kb0 + k + kPfDist) * nbt;
+            const size_t pk = (size_t)(kb_base + kb0 + k + kPfDist) * nbt;
             ptx::bulk_prefetch_l2(St + (pk + blkA) * kTileBytes, kTileBytes);
             if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kTileBytes, kTileBytes);
           }
@@ -299,7 +300,8 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
             const int c = half * (kN / 2) + e;
             const int64_t gj = (int64_t)(2 * qq) * kBlk + c;
             if (gj > gi) break;
-            Gp[gi * (gi + 1) / 2 + gj] = sc[(size_t)e * kBlk] + (gi == gj ? lam : 0.0);
+            double* g = Gp + gi * (gi + 1) / 2 + gj;
+            *g = (accum ? *g : 0.0) + sc[(size_t)e * kBlk] + (gi == gj ? lam : 0.0);
           }
         }
       }
@@ -314,7 +316,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
 // Block (t, c): pair tile t, CTA half c (row block 2p+c).
 constexpr int kRedSplit = 16;   // blocks per (pair tile, CTA half): 2048 elements each
 __global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, int64_t n, double lam,
-                               double* __restrict__ Gp) {
+                               double* __restrict__ Gp, int accum) {
   const int tc = blockIdx.x / kRedSplit, part = blockIdx.x % kRedSplit;
   int pp, qq;
   pair_of(tile0 + (tc >> 1), pp, qq);
@@ -326,11 +328,12 @@ __global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, 
     if (gi >= n || gj > gi) continue;
     double s = 0.0;
     for (int q = 0; q < P; ++q) s += ws[(((size_t)(tc >> 1) * P + q) * 2 + c) * kBlk * kN + e];
-    Gp[gi * (gi + 1) / 2 + gj] = s + (gi == gj ? lam : 0.0);
+    double* g = Gp + gi * (gi + 1) / 2 + gj;
+    *g = (accum ? *g : 0.0) + s + (gi == gj ? lam : 0.0);
   }
 }
 
-Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1) {
+Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1, int kb_begin = 0, int kb_end = -1) {
   Plan p;
   p.nb = (int)((n + kBlk - 1) / kBlk);
   p.np = (p.nb + 1) / 2;
@@ -338,6 +341,9 @@ Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1)
   p.tile0 = prow0 * (prow0 + 1) / 2;
   p.tiles = prow1 * (prow1 + 1) / 2 - p.tile0;
   p.KB = (int)((m + kBK - 1) / kBK);
+  if (kb_end < 0 || kb_end > p.KB) kb_end = p.KB;
+  p.kb_base = kb_begin;
+  p.KB = kb_end - kb_begin;
   const int max_clusters = num_sms / 2;
   p.P = p.tiles >= max_clusters ? 1 : std::max(1, std::min(max_clusters / p.tiles, p.KB / 8));
   p.KC = (p.KB + p.P - 1) / p.P;          // K-blocks per split, contiguous in m
@@ -367,9 +373,9 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
 }
 
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
-                    cudaStream_t st, int* launches, int prow0, int prow1) {
-  Plan p = make_plan(n, m, num_sms, prow0, prow1);
-  if (p.tiles <= 0) return cudaSuccess;
+                    cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum) {
+  Plan p = make_plan(n, m, num_sms, prow0, prow1, kb_begin, kb_end);
+  if (p.tiles <= 0 || p.KB <= 0) return cudaSuccess;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
@@ -379,10 +385,10 @@ cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double*
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
   syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC,
                                                                p.D,
-                                                               ws, G_packed, lam, p.direct ? 1 : 0, dbg);
+                                                               ws, G_packed, lam, p.direct ? 1 : 0, dbg, p.kb_base, accum);
   if (launches) *launches += 1;
   if (!p.direct) {
-    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed);
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
