@@ -7,12 +7,16 @@
 // (fs_unpack_lower leaves it exactly zero: clean=1, test_solvers.py:455).
 //
 // Blocked right-looking algorithm with 64-wide block columns, ONE launch per block column:
-//   step k, CTA (I,J) for k < J <= I:   X_I = A_Ik Linv_kk^T   (TRSM through the inverted
-//   diagonal block; X_J likewise), A_IJ -= X_I X_J^T, and
+//   step k, CTA (I,J) for k < J <= I:   X_I = A_Ik Linv_kk^T   (the TRSM as a GEMM with the
+//   inverted diagonal block; X_J likewise), A_IJ -= X_I X_J^T, and
 //     * the CTA with J == k+1 stores X_I as the panel L_Ik (double-buffered panel, copied into
 //       W by the next step, so no CTA ever overwrites data another CTA of its step still reads)
-//     * the CTA with I == J == k+1 factors the freshly updated diagonal block and inverts it
-//       (next step's Linv, also kept for the TRSV pair).
+//     * the CTA with I == J == k+1 factors the freshly updated diagonal block AND inverts it
+//       in the same sweep (next step's Linv, also kept for the TRSV pair).
+// The diagonal block: recursive 2x2 split into 32x32 halves; each half is factored by one
+// warp with its rows in registers, the pivot column broadcast by shuffles, and the inverse
+// accumulated alongside (right-looking forward substitution on the identity) — no barriers,
+// no shared-memory round trips; the off-diagonal pieces are 32^3 GEMMs by the whole CTA.
 // Every kernel first checks the status word, so a breakdown stops the remaining work.
 // Deterministic: fixed operation order, no atomics.
 #include "common.cuh"
@@ -81,95 +85,140 @@ __device__ void invert_64(const double (*L)[kLd], double (*X)[kLd], double (*T)[
   __syncthreads();
 }
 
-// In-place Cholesky of the identity-padded 64x64 block A (smem, lower) by 256 threads.
-// Thread (r = tid/4, q = tid%4) keeps its row's 16 elements A[r][q + 4cc] in REGISTERS for the
-// whole factorisation (smem round trips through an aliased array serialise at ~50 cycles each).
-// Step j: the pivot column j lives in a double-buffered smem vector col[] written by its owners
-// at the end of step j-1, together with 1/d_j computed (one __drcp_rn) by the thread that
-// finalised A[j][j]; one barrier per column.  Unscaled update A[r][c] -= A[r][j] A[c][j] / d_j;
-// a final pass scales L[r][c] = A[r][c] * rsqrt(d_c).  Sets *fail (first bad pivot or -1).
-__device__ void factor_block(double (*A)[kLd], int b, int* fail) {
-  __shared__ double col[2][kNB];
-  __shared__ double dinv[2];
-  __shared__ double dval[kNB];
-  const int tid = threadIdx.x, r = tid >> 2, q = tid & 3;
-  double a[kNB / 4];
-#pragma unroll
-  for (int cc = 0; cc < kNB / 4; ++cc) a[cc] = A[r][q + 4 * cc];
-  if (q == 0) col[0][r] = A[r][0];
-  if (tid == 0) {
-    *fail = -1;
-    dinv[0] = __drcp_rn(A[0][0]);
-  }
-#pragma unroll 1
-  for (int j = 0; j < b; ++j) {
-    __syncthreads();
-    const int buf = j & 1;
-    const double d = col[buf][j];
-    if (!(d > 0.0)) {                  // uniform: every thread reads the same pivot
-      if (tid == 0) *fail = j;
-      __syncthreads();
-      return;
-    }
-    if (tid == 0) dval[j] = d;
-    const double s = (r > j) ? col[buf][r] * dinv[buf] : 0.0;
-    double cj[kNB / 4];
-#pragma unroll
-    for (int cc = 0; cc < kNB / 4; ++cc) cj[cc] = col[buf][q + 4 * cc];
-#pragma unroll
-    for (int cc = 0; cc < kNB / 4; ++cc) {
-      const int c = q + 4 * cc;
-      if (r > j && c > j && c <= r) a[cc] = fma(-s, cj[cc], a[cc]);
-      // publish column j+1 (final after this update) and its pivot reciprocal; predicated
-      // stores with a compile-time register index keep a[] out of local memory
-      if (c == j + 1 && j + 1 < b) {
-        col[buf ^ 1][r] = a[cc];
-        if (r == j + 1) dinv[buf ^ 1] = __drcp_rn(a[cc]);
-      }
-    }
-  }
-  __syncthreads();
-  // scale: L[r][c] = A[r][c] * rsqrt(d_c) (diagonal: d_c * rsqrt(d_c) = sqrt(d_c))
-#pragma unroll
-  for (int cc = 0; cc < kNB / 4; ++cc) {
-    const int c = q + 4 * cc;
-    double v = (c <= r) ? a[cc] : 0.0;
-    if (c < b && c <= r) v *= rsqrt(dval[c]);
-    if (r >= b || c >= b) v = (r == c) ? 1.0 : 0.0;   // identity padding
-    A[r][c] = v;
-  }
-  __syncthreads();
+// 1/d and 1/sqrt(d) without the library's special-case subroutines: hardware approximation
+// + Newton steps (~1 ulp for positive normal d; the pivot test rejects everything else).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_rsqrt(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double h = 0.5 * d * y * y;            // y (1.5 - d y^2 / 2), twice
+  y = fma(y, 1.5 - h, 0.0);
+  h = 0.5 * d * y * y;
+  return y * (1.5 - h);
 }
 
-// X <- X L^-T: each of the 64 rows of X solved against the lower 64x64 L (rdiag = 1/L_jj).
-// Thread (r, q) handles columns p = q + 4cc of row r.  Step j issues its 32 smem loads up
-// front (X[r][.] and L[j][.], all independent), four predicated FMA chains, a 4-lane shuffle
-// reduction, and the owner lane stores x_j: one store per step, so nothing serialises on
-// smem aliasing.  No block barriers (a row lives in one warp).
-__device__ void trsm_rows(const double (*L)[kLd], const double* rdiag, double (*X)[kLd]) {
-  const int tid = threadIdx.x, r = tid >> 2, q = tid & 3;
-#pragma unroll 1
-  for (int j = 0; j < kNB; ++j) {
-    double xv[kNB / 4], lj[kNB / 4];
+// One warp factors the lower 32x32 window A (stride kLd) in place, A = L L^T, and writes
+// X = L^-1.  Lane r keeps row r of A and column r of the inverse's right-hand side in
+// registers.  Unscaled (LDL^T) sweep: step j publishes the raw column A[.][j] in a
+// double-buffered smem vector (one store per lane); every lane reads the pivot and the rows
+// c > j back with 16-byte broadcast loads; A[r][c] -= (A[r][j] / d_j) A[c][j] and the
+// inverse's forward substitution on the unit-lower factor s[c] -= A[c][j] (x_j / d_j) share
+// each load.  The sqrt scaling is applied once at the end: L[r][c] = A[r][c] / sqrt(d_c),
+// X[r][c] = x~[r][c] / sqrt(d_r).  Straight-line code (no early exit, no per-lane
+// predicates); entries a[c] with c > lane are never read back.  Returns the first
+// non-positive (or NaN) pivot, or -1.  (A shuffle broadcast measured slower: 2 SHFL per
+// double, tools/ubench/chol32_steps.cu.)
+__device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbuf)[32]) {
+  const int lane = threadIdx.x & 31;
+  double a[32], sx[32], rsq[32];
 #pragma unroll
-    for (int cc = 0; cc < kNB / 4; ++cc) {
-      xv[cc] = X[r][q + 4 * cc];
-      lj[cc] = L[j][q + 4 * cc];
-    }
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int cc = 0; cc < kNB / 4; cc += 4) {
-      if (q + 4 * cc < j) s0 = fma(xv[cc], lj[cc], s0);
-      if (q + 4 * (cc + 1) < j) s1 = fma(xv[cc + 1], lj[cc + 1], s1);
-      if (q + 4 * (cc + 2) < j) s2 = fma(xv[cc + 2], lj[cc + 2], s2);
-      if (q + 4 * (cc + 3) < j) s3 = fma(xv[cc + 3], lj[cc + 3], s3);
-    }
-    double sum = (s0 + s1) + (s2 + s3);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    if (q == (j & 3)) X[r][j] = (X[r][j] - sum) * rdiag[j];
-    __syncwarp();
+  for (int c = 0; c < 32; ++c) {
+    a[c] = (c <= lane) ? A[lane * kLd + c] : 0.0;
+    sx[c] = (c == lane) ? 1.0 : 0.0;
   }
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double* cb = colbuf[j & 1];
+    cb[lane] = a[j];
+    __syncwarp();
+    const double d = cb[j];
+    fail = (fail < 0 && !(d > 0.0)) ? j : fail;
+    const double dinv = fast_rcp(d);
+    rsq[j] = fast_rsqrt(d);
+    const double t = a[j] * dinv;
+    const double y = sx[j] * dinv;
+#pragma unroll
+    for (int c = (j + 1) & ~1; c < 32; c += 2) {
+      const double2 lc = *reinterpret_cast<const double2*>(cb + c);
+      if (c > j) {
+        a[c] = fma(-t, lc.x, a[c]);
+        sx[c] = fma(-lc.x, y, sx[c]);
+      }
+      a[c + 1] = fma(-t, lc.y, a[c + 1]);
+      sx[c + 1] = fma(-lc.y, y, sx[c + 1]);
+    }
+  }
+  if (fail < 0) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      A[lane * kLd + c] = (c <= lane) ? a[c] * rsq[c] : 0.0;
+      X[c * kLd + lane] = sx[c] * rsq[c];
+    }
+  }
+  return fail;
+}
+
+// C = A B^T (kNT) or A B on 32x32 windows (stride kLd), all 256 threads, 2x2 outputs each.
+template <bool kNT>
+__device__ void gemm32(const double* A, const double* B, double acc[2][2]) {
+  const int r = (threadIdx.x >> 4) * 2, c = (threadIdx.x & 15) * 2;
+  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+#pragma unroll 8
+  for (int p = 0; p < 32; ++p) {
+    const double a0 = A[r * kLd + p], a1 = A[(r + 1) * kLd + p];
+    const double b0 = kNT ? B[c * kLd + p] : B[p * kLd + c];
+    const double b1 = kNT ? B[(c + 1) * kLd + p] : B[p * kLd + c + 1];
+    acc[0][0] = fma(a0, b0, acc[0][0]); acc[0][1] = fma(a0, b1, acc[0][1]);
+    acc[1][0] = fma(a1, b0, acc[1][0]); acc[1][1] = fma(a1, b1, acc[1][1]);
+  }
+}
+
+__device__ void store32(double* C, const double acc[2][2], double scale, bool accumulate) {
+  const int r = (threadIdx.x >> 4) * 2, c = (threadIdx.x & 15) * 2;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double* d = C + (r + i) * kLd + c + j;
+      *d = (accumulate ? *d : 0.0) + scale * acc[i][j];
+    }
+}
+
+// A (64x64 smem, identity-padded lower) = L L^T in place, X = L^-1; T scratch.  Returns the
+// first failing local pivot or -1 (block-uniform).
+//   [L00 0; L10 L11]:  L00 = chol(A00), L10 = A10 L00^-T, L11 = chol(A11 - L10 L10^T)
+//   [X00 0; X10 X11]:  X00 = L00^-1, X11 = L11^-1, X10 = -X11 L10 X00
+__device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) {
+  __shared__ int sfail;
+  __shared__ __align__(16) double colbuf[2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const int f = warp_chol_inv32(&A[0][0], &X[0][0], colbuf);
+    if (lane == 0) sfail = f;
+  } else if (warp == 1) {
+    for (int c = 0; c < 32; ++c) X[lane][32 + c] = 0.0;
+  }
+  __syncthreads();
+  if (sfail >= 0) return sfail;
+  double acc[2][2];
+  gemm32<true>(&A[32][0], &X[0][0], acc);          // L10 = A10 X00^T
+  __syncthreads();
+  store32(&A[32][0], acc, 1.0, false);
+  __syncthreads();
+  gemm32<true>(&A[32][0], &A[32][0], acc);         // A11 -= L10 L10^T (reads A10, writes A11)
+  store32(&A[32][32], acc, -1.0, true);
+  __syncthreads();
+  if (warp == 0) {
+    const int f = warp_chol_inv32(&A[32][32], &X[32][32], colbuf);
+    if (lane == 0) sfail = f < 0 ? -1 : 32 + f;
+  }
+  __syncthreads();
+  if (sfail >= 0) return sfail;
+  gemm32<false>(&A[32][0], &X[0][0], acc);         // T = L10 X00
+  store32(&T[0][0], acc, 1.0, false);
+  __syncthreads();
+  gemm32<false>(&X[32][32], &T[0][0], acc);        // X10 = -X11 T
+  store32(&X[32][0], acc, -1.0, false);
+  __syncthreads();
+  return -1;
 }
 
 // C (64x64, smem) = A (64x64 smem) * B^T (64x64 smem); each thread a 4x4 sub-block.
@@ -193,11 +242,39 @@ __device__ void gemm_nt(const double (*A)[kLd], const double (*B)[kLd], double a
   }
 }
 
+// 64x64 tile -> smem: all 16 loads of a thread are issued before its first store (L2
+// latency once per tile, not once per element).
+constexpr int kPer = kNB * kNB / kThreads;   // 16 elements per thread
 __device__ void load_tile(const double* W, int64_t n, int64_t ld, int64_t r0, int64_t c0, double (*T)[kLd]) {
-  for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
-    const int r = e / kNB, c = e % kNB;
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
     const int64_t gr = r0 + r, gc = c0 + c;
-    T[r][c] = (gr < n && gc < n) ? W[gr * ld + gc] : 0.0;
+    v[u] = (gr < n && gc < n) ? W[gr * ld + gc] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = u * kThreads + threadIdx.x;
+    T[e >> 6][e & 63] = v[u];
+  }
+}
+
+// dst rows [rb, rb+64) x 64 columns <- src (row-major, 64 per row), batched like load_tile
+__device__ void copy_panel(double* __restrict__ dst, int64_t ld, const double* __restrict__ src, int64_t rb,
+                           int64_t n) {
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = u * kThreads + threadIdx.x;
+    const int64_t gr = rb + (e >> 6);
+    v[u] = gr < n ? src[gr * kNB + (e & 63)] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = u * kThreads + threadIdx.x;
+    const int64_t gr = rb + (e >> 6);
+    if (gr < n) dst[gr * ld + (e & 63)] = v[u];
   }
 }
 
@@ -209,25 +286,30 @@ __device__ void tile_coords(int t, int& I, int& J) {  // lower tiles in row-majo
   J = t - i * (i + 1) / 2;
 }
 
-// Factor diagonal block kk of W (already fully updated) in place.
-__device__ void factor_diag(double* W, int64_t n, int64_t ld, int kk, int64_t* status, double (*A)[kLd], int* fail) {
+// Factor diagonal block kk of W (already fully updated) in place and store its inverse in
+// Linv[kk] (dense 64x64, identity-padded).  A, X, T: three smem tiles.
+__device__ void factor_diag(double* W, int64_t n, int64_t ld, int kk, int64_t* status, double* Linv,
+                            double (*A)[kLd], double (*X)[kLd], double (*T)[kLd], bool preloaded) {
   const int64_t r0 = (int64_t)kk * kNB;
   const int b = (int)(n - r0 < kNB ? n - r0 : kNB);
-  load_tile(W, n, ld, r0, r0, A);
+  if (!preloaded) load_tile(W, n, ld, r0, r0, A);
   __syncthreads();
   for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {   // identity padding, lower only
     const int r = e >> 6, c = e & 63;
     if (c > r) A[r][c] = 0.0;
     else if (r >= b) A[r][c] = (r == c) ? 1.0 : 0.0;
   }
-  factor_block(A, b, fail);
-  if (*fail >= 0) {
-    if (threadIdx.x == 0) *status = r0 + *fail + 1;
+  __syncthreads();
+  const int f = chol_inv64(A, X, T);
+  if (f >= 0) {
+    if (threadIdx.x == 0) *status = r0 + f + 1;
     return;
   }
+  double* li = Linv + (size_t)kk * kNB * kNB;
   for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
     const int r = e >> 6, c = e & 63;
     if (r < b && c <= r) W[(r0 + r) * ld + r0 + c] = A[r][c];
+    li[e] = X[r][c];
   }
 }
 
@@ -246,23 +328,23 @@ __global__ void unpack_lower_kernel(const double* __restrict__ Gp, int64_t n, do
 constexpr size_t kTileSmem = sizeof(double) * kNB * kLd;
 
 __global__ void __launch_bounds__(kThreads)
-potrf_first_kernel(double* W, int64_t n, int64_t ld, int64_t* status) {
+potrf_first_kernel(double* W, int64_t n, int64_t ld, double* Linv, int64_t* status) {
   extern __shared__ double dsm[];
   double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
-  __shared__ int fail;
+  double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+  double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
   if (*(volatile int64_t*)status != 0) return;
-  factor_diag(W, n, ld, 0, status, A, &fail);
+  factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
 }
 
 // Step k: tiles (I, J) of the trailing matrix, k < J <= I < nb, indexed relative to k+1.
 __global__ void __launch_bounds__(kThreads)
-potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* panel0, double* panel1, int64_t* status) {
+potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double* panel0, double* panel1,
+                  int64_t* status) {
   extern __shared__ double dsm[];
-  double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);              // L_kk, later scratch
+  double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);              // Linv_kk, later scratch
   double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
   double (*XJ)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
-  __shared__ double rdiag[kNB];
-  __shared__ int fail;
   if (*(volatile int64_t*)status != 0) return;
   int I, J;
   tile_coords(blockIdx.x, I, J);
@@ -274,28 +356,29 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* panel0, doubl
   // materialise the previous panel L_{.,k-1} into W (nobody reads W column k-1 any more):
   // row block I by the CTA (I, k+1); row block k by the diagonal CTA (k+1, k+1)
   if (J == k + 1 && k >= 1) {
-    for (int pass = 0; pass < (I == k + 1 ? 2 : 1); ++pass) {
-      const int64_t rb = pass == 0 ? rI : kc;
-      for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
-        const int r = e >> 6, c = e & 63;
-        const int64_t gr = rb + r;
-        if (gr < n) W[gr * ld + (kc - kNB) + c] = pan_prev[gr * kNB + c];
-      }
-    }
+    copy_panel(W + (kc - kNB), ld, pan_prev, rI, n);
+    if (I == k + 1) copy_panel(W + (kc - kNB), ld, pan_prev, kc, n);
   }
-  load_tile(W, n, ld, kc, kc, Lk);                 // L_kk (factored by the previous step)
+  {
+    const double* li = Linv + (size_t)k * kNB * kNB;
+    for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) Lk[e >> 6][e & 63] = li[e];
+  }
   load_tile(W, n, ld, rI, kc, XI);                 // A_Ik
   if (I != J) load_tile(W, n, ld, rJ, kc, XJ);     // A_Jk
   __syncthreads();
-  if (threadIdx.x < kNB) {
-    const int j = threadIdx.x;
-    const double d = Lk[j][j];
-    rdiag[j] = (kc + j < n) ? 1.0 / d : 1.0;
-    if (kc + j >= n) Lk[j][j] = 1.0;
-  }
+  // X_I = A_Ik Linv_kk^T, X_J = A_Jk Linv_kk^T (the panel TRSM as GEMMs)
+  double accI[4][4], accJ[4][4];
+  gemm_nt(XI, Lk, accI);
+  if (I != J) gemm_nt(XJ, Lk, accJ);
   __syncthreads();
-  trsm_rows(Lk, rdiag, XI);                        // X_I = A_Ik L_kk^-T
-  if (I != J) trsm_rows(Lk, rdiag, XJ);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      XI[ty + 16 * i][tx + 16 * j] = accI[i][j];
+      if (I != J) XJ[ty + 16 * i][tx + 16 * j] = accJ[i][j];
+    }
   __syncthreads();
   if (J == k + 1) {   // store the panel L_Ik
     for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
@@ -304,20 +387,33 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* panel0, doubl
       if (gr < n) pan_cur[gr * kNB + c] = XI[r][c];
     }
   }
-  // A_IJ -= X_I X_J^T
-  double acc[4][4];
-  gemm_nt(XI, (I != J) ? XJ : XI, acc);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // A_IJ -= X_I X_J^T (old values loaded up front, the GEMM overlaps their latency)
+  double old[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t gi = rI + ty + 16 * i, gj = rJ + tx + 16 * j;
-      if (gi < n && gj <= gi) W[gi * ld + gj] -= acc[i][j];
+      old[i][j] = (gi < n && gj <= gi) ? W[gi * ld + gj] : 0.0;
+    }
+  double acc[4][4];
+  gemm_nt(XI, (I != J) ? XJ : XI, acc);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gi = rI + ty + 16 * i, gj = rJ + tx + 16 * j;
+      acc[i][j] = old[i][j] - acc[i][j];
+      if (gi < n && gj <= gi) W[gi * ld + gj] = acc[i][j];
     }
   if (I == J && I == k + 1) {
-    __syncthreads();   // (block-uniform branch) this CTA's tile update is complete and visible
-    factor_diag(W, n, ld, I, status, Lk, &fail);
+    // (block-uniform branch) the updated diagonal tile goes straight into smem for its factor
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Lk[ty + 16 * i][tx + 16 * j] = acc[i][j];
+    factor_diag(W, n, ld, I, status, Linv, Lk, XI, XJ, true);
   }
 }
 
@@ -390,16 +486,17 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
   double* panel1 = panel0 + n * kNB;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(potrf_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSmem));
+    cudaFuncSetAttribute(potrf_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
     cudaFuncSetAttribute(potrf_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
     attr = true;
   }
   int count = 0;
-  potrf_first_kernel<<<1, kThreads, kTileSmem, st>>>(W, n, ldW, d_status);
+  potrf_first_kernel<<<1, kThreads, 3 * kTileSmem, st>>>(W, n, ldW, Linv, d_status);
   ++count;
   for (int k = 0; k + 1 < nb; ++k) {
     const int t = nb - k - 1;   // trailing block count
-    potrf_step_kernel<<<t * (t + 1) / 2, kThreads, 3 * kTileSmem, st>>>(W, n, ldW, k, panel0, panel1, d_status);
+    potrf_step_kernel<<<t * (t + 1) / 2, kThreads, 3 * kTileSmem, st>>>(W, n, ldW, k, Linv, panel0, panel1,
+                                                                          d_status);
     ++count;
   }
   if (nb >= 2) {
@@ -408,8 +505,7 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
     ++count;
   }
   if (launches) *launches += count;
-  // inverted diagonal blocks for the TRSV pair (all blocks in parallel, off the factor's path)
-  return invert_diag_blocks(W, n, ldW, Linv, st, launches);
+  return cudaGetLastError();   // Linv (the TRSV pair's inverted diagonal blocks) comes with the factor
 }
 
 }  // namespace fs
