@@ -309,11 +309,17 @@ def run_b200(args, rank, world, local):
     es = dtype.itemsize
     gemv = {}
     if st.get("gemv_sv"):
-        bytes_sv = n * m_local * es + m_local * es + n * 8
+        # tf32x3: the retile pass reads S once and writes the tiled copy S_t (tiles.cuh) + u = S v
+        tiles = (-(-n // 256) * 256) * (-(-m_local // 32) * 32) * 4 if args.precision == "tf32x3" else 0
+        bytes_sv = n * m_local * es + tiles + m_local * es + n * 8
         gemv["gemv_sv_GBps"] = bytes_sv / (st["gemv_sv"] * 1e-3) / 1e9
     if st.get("gemv_stz"):
+        # fused x = (v - S^T z)/lam and y = S x: S from HBM once (its second read hits L2)
         bytes_stz = n * m_local * es + m_local * es + m_local * 8 + n * 8
         gemv["gemv_stz_GBps"] = bytes_stz / (st["gemv_stz"] * 1e-3) / 1e9
+    if st.get("residual"):
+        bytes_res = n * m_local * es + m_local * (es + 8) + n * 8
+        gemv["residual_GBps"] = bytes_res / (st["residual"] * 1e-3) / 1e9
     if gemv:
         gemv = {"bound": "hbm", "peak": pk["hbm_gbs"], "unit": "GB/s",
                 **gemv, **{k.replace("GBps", "frac"): val / pk["hbm_gbs"] for k, val in list(gemv.items())}}

@@ -205,15 +205,36 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
   prof_mark(ctx, FS_PROF_TRSV, st);
-  // 3. x = (v - S^T z) / lam on the local shard
-  if ((rc = fs_gemv_cols_solve(ctx, dtype, S, n, m, ldS, ctx->d_z, v, vdt, lam, 0, x, stream))) return rc;
-  prof_mark(ctx, FS_PROF_GEMV_STZ, st);
   const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
   const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
+  // 3. x = (v - S^T z) / lam on the local shard; with diagnostics fused with y = S x (one
+  //    HBM pass; falls back to two passes when n is too large for the fused kernel)
+  bool y_ready = false;
+  auto solve_cols = [&](const void* rhs, int rhs_f64, double l, bool accumulate) -> int {
+    int lc = 0;
+    cudaError_t e = cudaErrorNotSupported;
+    if (want_res)
+      e = fs::gemv_cols_solve_y(dtype == FS_F64, S, n, m, ldS, ctx->d_z, rhs, rhs_f64, l, accumulate, x,
+                                ctx->d_partials, fs::gemv_rows_chunks(ctx->m_max, true) * ctx->n_max / n, ctx->d_y,
+                                ctx->num_sms,
+                                st, &lc);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      y_ready = false;
+      e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, ctx->d_z, rhs, rhs_f64, l, accumulate, x, st, &lc);
+    } else {
+      y_ready = true;
+    }
+    ctx->launches += lc;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve");
+    return FS_OK;
+  };
+  if ((rc = solve_cols(v, vdt == FS_F64, lam, false))) return rc;
+  prof_mark(ctx, FS_PROF_GEMV_STZ, st);
   double abs_res = NAN, rel_res = NAN;
   for (int pass = 0; want_res && pass < 2; ++pass) {
     // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
-    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
+    if (!y_ready && (rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
     if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
       return fail(ctx, FS_ECUDA, "allreduce of y failed");
     {
@@ -246,13 +267,7 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
       if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
     }
     // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
-    {
-      int l = 0;
-      cudaError_t e = fs::gemv_cols_solve(dtype == FS_F64, S, n, m, ldS, ctx->d_z, ctx->d_r, true, -lam,
-                                          true, x, st, &l);
-      ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve (refine)");
-    }
+    if ((rc = solve_cols(ctx->d_r, 1, -lam, true))) return rc;
   }
   if (!want_res) {
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
@@ -385,8 +400,16 @@ int fs_gemv_rows(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, in
   if (rc) return rc;
   if (!w || !u) return fail(ctx, FS_EINVAL, "NULL vector");
   int l = 0;
-  cudaError_t e = fs::gemv_rows(dtype == FS_F64, S, n, m, ldS, w, wdtype == FS_F64, ctx->d_partials, u,
-                                (cudaStream_t)stream, &l);
+  cudaError_t e = cudaErrorNotSupported;
+  if (wdtype == FS_F64)   // exact fp64 products: the panel pass (same order as the fused solve's y)
+    e = fs::gemv_rows_panel(dtype == FS_F64, S, n, m, ldS, (const double*)w, ctx->d_partials,
+                            fs::gemv_rows_chunks(ctx->m_max, true) * ctx->n_max / n, u, ctx->num_sms,
+                            (cudaStream_t)stream, &l);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    e = fs::gemv_rows(dtype == FS_F64, S, n, m, ldS, w, wdtype == FS_F64, ctx->d_partials, u, (cudaStream_t)stream,
+                      &l);
+  }
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_rows");
   return FS_OK;

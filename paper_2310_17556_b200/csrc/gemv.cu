@@ -12,6 +12,8 @@
 #include "kernels.h"
 #include "tiles.cuh"
 
+#include <algorithm>
+
 namespace fs {
 namespace {
 
@@ -243,6 +245,162 @@ gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t l
   }
 }
 
+// Fused x = (v - S^T z)/λ (optionally x += ...) and the residual's first product y = S x.
+// Persistent CTAs (one per SM; 512 threads = 16 column groups of one 16-byte vector x 32 row
+// groups) walk column panels of 256-byte row segments (fp32: 64 columns).  Per panel:
+//   (1) x: each thread sums its rows' z-weighted vectors (Zt partial sums of 8 rows, fp64
+//       across them); the row groups are added in fixed order (warp xor, then warps) -> x;
+//   (2) y: the panel is read again (L2 hit) and S[i, panel] . x[panel] (exact fp64 products)
+//       is added to a per-CTA smem accumulator yacc[column group][row] (one owner per slot).
+// At the end each CTA writes sum_cg yacc[cg][.] as its y partial; reduce_chunks adds the CTA
+// partials in order.  S leaves HBM once instead of twice (gemv_cols_solve + gemv_rows).
+constexpr int kCYThreads = 512;
+constexpr int kCYCG = 16;                      // column groups: 256-byte fp32 row segments
+constexpr int kCYRG = kCYThreads / kCYCG;      // 32 row groups
+constexpr int kCYWarps = kCYThreads / kWarp;   // 16 (2 row groups each)
+constexpr int kCYU = 8;                        // rows per unrolled batch (per thread)
+
+template <typename TS> constexpr int cy_cols() { return kCYCG * VecOf<TS>::N; }
+
+// yacc row stride: n rounded to 16 plus one (the 16 column groups of a row on distinct banks)
+__host__ __device__ inline int64_t cy_pitch(int64_t n) { return ((n + 15) & ~(int64_t)15) + 1; }
+
+template <typename TS>
+size_t cy_smem_bytes(int64_t n) {
+  return (size_t)kCYCG * cy_pitch(n) * sizeof(double) + (size_t)kCYWarps * cy_cols<TS>() * sizeof(double) +
+         cy_cols<TS>() * sizeof(double) + (size_t)n * sizeof(double);
+}
+
+template <typename TS, typename TV>
+__global__ void __launch_bounds__(kCYThreads, 1)
+cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS, const double* __restrict__ z,
+                    const TV* __restrict__ v, double lam, int accumulate, double* __restrict__ x,
+                    double* __restrict__ ypart, int y_only) {
+  using VT = typename VecOf<TS>::V;
+  constexpr int VN = VecOf<TS>::N;
+  constexpr int CW = cy_cols<TS>();
+  using Zt = typename std::conditional<sizeof(TV) == 8, double, float>::type;
+  extern __shared__ double cy_sm[];
+  const int64_t P = cy_pitch(n);
+  double* yacc = cy_sm;                                   // [kCYCG][P]
+  double* red = yacc + (size_t)kCYCG * P;                 // [kCYWarps][CW]
+  double* xs = red + kCYWarps * CW;                       // [CW]
+  double* zs = xs + CW;                                   // [n]
+  const int cg = threadIdx.x % kCYCG, rg = threadIdx.x / kCYCG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (!y_only)
+    for (int64_t i = threadIdx.x; i < n; i += kCYThreads) zs[i] = z[i];
+  for (int64_t i = threadIdx.x; i < (int64_t)kCYCG * P; i += kCYThreads) yacc[i] = 0.0;
+  const int64_t panels = (m + CW - 1) / CW;
+  __syncthreads();
+  for (int64_t q = blockIdx.x; q < panels; q += gridDim.x) {
+    const int64_t col = q * CW + cg * VN;
+    const bool full = col + VN <= m;
+    if (y_only) {
+      if (threadIdx.x < CW) {
+        const int64_t c = q * CW + threadIdx.x;
+        xs[threadIdx.x] = c < m ? x[c] : 0.0;
+      }
+    } else {
+      // ---- (1) x for the panel ----
+      double acc[VN];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[e] = 0.0;
+      if (col < m) {
+        for (int64_t i0 = rg; i0 < n; i0 += (int64_t)kCYRG * kCYU) {
+          Zt part[VN];
+#pragma unroll
+          for (int e = 0; e < VN; ++e) part[e] = 0;
+          if (full && i0 + (int64_t)kCYRG * (kCYU - 1) < n) {
+            VT buf[kCYU];
+#pragma unroll
+            for (int u = 0; u < kCYU; ++u) buf[u] = __ldg(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col));
+#pragma unroll
+            for (int u = 0; u < kCYU; ++u) {
+              TS a[VN];
+              vec_to_array(buf[u], a);
+#pragma unroll
+              for (int e = 0; e < VN; ++e) part[e] = fma((Zt)zs[i0 + kCYRG * u], (Zt)a[e], part[e]);
+            }
+          } else {
+            for (int u = 0; u < kCYU; ++u) {
+              const int64_t i = i0 + kCYRG * u;
+              if (i >= n) break;
+#pragma unroll
+              for (int e = 0; e < VN; ++e)
+                if (col + e < m) part[e] = fma((Zt)zs[i], (Zt)__ldg(S + i * ldS + col + e), part[e]);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < VN; ++e) acc[e] += (double)part[e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);   // the warp's 2 row groups
+      if (lane < kCYCG) {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) red[warp * CW + cg * VN + e] = acc[e];
+      }
+      __syncthreads();
+      if (threadIdx.x < CW) {
+        const int t = threadIdx.x;
+        double sum = 0.0;
+#pragma unroll
+        for (int g = 0; g < kCYWarps; ++g) sum += red[g * CW + t];
+        const int64_t c = q * CW + t;
+        double xv = 0.0;
+        if (c < m) {
+          xv = ((double)v[c] - sum) / lam;   // true IEEE division, as gemv_cols_solve
+          if (accumulate) xv = x[c] + xv;
+          x[c] = xv;
+        }
+        xs[t] = xv;
+      }
+    }
+    __syncthreads();
+    // ---- (2) y += S[:, panel] x[panel] (exact fp64 products; the panel is re-read from L2) ----
+    if (col < m) {
+      double xv[VN];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) xv[e] = xs[cg * VN + e];
+      double* ya = yacc + (size_t)cg * P;
+      for (int64_t i0 = rg; i0 < n; i0 += (int64_t)kCYRG * kCYU) {
+        if (full && i0 + (int64_t)kCYRG * (kCYU - 1) < n) {
+          VT buf[kCYU];
+#pragma unroll
+          for (int u = 0; u < kCYU; ++u) buf[u] = ld_stream(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col));
+#pragma unroll
+          for (int u = 0; u < kCYU; ++u) {
+            TS a[VN];
+            vec_to_array(buf[u], a);
+            double p = 0.0;
+#pragma unroll
+            for (int e = 0; e < VN; ++e) p = fma((double)a[e], xv[e], p);
+            ya[i0 + kCYRG * u] += p;
+          }
+        } else {
+          for (int u = 0; u < kCYU; ++u) {
+            const int64_t i = i0 + kCYRG * u;
+            if (i >= n) break;
+            double p = 0.0;
+#pragma unroll
+            for (int e = 0; e < VN; ++e)
+              if (col + e < m) p = fma((double)__ldg(S + i * ldS + col + e), xv[e], p);
+            ya[i] += p;
+          }
+        }
+      }
+    }
+    __syncthreads();   // xs / red reuse by the next panel
+  }
+  for (int64_t i = threadIdx.x; i < n; i += kCYThreads) {
+    double sum = 0.0;
+#pragma unroll
+    for (int g = 0; g < kCYCG; ++g) sum += yacc[(size_t)g * P + i];
+    ypart[(int64_t)blockIdx.x * n + i] = sum;
+  }
+}
+
 // r = S^T y + λx - v with exact fp64 products; per-block ||r||², ||v||² partials.
 template <typename TS, typename TV, bool kVec>
 __global__ void __launch_bounds__(kColThreads)
@@ -390,6 +548,33 @@ cudaError_t gemv_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const do
 }
 
 template <typename TS>
+cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const double* z, const void* v,
+                           bool v_f64, double lam, bool accumulate, double* x, double* ypart, int64_t ypart_rows,
+                           double* y, int num_sms, cudaStream_t st, int* launches, int y_only = 0) {
+  // one support rule and one grid size for the fused pass and the y-only pass, so that a
+  // recomputed y = S x is bit-identical to the solve's (test_solvers.py:109-114)
+  const size_t smem = cy_smem_bytes<TS>(n);
+  if (smem > 200 * 1024 || !aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
+  const int64_t panels = (m + cy_cols<TS>() - 1) / cy_cols<TS>();
+  const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
+  int64_t G = std::min<int64_t>((int64_t)num_sms, std::min(panels, cap));
+  if (ypart_rows < G) return cudaErrorInvalidValue;
+  const int acc = accumulate ? 1 : 0;
+  if (v_f64) {
+    auto kfn = cols_solve_y_kernel<TS, double>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const double*)v, lam, acc, x, ypart, y_only);
+  } else {
+    auto kfn = cols_solve_y_kernel<TS, float>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const float*)v, lam, acc, x, ypart, y_only);
+  }
+  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(ypart, G, n, n, y);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+template <typename TS>
 cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const double* y,
                             const double* x, const void* v, bool v_f64, double lam, double* r,
                             double* block_sums, double* sums, cudaStream_t st, int* launches) {
@@ -488,6 +673,26 @@ cudaError_t gemv_cols_solve(bool s_f64, const void* S, int64_t n, int64_t m, int
                             double* x, cudaStream_t st, int* launches) {
   if (s_f64) return gemv_cols_t<double>((const double*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, st, launches);
   return gemv_cols_t<float>((const float*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, st, launches);
+}
+
+cudaError_t gemv_cols_solve_y(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const double* z,
+                              const void* v, bool v_f64, double lam, bool accumulate, double* x, double* ypart,
+                              int64_t ypart_rows, double* y, int num_sms, cudaStream_t st, int* launches) {
+  if (s_f64)
+    return cols_solve_y_t<double>((const double*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y,
+                                  num_sms, st, launches);
+  return cols_solve_y_t<float>((const float*)S, n, m, ldS, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y,
+                               num_sms, st, launches);
+}
+
+cudaError_t gemv_rows_panel(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const double* x,
+                            double* ypart, int64_t ypart_rows, double* y, int num_sms, cudaStream_t st,
+                            int* launches) {
+  if (s_f64)
+    return cols_solve_y_t<double>((const double*)S, n, m, ldS, nullptr, x, true, 1.0, false, const_cast<double*>(x),
+                                  ypart, ypart_rows, y, num_sms, st, launches, 1);
+  return cols_solve_y_t<float>((const float*)S, n, m, ldS, nullptr, x, true, 1.0, false, const_cast<double*>(x), ypart,
+                               ypart_rows, y, num_sms, st, launches, 1);
 }
 
 cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,

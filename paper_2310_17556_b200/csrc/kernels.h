@@ -30,6 +30,18 @@ cudaError_t gemv_cols_solve(bool s_f64, const void* S, int64_t n, int64_t m, int
                             const double* z, const void* v, bool v_f64, double lam, bool accumulate,
                             double* x, cudaStream_t st, int* launches);
 int64_t residual_cols_blocks(int64_t m, bool s_is_f64);
+// x = (v - S^T z)/lam (x += ... if accumulate) fused with y = S x (exact fp64 products):
+// one HBM pass, the second read of each column panel hits L2.  ypart: >= ypart_rows x n
+// doubles of scratch.  Returns cudaErrorNotSupported when n is too large for the per-CTA
+// accumulators (callers then run gemv_cols_solve + gemv_rows).
+cudaError_t gemv_cols_solve_y(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const double* z,
+                              const void* v, bool v_f64, double lam, bool accumulate, double* x, double* ypart,
+                              int64_t ypart_rows, double* y, int num_sms, cudaStream_t st, int* launches);
+// y = S x (fp64 x, exact fp64 products) with the panel order of gemv_cols_solve_y (same
+// support rule: cudaErrorNotSupported -> use gemv_rows)
+cudaError_t gemv_rows_panel(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, const double* x,
+                            double* ypart, int64_t ypart_rows, double* y, int num_sms, cudaStream_t st,
+                            int* launches);
 cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS,
                           const double* y, const double* x, const void* v, bool v_f64, double lam,
                           double* r, double* block_sums, double* sums, cudaStream_t st,
