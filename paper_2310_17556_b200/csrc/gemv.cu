@@ -87,7 +87,7 @@ gemv_rows_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 // fp32 u = S w that also writes the tiled copy S_t (tiles.cuh) of the CTA's column chunk:
 // each lane's float4 is exactly one 16-byte chunk of one tile row, so every warp store is
 // four full 128-byte tile rows.  Columns in [m, KB*32) and rows in [n, nb*128) are zeroed.
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, 2)
 gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
                         const float* __restrict__ w, double* __restrict__ partials, uint8_t* __restrict__ St,
                         int has_w, int vec_ok, int64_t r0, int64_t r1, int64_t rz, int* __restrict__ nonfinite,
@@ -98,14 +98,18 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
   const int64_t cb = cb0 + blockIdx.x;                   // global column chunk
   const int64_t c0 = cb * CW;
   const int64_t nb = tiles_nb(n), KB = tiles_kb(m);
-  float wr[kRowUnroll][VN];
-#pragma unroll
-  for (int u = 0; u < kRowUnroll; ++u)
+  // the chunk's weights live in smem (registers go to the loads in flight: 2 CTAs per SM)
+  __shared__ float4 wsm[CW / VN];
+  for (int t = threadIdx.x; t < CW / VN; t += kRowThreads) {
+    float a[VN];
 #pragma unroll
     for (int e = 0; e < VN; ++e) {
-      const int64_t c = c0 + (int64_t)(u * kWarp + lane) * VN + e;
-      wr[u][e] = (has_w && c < m) ? w[c] : 0.f;
+      const int64_t c = c0 + (int64_t)t * VN + e;
+      a[e] = (has_w && c < m) ? w[c] : 0.f;
     }
+    wsm[t] = make_float4(a[0], a[1], a[2], a[3]);
+  }
+  __syncthreads();
   const bool full = vec_ok && c0 + CW <= m;
   const int chunk = lane & 7;
   // rows [r0, r1) are read from S; rows [r1, rz) are zero padding of the tiled copy
@@ -143,8 +147,9 @@ gemv_rows_retile_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64
       float acc = 0.f;
 #pragma unroll
       for (int u = 0; u < kRowUnroll; ++u) {
-        acc = fmaf(buf[u].x, wr[u][0], acc); acc = fmaf(buf[u].y, wr[u][1], acc);
-        acc = fmaf(buf[u].z, wr[u][2], acc); acc = fmaf(buf[u].w, wr[u][3], acc);
+        const float4 wv = wsm[u * kWarp + lane];
+        acc = fmaf(buf[u].x, wv.x, acc); acc = fmaf(buf[u].y, wv.y, acc);
+        acc = fmaf(buf[u].z, wv.z, acc); acc = fmaf(buf[u].w, wv.w, acc);
       }
       const double s = warp_sum((double)acc);
       if (lane == 0) partials[cb * n + i] = s;
@@ -246,8 +251,8 @@ gemv_cols_solve_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t l
 }
 
 // Fused x = (v - S^T z)/λ (optionally x += ...) and the residual's first product y = S x.
-// Persistent CTAs (one per SM; 512 threads = 16 column groups of one 16-byte vector x 32 row
-// groups) walk column panels of 256-byte row segments (fp32: 64 columns).  Per panel:
+// Persistent CTAs (one per SM; 512 threads = 16 column groups of two 16-byte vectors x 32 row
+// groups) walk column panels of 512-byte row segments (fp32: 128 columns).  Per panel:
 //   (1) x: each thread sums its rows' z-weighted vectors (Zt partial sums of 8 rows, fp64
 //       across them); the row groups are added in fixed order (warp xor, then warps) -> x;
 //   (2) y: the panel is read again (L2 hit) and S[i, panel] . x[panel] (exact fp64 products)
@@ -259,8 +264,9 @@ constexpr int kCYCG = 16;                      // column groups: 256-byte fp32 r
 constexpr int kCYRG = kCYThreads / kCYCG;      // 32 row groups
 constexpr int kCYWarps = kCYThreads / kWarp;   // 16 (2 row groups each)
 constexpr int kCYU = 8;                        // rows per unrolled batch (per thread)
+constexpr int kCYV = 2;                        // adjacent 16-byte vectors per thread and row
 
-template <typename TS> constexpr int cy_cols() { return kCYCG * VecOf<TS>::N; }
+template <typename TS> constexpr int cy_cols() { return kCYCG * kCYV * VecOf<TS>::N; }
 
 // yacc row stride: n rounded to 16 plus one (the 16 column groups of a row on distinct banks)
 __host__ __device__ inline int64_t cy_pitch(int64_t n) { return ((n + 15) & ~(int64_t)15) + 1; }
@@ -277,7 +283,8 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
                     const TV* __restrict__ v, double lam, int accumulate, double* __restrict__ x,
                     double* __restrict__ ypart, int y_only) {
   using VT = typename VecOf<TS>::V;
-  constexpr int VN = VecOf<TS>::N;
+  constexpr int VN1 = VecOf<TS>::N;
+  constexpr int VN = VN1 * kCYV;                // columns per thread
   constexpr int CW = cy_cols<TS>();
   using Zt = typename std::conditional<sizeof(TV) == 8, double, float>::type;
   extern __shared__ double cy_sm[];
@@ -312,13 +319,17 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 #pragma unroll
           for (int e = 0; e < VN; ++e) part[e] = 0;
           if (full && i0 + (int64_t)kCYRG * (kCYU - 1) < n) {
-            VT buf[kCYU];
+            VT buf[kCYU][kCYV];
 #pragma unroll
-            for (int u = 0; u < kCYU; ++u) buf[u] = __ldg(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col));
+            for (int u = 0; u < kCYU; ++u)
+#pragma unroll
+              for (int w = 0; w < kCYV; ++w)
+                buf[u][w] = __ldg(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col + w * VN1));
 #pragma unroll
             for (int u = 0; u < kCYU; ++u) {
               TS a[VN];
-              vec_to_array(buf[u], a);
+#pragma unroll
+              for (int w = 0; w < kCYV; ++w) vec_to_array(buf[u][w], a + w * VN1);
 #pragma unroll
               for (int e = 0; e < VN; ++e) part[e] = fma((Zt)zs[i0 + kCYRG * u], (Zt)a[e], part[e]);
             }
@@ -366,13 +377,17 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
       double* ya = yacc + (size_t)cg * P;
       for (int64_t i0 = rg; i0 < n; i0 += (int64_t)kCYRG * kCYU) {
         if (full && i0 + (int64_t)kCYRG * (kCYU - 1) < n) {
-          VT buf[kCYU];
+          VT buf[kCYU][kCYV];
 #pragma unroll
-          for (int u = 0; u < kCYU; ++u) buf[u] = ld_stream(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col));
+          for (int u = 0; u < kCYU; ++u)
+#pragma unroll
+            for (int w = 0; w < kCYV; ++w)
+              buf[u][w] = ld_stream(reinterpret_cast<const VT*>(S + (i0 + kCYRG * u) * ldS + col + w * VN1));
 #pragma unroll
           for (int u = 0; u < kCYU; ++u) {
             TS a[VN];
-            vec_to_array(buf[u], a);
+#pragma unroll
+            for (int w = 0; w < kCYV; ++w) vec_to_array(buf[u][w], a + w * VN1);
             double p = 0.0;
 #pragma unroll
             for (int e = 0; e < VN; ++e) p = fma((double)a[e], xv[e], p);
