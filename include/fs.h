@@ -41,7 +41,11 @@ typedef enum { FS_F32 = 0, FS_F64 = 1 } fs_dtype;
 typedef enum {
   FS_PREC_FP64 = 0,   /* exact-product fp64 FMA (the reference's arithmetic)            */
   FS_PREC_TF32X3 = 1, /* fp32 input, tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, fp64 drain */
-  FS_PREC_AUTO = 2    /* FP64 for fp64 input, TF32X3 for fp32 input                     */
+  FS_PREC_AUTO = 2,   /* FP64 for fp64 input, F16X2 for fp32 input                      */
+  FS_PREC_F16X2 = 3   /* fp32 input split per row-scaled element into two fp16 planes
+                         (22 significant bits), tcgen05 kind::f16 hi*hi + hi*lo + lo*hi,
+                         fp64 drain; an fp16 overflow (a row whose magnitude range defeats
+                         the sampled scale) transparently recomputes with TF32X3           */
 } fs_precision;
 
 /* Host-supplied sum-all-reduce over ranks of `count` doubles in device memory,

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfisher_b
 
 FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED = range(6)
 FS_F32, FS_F64 = 0, 1
-FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO = 0, 1, 2
+FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO, FS_PREC_F16X2 = 0, 1, 2, 3
 FS_FLAG_RESIDUAL, FS_FLAG_REFINE = 1, 2
 PROF_STAGES = ("gram", "gemv_sv", "allreduce", "potrf", "trsv", "gemv_stz", "residual")
 

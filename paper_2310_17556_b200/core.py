@@ -318,16 +318,20 @@ def _check(ctx, rc: int, what: str):
     raise _lib.NativeLibraryError(msg)
 
 
-PRECISIONS = {"fp64": _lib.FS_PREC_FP64, "tf32x3": _lib.FS_PREC_TF32X3, "auto": _lib.FS_PREC_AUTO}
+PRECISIONS = {"fp64": _lib.FS_PREC_FP64, "tf32x3": _lib.FS_PREC_TF32X3, "f16x2": _lib.FS_PREC_F16X2,
+              "auto": _lib.FS_PREC_AUTO}
 
 
 def resolve_precision(precision: str, dtype: torch.dtype) -> str:
+    """fp64: exact fp64 products.  f16x2 (default for float32 scores): each element split into two
+    row-scaled fp16 planes (22 significant bits), kind::f16 tensor-core Gram.  tf32x3: the
+    kind::tf32 three-product split.  Both fp32 modes carry the stated 4 u32 sigma^2/lam bound."""
     if precision not in PRECISIONS:
         raise ValueError(f"unknown precision {precision!r}; expected one of {sorted(PRECISIONS)}")
     if precision == "auto":
-        return "tf32x3" if dtype == torch.float32 else "fp64"
-    if precision == "tf32x3" and dtype != torch.float32:
-        raise ValueError("precision 'tf32x3' needs float32 scores")
+        return "f16x2" if dtype == torch.float32 else "fp64"
+    if precision in ("tf32x3", "f16x2") and dtype != torch.float32:
+        raise ValueError(f"precision {precision!r} needs float32 scores")
     return precision
 
 

@@ -40,8 +40,12 @@ struct fs_ctx {
   size_t ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
-  uint8_t* d_St = nullptr;      // tiled fp32 copy of S for the tensor-core Gram (lazy, tiles.cuh)
+  uint8_t* d_St = nullptr;      // tiled copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
+  float* d_scale = nullptr;     // F16X2 row scales (n_max)
+  double* d_inv_scale = nullptr;
+  int* d_ovf = nullptr;         // F16X2 retile flags (bit 1: fp16 overflow)
+  int* h_ovf = nullptr;         // pinned
   // host-buffer entry (fs_chol_solve_host): device copies of S, v, x, an upload stream and
   // one event per uploaded row chunk (all lazy)
   void* d_Sin = nullptr;
@@ -126,15 +130,16 @@ int check_lam(fs_ctx* ctx, double lam) {
   return FS_OK;
 }
 
+// use_tc: 0 = fp64 SIMT, 1 = TF32X3, 2 = F16X2
 int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t ldS, int* use_tc) {
   *use_tc = 0;
   if (precision == FS_PREC_FP64) return FS_OK;
-  if (precision == FS_PREC_TF32X3 || precision == FS_PREC_AUTO) {
+  if (precision == FS_PREC_TF32X3 || precision == FS_PREC_F16X2 || precision == FS_PREC_AUTO) {
     if (dtype != FS_F32) {
       if (precision == FS_PREC_AUTO) return FS_OK;
-      return fail(ctx, FS_EUNSUPPORTED, "TF32X3 precision needs fp32 scores");
+      return fail(ctx, FS_EUNSUPPORTED, "TF32X3 / F16X2 precision needs fp32 scores");
     }
-    *use_tc = 1;
+    *use_tc = precision == FS_PREC_TF32X3 ? 1 : 2;
     return FS_OK;
   }
   return fail(ctx, FS_EINVAL, "unknown precision mode");
@@ -143,7 +148,7 @@ int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int6
 // The tiled copy S_t is sized for the context's (n_max, m_max) and allocated on the first
 // TF32X3 use (fp64-only users never pay for it).
 int ensure_tiles(fs_ctx* ctx) {
-  const size_t need = fs::tiles_bytes(ctx->n_max, ctx->m_max);
+  const size_t need = std::max(fs::tiles_bytes(ctx->n_max, ctx->m_max), fs::tiles16_bytes(ctx->n_max, ctx->m_max));
   if (ctx->St_bytes >= need) return FS_OK;
   if (ctx->d_St) cudaFree(ctx->d_St);
   ctx->d_St = nullptr;
@@ -166,7 +171,20 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
   if (rc) return rc;
   int l = 0;
   cudaError_t e;
-  if (use_tc) {
+  if (use_tc == 2) {
+    // F16X2: row scales from a sample, split planes (+ u = S w), kind::f16 SYRK.  The overflow
+    // flag is checked by the caller at its next host synchronisation.
+    if ((rc = ensure_tiles(ctx))) return rc;
+    e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = fs::row_scales((const float*)S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, &l);
+    if (e == cudaSuccess)
+      e = fs::retile16_cols((const float*)S, n, m, ldS, w32, ctx->d_partials, ctx->d_St, ctx->d_scale, 0, m,
+                            ctx->d_ovf, st, &l);
+    if (e == cudaSuccess && w32) e = fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l);
+    if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
+    if (e == cudaSuccess)
+      e = fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  } else if (use_tc) {
     if ((rc = ensure_tiles(ctx))) return rc;
     e = fs::gemv_rows_retile((const float*)S, n, m, ldS, w32, ctx->d_partials, u, ctx->d_St, st, &l);
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
@@ -184,10 +202,16 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
 
 // Everything after the Gram/u stage of _solve_chol_impl: all-reduce, potrf, _chol_apply,
 // residual, optional refinement, status + norms read-back (one host synchronisation per pass).
+// internal: the F16X2 Gram overflowed on some rank -> recompute with TF32X3
+constexpr int kRetryTf32 = 100;
+
+// ovf: F16X2 retile flag word (bit 2 = fp16 overflow) or NULL.  The bit joins the norms
+// all-reduce, so every rank takes the same retry decision.
 static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
                double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
-               double refine_above, int64_t* pivot, double* out_res, cudaStream_t st) {
+               double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf = nullptr) {
   int rc = FS_OK;
+  const int nsums = ovf ? 3 : 2;
   void* stream = (void*)st;
   double* u = ctx->d_packed + n * (n + 1) / 2;
   if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
@@ -245,12 +269,18 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
       ctx->launches += l;
       if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
     }
-    if (allreduce && allreduce(ctx->d_sums, 2, allreduce_user, stream) != 0)
+    if (ovf) {
+      int lf = 0;
+      FS_CK(fs::flag_bit_to_double(ovf, 2, ctx->d_sums + 2, st, &lf), "overflow flag");
+      ctx->launches += lf;
+    }
+    if (allreduce && allreduce(ctx->d_sums, nsums, allreduce_user, stream) != 0)
       return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
     prof_mark(ctx, FS_PROF_RESIDUAL, st);
-    FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
+    FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
+    if (ovf && ctx->h_sums[2] > 0.0) return kRetryTf32;
     if (*ctx->h_status != 0) break;
     abs_res = sqrt(ctx->h_sums[0]);
     rel_res = abs_res / std::max(sqrt(ctx->h_sums[1]), kEps);
@@ -270,8 +300,17 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     if ((rc = solve_cols(ctx->d_r, 1, -lam, true))) return rc;
   }
   if (!want_res) {
+    if (ovf) {
+      int lf = 0;
+      FS_CK(fs::flag_bit_to_double(ovf, 2, ctx->d_sums + 2, st, &lf), "overflow flag");
+      ctx->launches += lf;
+      if (allreduce && allreduce(ctx->d_sums + 2, 1, allreduce_user, stream) != 0)
+        return fail(ctx, FS_ECUDA, "allreduce of the overflow flag failed");
+      FS_CK(cudaMemcpyAsync(ctx->h_sums + 2, ctx->d_sums + 2, sizeof(double), cudaMemcpyDeviceToHost, st), "flag d2h");
+    }
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
+    if (ovf && ctx->h_sums[2] > 0.0) return kRetryTf32;
   }
   if (ctx->prof_on) {
     // each mark closes the stage it names (refinement passes fold into their stages)
@@ -332,6 +371,10 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
   A((void**)&ctx->d_syrk_ws, s.syrk);
   A((void**)&ctx->d_potrf, s.potrf);
   A((void**)&ctx->d_status, sizeof(int64_t));
+  A((void**)&ctx->d_scale, n_max * sizeof(float));
+  A((void**)&ctx->d_inv_scale, n_max * sizeof(double));
+  A((void**)&ctx->d_ovf, sizeof(int));
+  if (ok && cudaMallocHost((void**)&ctx->h_ovf, sizeof(int)) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&ctx->h_status, sizeof(int64_t)) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&ctx->h_sums, 4 * sizeof(double)) != cudaSuccess) ok = false;
   if (!ok) {
@@ -342,6 +385,7 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
   for (int i = 0; i < fs_ctx::kMaxMarks; ++i) cudaEventCreate(&ctx->ev[i]);
   ctx->ws_bytes = s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + s.r + s.syrk;
   cudaMemset(ctx->d_status, 0, sizeof(int64_t));
+  cudaMemset(ctx->d_ovf, 0, sizeof(int));
   *out = ctx;
   return FS_OK;
 }
@@ -352,6 +396,8 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_partials); cudaFree(ctx->d_block_sums); cudaFree(ctx->d_sums);
   cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
   cudaFree(ctx->d_potrf);
+  cudaFree(ctx->d_scale); cudaFree(ctx->d_inv_scale); cudaFree(ctx->d_ovf);
+  if (ctx->h_ovf) cudaFreeHost(ctx->h_ovf);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
   for (int i = 0; i < fs_ctx::kMaxMarks; ++i)
@@ -391,7 +437,16 @@ int fs_gram_packed(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t
   if (rc) return rc;
   if (!(lam >= 0.0) || !isfinite(lam)) return fail(ctx, FS_EINVAL, "diagonal shift must be finite and >= 0");
   if (!G_packed) return fail(ctx, FS_EINVAL, "G_packed is NULL");
-  return gram_impl(ctx, dtype, precision, S, n, m, ldS, lam, G_packed, (cudaStream_t)stream);
+  int use_tc = 0;
+  if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+  if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, lam, G_packed, (cudaStream_t)stream))) return rc;
+  if (use_tc == 2) {   // F16X2 overflow -> TF32X3 (one host synchronisation)
+    cudaStream_t st = (cudaStream_t)stream;
+    FS_CK(cudaMemcpyAsync(ctx->h_ovf, ctx->d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+    if (*ctx->h_ovf & 2) return gram_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, lam, G_packed, st);
+  }
+  return FS_OK;
 }
 
 int fs_gemv_rows(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS,
@@ -535,8 +590,14 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
       prof_mark(ctx, FS_PROF_GEMV_SV, st);
     }
   }
-  return solve_tail(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
-                    out_res, st);
+  int use_tc = 0;
+  resolve_precision(ctx, dtype, precision, S, ldS, &use_tc);
+  rc = solve_tail(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
+                  out_res, st, use_tc == 2 ? ctx->d_ovf : nullptr);
+  if (rc == kRetryTf32)
+    return fs_chol_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
+                         refine_above, pivot, out_res, stream);
+  return rc;
 }
 
 int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host, int64_t n, int64_t m,
@@ -619,18 +680,34 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     for (int64_t c0 = 0; c0 < m; c0 += W, ++c) {
       const int64_t c1 = std::min(m, c0 + W);
       FS_CK(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
-      FS_CK(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
-                            ctx->d_flag, st, &l),
-            "retile");
-      FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
-                        (int)(c0 / fs::kTileCols), (int)((c1 + fs::kTileCols - 1) / fs::kTileCols), c > 0),
-            "syrk_tc");
+      if (use_tc == 2) {
+        // F16X2: row scales from the first chunk's columns, then split planes + K-range SYRK
+        if (c == 0)
+          FS_CK(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
+        FS_CK(fs::retile16_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St,
+                                ctx->d_scale, c0, c1, ctx->d_flag, st, &l),
+              "retile16");
+        FS_CK(fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st,
+                           &l, (int)(c0 / fs::kTile16Cols), (int)((c1 + fs::kTile16Cols - 1) / fs::kTile16Cols),
+                           c > 0),
+              "syrk_f16");
+      } else {
+        FS_CK(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
+                              ctx->d_flag, st, &l),
+              "retile");
+        FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
+                          (int)(c0 / fs::kTileCols), (int)((c1 + fs::kTileCols - 1) / fs::kTileCols), c > 0),
+              "syrk_tc");
+      }
     }
     FS_CK(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
     ctx->launches += l;
     prof_mark(ctx, FS_PROF_GRAM, st);
     rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
-                    pivot, out_res, st);
+                    pivot, out_res, st, use_tc == 2 ? ctx->d_flag : nullptr);
+    if (rc == kRetryTf32)   // fp16 overflow: S is on the device already
+      rc = fs_chol_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
+                         refine_above, pivot, out_res, stream);
   } else {
     FS_CK(upload(0, m, 0), "S h2d");
     FS_CK(fs::check_finite(S, dtype == FS_F64, n, m, ldd, ctx->d_flag, ctx->num_sms, st, &l), "check S");
@@ -642,7 +719,7 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
   FS_CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
   if (rc == FS_OK) FS_CK(cudaMemcpyAsync(x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, st), "x d2h");
   FS_CK(cudaStreamSynchronize(st), "sync");
-  if (*ctx->h_flag) {
+  if (*ctx->h_flag & 1) {
     if (pivot) *pivot = -1;
     return fail(ctx, FS_EINVAL, "score matrix and right-hand side must contain only finite entries");
   }

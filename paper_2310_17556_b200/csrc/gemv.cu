@@ -8,6 +8,8 @@
 // sized to keep ~32–64 KB of loads in flight per SM (Little's law at ~6.5 TB/s) and
 // use 16-byte L1::no_allocate / L2::evict_first loads.  All reductions are fixed-order
 // (per-chunk partials reduced in chunk order) so results are bit-reproducible.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tiles.cuh"
@@ -606,7 +608,142 @@ cudaError_t residual_cols_t(const TS* S, int64_t n, int64_t m, int64_t ldS, cons
   return cudaGetLastError();
 }
 
+// ---- F16X2 split (tiles.cuh) ----
+// Row scales from a sample of each row (its first kScaleSample columns): s_i = 2^k with the
+// sample maximum scaled into [2^6, 2^7), leaving 2^9 of headroom below the fp16 maximum for the
+// rest of the row; an element that still overflows sets bit 1 of the flag word and the caller
+// recomputes the Gram with TF32X3.  Power-of-two scales are exact in both directions.
+constexpr int kScaleSample = 4096;
+__global__ void row_scale_kernel(const float* __restrict__ S, int64_t n, int64_t cols, int64_t ldS,
+                                 float* __restrict__ scale, double* __restrict__ inv_scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x / kWarp) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  float mx = 0.f;
+  for (int64_t c = lane; c < cols; c += kWarp) mx = fmaxf(mx, fabsf(S[i * ldS + c]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int k = 0;
+  if (mx > 0.f && isfinite(mx)) {
+    int e;
+    frexpf(mx, &e);                     // mx in [2^(e-1), 2^e)
+    k = 7 - e;                          // mx * 2^k in [2^6, 2^7)
+    k = k > 100 ? 100 : (k < -100 ? -100 : k);
+  }
+  if (lane == 0) {
+    scale[i] = ldexpf(1.f, k);
+    inv_scale[i] = ldexp(1.0, -k);
+  }
+}
+
+// Column range [c0, c1) of all rows (c0 a multiple of 1024): the F16X2 planes of S_t16 and the
+// u = S w partials of the column chunks (fp32 products, like gemv_rows_retile).  Each lane
+// moves 8 consecutive floats = one 16-byte fp16 chunk per plane; 8 lanes write one full
+// 128-byte tile row of each plane.
+constexpr int kR16Unroll = 4;   // 4 x 256 columns = one 1024-column chunk
+__global__ void __launch_bounds__(kRowThreads, 2)
+retile16_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS, const float* __restrict__ w,
+                double* __restrict__ partials, uint8_t* __restrict__ St, const float* __restrict__ scale,
+                int has_w, int vec_ok, int* __restrict__ flags, int64_t cb0) {
+  constexpr int CW = 1024;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cb = cb0 + blockIdx.x;
+  const int64_t c0 = cb * CW;
+  const int64_t nb = tiles_nb(n), KB = tiles16_kb(m);
+  __shared__ float4 wsm[CW / 4];
+  for (int t = threadIdx.x; t < CW / 4; t += kRowThreads) {
+    float a[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = c0 + (int64_t)t * 4 + e;
+      a[e] = (has_w && c < m) ? w[c] : 0.f;
+    }
+    wsm[t] = make_float4(a[0], a[1], a[2], a[3]);
+  }
+  __syncthreads();
+  const bool full = vec_ok && c0 + CW <= m;
+  const int chunk = lane & 7;
+  const int64_t rz = nb * kTileRows;
+  bool bad = false, ovf = false;
+  for (int64_t i = warp; i < rz; i += kRowThreads / kWarp) {
+    float4 buf[kR16Unroll][2];
+    if (i < n) {
+      const float* row = S + i * ldS + c0;
+      if (full) {
+#pragma unroll
+        for (int u = 0; u < kR16Unroll; ++u) {
+          buf[u][0] = ld_stream(reinterpret_cast<const float4*>(row + u * 256 + lane * 8));
+          buf[u][1] = ld_stream(reinterpret_cast<const float4*>(row + u * 256 + lane * 8 + 4));
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kR16Unroll; ++u) {
+          float a[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int64_t c = (int64_t)u * 256 + lane * 8 + e;
+            a[e] = (c0 + c < m) ? __ldg(row + c) : 0.f;
+          }
+          buf[u][0] = make_float4(a[0], a[1], a[2], a[3]);
+          buf[u][1] = make_float4(a[4], a[5], a[6], a[7]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kR16Unroll; ++u) buf[u][0] = buf[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float sc = i < n ? scale[i] : 1.f;
+#pragma unroll
+    for (int u = 0; u < kR16Unroll; ++u) {
+      const int64_t kb = (c0 >> 6) + u * 4 + (lane >> 3);
+      const float xs[8] = {buf[u][0].x, buf[u][0].y, buf[u][0].z, buf[u][0].w,
+                           buf[u][1].x, buf[u][1].y, buf[u][1].z, buf[u][1].w};
+      __align__(16) __half hi[8], lo[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bad |= !isfinite(xs[e]);
+        const float y = xs[e] * sc;
+        hi[e] = __float2half_rn(y);
+        const float hf = __half2float(hi[e]);
+        ovf |= isinf(hf);
+        lo[e] = __float2half_rn(y - hf);
+      }
+      if (kb < KB) {
+        *reinterpret_cast<uint4*>(St + tile16_chunk_offset(nb, kb, i, chunk, 0)) = *reinterpret_cast<const uint4*>(hi);
+        *reinterpret_cast<uint4*>(St + tile16_chunk_offset(nb, kb, i, chunk, 1)) = *reinterpret_cast<const uint4*>(lo);
+      }
+    }
+    if (i < n && has_w) {
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < kR16Unroll; ++u) {
+        const float4 w0 = wsm[u * 64 + lane * 2], w1 = wsm[u * 64 + lane * 2 + 1];
+        acc = fmaf(buf[u][0].x, w0.x, acc); acc = fmaf(buf[u][0].y, w0.y, acc);
+        acc = fmaf(buf[u][0].z, w0.z, acc); acc = fmaf(buf[u][0].w, w0.w, acc);
+        acc = fmaf(buf[u][1].x, w1.x, acc); acc = fmaf(buf[u][1].y, w1.y, acc);
+        acc = fmaf(buf[u][1].z, w1.z, acc); acc = fmaf(buf[u][1].w, w1.w, acc);
+      }
+      const double s = warp_sum((double)acc);
+      if (lane == 0) partials[cb * n + i] = s;
+    }
+  }
+  if (flags) {
+    const unsigned bb = __ballot_sync(0xffffffffu, bad), bo = __ballot_sync(0xffffffffu, ovf);
+    if (lane == 0 && (bb | bo)) atomicOr(flags, (bb ? 1 : 0) | (bo ? 2 : 0));
+  }
+}
+
+__global__ void flag_bit_kernel(const int* __restrict__ flags, int bit, double* __restrict__ out) {
+  *out = (*flags & bit) ? 1.0 : 0.0;
+}
+
 }  // namespace
+
+cudaError_t flag_bit_to_double(const int* flags, int bit, double* out, cudaStream_t st, int* launches) {
+  flag_bit_kernel<<<1, 1, 0, st>>>(flags, bit, out);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
                          cudaStream_t st, int* launches) {
@@ -651,6 +788,29 @@ cudaError_t retile_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const
   const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
   gemv_rows_retile_kernel<<<(unsigned)(cb1 - cb0), kRowThreads, 0, st>>>(
       S, n, m, ldS, w, partials, St, w != nullptr, vec_ok, 0, n, tiles_nb(n) * kTileRows, nonfinite, cb0);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t row_scales(const float* S, int64_t n, int64_t m, int64_t ldS, float* scale, double* inv_scale,
+                       cudaStream_t st, int* launches, int64_t sample_cols) {
+  int64_t cols = m < kScaleSample ? m : kScaleSample;
+  if (sample_cols > 0 && sample_cols < cols) cols = sample_cols;
+  row_scale_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(S, n, cols, ldS, scale, inv_scale);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t retile16_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                          uint8_t* St, const float* scale, int64_t c0, int64_t c1, int* flags, cudaStream_t st,
+                          int* launches) {
+  constexpr int CW = 1024;
+  if (c0 % CW) return cudaErrorInvalidValue;
+  const int64_t cb0 = c0 / CW, cb1 = (c1 + CW - 1) / CW;
+  if (cb1 <= cb0) return cudaSuccess;
+  const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
+  retile16_kernel<<<(unsigned)(cb1 - cb0), kRowThreads, 0, st>>>(S, n, m, ldS, w, partials, St, scale, w != nullptr,
+                                                                  vec_ok, flags, cb0);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -19,6 +19,15 @@ cudaError_t gemv_rows_retile(const float* S, int64_t n, int64_t m, int64_t ldS, 
 // u-partials of its column chunks; no reduction (reduce_row_partials finishes u)
 cudaError_t retile_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
                         uint8_t* St, int64_t c0, int64_t c1, int* nonfinite, cudaStream_t st, int* launches);
+// F16X2 (tiles.cuh): per-row power-of-two scales from a column sample, then the split planes
+// of columns [c0, c1) of all rows (+ u partials of w, flags |= 1 non-finite, |= 2 fp16 overflow)
+cudaError_t row_scales(const float* S, int64_t n, int64_t m, int64_t ldS, float* scale, double* inv_scale,
+                       cudaStream_t st, int* launches, int64_t sample_cols = 0);
+// *out = (*flags & bit) ? 1 : 0 (an overflow flag joins a norms all-reduce)
+cudaError_t flag_bit_to_double(const int* flags, int bit, double* out, cudaStream_t st, int* launches);
+cudaError_t retile16_cols(const float* S, int64_t n, int64_t m, int64_t ldS, const float* w, double* partials,
+                          uint8_t* St, const float* scale, int64_t c0, int64_t c1, int* flags, cudaStream_t st,
+                          int* launches);
 cudaError_t reduce_row_partials(const double* partials, int64_t n, int64_t m, double* u, cudaStream_t st,
                                 int* launches);
 int64_t gemv_rows_chunk_cols();
@@ -62,6 +71,11 @@ size_t syrk_tc_plan_bytes(int64_t n, int64_t m, int num_sms);
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
                     cudaStream_t st, int* launches, int prow0 = 0, int prow1 = -1, int kb_begin = 0, int kb_end = -1,
                     int accum = 0);
+// F16X2 Gram on the split planes (tiles.cuh): kind::f16 MMAs hi*hi + hi*lo + lo*hi per
+// 64-column K-block; inv_scale[i] = 2^-k_i undoes the row scales in the fp64 result
+cudaError_t syrk_f16(const uint8_t* St16, int64_t n, int64_t m, const double* inv_scale, double lam, double* G_packed,
+                     double* ws, int num_sms, cudaStream_t st, int* launches, int kb_begin = 0, int kb_end = -1,
+                     int accum = 0);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,

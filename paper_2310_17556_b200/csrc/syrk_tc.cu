@@ -59,7 +59,15 @@ constexpr int kFlushChunks = 64;
 constexpr int kPfDist = 8;                // K-blocks between an L2 prefetch and its bulk load
 constexpr int kRegsProducer = 56, kRegsConverter = 80, kRegsEpilogue = 184;
 constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
-constexpr size_t kSmemBytes = (size_t)(kRaw + kLo) * kStageBytes + 1024 + 512;
+// F16X2 (tiles.cuh): a stage holds the hi+lo tiles of the A and B row blocks (4 x 16 KB), no
+// converter ring; kind::f16 MMAs (K = 16) on 64-column K-blocks
+template <bool kF16> constexpr int raw_stages() { return kF16 ? 3 : kRaw; }
+template <bool kF16> constexpr int lo_stages() { return kF16 ? 0 : kLo; }
+template <bool kF16> constexpr int stage_bytes() { return kF16 ? 4 * kBoxBytes : kStageBytes; }
+template <bool kF16> constexpr size_t smem_bytes() {
+  return (size_t)(raw_stages<kF16>() * stage_bytes<kF16>() + lo_stages<kF16>() * kStageBytes) + 1024 + 512;
+}
+constexpr uint32_t kIdescF16 = ptx::idesc_f16(2 * kBlk, kN);
 
 struct Plan {
   int nb, np, tile0, tiles, P, clusters, KB, KC, D, kb_base;
@@ -88,20 +96,25 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
   FS_DEVINL void next(int depth) { if (++s == depth) { s = 0; ph ^= 1; } }
 };
 
+template <bool kF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
                double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg, int kb_base,
-               int accum) {
+               int accum, const double* __restrict__ inv_scale) {
+  constexpr int kRawS = raw_stages<kF16>();
+  constexpr int kLoS = lo_stages<kF16>();
+  constexpr int kSB = stage_bytes<kF16>();
+  constexpr int kBlkBytes = kF16 ? 2 * kBoxBytes : kBoxBytes;   // one row block's K-block (hi+lo for F16X2)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw = smem;
-  uint8_t* lo = smem + (size_t)kRaw * kStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)(kRaw + kLo) * kStageBytes);
-  uint64_t* full = bars;                 // local TMA -> local converters           [kRaw]
-  uint64_t* conv = full + kRaw;          // both CTAs' converters -> leader MMA     [kRaw]
-  uint64_t* empty = conv + kRaw;         // MMA (multicast) -> each producer        [kRaw]
-  uint64_t* lo_free = empty + kRaw;      // MMA (multicast) -> each converter group [kLo]
-  uint64_t* tfull = lo_free + kLo;       // MMA (multicast) -> each epilogue        [2]
+  uint8_t* lo = smem + (size_t)kRawS * kSB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kRawS * kSB + (size_t)kLoS * kStageBytes);
+  uint64_t* full = bars;                 // local TMA -> local converters / relay   [kRawS]
+  uint64_t* conv = full + kRawS;         // both CTAs' converters -> leader MMA     [kRawS]
+  uint64_t* empty = conv + kRawS;        // MMA (multicast) -> each producer        [kRawS]
+  uint64_t* lo_free = empty + kRawS;     // MMA (multicast) -> each converter group [kLoS]
+  uint64_t* tfull = lo_free + kLoS;      // MMA (multicast) -> each epilogue        [2]
   uint64_t* tempty = tfull + 2;          // both CTAs' epilogues -> leader MMA      [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -109,12 +122,12 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
   const uint32_t crank = ptx::cluster_ctarank();   // 0 = leader
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRaw; ++s) {
+    for (int s = 0; s < kRawS; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&conv[s], 2);                 // one elected arrive per CTA
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < kLo; ++s) ptx::mbar_init(&lo_free[s], 1);
+    for (int s = 0; s < kLoS; ++s) ptx::mbar_init(&lo_free[s], 1);
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 2);                // one elected arrive per CTA
@@ -139,22 +152,22 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         int pp, qq; pair_of(tile0 + t, pp, qq);
         const int blkA = 2 * pp + (int)crank, blkB = 2 * qq + (int)crank;
         const bool diag = pp == qq;                       // A == B: one tile
-        const uint32_t bytes = (diag ? 1 : 2) * kBoxBytes;
+        const uint32_t bytes = (diag ? 1 : 2) * kBlkBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         for (int k = 0; k < nk; ++k) {
           const size_t krow = (size_t)(kb_base + kb0 + k) * nbt;
           if (!(dbg & 32) && k + kPfDist < nk) {
             const size_t pk = (size_t)(kb_base + kb0 + k + kPfDist) * nbt;
-            ptx::bulk_prefetch_l2(St + (pk + blkA) * kTileBytes, kTileBytes);
-            if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kTileBytes, kTileBytes);
+            ptx::bulk_prefetch_l2(St + (pk + blkA) * kBlkBytes, kBlkBytes);
+            if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kBlkBytes, kBlkBytes);
           }
           ptx::mbar_wait(&empty[rr.s], rr.ph ^ 1);
-          if (dbg & 1) { ptx::mbar_arrive(&full[rr.s]); rr.next(kRaw); continue; }
+          if (dbg & 1) { ptx::mbar_arrive(&full[rr.s]); rr.next(kRawS); continue; }
           ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
-          uint8_t* st = raw + (size_t)rr.s * kStageBytes;
-          ptx::bulk_load(st, St + (krow + blkA) * kTileBytes, kTileBytes, &full[rr.s]);
-          if (!diag) ptx::bulk_load(st + kBoxBytes, St + (krow + blkB) * kTileBytes, kTileBytes, &full[rr.s]);
-          rr.next(kRaw);
+          uint8_t* st = raw + (size_t)rr.s * kSB;
+          ptx::bulk_load(st, St + (krow + blkA) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          if (!diag) ptx::bulk_load(st + kBlkBytes, St + (krow + blkB) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          rr.next(kRawS);
         }
       }
     } else if (warp == 1 && lane == 0 && crank == 0) {
@@ -164,7 +177,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
         int pp, qq; pair_of(tile0 + t, pp, qq);
-        const int b_off = (pp == qq) ? 0 : kBoxBytes;
+        const int b_off = (pp == qq) ? 0 : kBlkBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         uint32_t dacc = 0;
         for (int k = 0; k < nk; ++k) {
@@ -177,34 +190,65 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           }
           ptx::mbar_wait(&conv[rr.s], rr.ph);
           ptx::tc_fence_after();
-          const uint32_t rs = ptx::smem_u32(raw + (size_t)rr.s * kStageBytes);
-          const uint32_t ls = ptx::smem_u32(lo + (size_t)lr.s * kStageBytes);
+          const uint32_t rs = ptx::smem_u32(raw + (size_t)rr.s * kSB);
+          // hi operands: the raw stage (TF32X3: the fp32 tile, truncated by the tensor core) or
+          // the hi plane (F16X2); lo operands: the converter ring or the lo plane
+          const uint32_t ha = rs, hb = rs + b_off;
+          const uint32_t la = kF16 ? rs + kBoxBytes : ptx::smem_u32(lo + (size_t)lr.s * kStageBytes);
+          const uint32_t lb = kF16 ? rs + b_off + kBoxBytes : la + b_off;
           // small correction products first (while this chunk's accumulator is still small, the
           // tensor core's truncating accumulation loses least), then the four hi*hi products
           if (!(dbg & 4)) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
-              const uint32_t off = kk * 32;
-              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(ls + off), ptx::desc_kmajor<kRowBytes>(rs + b_off + off),
-                             kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
-              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(rs + off), ptx::desc_kmajor<kRowBytes>(ls + b_off + off),
-                             kIdesc, 1u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t off = kk * 32;   // 8 tf32 / 16 fp16 = 32 bytes of K per MMA
+              if constexpr (kF16) {
+                ptx::mma2_f16(dacc, ptx::desc_kmajor<kRowBytes>(la + off), ptx::desc_kmajor<kRowBytes>(hb + off),
+                              kIdescF16, (kin > 0 || kk > 0) ? 1u : 0u);
+                ptx::mma2_f16(dacc, ptx::desc_kmajor<kRowBytes>(ha + off), ptx::desc_kmajor<kRowBytes>(lb + off),
+                              kIdescF16, 1u);
+              } else {
+                ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(la + off), ptx::desc_kmajor<kRowBytes>(hb + off),
+                               kIdesc, (kin > 0 || kk > 0) ? 1u : 0u);
+                ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(ha + off), ptx::desc_kmajor<kRowBytes>(lb + off),
+                               kIdesc, 1u);
+              }
             }
 #pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
+            for (int kk = 0; kk < 4; ++kk) {
               const uint32_t off = kk * 32;
-              ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(rs + off), ptx::desc_kmajor<kRowBytes>(rs + b_off + off),
-                             kIdesc, 1u);
+              if constexpr (kF16)
+                ptx::mma2_f16(dacc, ptx::desc_kmajor<kRowBytes>(ha + off), ptx::desc_kmajor<kRowBytes>(hb + off),
+                              kIdescF16, 1u);
+              else
+                ptx::mma2_tf32(dacc, ptx::desc_kmajor<kRowBytes>(ha + off), ptx::desc_kmajor<kRowBytes>(hb + off),
+                               kIdesc, 1u);
             }
           }
           ptx::mma2_commit_mc(&empty[rr.s], 0x3);
-          ptx::mma2_commit_mc(&lo_free[lr.s], 0x3);
+          if constexpr (!kF16) ptx::mma2_commit_mc(&lo_free[lr.s], 0x3);
           if (kin == D - 1 || k == nk - 1) {
             ptx::mma2_commit_mc(&tfull[chunk & 1], 0x3);
             ++chunk;
           }
-          rr.next(kRaw);
-          lr.next(kLo);
+          rr.next(kRawS);
+          if constexpr (!kF16) lr.next(kLo);
+        }
+      }
+    }
+  } else if (wg == 1 && kF16) {
+    // ================ relay (F16X2): own TMA completion -> leader's conv barrier ================
+    ptx::setmaxnreg_dec<kRegsConverter>();
+    if (threadIdx.x == 128) {
+      const uint32_t conv0 = ptx::mapa(ptx::smem_u32(conv), 0);
+      Ring rr;
+      for (int u = cluster; u < units; u += nclusters) {
+        const int q = u % P;
+        const int kb0 = q * KC, nk = min(KC, KB - kb0);
+        for (int k = 0; k < nk; ++k) {
+          ptx::mbar_wait(&full[rr.s], rr.ph);
+          ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
+          rr.next(kRawS);
         }
       }
     }
@@ -225,7 +269,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         if (!(dbg & 2)) {
           // the tensor core truncates fp32 operands to tf32 (measured: tools/probe_tf32.py), so the
           // raw tile already IS hi = trunc(x); only lo = x - trunc(x) (exact in fp32) is written
-          const uint4* r4 = reinterpret_cast<const uint4*>(raw + (size_t)rr.s * kStageBytes);
+          const uint4* r4 = reinterpret_cast<const uint4*>(raw + (size_t)rr.s * kSB);
           float4* l4 = reinterpret_cast<float4*>(lo + (size_t)lr.s * kStageBytes);
 #pragma unroll 8
           for (int i = ct; i < nvec; i += 128) {
@@ -238,7 +282,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         }
         ptx::named_bar_sync(1, 128);                 // all converter writes of this stage done
         if (ct == 0) ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
-        rr.next(kRaw);
+        rr.next(kRawS);
         lr.next(kLo);
       }
     }
@@ -301,7 +345,9 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
             const int64_t gj = (int64_t)(2 * qq) * kBlk + c;
             if (gj > gi) break;
             double* g = Gp + gi * (gi + 1) / 2 + gj;
-            *g = (accum ? *g : 0.0) + sc[(size_t)e * kBlk] + (gi == gj ? lam : 0.0);
+            double val = sc[(size_t)e * kBlk];
+            if (kF16) val *= inv_scale[gi] * inv_scale[gj];       // exact: powers of two
+            *g = (accum ? *g : 0.0) + val + (gi == gj ? lam : 0.0);
           }
         }
       }
@@ -316,7 +362,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
 // Block (t, c): pair tile t, CTA half c (row block 2p+c).
 constexpr int kRedSplit = 16;   // blocks per (pair tile, CTA half): 2048 elements each
 __global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, int64_t n, double lam,
-                               double* __restrict__ Gp, int accum) {
+                               double* __restrict__ Gp, int accum, const double* __restrict__ inv_scale) {
   const int tc = blockIdx.x / kRedSplit, part = blockIdx.x % kRedSplit;
   int pp, qq;
   pair_of(tile0 + (tc >> 1), pp, qq);
@@ -328,19 +374,21 @@ __global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, 
     if (gi >= n || gj > gi) continue;
     double s = 0.0;
     for (int q = 0; q < P; ++q) s += ws[(((size_t)(tc >> 1) * P + q) * 2 + c) * kBlk * kN + e];
+    if (inv_scale) s *= inv_scale[gi] * inv_scale[gj];
     double* g = Gp + gi * (gi + 1) / 2 + gj;
     *g = (accum ? *g : 0.0) + s + (gi == gj ? lam : 0.0);
   }
 }
 
-Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1, int kb_begin = 0, int kb_end = -1) {
+Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1, int kb_begin = 0, int kb_end = -1,
+               int bk = kBK) {
   Plan p;
   p.nb = (int)((n + kBlk - 1) / kBlk);
   p.np = (p.nb + 1) / 2;
   if (prow1 < 0 || prow1 > p.np) prow1 = p.np;
   p.tile0 = prow0 * (prow0 + 1) / 2;
   p.tiles = prow1 * (prow1 + 1) / 2 - p.tile0;
-  p.KB = (int)((m + kBK - 1) / kBK);
+  p.KB = (int)((m + bk - 1) / bk);
   if (kb_end < 0 || kb_end > p.KB) kb_end = p.KB;
   p.kb_base = kb_begin;
   p.KB = kb_end - kb_begin;
@@ -372,26 +420,43 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
   return (size_t)num_sms * kBlk * kN * sizeof(double);
 }
 
-cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
-                    cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum) {
-  Plan p = make_plan(n, m, num_sms, prow0, prow1, kb_begin, kb_end);
+namespace {
+template <bool kF16>
+cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
+                        cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum,
+                        const double* inv_scale) {
+  Plan p = make_plan(n, m, num_sms, prow0, prow1, kb_begin, kb_end, kF16 ? kTile16Cols : kBK);
   if (p.tiles <= 0 || p.KB <= 0) return cudaSuccess;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel<kF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<kF16>());
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
-  syrk_tc_kernel<<<2 * p.clusters, kThreads, kSmemBytes, st>>>(St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC,
-                                                               p.D,
-                                                               ws, G_packed, lam, p.direct ? 1 : 0, dbg, p.kb_base, accum);
+  syrk_tc_kernel<kF16><<<2 * p.clusters, kThreads, smem_bytes<kF16>(), st>>>(
+      St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
+      p.kb_base, accum, inv_scale);
   if (launches) *launches += 1;
   if (!p.direct) {
-    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum);
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum, inv_scale);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
+                    cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum) {
+  return syrk_launch<false>(St, n, m, lam, G_packed, ws, num_sms, st, launches, prow0, prow1, kb_begin, kb_end, accum,
+                            nullptr);
+}
+
+cudaError_t syrk_f16(const uint8_t* St16, int64_t n, int64_t m, const double* inv_scale, double lam, double* G_packed,
+                     double* ws, int num_sms, cudaStream_t st, int* launches, int kb_begin, int kb_end, int accum) {
+  return syrk_launch<true>(St16, n, m, lam, G_packed, ws, num_sms, st, launches, 0, -1, kb_begin, kb_end, accum,
+                           inv_scale);
 }
 
 }  // namespace fs

@@ -144,6 +144,11 @@ def test_golden_fp32_tf32x3(fsb, name, golden, manifest):
     # the exact-product fp64 mode on the identical fp32 system matches to fp64 accuracy
     sol64 = fsb.solve_chol(system, precision="fp64")
     assert O.rel_err(sol64.x, ref) <= 1e-10
+    # the default fp32 mode (F16X2 split) meets the same tolerance
+    sol16 = fsb.solve_chol(system)
+    assert sol16.precision == "f16x2"
+    assert O.rel_err(sol16.x, ref) <= 1e-6, O.rel_err(sol16.x, ref)
+    assert sol16.rel_residual <= 4 * U32 * sigma2_max(S) / lam
 
 
 # ---------------------------------------------------------------- stage kernels vs the oracle
@@ -152,7 +157,7 @@ SHAPES = [(1, 7), (3, 5), (100, 1000), (129, 3001), (257, 4097), (300, 10000), (
 
 
 @pytest.mark.parametrize("n,m", SHAPES)
-@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3", "f16x2"])
 def test_gram_stage(fsb, n, m, precision):
     rng = np.random.Generator(np.random.PCG64(n * 7 + m))
     S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(np.float32)
@@ -163,11 +168,12 @@ def test_gram_stage(fsb, n, m, precision):
     assert np.array_equal(W, W.T)
 
 
-def test_tf32x3_gram_error_is_fp32_level(fsb):
-    """3xTF32 must be far more accurate than plain TF32 (2^-11): check ~fp32 accuracy per entry."""
+@pytest.mark.parametrize("precision", ["tf32x3", "f16x2"])
+def test_split_gram_error_is_fp32_level(fsb, precision):
+    """3xTF32 / F16X2 must be far more accurate than one tf32/fp16 product (2^-11): ~fp32 per entry."""
     rng = np.random.Generator(np.random.PCG64(5))
     S = rng.standard_normal((256, 65536)).astype(np.float32) / 16
-    W = fsb.gram(fsb.ScoreMatrix(S), 1e-3, precision="tf32x3")
+    W = fsb.gram(fsb.ScoreMatrix(S), 1e-3, precision=precision)
     ref = O.gram(S.astype(np.float64), 1e-3)
     scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
     rel = np.abs(W - ref) / scale
@@ -255,7 +261,7 @@ def test_large_damping_limit(fsb):
     assert O.rel_err(sol.x, v / lam) <= 1e-6
 
 
-@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3", "f16x2"])
 def test_run_to_run_bit_identical(fsb, precision):
     """test_acceptance.py:191-197 (criterion 10) — determinism of x."""
     S, v, lam = O.generate_problem(0, 200, 20000, 1e-3)
@@ -438,7 +444,7 @@ def test_host_entry_matches_device_entry(fsb, n, m):
     the fp64 drain order differs."""
     S, v, lam = O.generate_problem(11, n, m, 1e-3)
     dev = torch.device("cuda", 0)
-    for dt, prec in ((np.float64, "fp64"), (np.float32, "tf32x3"), (np.float32, "fp64")):
+    for dt, prec in ((np.float64, "fp64"), (np.float32, "tf32x3"), (np.float32, "f16x2"), (np.float32, "fp64")):
         Sh, vh = S.astype(dt), v.astype(dt)
         host = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=prec)
         assert isinstance(host.x, np.ndarray)
@@ -509,3 +515,45 @@ def test_host_entry_abi_pitched_rows(fsb, pinned):
                                   ctypes.byref(piv), res, 0) == _lib.FS_EINVAL
     ctx.close()
 
+
+
+# ---------------------------------------------------------------- F16X2 row-scale overflow fallback
+
+@pytest.mark.parametrize("entry", ["gram", "device", "host"])
+def test_f16x2_overflow_falls_back_to_tf32x3(fsb, entry):
+    """A row whose sampled head is tiny but whose tail is huge defeats the sampled fp16 scale:
+    the overflow is detected and the Gram recomputed with TF32X3 — same results as asking for it."""
+    S, v, lam = O.generate_problem(21, 40, 12000, 1e-2)
+    S = S.astype(np.float32)
+    S[7, :5000] *= 1e-6          # sample region (first 4096 columns) tiny
+    S[7, 9000] = 50.0            # 2^9+ beyond the scaled sample maximum
+    v = v.astype(np.float32)
+    if entry == "gram":
+        W16 = fsb.gram(fsb.ScoreMatrix(S), 0.5, precision="f16x2")
+        W32 = fsb.gram(fsb.ScoreMatrix(S), 0.5, precision="tf32x3")
+        assert np.array_equal(W16, W32)
+        return
+    if entry == "device":
+        dev = torch.device("cuda", 0)
+        mk = lambda: fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam, torch.from_numpy(v).to(dev))
+        a = fsb.solve_chol(mk(), precision="f16x2")
+        b = fsb.solve_chol(mk(), precision="tf32x3")
+        assert torch.equal(a.x, b.x)
+        x = a.x.cpu().numpy()
+    else:
+        a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="f16x2")
+        x = a.x
+    ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
+    assert O.rel_err(x, ref.x) <= 1e-6
+
+
+def test_f16x2_scales_cover_wide_row_ranges(fsb):
+    """Rows of very different magnitudes (1e-8 .. 1e8): per-row power-of-two scales keep every
+    row in fp16 range without overflow, and the Gram stays at fp32-level accuracy."""
+    rng = np.random.Generator(np.random.PCG64(8))
+    S = rng.standard_normal((300, 20000)).astype(np.float32)
+    S *= (10.0 ** rng.uniform(-8, 8, size=(300, 1))).astype(np.float32)
+    W = fsb.gram(fsb.ScoreMatrix(S), 0.0 + 1e-30, precision="f16x2")
+    ref = O.gram(S.astype(np.float64), 1e-30)
+    scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
+    assert (np.abs(W - ref) / scale).max() <= 1e-6
