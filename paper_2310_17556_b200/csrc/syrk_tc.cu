@@ -156,7 +156,9 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
         for (int k = 0; k < nk; ++k) {
           const size_t krow = (size_t)(kb_base + kb0 + k) * nbt;
-          if (!(dbg & 32) && k + kPfDist < nk) {
+          // L2 bulk prefetch kPfDist K-blocks ahead: off by default (measured neutral for TF32X3 and
+          // ~5% slower for F16X2, tools/syrk_ablate.sh); FS_SYRK_DBG bit 64 re-enables it
+          if ((dbg & 64) && k + kPfDist < nk) {
             const size_t pk = (size_t)(kb_base + kb0 + k + kPfDist) * nbt;
             ptx::bulk_prefetch_l2(St + (pk + blkA) * kBlkBytes, kBlkBytes);
             if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kBlkBytes, kBlkBytes);

@@ -9,12 +9,12 @@ m = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 prec = sys.argv[3] if len(sys.argv) > 3 else "tf32x3"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 dev = torch.device("cuda", 0)
-dt = torch.float32 if prec == "tf32x3" else torch.float64
+dt = torch.float64 if prec == "fp64" else torch.float32
 S = torch.randn(n, m, device=dev, dtype=dt) / n ** 0.5
 G = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=dev)
 ctx = _lib.context_for(0, n, m)
 st = torch.cuda.current_stream().cuda_stream
-P = {"tf32x3": _lib.FS_PREC_TF32X3, "fp64": _lib.FS_PREC_FP64}[prec]
+P = {"tf32x3": _lib.FS_PREC_TF32X3, "f16x2": _lib.FS_PREC_F16X2, "fp64": _lib.FS_PREC_FP64}[prec]
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for i in range(reps):
     e0.record()

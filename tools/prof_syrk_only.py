@@ -13,6 +13,9 @@ del S
 ctx = _lib.context_for(0, n, m); ctx.profile(True)
 g = []
 for i in range(4):
-    fsb.solve_chol(system, precision="tf32x3", diagnostics=False, refine=False)
+    try:   # ablated kernels produce garbage Grams: a failed factorization still records the stage times
+        fsb.solve_chol(system, precision=os.environ.get("FS_PREC", "f16x2"), diagnostics=False, refine=False)
+    except fsb.FactorizationError:
+        pass
     g.append(ctx.stage_ms())
 print("gram %.3f ms  gemv_sv+retile %.3f ms" % (min(x["gram"] for x in g[1:]), min(x["gemv_sv"] for x in g[1:])))
