@@ -72,15 +72,16 @@ def peaks():
             "source": "B200_PROFILING.md fallback"}
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the SYRK kernel from the committed ncu --set full summary."""
+def ncu_traffic(precision):
+    """Per-launch DRAM bytes of the SYRK kernel (this precision mode) from the committed ncu
+    --set full summary (profiles/ncu_summary.json, written by tools/ncu_summarize.py)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
         return None
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("syrk_tc_kernel", {}).get("dram_bytes_per_launch")
+        return d.get(f"syrk_tc_kernel:{precision}", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -307,7 +308,7 @@ def run_b200(args, rank, world, local):
         achieved = syrk_flops / (st["gram"] * 1e-3) / 1e12
         roofline = {"bound": "tensor", "kernel": "syrk_tc_kernel (+split-K reduce)", "achieved": achieved,
                     "peak": peak_mode, "unit": "TFLOP/s", "frac": achieved / peak_mode,
-                    "traffic": ncu_traffic(), "flops_per_launch": syrk_flops,
+                    "traffic": ncu_traffic(args.precision), "flops_per_launch": syrk_flops,
                     "peak_source": f"{pk['source']}: {peak_note}"}
     es = dtype.itemsize
     gemv = {}

@@ -12,6 +12,6 @@ S = torch.randn(n, m, device=dev, dtype=torch.float32) / n ** 0.5
 v = torch.randn(m, device=dev, dtype=torch.float32)
 system = fsb.DampedSystem(fsb.ScoreMatrix(S), 1e-3, v)
 for _ in range(reps):
-    sol = fsb.solve_chol(system, precision="tf32x3")
+    sol = fsb.solve_chol(system, precision=os.environ.get("FS_PREC", "auto"))
     torch.cuda.synchronize()
 print("rel_residual", sol.rel_residual)
