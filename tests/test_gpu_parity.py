@@ -557,3 +557,22 @@ def test_f16x2_scales_cover_wide_row_ranges(fsb):
     ref = O.gram(S.astype(np.float64), 1e-30)
     scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
     assert (np.abs(W - ref) / scale).max() <= 1e-6
+
+
+def test_host_solutions_stay_independent(fsb):
+    """Host solves write x into recycled page-locked buffers; a buffer is reused only after the
+    caller dropped the array, so held results never change."""
+    S, v, lam = O.generate_problem(31, 50, 3000, 1e-3)
+    S32, v32 = S.astype(np.float32), v.astype(np.float32)
+    held = []
+    for k in range(6):
+        sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32 * (k + 1)))
+        held.append((k + 1, sol.x, sol.x.copy()))
+    for k, x, snapshot in held:
+        assert np.array_equal(x, snapshot)
+        ref = O.solve_chol(S32.astype(np.float64), (v32 * k).astype(np.float64), lam)
+        assert O.rel_err(x, ref.x) <= 1e-6
+    del held
+    a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)).x
+    ref = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
+    assert O.rel_err(a, ref.x) <= 1e-6
