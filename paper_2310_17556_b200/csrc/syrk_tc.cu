@@ -32,7 +32,9 @@
 // MMA completion is tcgen05.commit.cta_group::2 ... multicast::cluster to both CTAs.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -90,6 +92,10 @@ FS_DEVINL float tf32_lo(uint32_t xb) {
   return __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
 }
 
+// FS_SYRK_DBG bit 256: the leader's MMA thread records cycles spent waiting for operands / for
+// a free TMEM buffer, and the total (one row per cluster), printed by the host after the launch
+__device__ unsigned long long g_syrk_wait[74 * 4];
+
 struct Ring {  // stage index + mbarrier phase of a circular buffer
   int s = 0;
   uint32_t ph = 0;
@@ -100,7 +106,7 @@ template <bool kF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
                double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg, int kb_base,
-               int accum, const double* __restrict__ inv_scale) {
+               int accum, const double* __restrict__ inv_scale, const __grid_constant__ CUtensorMap tmap) {
   constexpr int kRawS = raw_stages<kF16>();
   constexpr int kLoS = lo_stages<kF16>();
   constexpr int kSB = stage_bytes<kF16>();
@@ -123,7 +129,8 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRawS; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      // F16X2: both CTAs' producers arrive (with their byte counts) on the LEADER's full barrier
+      ptx::mbar_init(&full[s], kF16 ? 2 : 1);
       ptx::mbar_init(&conv[s], 2);                 // one elected arrive per CTA
       ptx::mbar_init(&empty[s], 1);
     }
@@ -146,6 +153,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     ptx::setmaxnreg_dec<kRegsProducer>();
     if (warp == 0 && lane == 0) {
       // ============ bulk-copy producer (each CTA: its own pre-swizzled S_t tiles) ============
+      const uint32_t full0 = ptx::mapa(ptx::smem_u32(full), 0);   // leader's full[0]
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
@@ -164,11 +172,21 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
             if (!diag) ptx::bulk_prefetch_l2(St + (pk + blkB) * kBlkBytes, kBlkBytes);
           }
           ptx::mbar_wait(&empty[rr.s], rr.ph ^ 1);
-          if (dbg & 1) { ptx::mbar_arrive(&full[rr.s]); rr.next(kRawS); continue; }
-          ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
           uint8_t* st = raw + (size_t)rr.s * kSB;
-          ptx::bulk_load(st, St + (krow + blkA) * kBlkBytes, kBlkBytes, &full[rr.s]);
-          if (!diag) ptx::bulk_load(st + kBlkBytes, St + (krow + blkB) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          if constexpr (kF16) {
+            // one 32 KB tensor copy per row block (hi + lo tiles = 256 rows of 128 B, already in
+            // the swizzled smem image), completing on the leader's barrier (cta_group::2)
+            const uint32_t lfull = full0 + rr.s * 8;
+            if (dbg & 1) { ptx::mbar_arrive_cluster(lfull); rr.next(kRawS); continue; }
+            ptx::mbar_arrive_expect_tx_cluster(lfull, bytes);
+            ptx::tma_load_2d_pair(st, &tmap, lfull, 0, (int32_t)((krow + blkA) * 2 * kTileRows));
+            if (!diag) ptx::tma_load_2d_pair(st + kBlkBytes, &tmap, lfull, 0, (int32_t)((krow + blkB) * 2 * kTileRows));
+          } else {
+            if (dbg & 1) { ptx::mbar_arrive(&full[rr.s]); rr.next(kRawS); continue; }
+            ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
+            ptx::bulk_load(st, St + (krow + blkA) * kBlkBytes, kBlkBytes, &full[rr.s]);
+            if (!diag) ptx::bulk_load(st + kBlkBytes, St + (krow + blkB) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          }
           rr.next(kRawS);
         }
       }
@@ -176,6 +194,10 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       // ======================= MMA issuer (leader CTA) =======================
       Ring rr, lr;
       uint32_t chunk = 0;
+      long long w_data = 0, w_tmem = 0;
+      const long long t_start = clock64();
+      uint64_t g_start;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
       for (int u = cluster; u < units; u += nclusters) {
         const int t = u / P, q = u % P;
         int pp, qq; pair_of(tile0 + t, pp, qq);
@@ -186,11 +208,15 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           const int kin = k % D;
           if (kin == 0) {
             const uint32_t b = chunk & 1;
+            const long long t0 = (dbg & 256) ? clock64() : 0;
             ptx::mbar_wait(&tempty[b], ((chunk >> 1) & 1) ^ 1);
+            if (dbg & 256) w_tmem += clock64() - t0;
             ptx::tc_fence_after();
             dacc = tmem + b * kN;
           }
-          ptx::mbar_wait(&conv[rr.s], rr.ph);
+          const long long t1 = (dbg & 256) ? clock64() : 0;
+          ptx::mbar_wait(kF16 ? &full[rr.s] : &conv[rr.s], rr.ph);
+          if (dbg & 256) w_data += clock64() - t1;
           ptx::tc_fence_after();
           const uint32_t rs = ptx::smem_u32(raw + (size_t)rr.s * kSB);
           // hi operands: the raw stage (TF32X3: the fp32 tile, truncated by the tensor core) or
@@ -202,7 +228,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           // tensor core's truncating accumulation loses least), then the four hi*hi products
           if (!(dbg & 4)) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < ((dbg & 128) ? 0 : 4); ++kk) {
               const uint32_t off = kk * 32;   // 8 tf32 / 16 fp16 = 32 bytes of K per MMA
               if constexpr (kF16) {
                 ptx::mma2_f16(dacc, ptx::desc_kmajor<kRowBytes>(la + off), ptx::desc_kmajor<kRowBytes>(hb + off),
@@ -237,23 +263,17 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           if constexpr (!kF16) lr.next(kLo);
         }
       }
-    }
-  } else if (wg == 1 && kF16) {
-    // ================ relay (F16X2): own TMA completion -> leader's conv barrier ================
-    ptx::setmaxnreg_dec<kRegsConverter>();
-    if (threadIdx.x == 128) {
-      const uint32_t conv0 = ptx::mapa(ptx::smem_u32(conv), 0);
-      Ring rr;
-      for (int u = cluster; u < units; u += nclusters) {
-        const int q = u % P;
-        const int kb0 = q * KC, nk = min(KC, KB - kb0);
-        for (int k = 0; k < nk; ++k) {
-          ptx::mbar_wait(&full[rr.s], rr.ph);
-          ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
-          rr.next(kRawS);
-        }
+      if ((dbg & 256) && cluster < 74) {
+        g_syrk_wait[cluster * 4 + 0] = w_data;
+        g_syrk_wait[cluster * 4 + 1] = w_tmem;
+        g_syrk_wait[cluster * 4 + 2] = clock64() - t_start;
+        uint64_t g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        g_syrk_wait[cluster * 4 + 3] = g_end - g_start;
       }
     }
+  } else if (wg == 1 && kF16) {
+    ptx::setmaxnreg_dec<kRegsConverter>();   // F16X2: no conversion, the TMA signals the leader
   } else if (wg == 1) {
     // ======================= converters (each CTA: its own smem) =======================
     ptx::setmaxnreg_dec<kRegsConverter>();
@@ -423,6 +443,32 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
 }
 
 namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// S_t16 viewed as a 2-D fp16 tensor of 128-byte rows: box = one (K-block, row block) hi+lo pair
+// (256 rows), no swizzle (the tiles are stored in the swizzled smem image already).
+cudaError_t st16_tensor_map(CUtensorMap* map, const uint8_t* St16, int64_t n, int64_t m) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    enc = (EncodeTiledFn)fn;
+  }
+  const cuuint64_t rows = (cuuint64_t)tiles_nb(n) * tiles16_kb(m) * 2 * kTileRows;
+  const cuuint64_t gdim[2] = {(cuuint64_t)kTile16Cols, rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)kTile16Cols * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kTile16Cols, (cuuint32_t)(2 * kTileRows)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint8_t*>(St16), gdim, gstride, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <bool kF16>
 cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
                         cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum,
@@ -437,10 +483,27 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  if (kF16) {
+    cudaError_t e = st16_tensor_map(&tmap, St, n, m);
+    if (e != cudaSuccess) return e;
+  }
   syrk_tc_kernel<kF16><<<2 * p.clusters, kThreads, smem_bytes<kF16>(), st>>>(
       St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
-      p.kb_base, accum, inv_scale);
+      p.kb_base, accum, inv_scale, tmap);
   if (launches) *launches += 1;
+  if (dbg & 256) {
+    unsigned long long h[74 * 4] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_syrk_wait, sizeof h);
+    double wd = 0, wt = 0, tot = 0, ns = 0;
+    int c = 0;
+    for (int i = 0; i < 74; ++i)
+      if (h[i * 4 + 3]) { wd += h[i * 4]; wt += h[i * 4 + 1]; tot += h[i * 4 + 2]; ns += h[i * 4 + 3]; ++c; }
+    if (c) fprintf(stderr, "syrk mma thread: wait operands %.0f%%, wait tmem %.0f%%, %.0f kcycles in %.3f ms -> %.0f MHz (%d clusters)\n",
+                   100 * wd / tot, 100 * wt / tot, tot / c / 1e3, ns / c / 1e6, tot / ns * 1e3, c);
+  }
   if (!p.direct) {
     syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum, inv_scale);
     if (launches) *launches += 1;

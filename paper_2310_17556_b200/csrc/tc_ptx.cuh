@@ -72,6 +72,21 @@ FS_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_
       : "memory");
 }
 
+// CTA-pair TMA: the bytes land in THIS CTA's smem, the completion is signalled on the mbarrier at
+// shared::cluster address `bar_cluster` (the leader CTA's, via mapa), so the leader's MMA waits on
+// one barrier for both halves of the operand.
+FS_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+// arrive + expect_tx on an mbarrier of another CTA of the cluster (shared::cluster address)
+FS_DEV void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster), "r"(bytes) : "memory");
+}
+
 // 1-D bulk copy global -> shared (contiguous `bytes`, multiple of 16), completes on `bar`.
 FS_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
