@@ -95,7 +95,7 @@ Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
   s.partials = (size_t)fs::gemv_rows_chunks(m, true) * n * sizeof(double);
   s.block_sums = (size_t)fs::residual_cols_blocks(m, true) * 2 * sizeof(double);
   s.r = (size_t)m * sizeof(double);
-  s.syrk = std::max(fs::syrk_simt_workspace_bytes(n, m, num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
+  s.syrk = std::max(fs::syrk_dmma_workspace_bytes(num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
   s.potrf = (size_t)fs::potrf_scratch_doubles(n) * sizeof(double);
   return s;
 }
@@ -190,7 +190,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
     if (e == cudaSuccess) e = fs::syrk_tc(ctx->d_St, n, m, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
   } else {
-    e = fs::syrk_simt(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+    e = fs::syrk_dmma(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
   }
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gram");
@@ -339,7 +339,7 @@ size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision) {
   // device bytes one solve of (n, m) touches besides S, v and x (feeds WorkspaceMeter)
   Sizes s = sizes_for(n, m, 148);
   const bool tc = dtype == FS_F32 && precision != FS_PREC_FP64;
-  const size_t gram = tc ? fs::syrk_tc_plan_bytes(n, m, 148) : fs::syrk_simt_plan_bytes(n, m, 148);
+  const size_t gram = tc ? fs::syrk_tc_plan_bytes(n, m, 148) : fs::syrk_dmma_plan_bytes(n, m, 148);
   return s.packed + s.W + 2 * s.vec + s.partials + s.block_sums + 4 * sizeof(double) + 2 * s.r + gram + s.potrf +
          sizeof(int64_t);
 }

@@ -56,11 +56,11 @@ cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64
                           double* r, double* block_sums, double* sums, cudaStream_t st,
                           int* launches);
 
-// ---- syrk_simt.cu (exact-product fp64 Gram, any dtype) ----
-size_t syrk_simt_workspace_bytes(int64_t n, int64_t m, int num_sms);  // bound for any smaller problem
-size_t syrk_simt_plan_bytes(int64_t n, int64_t m, int num_sms);       // exact for (n, m)
-cudaError_t syrk_simt(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam,
-                      double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches);
+// ---- syrk_dmma.cu (exact-product fp64 Gram on the fp64 tensor cores, any dtype) ----
+size_t syrk_dmma_workspace_bytes(int num_sms);                        // bound for any problem
+size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms);       // exact for (n, m)
+cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam, double* Gp,
+                      double* ws, int num_sms, cudaStream_t st, int* launches);
 
 // ---- syrk_tc.cu (tcgen05 3xTF32 Gram, fp32 input) ----
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);

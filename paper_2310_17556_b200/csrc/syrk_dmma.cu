@@ -1,0 +1,224 @@
+// syrk_dmma.cu — exact-product fp64 Gram G = S S^T + λI on the fp64 tensor cores (DMMA).
+//
+// Replaces core.py:284-289 (numpy A @ A.T -> OpenBLAS dsyrk, symmetrize, += lam) for
+// FS_PREC_FP64: every product s_ik * s_jk is an IEEE fp64 FMA (fp32 scores are widened
+// exactly), i.e. the reference's own arithmetic — executed as mma.sync.m8n8k4.f64, the
+// fp64 tensor-core instruction (tcgen05 has no fp64 kind on sm_100a).
+//
+// 128 x 128 lower tiles of G, 256 threads = 8 warps of 64 x 32 (8 x 4 MMA tiles of 8 x 8: 64
+// fp64 accumulator registers per thread).  K advances in 32-column stages, double-buffered
+// through shared memory: the next stage's global loads are issued into registers before the
+// current stage's MMAs and stored after them.  Shared rows are 36 doubles apart, so the eight
+// 32-byte fragment rows a warp reads hit distinct bank groups (two wavefronts, the minimum).
+// Split-K over P CTAs per tile (contiguous column ranges) with a fixed-order fp64 reduction of
+// the partial tiles: deterministic.  The roofline is the fp64 tensor rate; the loads are a few
+// bytes per clock per SM.
+#include "common.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace fs {
+namespace {
+
+constexpr int kT = 128;                 // tile edge
+constexpr int kK = 32;                  // K columns per stage
+constexpr int kLd = kK + 4;             // smem row pitch (doubles)
+constexpr int kThreads = 256;
+constexpr int kStageDoubles = 2 * kT * kLd;   // A and B
+constexpr size_t kSmemBytes = 2 * kStageDoubles * sizeof(double);   // 147 KB
+
+FS_DEVINL void tile_ij(int t, int& I, int& J) {   // lower tiles, row-major
+  int i = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  I = i;
+  J = t - i * (i + 1) / 2;
+}
+
+FS_DEVINL void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Stage loader: rows [r0, r0+128) x cols [k0, k0+32) of S -> 16 doubles per thread in registers.
+// Thread t covers row (t >> 1) and 16 consecutive columns ((t & 1) * 16 ...).
+template <typename T>
+struct Loader {
+  double v[16];
+  FS_DEVINL void load(const T* __restrict__ S, int64_t n, int64_t kend, int64_t ldS, int64_t r0, int64_t k0,
+                      bool vec) {
+    const int r = threadIdx.x >> 1, c = (threadIdx.x & 1) * 16;
+    const int64_t gr = r0 + r, gc = k0 + c;
+    if (gr < n && vec && gc + 16 <= kend) {
+      const T* p = S + gr * ldS + gc;
+      if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(p) + q);
+          v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double2 f = __ldg(reinterpret_cast<const double2*>(p) + q);
+          v[2 * q] = f.x; v[2 * q + 1] = f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = (gr < n && gc + e < kend) ? (double)__ldg(S + gr * ldS + gc + e) : 0.0;
+    }
+  }
+  FS_DEVINL void store(double* __restrict__ dst) const {
+    const int r = threadIdx.x >> 1, c = (threadIdx.x & 1) * 16;
+    double2* d = reinterpret_cast<double2*>(dst + r * kLd + c);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = make_double2(v[2 * q], v[2 * q + 1]);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P, double lam,
+                 double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec) {
+  extern __shared__ __align__(16) double dsm[];
+  int I, J;
+  tile_ij(blockIdx.x / P, I, J);
+  const int split = blockIdx.x % P;
+  const bool diag = I == J;
+  const int64_t kbeg = (int64_t)split * kchunk;
+  const int64_t kend = std::min<int64_t>(m, kbeg + kchunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 2) * 64, wc = (warp & 3) * 32;   // warp tile origin (rows of A, rows of B)
+  const int fr = lane >> 2, fk = lane & 3;                 // fragment row / k within an 8 x 4 slab
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  Loader<T> la, lb;
+  const int64_t rA = (int64_t)I * kT, rB = (int64_t)J * kT;
+  int buf = 0;
+  if (kbeg < kend) {
+    la.load(S, n, kend, ldS, rA, kbeg, vec);
+    if (!diag) lb.load(S, n, kend, ldS, rB, kbeg, vec);
+    la.store(dsm);
+    if (!diag) lb.store(dsm + kT * kLd);
+  }
+  __syncthreads();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += kK) {
+    const bool more = k0 + kK < kend;
+    if (more) {                                           // next stage -> registers
+      la.load(S, n, kend, ldS, rA, k0 + kK, vec);
+      if (!diag) lb.load(S, n, kend, ldS, rB, k0 + kK, vec);
+    }
+    const double* A = dsm + buf * kStageDoubles;
+    const double* B = diag ? A : A + kT * kLd;
+#pragma unroll
+    for (int ks = 0; ks < kK; ks += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = A[(wr + 8 * a + fr) * kLd + ks + fk];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = B[(wc + 8 * b + fr) * kLd + ks + fk];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+    }
+    if (more) {
+      double* nxt = dsm + (buf ^ 1) * kStageDoubles;
+      la.store(nxt);
+      if (!diag) lb.store(nxt + kT * kLd);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  // accumulator fragment (m8n8 f64): thread holds rows fr, columns 2*(lane&3) + {0,1}
+  const int cc = 2 * (lane & 3);
+  if (direct) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t gi = rA + wr + 8 * a + fr, gj = rB + wc + 8 * b + cc + e;
+          if (gi < n && gj <= gi) Gp[gi * (gi + 1) / 2 + gj] = acc[a][b][e] + (gi == gj ? lam : 0.0);
+        }
+  } else {
+    double* out = ws + (size_t)blockIdx.x * kT * kT;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        *reinterpret_cast<double2*>(out + (wr + 8 * a + fr) * kT + wc + 8 * b + cc) =
+            make_double2(acc[a][b][0], acc[a][b][1]);
+  }
+}
+
+// fixed-order sum of the P split partials of each tile -> packed lower Gram (+λ)
+__global__ void syrk_dmma_reduce(const double* __restrict__ ws, int P, int64_t n, double lam, double* __restrict__ Gp) {
+  int I, J;
+  tile_ij(blockIdx.x, I, J);
+  for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+    const int r = e / kT, c = e % kT;
+    const int64_t gi = (int64_t)I * kT + r, gj = (int64_t)J * kT + c;
+    if (gi >= n || gj > gi) continue;
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += ws[((size_t)blockIdx.x * P + q) * kT * kT + e];
+    Gp[gi * (gi + 1) / 2 + gj] = s + (gi == gj ? lam : 0.0);
+  }
+}
+
+struct DPlan {
+  int tiles, P;
+  int64_t kchunk;
+};
+
+DPlan dplan(int64_t n, int64_t m, int num_sms) {
+  DPlan p;
+  const int nb = (int)((n + kT - 1) / kT);
+  p.tiles = nb * (nb + 1) / 2;
+  const int64_t kblocks = (m + kK - 1) / kK;
+  p.P = p.tiles >= num_sms ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(num_sms / p.tiles, kblocks / 4));
+  p.kchunk = ((kblocks + p.P - 1) / p.P) * kK;
+  p.P = (int)((m + p.kchunk - 1) / p.kchunk);
+  return p;
+}
+
+}  // namespace
+
+size_t syrk_dmma_workspace_bytes(int num_sms) { return (size_t)num_sms * kT * kT * sizeof(double); }
+
+size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms) {
+  DPlan p = dplan(n, m, num_sms);
+  return p.P > 1 ? (size_t)p.tiles * p.P * kT * kT * sizeof(double) : 0;
+}
+
+cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam, double* Gp,
+                      double* ws, int num_sms, cudaStream_t st, int* launches) {
+  DPlan p = dplan(n, m, num_sms);
+  const int direct = p.P == 1 ? 1 : 0;
+  const int vec = ((reinterpret_cast<uintptr_t>(S) | (uintptr_t)(ldS * (s_f64 ? 8 : 4))) & 15) == 0 ? 1 : 0;
+  const unsigned grid = (unsigned)(p.tiles * p.P);
+  if (s_f64) {
+    cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
+                                                                 Gp, direct, vec);
+  } else {
+    cudaFuncSetAttribute(syrk_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    syrk_dmma_kernel<float><<<grid, kThreads, kSmemBytes, st>>>((const float*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
+                                                                Gp, direct, vec);
+  }
+  if (launches) *launches += 1;
+  if (!direct) {
+    syrk_dmma_reduce<<<p.tiles, 256, 0, st>>>(ws, p.P, n, lam, Gp);
+    if (launches) *launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fs
