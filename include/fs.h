@@ -132,6 +132,9 @@ int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m
  * out_res: host double[2] = {abs_residual, rel_residual} (if bit0).  Synchronizes. */
 #define FS_FLAG_RESIDUAL 1
 #define FS_FLAG_REFINE 2
+/* iterative refinement: up to k correction steps with the same factor while
+ * rel_residual > refine_above and each step at least halves it; k = 1 is the reference rule */
+#define FS_FLAG_REFINE_STEPS(k) (FS_FLAG_REFINE | (((k) & 0xFF) << 8))
 int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
                   int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
                   void* allreduce_user, int flags, double refine_above, int64_t* pivot,

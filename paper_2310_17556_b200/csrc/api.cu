@@ -256,7 +256,10 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
   if ((rc = solve_cols(v, vdt == FS_F64, lam, false))) return rc;
   prof_mark(ctx, FS_PROF_GEMV_STZ, st);
   double abs_res = NAN, rel_res = NAN;
-  for (int pass = 0; want_res && pass < 2; ++pass) {
+  // refinement steps: FS_FLAG_REFINE alone = the reference's single step; bits 8-15 raise it
+  const int max_steps = want_refine ? std::max(1, (flags >> 8) & 0xFF) : 0;
+  double prev_rel = INFINITY;
+  for (int pass = 0; want_res && pass <= max_steps; ++pass) {
     // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
     if (!y_ready && (rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
     if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
@@ -264,7 +267,7 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     {
       int l = 0;
       cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
-                                        want_refine && pass == 0 ? ctx->d_r : nullptr, ctx->d_block_sums,
+                                        pass < max_steps ? ctx->d_r : nullptr, ctx->d_block_sums,
                                         ctx->d_sums, st, &l);
       ctx->launches += l;
       if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
@@ -284,7 +287,10 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     if (*ctx->h_status != 0) break;
     abs_res = sqrt(ctx->h_sums[0]);
     rel_res = abs_res / std::max(sqrt(ctx->h_sums[1]), kEps);
-    if (pass == 1 || !want_refine || !(rel_res > refine_above)) break;
+    if (pass == max_steps || !(rel_res > refine_above)) break;
+    // iterative mode: stop once a step no longer halves the residual (no contraction left)
+    if (pass > 0 && !(rel_res < 0.5 * prev_rel)) break;
+    prev_rel = rel_res;
     // one correction pass with the same factor (solvers.py:183-194): d = chol_apply(-r)
     // residual_cols stored r = (S^T y + lam x) - v; refinement right-hand side is -r
     if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream))) return rc;

@@ -120,14 +120,17 @@ def _meter_slots(n: int, m: int, dtype: int, precision: int) -> int:
 
 
 def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
-               refine: str | bool = "auto", diagnostics: bool = True) -> Solution:
+               refine: str | bool | int = "auto", diagnostics: bool = True) -> Solution:
     """Solve (S^T S + lam I) x = v through the n-by-n Gram factorization (solvers.py:197-206).
 
-    precision: "fp64" (exact fp64 products, the reference's arithmetic), "tf32x3" (fp32 scores,
-    tcgen05 3xTF32 Gram with fp64 drains) or "auto" (by the scores' dtype).
+    precision: "fp64" (exact fp64 products, the reference's arithmetic), "f16x2" (default for
+    fp32 scores: row-scaled two-plane fp16 split on the tensor cores), "tf32x3", or "auto".
     refine: "auto" applies the reference's one-step refinement rule (rel_residual > 1e-10,
-    solvers.py:171-194) in fp64 mode and no refinement in tf32x3 mode, whose stated bound is
-    4 u32 sigma_max^2/lam; True forces the reference rule, False disables it.
+    solvers.py:171-194) in fp64 mode and none in the fp32 modes, whose stated bound is
+    4 u32 sigma_max^2/lam; True forces the reference rule; an int k > 1 runs up to k correction
+    steps with the same factor and fp64 residuals (mixed-precision iterative refinement,
+    SURVEY §8f-1), stopping at rel_residual <= 1e-10 or when a step no longer halves it —
+    it contracts when u32 sigma_max^2/lam << 1; False disables refinement.
     diagnostics: compute abs/rel residual on the GPU (two extra passes over S), as the
     reference does inside solve_chol (solvers.py:160-170).
     """
@@ -136,13 +139,19 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
     t0 = perf_counter()
     n, m = system.n, system.m
     prec = resolve_precision(precision, system.S.dtype)
+    steps = 0
     if refine == "auto":
-        do_refine = prec == "fp64"
+        steps = 1 if prec == "fp64" else 0
+    elif isinstance(refine, bool):
+        steps = 1 if refine else 0
+    elif isinstance(refine, (int, np.integer)) and 0 <= int(refine) <= 255:
+        steps = int(refine)
     else:
-        do_refine = bool(refine)
+        raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
+    do_refine = steps > 0
     if do_refine and not diagnostics:
         raise ValueError("refinement needs the residual diagnostics")
-    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (_lib.FS_FLAG_REFINE if do_refine else 0)
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (steps << 8)) if do_refine else 0)
     dt = _lib.FS_F32 if system.S.dtype == torch.float32 else _lib.FS_F64
     device = system.S.device
     ctx = _lib.context_for(device.index, n, m)

@@ -576,3 +576,34 @@ def test_host_solutions_stay_independent(fsb):
     a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)).x
     ref = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
     assert O.rel_err(a, ref.x) <= 1e-6
+
+
+# ---------------------------------------------------------------- iterative refinement
+
+@pytest.mark.parametrize("precision", ["f16x2", "tf32x3"])
+def test_iterative_refinement_contracts_in_fp32_modes(fsb, precision):
+    """u32 sigma^2/lam ~ 0.02: each correction step (fp32-split factor, fp64 residual) contracts the
+    residual ~5x (tools/refine_probe.py: 1.4e-2 -> 1.5e-10 in 12 steps); x converges to the fp64
+    solve of the identical system."""
+    S, v, lam = O.generate_problem(41, 256, 65536, 1e-3)
+    S32, v32 = S.astype(np.float32), v.astype(np.float32)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)
+    ref = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
+    rels, errs = [], []
+    for k in (0, 1, 2, 8):
+        sol = fsb.solve_chol(system, precision=precision, refine=k)
+        rels.append(sol.rel_residual)
+        errs.append(O.rel_err(sol.x, ref.x))
+    assert rels[1] < 0.5 * rels[0] and rels[2] < 0.5 * rels[1] and rels[3] < rels[2], rels
+    assert rels[3] <= 1e-6, rels
+    assert errs[3] <= 1e-11 and errs[3] < errs[0], errs
+
+
+def test_refinement_argument_validation(fsb):
+    S, v, lam = O.generate_problem(42, 8, 50, 1e-3)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    for bad in (-1, 256, 1.5, "always"):
+        with pytest.raises(ValueError):
+            fsb.solve_chol(system, refine=bad)
+    with pytest.raises(ValueError):
+        fsb.solve_chol(system, refine=2, diagnostics=False)
