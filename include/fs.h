@@ -32,7 +32,8 @@ typedef enum {
   FS_NOT_PD = 2,      /* Cholesky breakdown -> FactorizationError(pivot) (solvers.py:82-87) */
   FS_ECUDA = 3,       /* CUDA runtime/driver error                                      */
   FS_ENOMEM = 4,      /* problem larger than the context was created for               */
-  FS_EUNSUPPORTED = 5 /* e.g. precision mode not available for this dtype              */
+  FS_EUNSUPPORTED = 5, /* e.g. precision mode not available for this dtype             */
+  FS_ENOCONV = 6       /* eigendecomposition did not converge (solvers.py:262-263)       */
 } fs_status;
 
 typedef enum { FS_F32 = 0, FS_F64 = 1 } fs_dtype;
@@ -151,6 +152,19 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
                        int64_t ldS, const void* v_host, double lam, double* x_host, fs_allreduce_fn allreduce,
                        void* allreduce_user, int flags, double refine_above, int64_t* pivot,
                        double* out_res, void* stream);
+
+/* ---- eigh comparison route (solvers.py:243-277, :294-354) ----
+ * fs_syevj_packed: eigenpairs of a packed lower symmetric fp64 matrix (device): w (n) descending,
+ * U (n x n, leading dimension ldU, column j <-> w[j]); parallel Jacobi on the GPU (replaces
+ * np.linalg.eigh -> dsyevd).  n <= 8192.  *sweeps = Jacobi sweeps run.  Synchronizes.
+ * fs_eigh_solve: solve_svd_eigh — Gram (precision as fs_chol_solve), eigh, singular values
+ * floored at sigma_floor * sigma_max (*rank = kept count), x from the kept eigenpairs, residual
+ * against S (flags: FS_FLAG_RESIDUAL only; no refinement on this route).  Synchronizes. */
+int fs_syevj_packed(fs_ctx* ctx, const double* G_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
+                    void* stream);
+int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m, int64_t ldS,
+                  const void* v, double lam, double sigma_floor, double* x, fs_allreduce_fn allreduce,
+                  void* allreduce_user, int flags, int64_t* rank, double* out_res, void* stream);
 
 #ifdef __cplusplus
 }

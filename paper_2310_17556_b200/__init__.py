@@ -37,6 +37,9 @@ from .solvers import (
     solve_realpart,
     solve_svd_direct,
     solve_svd_eigh,
+    ThinSvd,
+    eigh_gram,
+    thin_svd_eigh,
 )
 
 __version__ = "0.1.0"

@@ -12,7 +12,7 @@ import threading
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfisher_b200.so")
 
-FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED = range(6)
+FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED, FS_ENOCONV = range(7)
 FS_F32, FS_F64 = 0, 1
 FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO, FS_PREC_F16X2 = 0, 1, 2, 3
 FS_FLAG_RESIDUAL, FS_FLAG_REFINE = 1, 2
@@ -48,6 +48,10 @@ SIGNATURES = {
                                         ctypes.c_int, ctypes.c_double, _vp, _vp, _vp]),
     "fs_chol_solve": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                      ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,
+                                     ctypes.POINTER(_c_int64), _dp, _vp]),
+    "fs_syevj_packed": (ctypes.c_int, [_vp, _vp, _c_int64, _vp, _vp, _c_int64, ctypes.POINTER(ctypes.c_int), _vp]),
+    "fs_eigh_solve": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
+                                     ctypes.c_double, ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int,
                                      ctypes.POINTER(_c_int64), _dp, _vp]),
     "fs_chol_solve_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                           ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,

@@ -42,6 +42,14 @@ struct fs_ctx {
   std::string err;
   uint8_t* d_St = nullptr;      // tiled copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
+  // eigh comparison route (lazy): Jacobi workspace, U (n_max^2), w, scratch, info
+  void* d_eig = nullptr;
+  double* d_U = nullptr;
+  double* d_w = nullptr;
+  double* d_t = nullptr;
+  int* d_info = nullptr;
+  int* h_info = nullptr;        // pinned [2]
+  double* h_w = nullptr;        // pinned n_max
   float* d_scale = nullptr;     // F16X2 row scales (n_max)
   double* d_inv_scale = nullptr;
   int* d_ovf = nullptr;         // F16X2 retile flags (bit 1: fp16 overflow)
@@ -161,6 +169,41 @@ int ensure_tiles(fs_ctx* ctx) {
   return FS_OK;
 }
 
+int ensure_eig(fs_ctx* ctx) {
+  if (ctx->d_eig) return FS_OK;
+  if (ctx->n_max > fs::syevj_max_n()) return fail(ctx, FS_EUNSUPPORTED, "eigh route supports n <= 8192");
+  const int64_t n = ctx->n_max;
+  bool ok = cudaMalloc(&ctx->d_eig, fs::syevj_workspace_bytes(n, ctx->num_sms)) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_U, (size_t)n * n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_w, (size_t)n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_t, (size_t)n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_info, 2 * sizeof(int)) == cudaSuccess &&
+            cudaMallocHost((void**)&ctx->h_info, 2 * sizeof(int)) == cudaSuccess &&
+            cudaMallocHost((void**)&ctx->h_w, (size_t)n * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    return fail(ctx, FS_ENOMEM, "cannot allocate the eigensolver workspace");
+  }
+  return FS_OK;
+}
+
+// Eigenpairs of the packed Gram (no shift) into ctx->d_w (descending) / ctx->d_U; synchronises
+// to read the convergence word and w (ctx->h_w).
+int eig_impl(fs_ctx* ctx, const double* Gp, int64_t n, cudaStream_t st) {
+  int rc = ensure_eig(ctx);
+  if (rc) return rc;
+  int l = 0;
+  // tolerance: off(A) <= 1e-14 ||A||_F, at most 40 sweeps (quadratic convergence: ~6-10)
+  cudaError_t e = fs::syevj(Gp, n, ctx->d_w, ctx->d_U, n, 40, 1e-14, ctx->d_eig, ctx->num_sms, ctx->d_info, st, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "syevj");
+  FS_CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "info d2h");
+  FS_CK(cudaMemcpyAsync(ctx->h_w, ctx->d_w, n * sizeof(double), cudaMemcpyDeviceToHost, st), "w d2h");
+  FS_CK(cudaStreamSynchronize(st), "sync");
+  if (ctx->h_info[1]) return fail(ctx, FS_ENOCONV, "eigendecomposition did not converge");
+  return FS_OK;
+}
+
 // Gram stage.  TF32X3: retile S into S_t (optionally fused with u = S w), then the CTA-pair
 // tcgen05 SYRK on S_t.  FP64: exact-product SIMT SYRK on S.
 int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
@@ -205,6 +248,10 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
 // internal: the F16X2 Gram overflowed on some rank -> recompute with TF32X3
 constexpr int kRetryTf32 = 100;
 
+static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
+                    double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
+                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf);
+
 // ovf: F16X2 retile flag word (bit 2 = fp16 overflow) or NULL.  The bit joins the norms
 // all-reduce, so every rank takes the same retry decision.
 static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
@@ -229,6 +276,18 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
   prof_mark(ctx, FS_PROF_TRSV, st);
+  return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
+                  out_res, st, ovf);
+}
+
+// From z (in ctx->d_z) to x = (v - S^T z)/lam, the residual diagnostics and the optional
+// refinement with the Cholesky factor in ctx->d_W (solvers.py:122-126, :160-194).
+static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
+                    double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
+                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf) {
+  int rc = FS_OK;
+  void* stream = (void*)st;
+  const int nsums = ovf ? 3 : 2;
   const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
   const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
   // 3. x = (v - S^T z) / lam on the local shard; with diagnostics fused with y = S x (one
@@ -403,6 +462,13 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
   cudaFree(ctx->d_potrf);
   cudaFree(ctx->d_scale); cudaFree(ctx->d_inv_scale); cudaFree(ctx->d_ovf);
+  if (ctx->d_eig) cudaFree(ctx->d_eig);
+  if (ctx->d_U) cudaFree(ctx->d_U);
+  if (ctx->d_w) cudaFree(ctx->d_w);
+  if (ctx->d_t) cudaFree(ctx->d_t);
+  if (ctx->d_info) cudaFree(ctx->d_info);
+  if (ctx->h_info) cudaFreeHost(ctx->h_info);
+  if (ctx->h_w) cudaFreeHost(ctx->h_w);
   if (ctx->h_ovf) cudaFreeHost(ctx->h_ovf);
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
   if (ctx->h_sums) cudaFreeHost(ctx->h_sums);
@@ -730,6 +796,87 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     return fail(ctx, FS_EINVAL, "score matrix and right-hand side must contain only finite entries");
   }
   return rc;
+}
+
+int fs_syevj_packed(fs_ctx* ctx, const double* G_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
+                    void* stream) {
+  if (!ctx || !G_packed || !w || !U || n < 1 || ldU < n) return fail(ctx, FS_EINVAL, "bad syevj arguments");
+  if (n > ctx->n_max) return fail(ctx, FS_ENOMEM, "n exceeds n_max");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = eig_impl(ctx, G_packed, n, st);
+  if (sweeps && ctx->h_info) *sweeps = ctx->h_info[0];
+  if (rc) return rc;
+  FS_CK(cudaMemcpyAsync(w, ctx->d_w, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "w copy");
+  FS_CK(cudaMemcpy2DAsync(U, ldU * sizeof(double), ctx->d_U, n * sizeof(double), n * sizeof(double), n,
+                          cudaMemcpyDeviceToDevice, st),
+        "U copy");
+  return FS_OK;
+}
+
+int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m, int64_t ldS,
+                  const void* v, double lam, double sigma_floor, double* x, fs_allreduce_fn allreduce,
+                  void* allreduce_user, int flags, int64_t* rank, double* out_res, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if ((rc = check_lam(ctx, lam))) return rc;
+  if (!(sigma_floor >= 0.0) || !isfinite(sigma_floor)) return fail(ctx, FS_EINVAL, "sigma_floor must be finite and >= 0");
+  if (n > m) return fail(ctx, FS_EINVAL, "the eigh route requires n <= m (solvers.py:254-255)");
+  if (!v || !x) return fail(ctx, FS_EINVAL, "NULL vector");
+  cudaStream_t st = (cudaStream_t)stream;
+  int use_tc = 0;
+  if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+  int vdt = dtype;
+  if (dtype == FS_F32 && !use_tc) {
+    int l = 0;
+    cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "widen v");
+    v = ctx->d_v64;
+    vdt = FS_F64;
+  }
+  double* u = ctx->d_packed + n * (n + 1) / 2;
+  ctx->n_marks = 0;
+  prof_mark(ctx, -1, st);
+  // 1. Gram (no shift) and u = S v, packed for one all-reduce (solvers.py:257-259)
+  if (use_tc && vdt == FS_F32) {
+    if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st, (const float*)v, u))) return rc;
+  } else {
+    if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
+    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+    prof_mark(ctx, FS_PROF_GEMV_SV, st);
+  }
+  if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
+    return fail(ctx, FS_ECUDA, "allreduce of [G | u] failed");
+  prof_mark(ctx, FS_PROF_ALLREDUCE, st);
+  // 2. G = U diag(w) U^T, w descending (solvers.py:261-266); sigma floor (solvers.py:267-271)
+  if ((rc = eig_impl(ctx, ctx->d_packed, n, st))) return rc;
+  if (use_tc == 2) {   // an F16X2 overflow shows up here already (the eigh path synchronises)
+    FS_CK(cudaMemcpyAsync(ctx->h_ovf, ctx->d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
+    FS_CK(cudaStreamSynchronize(st), "sync");
+    if (*ctx->h_ovf & 2)
+      return fs_eigh_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, sigma_floor, x, allreduce,
+                           allreduce_user, flags, rank, out_res, stream);
+  }
+  prof_mark(ctx, FS_PROF_POTRF, st);
+  const double s0 = sqrt(std::max(ctx->h_w[0], 0.0));
+  int64_t r = 0;
+  while (r < n && sqrt(std::max(ctx->h_w[r], 0.0)) > sigma_floor * s0) ++r;
+  if (rank) *rank = r;
+  // 3. z = U_r (w_r + lam)^-1 U_r^T u  ==  the V (s^2+lam)^-1 V^T v part of solvers.py:315-317
+  //    rewritten through S^T: x = (v - S^T z') / lam with z' = -(...); here z = U_r diag(...) U_r^T u
+  //    and x = (v - S^T z)/lam follows from (v - V V^T v)/lam + V (s^2+lam)^-1 V^T v.
+  {
+    int l = 0;
+    cudaError_t e = fs::eig_apply(ctx->d_U, n, n, r, u, ctx->d_w, lam, ctx->d_t, ctx->d_z, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "eig_apply");
+  }
+  prof_mark(ctx, FS_PROF_TRSV, st);
+  FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "status reset");
+  // 4. x and the residual against S (solvers.py:318-322 -> _finish); no refinement on this route
+  int64_t piv = -1;
+  return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags & FS_FLAG_RESIDUAL, 0.0,
+                  &piv, out_res, st, nullptr);
 }
 
 }  // extern "C"

@@ -90,4 +90,15 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
                       const int64_t* d_status, cudaStream_t st, int* launches);
 
+// ---- syevj.cu (eigh comparison route) ----
+size_t syevj_workspace_bytes(int64_t n, int num_sms);
+int64_t syevj_max_n();
+// eigenpairs of the packed lower symmetric Gp: w descending, U (n x n, ldu) column j <-> w[j];
+// d_info[0] = sweeps run, d_info[1] = 1 if not converged within max_sweeps
+cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu, int max_sweeps, double tol,
+                  void* ws, int num_sms, int* d_info, cudaStream_t st, int* launches);
+// z = U_r diag(1/(max(w,0)+lam)) U_r^T u (t: r doubles of scratch)
+cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const double* u, const double* w, double lam,
+                      double* t, double* z, cudaStream_t st, int* launches);
+
 }  // namespace fs

@@ -205,9 +205,116 @@ def solve_realpart(system, meter=None):
     _not_yet("solve_realpart")
 
 
-def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOOR) -> Solution:
-    """solvers.py:347-354 comparison route."""
-    _not_yet("solve_svd_eigh")
+@dataclass(frozen=True)
+class ThinSvd:
+    """Thin SVD factors S = U diag(sigma) V^T (solvers.py ThinSvd): U n x r, sigma (r,), V m x r."""
+
+    U: object
+    sigma: object
+    V: object
+
+    @property
+    def r(self) -> int:
+        return int(self.sigma.shape[0])
+
+    @property
+    def m(self) -> int:
+        return int(self.V.shape[0])
+
+
+def _check_floor(sigma_floor) -> float:
+    sigma_floor = float(sigma_floor)
+    if not np.isfinite(sigma_floor) or sigma_floor < 0.0:
+        raise ValueError(f"sigma_floor must be finite and >= 0, got {sigma_floor}")
+    return sigma_floor
+
+
+def eigh_gram(S: ScoreMatrix, precision: str = "auto") -> tuple[torch.Tensor, torch.Tensor, int]:
+    """Eigenpairs of the Gram S S^T on the GPU (solvers.py:257-266): w descending (fp64, device),
+    U (n x n fp64, device, column j <-> w[j]), and the Jacobi sweep count."""
+    t = S.tensor
+    n = S.n
+    Gp = _gram_packed_unshifted(S, precision)
+    ctx = _lib.context_for(t.device.index, n, S.m)
+    w = torch.empty(n, dtype=torch.float64, device=t.device)
+    U = torch.empty((n, n), dtype=torch.float64, device=t.device)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_syevj_packed(ctx.handle, Gp.data_ptr(), n, w.data_ptr(), U.data_ptr(), n, ctypes.byref(sweeps),
+                                 _stream(t.device))
+    if rc == _lib.FS_ENOCONV:
+        raise FactorizationError(f"eigendecomposition did not converge: {ctx.last_error()}")
+    _check(ctx, rc, "fs_syevj_packed")
+    return w, U, int(sweeps.value)
+
+
+def _gram_packed_unshifted(S: ScoreMatrix, precision: str) -> torch.Tensor:
+    t = S.tensor
+    n, m = S.n, S.m
+    prec = resolve_precision(precision, t.dtype)
+    ctx = _lib.context_for(t.device.index, n, m)
+    out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
+    rc = ctx.lib.fs_gram_packed(ctx.handle, _dt(t), PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0), 0.0,
+                                out.data_ptr(), _stream(t.device))
+    _check(ctx, rc, "fs_gram_packed")
+    return out
+
+
+def thin_svd_eigh(S: ScoreMatrix, sigma_floor: float = DEFAULT_SIGMA_FLOOR, *, precision: str = "auto") -> ThinSvd:
+    """Thin SVD via the eigendecomposition of the n-by-n Gram matrix (solvers.py:243-277) on the GPU.
+
+    Eigenvalues made negative by round-off are clamped to zero; singular values at or below
+    sigma_floor * sigma_max are truncated; V = S^T (U / sigma).  The Gram and the Jacobi
+    eigensolver are this package's kernels; the explicit m x r factor V is one plain dense
+    product (torch.matmul) — the solve route (solve_svd_eigh) never forms it.
+    """
+    sigma_floor = _check_floor(sigma_floor)
+    if S.n > S.m:
+        raise ValueError(f"thin_svd_eigh requires n <= m, got shape {S.shape}")
+    w, U, _ = eigh_gram(S, precision)
+    sigma = torch.sqrt(torch.clamp(w, min=0.0))
+    keep = sigma > sigma_floor * sigma[0]
+    U = U[:, keep].contiguous()
+    sigma = sigma[keep].contiguous()
+    if sigma.numel() == 0:
+        V = torch.zeros((S.m, 0), dtype=torch.float64, device=U.device)
+    else:
+        V = S.tensor.to(torch.float64).T @ (U / sigma)
+    if S.host_origin:
+        return ThinSvd(U=U.cpu().numpy(), sigma=sigma.cpu().numpy(), V=V.cpu().numpy())
+    return ThinSvd(U=U, sigma=sigma, V=V)
+
+
+def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOOR, *, precision: str = "auto",
+                   diagnostics: bool = True) -> Solution:
+    """solve_svd_eigh (solvers.py:347-354): thin SVD through the Gram eigendecomposition, then
+    x = V (sigma^2 + lam)^-1 V^T v + (v - V V^T v) / lam (solvers.py:315-317), residual against S.
+
+    On the GPU (fs_eigh_solve): Gram + u = S v (same kernels and precision modes as solve_chol),
+    Jacobi eigendecomposition, and the solve through S^T without forming V:
+    x = (v - S^T z) / lam with z = U_r diag(1 / (w_r + lam)) U_r^T u over the kept eigenpairs.
+    """
+    sigma_floor = _check_floor(sigma_floor)
+    t0 = perf_counter()
+    S = system.S.tensor
+    v = system.v_tensor
+    n, m = system.n, system.m
+    if n > m:
+        raise ValueError(f"thin_svd_eigh requires n <= m, got shape {(n, m)}")
+    prec = resolve_precision(precision, S.dtype)
+    ctx = _lib.context_for(S.device.index, n, m)
+    x = torch.empty(m, dtype=torch.float64, device=S.device)
+    rank = ctypes.c_int64(0)
+    res = (ctypes.c_double * 2)(float("nan"), float("nan"))
+    flags = _lib.FS_FLAG_RESIDUAL if diagnostics else 0
+    rc = ctx.lib.fs_eigh_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0), v.data_ptr(),
+                               system.lam, sigma_floor, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
+                               ctypes.byref(rank), res, _stream(S.device))
+    if rc == _lib.FS_ENOCONV:
+        raise FactorizationError(f"eigendecomposition did not converge: {ctx.last_error()}")
+    _check(ctx, rc, "fs_eigh_solve")
+    xo = x.cpu().numpy() if system.S.host_origin else x
+    return Solution(x=xo, method=Method.SVD_EIGH, abs_residual=float(res[0]), rel_residual=float(res[1]),
+                    wall_seconds=perf_counter() - t0, precision=prec)
 
 
 def solve_svd_direct(system: DampedSystem) -> Solution:

@@ -607,3 +607,87 @@ def test_refinement_argument_validation(fsb):
             fsb.solve_chol(system, refine=bad)
     with pytest.raises(ValueError):
         fsb.solve_chol(system, refine=2, diagnostics=False)
+
+
+# ---------------------------------------------------------------- eigh comparison route
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64, 129, 300, 1024])
+def test_syevj_matches_lapack(fsb, n):
+    """The Jacobi eigensolver vs numpy/LAPACK eigh on a Gram matrix: eigenvalues, orthonormality,
+    reconstruction, descending order (solvers.py:261-266)."""
+    from paper_2310_17556_b200 import _lib
+    rng = np.random.Generator(np.random.PCG64(100 + n))
+    A = rng.standard_normal((n, 2 * n + 3))
+    G = A @ A.T
+    dev = torch.device("cuda", 0)
+    Gp = torch.from_numpy(G[np.tril_indices(n)].copy()).to(dev)
+    ctx = _lib.context_for(0, n, 8)
+    w = torch.empty(n, dtype=torch.float64, device=dev)
+    U = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_syevj_packed(ctx.handle, Gp.data_ptr(), n, w.data_ptr(), U.data_ptr(), n, ctypes.byref(sweeps),
+                                 torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, ctx.last_error()
+    w, U = w.cpu().numpy(), U.cpu().numpy()
+    ref = np.linalg.eigvalsh(G)[::-1]
+    scale = np.abs(ref).max()
+    assert np.all(np.diff(w) <= 0)
+    assert np.abs(w - ref).max() <= 1e-12 * scale, np.abs(w - ref).max() / scale
+    assert np.abs(U.T @ U - np.eye(n)).max() <= 1e-12
+    assert np.abs(U @ np.diag(w) @ U.T - G).max() <= 1e-12 * scale
+    assert sweeps.value <= 20
+
+
+@pytest.mark.parametrize("name", FP64_CASES)
+def test_golden_eigh_route(fsb, name, golden, manifest):
+    """solve_svd_eigh vs the real reference's eigh-route x (tests/golden), fp64 arithmetic."""
+    key = f"{name}_eigh_x"
+    if key not in golden:
+        pytest.skip("case without an eigh golden")
+    S, v, lam = regenerate(manifest["cases"][name])
+    sol = fsb.solve_svd_eigh(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="fp64")
+    assert sol.method is fsb.Method.SVD_EIGH
+    assert O.rel_err(sol.x, golden[key]) <= 1e-8, O.rel_err(sol.x, golden[key])
+    ref = O.solve_chol(S, v, lam)
+    assert sol.rel_residual <= max(1e-8, 16 * U64 * sigma2_max(S) / lam)
+    assert O.rel_err(sol.x, ref.x) <= 1e-8
+
+
+def test_thin_svd_eigh_factors(fsb):
+    """solvers.py:243-277 contract (test_solvers.py eigh cases): reconstruction, orthonormality,
+    singular values vs LAPACK."""
+    S, v, lam = O.generate_problem(51, 60, 900, 1e-2)
+    svd = fsb.thin_svd_eigh(fsb.ScoreMatrix(S), precision="fp64")
+    U, s, V = svd.U, svd.sigma, svd.V
+    assert svd.r == 60 and svd.m == 900
+    assert np.abs((U * s) @ V.T - S).max() <= 1e-8 * np.abs(S).max()
+    assert np.abs(U.T @ U - np.eye(60)).max() <= 1e-10
+    assert np.abs(V.T @ V - np.eye(60)).max() <= 1e-8
+    ref = np.linalg.svd(S, compute_uv=False)
+    assert np.abs(s - ref).max() <= 1e-10 * ref.max()
+
+
+def test_eigh_route_sigma_floor_rank_deficient(fsb):
+    """Duplicated rows: the floored singular values are dropped (rank < n), x still matches."""
+    S, v, lam = O.generate_problem(52, 40, 500, 1e-2)
+    S[20:] = S[:20]                    # rank 20
+    sol = fsb.solve_svd_eigh(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), sigma_floor=1e-6, precision="fp64")
+    ref = O.solve_svd_eigh(S, v, lam, 1e-6)
+    assert O.rel_err(sol.x, ref.x) <= 1e-8
+    svd = fsb.thin_svd_eigh(fsb.ScoreMatrix(S), sigma_floor=1e-6, precision="fp64")
+    assert svd.r == 20
+    with pytest.raises(ValueError):
+        fsb.solve_svd_eigh(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), sigma_floor=-1.0)
+
+
+@pytest.mark.parametrize("precision", ["f16x2", "fp64"])
+def test_eigh_route_agrees_with_chol(fsb, precision):
+    """Same system, two routes: chol and eigh give the same x (fp32 scores, both precisions)."""
+    S, v, lam = O.generate_problem(53, 512, 30000, 1e-3)
+    S32, v32 = S.astype(np.float32), v.astype(np.float32)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)
+    a = fsb.solve_chol(system, precision=precision)
+    b = fsb.solve_svd_eigh(system, precision=precision)
+    tol = 1e-10 if precision == "fp64" else 1e-6
+    assert O.rel_err(a.x, b.x) <= tol, O.rel_err(a.x, b.x)
+    assert b.rel_residual <= 4 * U32 * sigma2_max(S32) / lam
