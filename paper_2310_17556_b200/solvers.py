@@ -317,6 +317,15 @@ def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOO
                     wall_seconds=perf_counter() - t0, precision=prec)
 
 
-def solve_svd_direct(system: DampedSystem) -> Solution:
-    """solvers.py:357-364 comparison route."""
-    _not_yet("solve_svd_direct")
+def solve_svd_direct(system: DampedSystem, *, precision: str = "auto", diagnostics: bool = True) -> Solution:
+    """solve_svd_direct (solvers.py:357-364, the "svda" comparison route): thin SVD of S, exact-zero
+    singular values dropped (solvers.py:280-291), then the factor solve with the residual against S.
+
+    The reference calls dgesdd; the paper's GPU svda called cuSOLVER gesvda, a Gram-based
+    approximate tall-skinny SVD.  This route follows the paper's algorithm class: the thin SVD
+    comes from the Jacobi eigendecomposition of S S^T (fs_eigh_solve) with NO floor — only
+    singular values that are exactly zero (eigenvalues <= 0) are dropped, as in the reference.
+    """
+    sol = solve_svd_eigh(system, 0.0, precision=precision, diagnostics=diagnostics)
+    return Solution(x=sol.x, method=Method.SVD_DIRECT, abs_residual=sol.abs_residual,
+                    rel_residual=sol.rel_residual, wall_seconds=sol.wall_seconds, precision=sol.precision)

@@ -691,3 +691,15 @@ def test_eigh_route_agrees_with_chol(fsb, precision):
     tol = 1e-10 if precision == "fp64" else 1e-6
     assert O.rel_err(a.x, b.x) <= tol, O.rel_err(a.x, b.x)
     assert b.rel_residual <= 4 * U32 * sigma2_max(S32) / lam
+
+
+@pytest.mark.parametrize("name", FP64_CASES)
+def test_golden_svd_direct_route(fsb, name, golden, manifest):
+    """solve_svd_direct vs the real reference's dgesdd-route x (tests/golden), fp64 arithmetic."""
+    key = f"{name}_svd_x"
+    if key not in golden:
+        pytest.skip("case without an svd golden")
+    S, v, lam = regenerate(manifest["cases"][name])
+    sol = fsb.solve_svd_direct(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="fp64")
+    assert sol.method is fsb.Method.SVD_DIRECT
+    assert O.rel_err(sol.x, golden[key]) <= 1e-8, O.rel_err(sol.x, golden[key])
