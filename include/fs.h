@@ -166,6 +166,15 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
                   const void* v, double lam, double sigma_floor, double* x, fs_allreduce_fn allreduce,
                   void* allreduce_user, int flags, int64_t* rank, double* out_res, void* stream);
 
+/* ---- complex scores (solvers.py:209-240) ----
+ * S: device, n x m complex (interleaved re, im of `dtype`; ldS in complex elements).
+ * kind 0: out = [Re S; Im S] (2n x m) — solve_realpart's C (sr.py:61-70), C^T C = Re[S^H S].
+ * kind 1: out = [[Re S, -Im S], [Im S, Re S]] (2n x 2m) — the real representation under which
+ *         solve_chol_hermitian's (S^H S + lam I) x = v is the plain system on [Re x; Im x].
+ * out: device, real `dtype`, leading dimension ldo.  The caller then runs fs_chol_solve. */
+int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, void* out,
+                     int64_t ldo, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -143,6 +143,67 @@ def solve_chol(S: np.ndarray, v: np.ndarray, lam: float, refine_above: float = R
     return OracleSolution(x, abs_res, rel_res, perf_counter() - t0, refined=True)
 
 
+# ---------------------------------------------------------------- complex scores
+
+def generate_problem_complex(seed: int, n: int, m: int, lam: float = 1e-3):
+    """Restates bench.py:161-165 (Kind.COMPLEX_GAUSSIAN): PCG64(seed); the full real block, then
+    the full imaginary block (row-major), S = (re + 1j im)/sqrt(n); v = normal(m) + 1j normal(m)."""
+    rng = np.random.Generator(np.random.PCG64(int(seed)))
+    re = rng.standard_normal((int(n), int(m)))
+    im = rng.standard_normal((int(n), int(m)))
+    S = (re + 1j * im) / np.sqrt(float(n))
+    v = rng.standard_normal(int(m)) + 1j * rng.standard_normal(int(m))
+    return S, v, float(lam)
+
+
+def solve_chol_hermitian(S: np.ndarray, v: np.ndarray, lam: float, refine_above: float = REFINE_ABOVE_REL):
+    """Restates _solve_chol_impl for Variant.HERMITIAN (solvers.py:151-213): W = S S^H + lam I
+    symmetrised (core.py:280-290), complex potrf, x = (b - S^H L^-H L^-1 S b)/lam (solvers.py:101-127),
+    residual of S^H S x + lam x - v (core.py:299-302), one refinement pass when rel > 1e-10."""
+    t0 = perf_counter()
+    A = np.ascontiguousarray(S, dtype=np.complex128)
+    v = np.ascontiguousarray(v, dtype=np.complex128)
+    W = A @ A.conj().T                                     # core.py:282
+    W = 0.5 * (W + W.conj().T)                             # core.py:287
+    W[np.diag_indices(A.shape[0])] += lam                  # core.py:289
+    L = cholesky_lower(W)
+
+    def apply(b):                                          # solvers.py:101-127, hermitian branch
+        t1 = A @ b
+        t2 = solve_triangular(L, t1, lower=True, trans="N", check_finite=False)
+        t3 = solve_triangular(L, t2, lower=True, trans="C", check_finite=False)
+        w = np.conj(np.conj(t3) @ A)
+        return (b - w) / lam
+
+    def op(x):                                             # core.py:299-302
+        return np.conj(np.conj(A @ x) @ A) + lam * x
+
+    x = apply(v)
+    r = op(x) - v
+    abs_res = float(np.linalg.norm(r))
+    rel_res = abs_res / max(float(np.linalg.norm(v)), EPS)
+    if rel_res <= refine_above:
+        return OracleSolution(x, abs_res, rel_res, perf_counter() - t0, refined=False)
+    x = x + apply(-r)                                      # solvers.py:186-188
+    r = op(x) - v
+    abs_res = float(np.linalg.norm(r))
+    return OracleSolution(x, abs_res, abs_res / max(float(np.linalg.norm(v)), EPS), perf_counter() - t0,
+                          refined=True)
+
+
+def solve_realpart(S: np.ndarray, v: np.ndarray, lam: float):
+    """Restates solve_realpart (solvers.py:216-240): C = [Re S; Im S] (sr.py:61-70), the plain route
+    on C, residual of the REALPART operator (core.py:303-305) against the real v."""
+    A = np.ascontiguousarray(S, dtype=np.complex128)
+    C = np.concatenate([A.real, A.imag], axis=0)
+    inner = solve_chol(C, np.asarray(v, dtype=np.float64), lam)
+    re, im = A.real, A.imag
+    r = (re @ inner.x) @ re + (im @ inner.x) @ im + lam * inner.x - v
+    abs_res = float(np.linalg.norm(r))
+    return OracleSolution(inner.x, abs_res, abs_res / max(float(np.linalg.norm(v)), EPS), inner.wall_seconds,
+                          refined=inner.refined)
+
+
 def thin_svd_eigh(S: np.ndarray, sigma_floor: float = DEFAULT_SIGMA_FLOOR):
     """Thin SVD from the Gram eigendecomposition (solvers.py:243-277, real)."""
     A = np.ascontiguousarray(S, dtype=np.float64)

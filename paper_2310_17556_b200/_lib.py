@@ -53,6 +53,8 @@ SIGNATURES = {
     "fs_eigh_solve": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                      ctypes.c_double, ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int,
                                      ctypes.POINTER(_c_int64), _dp, _vp]),
+    "fs_embed_complex": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
+                                        _c_int64, _vp]),
     "fs_chol_solve_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                           ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,
                                           ctypes.POINTER(_c_int64), _dp, _vp]),

@@ -98,18 +98,12 @@ def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.T
     if isinstance(a, torch.Tensor):
         t = a
         if t.is_complex():
-            raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
-        if t.dtype not in (torch.float32, torch.float64):
+            if t.dtype not in (torch.complex64, torch.complex128):
+                t = t.to(torch.complex128)
+        elif t.dtype not in (torch.float32, torch.float64):
             t = t.to(torch.float64)
     else:
-        arr = np.asarray(a)
-        if np.iscomplexobj(arr):
-            raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
-        if not (np.issubdtype(arr.dtype, np.number) or arr.dtype == np.bool_):
-            raise ValueError(f"{name} must be numeric, got dtype {arr.dtype}")
-        if arr.dtype not in (np.float32, np.float64):
-            arr = arr.astype(np.float64)
-        t = torch.from_numpy(np.ascontiguousarray(arr))
+        t = torch.from_numpy(_coerce_host(a, name))
     dev = device if device is not None else (t.device if t.is_cuda else default_device())
     if t.dim() == 2 and t.shape[1] > 0:
         # rows start on 16-byte boundaries (TMA / vector-load requirement); pad columns are never read
@@ -132,8 +126,8 @@ def _coerce_host(a, name: str) -> np.ndarray:
     """numpy side of core.py:108-119: numeric dtype -> C-contiguous float32/float64 (no copy when it
     already is one).  Finiteness is checked on the device during the upload (fs_chol_solve_host)."""
     arr = np.asarray(a)
-    if np.iscomplexobj(arr):
-        raise ValueError(f"{name}: complex scores are not supported by the B200 path (SURVEY §8f-3)")
+    if np.iscomplexobj(arr):      # complex scores (SURVEY §8f-3): complex64 kept, else complex128
+        return np.ascontiguousarray(arr if arr.dtype in (np.complex64, np.complex128) else arr.astype(np.complex128))
     if not (np.issubdtype(arr.dtype, np.number) or arr.dtype == np.bool_):
         raise ValueError(f"{name} must be numeric, got dtype {arr.dtype}")
     if arr.dtype not in (np.float32, np.float64):
@@ -171,6 +165,17 @@ class ScoreMatrix:
         self._shape = (int(shape[0]), int(shape[1]))
         # numpy in -> numpy out (drop-in semantics); CUDA tensor in -> CUDA tensor out
         self.host_origin = not (isinstance(src, torch.Tensor) and src.is_cuda)
+
+    @classmethod
+    def _owned(cls, t: torch.Tensor) -> "ScoreMatrix":
+        """Wrap a device tensor this package produced (aligned rows, finite): no copy, no check."""
+        sm = cls.__new__(cls)
+        sm._host = None
+        sm._t = t
+        sm._device = t.device
+        sm._shape = (int(t.shape[0]), int(t.shape[1]))
+        sm.host_origin = False
+        return sm
 
     @property
     def is_uploaded(self) -> bool:
@@ -210,13 +215,14 @@ class ScoreMatrix:
 
     @property
     def is_complex(self) -> bool:
-        return False
+        return self.dtype in (torch.complex64, torch.complex128)
 
     @property
     def dtype(self) -> torch.dtype:
         if self._t is not None:
             return self._t.dtype
-        return torch.float32 if self._src.dtype == np.float32 else torch.float64
+        return {np.dtype(np.float32): torch.float32, np.dtype(np.complex64): torch.complex64,
+                np.dtype(np.complex128): torch.complex128}.get(self._src.dtype, torch.float64)
 
     @property
     def device(self) -> torch.device:
@@ -226,7 +232,14 @@ class ScoreMatrix:
 
     @property
     def scalar_kind(self) -> ScalarKind:
+        if self.is_complex:
+            return ScalarKind.COMPLEX128
         return ScalarKind.REAL64 if self.dtype == torch.float64 else ScalarKind.REAL32
+
+    @property
+    def real_dtype(self) -> torch.dtype:
+        """The real scalar type of the scores (float32 for complex64, float64 for complex128)."""
+        return {torch.complex64: torch.float32, torch.complex128: torch.float64}.get(self.dtype, self.dtype)
 
 
 class DampedSystem:
@@ -237,11 +250,23 @@ class DampedSystem:
             S = ScoreMatrix(S)
         self.S = S
         self.lam = _coerce_damping(lam)
-        if isinstance(v, torch.Tensor) and v.is_complex() or (not isinstance(v, torch.Tensor) and np.iscomplexobj(np.asarray(v))):
+        v_complex = v.is_complex() if isinstance(v, torch.Tensor) else np.iscomplexobj(np.asarray(v))
+        if v_complex and not S.is_complex:
             raise ValueError("real score matrix with complex right-hand side")
         self._v = None
         self._vh = None
         self._host_v = None
+        if S.is_complex:
+            # complex scores: v keeps its own kind (the real-part variant needs a
+            # real v), in the scores' precision
+            t = _to_device_tensor(v, "right-hand side", S.tensor.device,
+                                  force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
+            if t.dim() != 1:
+                raise ValueError(f"right-hand side must be 1-D, got shape {tuple(t.shape)}")
+            if t.shape[0] != S.m:
+                raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
+            self._v = t.to(S.dtype if t.is_complex() else S.real_dtype)
+            return
         if not S.is_uploaded and not (isinstance(v, torch.Tensor) and v.is_cuda):
             # host system: v stays on the host beside S (validated here, it is small)
             vh = _coerce_host(v.numpy() if isinstance(v, torch.Tensor) else v, "right-hand side")
@@ -384,12 +409,55 @@ def residual_device(system: DampedSystem, x: torch.Tensor) -> tuple[float, float
     return abs_res, abs_res / max(float(np.sqrt(vv)), EPS)
 
 
+def embed_complex(S: ScoreMatrix, kind: int) -> ScoreMatrix:
+    """Real stand-ins for complex scores on the device (fs_embed_complex):
+    kind 0 -> C = [Re S; Im S] (sr.py:61-70), kind 1 -> [[Re S, -Im S], [Im S, Re S]]."""
+    if not S.is_complex:
+        raise ValueError("embed_complex expects a complex score matrix")
+    t = S.tensor
+    n, m = S.n, S.m
+    rdt = S.real_dtype
+    cols = m if kind == 0 else 2 * m
+    per16 = 16 // torch.empty((), dtype=rdt).element_size()
+    ld = -(-cols // per16) * per16
+    buf = torch.empty((2 * n, ld), dtype=rdt, device=t.device)
+    ctx = _lib.context_for(t.device.index, n, m)
+    rc = ctx.lib.fs_embed_complex(ctx.handle, kind, _lib.FS_F64 if rdt == torch.float64 else _lib.FS_F32,
+                                  t.data_ptr(), n, m, t.stride(0), buf.data_ptr(), ld, _stream(t.device))
+    _check(ctx, rc, "fs_embed_complex")
+    return ScoreMatrix._owned(buf[:, :cols])
+
+
+def stack_complex_vector(v: torch.Tensor, real_dtype: torch.dtype) -> torch.Tensor:
+    """[Re v; Im v] (2m), the right-hand side of the real representation."""
+    if v.is_complex():
+        return torch.cat([v.real, v.imag]).to(real_dtype).contiguous()
+    return torch.cat([v.to(real_dtype), torch.zeros_like(v, dtype=real_dtype)]).contiguous()
+
+
 def residual(system: DampedSystem, x, variant: Variant = Variant.PLAIN) -> tuple[float, float]:
-    """Absolute and relative residual of x (core.py:307-322), evaluated on the GPU."""
+    """Absolute and relative residual of x (core.py:307-322), evaluated on the GPU.
+
+    HERMITIAN (S^H S + lam I) and REALPART (Re[S^H S] + lam I) are evaluated through the real
+    representation / the stacked real matrix (fs_embed_complex): the same norms."""
     if not isinstance(variant, Variant):
         raise ValueError(f"unknown operator variant: {variant!r}")
     if variant is not Variant.PLAIN:
-        raise ValueError("the B200 path implements the PLAIN (real) operator only")
+        if not system.S.is_complex:
+            raise ValueError(f"variant {variant.value} expects complex scores")
+        dev = system.S.tensor.device
+        xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+        xt = xt.to(dev)
+        if xt.dim() != 1 or xt.shape[0] != system.m:
+            raise ValueError(f"solution vector has shape {tuple(xt.shape)}, expected ({system.m},)")
+        if variant is Variant.HERMITIAN:
+            inner = DampedSystem(embed_complex(system.S, 1), system.lam,
+                                 stack_complex_vector(system.v_tensor, system.S.real_dtype))
+            return residual_device(inner, stack_complex_vector(xt, torch.float64))
+        if system.v_tensor.is_complex() or xt.is_complex():
+            raise ValueError("the real-part operator needs a real right-hand side and solution")
+        inner = DampedSystem(embed_complex(system.S, 0), system.lam, system.v_tensor)
+        return residual_device(inner, xt.to(torch.float64).contiguous())
     if isinstance(x, torch.Tensor):
         xt = x.to(system.S.tensor.device, torch.float64).contiguous()
     else:

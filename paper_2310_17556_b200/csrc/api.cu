@@ -879,4 +879,17 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
                   &piv, out_res, st, nullptr);
 }
 
+int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, void* out,
+                     int64_t ldo, void* stream) {
+  if (!ctx || !S || !out || n < 1 || m < 1 || ldS < m || (kind != 0 && kind != 1))
+    return fail(ctx, FS_EINVAL, "bad embed arguments");
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(ctx, FS_EINVAL, "dtype must be FS_F32 or FS_F64");
+  if (ldo < (kind == 0 ? m : 2 * m)) return fail(ctx, FS_EINVAL, "ldo too small");
+  int l = 0;
+  cudaError_t e = fs::embed_complex(dtype == FS_F64, S, n, m, ldS, kind, out, ldo, ctx->num_sms, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "embed_complex");
+  return FS_OK;
+}
+
 }  // extern "C"

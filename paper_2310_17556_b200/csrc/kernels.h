@@ -101,4 +101,8 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
 cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const double* u, const double* w, double lam,
                       double* t, double* z, cudaStream_t st, int* launches);
 
+// ---- complex.cu: kind 0 -> [Re S; Im S] (2n x m), kind 1 -> [[Re, -Im], [Im, Re]] (2n x 2m) ----
+cudaError_t embed_complex(bool f64, const void* S, int64_t n, int64_t m, int64_t ldS, int kind, void* out, int64_t ldo,
+                          int num_sms, cudaStream_t st, int* launches);
+
 }  // namespace fs

@@ -30,7 +30,9 @@ from .core import (
     _check,
     _dt,
     _stream,
+    embed_complex,
     resolve_precision,
+    stack_complex_vector,
 )
 
 DEFAULT_NAIVE_CAP = 4096            # solvers.py:38
@@ -189,20 +191,40 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
                     wall_seconds=perf_counter() - t0, precision=prec)
 
 
-def _not_yet(name: str):
-    raise NotImplementedError(
-        f"{name}: the GPU route is scheduled after the chol hot path (SURVEY §8f-2); "
-        "there is deliberately no CPU fallback in this package")
+def solve_chol_hermitian(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
+                         refine: str | bool | int = "auto") -> Solution:
+    """(S^H S + lam I) x = v for complex scores (solvers.py:209-213), through the real
+    representation rho(S) = [[Re S, -Im S], [Im S, Re S]] (rho(S)^T rho(S) = rho(S^H S)): the plain
+    route on 2n rows and 2m columns solves for [Re x; Im x] (fs_embed_complex + fs_chol_solve)."""
+    if not system.S.is_complex:
+        raise ValueError("solve_chol_hermitian expects complex scores; use solve_chol")
+    t0 = perf_counter()
+    m = system.m
+    emb = embed_complex(system.S, 1)
+    vhat = stack_complex_vector(system.v_tensor, system.S.real_dtype)
+    inner = solve_chol(DampedSystem(emb, system.lam, vhat), meter, precision=precision, refine=refine)
+    xh = inner.x
+    x = torch.complex(xh[:m], xh[m:])
+    xo = x.cpu().numpy() if system.S.host_origin else x
+    return Solution(x=xo, method=Method.CHOL, abs_residual=inner.abs_residual, rel_residual=inner.rel_residual,
+                    wall_seconds=perf_counter() - t0, precision=inner.precision)
 
 
-def solve_chol_hermitian(system, meter=None):
-    """solvers.py:209-213 — complex variants are SURVEY §8f row 3 (not in this build)."""
-    _not_yet("solve_chol_hermitian")
-
-
-def solve_realpart(system, meter=None):
-    """solvers.py:216-240 — complex variants are SURVEY §8f row 3 (not in this build)."""
-    _not_yet("solve_realpart")
+def solve_realpart(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
+                   refine: str | bool | int = "auto") -> Solution:
+    """(Re[S^H S] + lam I) x = v for complex scores and a real v (solvers.py:216-240): the plain
+    route on C = [Re S; Im S] (sr.py:61-70, built on the device by fs_embed_complex); the
+    residual of the real-part operator equals C's plain residual."""
+    if not system.S.is_complex:
+        raise ValueError("real-part variant expects complex scores")
+    if system.v_tensor.is_complex():
+        raise ValueError("real-part variant requires a real right-hand side")
+    t0 = perf_counter()
+    C = embed_complex(system.S, 0)
+    inner = solve_chol(DampedSystem(C, system.lam, system.v_tensor), meter, precision=precision, refine=refine)
+    xo = inner.x.cpu().numpy() if system.S.host_origin else inner.x
+    return Solution(x=xo, method=Method.CHOL, abs_residual=inner.abs_residual, rel_residual=inner.rel_residual,
+                    wall_seconds=perf_counter() - t0, precision=inner.precision)
 
 
 @dataclass(frozen=True)

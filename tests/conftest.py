@@ -35,6 +35,8 @@ def regenerate(case):
     from oracle import fisher_oracle as O
     if case["gen"] == "random_system":
         S, v, lam = O.random_system(case["seed"], case["n"], case["m"], case["lam"])
+    elif case["gen"] == "generate_problem+complex":
+        return O.generate_problem_complex(case["seed"], case["n"], case["m"], case["lam"])
     else:
         S, v, lam = O.generate_problem(case["seed"], case["n"], case["m"], case["lam"])
     if case["gen"].endswith("+f32"):

@@ -102,6 +102,21 @@ def main():
                                    "lam": lam, "S_checksum": checksum(S32),
                                    "rel_residual": sol.rel_residual}
 
+    # --- complex scores (Kind.COMPLEX_GAUSSIAN): Hermitian and real-part variants ---------
+    cx_cases = [("cx_10_16_200", 10, 16, 200, 1e-3), ("cx_11_64_2048", 11, 64, 2048, 1e-2)]
+    for name, seed, n, m, lam in cx_cases:
+        system = fs.generate_problem(seed, n, m, lam, "complex").system
+        sol = fs.solve_chol_hermitian(system)
+        out[f"{name}_herm_x"] = sol.x
+        out[f"{name}_herm_res"] = np.array([sol.abs_residual, sol.rel_residual])
+        rp = fs.DampedSystem(system.S, lam, system.v.real.copy())
+        solr = fs.solve_realpart(rp)
+        out[f"{name}_real_x"] = solr.x
+        out[f"{name}_real_res"] = np.array([solr.abs_residual, solr.rel_residual])
+        manifest["cases"][name] = {"gen": "generate_problem+complex", "seed": seed, "n": n, "m": m, "lam": lam,
+                                   "S_checksum": checksum(system.S.data.real) + checksum(system.S.data.imag),
+                                   "rel_residual": sol.rel_residual}
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
         json.dump(manifest, f, indent=1)

@@ -703,3 +703,61 @@ def test_golden_svd_direct_route(fsb, name, golden, manifest):
     sol = fsb.solve_svd_direct(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="fp64")
     assert sol.method is fsb.Method.SVD_DIRECT
     assert O.rel_err(sol.x, golden[key]) <= 1e-8, O.rel_err(sol.x, golden[key])
+
+
+# ---------------------------------------------------------------- complex variants
+
+CX_CASES = ["cx_10_16_200", "cx_11_64_2048"]
+
+
+@pytest.mark.parametrize("name", CX_CASES)
+def test_golden_complex_variants(fsb, name, golden, manifest):
+    """solve_chol_hermitian / solve_realpart vs the real reference (complex128 -> fp64 mode)."""
+    S, v, lam = regenerate(manifest["cases"][name])
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    h = fsb.solve_chol_hermitian(system)
+    assert np.iscomplexobj(h.x) and h.precision == "fp64"
+    assert O.rel_err(h.x, golden[f"{name}_herm_x"]) <= 1e-10, O.rel_err(h.x, golden[f"{name}_herm_x"])
+    assert h.rel_residual <= 1e-8
+    a, r = fsb.residual(system, h.x, fsb.Variant.HERMITIAN)
+    assert a == h.abs_residual and r == h.rel_residual
+    rsys = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v.real.copy())
+    rp = fsb.solve_realpart(rsys)
+    assert not np.iscomplexobj(rp.x)
+    assert O.rel_err(rp.x, golden[f"{name}_real_x"]) <= 1e-10
+    a, r = fsb.residual(rsys, rp.x, fsb.Variant.REALPART)
+    assert a == rp.abs_residual and r == rp.rel_residual
+
+
+def test_complex64_scores_take_the_tensor_core_path(fsb):
+    """complex64 scores: the real representation is fp32, so the f16x2 Gram applies (same tolerance
+    as real fp32 scores, against the fp64 solve of the identical fp32-rounded complex system)."""
+    S, v, lam = O.generate_problem_complex(12, 100, 6000, 1e-2)
+    S64 = S.astype(np.complex64)
+    v64 = v.astype(np.complex64)
+    sol = fsb.solve_chol_hermitian(fsb.DampedSystem(fsb.ScoreMatrix(S64), lam, v64))
+    assert sol.precision == "f16x2"
+    ref = O.solve_chol_hermitian(S64.astype(np.complex128), v64.astype(np.complex128), lam)
+    assert O.rel_err(sol.x, ref.x) <= 1e-6, O.rel_err(sol.x, ref.x)
+    dev = torch.device("cuda", 0)
+    solt = fsb.solve_realpart(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S64).to(dev)), lam,
+                                               torch.from_numpy(v64.real.copy()).to(dev)))
+    assert isinstance(solt.x, torch.Tensor) and solt.x.is_cuda
+    refr = O.solve_realpart(S64.astype(np.complex128), v64.real.astype(np.float64), lam)
+    assert O.rel_err(solt.x.cpu().numpy(), refr.x) <= 1e-6
+
+
+def test_complex_argument_errors(fsb):
+    S, v, lam = O.generate_problem_complex(13, 4, 30, 1e-2)
+    cs = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    with pytest.raises(ValueError):
+        fsb.solve_chol(cs)                                   # solvers.py:204-205
+    with pytest.raises(ValueError):
+        fsb.solve_realpart(cs)                               # complex v
+    real = fsb.DampedSystem(fsb.ScoreMatrix(S.real.copy()), lam, v.real.copy())
+    with pytest.raises(ValueError):
+        fsb.solve_chol_hermitian(real)
+    with pytest.raises(ValueError):
+        fsb.solve_realpart(real)
+    with pytest.raises(ValueError):
+        fsb.DampedSystem(fsb.ScoreMatrix(S.real.copy()), lam, v)   # real S, complex v

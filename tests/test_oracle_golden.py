@@ -14,8 +14,23 @@ def test_generator_restatement_matches_reference(manifest):
         S, v, lam = regenerate(case)
         cs = case["S_checksum"]
         assert S.shape == (case["n"], case["m"])
-        assert float(S.ravel()[0]) == cs[2] and float(S.ravel()[-1]) == cs[3], name
-        assert abs(float(S.sum()) - cs[0]) <= 1e-9 * max(1.0, abs(cs[1])), name
+        parts = [S.real, S.imag] if np.iscomplexobj(S) else [S]
+        for k, P in enumerate(parts):
+            c = cs[4 * k: 4 * k + 4]
+            assert float(P.ravel()[0]) == c[2] and float(P.ravel()[-1]) == c[3], name
+            assert abs(float(P.sum()) - c[0]) <= 1e-9 * max(1.0, abs(c[1])), name
+
+
+@pytest.mark.parametrize("name", ["cx_10_16_200", "cx_11_64_2048"])
+def test_complex_variants_match_reference(name, golden, manifest):
+    """Oracle restatements of solve_chol_hermitian and solve_realpart vs the real reference."""
+    S, v, lam = regenerate(manifest["cases"][name])
+    h = O.solve_chol_hermitian(S, v, lam)
+    assert O.rel_err(h.x, golden[f"{name}_herm_x"]) <= 1e-12
+    assert abs(h.rel_residual - golden[f"{name}_herm_res"][1]) <= 1e-3 * golden[f"{name}_herm_res"][1] + 1e-18
+    r = O.solve_realpart(S, v.real.copy(), lam)
+    assert O.rel_err(r.x, golden[f"{name}_real_x"]) <= 1e-12
+    assert abs(r.rel_residual - golden[f"{name}_real_res"][1]) <= 1e-3 * golden[f"{name}_real_res"][1] + 1e-18
 
 
 def test_hand_kats(golden):
