@@ -22,6 +22,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace fs {
 namespace {
 
@@ -171,6 +173,41 @@ __device__ void gemm32(const double* A, const double* B, double acc[2][2]) {
   }
 }
 
+// The same 32x32x32 products on the fp64 tensor cores (mma.sync m8n8k4 f64): warp w owns the
+// two 8x8 output tiles (w/2, 2(w%2)) and (w/2, 2(w%2)+1); eight k-steps of 4.
+template <bool kNT>
+__device__ void gemm32_dmma(const double* A, const double* B, double acc[2][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tr = (warp >> 1) * 8, tc = (warp & 1) * 16;
+  const int fr = lane >> 2, fk = lane & 3;
+  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    const double a = A[(tr + fr) * kLd + k0 + fk];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      // B operand (4 x 8, "col"): element (k, col) = kNT ? B[col][k] : B[k][col]
+      const int col = tc + 8 * j + fr;
+      const double b = kNT ? B[col * kLd + k0 + fk] : B[(k0 + fk) * kLd + col];
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(acc[j][0]), "+d"(acc[j][1])
+                   : "d"(a), "d"(b));
+    }
+  }
+}
+
+__device__ void store32_dmma(double* C, const double acc[2][2], double scale, bool accumulate) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = (warp >> 1) * 8 + (lane >> 2), c0 = (warp & 1) * 16 + 2 * (lane & 3);
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double* d = C + r * kLd + c0 + 8 * j + e;
+      *d = (accumulate ? *d : 0.0) + scale * acc[j][e];
+    }
+}
+
 __device__ void store32(double* C, const double acc[2][2], double scale, bool accumulate) {
   const int r = (threadIdx.x >> 4) * 2, c = (threadIdx.x & 15) * 2;
 #pragma unroll
@@ -199,12 +236,12 @@ __device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) 
   __syncthreads();
   if (sfail >= 0) return sfail;
   double acc[2][2];
-  gemm32<true>(&A[32][0], &X[0][0], acc);          // L10 = A10 X00^T
+  gemm32_dmma<true>(&A[32][0], &X[0][0], acc);     // L10 = A10 X00^T
   __syncthreads();
-  store32(&A[32][0], acc, 1.0, false);
+  store32_dmma(&A[32][0], acc, 1.0, false);
   __syncthreads();
-  gemm32<true>(&A[32][0], &A[32][0], acc);         // A11 -= L10 L10^T (reads A10, writes A11)
-  store32(&A[32][32], acc, -1.0, true);
+  gemm32_dmma<true>(&A[32][0], &A[32][0], acc);    // A11 -= L10 L10^T (reads A10, writes A11)
+  store32_dmma(&A[32][32], acc, -1.0, true);
   __syncthreads();
   if (warp == 0) {
     const int f = warp_chol_inv32(&A[32][32], &X[32][32], colbuf);
@@ -212,11 +249,11 @@ __device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) 
   }
   __syncthreads();
   if (sfail >= 0) return sfail;
-  gemm32<false>(&A[32][0], &X[0][0], acc);         // T = L10 X00
-  store32(&T[0][0], acc, 1.0, false);
+  gemm32_dmma<false>(&A[32][0], &X[0][0], acc);    // T = L10 X00
+  store32_dmma(&T[0][0], acc, 1.0, false);
   __syncthreads();
-  gemm32<false>(&X[32][32], &T[0][0], acc);        // X10 = -X11 T
-  store32(&X[32][0], acc, -1.0, false);
+  gemm32_dmma<false>(&X[32][32], &T[0][0], acc);   // X10 = -X11 T
+  store32_dmma(&X[32][0], acc, -1.0, false);
   __syncthreads();
   return -1;
 }
@@ -337,17 +374,15 @@ potrf_first_kernel(double* W, int64_t n, int64_t ld, double* Linv, int64_t* stat
   factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
 }
 
-// Step k: tiles (I, J) of the trailing matrix, k < J <= I < nb, indexed relative to k+1.
-__global__ void __launch_bounds__(kThreads)
-potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double* panel0, double* panel1,
-                  int64_t* status) {
-  extern __shared__ double dsm[];
+// Step k, trailing tile `tile` = (I, J), k < J <= I < nb, indexed relative to k+1 (tile 0 is the
+// next diagonal block, whose CTA also factors it).
+__device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv, double* panel0, double* panel1,
+                          int64_t* status, int tile, double* dsm) {
   double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);              // Linv_kk, later scratch
   double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
   double (*XJ)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
-  if (*(volatile int64_t*)status != 0) return;
   int I, J;
-  tile_coords(blockIdx.x, I, J);
+  tile_coords(tile, I, J);
   I += k + 1;
   J += k + 1;
   const int64_t kc = (int64_t)k * kNB, rI = (int64_t)I * kNB, rJ = (int64_t)J * kNB;
@@ -417,6 +452,71 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double*
   }
 }
 
+__global__ void __launch_bounds__(kThreads)
+potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double* panel0, double* panel1,
+                  int64_t* status) {
+  extern __shared__ double dsm[];
+  if (*(volatile int64_t*)status != 0) return;
+  step_tile(W, n, ld, k, Linv, panel0, panel1, status, blockIdx.x, dsm);
+}
+
+// sense-reversing grid barrier (cooperative launch: all CTAs co-resident)
+__device__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd((unsigned*)gen, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole factorisation in one persistent cooperative kernel: CTA 0 factors block 0, then
+// every step's trailing tiles are spread over the CTAs (tile 0 — the next diagonal block and its
+// factorisation, the critical path — always on CTA 0, whose instruction cache stays warm) with
+// one grid barrier per step instead of a kernel boundary.  Ends with the last panel's copy.
+__global__ void __launch_bounds__(kThreads, 1)
+potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* panel0, double* panel1,
+                        int64_t* status, unsigned* ctl) {
+  extern __shared__ double dsm[];
+  const int nb = (int)((n + kNB - 1) / kNB);
+  if (blockIdx.x == 0 && *(volatile int64_t*)status == 0) {
+    double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
+    double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+    double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
+    factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
+  }
+  grid_barrier(ctl, ctl + 1);
+  int k = 0;
+  for (; k + 1 < nb; ++k) {
+    if (*(volatile int64_t*)status != 0) break;          // uniform: read after the barrier
+    const int t = nb - k - 1, tiles = t * (t + 1) / 2;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      __syncthreads();
+      step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm);
+    }
+    grid_barrier(ctl, ctl + 1);
+  }
+  if (nb >= 2 && *(volatile int64_t*)status == 0) {      // last panel L_{., nb-2} into W
+    const int kk = nb - 2;
+    const int64_t kc = (int64_t)kk * kNB;
+    const double* panel = (kk & 1) ? panel1 : panel0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (n - kc - kNB) * kNB;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t gr = kc + kNB + e / kNB, c = e % kNB;
+      W[gr * ld + kc + c] = panel[gr * kNB + c];
+    }
+  }
+}
+
 __global__ void potrf_tail_kernel(double* W, int64_t n, int64_t ld, int k, const double* panel,
                                   const int64_t* status) {
   // copy the last panel L_{.,k} (rows below block k) into W
@@ -467,7 +567,7 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 
 int64_t potrf_scratch_doubles(int64_t n) {
   const int64_t nb = (n + kNB - 1) / kNB;
-  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */;
+  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 2 /* grid barrier words */;
 }
 
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
@@ -489,6 +589,34 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
     cudaFuncSetAttribute(potrf_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
     cudaFuncSetAttribute(potrf_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
     attr = true;
+  }
+  // one persistent cooperative kernel when the grid fits (it always does: one CTA per SM)
+  {
+    static int coop = -1;
+    static int grid = 0;
+    if (coop < 0) {
+      int dev = 0, sms = 0, per_sm = 0, ok = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(potrf_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, potrf_persistent_kernel, kThreads, 3 * kTileSmem);
+      coop = (ok && per_sm >= 1) ? 1 : 0;
+      grid = sms;
+    }
+    if (coop == 1) {
+      unsigned* ctl = reinterpret_cast<unsigned*>(panel1 + n * kNB);
+      cudaError_t e = cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), st);
+      if (e != cudaSuccess) return e;
+      const int tiles0 = (nb - 1) * nb / 2;
+      const int g = std::max(1, std::min(grid, tiles0));
+      int64_t nn = n, ldd = ldW;
+      void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl};
+      e = cudaLaunchCooperativeKernel((const void*)potrf_persistent_kernel, dim3(g), dim3(kThreads), args,
+                                      3 * kTileSmem, st);
+      if (launches) *launches += 1;
+      return e;
+    }
   }
   int count = 0;
   potrf_first_kernel<<<1, kThreads, 3 * kTileSmem, st>>>(W, n, ldW, Linv, d_status);

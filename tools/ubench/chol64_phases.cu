@@ -17,13 +17,13 @@ __device__ int chol_inv64_t(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]
   long long t1 = clock64();
   if (sfail >= 0) return sfail;
   double acc[2][2];
-  gemm32<true>(&A[32][0], &X[0][0], acc);
+  gemm32_dmma<true>(&A[32][0], &X[0][0], acc);
   __syncthreads();
-  store32(&A[32][0], acc, 1.0, false);
+  store32_dmma(&A[32][0], acc, 1.0, false);
   __syncthreads();
   long long t2 = clock64();
-  gemm32<true>(&A[32][0], &A[32][0], acc);
-  store32(&A[32][32], acc, -1.0, true);
+  gemm32_dmma<true>(&A[32][0], &A[32][0], acc);
+  store32_dmma(&A[32][32], acc, -1.0, true);
   __syncthreads();
   long long t3 = clock64();
   if (warp == 0) {
@@ -33,11 +33,11 @@ __device__ int chol_inv64_t(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]
   __syncthreads();
   long long t4 = clock64();
   if (sfail >= 0) return sfail;
-  gemm32<false>(&A[32][0], &X[0][0], acc);
-  store32(&T[0][0], acc, 1.0, false);
+  gemm32_dmma<false>(&A[32][0], &X[0][0], acc);
+  store32_dmma(&T[0][0], acc, 1.0, false);
   __syncthreads();
-  gemm32<false>(&X[32][32], &T[0][0], acc);
-  store32(&X[32][0], acc, -1.0, false);
+  gemm32_dmma<false>(&X[32][32], &T[0][0], acc);
+  store32_dmma(&X[32][0], acc, -1.0, false);
   __syncthreads();
   long long t5 = clock64();
   if (threadIdx.x == 0) { ts[0] = t1 - t0; ts[1] = t2 - t1; ts[2] = t3 - t2; ts[3] = t4 - t3; ts[4] = t5 - t4; }
