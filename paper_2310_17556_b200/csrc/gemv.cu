@@ -15,6 +15,8 @@
 #include "tiles.cuh"
 
 #include <algorithm>
+#include <stdlib.h>
+#include <string.h>
 
 namespace fs {
 namespace {
@@ -283,7 +285,7 @@ template <typename TS, typename TV>
 __global__ void __launch_bounds__(kCYThreads, 1)
 cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS, const double* __restrict__ z,
                     const TV* __restrict__ v, double lam, int accumulate, double* __restrict__ x,
-                    double* __restrict__ ypart, int y_only) {
+                    double* __restrict__ ypart, int y_only, const __grid_constant__ CUtensorMap pmap, int use_pf) {
   using VT = typename VecOf<TS>::V;
   constexpr int VN1 = VecOf<TS>::N;
   constexpr int VN = VN1 * kCYV;                // columns per thread
@@ -301,8 +303,18 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
     for (int64_t i = threadIdx.x; i < n; i += kCYThreads) zs[i] = z[i];
   for (int64_t i = threadIdx.x; i < (int64_t)kCYCG * P; i += kCYThreads) yacc[i] = 0.0;
   const int64_t panels = (m + CW - 1) / CW;
+  // TMA L2 prefetch of a whole panel: n/256 box requests issued by one thread
+  auto prefetch = [&](int64_t q) {
+    if (!use_pf || threadIdx.x != 0 || q >= panels) return;
+    for (int64_t r = 0; r < n; r += 256)
+      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&pmap), "r"((int)(q * CW)),
+                   "r"((int)r)
+                   : "memory");
+  };
+  prefetch(blockIdx.x);
   __syncthreads();
   for (int64_t q = blockIdx.x; q < panels; q += gridDim.x) {
+    prefetch(q + gridDim.x);            // the next panel streams into L2 while this one is computed
     const int64_t col = q * CW + cg * VN;
     const bool full = col + VN <= m;
     if (y_only) {
@@ -577,14 +589,28 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
   int64_t G = std::min<int64_t>((int64_t)num_sms, std::min(panels, cap));
   if (ypart_rows < G) return cudaErrorInvalidValue;
   const int acc = accumulate ? 1 : 0;
+  CUtensorMap pmap;
+  memset(&pmap, 0, sizeof pmap);
+  // TMA L2 prefetch of the next panel: measured slower (1.0 -> 1.38 ms with 512-B panels: the two
+  // panels per SM overflow L2; 1.15 ms with 256-B panels), so off unless FS_CY_PF=1
+  static const int pf_env = getenv("FS_CY_PF") ? atoi(getenv("FS_CY_PF")) : 0;
+  int use_pf = pf_env;
+  if (use_pf)
+    use_pf = make_tensor_map_2d(&pmap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                S, (uint64_t)m, (uint64_t)n, (uint64_t)ldS * sizeof(TS), cy_cols<TS>(), 256) ==
+                     cudaSuccess
+                 ? 1
+                 : 0;
   if (v_f64) {
     auto kfn = cols_solve_y_kernel<TS, double>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const double*)v, lam, acc, x, ypart, y_only);
+    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const double*)v, lam, acc, x, ypart, y_only, pmap,
+                                               use_pf);
   } else {
     auto kfn = cols_solve_y_kernel<TS, float>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const float*)v, lam, acc, x, ypart, y_only);
+    kfn<<<(unsigned)G, kCYThreads, smem, st>>>(S, n, m, ldS, z, (const float*)v, lam, acc, x, ypart, y_only, pmap,
+                                               use_pf);
   }
   reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(ypart, G, n, n, y);
   if (launches) *launches += 2;

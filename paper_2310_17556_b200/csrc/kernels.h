@@ -1,5 +1,6 @@
 // kernels.h — host-side launchers of the fisher-b200 CUDA kernels (internal, C++).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -104,5 +105,9 @@ cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const 
 // ---- complex.cu: kind 0 -> [Re S; Im S] (2n x m), kind 1 -> [[Re, -Im], [Im, Re]] (2n x 2m) ----
 cudaError_t embed_complex(bool f64, const void* S, int64_t n, int64_t m, int64_t ldS, int kind, void* out, int64_t ldo,
                           int num_sms, cudaStream_t st, int* launches);
+
+// ---- tmap.cu: 2-D tensor map (no swizzle) over a row-major array of `outer` rows ----
+cudaError_t make_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
+                               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace fs

@@ -443,30 +443,12 @@ size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
 }
 
 namespace {
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 // S_t16 viewed as a 2-D fp16 tensor of 128-byte rows: box = one (K-block, row block) hi+lo pair
 // (256 rows), no swizzle (the tiles are stored in the swizzled smem image already).
 cudaError_t st16_tensor_map(CUtensorMap* map, const uint8_t* St16, int64_t n, int64_t m) {
-  static EncodeTiledFn enc = nullptr;
-  if (!enc) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
-    enc = (EncodeTiledFn)fn;
-  }
-  const cuuint64_t rows = (cuuint64_t)tiles_nb(n) * tiles16_kb(m) * 2 * kTileRows;
-  const cuuint64_t gdim[2] = {(cuuint64_t)kTile16Cols, rows};
-  const cuuint64_t gstride[1] = {(cuuint64_t)kTile16Cols * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kTile16Cols, (cuuint32_t)(2 * kTileRows)};
-  const cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint8_t*>(St16), gdim, gstride, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+  const uint64_t rows = (uint64_t)tiles_nb(n) * tiles16_kb(m) * 2 * kTileRows;
+  return make_tensor_map_2d(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, St16, kTile16Cols, rows, kTile16Cols * 2,
+                            kTile16Cols, 2 * kTileRows);
 }
 
 template <bool kF16>
