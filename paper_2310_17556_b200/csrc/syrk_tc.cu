@@ -96,6 +96,13 @@ FS_DEVINL float tf32_lo(uint32_t xb) {
 // a free TMEM buffer, and the total (one row per cluster), printed by the host after the launch
 __device__ unsigned long long g_syrk_wait[74 * 4];
 
+// K progress of each cluster (split mode with one unit per cluster): the clusters that stream the
+// same K range (same split q, different pair tiles sharing row blocks) are kept within kLag
+// K-blocks of each other so that each row block's tiles are fetched from DRAM ~once and then hit
+// in L2 (FS_SYRK_DBG bit 512 enables it: an experiment)
+__device__ int g_syrk_prog[128];
+constexpr int kSyncEvery = 16, kLag = 48;
+
 struct Ring {  // stage index + mbarrier phase of a circular buffer
   int s = 0;
   uint32_t ph = 0;
@@ -162,7 +169,18 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         const bool diag = pp == qq;                       // A == B: one tile
         const uint32_t bytes = (diag ? 1 : 2) * kBlkBytes;
         const int kb0 = q * KC, nk = min(KC, KB - kb0);
+        const bool lockstep = (dbg & 512) && units <= nclusters && crank == 0;
         for (int k = 0; k < nk; ++k) {
+          if (lockstep && (k % kSyncEvery) == 0) {
+            volatile int* prog = g_syrk_prog;
+            prog[cluster] = k;
+            for (int t2 = 0; t2 < tiles; ++t2) {
+              const int c2 = t2 * P + q;
+              if (c2 == cluster) continue;
+              while (prog[c2] < k - kLag) {
+              }
+            }
+          }
           const size_t krow = (size_t)(kb_base + kb0 + k) * nbt;
           // L2 bulk prefetch kPfDist K-blocks ahead: off by default (measured neutral for TF32X3 and
           // ~5% slower for F16X2, tools/syrk_ablate.sh); FS_SYRK_DBG bit 64 re-enables it
@@ -189,6 +207,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           }
           rr.next(kRawS);
         }
+        if (lockstep) g_syrk_prog[cluster] = 1 << 30;   // done: never holds anyone back
       }
     } else if (warp == 1 && lane == 0 && crank == 0) {
       // ======================= MMA issuer (leader CTA) =======================
@@ -465,6 +484,11 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
     attr_set = true;
   }
   static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;  // ablation experiments only
+  if (dbg & 512) {
+    void* prog = nullptr;
+    cudaGetSymbolAddress(&prog, g_syrk_prog);
+    cudaMemsetAsync(prog, 0, sizeof(int) * 128, st);
+  }
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if (kF16) {
