@@ -158,22 +158,7 @@ __device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbu
   return fail;
 }
 
-// C = A B^T (kNT) or A B on 32x32 windows (stride kLd), all 256 threads, 2x2 outputs each.
-template <bool kNT>
-__device__ void gemm32(const double* A, const double* B, double acc[2][2]) {
-  const int r = (threadIdx.x >> 4) * 2, c = (threadIdx.x & 15) * 2;
-  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
-#pragma unroll 8
-  for (int p = 0; p < 32; ++p) {
-    const double a0 = A[r * kLd + p], a1 = A[(r + 1) * kLd + p];
-    const double b0 = kNT ? B[c * kLd + p] : B[p * kLd + c];
-    const double b1 = kNT ? B[(c + 1) * kLd + p] : B[p * kLd + c + 1];
-    acc[0][0] = fma(a0, b0, acc[0][0]); acc[0][1] = fma(a0, b1, acc[0][1]);
-    acc[1][0] = fma(a1, b0, acc[1][0]); acc[1][1] = fma(a1, b1, acc[1][1]);
-  }
-}
-
-// The same 32x32x32 products on the fp64 tensor cores (mma.sync m8n8k4 f64): warp w owns the
+// C = A B^T (kNT) or A B on 32x32 windows (stride kLd) on the fp64 tensor cores (mma.sync m8n8k4 f64): warp w owns the
 // two 8x8 output tiles (w/2, 2(w%2)) and (w/2, 2(w%2)+1); eight k-steps of 4.
 template <bool kNT>
 __device__ void gemm32_dmma(const double* A, const double* B, double acc[2][2]) {
@@ -208,16 +193,6 @@ __device__ void store32_dmma(double* C, const double acc[2][2], double scale, bo
     }
 }
 
-__device__ void store32(double* C, const double acc[2][2], double scale, bool accumulate) {
-  const int r = (threadIdx.x >> 4) * 2, c = (threadIdx.x & 15) * 2;
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      double* d = C + (r + i) * kLd + c + j;
-      *d = (accumulate ? *d : 0.0) + scale * acc[i][j];
-    }
-}
 
 // A (64x64 smem, identity-padded lower) = L L^T in place, X = L^-1; T scratch.  Returns the
 // first failing local pivot or -1 (block-uniform).
@@ -259,23 +234,34 @@ __device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) 
 }
 
 // C (64x64, smem) = A (64x64 smem) * B^T (64x64 smem); each thread a 4x4 sub-block.
+// C (64x64) = A (64x64 smem) * B^T (64x64 smem) on the fp64 tensor cores (mma.sync m8n8k4 f64).
+// Warp w owns rows [16 (w/2), +16) x cols [32 (w%2), +32): 2 x 4 tiles of 8x8.  The thread's 16
+// results: acc[i][j] is element (frag_row(i), frag_col(i, j)).
+FS_DEVINL int frag_row(int i) { return ((threadIdx.x >> 5) >> 1) * 16 + 8 * (i >> 1) + ((threadIdx.x & 31) >> 2); }
+FS_DEVINL int frag_col(int i, int j) {
+  return ((threadIdx.x >> 5) & 1) * 32 + 8 * j + 2 * (threadIdx.x & 3) + (i & 1);
+}
 __device__ void gemm_nt(const double (*A)[kLd], const double (*B)[kLd], double acc[4][4]) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32, fr = lane >> 2, fk = lane & 3;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-#pragma unroll 8
-  for (int p = 0; p < kNB; ++p) {
-    double a[4], b[4];
+#pragma unroll 4
+  for (int k0 = 0; k0 < kNB; k0 += 4) {
+    double a[2], b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = A[ty + 16 * i][p];
+    for (int t = 0; t < 2; ++t) a[t] = A[wr + 8 * t + fr][k0 + fk];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = B[tx + 16 * j][p];
+    for (int t = 0; t < 4; ++t) b[t] = B[wc + 8 * t + fr][k0 + fk];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int t = 0; t < 2; ++t)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      for (int u = 0; u < 4; ++u)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(acc[2 * t][u]), "+d"(acc[2 * t + 1][u])
+                     : "d"(a[t]), "d"(b[u]));
   }
 }
 
@@ -406,13 +392,12 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
   gemm_nt(XI, Lk, accI);
   if (I != J) gemm_nt(XJ, Lk, accJ);
   __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      XI[ty + 16 * i][tx + 16 * j] = accI[i][j];
-      if (I != J) XJ[ty + 16 * i][tx + 16 * j] = accJ[i][j];
+      XI[frag_row(i)][frag_col(i, j)] = accI[i][j];
+      if (I != J) XJ[frag_row(i)][frag_col(i, j)] = accJ[i][j];
     }
   __syncthreads();
   if (J == k + 1) {   // store the panel L_Ik
@@ -428,7 +413,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int64_t gi = rI + ty + 16 * i, gj = rJ + tx + 16 * j;
+      const int64_t gi = rI + frag_row(i), gj = rJ + frag_col(i, j);
       old[i][j] = (gi < n && gj <= gi) ? W[gi * ld + gj] : 0.0;
     }
   double acc[4][4];
@@ -437,7 +422,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int64_t gi = rI + ty + 16 * i, gj = rJ + tx + 16 * j;
+      const int64_t gi = rI + frag_row(i), gj = rJ + frag_col(i, j);
       acc[i][j] = old[i][j] - acc[i][j];
       if (gi < n && gj <= gi) W[gi * ld + gj] = acc[i][j];
     }
@@ -447,7 +432,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) Lk[ty + 16 * i][tx + 16 * j] = acc[i][j];
+      for (int j = 0; j < 4; ++j) Lk[frag_row(i)][frag_col(i, j)] = acc[i][j];
     factor_diag(W, n, ld, I, status, Linv, Lk, XI, XJ, true);
   }
 }
