@@ -203,7 +203,7 @@ def run_b200(args, rank, world, local):
 
     import paper_2310_17556_b200 as fsb
     from paper_2310_17556_b200 import _lib
-    from paper_2310_17556_b200.distributed import CudaStageOps, column_shard, sharded_solve_chol
+    from paper_2310_17556_b200.distributed import column_shard, sharded_solve_chol_fused
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
@@ -231,8 +231,9 @@ def run_b200(args, rank, world, local):
             for k, val in ctx.stage_ms().items():
                 stage_acc[k].append(val)
             return sol.rel_residual
-        ops = CudaStageOps(device, n, m_local, args.precision, dtype, ctx=ctx)
-        sol = sharded_solve_chol(S, v, lam, n, ops, lambda buf: dist.all_reduce(buf))
+        sol = sharded_solve_chol_fused(S, v, lam, precision=args.precision)
+        for k, val in ctx.stage_ms().items():
+            stage_acc[k].append(val)
         return sol.rel_residual
 
     for _ in range(args.warmup):

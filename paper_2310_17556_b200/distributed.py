@@ -167,3 +167,56 @@ def torch_allreduce(buf) -> None:
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(buf)
+
+
+class _DeviceBuffer:
+    """Zero-copy torch view of a raw device pointer (the C ABI hands its all-reduce buffers out as
+    plain pointers): __cuda_array_interface__ import, no allocation."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": (int(count),), "typestr": "<f8",
+                                         "version": 3, "strides": None}
+
+
+def nccl_allreduce_fn(device: torch.device, group=None):
+    """An fs_allreduce_fn for fs_chol_solve: sums `count` doubles at `buf` across the ranks of
+    `group` with torch.distributed (NCCL over NVLink/NVSwitch on GPUs), in place, ordered on the
+    solve stream (the call is issued on torch's current stream, which is the stream passed to
+    fs_chol_solve).  Returns 0 on success."""
+    import torch.distributed as dist
+
+    def fn(buf, count, user, stream):
+        try:
+            t = torch.as_tensor(_DeviceBuffer(buf, count), device=device)
+            dist.all_reduce(t, group=group)
+            return 0
+        except Exception:          # surfaced by fs_chol_solve as FS_ECUDA with its message
+            return 1
+
+    return _lib.ALLREDUCE_FN(fn)
+
+
+def sharded_solve_chol_fused(S_local: torch.Tensor, v_local: torch.Tensor, lam: float, *, precision: str = "auto",
+                             diagnostics: bool = True, refine: int = 0, group=None) -> ShardedSolution:
+    """The column-sharded solve through ONE fs_chol_solve call per rank: the same fused kernels as
+    the single-GPU path on the local shard (retile + u, tcgen05 SYRK, x + y pass, residual), with
+    the C ABI's all-reduce callback doing the three exchanges ([G | u], y, the norms) over NCCL."""
+    from .core import _to_device_tensor
+    dev = S_local.device
+    S = _to_device_tensor(S_local, "score matrix", dev)        # aligned rows (no copy when already)
+    v = v_local.to(dev).to(S.dtype).contiguous()
+    n, m = int(S.shape[0]), int(S.shape[1])
+    prec = resolve_precision(precision, S.dtype)
+    ctx = _lib.context_for(dev.index, n, m)
+    x = torch.empty(m, dtype=torch.float64, device=dev)
+    piv = ctypes.c_int64(-1)
+    res = (ctypes.c_double * 2)(float("nan"), float("nan"))
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (refine << 8)) if refine else 0)
+    cb = nccl_allreduce_fn(dev, group)
+    rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0), v.data_ptr(),
+                               float(lam), x.data_ptr(), cb, None, flags, REFINE_ABOVE_REL, ctypes.byref(piv), res,
+                               _stream(dev))
+    if rc == _lib.FS_NOT_PD:
+        raise FactorizationError(f"Gram matrix is not positive definite at pivot {piv.value}", pivot=int(piv.value))
+    _check(ctx, rc, "fs_chol_solve")
+    return ShardedSolution(x_local=x, abs_residual=float(res[0]), rel_residual=float(res[1]), refined=refine > 0)

@@ -761,3 +761,29 @@ def test_complex_argument_errors(fsb):
         fsb.solve_realpart(real)
     with pytest.raises(ValueError):
         fsb.DampedSystem(fsb.ScoreMatrix(S.real.copy()), lam, v)   # real S, complex v
+
+
+def test_fused_sharded_entry_with_nccl_callback(fsb):
+    """The multi-GPU entry (one fs_chol_solve per rank, NCCL all-reduce through the C-ABI callback
+    on zero-copy views of the library's buffers) on a one-rank NCCL group: same x as solve_chol."""
+    import os
+    import torch.distributed as dist
+    from paper_2310_17556_b200.distributed import sharded_solve_chol_fused
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dev = torch.device("cuda", 0)
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        created = True
+    try:
+        S, v, lam = O.generate_problem(61, 128, 20000, 1e-3)
+        St = torch.from_numpy(S.astype(np.float32)).to(dev)
+        vt = torch.from_numpy(v.astype(np.float32)).to(dev)
+        a = sharded_solve_chol_fused(St, vt, lam, precision="f16x2")
+        b = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(St), lam, vt), precision="f16x2")
+        assert torch.equal(a.x_local, b.x)
+        assert a.rel_residual == b.rel_residual
+    finally:
+        if created:
+            dist.destroy_process_group()
