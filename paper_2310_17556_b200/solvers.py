@@ -107,9 +107,13 @@ class _PinnedOut:
                 return arr
         if len(slots) >= self.cap:
             return np.empty(m, dtype=np.float64)
-        t = torch.empty(m, dtype=torch.float64, pin_memory=True)
-        arr = t.numpy()
-        slots.append([t, weakref.ref(arr)])
+        # allocate two at a time: a caller that keeps the previous result while solving again
+        # (x = solve(...) in a loop) alternates between them without a cudaHostAlloc per call
+        for _ in range(2 if not slots else 1):
+            slots.append([torch.empty(m, dtype=torch.float64, pin_memory=True), None])
+        slot = slots[-1]
+        arr = slot[0].numpy()
+        slot[1] = weakref.ref(arr)
         return arr
 
 
