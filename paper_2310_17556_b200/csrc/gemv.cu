@@ -662,100 +662,116 @@ __global__ void row_scale_kernel(const float* __restrict__ S, int64_t n, int64_t
   }
 }
 
-// Column range [c0, c1) of all rows (c0 a multiple of 1024): the F16X2 planes of S_t16 and the
-// u = S w partials of the column chunks (fp32 products, like gemv_rows_retile).  Each lane
-// moves 8 consecutive floats = one 16-byte fp16 chunk per plane; 8 lanes write one full
-// 128-byte tile row of each plane.
-constexpr int kR16Unroll = 4;   // 4 x 256 columns = one 1024-column chunk
-__global__ void __launch_bounds__(kRowThreads, 2)
-retile16_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS, const float* __restrict__ w,
-                double* __restrict__ partials, uint8_t* __restrict__ St, const float* __restrict__ scale,
-                int has_w, int vec_ok, int* __restrict__ flags, int64_t cb0) {
+// Column range [c0, c1) of all rows (c0 a multiple of 1024): the F16X2 planes of S_t16 (tiles.cuh)
+// and the u = S w partials of the 1024-column chunks.  CTA = (128-row block, 1024-column chunk =
+// 16 K-blocks);
+// warp w owns K-blocks w and w+8.  A warp instruction covers 4 consecutive tile rows of one
+// K-block (lane -> row 4g + lane/8, 16-byte chunk lane%8), so each store writes 512 contiguous
+// bytes of a tile (a row-per-warp mapping scatters 128-byte rows over 4 tiles: 1.60 vs 1.33 ms
+// for the pass at the headline).  u partials: per-warp per-row sums in shared memory, added in warp order.
+constexpr int kRTRows = 128;
+constexpr int kRTThreads = 256;
+constexpr int kRTGroup = 4;                       // 4-row groups per unrolled batch (16 rows)
+__global__ void __launch_bounds__(kRTThreads, 3)
+retile16_tiles_kernel(const float* __restrict__ S, int64_t n, int64_t m, int64_t ldS, const float* __restrict__ w,
+                      double* __restrict__ partials, uint8_t* __restrict__ St, const float* __restrict__ scale,
+                      int has_w, int vec_ok, int* __restrict__ flags, int64_t cb0, int64_t ncb) {
   constexpr int CW = 1024;
+  __shared__ float usm[kRTThreads / 32][kRTRows];
+  __shared__ float ssm[kRTRows];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t cb = cb0 + blockIdx.x;
-  const int64_t c0 = cb * CW;
   const int64_t nb = tiles_nb(n), KB = tiles16_kb(m);
-  __shared__ float4 wsm[CW / 4];
-  for (int t = threadIdx.x; t < CW / 4; t += kRowThreads) {
-    float a[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t c = c0 + (int64_t)t * 4 + e;
-      a[e] = (has_w && c < m) ? w[c] : 0.f;
-    }
-    wsm[t] = make_float4(a[0], a[1], a[2], a[3]);
+  const int64_t cb = cb0 + blockIdx.x % ncb;
+  const int64_t rb = blockIdx.x / ncb;
+  for (int t = threadIdx.x; t < kRTRows; t += kRTThreads) {
+    const int64_t i = rb * kRTRows + t;
+    ssm[t] = i < n ? scale[i] : 1.f;
   }
+  for (int t = threadIdx.x; t < (kRTThreads / 32) * kRTRows; t += kRTThreads) (&usm[0][0])[t] = 0.f;
   __syncthreads();
-  const bool full = vec_ok && c0 + CW <= m;
-  const int chunk = lane & 7;
-  const int64_t rz = nb * kTileRows;
+  const int j = lane & 7, rl = lane >> 3;        // chunk in the tile row, row within the 4-row group
   bool bad = false, ovf = false;
-  for (int64_t i = warp; i < rz; i += kRowThreads / kWarp) {
-    float4 buf[kR16Unroll][2];
-    if (i < n) {
-      const float* row = S + i * ldS + c0;
-      if (full) {
-#pragma unroll
-        for (int u = 0; u < kR16Unroll; ++u) {
-          buf[u][0] = ld_stream(reinterpret_cast<const float4*>(row + u * 256 + lane * 8));
-          buf[u][1] = ld_stream(reinterpret_cast<const float4*>(row + u * 256 + lane * 8 + 4));
-        }
+  for (int q = 0; q < 2; ++q) {
+    const int64_t kb = cb * (CW / 64) + warp + 8 * q;
+    if (kb >= KB) continue;
+    const int64_t c = kb * 64 + j * 8;            // this lane's 8 columns
+    float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
+    if (has_w) {
+      if (c + 8 <= m) {
+        w0 = __ldg(reinterpret_cast<const float4*>(w + c));
+        w1 = __ldg(reinterpret_cast<const float4*>(w + c) + 1);
       } else {
+        float a[8];
 #pragma unroll
-        for (int u = 0; u < kR16Unroll; ++u) {
+        for (int e = 0; e < 8; ++e) a[e] = (c + e < m) ? __ldg(w + c + e) : 0.f;
+        w0 = make_float4(a[0], a[1], a[2], a[3]);
+        w1 = make_float4(a[4], a[5], a[6], a[7]);
+      }
+    }
+    uint8_t* tile = St + ((size_t)kb * nb + rb) * 2 * kTileBytes;     // hi tile, lo tile follows
+    const bool fullc = vec_ok && c + 8 <= m;
+    for (int g0 = 0; g0 < kRTRows / 4; g0 += kRTGroup) {
+      float4 buf[kRTGroup][2];
+#pragma unroll
+      for (int u = 0; u < kRTGroup; ++u) {
+        const int r = (g0 + u) * 4 + rl;
+        const int64_t i = rb * kRTRows + r;
+        const float* row = S + i * ldS + c;
+        if (i < n && fullc) {
+          buf[u][0] = ld_stream(reinterpret_cast<const float4*>(row));
+          buf[u][1] = ld_stream(reinterpret_cast<const float4*>(row) + 1);
+        } else {
           float a[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int64_t c = (int64_t)u * 256 + lane * 8 + e;
-            a[e] = (c0 + c < m) ? __ldg(row + c) : 0.f;
-          }
+          for (int e = 0; e < 8; ++e) a[e] = (i < n && c + e < m) ? __ldg(row + e) : 0.f;
           buf[u][0] = make_float4(a[0], a[1], a[2], a[3]);
           buf[u][1] = make_float4(a[4], a[5], a[6], a[7]);
         }
       }
-    } else {
 #pragma unroll
-      for (int u = 0; u < kR16Unroll; ++u) buf[u][0] = buf[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const float sc = i < n ? scale[i] : 1.f;
+      for (int u = 0; u < kRTGroup; ++u) {
+        const int r = (g0 + u) * 4 + rl;
+        const float sc = ssm[r];
+        const float xs[8] = {buf[u][0].x, buf[u][0].y, buf[u][0].z, buf[u][0].w,
+                             buf[u][1].x, buf[u][1].y, buf[u][1].z, buf[u][1].w};
+        __align__(16) __half hi[8], lo[8];
 #pragma unroll
-    for (int u = 0; u < kR16Unroll; ++u) {
-      const int64_t kb = (c0 >> 6) + u * 4 + (lane >> 3);
-      const float xs[8] = {buf[u][0].x, buf[u][0].y, buf[u][0].z, buf[u][0].w,
-                           buf[u][1].x, buf[u][1].y, buf[u][1].z, buf[u][1].w};
-      __align__(16) __half hi[8], lo[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        bad |= !isfinite(xs[e]);
-        const float y = xs[e] * sc;
-        hi[e] = __float2half_rn(y);
-        const float hf = __half2float(hi[e]);
-        ovf |= isinf(hf);
-        lo[e] = __float2half_rn(y - hf);
+        for (int e = 0; e < 8; ++e) {
+          bad |= !isfinite(xs[e]);
+          const float y = xs[e] * sc;
+          hi[e] = __float2half_rn(y);
+          const float hf = __half2float(hi[e]);
+          ovf |= isinf(hf);
+          lo[e] = __float2half_rn(y - hf);
+        }
+        const int off = r * 128 + ((j ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(tile + off) = *reinterpret_cast<const uint4*>(hi);
+        *reinterpret_cast<uint4*>(tile + kTileBytes + off) = *reinterpret_cast<const uint4*>(lo);
+        if (has_w) {
+          float p = 0.f;
+          p = fmaf(xs[0], w0.x, p); p = fmaf(xs[1], w0.y, p); p = fmaf(xs[2], w0.z, p); p = fmaf(xs[3], w0.w, p);
+          p = fmaf(xs[4], w1.x, p); p = fmaf(xs[5], w1.y, p); p = fmaf(xs[6], w1.z, p); p = fmaf(xs[7], w1.w, p);
+          p += __shfl_xor_sync(0xffffffffu, p, 1);     // the row's 8 lanes (64 columns)
+          p += __shfl_xor_sync(0xffffffffu, p, 2);
+          p += __shfl_xor_sync(0xffffffffu, p, 4);
+          if (j == 0) usm[warp][r] += p;
+        }
       }
-      if (kb < KB) {
-        *reinterpret_cast<uint4*>(St + tile16_chunk_offset(nb, kb, i, chunk, 0)) = *reinterpret_cast<const uint4*>(hi);
-        *reinterpret_cast<uint4*>(St + tile16_chunk_offset(nb, kb, i, chunk, 1)) = *reinterpret_cast<const uint4*>(lo);
-      }
-    }
-    if (i < n && has_w) {
-      float acc = 0.f;
-#pragma unroll
-      for (int u = 0; u < kR16Unroll; ++u) {
-        const float4 w0 = wsm[u * 64 + lane * 2], w1 = wsm[u * 64 + lane * 2 + 1];
-        acc = fmaf(buf[u][0].x, w0.x, acc); acc = fmaf(buf[u][0].y, w0.y, acc);
-        acc = fmaf(buf[u][0].z, w0.z, acc); acc = fmaf(buf[u][0].w, w0.w, acc);
-        acc = fmaf(buf[u][1].x, w1.x, acc); acc = fmaf(buf[u][1].y, w1.y, acc);
-        acc = fmaf(buf[u][1].z, w1.z, acc); acc = fmaf(buf[u][1].w, w1.w, acc);
-      }
-      const double s = warp_sum((double)acc);
-      if (lane == 0) partials[cb * n + i] = s;
     }
   }
   if (flags) {
     const unsigned bb = __ballot_sync(0xffffffffu, bad), bo = __ballot_sync(0xffffffffu, ovf);
     if (lane == 0 && (bb | bo)) atomicOr(flags, (bb ? 1 : 0) | (bo ? 2 : 0));
+  }
+  if (has_w) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < kRTRows; t += kRTThreads) {
+      const int64_t i = rb * kRTRows + t;
+      double sum = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < kRTThreads / 32; ++w2) sum += (double)usm[w2][t];
+      if (i < n) partials[cb * n + i] = sum;
+    }
   }
 }
 
@@ -835,8 +851,9 @@ cudaError_t retile16_cols(const float* S, int64_t n, int64_t m, int64_t ldS, con
   const int64_t cb0 = c0 / CW, cb1 = (c1 + CW - 1) / CW;
   if (cb1 <= cb0) return cudaSuccess;
   const int vec_ok = aligned16(S, ldS, 4) ? 1 : 0;
-  retile16_kernel<<<(unsigned)(cb1 - cb0), kRowThreads, 0, st>>>(S, n, m, ldS, w, partials, St, scale, w != nullptr,
-                                                                  vec_ok, flags, cb0);
+  const int64_t ncb = cb1 - cb0;
+  retile16_tiles_kernel<<<(unsigned)(ncb * tiles_nb(n)), kRTThreads, 0, st>>>(S, n, m, ldS, w, partials, St, scale,
+                                                                                w != nullptr, vec_ok, flags, cb0, ncb);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

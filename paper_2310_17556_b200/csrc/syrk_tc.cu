@@ -438,7 +438,7 @@ Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1,
   p.KC = (p.KB + p.P - 1) / p.P;          // K-blocks per split, contiguous in m
   p.P = (p.KB + p.KC - 1) / p.KC;          // every split non-empty
   p.clusters = std::min(p.tiles * p.P, max_clusters);
-  p.D = kDrainBlocks;
+  p.D = getenv("FS_SYRK_DRAIN") ? atoi(getenv("FS_SYRK_DRAIN")) : kDrainBlocks;
   p.direct = p.P == 1;
   return p;
 }
