@@ -266,10 +266,18 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
   prof_mark(ctx, FS_PROF_ALLREDUCE, st);
   // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
   if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
-  if ((rc = fs_potrf_async(ctx, ctx->d_W, n, n, stream))) return rc;
-  prof_mark(ctx, FS_PROF_POTRF, st);
-  FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
+  // L = chol(W) with the TRSV pair z = L^-T L^-1 u fused into the same persistent kernel
+  bool solved = false;
   {
+    FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
+    int l = 0;
+    cudaError_t e = fs::potrf_lower(ctx->d_W, n, n, ctx->d_status, ctx->d_potrf, st, &l, u, ctx->d_z, &solved);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "potrf");
+  }
+  prof_mark(ctx, FS_PROF_POTRF, st);
+  if (!solved) {
+    FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
     int l = 0;
     cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
     ctx->launches += l;

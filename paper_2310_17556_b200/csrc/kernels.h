@@ -84,8 +84,11 @@ cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W
 // scratch = potrf_scratch_doubles(n) doubles; on return it starts with the inverted 64x64
 // diagonal blocks of L (Linv), which trsv_pair consumes
 int64_t potrf_scratch_doubles(int64_t n);
+// u / z (optional): the TRSV pair z = L^-T L^-1 u fused into the factorisation's persistent
+// kernel (*solved = true when it ran; otherwise call trsv_pair)
 cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch,
-                        cudaStream_t st, int* launches);
+                        cudaStream_t st, int* launches, const double* u = nullptr, double* z = nullptr,
+                        bool* solved = nullptr);
 cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* scratch, cudaStream_t st,
                                int* launches);
 cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,

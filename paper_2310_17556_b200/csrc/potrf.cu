@@ -360,10 +360,30 @@ potrf_first_kernel(double* W, int64_t n, int64_t ld, double* Linv, int64_t* stat
   factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
 }
 
+// out[o] = sum_k M(o, k) x[k] for a 64 x 64 block (M(o, k) = M[o * ld + k], or M[k * ld + o] when
+// kTrans), all 256 threads: 4 threads per output, 16 unrolled independent loads each, shuffle
+// reduction (fixed order).  x in shared memory; out written by the q == 0 lane (if out != null).
+template <bool kTrans>
+__device__ double gemv64(const double* __restrict__ M, int64_t ld, const double* x, int rows_valid) {
+  const int o = threadIdx.x >> 2, q = threadIdx.x & 3;
+  double v[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const int k = q * 16 + t;
+    v[t] = (kTrans ? k : o) < rows_valid ? (kTrans ? M[(int64_t)k * ld + o] : M[(int64_t)o * ld + k]) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) acc = fma(v[t], x[q * 16 + t], acc);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  return acc;                                   // valid in the q == 0 lane of each output
+}
+
 // Step k, trailing tile `tile` = (I, J), k < J <= I < nb, indexed relative to k+1 (tile 0 is the
 // next diagonal block, whose CTA also factors it).
 __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv, double* panel0, double* panel1,
-                          int64_t* status, int tile, double* dsm) {
+                          int64_t* status, int tile, double* dsm, double* ut = nullptr, double* tb = nullptr) {
   double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);              // Linv_kk, later scratch
   double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
   double (*XJ)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
@@ -405,6 +425,27 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
       const int r = e >> 6, c = e & 63;
       const int64_t gr = rI + r;
       if (gr < n) pan_cur[gr * kNB + c] = XI[r][c];
+    }
+    if (ut) {
+      // fused forward substitution (L t = u, right-looking): t_k = Linv_kk ut_k (ut_k is final:
+      // its last update came from step k-1), then ut_I -= L_Ik t_k for this CTA's row block
+      __shared__ double uk[kNB], tk[kNB];
+      if (threadIdx.x < kNB) uk[threadIdx.x] = (kc + threadIdx.x < n) ? ut[kc + threadIdx.x] : 0.0;
+      __syncthreads();
+      {
+        const double acc = gemv64<false>(&Lk[0][0], kLd, uk, kNB);
+        const int o = threadIdx.x >> 2;
+        if ((threadIdx.x & 3) == 0) {
+          tk[o] = acc;
+          if (I == k + 1 && kc + o < n) tb[kc + o] = acc;   // the diagonal CTA records t_k
+        }
+      }
+      __syncthreads();
+      {
+        const double acc = gemv64<false>(&XI[0][0], kLd, tk, kNB);
+        const int o = threadIdx.x >> 2;
+        if ((threadIdx.x & 3) == 0 && rI + o < n) ut[rI + o] -= acc;
+      }
     }
   }
   // A_IJ -= X_I X_J^T (old values loaded up front, the GEMM overlaps their latency)
@@ -470,9 +511,13 @@ __device__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
 // one grid barrier per step instead of a kernel boundary.  Ends with the last panel's copy.
 __global__ void __launch_bounds__(kThreads, 1)
 potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* panel0, double* panel1,
-                        int64_t* status, unsigned* ctl) {
+                        int64_t* status, unsigned* ctl, const double* __restrict__ u, double* ut, double* tb,
+                        double* __restrict__ z) {
   extern __shared__ double dsm[];
   const int nb = (int)((n + kNB - 1) / kNB);
+  if (u)                                                  // working right-hand side of L t = u
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+      ut[e] = u[e];
   if (blockIdx.x == 0 && *(volatile int64_t*)status == 0) {
     double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
     double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
@@ -486,10 +531,11 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
     const int t = nb - k - 1, tiles = t * (t + 1) / 2;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       __syncthreads();
-      step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm);
+      step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm, u ? ut : nullptr, tb);
     }
     grid_barrier(ctl, ctl + 1);
   }
+  const bool solve = u && *(volatile int64_t*)status == 0;
   if (nb >= 2 && *(volatile int64_t*)status == 0) {      // last panel L_{., nb-2} into W
     const int kk = nb - 2;
     const int64_t kc = (int64_t)kk * kNB;
@@ -499,6 +545,41 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
       const int64_t gr = kc + kNB + e / kNB, c = e % kNB;
       W[gr * ld + kc + c] = panel[gr * kNB + c];
     }
+  }
+  if (!solve) return;
+  __shared__ double zb[kNB], xb[kNB];
+  if (blockIdx.x == 0) {
+    // last block of the forward solve: t_{nb-1} = Linv ut_{nb-1}
+    const int64_t kc = (int64_t)(nb - 1) * kNB;
+    if (threadIdx.x < kNB) xb[threadIdx.x] = (kc + threadIdx.x < n) ? ut[kc + threadIdx.x] : 0.0;
+    __syncthreads();
+    const double acc = gemv64<false>(Linv + (size_t)(nb - 1) * kNB * kNB, kNB, xb, kNB);
+    const int o = threadIdx.x >> 2;
+    if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = acc;
+  }
+  grid_barrier(ctl, ctl + 1);                             // tb = t complete, W holds all of L
+  // backward solve L^T z = t, right-looking: z_B = Linv_BB^T tb_B (every CTA, redundantly), then
+  // tb_C -= L_BC^T z_B for C < B spread over the CTAs; one grid barrier per block
+  for (int B = nb - 1; B >= 0; --B) {
+    const int64_t rB = (int64_t)B * kNB;
+    if (B >= (int)blockIdx.x || blockIdx.x == 0) {        // CTAs with work this step (C < B) and CTA 0
+      if (threadIdx.x < kNB) xb[threadIdx.x] = (rB + threadIdx.x < n) ? tb[rB + threadIdx.x] : 0.0;
+      __syncthreads();
+      const double acc = gemv64<true>(Linv + (size_t)B * kNB * kNB, kNB, xb, kNB);   // Linv_BB^T tb_B
+      const int o = threadIdx.x >> 2;
+      if ((threadIdx.x & 3) == 0) {
+        zb[o] = acc;
+        if (blockIdx.x == 0 && rB + o < n) z[rB + o] = acc;
+      }
+      __syncthreads();
+      for (int C = blockIdx.x; C < B; C += gridDim.x) {   // tb_C -= L_BC^T z_B
+        const int64_t rC = (int64_t)C * kNB;
+        const int valid = (int)(n - rB < kNB ? n - rB : kNB);
+        const double upd = gemv64<true>(W + rB * ld + rC, ld, zb, valid);
+        if ((threadIdx.x & 3) == 0) tb[rC + (threadIdx.x >> 2)] -= upd;
+      }
+    }
+    grid_barrier(ctl, ctl + 1);
   }
 }
 
@@ -552,7 +633,7 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 
 int64_t potrf_scratch_doubles(int64_t n) {
   const int64_t nb = (n + kNB - 1) / kNB;
-  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 2 /* grid barrier words */;
+  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 1 /* grid barrier words */ + 2 * n /* solve */;
 }
 
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
@@ -564,7 +645,8 @@ cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W
 }
 
 cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch,
-                        cudaStream_t st, int* launches) {
+                        cudaStream_t st, int* launches, const double* u, double* z, bool* solved) {
+  if (solved) *solved = false;
   const int nb = (int)((n + kNB - 1) / kNB);
   double* Linv = scratch;
   double* panel0 = Linv + (int64_t)nb * kNB * kNB;
@@ -596,10 +678,13 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
       const int tiles0 = (nb - 1) * nb / 2;
       const int g = std::max(1, std::min(grid, tiles0));
       int64_t nn = n, ldd = ldW;
-      void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl};
+      double* ut = panel1 + n * kNB + 1;                 // after the barrier words
+      double* tb = ut + n;
+      void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl, &u, &ut, &tb, &z};
       e = cudaLaunchCooperativeKernel((const void*)potrf_persistent_kernel, dim3(g), dim3(kThreads), args,
                                       3 * kTileSmem, st);
       if (launches) *launches += 1;
+      if (solved && u && e == cudaSuccess) *solved = true;
       return e;
     }
   }
