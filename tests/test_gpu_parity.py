@@ -787,3 +787,22 @@ def test_fused_sharded_entry_with_nccl_callback(fsb):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,m", [(4096, 9000), (2500, 7001)])
+def test_large_n_takes_the_direct_and_two_pass_paths(fsb, n, m):
+    """n beyond the fused x+y pass's limit and with >= 74 pair tiles (direct-mode SYRK, no split-K),
+    many potrf steps: f16x2 and fp64 against the fp64 oracle."""
+    rng = np.random.Generator(np.random.PCG64(n + m))
+    S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(np.float32)
+    v = rng.standard_normal(m).astype(np.float32)
+    lam = 1e-2
+    ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam, torch.from_numpy(v).to(dev))
+    a = fsb.solve_chol(system, precision="f16x2")
+    assert O.rel_err(a.x.cpu().numpy(), ref.x) <= 1e-6
+    b = fsb.solve_chol(system, precision="fp64")
+    assert O.rel_err(b.x.cpu().numpy(), ref.x) <= 1e-10
+    a2, r2 = fsb.residual(system, b.x)
+    assert r2 == b.rel_residual
