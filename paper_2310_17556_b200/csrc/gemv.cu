@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 #include "tiles.cuh"
 
 #include <algorithm>
@@ -430,6 +431,257 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
   }
 }
 
+// Cluster variant for n <= kCLMaxRows (the headline n = 1024).  The TMA engine moves ~one box row
+// per 8 SM clocks, so 128-byte-wide boxes cap a full strided read of S at ~4.6 TB/s while
+// 256-byte rows reach ~6.6 TB/s (tools/ubench/tma_seg.cu).  A panel is therefore 256 bytes of
+// columns (64 fp32 / 32 fp64), split by ROWS over a cluster of kCL CTAs: CTA r streams rows
+// [r*NCH*30, (r+1)*NCH*30) of each panel as NCH 30-row TMA boxes (rows past n arrive as zeros)
+// into one slot-set of a ring, completing on the set's single mbarrier.  x needs the column sums
+// over all n rows: each CTA reduces its rows and pushes its partial column sums into every peer's
+// exchange buffer with st.async (the data and the peer's mbarrier complete_tx travel together);
+// every CTA adds the kCL partials in rank order, so x is identical everywhere.  Software
+// pipeline, one CTA barrier per panel: iteration j
+//   warps 2-3  x of panel j-1 from the exchange (pushed an iteration ago, latency hidden)
+//   all warps  x-phase of panel j: partial column sums
+//   -- barrier --
+//   warps 0-1  sum the per-warp partials of panel j, push them to the cluster
+//   all warps  y += S_{panel j-1} x_{j-1} from the still-resident set, release the set
+// S is read from HBM exactly once.
+constexpr int kCL = 4;                           // CTAs per cluster (row split)
+// 15 consumer warps + 1 producer warp: 4 warps per SM sub-partition, so up to 128 registers per
+// thread (a 17th warp would cap every thread at 96)
+constexpr int kCLCW = 15;                        // consumer warps
+constexpr int kCLCons = kCLCW * kWarp;
+constexpr int kCLThreads = kCLCons + kWarp;
+constexpr int kCLRows = 2 * kCLCW;               // rows per chunk (TMA box outer dimension): 2 per warp
+constexpr int kCLChunk = kCLRows * 256;          // 7.5 KB per chunk slot (128-byte aligned)
+constexpr int kCLMaxV = 10;                      // chunks per CTA and panel -> 300 rows per CTA
+constexpr int kCLMaxRows = kCL * kCLRows * kCLMaxV;   // n <= 1200
+constexpr int kCLG = 5;                          // chunks per batch of shared loads
+constexpr int kCLSets = 8;                       // max panel slot-sets in the ring
+constexpr int kCLSlotsMax = 27;                  // 27 x 7.5 KB + the fixed buffers fit 227 KB
+constexpr size_t kCLFixed = 2 * kCLCW * 64 * 8 + 2 * (kCL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
+constexpr size_t kCLSmem = 1024 + (size_t)kCLSlotsMax * kCLChunk + kCLFixed;
+
+// chunks per CTA: the template instance (3, 6, 9 or 10) covering ceil(n / (kCL * 30))
+inline int cl_nch(int64_t n) {
+  const int c = (int)((n + kCL * kCLRows - 1) / (kCL * kCLRows));
+  return c <= 3 ? 3 : c <= 6 ? 6 : c <= 9 ? 9 : 10;
+}
+
+// remote (DSMEM) store that completes 8 transaction bytes on the receiving CTA's mbarrier: the
+// data and its signal travel together, no cluster-scope fence (a release.cluster arrive compiles
+// to MEMBAR.GPU and cost more than a whole panel)
+FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
+               "r"(bar) : "memory");
+}
+template <typename TS, typename TV, int NCH>
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCLThreads, 1)
+cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int64_t m, const double* __restrict__ z,
+                       const TV* __restrict__ v, double lam, int accumulate, double* __restrict__ x,
+                       double* __restrict__ ypart, int y_only) {
+  constexpr int VN1 = 16 / (int)sizeof(TS);       // columns per 16-byte vector
+  constexpr int CW = 16 * VN1;                    // columns per panel (256 bytes)
+  constexpr int R = kCLSlotsMax / NCH < kCLSets ? kCLSlotsMax / NCH : kCLSets;   // slot-sets
+  constexpr int RPC = NCH * kCLRows;              // rows per CTA
+  constexpr uint32_t kSetBytes = NCH * kCLChunk;
+  static_assert(R >= 2, "panel j's x-phase runs beside panel j-1's y-phase");
+  using VT = typename VecOf<TS>::V;
+  using Zt = typename std::conditional<sizeof(TV) == 8, double, float>::type;
+  extern __shared__ __align__(1024) unsigned char cl_raw[];
+  unsigned char* ring = cl_raw + ((1024u - (ptx::smem_u32(cl_raw) & 1023u)) & 1023u);   // [R][NCH][7.5 KB]
+  double* red = (double*)(ring + (size_t)kCLSlotsMax * kCLChunk);  // [2][15 warps][64]
+  double* xch = red + 2 * kCLCW * 64;                              // [2][kCL][64] partial column sums
+  double* xo = xch + 2 * kCL * 64;                                 // [2][64] old x (accumulate; from rank 0)
+  double* xs = xo + 2 * 64;                                        // [2][64]
+  uint64_t* full = (uint64_t*)(xs + 2 * 64);                       // [sets]
+  uint64_t* empty = full + kCLSets;                                // [sets]
+  uint64_t* xbar = empty + kCLSets;                                // [2]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)ptx::cluster_ctarank();
+  const int64_t cid = blockIdx.x / kCL, ncl = gridDim.x / kCL;
+  const int64_t row0 = (int64_t)rank * RPC;
+  const int64_t panels = (m + CW - 1) / CW;
+  const int64_t np = panels > cid ? (panels - 1 - cid) / ncl + 1 : 0;
+  if (tid == 0) {
+    for (int s = 0; s < R; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], kCLCW); }
+    ptx::mbar_init(&xbar[0], 1);
+    ptx::mbar_init(&xbar[1], 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::cluster_sync();                             // peers' exchange barriers exist before use
+  if (warp == kCLCW) {
+    // ---------------- producer: one slot-set (NCH boxes, one mbarrier) per panel ----------------
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&smap);
+      int set = 0;
+      uint32_t use = 0;                            // completed passes over the ring
+      for (int64_t j = 0; j < np; ++j) {
+        if (use > 0) ptx::mbar_wait(&empty[set], (use - 1) & 1);
+        const int32_t col = (int32_t)((cid + j * ncl) * CW);
+        ptx::mbar_arrive_expect_tx(&full[set], kSetBytes);
+#pragma unroll
+        for (int k = 0; k < NCH; ++k)
+          ptx::tma_load_2d(ring + (size_t)(set * NCH + k) * kCLChunk, &smap, &full[set], col,
+                           (int32_t)(row0 + k * kCLRows));
+        if (++set == R) { set = 0; ++use; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- consumers ----------------
+    // chunk k: warp w owns rows 2w, 2w+1 (lane >> 4); lane & 15 = 16-byte vector of the row
+    const int lr = 2 * warp + (lane >> 4), vq = lane & 15;
+    const int off = lr * 256 + vq * 16;
+    Zt zr[NCH];
+    double yreg[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int64_t row = row0 + k * kCLRows + lr;
+      zr[k] = (!y_only && row < n) ? (Zt)z[row] : (Zt)0;
+      yreg[k] = 0.0;
+    }
+    const double rlam = 1.0 / lam;
+    int setx = 0, sety = 0;                        // slot-sets of panels j and j-1
+    uint32_t phx = 0, phy = 0;
+    for (int64_t j = 0; j <= np; ++j) {
+      const int rb = (int)(j & 1);
+      // warps 2-3: x of panel j-1 (its partial sums were pushed during iteration j-1)
+      if (j >= 1 && tid >= 64 && tid < 64 + CW) {
+        const int t = tid - 64;
+        const int64_t c = (cid + (j - 1) * ncl) * CW + t;
+        double xv = 0.0;
+        if (y_only) {
+          xv = c < m ? x[c] : 0.0;
+        } else {
+          const int b = 1 - rb;
+          ptx::mbar_wait(&xbar[b], (uint32_t)(((j - 1) >> 1) & 1));
+          double sum = 0.0;
+#pragma unroll
+          for (int r = 0; r < kCL; ++r) sum += xch[(b * kCL + r) * 64 + t];
+          if (c < m) {
+            xv = ((double)v[c] - sum) * rlam;
+            // accumulate: the old x travels with rank 0's partials (read there before the push,
+            // so no rank can see rank 0's overwrite of x[c])
+            if (accumulate) xv = xo[b * 64 + t] + xv;
+            if (rank == 0) x[c] = xv;
+          }
+        }
+        xs[(1 - rb) * 64 + t] = xv;
+      }
+      // x-phase of panel j
+      if (j < np && !y_only) {
+        Zt acc[VN1];
+#pragma unroll
+        for (int e = 0; e < VN1; ++e) acc[e] = 0;
+        ptx::mbar_wait(&full[setx], phx);
+        const unsigned char* src = ring + (size_t)setx * kSetBytes + off;
+#pragma unroll
+        for (int g = 0; g < NCH; g += kCLG) {
+          VT b[kCLG];
+#pragma unroll
+          for (int k = 0; k < kCLG; ++k)
+            if (g + k < NCH) b[k] = *reinterpret_cast<const VT*>(src + (g + k) * kCLChunk);
+#pragma unroll
+          for (int k = 0; k < kCLG; ++k) {
+            if (g + k < NCH) {
+              TS a[VN1];
+              vec_to_array(b[k], a);
+#pragma unroll
+              for (int e = 0; e < VN1; ++e) acc[e] = fma((Zt)a[e], zr[g + k], acc[e]);
+            }
+          }
+        }
+        double* rw = red + rb * kCLCW * 64 + warp * 64;
+#pragma unroll
+        for (int e = 0; e < VN1; ++e) {
+          double d = (double)acc[e];
+          d += __shfl_xor_sync(0xffffffffu, d, 16);
+          if (lane < 16) rw[vq * VN1 + e] = d;
+        }
+      }
+      ptx::named_bar_sync(1, kCLCons);             // red[rb] (panel j) and xs[1-rb] (panel j-1) ready
+      // warps 0-1: push panel j's partial column sums to every CTA of the cluster
+      if (j < np && !y_only && tid < CW) {
+        double part = 0.0;
+#pragma unroll
+        for (int w = 0; w < kCLCW; ++w) part += red[(rb * kCLCW + w) * 64 + tid];
+        // the local barrier expects all kCL partial vectors (a peer's complete_tx may land before
+        // this expect_tx: the phase cannot complete until this one arrival is made)
+        if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (kCL + (accumulate ? 1 : 0)) * CW * 8);
+        const uint32_t mine = ptx::smem_u32(xch + (rb * kCL + rank) * 64 + tid);
+        const uint32_t bar = ptx::smem_u32(&xbar[rb]);
+#pragma unroll
+        for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
+        if (accumulate && rank == 0) {
+          const int64_t c = (cid + j * ncl) * CW + tid;
+          const double xold = c < m ? x[c] : 0.0;
+          const uint32_t xa = ptx::smem_u32(xo + rb * 64 + tid);
+#pragma unroll
+          for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
+        }
+      }
+      // y-phase of panel j-1
+      if (j >= 1) {
+        double xv[VN1];
+#pragma unroll
+        for (int e = 0; e < VN1; ++e) xv[e] = xs[(1 - rb) * 64 + vq * VN1 + e];
+        if (y_only) ptx::mbar_wait(&full[sety], phy);
+        const unsigned char* src = ring + (size_t)sety * kSetBytes + off;
+#pragma unroll
+        for (int g = 0; g < NCH; g += kCLG) {
+          VT b[kCLG];
+#pragma unroll
+          for (int k = 0; k < kCLG; ++k)
+            if (g + k < NCH) b[k] = *reinterpret_cast<const VT*>(src + (g + k) * kCLChunk);
+#pragma unroll
+          for (int k = 0; k < kCLG; ++k) {
+            if (g + k < NCH) {
+              TS a[VN1];
+              vec_to_array(b[k], a);
+#pragma unroll
+              for (int e = 0; e < VN1; ++e) yreg[g + k] = fma((double)a[e], xv[e], yreg[g + k]);
+            }
+          }
+        }
+        __syncwarp();                              // the whole warp has consumed the slot-set
+        if (lane == 0) ptx::mbar_arrive(&empty[sety]);
+        if (++sety == R) { sety = 0; phy ^= 1; }
+      }
+      if (j < np && ++setx == R) { setx = 0; phx ^= 1; }
+    }
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      double t = yreg[k];
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 8);
+      const int64_t row = row0 + k * kCLRows + lr;
+      if (vq == 0 && row < n) ypart[cid * n + row] = t;
+    }
+  }
+  ptx::cluster_sync();                             // no CTA leaves while a peer may still signal it
+}
+
+template <typename TS, typename TV>
+cudaError_t launch_cols_solve_y_cl(int nch, unsigned grid, cudaStream_t st, const CUtensorMap& smap, int64_t n,
+                                   int64_t m, const double* z, const TV* v, double lam, int acc, double* x,
+                                   double* ypart, int y_only) {
+  auto pick = [&](auto kfn) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCLSmem);
+    kfn<<<grid, kCLThreads, kCLSmem, st>>>(smap, n, m, z, v, lam, acc, x, ypart, y_only);
+  };
+  switch (nch) {
+    case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3>); break;
+    case 6: pick(cols_solve_y_cl_kernel<TS, TV, 6>); break;
+    case 9: pick(cols_solve_y_cl_kernel<TS, TV, 9>); break;
+    default: pick(cols_solve_y_cl_kernel<TS, TV, 10>); break;
+  }
+  return cudaGetLastError();
+}
+
 // r = S^T y + λx - v with exact fp64 products; per-block ||r||², ||v||² partials.
 template <typename TS, typename TV, bool kVec>
 __global__ void __launch_bounds__(kColThreads)
@@ -584,6 +836,52 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
   // recomputed y = S x is bit-identical to the solve's (test_solvers.py:109-114)
   const size_t smem = cy_smem_bytes<TS>(n);
   if (smem > 200 * 1024 || !aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
+  // n <= 1200: the cluster kernel (S read from HBM once, in 256-byte TMA rows)
+  static const int cl_env = getenv("FS_CY_CL") ? atoi(getenv("FS_CY_CL")) : 1;
+  CUtensorMap smap;
+  memset(&smap, 0, sizeof smap);
+  if (cl_env && n <= kCLMaxRows &&
+      make_tensor_map_2d(&smap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, S,
+                         (uint64_t)m, (uint64_t)n, (uint64_t)ldS * sizeof(TS), 256 / sizeof(TS), kCLRows) ==
+          cudaSuccess) {
+    const int64_t panels = (m + 256 / (int64_t)sizeof(TS) - 1) / (256 / (int64_t)sizeof(TS));
+    static int max_cl = 0;
+    if (!max_cl) {
+      auto probe = cols_solve_y_cl_kernel<TS, float, 9>;
+      cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCLSmem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(kCL * 64));
+      cfg.blockDim = dim3(kCLThreads);
+      cfg.dynamicSmemBytes = kCLSmem;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = kCL;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)probe, &cfg) != cudaSuccess || mc < 1) {
+        cudaGetLastError();
+        mc = num_sms / kCL;
+      }
+      max_cl = mc;
+    }
+    // ypart holds one row per cluster; same capacity bound as the panel kernel's grid
+    const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
+    const int64_t ncl = std::min<int64_t>(std::min<int64_t>(max_cl, num_sms / kCL), std::min(panels, cap));
+    if (ypart_rows < ncl) return cudaErrorInvalidValue;
+    const unsigned grid = (unsigned)(ncl * kCL);
+    const int nch = cl_nch(n);
+    cudaError_t e = v_f64 ? launch_cols_solve_y_cl<TS, double>(nch, grid, st, smap, n, m, z, (const double*)v, lam,
+                                                               accumulate ? 1 : 0, x, ypart, y_only)
+                          : launch_cols_solve_y_cl<TS, float>(nch, grid, st, smap, n, m, z, (const float*)v, lam,
+                                                              accumulate ? 1 : 0, x, ypart, y_only);
+    if (e != cudaSuccess) return e;
+    reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(ypart, ncl, n, n, y);
+    if (launches) *launches += 2;
+    return cudaGetLastError();
+  }
   const int64_t panels = (m + cy_cols<TS>() - 1) / cy_cols<TS>();
   const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
   int64_t G = std::min<int64_t>((int64_t)num_sms, std::min(panels, cap));

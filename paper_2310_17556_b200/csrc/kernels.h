@@ -111,6 +111,7 @@ cudaError_t embed_complex(bool f64, const void* S, int64_t n, int64_t m, int64_t
 
 // ---- tmap.cu: 2-D tensor map (no swizzle) over a row-major array of `outer` rows ----
 cudaError_t make_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
-                               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer);
+                               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                               CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE);
 
 }  // namespace fs

@@ -9,7 +9,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 }  // namespace
 
 cudaError_t make_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
-                               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+                               uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                               CUtensorMapSwizzle swizzle) {
   static EncodeTiledFn enc = nullptr;
   if (!enc) {
     void* fn = nullptr;
@@ -23,7 +24,7 @@ cudaError_t make_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, cons
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, dtype, 2, const_cast<void*>(base), gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
