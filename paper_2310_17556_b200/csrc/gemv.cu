@@ -457,10 +457,13 @@ constexpr int kCLRows = 2 * kCLCW;               // rows per chunk (TMA box oute
 constexpr int kCLChunk = kCLRows * 256;          // 7.5 KB per chunk slot (128-byte aligned)
 constexpr int kCLMaxV = 10;                      // chunks per CTA and panel -> 300 rows per CTA
 constexpr int kCLMaxRows = kCL * kCLRows * kCLMaxV;   // n <= 1200
-constexpr int kCLG = 5;                          // chunks per batch of shared loads
+constexpr int kCLG = 3;                          // chunks per batch of shared loads (y group)
+constexpr int kCLXW = 7;                         // x-group warps (partial sums, exchange, x)
+constexpr int kCLYW = kCLCW - kCLXW;             // y-group warps (8)
+constexpr int kCLXThreads = kCLXW * kWarp;
 constexpr int kCLSets = 8;                       // max panel slot-sets in the ring
 constexpr int kCLSlotsMax = 27;                  // 27 x 7.5 KB + the fixed buffers fit 227 KB
-constexpr size_t kCLFixed = 2 * kCLCW * 64 * 8 + 2 * (kCL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
+constexpr size_t kCLFixed = 2 * kCLXW * 64 * 8 + 2 * (kCL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
 constexpr size_t kCLSmem = 1024 + (size_t)kCLSlotsMax * kCLChunk + kCLFixed;
 
 // chunks per CTA: the template instance (3, 6, 9 or 10) covering ceil(n / (kCL * 30))
@@ -476,6 +479,8 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
                "r"(bar) : "memory");
 }
+FS_DEVINL void bar_arrive_n(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+
 template <typename TS, typename TV, int NCH>
 __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCLThreads, 1)
 cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int64_t m, const double* __restrict__ z,
@@ -485,14 +490,17 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   constexpr int CW = 16 * VN1;                    // columns per panel (256 bytes)
   constexpr int R = kCLSlotsMax / NCH < kCLSets ? kCLSlotsMax / NCH : kCLSets;   // slot-sets
   constexpr int RPC = NCH * kCLRows;              // rows per CTA
+  constexpr int RP = kCLRows / 2;                 // row pairs per chunk (one warp-wide load each)
   constexpr uint32_t kSetBytes = NCH * kCLChunk;
+  constexpr int PA = (RP + kCLXW - 1) / kCLXW;    // row pairs per x-group warp (3)
+  constexpr int PB = (RP + kCLYW - 1) / kCLYW;    // row pairs per y-group warp (2)
   static_assert(R >= 2, "panel j's x-phase runs beside panel j-1's y-phase");
   using VT = typename VecOf<TS>::V;
   using Zt = typename std::conditional<sizeof(TV) == 8, double, float>::type;
   extern __shared__ __align__(1024) unsigned char cl_raw[];
   unsigned char* ring = cl_raw + ((1024u - (ptx::smem_u32(cl_raw) & 1023u)) & 1023u);   // [R][NCH][7.5 KB]
-  double* red = (double*)(ring + (size_t)kCLSlotsMax * kCLChunk);  // [2][15 warps][64]
-  double* xch = red + 2 * kCLCW * 64;                              // [2][kCL][64] partial column sums
+  double* red = (double*)(ring + (size_t)kCLSlotsMax * kCLChunk);  // [2][x warps][64]
+  double* xch = red + 2 * kCLXW * 64;                              // [2][kCL][64] partial column sums
   double* xo = xch + 2 * kCL * 64;                                 // [2][64] old x (accumulate; from rank 0)
   double* xs = xo + 2 * 64;                                        // [2][64]
   uint64_t* full = (uint64_t*)(xs + 2 * 64);                       // [sets]
@@ -505,12 +513,14 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   const int64_t panels = (m + CW - 1) / CW;
   const int64_t np = panels > cid ? (panels - 1 - cid) / ncl + 1 : 0;
   if (tid == 0) {
-    for (int s = 0; s < R; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], kCLCW); }
+    for (int s = 0; s < R; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], kCLYW); }
     ptx::mbar_init(&xbar[0], 1);
     ptx::mbar_init(&xbar[1], 1);
     ptx::fence_mbar_init();
   }
   ptx::cluster_sync();                             // peers' exchange barriers exist before use
+  const int vq = lane & 15, half = lane >> 4;
+  const int off = half * 256 + vq * 16;            // within a row pair
   if (warp == kCLCW) {
     // ---------------- producer: one slot-set (NCH boxes, one mbarrier) per panel ----------------
     if (lane == 0) {
@@ -529,48 +539,60 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
       }
     }
     __syncwarp();
-  } else {
-    // ---------------- consumers ----------------
-    // chunk k: warp w owns rows 2w, 2w+1 (lane >> 4); lane & 15 = 16-byte vector of the row
-    const int lr = 2 * warp + (lane >> 4), vq = lane & 15;
-    const int off = lr * 256 + vq * 16;
-    Zt zr[NCH];
-    double yreg[NCH];
+  } else if (warp < kCLXW) {
+    // ---------------- x group: partial column sums, the cluster exchange, x ----------------
+    // warp a owns row pairs a, a + 7, a + 14 of every chunk
+    Zt zr[NCH][PA];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) {
-      const int64_t row = row0 + k * kCLRows + lr;
-      zr[k] = (!y_only && row < n) ? (Zt)z[row] : (Zt)0;
-      yreg[k] = 0.0;
-    }
+    for (int k = 0; k < NCH; ++k)
+#pragma unroll
+      for (int p = 0; p < PA; ++p) {
+        const int rp = warp + p * kCLXW;
+        const int64_t row = row0 + k * kCLRows + 2 * rp + half;
+        zr[k][p] = (!y_only && rp < RP && row < n) ? (Zt)z[row] : (Zt)0;
+      }
     const double rlam = 1.0 / lam;
-    int setx = 0, sety = 0;                        // slot-sets of panels j and j-1
-    uint32_t phx = 0, phy = 0;
+    // warps 2-3 form x of panel j-1 and load v (or x, y-only) one iteration ahead
+    const bool xw = tid >= 64 && tid < 64 + CW;
+    const int t = tid - 64;
+    double vnext = 0.0;
+    if (xw && np > 0) {
+      const int64_t c = cid * CW + t;
+      vnext = c < m ? (y_only ? x[c] : (double)v[c]) : 0.0;
+    }
+    int setx = 0;
+    uint32_t phx = 0;
     for (int64_t j = 0; j <= np; ++j) {
       const int rb = (int)(j & 1);
-      // warps 2-3: x of panel j-1 (its partial sums were pushed during iteration j-1)
-      if (j >= 1 && tid >= 64 && tid < 64 + CW) {
-        const int t = tid - 64;
-        const int64_t c = (cid + (j - 1) * ncl) * CW + t;
+      if (j >= 1 && xw) {
+        const int64_t p = j - 1;                   // panel whose x is formed now
+        const int b = (int)(p & 1);
+        const int64_t c = (cid + p * ncl) * CW + t;
+        const double vc = vnext;
+        if (j < np) {
+          const int64_t cn = c + ncl * CW;
+          vnext = cn < m ? (y_only ? x[cn] : (double)v[cn]) : 0.0;
+        }
         double xv = 0.0;
         if (y_only) {
-          xv = c < m ? x[c] : 0.0;
+          xv = vc;
         } else {
-          const int b = 1 - rb;
-          ptx::mbar_wait(&xbar[b], (uint32_t)(((j - 1) >> 1) & 1));
+          ptx::mbar_wait(&xbar[b], (uint32_t)((p >> 1) & 1));
           double sum = 0.0;
 #pragma unroll
           for (int r = 0; r < kCL; ++r) sum += xch[(b * kCL + r) * 64 + t];
           if (c < m) {
-            xv = ((double)v[c] - sum) * rlam;
+            xv = (vc - sum) * rlam;
             // accumulate: the old x travels with rank 0's partials (read there before the push,
             // so no rank can see rank 0's overwrite of x[c])
             if (accumulate) xv = xo[b * 64 + t] + xv;
             if (rank == 0) x[c] = xv;
           }
         }
-        xs[(1 - rb) * 64 + t] = xv;
+        if (p >= 2) ptx::named_bar_sync(4 + b, CW + kCLYW * kWarp);   // y group done with xs[b]
+        xs[b * 64 + t] = xv;
+        bar_arrive_n(2 + b, CW + kCLYW * kWarp);                   // xs[b] ready
       }
-      // x-phase of panel j
       if (j < np && !y_only) {
         Zt acc[VN1];
 #pragma unroll
@@ -578,89 +600,107 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         ptx::mbar_wait(&full[setx], phx);
         const unsigned char* src = ring + (size_t)setx * kSetBytes + off;
 #pragma unroll
-        for (int g = 0; g < NCH; g += kCLG) {
-          VT b[kCLG];
+        for (int k = 0; k < NCH; ++k) {
+          VT bv[PA];
 #pragma unroll
-          for (int k = 0; k < kCLG; ++k)
-            if (g + k < NCH) b[k] = *reinterpret_cast<const VT*>(src + (g + k) * kCLChunk);
+          for (int p = 0; p < PA; ++p)
+            if (warp + p * kCLXW < RP) bv[p] = *reinterpret_cast<const VT*>(src + k * kCLChunk + (warp + p * kCLXW) * 512);
 #pragma unroll
-          for (int k = 0; k < kCLG; ++k) {
-            if (g + k < NCH) {
+          for (int p = 0; p < PA; ++p) {
+            if (warp + p * kCLXW < RP) {
               TS a[VN1];
-              vec_to_array(b[k], a);
+              vec_to_array(bv[p], a);
 #pragma unroll
-              for (int e = 0; e < VN1; ++e) acc[e] = fma((Zt)a[e], zr[g + k], acc[e]);
+              for (int e = 0; e < VN1; ++e) acc[e] = fma((Zt)a[e], zr[k][p], acc[e]);
             }
           }
         }
-        double* rw = red + rb * kCLCW * 64 + warp * 64;
+        double* rw = red + rb * kCLXW * 64 + warp * 64;
 #pragma unroll
         for (int e = 0; e < VN1; ++e) {
           double d = (double)acc[e];
           d += __shfl_xor_sync(0xffffffffu, d, 16);
           if (lane < 16) rw[vq * VN1 + e] = d;
         }
-      }
-      ptx::named_bar_sync(1, kCLCons);             // red[rb] (panel j) and xs[1-rb] (panel j-1) ready
-      // warps 0-1: push panel j's partial column sums to every CTA of the cluster
-      if (j < np && !y_only && tid < CW) {
-        double part = 0.0;
+        ptx::named_bar_sync(1, kCLXThreads);       // red[rb] holds panel j's per-warp partials
+        if (tid < CW) {                            // warps 0-1 push them to every CTA
+          double part = 0.0;
 #pragma unroll
-        for (int w = 0; w < kCLCW; ++w) part += red[(rb * kCLCW + w) * 64 + tid];
-        // the local barrier expects all kCL partial vectors (a peer's complete_tx may land before
-        // this expect_tx: the phase cannot complete until this one arrival is made)
-        if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (kCL + (accumulate ? 1 : 0)) * CW * 8);
-        const uint32_t mine = ptx::smem_u32(xch + (rb * kCL + rank) * 64 + tid);
-        const uint32_t bar = ptx::smem_u32(&xbar[rb]);
+          for (int w = 0; w < kCLXW; ++w) part += red[(rb * kCLXW + w) * 64 + tid];
+          // the local barrier expects all kCL partial vectors (a peer's complete_tx may land
+          // before this expect_tx: the phase cannot complete until this one arrival is made)
+          if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (kCL + (accumulate ? 1 : 0)) * CW * 8);
+          const uint32_t mine = ptx::smem_u32(xch + (rb * kCL + rank) * 64 + tid);
+          const uint32_t bar = ptx::smem_u32(&xbar[rb]);
 #pragma unroll
-        for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
-        if (accumulate && rank == 0) {
-          const int64_t c = (cid + j * ncl) * CW + tid;
-          const double xold = c < m ? x[c] : 0.0;
-          const uint32_t xa = ptx::smem_u32(xo + rb * 64 + tid);
+          for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
+          if (accumulate && rank == 0) {
+            const int64_t c = (cid + j * ncl) * CW + tid;
+            const double xold = c < m ? x[c] : 0.0;
+            const uint32_t xa = ptx::smem_u32(xo + rb * 64 + tid);
 #pragma unroll
-          for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
-        }
-      }
-      // y-phase of panel j-1
-      if (j >= 1) {
-        double xv[VN1];
-#pragma unroll
-        for (int e = 0; e < VN1; ++e) xv[e] = xs[(1 - rb) * 64 + vq * VN1 + e];
-        if (y_only) ptx::mbar_wait(&full[sety], phy);
-        const unsigned char* src = ring + (size_t)sety * kSetBytes + off;
-#pragma unroll
-        for (int g = 0; g < NCH; g += kCLG) {
-          VT b[kCLG];
-#pragma unroll
-          for (int k = 0; k < kCLG; ++k)
-            if (g + k < NCH) b[k] = *reinterpret_cast<const VT*>(src + (g + k) * kCLChunk);
-#pragma unroll
-          for (int k = 0; k < kCLG; ++k) {
-            if (g + k < NCH) {
-              TS a[VN1];
-              vec_to_array(b[k], a);
-#pragma unroll
-              for (int e = 0; e < VN1; ++e) yreg[g + k] = fma((double)a[e], xv[e], yreg[g + k]);
-            }
+            for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
           }
         }
-        __syncwarp();                              // the whole warp has consumed the slot-set
-        if (lane == 0) ptx::mbar_arrive(&empty[sety]);
-        if (++sety == R) { sety = 0; phy ^= 1; }
+        if (++setx == R) { setx = 0; phx ^= 1; }
       }
-      if (j < np && ++setx == R) { setx = 0; phx ^= 1; }
+    }
+  } else {
+    // ---------------- y group: y += S_panel x_panel, releases the slot-set ----------------
+    const int wb = warp - kCLXW;                   // warp b owns row pairs b, b + 8 of every chunk
+    double yreg[NCH][PB];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+#pragma unroll
+      for (int p = 0; p < PB; ++p) yreg[k][p] = 0.0;
+    int sety = 0;
+    uint32_t phy = 0;
+    for (int64_t p = 0; p < np; ++p) {
+      const int b = (int)(p & 1);
+      ptx::named_bar_sync(2 + b, CW + kCLYW * kWarp);             // xs[b] holds x of panel p
+      double xv[VN1];
+#pragma unroll
+      for (int e = 0; e < VN1; ++e) xv[e] = xs[b * 64 + vq * VN1 + e];
+      if (p + 2 < np) bar_arrive_n(4 + b, CW + kCLYW * kWarp);     // xs[b] may be rewritten
+      ptx::mbar_wait(&full[sety], phy);            // (already complete: makes the TMA data visible here)
+      const unsigned char* src = ring + (size_t)sety * kSetBytes + off;
+#pragma unroll
+      for (int k0 = 0; k0 < NCH; k0 += kCLG) {
+        VT bv[kCLG][PB];
+#pragma unroll
+        for (int k = 0; k < kCLG; ++k)
+#pragma unroll
+          for (int q = 0; q < PB; ++q)
+            if (k0 + k < NCH && wb + q * kCLYW < RP)
+              bv[k][q] = *reinterpret_cast<const VT*>(src + (k0 + k) * kCLChunk + (wb + q * kCLYW) * 512);
+#pragma unroll
+        for (int k = 0; k < kCLG; ++k)
+#pragma unroll
+          for (int q = 0; q < PB; ++q)
+            if (k0 + k < NCH && wb + q * kCLYW < RP) {
+              TS a[VN1];
+              vec_to_array(bv[k][q], a);
+#pragma unroll
+              for (int e = 0; e < VN1; ++e) yreg[k0 + k][q] = fma((double)a[e], xv[e], yreg[k0 + k][q]);
+            }
+      }
+      __syncwarp();                                // the whole warp has consumed the slot-set
+      if (lane == 0) ptx::mbar_arrive(&empty[sety]);
+      if (++sety == R) { sety = 0; phy ^= 1; }
     }
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) {
-      double t = yreg[k];
-      t += __shfl_xor_sync(0xffffffffu, t, 1);
-      t += __shfl_xor_sync(0xffffffffu, t, 2);
-      t += __shfl_xor_sync(0xffffffffu, t, 4);
-      t += __shfl_xor_sync(0xffffffffu, t, 8);
-      const int64_t row = row0 + k * kCLRows + lr;
-      if (vq == 0 && row < n) ypart[cid * n + row] = t;
-    }
+    for (int k = 0; k < NCH; ++k)
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        double t = yreg[k][q];
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
+        const int rp = wb + q * kCLYW;
+        const int64_t row = row0 + k * kCLRows + 2 * rp + half;
+        if (rp < RP && vq == 0 && row < n) ypart[cid * n + row] = t;
+      }
   }
   ptx::cluster_sync();                             // no CTA leaves while a peer may still signal it
 }
