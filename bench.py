@@ -324,7 +324,7 @@ def run_b200(args, rank, world, local):
         bytes_sv = n * m_local * es + tiles + m_local * es + n * 8
         gemv["gemv_sv_GBps"] = bytes_sv / (st["gemv_sv"] * 1e-3) / 1e9
     if st.get("gemv_stz"):
-        # fused x = (v - S^T z)/lam and y = S x: S from HBM once (its second read hits L2)
+        # fused x = (v - S^T z)/lam and y = S x (cluster kernel): S from HBM exactly once
         bytes_stz = n * m_local * es + m_local * es + m_local * 8 + n * 8
         gemv["gemv_stz_GBps"] = bytes_stz / (st["gemv_stz"] * 1e-3) / 1e9
     if st.get("residual"):

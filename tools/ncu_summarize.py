@@ -22,6 +22,7 @@ METRICS = {
     "registers_per_thread": ("launch__registers_per_thread", 1),
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1,
+        "ns": 1e-6, "us": 1e-3, "ms": 1,
         "second": 1e3}
 
 
