@@ -174,7 +174,7 @@ __device__ void gemm32_dmma(const double* A, const double* B, double acc[2][2]) 
       // B operand (4 x 8, "col"): element (k, col) = kNT ? B[col][k] : B[k][col]
       const int col = tc + 8 * j + fr;
       const double b = kNT ? B[col * kLd + k0 + fk] : B[(k0 + fk) * kLd + col];
-      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                    : "+d"(acc[j][0]), "+d"(acc[j][1])
                    : "d"(a), "d"(b));
     }
@@ -248,7 +248,7 @@ __device__ void gemm_nt(const double (*A)[kLd], const double (*B)[kLd], double a
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-#pragma unroll 4
+#pragma unroll
   for (int k0 = 0; k0 < kNB; k0 += 4) {
     double a[2], b[4];
 #pragma unroll
@@ -259,7 +259,7 @@ __device__ void gemm_nt(const double (*A)[kLd], const double (*B)[kLd], double a
     for (int t = 0; t < 2; ++t)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                      : "+d"(acc[2 * t][u]), "+d"(acc[2 * t + 1][u])
                      : "d"(a[t]), "d"(b[u]));
   }
@@ -276,6 +276,18 @@ __device__ void load_tile(const double* W, int64_t n, int64_t ld, int64_t r0, in
     const int64_t gr = r0 + r, gc = c0 + c;
     v[u] = (gr < n && gc < n) ? W[gr * ld + gc] : 0.0;
   }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = u * kThreads + threadIdx.x;
+    T[e >> 6][e & 63] = v[u];
+  }
+}
+
+// contiguous 64x64 block (an inverted diagonal block) -> smem, batched like load_tile
+__device__ void load_block64(const double* __restrict__ src, double (*T)[kLd]) {
+  double v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) v[u] = src[u * kThreads + threadIdx.x];
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int e = u * kThreads + threadIdx.x;
@@ -311,10 +323,28 @@ __device__ void tile_coords(int t, int& I, int& J) {  // lower tiles in row-majo
 
 // Factor diagonal block kk of W (already fully updated) in place and store its inverse in
 // Linv[kk] (dense 64x64, identity-padded).  A, X, T: three smem tiles.
+#ifdef FS_POTRF_TRACE
+__device__ unsigned long long g_potrf_trace[128];
+#define POTRF_MARK(i)                                                                              \
+  do {                                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                                     \
+      unsigned long long t_;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                       \
+      g_potrf_trace[(i)] = t_;                                                                     \
+    }                                                                                              \
+  } while (0)
+#else
+#define POTRF_MARK(i) \
+  do {                \
+  } while (0)
+#endif
+
 __device__ void factor_diag(double* W, int64_t n, int64_t ld, int kk, int64_t* status, double* Linv,
-                            double (*A)[kLd], double (*X)[kLd], double (*T)[kLd], bool preloaded) {
+                            double (*A)[kLd], double (*X)[kLd], double (*T)[kLd], bool preloaded,
+                            bool tr = false) {
   const int64_t r0 = (int64_t)kk * kNB;
   const int b = (int)(n - r0 < kNB ? n - r0 : kNB);
+  if (tr) POTRF_MARK(85);
   if (!preloaded) load_tile(W, n, ld, r0, r0, A);
   __syncthreads();
   for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {   // identity padding, lower only
@@ -323,7 +353,9 @@ __device__ void factor_diag(double* W, int64_t n, int64_t ld, int kk, int64_t* s
     else if (r >= b) A[r][c] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
+  if (tr) POTRF_MARK(86);
   const int f = chol_inv64(A, X, T);
+  if (tr) POTRF_MARK(87);
   if (f >= 0) {
     if (threadIdx.x == 0) *status = r0 + f + 1;
     return;
@@ -396,6 +428,8 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
   double* pan_prev = (k & 1) ? panel0 : panel1;    // previous step's panel L_{.,k-1}
   // materialise the previous panel L_{.,k-1} into W (nobody reads W column k-1 any more):
   // row block I by the CTA (I, k+1); row block k by the diagonal CTA (k+1, k+1)
+  const bool tr = (tile == 0 && k == 5);
+  if (tr) POTRF_MARK(80);
   if (J == k + 1 && k >= 1) {
     copy_panel(W + (kc - kNB), ld, pan_prev, rI, n);
     if (I == k + 1) copy_panel(W + (kc - kNB), ld, pan_prev, kc, n);
@@ -404,9 +438,11 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
     const double* li = Linv + (size_t)k * kNB * kNB;
     for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) Lk[e >> 6][e & 63] = li[e];
   }
+  if (tr) POTRF_MARK(81);
   load_tile(W, n, ld, rI, kc, XI);                 // A_Ik
   if (I != J) load_tile(W, n, ld, rJ, kc, XJ);     // A_Jk
   __syncthreads();
+  if (tr) POTRF_MARK(82);
   // X_I = A_Ik Linv_kk^T, X_J = A_Jk Linv_kk^T (the panel TRSM as GEMMs)
   double accI[4][4], accJ[4][4];
   gemm_nt(XI, Lk, accI);
@@ -420,6 +456,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
       if (I != J) XJ[frag_row(i)][frag_col(i, j)] = accJ[i][j];
     }
   __syncthreads();
+  if (tr) POTRF_MARK(83);
   if (J == k + 1) {   // store the panel L_Ik
     for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
       const int r = e >> 6, c = e & 63;
@@ -448,6 +485,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
       }
     }
   }
+  if (tr) POTRF_MARK(84);
   // A_IJ -= X_I X_J^T (old values loaded up front, the GEMM overlaps their latency)
   double old[4][4];
 #pragma unroll
@@ -467,6 +505,7 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
       acc[i][j] = old[i][j] - acc[i][j];
       if (gi < n && gj <= gi) W[gi * ld + gj] = acc[i][j];
     }
+  if (tr) POTRF_MARK(85);
   if (I == J && I == k + 1) {
     // (block-uniform branch) the updated diagonal tile goes straight into smem for its factor
     __syncthreads();
@@ -474,8 +513,9 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) Lk[frag_row(i)][frag_col(i, j)] = acc[i][j];
-    factor_diag(W, n, ld, I, status, Linv, Lk, XI, XJ, true);
+    factor_diag(W, n, ld, I, status, Linv, Lk, XI, XJ, true, tr);
   }
+  if (tr) POTRF_MARK(89);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -484,6 +524,106 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double*
   extern __shared__ double dsm[];
   if (*(volatile int64_t*)status != 0) return;
   step_tile(W, n, ld, k, Linv, panel0, panel1, status, blockIdx.x, dsm);
+}
+
+// The persistent kernel's step k splits tile 0 = (k+1, k+1) in two:
+//  * critical_tile (CTA 0, the step's critical path): X = A_{k+1,k} Linv_kk^T with Linv_kk still in
+//    smem from CTA 0's own previous factorisation, the diagonal update A -= X X^T straight into
+//    smem, then the factorisation + inversion of block k+1 (kept in smem for step k+1);
+//  * aux_tile (the last CTA): everything else tile 0 used to do — copy the previous panel's rows
+//    {k, k+1} into W, recompute X, store the panel rows of block k+1, and the fused forward
+//    substitution for row block k+1 (t_k = Linv_kk ut_k, ut_{k+1} -= L_{k+1,k} t_k).
+// (tools/ubench/potrf_trace.cu: the old tile 0 took 32 us per step, 12 of them off the chain.)
+__device__ void critical_tile(double* W, int64_t n, int64_t ld, int k, double* Linv, int64_t* status, double* dsm,
+                              double (*P)[kLd]) {
+  double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
+  double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+  double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
+  const int I = k + 1;
+  const int64_t kc = (int64_t)k * kNB, rI = (int64_t)I * kNB;
+  const bool tr = (k == 5);
+  if (tr) POTRF_MARK(80);
+  load_tile(W, n, ld, rI, kc, X);                  // A_{I,k}
+  double old[4][4];                                // the diagonal tile's current lower values
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gi = rI + frag_row(i), gj = rI + frag_col(i, j);
+      old[i][j] = (gi < n && gj <= gi) ? W[gi * ld + gj] : 0.0;
+    }
+  __syncthreads();
+  if (tr) POTRF_MARK(81);
+  double acc[4][4];
+  gemm_nt(X, P, acc);                              // X_I = A_Ik Linv_kk^T
+  __syncthreads();
+  if (tr) POTRF_MARK(82);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) X[frag_row(i)][frag_col(i, j)] = acc[i][j];
+  __syncthreads();
+  if (tr) POTRF_MARK(83);
+  gemm_nt(X, X, acc);                              // A_II -= X_I X_I^T
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) A[frag_row(i)][frag_col(i, j)] = old[i][j] - acc[i][j];
+  if (tr) POTRF_MARK(84);
+  factor_diag(W, n, ld, I, status, Linv, A, X, T, true, tr);   // L_II -> W, Linv_II -> Linv and X
+  __syncthreads();
+  if (tr) POTRF_MARK(88);
+  for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) P[e >> 6][e & 63] = X[e >> 6][e & 63];
+  if (tr) POTRF_MARK(89);
+}
+
+__device__ void aux_tile(double* W, int64_t n, int64_t ld, int k, const double* Linv, double* panel0,
+                         double* panel1, double* dsm, double* ut, double* tb) {
+  double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
+  double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+  const int I = k + 1;
+  const int64_t kc = (int64_t)k * kNB, rI = (int64_t)I * kNB;
+  double* pan_cur = (k & 1) ? panel1 : panel0;
+  const double* pan_prev = (k & 1) ? panel0 : panel1;
+  if (k >= 1) {                                    // previous panel L_{.,k-1}: rows of blocks k+1, k
+    copy_panel(W + (kc - kNB), ld, pan_prev, rI, n);
+    copy_panel(W + (kc - kNB), ld, pan_prev, kc, n);
+  }
+  load_block64(Linv + (size_t)k * kNB * kNB, Lk);
+  load_tile(W, n, ld, rI, kc, XI);
+  __syncthreads();
+  double acc[4][4];
+  gemm_nt(XI, Lk, acc);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) XI[frag_row(i)][frag_col(i, j)] = acc[i][j];
+  __syncthreads();
+  for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {   // the panel rows L_{I,k}
+    const int r = e >> 6, c = e & 63;
+    const int64_t gr = rI + r;
+    if (gr < n) pan_cur[gr * kNB + c] = XI[r][c];
+  }
+  if (ut) {
+    __shared__ double uk[kNB], tk[kNB];
+    if (threadIdx.x < kNB) uk[threadIdx.x] = (kc + threadIdx.x < n) ? ut[kc + threadIdx.x] : 0.0;
+    __syncthreads();
+    {
+      const double a = gemv64<false>(&Lk[0][0], kLd, uk, kNB);
+      const int o = threadIdx.x >> 2;
+      if ((threadIdx.x & 3) == 0) {
+        tk[o] = a;
+        if (kc + o < n) tb[kc + o] = a;           // t_k
+      }
+    }
+    __syncthreads();
+    {
+      const double a = gemv64<false>(&XI[0][0], kLd, tk, kNB);
+      const int o = threadIdx.x >> 2;
+      if ((threadIdx.x & 3) == 0 && rI + o < n) ut[rI + o] -= a;
+    }
+  }
 }
 
 // sense-reversing grid barrier (cooperative launch: all CTAs co-resident)
@@ -514,27 +654,48 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
                         int64_t* status, unsigned* ctl, const double* __restrict__ u, double* ut, double* tb,
                         double* __restrict__ z) {
   extern __shared__ double dsm[];
+  double (*P)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 3 * kNB * kLd);   // CTA 0: Linv_kk
   const int nb = (int)((n + kNB - 1) / kNB);
   if (u)                                                  // working right-hand side of L t = u
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
       ut[e] = u[e];
+  POTRF_MARK(0);
   if (blockIdx.x == 0 && *(volatile int64_t*)status == 0) {
     double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
     double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
     double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
     factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) P[e >> 6][e & 63] = X[e >> 6][e & 63];
   }
+  POTRF_MARK(1);
   grid_barrier(ctl, ctl + 1);
+  POTRF_MARK(2);
   int k = 0;
+  const int G = gridDim.x;
   for (; k + 1 < nb; ++k) {
     if (*(volatile int64_t*)status != 0) break;          // uniform: read after the barrier
     const int t = nb - k - 1, tiles = t * (t + 1) / 2;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (blockIdx.x == 0) {
       __syncthreads();
-      step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm, u ? ut : nullptr, tb);
+      critical_tile(W, n, ld, k, Linv, status, dsm, P);
     }
+    if (blockIdx.x == G - 1) {
+      __syncthreads();
+      aux_tile(W, n, ld, k, Linv, panel0, panel1, dsm, u ? ut : nullptr, tb);
+    }
+    // tiles 1.. over CTAs 1..G-1 (CTA 0 keeps to the critical path when G > 1)
+    const int first = G > 1 ? (int)blockIdx.x : (int)blockIdx.x + 1, stride = G > 1 ? G - 1 : 1;
+    if (G == 1 || blockIdx.x >= 1)
+      for (int tile = first; tile < tiles; tile += stride) {
+        __syncthreads();
+        step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm, u ? ut : nullptr, tb);
+      }
+    if (k < 30) POTRF_MARK(3 + 2 * k);
     grid_barrier(ctl, ctl + 1);
+    if (k < 30) POTRF_MARK(4 + 2 * k);
   }
+  POTRF_MARK(70);
   const bool solve = u && *(volatile int64_t*)status == 0;
   if (nb >= 2 && *(volatile int64_t*)status == 0) {      // last panel L_{., nb-2} into W
     const int kk = nb - 2;
@@ -557,30 +718,57 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
     const int o = threadIdx.x >> 2;
     if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = acc;
   }
+  POTRF_MARK(71);
   grid_barrier(ctl, ctl + 1);                             // tb = t complete, W holds all of L
-  // backward solve L^T z = t, right-looking: z_B = Linv_BB^T tb_B (every CTA, redundantly), then
-  // tb_C -= L_BC^T z_B for C < B spread over the CTAs; one grid barrier per block
-  for (int B = nb - 1; B >= 0; --B) {
-    const int64_t rB = (int64_t)B * kNB;
-    if (B >= (int)blockIdx.x || blockIdx.x == 0) {        // CTAs with work this step (C < B) and CTA 0
-      if (threadIdx.x < kNB) xb[threadIdx.x] = (rB + threadIdx.x < n) ? tb[rB + threadIdx.x] : 0.0;
-      __syncthreads();
-      const double acc = gemv64<true>(Linv + (size_t)B * kNB * kNB, kNB, xb, kNB);   // Linv_BB^T tb_B
-      const int o = threadIdx.x >> 2;
-      if ((threadIdx.x & 3) == 0) {
-        zb[o] = acc;
-        if (blockIdx.x == 0 && rB + o < n) z[rB + o] = acc;
+  POTRF_MARK(72);
+  // backward solve L^T z = t, left-looking per block with release/acquire flags instead of a grid
+  // barrier per block: CTA c owns block c (c = blockIdx.x + i*G, taken in decreasing order) and
+  // applies tb_c -= L_Bc^T z_B as each z_B (B > c) is published, then z_c = Linv_cc^T tb_c and
+  // publishes it.  The L_Bc tile is loaded before waiting for z_B, so a link of the dependency
+  // chain costs a flag round trip + a 64-vector load (tools/ubench/potrf_trace.cu: 85 -> ~30 us
+  // at n = 1024 against the barrier-per-block version).
+  unsigned* zflag = reinterpret_cast<unsigned*>(tb + n);
+  const int o = threadIdx.x >> 2, q = threadIdx.x & 3;
+  int c_top = (int)blockIdx.x;
+  while (c_top + (int)gridDim.x < nb) c_top += gridDim.x;
+  for (int c = c_top; c >= 0 && c < nb; c -= gridDim.x) {
+    const int64_t rC = (int64_t)c * kNB;
+    if (threadIdx.x < kNB) xb[threadIdx.x] = (rC + threadIdx.x < n) ? __ldcg(tb + rC + threadIdx.x) : 0.0;
+    for (int B = nb - 1; B > c; --B) {
+      const int64_t rB = (int64_t)B * kNB;
+      const int valid = (int)(n - rB < kNB ? n - rB : kNB);
+      double v[16];                                       // L_Bc^T: element (o, k) = W[rB + k][rC + o]
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int k = q * 16 + t;
+        v[t] = k < valid ? W[(rB + k) * ld + rC + o] : 0.0;
+      }
+      if (threadIdx.x == 0) {
+        unsigned f;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(zflag + B) : "memory");
+        } while (f == 0);
       }
       __syncthreads();
-      for (int C = blockIdx.x; C < B; C += gridDim.x) {   // tb_C -= L_BC^T z_B
-        const int64_t rC = (int64_t)C * kNB;
-        const int valid = (int)(n - rB < kNB ? n - rB : kNB);
-        const double upd = gemv64<true>(W + rB * ld + rC, ld, zb, valid);
-        if ((threadIdx.x & 3) == 0) tb[rC + (threadIdx.x >> 2)] -= upd;
-      }
+      if (threadIdx.x < kNB) zb[threadIdx.x] = (rB + threadIdx.x < n) ? __ldcg(z + rB + threadIdx.x) : 0.0;
+      __syncthreads();
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) acc = fma(v[t], zb[q * 16 + t], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (q == 0) xb[o] -= acc;
     }
-    grid_barrier(ctl, ctl + 1);
+    __syncthreads();
+    const double acc = gemv64<true>(Linv + (size_t)c * kNB * kNB, kNB, xb, kNB);   // Linv_cc^T tb_c
+    if (q == 0 && rC + o < n) z[rC + o] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(zflag + c), "r"(1u) : "memory");
+    }
   }
+  POTRF_MARK(73);
 }
 
 __global__ void potrf_tail_kernel(double* W, int64_t n, int64_t ld, int k, const double* panel,
@@ -633,7 +821,8 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 
 int64_t potrf_scratch_doubles(int64_t n) {
   const int64_t nb = (n + kNB - 1) / kNB;
-  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 1 /* grid barrier words */ + 2 * n /* solve */;
+  return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 1 /* grid barrier words */ + 2 * n /* solve */ +
+         (nb + 1) / 2 /* backward-solve block flags */;
 }
 
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
@@ -666,8 +855,8 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&ok, cudaDevAttrCooperativeLaunch, dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaFuncSetAttribute(potrf_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * kTileSmem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, potrf_persistent_kernel, kThreads, 3 * kTileSmem);
+      cudaFuncSetAttribute(potrf_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kTileSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, potrf_persistent_kernel, kThreads, 4 * kTileSmem);
       coop = (ok && per_sm >= 1) ? 1 : 0;
       grid = sms;
     }
@@ -675,6 +864,10 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
       unsigned* ctl = reinterpret_cast<unsigned*>(panel1 + n * kNB);
       cudaError_t e = cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), st);
       if (e != cudaSuccess) return e;
+      if (u) {                                           // backward-solve block flags (after tb)
+        e = cudaMemsetAsync(panel1 + n * kNB + 1 + 2 * n, 0, (size_t)nb * sizeof(unsigned), st);
+        if (e != cudaSuccess) return e;
+      }
       const int tiles0 = (nb - 1) * nb / 2;
       const int g = std::max(1, std::min(grid, tiles0));
       int64_t nn = n, ldd = ldW;
@@ -682,7 +875,7 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
       double* tb = ut + n;
       void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl, &u, &ut, &tb, &z};
       e = cudaLaunchCooperativeKernel((const void*)potrf_persistent_kernel, dim3(g), dim3(kThreads), args,
-                                      3 * kTileSmem, st);
+                                      4 * kTileSmem, st);
       if (launches) *launches += 1;
       if (solved && u && e == cudaSuccess) *solved = true;
       return e;

@@ -44,6 +44,10 @@ int main() {
       printf("  tail copy + last fwd block %.1f us, barrier %.1f us, backward solve %.1f us\n", (t[71] - t[70]) / 1e3,
              (t[72] - t[71]) / 1e3, (t[73] - t[72]) / 1e3);
       printf("  total (CTA 0) %.1f us\n", (t[73] - t[0]) / 1e3);
+      const char* nm[] = {"A + old loads", "GEMM X = A Linv^T", "X -> smem", "GEMM X X^T + diag -> smem",
+                          "(call)", "identity pad", "chol_inv64", "L/Linv store", "P copy"};
+      const int a0[] = {80, 81, 82, 83, 84, 85, 86, 87, 88}, a1[] = {81, 82, 83, 84, 85, 86, 87, 88, 89};
+      for (int i = 0; i < 9; ++i) printf("  step 5 critical: %-30s %.2f us\n", nm[i], (t[a1[i]] - t[a0[i]]) / 1e3);
     }
   }
   return 0;
