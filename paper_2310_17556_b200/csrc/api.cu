@@ -100,6 +100,8 @@ Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
   s.packed = packed_len(n) * sizeof(double);
   s.W = (size_t)n * n * sizeof(double);
   s.vec = (size_t)n * sizeof(double);
+  // row-GEMV chunk partials; also the F16X2 direct SYRK's per-split u partials (its split count
+  // P <= KB / 8 = ceil(m / 64) / 8 <= ceil(m / 512) = the fp64 chunk count)
   s.partials = (size_t)fs::gemv_rows_chunks(m, true) * n * sizeof(double);
   s.block_sums = (size_t)fs::residual_cols_blocks(m, true) * 2 * sizeof(double);
   s.r = (size_t)m * sizeof(double);
@@ -204,6 +206,15 @@ int eig_impl(fs_ctx* ctx, const double* Gp, int64_t n, cudaStream_t st) {
   return FS_OK;
 }
 
+// F16X2 direct (the SYRK splits fp32 S itself, no S_t16 copy), FS_F16_DIRECT=1.  Off by default:
+// the in-kernel split moves 288 KB of shared memory per K-block and CTA (TMA write + converter
+// read/write + MMA operand reads) against 160 KB for the pre-tiled planes, and the 128 B/clk
+// crossbar makes it slower than retile16 + the pre-tiled SYRK (4.3 vs 2.8 + 1.3 ms).
+bool f16_direct() {
+  static const int env = getenv("FS_F16_DIRECT") ? atoi(getenv("FS_F16_DIRECT")) : 0;
+  return env != 0;
+}
+
 // Gram stage.  TF32X3: retile S into S_t (optionally fused with u = S w), then the CTA-pair
 // tcgen05 SYRK on S_t.  FP64: exact-product SIMT SYRK on S.
 int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
@@ -214,7 +225,17 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
   if (rc) return rc;
   int l = 0;
   cudaError_t e;
-  if (use_tc == 2) {
+  if (use_tc == 2 && f16_direct() && fs::syrk_tc_supported(S, ldS)) {
+    // F16X2 direct: row scales from a sample, then the SYRK splits fp32 S itself (no S_t16 copy)
+    // and forms u = S w in the same pass.  The overflow flag is checked by the caller at its next
+    // host synchronisation.
+    e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = fs::row_scales((const float*)S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, &l);
+    if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
+    if (e == cudaSuccess)
+      e = fs::syrk_f16_direct((const float*)S, ldS, n, m, ctx->d_scale, ctx->d_inv_scale, w32, ctx->d_ovf,
+                              ctx->d_partials, u, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  } else if (use_tc == 2) {
     // F16X2: row scales from a sample, split planes (+ u = S w), kind::f16 SYRK.  The overflow
     // flag is checked by the caller at its next host synchronisation.
     if ((rc = ensure_tiles(ctx))) return rc;
@@ -721,7 +742,8 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
       return fail(ctx, FS_ENOMEM, "cannot allocate the host-entry buffers");
     }
   }
-  if (use_tc && (rc = ensure_tiles(ctx))) return rc;
+  const bool direct = use_tc == 2 && f16_direct() && fs::syrk_tc_supported(ctx->d_Sin, ldd);
+  if (use_tc && !direct && (rc = ensure_tiles(ctx))) return rc;
   ctx->n_marks = 0;
   prof_mark(ctx, -1, st);
   FS_CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st), "flag reset");
@@ -760,7 +782,17 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     for (int64_t c0 = 0; c0 < m; c0 += W, ++c) {
       const int64_t c1 = std::min(m, c0 + W);
       FS_CK(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
-      if (use_tc == 2) {
+      if (use_tc == 2 && direct) {
+        // F16X2 direct: row scales from the first chunk's columns, then the K-range SYRK splits the
+        // chunk in-kernel and accumulates u = S v
+        if (c == 0)
+          FS_CK(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
+        FS_CK(fs::syrk_f16_direct((const float*)S, ldd, n, m, ctx->d_scale, ctx->d_inv_scale, (const float*)v,
+                                  ctx->d_flag, ctx->d_partials, u, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms,
+                                  st, &l, (int)(c0 / fs::kTile16Cols),
+                                  (int)((c1 + fs::kTile16Cols - 1) / fs::kTile16Cols), c > 0),
+              "syrk_f16_direct");
+      } else if (use_tc == 2) {
         // F16X2: row scales from the first chunk's columns, then split planes + K-range SYRK
         if (c == 0)
           FS_CK(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
@@ -780,7 +812,7 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
               "syrk_tc");
       }
     }
-    FS_CK(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
+    if (!(use_tc == 2 && direct)) FS_CK(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
     ctx->launches += l;
     prof_mark(ctx, FS_PROF_GRAM, st);
     rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,

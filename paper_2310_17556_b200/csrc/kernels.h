@@ -77,6 +77,15 @@ cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double*
 cudaError_t syrk_f16(const uint8_t* St16, int64_t n, int64_t m, const double* inv_scale, double lam, double* G_packed,
                      double* ws, int num_sms, cudaStream_t st, int* launches, int kb_begin = 0, int kb_end = -1,
                      int accum = 0);
+// true when S (fp32, pitch ldS) meets the TMA alignment rules (16-byte base and pitch)
+bool syrk_tc_supported(const void* S, int64_t ldS);
+// F16X2 without the S_t16 copy: the SYRK reads fp32 S (row-major, pitch ldS) with 2-D TMA and
+// splits it in-kernel (identical hi/lo to retile16); u (+)= S v (v fp32, may be null) from the
+// diagonal tiles' converter pass via upart ([splits][n] doubles, splits <= num_sms / 2).
+cudaError_t syrk_f16_direct(const float* S, int64_t ldS, int64_t n, int64_t m, const float* scale,
+                            const double* inv_scale, const float* v, int* flags, double* upart, double* u, double lam,
+                            double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches,
+                            int kb_begin = 0, int kb_end = -1, int accum = 0);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,

@@ -64,12 +64,26 @@ constexpr int kRegsProducer = 56, kRegsConverter = 80, kRegsEpilogue = 184;
 constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 // F16X2 (tiles.cuh): a stage holds the hi+lo tiles of the A and B row blocks (4 x 16 KB), no
 // converter ring; kind::f16 MMAs (K = 16) on 64-column K-blocks
-template <bool kF16> constexpr int raw_stages() { return kF16 ? 3 : kRaw; }
+// F16X2 direct (kDirect): the SYRK reads fp32 S itself (2-D TMA, 64-column x 128-row boxes of
+// 256-byte rows) into a ring of kXS raw slots, and its converter warps write the hi/lo planes
+// into the same 2-stage operand ring the pre-tiled mode fills by bulk copy — no S_t16 round trip
+// through HBM (the 4.1 GB write + read that cost the retile pass 1.3 ms).
+constexpr int kXS = 3;                          // raw fp32 box slots (direct mode)
+constexpr int kXBytes = kBlk * kTile16Cols * 4; // one 128 x 64 fp32 box: 32 KB
+template <bool kF16, bool kDirect = false> constexpr int raw_stages() { return kDirect ? 2 : kF16 ? 3 : kRaw; }
 template <bool kF16> constexpr int lo_stages() { return kF16 ? 0 : kLo; }
 template <bool kF16> constexpr int stage_bytes() { return kF16 ? 4 * kBoxBytes : kStageBytes; }
-template <bool kF16> constexpr size_t smem_bytes() {
-  return (size_t)(raw_stages<kF16>() * stage_bytes<kF16>() + lo_stages<kF16>() * kStageBytes) + 1024 + 512;
+template <bool kF16, bool kDirect = false> constexpr size_t smem_bytes() {
+  return (size_t)(raw_stages<kF16, kDirect>() * stage_bytes<kF16>() + lo_stages<kF16>() * kStageBytes) +
+         (kDirect ? (size_t)kXS * kXBytes + 128 * 8 : 0) + 1024 + (kDirect ? 256 : 512);
 }
+struct DirectArgs {        // F16X2 direct mode inputs
+  const float* v;          // u = S v partials for the diagonal pair tiles' units (or null)
+  const float* scale;      // per-row power-of-two scales
+  int* flags;              // |= 1 non-finite input, |= 2 fp16 overflow
+  double* upart;           // [split][n] partial u
+  int64_t m;               // columns of S (v's length)
+};
 constexpr uint32_t kIdescF16 = ptx::idesc_f16(2 * kBlk, kN);
 
 struct Plan {
@@ -118,9 +132,16 @@ FS_DEVINL float tf32_lo(uint32_t xb) {
   return __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
 }
 
+FS_DEVINL float fmax3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // FS_SYRK_DBG bit 256: the leader's MMA thread records cycles spent waiting for operands / for
 // a free TMEM buffer, and the total (one row per cluster), printed by the host after the launch
 __device__ unsigned long long g_syrk_wait[74 * 4];
+__device__ unsigned long long g_conv_wait[74 * 4];   // FS_SYRK_DBG bit 512: converter warp 0 of the leader
 
 
 struct Ring {  // stage index + mbarrier phase of a circular buffer
@@ -129,28 +150,33 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
   FS_DEVINL void next(int depth) { if (++s == depth) { s = 0; ph ^= 1; } }
 };
 
-template <bool kF16>
+template <bool kF16, bool kDirect = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
                double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg, int kb_base,
                int accum, const double* __restrict__ inv_scale, const __grid_constant__ CUtensorMap tmap, int sym,
-               const __grid_constant__ UnitMap um, int units) {
-  constexpr int kRawS = raw_stages<kF16>();
+               const __grid_constant__ UnitMap um, int units, const DirectArgs da) {
+  constexpr int kRawS = raw_stages<kF16, kDirect>();
   constexpr int kLoS = lo_stages<kF16>();
   constexpr int kSB = stage_bytes<kF16>();
   constexpr int kBlkBytes = kF16 ? 2 * kBoxBytes : kBoxBytes;   // one row block's K-block (hi+lo for F16X2)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by offset, so the compiler keeps the shared window (LDS/STS, not generic)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* raw = smem;
   uint8_t* lo = smem + (size_t)kRawS * kSB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kRawS * kSB + (size_t)kLoS * kStageBytes);
+  uint8_t* xraw = smem + (size_t)kRawS * kSB + (size_t)kLoS * kStageBytes;   // direct: fp32 box slots
+  double* xu = reinterpret_cast<double*>(xraw + (kDirect ? (size_t)kXS * kXBytes : 0));   // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xu) + (kDirect ? 128 * 8 : 0));
   uint64_t* full = bars;                 // local TMA -> local converters / relay   [kRawS]
   uint64_t* conv = full + kRawS;         // both CTAs' converters -> leader MMA     [kRawS]
   uint64_t* empty = conv + kRawS;        // MMA (multicast) -> each producer        [kRawS]
   uint64_t* lo_free = empty + kRawS;     // MMA (multicast) -> each converter group [kLoS]
   uint64_t* tfull = lo_free + kLoS;      // MMA (multicast) -> each epilogue        [2]
   uint64_t* tempty = tfull + 2;          // both CTAs' epilogues -> leader MMA      [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xfull = tempty + 2;          // direct: TMA -> converters                [kXS]
+  uint64_t* xempty = xfull + kXS;        // direct: converters -> producer           [kXS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + kXS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();   // 0 = leader
@@ -166,6 +192,11 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 2);                // one elected arrive per CTA
     }
+    if (kDirect)
+      for (int s = 0; s < kXS; ++s) {
+        ptx::mbar_init(&xfull[s], 1);
+        ptx::mbar_init(&xempty[s], 1);
+      }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc2<kTmemCols>(tmem_slot);
@@ -177,7 +208,27 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
 
   if (wg == 0) {
     ptx::setmaxnreg_dec<kRegsProducer>();
-    if (warp == 0 && lane == 0) {
+    if (kDirect && warp == 0 && lane == 0) {
+      // ============ direct producer: fp32 boxes of S (own row blocks) -> raw slots ============
+      ptx::tma_prefetch_desc(&tmap);
+      Ring xr;
+      for (int u = cluster; u < units; u += nclusters) {
+        int t, kb0, nk;
+        unit_decode(um, u, P, KC, KB, t, kb0, nk);
+        int pp, qq; pair_of(tile0 + t, pp, qq);
+        const int rowA = (2 * pp + (int)crank) * kBlk, rowB = (2 * qq + (int)crank) * kBlk;
+        const bool diag = pp == qq;
+        for (int k = 0; k < nk; ++k) {
+          const int col = (kb_base + kb0 + k) * kTile16Cols;
+          for (int b = 0; b < (diag ? 1 : 2); ++b) {
+            ptx::mbar_wait(&xempty[xr.s], xr.ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&xfull[xr.s], kXBytes);
+            ptx::tma_load_2d(xraw + (size_t)xr.s * kXBytes, &tmap, &xfull[xr.s], col, b ? rowB : rowA);
+            xr.next(kXS);
+          }
+        }
+      }
+    } else if (!kDirect && warp == 0 && lane == 0) {
       // ============ bulk-copy producer (each CTA: its own pre-swizzled S_t tiles) ============
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
@@ -306,6 +357,134 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         g_syrk_wait[cluster * 4 + 3] = g_end - g_start;
       }
     }
+  } else if (wg == 1 && kDirect) {
+    // ====== F16X2 direct converters: fp32 box -> hi/lo fp16 planes (the retile16 arithmetic:
+    //        hi = fp16_rn(x s), lo = fp16_rn(x s - hi)) in the SWIZZLE_128B operand image; on
+    //        diagonal pair tiles also u = S v for this CTA's row block over the unit's K range ======
+    ptx::setmaxnreg_dec<kRegsConverter>();
+    const int ct = threadIdx.x - 128, cw = ct >> 5;
+    const int half16 = lane >> 4, cq = lane & 15, cj = cq >> 1, ch = cq & 1;
+    const uint32_t conv0 = ptx::mapa(ptx::smem_u32(conv), 0);
+    Ring cr, xr;
+    float amax = 0.f, xmax = 0.f;
+    long long cw_empty = 0, cw_full = 0, cw_work = 0, cw_bar = 0;
+    const long long cw_t0 = clock64();
+    for (int u = cluster; u < units; u += nclusters) {
+      int t, kb0, nk;
+      unit_decode(um, u, P, KC, KB, t, kb0, nk);
+      int pp, qq; pair_of(tile0 + t, pp, qq);
+      const bool diag = pp == qq;
+      const int64_t rowA = (int64_t)(2 * pp + (int)crank) * kBlk, rowB = (int64_t)(2 * qq + (int)crank) * kBlk;
+      const bool want_u = diag && da.v != nullptr;
+      if (want_u) xu[ct] = 0.0;
+      // lane l holds the scale of row (step l/2 of this warp, half l%2) for the A and B boxes;
+      // a step fetches its row's scale with one shuffle
+      float scA, scB;
+      {
+        const int r = ((lane >> 1) * 4 + cw) * 2 + (lane & 1);
+        scA = rowA + r < n ? __ldg(da.scale + rowA + r) : 1.f;
+        scB = rowB + r < n ? __ldg(da.scale + rowB + r) : 1.f;
+      }
+      ptx::named_bar_sync(1, 128);
+      for (int k = 0; k < nk; ++k) {
+        const int64_t col0 = (int64_t)(kb_base + kb0 + k) * kTile16Cols + 4 * cq;
+        float4 vv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (want_u) {
+          const float* vp = da.v + col0;
+          vv.x = col0 < da.m ? vp[0] : 0.f;
+          vv.y = col0 + 1 < da.m ? vp[1] : 0.f;
+          vv.z = col0 + 2 < da.m ? vp[2] : 0.f;
+          vv.w = col0 + 3 < da.m ? vp[3] : 0.f;
+        }
+        long long c0 = (dbg & 512) ? clock64() : 0;
+        ptx::mbar_wait(&empty[cr.s], cr.ph ^ 1);               // operand stage free (MMA done)
+        if (dbg & 512) { const long long c1 = clock64(); cw_empty += c1 - c0; c0 = c1; }
+        uint8_t* stg = raw + (size_t)cr.s * kSB;
+        for (int b = 0; b < (diag ? 1 : 2); ++b) {
+          if (dbg & 512) c0 = clock64();
+          ptx::mbar_wait(&xfull[xr.s], xr.ph);
+          if (dbg & 512) { const long long c1 = clock64(); cw_full += c1 - c0; c0 = c1; }
+          const uint8_t* src = xraw + (size_t)xr.s * kXBytes;
+          uint8_t* hi = stg + b * 2 * kBoxBytes;
+          const float scb = b ? scB : scA;
+          const bool ub = want_u && b == 0;
+          // row r = ((g + q) * 4 + cw) * 2 + half16 with g a multiple of 8: r & 7 is per-thread
+          // constant, so is the swizzled column offset
+          const int swz = ((cj ^ ((cw * 2 + half16) & 7)) << 4) + ch * 8;
+#pragma unroll 1
+          for (int g = 0; g < kBlk / 8; g += 8) {
+            // all eight shared loads of the group first (latency once per group, not per step)
+            float4 x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int r = ((g + q) * 4 + cw) * 2 + half16;
+              x[q] = *reinterpret_cast<const float4*>(src + r * (kTile16Cols * 4) + cq * 16);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int step = g + q;
+              const int r = (step * 4 + cw) * 2 + half16;
+              const float sc = __shfl_sync(0xffffffffu, scb, step * 2 + half16);
+              // packed fp32x2 arithmetic (FMUL2/FFMA2): the same IEEE results as the scalar ops
+              const float2 s2 = make_float2(sc, sc), m1 = make_float2(-1.f, -1.f);
+              const float2 y01 = __fmul2_rn(make_float2(x[q].x, x[q].y), s2);
+              const float2 y23 = __fmul2_rn(make_float2(x[q].z, x[q].w), s2);
+              const __half2 h01 = __float22half2_rn(y01), h23 = __float22half2_rn(y23);
+              const float2 r01 = __ffma2_rn(__half22float2(h01), m1, y01);   // y - hi, exact
+              const float2 r23 = __ffma2_rn(__half22float2(h23), m1, y23);
+              const __half2 l01 = __float22half2_rn(r01), l23 = __float22half2_rn(r23);
+              // NaN-propagating maxima: |x| (non-finite input) and |x s| (>= 65520: fp16 overflow)
+              amax = fmax3_nan(amax, fabsf(y01.x), fabsf(y01.y));
+              amax = fmax3_nan(amax, fabsf(y23.x), fabsf(y23.y));
+              xmax = fmax3_nan(xmax, fabsf(x[q].x), fabsf(x[q].y));
+              xmax = fmax3_nan(xmax, fabsf(x[q].z), fabsf(x[q].w));
+              const int off = r * 128 + swz;
+              uint2 hv, lv;
+              hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+              lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+              *reinterpret_cast<uint2*>(hi + off) = hv;
+              *reinterpret_cast<uint2*>(hi + kBoxBytes + off) = lv;
+            }
+            if (ub) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float p = fmaf(x[q].w, vv.w, fmaf(x[q].z, vv.z, fmaf(x[q].y, vv.y, x[q].x * vv.x)));
+                p += __shfl_xor_sync(0xffffffffu, p, 1);
+                p += __shfl_xor_sync(0xffffffffu, p, 2);
+                p += __shfl_xor_sync(0xffffffffu, p, 4);
+                p += __shfl_xor_sync(0xffffffffu, p, 8);
+                if (cq == 0) xu[((g + q) * 4 + cw) * 2 + half16] += (double)p;
+              }
+            }
+          }
+          if (dbg & 512) { const long long c1 = clock64(); cw_work += c1 - c0; c0 = c1; }
+          ptx::named_bar_sync(1, 128);                         // every read of the raw slot done
+          if (dbg & 512) { const long long c1 = clock64(); cw_bar += c1 - c0; c0 = c1; }
+          if (ct == 0) ptx::mbar_arrive(&xempty[xr.s]);
+          xr.next(kXS);
+        }
+        ptx::fence_async_smem();                               // generic writes -> async proxy
+        ptx::named_bar_sync(1, 128);
+        if (ct == 0) ptx::mbar_arrive_cluster(conv0 + cr.s * 8);
+        cr.next(kRawS);
+      }
+      if (want_u) {
+        ptx::named_bar_sync(1, 128);
+        const int64_t row = rowA + ct;
+        if (row < n) da.upart[(int64_t)(u - (um.nt ? um.base[t] : t * P)) * n + row] = xu[ct];
+      }
+    }
+    if ((dbg & 512) && ct == 0 && crank == 0 && cluster < 74) {
+      g_conv_wait[cluster * 4 + 0] = cw_empty;
+      g_conv_wait[cluster * 4 + 1] = cw_full;
+      g_conv_wait[cluster * 4 + 2] = cw_work;
+      g_conv_wait[cluster * 4 + 3] = clock64() - cw_t0;
+      (void)cw_bar;
+    }
+    // the retile16 rules: non-finite input; isinf(fp16_rn(x s)) <=> |x s| >= 65520
+    const bool bad = !isfinite(xmax), ovf = !bad && amax >= 65520.f;
+    const unsigned bb = __ballot_sync(0xffffffffu, bad), bo = __ballot_sync(0xffffffffu, ovf);
+    if (lane == 0 && (bb | bo)) atomicOr(da.flags, (bb ? 1 : 0) | (bo ? 2 : 0));
   } else if (wg == 1 && kF16) {
     // ====== F16X2 relay: own TMA completion -> leader's conv barrier; on diagonal pair tiles
     //        (symmetric mode) the hi/2 plane is written into the stage's free half first ======
@@ -533,16 +712,27 @@ cudaError_t st16_tensor_map(CUtensorMap* map, const uint8_t* St16, int64_t n, in
                             kTile16Cols, 2 * kTileRows);
 }
 
-template <bool kF16>
+// u[i] (+)= sum over the diagonal tiles' splits of the direct mode's partial u (fixed order)
+__global__ void reduce_upart_kernel(const double* __restrict__ upart, int nsplit, int64_t n, double* __restrict__ u,
+                                    int accum) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int q = 0; q < nsplit; ++q) s += upart[(int64_t)q * n + i];
+  u[i] = (accum ? u[i] : 0.0) + s;
+}
+
+template <bool kF16, bool kDirect = false>
 cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
                         cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum,
-                        const double* inv_scale) {
+                        const double* inv_scale, const float* S32 = nullptr, int64_t ldS = 0,
+                        DirectArgs da = DirectArgs{}, double* u = nullptr) {
   Plan p = make_plan(n, m, num_sms, prow0, prow1, kb_begin, kb_end, kF16 ? kTile16Cols : kBK);
   if (p.tiles <= 0 || p.KB <= 0) return cudaSuccess;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel<kF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes<kF16>());
+    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel<kF16, kDirect>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<kF16, kDirect>());
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -552,7 +742,7 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
   // measured: 10% fewer SM cycles but a 9% lower clock (the re-split K windows cost DRAM reads and
   // power) and a longer reduce: net slower at the headline, so off unless FS_SYRK_SYM=1
   static const int sym_env = getenv("FS_SYRK_SYM") ? atoi(getenv("FS_SYRK_SYM")) : 0;
-  const int sym = (kF16 && !p.direct && sym_env && p.tiles <= kMaxMapTiles) ? 1 : 0;
+  const int sym = (kF16 && !kDirect && !p.direct && sym_env && p.tiles <= kMaxMapTiles) ? 1 : 0;
   UnitMap um;
   memset(&um, 0, sizeof um);
   int units = p.tiles * p.P, clusters = p.clusters;
@@ -590,13 +780,18 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
   }
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
-  if (kF16) {
+  if (kDirect) {
+    // fp32 S: 64-column x 128-row boxes (256-byte rows, no swizzle; rows >= n / cols >= m read as 0)
+    cudaError_t e = make_tensor_map_2d(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, S32, (uint64_t)m, (uint64_t)n,
+                                       (uint64_t)ldS * 4, kTile16Cols, kBlk);
+    if (e != cudaSuccess) return e;
+  } else if (kF16) {
     cudaError_t e = st16_tensor_map(&tmap, St, n, m);
     if (e != cudaSuccess) return e;
   }
-  syrk_tc_kernel<kF16><<<2 * clusters, kThreads, smem_bytes<kF16>(), st>>>(
+  syrk_tc_kernel<kF16, kDirect><<<2 * clusters, kThreads, smem_bytes<kF16, kDirect>(), st>>>(
       St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
-      p.kb_base, accum, inv_scale, tmap, sym, um, units);
+      p.kb_base, accum, inv_scale, tmap, sym, um, units, da);
   if (launches) *launches += 1;
   if (dbg & 256) {
     unsigned long long h[74 * 4] = {};
@@ -609,9 +804,24 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
     if (c) fprintf(stderr, "syrk mma thread: wait operands %.0f%%, wait tmem %.0f%%, %.0f kcycles in %.3f ms -> %.0f MHz (%d clusters)\n",
                    100 * wd / tot, 100 * wt / tot, tot / c / 1e3, ns / c / 1e6, tot / ns * 1e3, c);
   }
+  if ((dbg & 512) && kDirect) {
+    unsigned long long h[74 * 4] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_conv_wait, sizeof h);
+    double we = 0, wf = 0, ww = 0, tot = 0;
+    for (int i = 0; i < 74; ++i)
+      if (h[i * 4 + 3]) { we += h[i * 4]; wf += h[i * 4 + 1]; ww += h[i * 4 + 2]; tot += h[i * 4 + 3]; }
+    if (tot > 0)
+      fprintf(stderr, "syrk converter warp: wait stage %.0f%%, wait fp32 box %.0f%%, convert %.0f%%, rest %.0f%%\n",
+              100 * we / tot, 100 * wf / tot, 100 * ww / tot, 100 * (tot - we - wf - ww) / tot);
+  }
   if (!p.direct) {
     syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum, inv_scale,
                                                             sym, um);
+    if (launches) *launches += 1;
+  }
+  if (kDirect && da.v && u) {   // the diagonal pair tiles' units (uniform split P) hold u's partials
+    reduce_upart_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(da.upart, p.P, n, u, accum);
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
@@ -622,6 +832,16 @@ cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double*
                     cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum) {
   return syrk_launch<false>(St, n, m, lam, G_packed, ws, num_sms, st, launches, prow0, prow1, kb_begin, kb_end, accum,
                             nullptr);
+}
+
+cudaError_t syrk_f16_direct(const float* S, int64_t ldS, int64_t n, int64_t m, const float* scale,
+                            const double* inv_scale, const float* v, int* flags, double* upart, double* u, double lam,
+                            double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches, int kb_begin,
+                            int kb_end, int accum) {
+  if (!syrk_tc_supported(S, ldS)) return cudaErrorNotSupported;
+  DirectArgs da{v, scale, flags, upart, m};
+  return syrk_launch<true, true>(nullptr, n, m, lam, G_packed, ws, num_sms, st, launches, 0, -1, kb_begin, kb_end,
+                                 accum, inv_scale, S, ldS, da, u);
 }
 
 cudaError_t syrk_f16(const uint8_t* St16, int64_t n, int64_t m, const double* inv_scale, double lam, double* G_packed,
