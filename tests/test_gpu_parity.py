@@ -806,3 +806,42 @@ def test_large_n_takes_the_direct_and_two_pass_paths(fsb, n, m):
     assert O.rel_err(b.x.cpu().numpy(), ref.x) <= 1e-10
     a2, r2 = fsb.residual(system, b.x)
     assert r2 == b.rel_residual
+
+
+# ---------------------------------------------------------------- cluster x+y pass boundaries
+
+@pytest.mark.parametrize("n", [1, 29, 30, 31, 121, 250, 1100, 1200, 1201])
+@pytest.mark.parametrize("m", [1, 65, 4099])
+def test_xy_pass_shapes_match_oracle(fsb, n, m):
+    """The fused x = (v - S^T z)/lam, y = S x pass (cols_solve_y_cl: 4-CTA clusters, 30-row chunks,
+    256-byte panels; n <= 1200) at chunk/panel/rank boundaries — n below one chunk, ranks with no
+    rows, partial last chunks and panels, and n = 1201 on the fallback kernel — in fp64 mode (exact
+    products), with the stored residual reproduced bit for bit by residual()."""
+    rng = np.random.Generator(np.random.PCG64(7 * n + m))
+    S = rng.standard_normal((n, m)) / np.sqrt(max(n, 1))
+    v = rng.standard_normal(m)
+    lam = 1e-2
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    sol = fsb.solve_chol(system, precision="fp64", refine=False)
+    ref = O.solve_chol(S, v, lam)
+    assert O.rel_err(sol.x, ref.x) <= 1e-10, O.rel_err(sol.x, ref.x)
+    assert abs(sol.rel_residual - ref.rel_residual) <= 1e-9 + 1e-6 * ref.rel_residual
+    abs_res, rel_res = fsb.residual(system, sol.x, fsb.Variant.PLAIN)
+    assert sol.abs_residual == abs_res and sol.rel_residual == rel_res
+
+
+@pytest.mark.parametrize("n,m", [(250, 4099), (1024, 20000)])
+def test_xy_pass_refinement_accumulates(fsb, n, m):
+    """Refinement steps run the x pass in accumulate mode (x += (r - S^T dz)/lam): in the cluster
+    kernel the old x reaches every CTA through rank 0's exchange, so no CTA can read an x that rank 0
+    already overwrote.  f16x2 + 4 refinement steps must land on the fp64 solve."""
+    rng = np.random.Generator(np.random.PCG64(n + 3 * m))
+    S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(np.float32)
+    v = rng.standard_normal(m).astype(np.float32)
+    lam = 1e-2
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
+    x0 = fsb.solve_chol(system, precision="f16x2", refine=False).x
+    x4 = fsb.solve_chol(system, precision="f16x2", refine=4).x
+    assert O.rel_err(x4, ref.x) < 0.1 * O.rel_err(x0, ref.x)
+    assert O.rel_err(x4, ref.x) <= 1e-9, O.rel_err(x4, ref.x)
