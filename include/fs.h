@@ -144,10 +144,12 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
 /* ---- one-shot solve from HOST buffers (the same call with S, v, x in host memory) ----
  * What a numpy caller of solvers.py:197 solve_chol(system) hands over: S (n x m, leading
  * dimension ldS, row-major), v (length m, S's dtype) and x (fp64 out) in host memory —
- * page-locked for full overlap.  S is uploaded in column chunks (>= 32 MB, at most 16; 2-D
+ * page-locked for full overlap.  S is uploaded in column chunks (>= 32 MB, about 16; 2-D
  * copies of all rows) on a second stream; the Gram and u = S v of each chunk's K range run
  * while the next chunk is in flight, so the transfer hides all but the last chunk's share.  Non-finite entries in S or v are detected on the device
- * and return FS_EINVAL (core.py:108-119 rejects them).  Synchronizes. */
+ * and return FS_EINVAL (core.py:108-119 rejects them).  The last chunks taper (halving widths)
+ * so little Gram work is left after the final transfer, and x is downloaded while the residual
+ * pass runs; unless FS_OK is returned the contents of x are unspecified.  Synchronizes. */
 int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host, int64_t n, int64_t m,
                        int64_t ldS, const void* v_host, double lam, double* x_host, fs_allreduce_fn allreduce,
                        void* allreduce_user, int flags, double refine_above, int64_t* pivot,

@@ -66,6 +66,11 @@ struct fs_ctx {
   static constexpr int kMaxChunks = 64;
   cudaEvent_t ev_chunk[kMaxChunks] = {};
   cudaEvent_t ev_free = nullptr;
+  // host entry: x is copied to the caller's buffer on up_st as soon as the first x pass ends,
+  // overlapping the residual pass (state 1 = the copy holds the final x, 2 = x changed since)
+  double* early_x_host = nullptr;
+  int early_x_state = 0;
+  cudaEvent_t ev_xready = nullptr, ev_xcopy = nullptr;
   // stage timing (fs_profile_enable): events recorded on the solve stream after each stage,
   // in chronological order; stage time = gap to the previous mark
   static constexpr int kMaxMarks = 24;
@@ -343,6 +348,14 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
   };
   if ((rc = solve_cols(v, vdt == FS_F64, lam, false))) return rc;
   prof_mark(ctx, FS_PROF_GEMV_STZ, st);
+  if (ctx->early_x_host) {   // host entry: x -> host on up_st while the residual pass runs
+    FS_CK(cudaEventRecord(ctx->ev_xready, st), "event");
+    FS_CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_xready, 0), "event wait");
+    FS_CK(cudaMemcpyAsync(ctx->early_x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->up_st),
+          "x d2h (early)");
+    FS_CK(cudaEventRecord(ctx->ev_xcopy, ctx->up_st), "event");
+    ctx->early_x_state = 1;
+  }
   double abs_res = NAN, rel_res = NAN;
   // refinement steps: FS_FLAG_REFINE alone = the reference's single step; bits 8-15 raise it
   const int max_steps = want_refine ? std::max(1, (flags >> 8) & 0xFF) : 0;
@@ -391,6 +404,10 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
       if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
     }
     // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
+    if (ctx->early_x_state == 1) {   // x changes: the early copy must finish reading it first
+      FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");
+      ctx->early_x_state = 2;
+    }
     if ((rc = solve_cols(ctx->d_r, 1, -lam, true))) return rc;
   }
   if (!want_res) {
@@ -512,6 +529,8 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   for (int i = 0; i < fs_ctx::kMaxChunks; ++i)
     if (ctx->ev_chunk[i]) cudaEventDestroy(ctx->ev_chunk[i]);
   if (ctx->ev_free) cudaEventDestroy(ctx->ev_free);
+  if (ctx->ev_xready) cudaEventDestroy(ctx->ev_xready);
+  if (ctx->ev_xcopy) cudaEventDestroy(ctx->ev_xcopy);
   if (ctx->up_st) cudaStreamDestroy(ctx->up_st);
   delete ctx;
 }
@@ -734,7 +753,9 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
               cudaMalloc((void**)&ctx->d_flag, sizeof(int)) == cudaSuccess &&
               cudaMallocHost((void**)&ctx->h_flag, sizeof(int)) == cudaSuccess &&
               cudaStreamCreateWithFlags(&ctx->up_st, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaEventCreateWithFlags(&ctx->ev_free, cudaEventDisableTiming) == cudaSuccess;
+              cudaEventCreateWithFlags(&ctx->ev_free, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_xready, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->ev_xcopy, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; ok && i < fs_ctx::kMaxChunks; ++i)
       ok = cudaEventCreateWithFlags(&ctx->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
@@ -769,8 +790,13 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
   const void* S = ctx->d_Sin;
   const void* v = ctx->d_vin;
   double* x = ctx->d_xin;
+  ctx->early_x_host = x_host;   // finish_x starts the x download as soon as x exists
+  struct EarlyReset {          // every exit path leaves the context without a pending host target
+    fs_ctx* c;
+    ~EarlyReset() { c->early_x_host = nullptr; c->early_x_state = 0; }
+  } early_reset{ctx};
   if (use_tc) {
-    // K-chunks of >= 32 MB (at most 16): upload columns [c0, c1) of all rows -> retile them (+ u
+    // K-chunks of >= 32 MB (about 16, then tapering): upload columns [c0, c1) of all rows -> retile them (+ u
     // partials + finiteness) -> SYRK over their K-blocks, accumulated into the packed Gram.  The
     // transfer of chunk c+1 overlaps the kernels of chunk c; only the last chunk's share is exposed.
     double* u = ctx->d_packed + n * (n + 1) / 2;
@@ -778,9 +804,16 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     const int64_t by_bytes = ((int64_t)(32 << 20) / (n * (int64_t)elem) + CW - 1) / CW * CW;
     const int64_t by_count = (m + 16 * CW - 1) / (16 * CW) * CW;
     const int64_t W = std::max<int64_t>(CW, std::max(by_bytes, by_count));
+    // tapered schedule: full chunks while more than two remain, then halving ones, so the Gram
+    // share left exposed after the last transfer is a few K-blocks instead of a full chunk
+    auto next_width = [&](int64_t rest) -> int64_t {
+      if (rest > 2 * W) return W;
+      const int64_t w = std::max<int64_t>(CW, (rest / 2 + CW - 1) / CW * CW);
+      return rest - w < CW ? rest : w;
+    };
     int c = 0;
-    for (int64_t c0 = 0; c0 < m; c0 += W, ++c) {
-      const int64_t c1 = std::min(m, c0 + W);
+    for (int64_t c0 = 0, c1 = 0; c0 < m; c0 = c1, ++c) {
+      c1 = std::min(m, c0 + (c + 1 < fs_ctx::kMaxChunks ? next_width(m - c0) : m - c0));
       FS_CK(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
       if (use_tc == 2 && direct) {
         // F16X2 direct: row scales from the first chunk's columns, then the K-range SYRK splits the
@@ -827,9 +860,17 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     rc = fs_chol_solve(ctx, dtype, precision, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
                        refine_above, pivot, out_res, stream);
   }
-  if (rc != FS_OK && rc != FS_NOT_PD) return rc;
+  const int early = ctx->early_x_state;
+  ctx->early_x_host = nullptr;
+  ctx->early_x_state = 0;
+  if (early) FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");   // the early copy is done
+  if (rc != FS_OK && rc != FS_NOT_PD) {
+    cudaStreamSynchronize(st);
+    return rc;
+  }
   FS_CK(cudaMemcpyAsync(ctx->h_flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
-  if (rc == FS_OK) FS_CK(cudaMemcpyAsync(x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, st), "x d2h");
+  if (rc == FS_OK && early != 1)
+    FS_CK(cudaMemcpyAsync(x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, st), "x d2h");
   FS_CK(cudaStreamSynchronize(st), "sync");
   if (*ctx->h_flag & 1) {
     if (pivot) *pivot = -1;
