@@ -177,6 +177,13 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
 int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, void* out,
                      int64_t ldo, void* stream);
 
+/* ---- input validation (core.py:108-119: np.isfinite(S).all() on construction) ----
+ * FS_OK when all rows x cols entries (row-major, leading dimension ld) of the device array a are
+ * finite, FS_EINVAL when one is not (or on bad arguments).  One streaming pass on the device of
+ * the current CUDA context, no temporaries; complex data is passed as its real view (2 cols per
+ * element).  No context needed.  Synchronizes `stream`. */
+int fs_all_finite(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,7 @@ SIGNATURES = {
                                      ctypes.POINTER(_c_int64), _dp, _vp]),
     "fs_embed_complex": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                         _c_int64, _vp]),
+    "fs_all_finite": (ctypes.c_int, [ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp]),
     "fs_chol_solve_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                           ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,
                                           ctypes.POINTER(_c_int64), _dp, _vp]),
@@ -128,6 +129,28 @@ class Context:
 
 
 _contexts: dict[int, Context] = {}
+
+
+def all_finite(t) -> bool:
+    """True when every entry of the CUDA tensor t (1-D, or 2-D row-major with unit column stride;
+    complex via its real view) is finite — fs_all_finite, one device pass, no temporaries
+    (replaces torch.isfinite(t).all(), which materialised |t| and a bool copy of S)."""
+    import torch
+    if t.is_complex():
+        r = torch.view_as_real(t)
+        rows, cols, ld = (1, 2 * t.numel(), 2 * t.numel()) if t.dim() == 1 else (t.shape[0], 2 * t.shape[1], 2 * t.stride(0))
+        base, dt = r, (FS_F64 if r.dtype == torch.float64 else FS_F32)
+    else:
+        rows, cols, ld = (1, t.numel(), t.numel()) if t.dim() == 1 else (t.shape[0], t.shape[1], t.stride(0))
+        base, dt = t, (FS_F64 if t.dtype == torch.float64 else FS_F32)
+    if t.dim() == 2 and t.stride(1) != 1 or t.dim() == 1 and t.stride(0) != 1:
+        raise ValueError("all_finite needs unit column stride")
+    lib = load()
+    with torch.cuda.device(t.device):
+        rc = lib.fs_all_finite(dt, base.data_ptr(), rows, cols, ld, torch.cuda.current_stream(t.device).cuda_stream)
+    if rc not in (0, 1):
+        raise NativeLibraryError(f"fs_all_finite failed (status {rc})")
+    return rc == 0
 
 
 def context_for(device: int, n: int, m: int) -> Context:

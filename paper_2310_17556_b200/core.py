@@ -117,7 +117,7 @@ def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.T
         t = t.to(dev, non_blocking=True).contiguous()
         if force_copy and isinstance(a, torch.Tensor) and t.data_ptr() == a.data_ptr():
             t = t.clone()
-    if t.numel() and not bool(torch.isfinite(t).all()):
+    if t.numel() and not _lib.all_finite(t):
         raise ValueError(f"{name} must contain only finite entries")
     return t
 

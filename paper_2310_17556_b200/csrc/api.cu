@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 
 #include "../../include/fs.h"
@@ -971,6 +972,32 @@ int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n,
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "embed_complex");
   return FS_OK;
+}
+
+int fs_all_finite(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, void* stream) {
+  if (!a || rows < 0 || cols < 0 || ld < cols || (dtype != FS_F32 && dtype != FS_F64)) return FS_EINVAL;
+  if (rows == 0 || cols == 0) return FS_OK;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return FS_ECUDA;
+  // one flag word per device (device int + page-locked host copy), created on first use
+  struct Flag { int* d = nullptr; int* h = nullptr; };
+  static Flag flags[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return FS_EINVAL;
+  Flag& f = flags[dev];
+  if (!f.d && (cudaMalloc((void**)&f.d, sizeof(int)) != cudaSuccess ||
+               cudaMallocHost((void**)&f.h, sizeof(int)) != cudaSuccess))
+    return FS_ENOMEM;
+  cudaStream_t st = (cudaStream_t)stream;
+  int l = 0;
+  if (cudaMemsetAsync(f.d, 0, sizeof(int), st) != cudaSuccess ||
+      fs::check_finite(a, dtype == FS_F64, rows, cols, ld, f.d, sms, st, &l) != cudaSuccess ||
+      cudaMemcpyAsync(f.h, f.d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return FS_ECUDA;
+  return (*f.h & 1) ? FS_EINVAL : FS_OK;
 }
 
 }  // extern "C"
