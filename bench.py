@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--precision", default="f16x2", choices=["f16x2", "tf32x3", "fp64"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU (column-sharded, NCCL) code path even at one rank (a 1-rank NCCL group)")
     ap.add_argument("--cpu-repeats", type=int, default=2)
     return ap.parse_args()
 
@@ -207,7 +209,12 @@ def run_b200(args, rank, world, local):
 
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=device)
     n, m, lam = args.n, args.m, args.lam
     a, b = column_shard(m, world, rank)
@@ -219,20 +226,25 @@ def run_b200(args, rank, world, local):
     ctx = _lib.context_for(local, n, m_local)
     ctx.profile(True)
     system = None
-    if world == 1:
+    sm = None
+    if not sharded:
         # device-resident public API: ScoreMatrix copies S once into its own aligned device buffer
         # (construction, outside the timed region; the reference copies its array the same way)
         system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    else:
+        # the shard is validated and aligned once (as the single-GPU DampedSystem is), then every
+        # step is one fs_chol_solve per rank with the NCCL all-reduce callback
+        sm = fsb.ScoreMatrix(S)
 
     stage_acc = {k: [] for k in _lib.PROF_STAGES}
 
     def one_step():
-        if world == 1:
+        if not sharded:
             sol = fsb.solve_chol(system, precision=args.precision)
             for k, val in ctx.stage_ms().items():
                 stage_acc[k].append(val)
             return sol.rel_residual
-        sol = sharded_solve_chol_fused(S, v, lam, precision=args.precision)
+        sol = sharded_solve_chol_fused(sm, v, lam, precision=args.precision)
         for k, val in ctx.stage_ms().items():
             stage_acc[k].append(val)
         return sol.rel_residual
@@ -246,7 +258,7 @@ def run_b200(args, rank, world, local):
     stream = torch.cuda.current_stream(device)
     launches0 = ctx.launches()
     with ClockSampler(local) as clk:
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -255,11 +267,11 @@ def run_b200(args, rank, world, local):
         rels = [one_step() for _ in range(args.steps)]
         ev1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             dist.barrier()
     launches = ctx.launches() - launches0
     elapsed = ev0.elapsed_time(ev1)
-    if world > 1:
+    if sharded:
         t = torch.tensor([elapsed], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
@@ -267,29 +279,48 @@ def run_b200(args, rank, world, local):
 
     # ---- end to end through the public API with host buffers (N=1, rank 0) ----
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         S_host = torch.empty((n, m_local), dtype=dtype, pin_memory=True)
         S_host.copy_(S)
         v_host = torch.empty(m_local, dtype=dtype, pin_memory=True)
         v_host.copy_(v)
         Sh, vh = S_host.numpy(), v_host.numpy()
-        fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=args.precision)  # warm
+
+        def e2e_step():
+            # the call a user makes with host (numpy) buffers: the single-GPU public API, or per rank
+            # the sharded one (same pipelined host entry + the NCCL all-reduce callback)
+            if not sharded:
+                out = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=args.precision).x
+            else:
+                out = sharded_solve_chol_fused(fsb.ScoreMatrix(Sh), vh, lam, precision=args.precision).x_local
+            assert isinstance(out, np.ndarray)
+
+        e2e_step()   # warm
         torch.cuda.synchronize()
+        if sharded:
+            dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=args.precision)
-            assert isinstance(sol.x, np.ndarray)
+            e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        e2e = {"value": e0.elapsed_time(e1) / args.e2e_steps, "unit": "ms",
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if sharded:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": e2e_ms, "unit": "ms",
                "h2d_bytes_per_step": int(Sh.nbytes + vh.nbytes), "d2h_bytes_per_step": int(m_local * 8 + 16),
-               "path": "solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v)) -> numpy x"}
+               "path": ("solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v)) -> numpy x"
+                        if not sharded else
+                        "per rank: sharded_solve_chol_fused(ScoreMatrix(pinned numpy shard), numpy v shard) -> numpy x"
+                        " shard; max over ranks")}
         del S_host, v_host
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.destroy_process_group()
         return 0
 
@@ -363,7 +394,7 @@ def run_b200(args, rank, world, local):
         "gpu_launches": launches,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 

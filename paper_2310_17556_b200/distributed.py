@@ -196,27 +196,59 @@ def nccl_allreduce_fn(device: torch.device, group=None):
     return _lib.ALLREDUCE_FN(fn)
 
 
-def sharded_solve_chol_fused(S_local: torch.Tensor, v_local: torch.Tensor, lam: float, *, precision: str = "auto",
+def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "auto",
                              diagnostics: bool = True, refine: int = 0, group=None) -> ShardedSolution:
-    """The column-sharded solve through ONE fs_chol_solve call per rank: the same fused kernels as
-    the single-GPU path on the local shard (retile + u, tcgen05 SYRK, x + y pass, residual), with
-    the C ABI's all-reduce callback doing the three exchanges ([G | u], y, the norms) over NCCL."""
-    from .core import _to_device_tensor
-    dev = S_local.device
-    S = _to_device_tensor(S_local, "score matrix", dev)        # aligned rows (no copy when already)
-    v = v_local.to(dev).to(S.dtype).contiguous()
-    n, m = int(S.shape[0]), int(S.shape[1])
-    prec = resolve_precision(precision, S.dtype)
-    ctx = _lib.context_for(dev.index, n, m)
-    x = torch.empty(m, dtype=torch.float64, device=dev)
+    """The column-sharded solve through ONE C-ABI call per rank: the same fused kernels as the
+    single-GPU path on the local shard (retile + u, tcgen05 SYRK, x + y pass, residual), with the
+    C ABI's all-reduce callback doing the three exchanges ([G | u], y, the norms) over NCCL.
+
+    S_local: a CUDA tensor (validated and aligned here), a ScoreMatrix already on the device (used
+    as is: validated once at construction), or a host shard (numpy / host-origin ScoreMatrix) —
+    the latter goes through fs_chol_solve_host (pipelined column-chunk upload overlapped with the
+    Gram) and returns x_local on the host."""
+    from .core import ScoreMatrix, _to_device_tensor
+    from .solvers import _pinned_out
+    dev = torch.device("cuda", torch.cuda.current_device())
+    host = None
+    if isinstance(S_local, ScoreMatrix):
+        if S_local.is_uploaded or not S_local.host_origin:
+            S = S_local.tensor
+            dev = S.device
+        else:
+            host = S_local.host_array
+    elif isinstance(S_local, torch.Tensor) and S_local.is_cuda:
+        dev = S_local.device
+        S = _to_device_tensor(S_local, "score matrix", dev)    # aligned rows (no copy when already)
+    else:
+        host = ScoreMatrix(S_local).host_array                 # numpy shard: validated on the device
     piv = ctypes.c_int64(-1)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
     flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (refine << 8)) if refine else 0)
     cb = nccl_allreduce_fn(dev, group)
-    rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0), v.data_ptr(),
-                               float(lam), x.data_ptr(), cb, None, flags, REFINE_ABOVE_REL, ctypes.byref(piv), res,
-                               _stream(dev))
+    if host is not None:
+        n, m = int(host.shape[0]), int(host.shape[1])
+        vh = np.ascontiguousarray(v_local.detach().cpu().numpy() if isinstance(v_local, torch.Tensor)
+                                  else np.asarray(v_local), dtype=host.dtype)
+        prec = resolve_precision(precision, torch.float32 if host.dtype == np.float32 else torch.float64)
+        ctx = _lib.context_for(dev.index, n, m)
+        x = _pinned_out.get(m)
+        dt = _lib.FS_F32 if host.dtype == np.float32 else _lib.FS_F64
+        rc = ctx.lib.fs_chol_solve_host(ctx.handle, dt, PRECISIONS[prec], host.ctypes.data, n, m,
+                                        host.strides[0] // host.itemsize, vh.ctypes.data, float(lam), x.ctypes.data,
+                                        cb, None, flags, REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(dev))
+        what = "fs_chol_solve_host"
+    else:
+        v = v_local.to(dev).to(S.dtype).contiguous() if isinstance(v_local, torch.Tensor) else \
+            torch.as_tensor(np.asarray(v_local), device=dev).to(S.dtype).contiguous()
+        n, m = int(S.shape[0]), int(S.shape[1])
+        prec = resolve_precision(precision, S.dtype)
+        ctx = _lib.context_for(dev.index, n, m)
+        x = torch.empty(m, dtype=torch.float64, device=dev)
+        rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
+                                   v.data_ptr(), float(lam), x.data_ptr(), cb, None, flags, REFINE_ABOVE_REL,
+                                   ctypes.byref(piv), res, _stream(dev))
+        what = "fs_chol_solve"
     if rc == _lib.FS_NOT_PD:
         raise FactorizationError(f"Gram matrix is not positive definite at pivot {piv.value}", pivot=int(piv.value))
-    _check(ctx, rc, "fs_chol_solve")
+    _check(ctx, rc, what)
     return ShardedSolution(x_local=x, abs_residual=float(res[0]), rel_residual=float(res[1]), refined=refine > 0)

@@ -784,6 +784,16 @@ def test_fused_sharded_entry_with_nccl_callback(fsb):
         b = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(St), lam, vt), precision="f16x2")
         assert torch.equal(a.x_local, b.x)
         assert a.rel_residual == b.rel_residual
+        # a pre-validated device ScoreMatrix (bench's per-step call) and a host (numpy) shard
+        # through the pipelined host entry with the same NCCL callback
+        c = sharded_solve_chol_fused(fsb.ScoreMatrix(St), vt, lam, precision="f16x2")
+        assert torch.equal(c.x_local, b.x)
+        S32, v32 = S.astype(np.float32), v.astype(np.float32)
+        h = sharded_solve_chol_fused(S32, v32, lam, precision="f16x2")
+        hb = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32), precision="f16x2")
+        assert isinstance(h.x_local, np.ndarray)
+        np.testing.assert_array_equal(h.x_local, hb.x)
+        assert O.rel_err(h.x_local, b.x.cpu().numpy()) <= 1e-6
     finally:
         if created:
             dist.destroy_process_group()
