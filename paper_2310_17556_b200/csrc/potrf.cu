@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kNB = 64;
 constexpr int kThreads = 256;
-constexpr int kLd = kNB + 1;   // padded smem row
+constexpr int kLd = kNB + 4;   // padded smem row (68: conflict-free DMMA fragment loads)
 
 // ---------------------------------------------------------------- block-level helpers
 
@@ -347,12 +347,15 @@ __device__ void factor_diag(double* W, int64_t n, int64_t ld, int kk, int64_t* s
   if (tr) POTRF_MARK(85);
   if (!preloaded) load_tile(W, n, ld, r0, r0, A);
   __syncthreads();
-  for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {   // identity padding, lower only
-    const int r = e >> 6, c = e & 63;
-    if (c > r) A[r][c] = 0.0;
-    else if (r >= b) A[r][c] = (r == c) ? 1.0 : 0.0;
+  // chol_inv64 reads only the lower triangle (its GEMMs touch A10, A11 and the factors), so only
+  // a partial last block needs padding: identity rows r >= b
+  if (b < kNB) {
+    for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) {
+      const int r = e >> 6, c = e & 63;
+      if (r >= b && c <= r) A[r][c] = (r == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (tr) POTRF_MARK(86);
   const int f = chol_inv64(A, X, T);
   if (tr) POTRF_MARK(87);
@@ -570,10 +573,8 @@ __device__ void critical_tile(double* W, int64_t n, int64_t ld, int k, double* L
 #pragma unroll
     for (int j = 0; j < 4; ++j) A[frag_row(i)][frag_col(i, j)] = old[i][j] - acc[i][j];
   if (tr) POTRF_MARK(84);
-  factor_diag(W, n, ld, I, status, Linv, A, X, T, true, tr);   // L_II -> W, Linv_II -> Linv and X
-  __syncthreads();
+  factor_diag(W, n, ld, I, status, Linv, A, P, T, true, tr);   // L_II -> W, Linv_II -> Linv and P
   if (tr) POTRF_MARK(88);
-  for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) P[e >> 6][e & 63] = X[e >> 6][e & 63];
   if (tr) POTRF_MARK(89);
 }
 
@@ -662,11 +663,8 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
   POTRF_MARK(0);
   if (blockIdx.x == 0 && *(volatile int64_t*)status == 0) {
     double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
-    double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
     double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
-    factor_diag(W, n, ld, 0, status, Linv, A, X, T, false);
-    __syncthreads();
-    for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) P[e >> 6][e & 63] = X[e >> 6][e & 63];
+    factor_diag(W, n, ld, 0, status, Linv, A, P, T, false);   // Linv_00 stays in P
   }
   POTRF_MARK(1);
   grid_barrier(ctl, ctl + 1);
