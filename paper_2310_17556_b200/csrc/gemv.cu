@@ -453,23 +453,25 @@ constexpr int kCL = 4;                           // CTAs per cluster (row split)
 constexpr int kCLCW = 15;                        // consumer warps
 constexpr int kCLCons = kCLCW * kWarp;
 constexpr int kCLThreads = kCLCons + kWarp;
-constexpr int kCLRows = 2 * kCLCW;               // rows per chunk (TMA box outer dimension): 2 per warp
-constexpr int kCLChunk = kCLRows * 256;          // 7.5 KB per chunk slot (128-byte aligned)
-constexpr int kCLMaxV = 10;                      // chunks per CTA and panel -> 300 rows per CTA
-constexpr int kCLMaxRows = kCL * kCLRows * kCLMaxV;   // n <= 1200
+// 28 rows per chunk (TMA box outer dimension) = 14 row pairs: two per x-group warp and at most
+// two per y-group warp (with 30 rows one x warp carried three pairs and paced the whole pass)
+constexpr int kCLRows = 28;
+constexpr int kCLChunk = kCLRows * 256;          // 7 KB per chunk slot (128-byte aligned)
+constexpr int kCLMaxV = 11;                      // chunks per CTA and panel -> 308 rows per CTA
+constexpr int kCLMaxRows = kCL * kCLRows * kCLMaxV;   // n <= 1232
 constexpr int kCLG = 3;                          // chunks per batch of shared loads (y group)
 constexpr int kCLXW = 7;                         // x-group warps (partial sums, exchange, x)
 constexpr int kCLYW = kCLCW - kCLXW;             // y-group warps (8)
 constexpr int kCLXThreads = kCLXW * kWarp;
 constexpr int kCLSets = 8;                       // max panel slot-sets in the ring
-constexpr int kCLSlotsMax = 27;                  // 27 x 7.5 KB + the fixed buffers fit 227 KB
+constexpr int kCLSlotsMax = 30;                  // 30 x 7 KB + the fixed buffers fit 227 KB
 constexpr size_t kCLFixed = 2 * kCLXW * 64 * 8 + 2 * (kCL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
 constexpr size_t kCLSmem = 1024 + (size_t)kCLSlotsMax * kCLChunk + kCLFixed;
 
-// chunks per CTA: the template instance (3, 6, 9 or 10) covering ceil(n / (kCL * 30))
+// chunks per CTA: the template instance (3, 6, 10 or 11) covering ceil(n / (kCL * 28))
 inline int cl_nch(int64_t n) {
   const int c = (int)((n + kCL * kCLRows - 1) / (kCL * kCLRows));
-  return c <= 3 ? 3 : c <= 6 ? 6 : c <= 9 ? 9 : 10;
+  return c <= 3 ? 3 : c <= 6 ? 6 : c <= 10 ? 10 : 11;
 }
 
 // remote (DSMEM) store that completes 8 transaction bytes on the receiving CTA's mbarrier: the
@@ -716,8 +718,8 @@ cudaError_t launch_cols_solve_y_cl(int nch, unsigned grid, cudaStream_t st, cons
   switch (nch) {
     case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3>); break;
     case 6: pick(cols_solve_y_cl_kernel<TS, TV, 6>); break;
-    case 9: pick(cols_solve_y_cl_kernel<TS, TV, 9>); break;
-    default: pick(cols_solve_y_cl_kernel<TS, TV, 10>); break;
+    case 10: pick(cols_solve_y_cl_kernel<TS, TV, 10>); break;
+    default: pick(cols_solve_y_cl_kernel<TS, TV, 11>); break;
   }
   return cudaGetLastError();
 }
@@ -884,7 +886,7 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
   // recomputed y = S x is bit-identical to the solve's (test_solvers.py:109-114)
   const size_t smem = cy_smem_bytes<TS>(n);
   if (smem > 200 * 1024 || !aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
-  // n <= 1200: the cluster kernel (S read from HBM once, in 256-byte TMA rows)
+  // n <= 1232: the cluster kernel (S read from HBM once, in 256-byte TMA rows)
   static const int cl_env = getenv("FS_CY_CL") ? atoi(getenv("FS_CY_CL")) : 1;
   CUtensorMap smap;
   memset(&smap, 0, sizeof smap);
@@ -895,7 +897,7 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
     const int64_t panels = (m + 256 / (int64_t)sizeof(TS) - 1) / (256 / (int64_t)sizeof(TS));
     static int max_cl = 0;
     if (!max_cl) {
-      auto probe = cols_solve_y_cl_kernel<TS, float, 9>;
+      auto probe = cols_solve_y_cl_kernel<TS, float, 10>;
       cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCLSmem);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(kCL * 64));
