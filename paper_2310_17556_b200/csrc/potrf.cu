@@ -117,9 +117,10 @@ __device__ __forceinline__ double fast_rsqrt(double d) {
 // predicates); entries a[c] with c > lane are never read back.  Returns the first
 // non-positive (or NaN) pivot, or -1.  (A shuffle broadcast measured slower: 2 SHFL per
 // double, tools/ubench/chol32_steps.cu.)
-__device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbuf)[32]) {
+// (single-warp version, kept for tools/ubench/chol64_phases.cu and potrf_parts.cu)
+[[maybe_unused]] __device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbuf)[32]) {
   const int lane = threadIdx.x & 31;
-  double a[32], sx[32], rsq[32];
+  double a[32], sx[32], dj[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     a[c] = (c <= lane) ? A[lane * kLd + c] : 0.0;
@@ -134,7 +135,7 @@ __device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbu
     const double d = cb[j];
     fail = (fail < 0 && !(d > 0.0)) ? j : fail;
     const double dinv = fast_rcp(d);
-    rsq[j] = fast_rsqrt(d);
+    dj[j] = d;                             // the sqrt scaling is formed after the sweep (off the chain)
     const double t = a[j] * dinv;
     const double y = sx[j] * dinv;
 #pragma unroll
@@ -151,8 +152,60 @@ __device__ __noinline__ int warp_chol_inv32(double* A, double* X, double (*colbu
   if (fail < 0) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
-      A[lane * kLd + c] = (c <= lane) ? a[c] * rsq[c] : 0.0;
-      X[c * kLd + lane] = sx[c] * rsq[c];
+      const double rsq = fast_rsqrt(dj[c]);
+      A[lane * kLd + c] = (c <= lane) ? a[c] * rsq : 0.0;
+      X[c * kLd + lane] = sx[c] * rsq;
+    }
+  }
+  return fail;
+}
+
+// The same factorisation + inverse with TWO warps (threads 0-63): thread (h, r) keeps row r's
+// columns c = 2i + h (i < 16) of A and of the inverse's right-hand side, so each warp issues half
+// of a step's fp64 updates.  Step j: the half owning column j publishes A[.][j] and x~[.][j]
+// (double-buffered), one 64-thread named barrier, then every thread updates its columns c > j.
+__device__ __noinline__ int chol_inv32_2w(double* A, double* X, double (*colbuf)[32], double (*ybuf)[32]) {
+  const int r = threadIdx.x & 31, h = (threadIdx.x >> 5) & 1;
+  double a[16], sx[16], dj[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int c = 2 * i + h;
+    a[i] = (c <= r) ? A[r * kLd + c] : 0.0;
+    sx[i] = (c == r) ? 1.0 : 0.0;
+  }
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double* cb = colbuf[j & 1];
+    double* yb = ybuf[j & 1];
+    if (h == (j & 1)) {
+      cb[r] = a[j >> 1];
+      yb[r] = sx[j >> 1];
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const double d = cb[j];
+    fail = (fail < 0 && !(d > 0.0)) ? j : fail;
+    const double dinv = fast_rcp(d);
+    if (h == (j & 1)) dj[j >> 1] = d;
+    const double t = cb[r] * dinv;
+    const double y = yb[r] * dinv;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 2 * i + h;
+      if (2 * i + 1 > j && c > j) {          // (the first test is compile-time)
+        const double lc = cb[c];
+        a[i] = fma(-t, lc, a[i]);
+        sx[i] = fma(-lc, y, sx[i]);
+      }
+    }
+  }
+  if (fail < 0) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 2 * i + h;
+      const double rsq = fast_rsqrt(dj[i]);
+      A[r * kLd + c] = (c <= r) ? a[i] * rsq : 0.0;
+      X[c * kLd + r] = sx[i] * rsq;
     }
   }
   return fail;
@@ -201,11 +254,12 @@ __device__ void store32_dmma(double* C, const double acc[2][2], double scale, bo
 __device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) {
   __shared__ int sfail;
   __shared__ __align__(16) double colbuf[2][32];
+  __shared__ __align__(16) double ybuf[2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) {
-    const int f = warp_chol_inv32(&A[0][0], &X[0][0], colbuf);
-    if (lane == 0) sfail = f;
-  } else if (warp == 1) {
+  if (warp < 2) {
+    const int f = chol_inv32_2w(&A[0][0], &X[0][0], colbuf, ybuf);
+    if (threadIdx.x == 0) sfail = f;
+  } else if (warp == 2) {
     for (int c = 0; c < 32; ++c) X[lane][32 + c] = 0.0;
   }
   __syncthreads();
@@ -218,9 +272,9 @@ __device__ int chol_inv64(double (*A)[kLd], double (*X)[kLd], double (*T)[kLd]) 
   gemm32_dmma<true>(&A[32][0], &A[32][0], acc);    // A11 -= L10 L10^T (reads A10, writes A11)
   store32_dmma(&A[32][32], acc, -1.0, true);
   __syncthreads();
-  if (warp == 0) {
-    const int f = warp_chol_inv32(&A[32][32], &X[32][32], colbuf);
-    if (lane == 0) sfail = f < 0 ? -1 : 32 + f;
+  if (warp < 2) {
+    const int f = chol_inv32_2w(&A[32][32], &X[32][32], colbuf, ybuf);
+    if (threadIdx.x == 0) sfail = f < 0 ? -1 : 32 + f;
   }
   __syncthreads();
   if (sfail >= 0) return sfail;

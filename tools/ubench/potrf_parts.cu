@@ -4,9 +4,9 @@
 using namespace fs;
 __global__ void __launch_bounds__(256) parts_kernel(const double* W, long long* t, int reps) {
   extern __shared__ double dsm[];
-  double (*A)[65] = reinterpret_cast<double (*)[65]>(dsm);
-  double (*X)[65] = reinterpret_cast<double (*)[65]>(dsm + 64 * 65);
-  double (*B)[65] = reinterpret_cast<double (*)[65]>(dsm + 2 * 64 * 65);
+  double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
+  double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 64 * kLd);
+  double (*B)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * 64 * kLd);
   for (int rep = 0; rep < reps; ++rep) {
     long long c0 = clock64();
     load_tile(W, 64, 64, 0, 0, A);
@@ -38,9 +38,9 @@ int main() {
   for (int i = 0; i < 64; ++i) for (int j = 0; j < 64; ++j) h[i * 64 + j] = (i == j ? 64.0 : 0.0) + 1.0 / (1 + i + j);
   double* d; cudaMalloc(&d, sizeof h); cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice);
   long long* t; cudaMalloc(&t, 6 * 8 * 4);
-  cudaFuncSetAttribute(parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 65 * 8);
+  cudaFuncSetAttribute(parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * kLd * 8);
   for (int launch = 0; launch < 2; ++launch) {
-    parts_kernel<<<1, 256, 3 * 64 * 65 * 8>>>(d, t, 3);
+    parts_kernel<<<1, 256, 3 * 64 * kLd * 8>>>(d, t, 3);
     long long ht[18]; cudaMemcpy(ht, t, sizeof ht, cudaMemcpyDeviceToHost);
     for (int rep = 0; rep < 3; ++rep)
       printf("launch %d rep %d cycles: load %lld  chol_inv32 %lld  chol_inv64 %lld  gemm_nt64 %lld  (%s)\n", launch, rep,
