@@ -491,13 +491,27 @@ __device__ void step_tile(double* W, int64_t n, int64_t ld, int k, double* Linv,
     copy_panel(W + (kc - kNB), ld, pan_prev, rI, n);
     if (I == k + 1) copy_panel(W + (kc - kNB), ld, pan_prev, kc, n);
   }
-  {
-    const double* li = Linv + (size_t)k * kNB * kNB;
-    for (int e = threadIdx.x; e < kNB * kNB; e += kThreads) Lk[e >> 6][e & 63] = li[e];
-  }
   if (tr) POTRF_MARK(81);
-  load_tile(W, n, ld, rI, kc, XI);                 // A_Ik
-  if (I != J) load_tile(W, n, ld, rJ, kc, XJ);     // A_Jk
+  {
+    // Linv_kk, A_Ik and A_Jk: all 48 loads of a thread in flight before the first store (one L2
+    // round trip instead of three)
+    const double* li = Linv + (size_t)k * kNB * kNB;
+    double vl[kPer], vi[kPer], vj[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      vl[u] = li[e];
+      vi[u] = (rI + r < n && kc + c < n) ? W[(rI + r) * ld + kc + c] : 0.0;
+      vj[u] = (I != J && rJ + r < n && kc + c < n) ? W[(rJ + r) * ld + kc + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      Lk[r][c] = vl[u];
+      XI[r][c] = vi[u];
+      if (I != J) XJ[r][c] = vj[u];
+    }
+  }
   __syncthreads();
   if (tr) POTRF_MARK(82);
   // X_I = A_Ik Linv_kk^T, X_J = A_Jk Linv_kk^T (the panel TRSM as GEMMs)
