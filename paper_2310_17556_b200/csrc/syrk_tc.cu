@@ -38,6 +38,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -86,6 +87,9 @@ struct DirectArgs {        // F16X2 direct mode inputs
 };
 constexpr uint32_t kIdescF16 = ptx::idesc_f16(2 * kBlk, kN);
 
+constexpr int kMaxSplitLarge = 8;                        // split-K factor cap when tiles >= clusters
+constexpr size_t kMaxSplitWsBytes = (size_t)2 << 30;      // ... and its fp64 partials (2 GB)
+
 struct Plan {
   int nb, np, tile0, tiles, P, clusters, KB, KC, D, kb_base;
   bool direct;
@@ -100,11 +104,19 @@ struct UnitMap {
   int kc[kMaxMapTiles];
 };
 
-FS_DEVINL void unit_decode(const UnitMap& um, int u, int P, int KC, int KB, int& t, int& kb0, int& nk) {
+// Uniform split, unit order: tile-major (u = t * P + q) while every unit has its own cluster —
+// measured faster at the headline (10 tiles x 7 splits: 2.76 vs 3.05 ms split-major) — and
+// split-major (u = q * tiles + t, signalled by a negative P) when the clusters run several units
+// each: the clusters of a round then walk the same K range of every tile, so tiles sharing a row
+// block share it in L2 (n = 8192: 205.6 vs 214.8 ms tile-major).
+FS_DEVINL int unit_split(const UnitMap& um, int u, int P, int tiles, int t) {
+  return um.nt ? u - um.base[t] : P < 0 ? u / tiles : u % P;
+}
+FS_DEVINL void unit_decode(const UnitMap& um, int u, int P, int KC, int KB, int tiles, int& t, int& kb0, int& nk) {
   int q;
   if (um.nt == 0) {
-    t = u / P;
-    q = u % P;
+    t = P < 0 ? u % tiles : u / P;
+    q = P < 0 ? u / tiles : u % P;
     kb0 = q * KC;
     nk = min(KC, KB - kb0);
     return;
@@ -214,7 +226,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       Ring xr;
       for (int u = cluster; u < units; u += nclusters) {
         int t, kb0, nk;
-        unit_decode(um, u, P, KC, KB, t, kb0, nk);
+        unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
         int pp, qq; pair_of(tile0 + t, pp, qq);
         const int rowA = (2 * pp + (int)crank) * kBlk, rowB = (2 * qq + (int)crank) * kBlk;
         const bool diag = pp == qq;
@@ -233,7 +245,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
         int t, kb0, nk;
-        unit_decode(um, u, P, KC, KB, t, kb0, nk);
+        unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
         int pp, qq; pair_of(tile0 + t, pp, qq);
         const int blkA = 2 * pp + (int)crank, blkB = 2 * qq + (int)crank;
         const bool diag = pp == qq;                       // A == B: one tile
@@ -269,7 +281,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
       for (int u = cluster; u < units; u += nclusters) {
         int t, kb0, nk;
-        unit_decode(um, u, P, KC, KB, t, kb0, nk);
+        unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
         int pp, qq; pair_of(tile0 + t, pp, qq);
         const int b_off = (pp == qq) ? 0 : kBlkBytes;
         uint32_t dacc = 0;
@@ -371,7 +383,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     const long long cw_t0 = clock64();
     for (int u = cluster; u < units; u += nclusters) {
       int t, kb0, nk;
-      unit_decode(um, u, P, KC, KB, t, kb0, nk);
+      unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
       int pp, qq; pair_of(tile0 + t, pp, qq);
       const bool diag = pp == qq;
       const int64_t rowA = (int64_t)(2 * pp + (int)crank) * kBlk, rowB = (int64_t)(2 * qq + (int)crank) * kBlk;
@@ -471,7 +483,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
       if (want_u) {
         ptx::named_bar_sync(1, 128);
         const int64_t row = rowA + ct;
-        if (row < n) da.upart[(int64_t)(u - (um.nt ? um.base[t] : t * P)) * n + row] = xu[ct];
+        if (row < n) da.upart[(int64_t)unit_split(um, u, P, tiles, t) * n + row] = xu[ct];
       }
     }
     if ((dbg & 512) && ct == 0 && crank == 0 && cluster < 74) {
@@ -494,7 +506,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     Ring rr;
     for (int u = cluster; u < units; u += nclusters) {
       int t, kb0, nk;
-      unit_decode(um, u, P, KC, KB, t, kb0, nk);
+      unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
       int pp, qq; pair_of(tile0 + t, pp, qq);
       const bool half_plane = sym && pp == qq;
       for (int k = 0; k < nk; ++k) {
@@ -526,7 +538,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     Ring rr, lr;
     for (int u = cluster; u < units; u += nclusters) {
       int t, kb0, nk;
-      unit_decode(um, u, P, KC, KB, t, kb0, nk);
+      unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
       int pp, qq; pair_of(tile0 + t, pp, qq);
       const int nvec = ((pp == qq) ? 1 : 2) * (kBoxBytes / 16);
       for (int k = 0; k < nk; ++k) {
@@ -563,7 +575,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     uint32_t chunk = 0;
     for (int u = cluster; u < units; u += nclusters) {
       int t, kb0, nk;
-      unit_decode(um, u, P, KC, KB, t, kb0, nk);
+      unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
       int pp, qq; pair_of(tile0 + t, pp, qq);
       const int nch = (nk + D - 1) / D;
       const size_t slot = direct ? (size_t)blockIdx.x : ((size_t)u * 2 + crank);
@@ -627,7 +639,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
 // Fixed-order sum of the P split-K partial tiles -> packed lower Gram (+λ on the diagonal).
 // Block (t, c): pair tile t, CTA half c (row block 2p+c).
 constexpr int kRedSplit = 16;   // blocks per (pair tile, CTA half): 2048 elements each
-__global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, int64_t n, double lam,
+__global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int tiles, int P, int64_t n, double lam,
                                double* __restrict__ Gp, int accum, const double* __restrict__ inv_scale, int sym,
                                const __grid_constant__ UnitMap um) {
   const int tc = blockIdx.x / kRedSplit, part = blockIdx.x % kRedSplit;
@@ -640,14 +652,19 @@ __global__ void syrk_tc_reduce(const double* __restrict__ ws, int tile0, int P, 
     const int64_t gi = (int64_t)(2 * pp + c) * kBlk + r, gj = (int64_t)(2 * qq) * kBlk + col;
     if (gi >= n || gj > gi) continue;
     const int tt = tc >> 1;
-    const int u0 = um.nt ? um.base[tt] : tt * P, nu = um.nt ? um.base[tt + 1] - um.base[tt] : P;
+    const int nu = um.nt ? um.base[tt + 1] - um.base[tt] : (P < 0 ? -P : P);
+    // unit of split q: map mode base[t] + q; uniform tile-major t * P + q, split-major (P < 0)
+    // q * tiles + t
+    auto unit = [&](int q) -> size_t {
+      return um.nt ? (size_t)um.base[tt] + q : P < 0 ? (size_t)q * tiles + tt : (size_t)tt * P + q;
+    };
     double s = 0.0;
-    for (int q = 0; q < nu; ++q) s += ws[(((size_t)u0 + q) * 2 + c) * kBlk * kN + e];
+    for (int q = 0; q < nu; ++q) s += ws[(unit(q) * 2 + c) * kBlk * kN + e];
     if (sym && pp == qq) {
       // symmetric mode on a diagonal pair tile: G = D + D^T; D(j, i) sits in the half of row j
       const int jl = (int)(gj - (int64_t)(2 * qq) * kBlk), il = c * kBlk + r;   // pair-local indices
       const int c2 = jl / kBlk, r2 = jl % kBlk;
-      for (int q = 0; q < nu; ++q) s += ws[(((size_t)u0 + q) * 2 + c2) * kBlk * kN + (size_t)il * kBlk + r2];
+      for (int q = 0; q < nu; ++q) s += ws[(unit(q) * 2 + c2) * kBlk * kN + (size_t)il * kBlk + r2];
     }
     if (inv_scale) s *= inv_scale[gi] * inv_scale[gj];
     double* g = Gp + gi * (gi + 1) / 2 + gj;
@@ -676,7 +693,25 @@ Plan make_plan(int64_t n, int64_t m, int num_sms, int prow0 = 0, int prow1 = -1,
   p.kb_base = kb_begin;
   p.KB = kb_end - kb_begin;
   const int max_clusters = num_sms / 2;
-  p.P = p.tiles >= max_clusters ? 1 : std::max(1, std::min(max_clusters / p.tiles, p.KB / 8));
+  if (p.tiles >= max_clusters) {
+    // whole pair tiles per unit leave a partial last round (n = 8192: 528 tiles on 74 clusters =
+    // 7.14 rounds run as 8); split-K units of 1/P tile even it out when the workspace allows:
+    // minimise ceil(tiles P / clusters) / P
+    // (a split costs L2 sharing and a reduce pass: only worth it when it removes > 8% of the
+    // rounds — n = 4096, 136 tiles: direct 41.2 ms, 7 splits 43.0 ms)
+    p.P = 1;
+    const double direct_rounds = std::ceil((double)p.tiles / max_clusters);
+    double best = direct_rounds;
+    for (int P = 2; P <= kMaxSplitLarge && p.KB / P >= 8; ++P) {
+      if ((size_t)2 * p.tiles * P * kBlk * kN * sizeof(double) > kMaxSplitWsBytes) break;
+      const double t = std::ceil((double)p.tiles * P / max_clusters) / P;
+      if (t < best - 1e-9) { best = t; p.P = P; }
+    }
+    static const int large_split = getenv("FS_SYRK_LARGE_SPLIT") ? atoi(getenv("FS_SYRK_LARGE_SPLIT")) : 1;
+    if (best > 0.92 * direct_rounds || !large_split) p.P = 1;
+  } else {
+    p.P = std::max(1, std::min(max_clusters / p.tiles, p.KB / 8));
+  }
   p.KC = (p.KB + p.P - 1) / p.P;          // K-blocks per split, contiguous in m
   p.P = (p.KB + p.KC - 1) / p.KC;          // every split non-empty
   p.clusters = std::min(p.tiles * p.P, max_clusters);
@@ -697,10 +732,17 @@ bool syrk_tc_supported(const void* S, int64_t ldS) {
 }
 
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms) {
-  // one fp64 128x256 partial per CTA of a split-K unit (<= num_sms CTAs) or per resident CTA
-  // (direct): never more than num_sms slots for ANY (n, m)
-  (void)n; (void)m;
-  return (size_t)num_sms * kBlk * kN * sizeof(double);
+  // one fp64 128x256 partial per CTA of a split-K unit, or per resident CTA (direct mode).  Units
+  // <= clusters while the pair tiles are fewer than the clusters; with more tiles make_plan may
+  // split each tile up to kMaxSplitLarge ways within kMaxSplitWsBytes — sized here for the
+  // largest n the context serves, which covers every smaller (n, m).
+  (void)m;
+  const int64_t nb = (n + kBlk - 1) / kBlk, np = (nb + 1) / 2, tiles = np * (np + 1) / 2;
+  size_t slots = (size_t)num_sms;
+  if (tiles >= num_sms / 2)
+    slots = std::max(slots, std::min((size_t)2 * tiles * kMaxSplitLarge,
+                                     kMaxSplitWsBytes / ((size_t)kBlk * kN * sizeof(double))));
+  return slots * kBlk * kN * sizeof(double);
 }
 
 namespace {
@@ -778,6 +820,8 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
     units = acc;
     clusters = std::min(units, maxc);
   }
+  // split-major unit order (signalled by a negative P) when clusters run several units each
+  const int p_arg = (p.P > 1 && p.tiles * p.P > p.clusters) ? -p.P : p.P;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
   if (kDirect) {
@@ -790,7 +834,7 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
     if (e != cudaSuccess) return e;
   }
   syrk_tc_kernel<kF16, kDirect><<<2 * clusters, kThreads, smem_bytes<kF16, kDirect>(), st>>>(
-      St, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
+      St, n, (int)tiles_nb(n), p.tile0, p.tiles, p_arg, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
       p.kb_base, accum, inv_scale, tmap, sym, um, units, da);
   if (launches) *launches += 1;
   if (dbg & 256) {
@@ -816,8 +860,8 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
               100 * we / tot, 100 * wf / tot, 100 * ww / tot, 100 * (tot - we - wf - ww) / tot);
   }
   if (!p.direct) {
-    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.P, n, lam, G_packed, accum, inv_scale,
-                                                            sym, um);
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.tiles, p_arg, n, lam, G_packed, accum,
+                                                            inv_scale, sym, um);
     if (launches) *launches += 1;
   }
   if (kDirect && da.v && u) {   // the diagonal pair tiles' units (uniform split P) hold u's partials
