@@ -597,6 +597,107 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double*
   step_tile(W, n, ld, k, Linv, panel0, panel1, status, blockIdx.x, dsm);
 }
 
+// ---- two-phase steps (large n: the step-0 trailing tiles outnumber the CTAs) ----
+// The one-phase step recomputes the panel product X_I = A_Ik Linv_kk^T in every tile (I, J) that
+// needs it (three 64^3 products per tile).  With many tiles per CTA it pays to form each X_I once:
+// phase A writes L_{I,k} = X_I in place into W (each row block by one CTA; CTA 0 forms X_{k+1}
+// on its critical path) plus the forward substitution ut_I -= X_I t_k; a grid barrier; phase B
+// updates every trailing tile with one product A_IJ -= X_I X_J^T from W's column block k.
+__device__ void panel_row_inplace(double* W, int64_t n, int64_t ld, int k, int I, const double* Linv, double* dsm,
+                                  double* ut, double* tb, bool record_t) {
+  double (*Lk)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
+  double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+  const int64_t kc = (int64_t)k * kNB, rI = (int64_t)I * kNB;
+  {
+    const double* li = Linv + (size_t)k * kNB * kNB;
+    double vl[kPer], vi[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      vl[u] = li[e];
+      vi[u] = (rI + r < n && kc + c < n) ? W[(rI + r) * ld + kc + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      Lk[r][c] = vl[u];
+      XI[r][c] = vi[u];
+    }
+  }
+  __syncthreads();
+  double acc[4][4];
+  gemm_nt(XI, Lk, acc);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      XI[frag_row(i)][frag_col(i, j)] = acc[i][j];
+      const int64_t gi = rI + frag_row(i);
+      if (gi < n) W[gi * ld + kc + frag_col(i, j)] = acc[i][j];
+    }
+  __syncthreads();
+  if (ut) {   // t_k = Linv_kk ut_k (ut_k final since step k-1), then ut_I -= L_Ik t_k
+    __shared__ double uk[kNB], tk[kNB];
+    if (threadIdx.x < kNB) uk[threadIdx.x] = (kc + threadIdx.x < n) ? ut[kc + threadIdx.x] : 0.0;
+    __syncthreads();
+    {
+      const double a = gemv64<false>(&Lk[0][0], kLd, uk, kNB);
+      const int o = threadIdx.x >> 2;
+      if ((threadIdx.x & 3) == 0) {
+        tk[o] = a;
+        if (record_t && kc + o < n) tb[kc + o] = a;
+      }
+    }
+    __syncthreads();
+    if (I < (n + kNB - 1) / kNB) {
+      const double a = gemv64<false>(&XI[0][0], kLd, tk, kNB);
+      const int o = threadIdx.x >> 2;
+      if ((threadIdx.x & 3) == 0 && rI + o < n) ut[rI + o] -= a;
+    }
+  }
+}
+
+// A_IJ -= X_I X_J^T with X_I = L_{I,k}, X_J = L_{J,k} from W's column block k (phase B)
+__device__ void update_tile(double* W, int64_t n, int64_t ld, int k, int I, int J, double* dsm) {
+  double (*XI)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
+  double (*XJ)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
+  const int64_t kc = (int64_t)k * kNB, rI = (int64_t)I * kNB, rJ = (int64_t)J * kNB;
+  {
+    double vi[kPer], vj[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      vi[u] = (rI + r < n) ? W[(rI + r) * ld + kc + c] : 0.0;
+      vj[u] = (I != J && rJ + r < n) ? W[(rJ + r) * ld + kc + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = u * kThreads + threadIdx.x, r = e >> 6, c = e & 63;
+      XI[r][c] = vi[u];
+      if (I != J) XJ[r][c] = vj[u];
+    }
+  }
+  double old[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gi = rI + frag_row(i), gj = rJ + frag_col(i, j);
+      old[i][j] = (gi < n && gj <= gi) ? W[gi * ld + gj] : 0.0;
+    }
+  __syncthreads();
+  double acc[4][4];
+  gemm_nt(XI, (I != J) ? XJ : XI, acc);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gi = rI + frag_row(i), gj = rJ + frag_col(i, j);
+      if (gi < n && gj <= gi) W[gi * ld + gj] = old[i][j] - acc[i][j];
+    }
+}
+
 // The persistent kernel's step k splits tile 0 = (k+1, k+1) in two:
 //  * critical_tile (CTA 0, the step's critical path): X = A_{k+1,k} Linv_kk^T with Linv_kk still in
 //    smem from CTA 0's own previous factorisation, the diagonal update A -= X X^T straight into
@@ -606,7 +707,7 @@ potrf_step_kernel(double* W, int64_t n, int64_t ld, int k, double* Linv, double*
 //    substitution for row block k+1 (t_k = Linv_kk ut_k, ut_{k+1} -= L_{k+1,k} t_k).
 // (tools/ubench/potrf_trace.cu: the old tile 0 took 32 us per step, 12 of them off the chain.)
 __device__ void critical_tile(double* W, int64_t n, int64_t ld, int k, double* Linv, int64_t* status, double* dsm,
-                              double (*P)[kLd]) {
+                              double (*P)[kLd], bool store_panel = false) {
   double (*A)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm);
   double (*X)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + kNB * kLd);
   double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 2 * kNB * kLd);
@@ -632,7 +733,11 @@ __device__ void critical_tile(double* W, int64_t n, int64_t ld, int k, double* L
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) X[frag_row(i)][frag_col(i, j)] = acc[i][j];
+    for (int j = 0; j < 4; ++j) {
+      X[frag_row(i)][frag_col(i, j)] = acc[i][j];
+      const int64_t gi = rI + frag_row(i);         // two-phase mode: L_{I,k} = X_I straight into W
+      if (store_panel && gi < n) W[gi * ld + kc + frag_col(i, j)] = acc[i][j];
+    }
   __syncthreads();
   if (tr) POTRF_MARK(83);
   gemm_nt(X, X, acc);                              // A_II -= X_I X_I^T
@@ -739,9 +844,57 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
   POTRF_MARK(2);
   int k = 0;
   const int G = gridDim.x;
+  // two-phase steps once the first step's trailing tiles reach ~4 per CTA (n >~ 2200; measured:
+  // n = 2048 1.04 vs 1.11 ms one- vs two-phase, n = 4096 6.3 -> 5.3 ms, n = 8192 60 -> 29 ms)
+  const bool two_phase = (nb - 1) * nb / 2 > 4 * G;
   for (; k + 1 < nb; ++k) {
     if (*(volatile int64_t*)status != 0) break;          // uniform: read after the barrier
     const int t = nb - k - 1, tiles = t * (t + 1) / 2;
+    if (two_phase) {
+      // phase A: CTA 0 the critical diagonal (X_{k+1} in place), the others the panel rows k+2..
+      if (blockIdx.x == 0) {
+        __syncthreads();
+        critical_tile(W, n, ld, k, Linv, status, dsm, P, true);
+      }
+      const int first = G > 1 ? (int)blockIdx.x - 1 : 0, stride = G > 1 ? G - 1 : 1;
+      if (G == 1 || blockIdx.x >= 1)
+        for (int I = k + 2 + first; I < nb; I += stride) {
+          __syncthreads();
+          panel_row_inplace(W, n, ld, k, I, Linv, dsm, u ? ut : nullptr, tb, I == k + 2);
+        }
+      if (u && k + 2 >= nb && blockIdx.x == G - 1) {   // no panel rows left: t_k still goes to tb
+        __syncthreads();
+        __shared__ double uk2[kNB];
+        const int64_t kc = (int64_t)k * kNB;
+        if (threadIdx.x < kNB) uk2[threadIdx.x] = (kc + threadIdx.x < n) ? ut[kc + threadIdx.x] : 0.0;
+        __syncthreads();
+        const double a = gemv64<false>(Linv + (size_t)k * kNB * kNB, kNB, uk2, kNB);
+        const int o = threadIdx.x >> 2;
+        if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = a;
+      }
+      grid_barrier(ctl, ctl + 1);
+      // phase B: every trailing tile but the factored diagonal, one product each; the forward
+      // substitution of row block k+1 (its panel rows came from CTA 0)
+      for (int tile = 1 + (int)blockIdx.x; tile < tiles; tile += G) {
+        __syncthreads();
+        int I, J;
+        tile_coords(tile, I, J);
+        update_tile(W, n, ld, k, I + k + 1, J + k + 1, dsm);
+      }
+      if (u && blockIdx.x == (G > 1 ? G - 1 : 0)) {
+        __syncthreads();
+        __shared__ double xk[kNB];
+        const int64_t kc = (int64_t)k * kNB, r1 = (int64_t)(k + 1) * kNB;
+        if (threadIdx.x < kNB) xk[threadIdx.x] = (kc + threadIdx.x < n) ? tb[kc + threadIdx.x] : 0.0;
+        __syncthreads();
+        const int valid = (int)(n - r1 < kNB ? n - r1 : kNB);
+        const double a = gemv64<false>(W + r1 * ld + kc, ld, xk, valid);   // rows r1.. of L_{.,k}
+        const int o = threadIdx.x >> 2;
+        if ((threadIdx.x & 3) == 0 && o < valid) ut[r1 + o] -= a;
+      }
+      grid_barrier(ctl, ctl + 1);
+      continue;
+    }
     if (blockIdx.x == 0) {
       __syncthreads();
       critical_tile(W, n, ld, k, Linv, status, dsm, P);
@@ -763,7 +916,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
   }
   POTRF_MARK(70);
   const bool solve = u && *(volatile int64_t*)status == 0;
-  if (nb >= 2 && *(volatile int64_t*)status == 0) {      // last panel L_{., nb-2} into W
+  if (!two_phase && nb >= 2 && *(volatile int64_t*)status == 0) {      // last panel L_{., nb-2} into W
     const int kk = nb - 2;
     const int64_t kc = (int64_t)kk * kNB;
     const double* panel = (kk & 1) ? panel1 : panel0;

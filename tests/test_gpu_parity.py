@@ -83,7 +83,7 @@ def test_potrf_pivot_and_factor_properties(fsb):
     np.testing.assert_allclose(L, O.cholesky_lower(W), rtol=1e-12, atol=1e-13)
 
 
-@pytest.mark.parametrize("n,bad", [(70, 3), (130, 65), (300, 299)])
+@pytest.mark.parametrize("n,bad", [(70, 3), (130, 65), (300, 299), (2500, 1500), (2500, 2499)])
 def test_potrf_pivot_index_blocked(fsb, n, bad):
     """The failing pivot is reported with LAPACK's 0-based index across panel boundaries."""
     from paper_2310_17556_b200.solvers import _cholesky_lower
@@ -99,6 +99,20 @@ def test_potrf_pivot_index_blocked(fsb, n, bad):
     with pytest.raises(fsb.FactorizationError) as eg:
         _cholesky_lower(W)
     assert eg.value.pivot == eo.value.pivot
+
+
+@pytest.mark.parametrize("n", [2500, 3001])
+def test_potrf_two_phase_factor_matches_lapack(fsb, n):
+    """n large enough for the two-phase block steps (panel rows written in place, one product per
+    trailing tile): the factor matches LAPACK's to fp64 rounding."""
+    from paper_2310_17556_b200.solvers import _cholesky_lower
+    rng = np.random.Generator(np.random.PCG64(n))
+    A = rng.standard_normal((n, n + 64))
+    W = A @ A.T / n + 0.1 * np.eye(n)
+    L = _cholesky_lower(W)
+    ref = O.cholesky_lower(W)
+    assert np.abs(L - ref).max() <= 1e-10 * np.abs(ref).max()
+    assert np.array_equal(np.triu(L, 1), np.zeros((n, n)))
 
 
 def test_workspace_stays_small(fsb):
