@@ -553,7 +553,6 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         const int64_t row = row0 + k * kCLRows + 2 * rp + half;
         zr[k][p] = (!y_only && rp < RP && row < n) ? (Zt)z[row] : (Zt)0;
       }
-    const double rlam = 1.0 / lam;
     // warps 2-3 form x of panel j-1 and load v (or x, y-only) one iteration ahead
     const bool xw = tid >= 64 && tid < 64 + CW;
     const int t = tid - 64;
@@ -584,7 +583,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
 #pragma unroll
           for (int r = 0; r < kCL; ++r) sum += xch[(b * kCL + r) * 64 + t];
           if (c < m) {
-            xv = (vc - sum) * rlam;
+            xv = (vc - sum) / lam;     // true division: x = v / lam exactly when S = 0 (solvers.py:124-126)
             // accumulate: the old x travels with rank 0's partials (read there before the push,
             // so no rank can see rank 0's overwrite of x[c])
             if (accumulate) xv = xo[b * 64 + t] + xv;

@@ -54,6 +54,25 @@ def test_zero_scores_reduce_to_scaled_identity_exactly(fsb, dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("lam", [3.0, 1e-3, 0.7])
+@pytest.mark.parametrize("n,m", [(3, 5), (40, 1001), (1024, 4099), (1300, 257)])
+def test_zero_scores_give_true_division(fsb, dtype, lam, n, m):
+    """S = 0: x = v / lam bit for bit (true IEEE division, not a multiplication by 1/lam —
+    SURVEY §8a-7) on every x-pass kernel (cluster pass n <= 1232, panel pass above), device and host
+    entries."""
+    rng = np.random.Generator(np.random.PCG64(n + m))
+    v = rng.standard_normal(m)
+    expect = v.astype(dtype).astype(np.float64) / lam     # v takes S's dtype (core.py:179-195)
+    S = np.zeros((n, m), dtype=dtype)
+    sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v))
+    assert np.array_equal(sol.x, expect)
+    dev = torch.device("cuda", 0)
+    sol_d = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam,
+                                            torch.from_numpy(v.astype(dtype)).to(dev)))
+    assert np.array_equal(sol_d.x.cpu().numpy(), expect)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_zero_rhs_gives_zero_exactly(fsb, dtype):
     S, _, _ = O.random_system(1, 4, 9, 0.1)
     sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S.astype(dtype)), 0.1, np.zeros(9)))
