@@ -889,3 +889,30 @@ def test_xy_pass_refinement_accumulates(fsb, n, m):
     x4 = fsb.solve_chol(system, precision="f16x2", refine=4).x
     assert O.rel_err(x4, ref.x) < 0.1 * O.rel_err(x0, ref.x)
     assert O.rel_err(x4, ref.x) <= 1e-9, O.rel_err(x4, ref.x)
+
+
+# ---------------------------------------------------------------- ill-conditioned family
+
+@pytest.mark.parametrize("lam", [1e-3, 1e-6])
+def test_ill_conditioned_geometric_spectrum(fsb, lam):
+    """S = U diag(s) V^T with s_i = 10^(-4 i/(n-1)) (cond(S S^T) = 1e8): the Gaussian headline
+    inputs never stress potrf, this family does.  fp64 mode against the oracle to cond * eps;
+    the fp32 modes against the oracle's fp64 solve of the identical fp32-rounded system, with the
+    u32 sigma_max^2 / lam error scale of SURVEY §8d."""
+    n, m = 256, 8192
+    rng = np.random.Generator(np.random.PCG64(17))
+    U, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    s = 10.0 ** (-4.0 * np.arange(n) / (n - 1))
+    S = (U * s) @ V.T
+    v = rng.standard_normal(m)
+    ref = O.solve_chol(S, v, lam)
+    sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="fp64")
+    cond = (1.0 + lam) / lam
+    assert O.rel_err(sol.x, ref.x) <= 50 * cond * 2.0 ** -52, O.rel_err(sol.x, ref.x)
+    S32, v32 = S.astype(np.float32), v.astype(np.float32)
+    ref32 = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
+    for prec in ("tf32x3", "f16x2"):
+        sol32 = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32), precision=prec)
+        bound = 64 * 2.0 ** -24 * 1.0 / lam          # u32 sigma_max^2 / lam (sigma_max = 1), widened
+        assert O.rel_err(sol32.x, ref32.x) <= max(1e-6, bound), (prec, O.rel_err(sol32.x, ref32.x))
