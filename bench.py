@@ -160,6 +160,22 @@ def cpu_reference(n, m, lam, steps, warmup, seed=0):
         cores = len(os.sched_getaffinity(0))
     except Exception:
         cores = os.cpu_count()
+    # one extra, separately timed pass through the oracle's phases (the CPU time next
+    # to its gram / potrf / chol_apply (GEMVs + TRSVs) / residual breakdown)
+    phases = {}
+    t = time.perf_counter()
+    W = O.gram(S, lam)
+    phases["gram"] = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    L = O.cholesky_lower(W)
+    phases["potrf"] = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    x = O.chol_apply(S, lam, L, v)
+    phases["chol_apply_gemv_trsv"] = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    O.residual(S, lam, v, x)
+    phases["residual"] = (time.perf_counter() - t) * 1e3
+    cpu_reference.phases_ms = phases
     return times, sol.rel_residual, cores
 
 
@@ -177,7 +193,7 @@ def run_reference(args, rank, world):
         "config": {"workload": WORKLOAD, "n": n, "m": m, "lam": args.lam, "l2": L2_NOTE},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
                          "sample": f"full workload n={n}, m={m} per step, median of {len(times)}",
-                         "rel_residual": rel},
+                         "rel_residual": rel, "phases_ms": getattr(cpu_reference, "phases_ms", None)},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -372,7 +388,7 @@ def run_b200(args, rank, world, local):
             times, rel_cpu, cores = cpu_reference(n, m_local, lam, args.cpu_repeats, 0)
             cpu = {"value": statistics.median(times) * 1e3, "unit": "ms", "cores": cores, "kind": "port",
                    "sample": f"full workload n={n}, m={m_local} fp64 oracle solve_chol, median of {len(times)}",
-                   "rel_residual": rel_cpu}
+                   "rel_residual": rel_cpu, "phases_ms": getattr(cpu_reference, "phases_ms", None)}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "port", "sample": f"failed: {e}"}
 
