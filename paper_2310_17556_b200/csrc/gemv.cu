@@ -431,15 +431,15 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
   }
 }
 
-// Cluster variant for n <= kCLMaxRows (the headline n = 1024).  The TMA engine moves ~one box row
+// Cluster variant for n <= 2464 (4-CTA clusters up to n = 1232, the headline n = 1024; 8 above).  The TMA engine moves ~one box row
 // per 8 SM clocks, so 128-byte-wide boxes cap a full strided read of S at ~4.6 TB/s while
 // 256-byte rows reach ~6.6 TB/s (tools/ubench/tma_seg.cu).  A panel is therefore 256 bytes of
-// columns (64 fp32 / 32 fp64), split by ROWS over a cluster of kCL CTAs: CTA r streams rows
+// columns (64 fp32 / 32 fp64), split by ROWS over a cluster of CL CTAs: CTA r streams rows
 // [r*NCH*30, (r+1)*NCH*30) of each panel as NCH 30-row TMA boxes (rows past n arrive as zeros)
 // into one slot-set of a ring, completing on the set's single mbarrier.  x needs the column sums
 // over all n rows: each CTA reduces its rows and pushes its partial column sums into every peer's
 // exchange buffer with st.async (the data and the peer's mbarrier complete_tx travel together);
-// every CTA adds the kCL partials in rank order, so x is identical everywhere.  Software
+// every CTA adds the CL partials in rank order, so x is identical everywhere.  Software
 // pipeline, one CTA barrier per panel: iteration j
 //   warps 2-3  x of panel j-1 from the exchange (pushed an iteration ago, latency hidden)
 //   all warps  x-phase of panel j: partial column sums
@@ -447,7 +447,7 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 //   warps 0-1  sum the per-warp partials of panel j, push them to the cluster
 //   all warps  y += S_{panel j-1} x_{j-1} from the still-resident set, release the set
 // S is read from HBM exactly once.
-constexpr int kCL = 4;                           // CTAs per cluster (row split)
+// CTAs per cluster (row split): 4 up to n = 1232, 8 up to n = 2464 (template parameter CL)
 // 15 consumer warps + 1 producer warp: 4 warps per SM sub-partition, so up to 128 registers per
 // thread (a 17th warp would cap every thread at 96)
 constexpr int kCLCW = 15;                        // consumer warps
@@ -458,19 +458,26 @@ constexpr int kCLThreads = kCLCons + kWarp;
 constexpr int kCLRows = 28;
 constexpr int kCLChunk = kCLRows * 256;          // 7 KB per chunk slot (128-byte aligned)
 constexpr int kCLMaxV = 11;                      // chunks per CTA and panel -> 308 rows per CTA
-constexpr int kCLMaxRows = kCL * kCLRows * kCLMaxV;   // n <= 1232
+constexpr int kCLMaxRows4 = 4 * kCLRows * kCLMaxV;   // n <= 1232 with 4-CTA clusters
+constexpr int kCLMaxRows8 = 8 * kCLRows * kCLMaxV;   // n <= 2464 with 8-CTA clusters
 constexpr int kCLG = 3;                          // chunks per batch of shared loads (y group)
 constexpr int kCLXW = 7;                         // x-group warps (partial sums, exchange, x)
 constexpr int kCLYW = kCLCW - kCLXW;             // y-group warps (8)
 constexpr int kCLXThreads = kCLXW * kWarp;
 constexpr int kCLSets = 8;                       // max panel slot-sets in the ring
-constexpr int kCLSlotsMax = 30;                  // 30 x 7 KB + the fixed buffers fit 227 KB
-constexpr size_t kCLFixed = 2 * kCLXW * 64 * 8 + 2 * (kCL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
-constexpr size_t kCLSmem = 1024 + (size_t)kCLSlotsMax * kCLChunk + kCLFixed;
+__host__ __device__ constexpr size_t cl_fixed(int CL) {
+  return 2 * kCLXW * 64 * 8 + 2 * (CL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
+}
+// as many 7 KB chunk slots as fit beside the fixed buffers in 227 KB (30 with CL = 4, 29 with 8)
+__host__ __device__ constexpr int cl_slots(int CL) {
+  return (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk) < 30 ? (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk)
+                                                                    : 30;
+}
+__host__ __device__ constexpr size_t cl_smem(int CL) { return 1024 + (size_t)cl_slots(CL) * kCLChunk + cl_fixed(CL); }
 
-// chunks per CTA: the template instance (3, 6, 10 or 11) covering ceil(n / (kCL * 28))
-inline int cl_nch(int64_t n) {
-  const int c = (int)((n + kCL * kCLRows - 1) / (kCL * kCLRows));
+// chunks per CTA: the template instance (3, 6, 10 or 11) covering ceil(n / (CL * 28))
+inline int cl_nch(int64_t n, int CL) {
+  const int c = (int)((n + CL * kCLRows - 1) / (CL * kCLRows));
   return c <= 3 ? 3 : c <= 6 ? 6 : c <= 10 ? 10 : 11;
 }
 
@@ -483,14 +490,15 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
 }
 FS_DEVINL void bar_arrive_n(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 
-template <typename TS, typename TV, int NCH>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCLThreads, 1)
+template <typename TS, typename TV, int NCH, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCLThreads, 1)
 cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int64_t m, const double* __restrict__ z,
                        const TV* __restrict__ v, double lam, int accumulate, double* __restrict__ x,
                        double* __restrict__ ypart, int y_only) {
   constexpr int VN1 = 16 / (int)sizeof(TS);       // columns per 16-byte vector
   constexpr int CW = 16 * VN1;                    // columns per panel (256 bytes)
-  constexpr int R = kCLSlotsMax / NCH < kCLSets ? kCLSlotsMax / NCH : kCLSets;   // slot-sets
+  constexpr int kSlots = cl_slots(CL);
+  constexpr int R = kSlots / NCH < kCLSets ? kSlots / NCH : kCLSets;   // slot-sets
   constexpr int RPC = NCH * kCLRows;              // rows per CTA
   constexpr int RP = kCLRows / 2;                 // row pairs per chunk (one warp-wide load each)
   constexpr uint32_t kSetBytes = NCH * kCLChunk;
@@ -501,16 +509,16 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   using Zt = typename std::conditional<sizeof(TV) == 8, double, float>::type;
   extern __shared__ __align__(1024) unsigned char cl_raw[];
   unsigned char* ring = cl_raw + ((1024u - (ptx::smem_u32(cl_raw) & 1023u)) & 1023u);   // [R][NCH][7.5 KB]
-  double* red = (double*)(ring + (size_t)kCLSlotsMax * kCLChunk);  // [2][x warps][64]
-  double* xch = red + 2 * kCLXW * 64;                              // [2][kCL][64] partial column sums
-  double* xo = xch + 2 * kCL * 64;                                 // [2][64] old x (accumulate; from rank 0)
+  double* red = (double*)(ring + (size_t)kSlots * kCLChunk);       // [2][x warps][64]
+  double* xch = red + 2 * kCLXW * 64;                              // [2][CL][64] partial column sums
+  double* xo = xch + 2 * CL * 64;                                  // [2][64] old x (accumulate; from rank 0)
   double* xs = xo + 2 * 64;                                        // [2][64]
   uint64_t* full = (uint64_t*)(xs + 2 * 64);                       // [sets]
   uint64_t* empty = full + kCLSets;                                // [sets]
   uint64_t* xbar = empty + kCLSets;                                // [2]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)ptx::cluster_ctarank();
-  const int64_t cid = blockIdx.x / kCL, ncl = gridDim.x / kCL;
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int64_t row0 = (int64_t)rank * RPC;
   const int64_t panels = (m + CW - 1) / CW;
   const int64_t np = panels > cid ? (panels - 1 - cid) / ncl + 1 : 0;
@@ -581,7 +589,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
           ptx::mbar_wait(&xbar[b], (uint32_t)((p >> 1) & 1));
           double sum = 0.0;
 #pragma unroll
-          for (int r = 0; r < kCL; ++r) sum += xch[(b * kCL + r) * 64 + t];
+          for (int r = 0; r < CL; ++r) sum += xch[(b * CL + r) * 64 + t];
           if (c < m) {
             xv = (vc - sum) / lam;     // true division: x = v / lam exactly when S = 0 (solvers.py:124-126)
             // accumulate: the old x travels with rank 0's partials (read there before the push,
@@ -628,19 +636,19 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
           double part = 0.0;
 #pragma unroll
           for (int w = 0; w < kCLXW; ++w) part += red[(rb * kCLXW + w) * 64 + tid];
-          // the local barrier expects all kCL partial vectors (a peer's complete_tx may land
+          // the local barrier expects all CL partial vectors (a peer's complete_tx may land
           // before this expect_tx: the phase cannot complete until this one arrival is made)
-          if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (kCL + (accumulate ? 1 : 0)) * CW * 8);
-          const uint32_t mine = ptx::smem_u32(xch + (rb * kCL + rank) * 64 + tid);
+          if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (CL + (accumulate ? 1 : 0)) * CW * 8);
+          const uint32_t mine = ptx::smem_u32(xch + (rb * CL + rank) * 64 + tid);
           const uint32_t bar = ptx::smem_u32(&xbar[rb]);
 #pragma unroll
-          for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
+          for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
           if (accumulate && rank == 0) {
             const int64_t c = (cid + j * ncl) * CW + tid;
             const double xold = c < m ? x[c] : 0.0;
             const uint32_t xa = ptx::smem_u32(xo + rb * 64 + tid);
 #pragma unroll
-            for (int r = 0; r < kCL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
+            for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
           }
         }
         if (++setx == R) { setx = 0; phx ^= 1; }
@@ -706,20 +714,72 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   ptx::cluster_sync();                             // no CTA leaves while a peer may still signal it
 }
 
-template <typename TS, typename TV>
+template <typename TS, typename TV, int CL>
 cudaError_t launch_cols_solve_y_cl(int nch, unsigned grid, cudaStream_t st, const CUtensorMap& smap, int64_t n,
                                    int64_t m, const double* z, const TV* v, double lam, int acc, double* x,
                                    double* ypart, int y_only) {
   auto pick = [&](auto kfn) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCLSmem);
-    kfn<<<grid, kCLThreads, kCLSmem, st>>>(smap, n, m, z, v, lam, acc, x, ypart, y_only);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL));
+    kfn<<<grid, kCLThreads, cl_smem(CL), st>>>(smap, n, m, z, v, lam, acc, x, ypart, y_only);
   };
   switch (nch) {
-    case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3>); break;
-    case 6: pick(cols_solve_y_cl_kernel<TS, TV, 6>); break;
-    case 10: pick(cols_solve_y_cl_kernel<TS, TV, 10>); break;
-    default: pick(cols_solve_y_cl_kernel<TS, TV, 11>); break;
+    case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3, CL>); break;
+    case 6: pick(cols_solve_y_cl_kernel<TS, TV, 6, CL>); break;
+    case 10: pick(cols_solve_y_cl_kernel<TS, TV, 10, CL>); break;
+    default: pick(cols_solve_y_cl_kernel<TS, TV, 11, CL>); break;
   }
+  return cudaGetLastError();
+}
+
+// most clusters of CL CTAs (one per SM, cl_smem) the GPU runs at once; cached per CL
+template <typename TS, int CL>
+int cl_max_active(int num_sms) {
+  static int max_cl = 0;
+  if (!max_cl) {
+    auto probe = cols_solve_y_cl_kernel<TS, float, 10, CL>;
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(CL * 32));
+    cfg.blockDim = dim3(kCLThreads);
+    cfg.dynamicSmemBytes = cl_smem(CL);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = CL;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, (void*)probe, &cfg) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      mc = num_sms / CL;
+    }
+    max_cl = mc;
+  }
+  return max_cl;
+}
+
+// the cluster pass for CL-CTA clusters (S read once); ypart gets one row per cluster
+template <typename TS, int CL>
+cudaError_t cols_solve_y_cl_t(const CUtensorMap& smap, int64_t n, int64_t m, const double* z, const void* v,
+                              bool v_f64, double lam, bool accumulate, double* x, double* ypart, int64_t ypart_rows,
+                              double* y, int num_sms, cudaStream_t st, int* launches, int y_only) {
+  constexpr int64_t CW = 256 / (int64_t)sizeof(TS);
+  const int64_t panels = (m + CW - 1) / CW;
+  // same capacity bound as the panel kernel's grid
+  const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
+  const int64_t ncl = std::min<int64_t>(std::min<int64_t>(cl_max_active<TS, CL>(num_sms), num_sms / CL),
+                                        std::min(panels, cap));
+  if (ypart_rows < ncl) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)(ncl * CL);
+  const int nch = cl_nch(n, CL);
+  cudaError_t e = v_f64 ? launch_cols_solve_y_cl<TS, double, CL>(nch, grid, st, smap, n, m, z, (const double*)v, lam,
+                                                                 accumulate ? 1 : 0, x, ypart, y_only)
+                        : launch_cols_solve_y_cl<TS, float, CL>(nch, grid, st, smap, n, m, z, (const float*)v, lam,
+                                                                accumulate ? 1 : 0, x, ypart, y_only);
+  if (e != cudaSuccess) return e;
+  reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(ypart, ncl, n, n, y);
+  if (launches) *launches += 2;
   return cudaGetLastError();
 }
 
@@ -883,54 +943,24 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
                            double* y, int num_sms, cudaStream_t st, int* launches, int y_only = 0) {
   // one support rule and one grid size for the fused pass and the y-only pass, so that a
   // recomputed y = S x is bit-identical to the solve's (test_solvers.py:109-114)
-  const size_t smem = cy_smem_bytes<TS>(n);
-  if (smem > 200 * 1024 || !aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
-  // n <= 1232: the cluster kernel (S read from HBM once, in 256-byte TMA rows)
+  if (!aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
+  // n <= 2464: the cluster kernel (S read from HBM once, in 256-byte TMA rows); 4-CTA clusters up
+  // to n = 1232, 8-CTA ones above
   static const int cl_env = getenv("FS_CY_CL") ? atoi(getenv("FS_CY_CL")) : 1;
-  CUtensorMap smap;
-  memset(&smap, 0, sizeof smap);
-  if (cl_env && n <= kCLMaxRows &&
-      make_tensor_map_2d(&smap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, S,
-                         (uint64_t)m, (uint64_t)n, (uint64_t)ldS * sizeof(TS), 256 / sizeof(TS), kCLRows) ==
-          cudaSuccess) {
-    const int64_t panels = (m + 256 / (int64_t)sizeof(TS) - 1) / (256 / (int64_t)sizeof(TS));
-    static int max_cl = 0;
-    if (!max_cl) {
-      auto probe = cols_solve_y_cl_kernel<TS, float, 10>;
-      cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCLSmem);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(kCL * 64));
-      cfg.blockDim = dim3(kCLThreads);
-      cfg.dynamicSmemBytes = kCLSmem;
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeClusterDimension;
-      attr.val.clusterDim.x = kCL;
-      attr.val.clusterDim.y = 1;
-      attr.val.clusterDim.z = 1;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      int mc = 0;
-      if (cudaOccupancyMaxActiveClusters(&mc, (void*)probe, &cfg) != cudaSuccess || mc < 1) {
-        cudaGetLastError();
-        mc = num_sms / kCL;
-      }
-      max_cl = mc;
-    }
-    // ypart holds one row per cluster; same capacity bound as the panel kernel's grid
-    const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
-    const int64_t ncl = std::min<int64_t>(std::min<int64_t>(max_cl, num_sms / kCL), std::min(panels, cap));
-    if (ypart_rows < ncl) return cudaErrorInvalidValue;
-    const unsigned grid = (unsigned)(ncl * kCL);
-    const int nch = cl_nch(n);
-    cudaError_t e = v_f64 ? launch_cols_solve_y_cl<TS, double>(nch, grid, st, smap, n, m, z, (const double*)v, lam,
-                                                               accumulate ? 1 : 0, x, ypart, y_only)
-                          : launch_cols_solve_y_cl<TS, float>(nch, grid, st, smap, n, m, z, (const float*)v, lam,
-                                                              accumulate ? 1 : 0, x, ypart, y_only);
-    if (e != cudaSuccess) return e;
-    reduce_chunks_kernel<<<(unsigned)((n + kRedRows - 1) / kRedRows), kRedRows * kRedWarps, 0, st>>>(ypart, ncl, n, n, y);
-    if (launches) *launches += 2;
-    return cudaGetLastError();
+  if (cl_env && n <= kCLMaxRows8) {
+    CUtensorMap smap;
+    memset(&smap, 0, sizeof smap);
+    if (make_tensor_map_2d(&smap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           S, (uint64_t)m, (uint64_t)n, (uint64_t)ldS * sizeof(TS), 256 / sizeof(TS), kCLRows) ==
+        cudaSuccess)
+      return n <= kCLMaxRows4
+                 ? cols_solve_y_cl_t<TS, 4>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
+                                            st, launches, y_only)
+                 : cols_solve_y_cl_t<TS, 8>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
+                                            st, launches, y_only);
   }
+  const size_t smem = cy_smem_bytes<TS>(n);
+  if (smem > 200 * 1024) return cudaErrorNotSupported;
   const int64_t panels = (m + cy_cols<TS>() - 1) / cy_cols<TS>();
   const int64_t cap = (m + row_chunk_cols<double>() - 1) / row_chunk_cols<double>();
   int64_t G = std::min<int64_t>((int64_t)num_sms, std::min(panels, cap));

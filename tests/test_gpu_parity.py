@@ -853,13 +853,13 @@ def test_large_n_takes_the_direct_and_two_pass_paths(fsb, n, m):
 
 # ---------------------------------------------------------------- cluster x+y pass boundaries
 
-@pytest.mark.parametrize("n", [1, 27, 28, 29, 113, 250, 1100, 1120, 1121, 1232, 1233])
+@pytest.mark.parametrize("n", [1, 27, 28, 29, 113, 250, 1100, 1120, 1121, 1232, 1233, 2200, 2464, 2465])
 @pytest.mark.parametrize("m", [1, 65, 4099])
 def test_xy_pass_shapes_match_oracle(fsb, n, m):
     """The fused x = (v - S^T z)/lam, y = S x pass (cols_solve_y_cl: 4-CTA clusters, 30-row chunks,
-    256-byte panels; n <= 1232) at chunk/panel/rank boundaries — n below one chunk, ranks with no
-    rows, partial last chunks and panels, the 10/11-chunk instances, and n = 1233 on the fallback
-    kernel — in fp64 mode (exact
+    256-byte panels; 4-CTA clusters to n = 1232, 8-CTA to 2464) at chunk/panel/rank boundaries — n
+    below one chunk, ranks with no rows, partial last chunks and panels, the 10/11-chunk instances,
+    both cluster sizes, and n = 2465 on the two-pass fallback — in fp64 mode (exact
     products), with the stored residual reproduced bit for bit by residual()."""
     rng = np.random.Generator(np.random.PCG64(7 * n + m))
     S = rng.standard_normal((n, m)) / np.sqrt(max(n, 1))
