@@ -431,7 +431,7 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
   }
 }
 
-// Cluster variant for n <= 2464 (4-CTA clusters up to n = 1232, the headline n = 1024; 8 above).  The TMA engine moves ~one box row
+// Cluster variant for n <= 4576 (4-CTA clusters up to n = 1144, the headline n = 1024; 8 and 16 above).  The TMA engine moves ~one box row
 // per 8 SM clocks, so 128-byte-wide boxes cap a full strided read of S at ~4.6 TB/s while
 // 256-byte rows reach ~6.6 TB/s (tools/ubench/tma_seg.cu).  A panel is therefore 256 bytes of
 // columns (64 fp32 / 32 fp64), split by ROWS over a cluster of CL CTAs: CTA r streams rows
@@ -447,19 +447,21 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 //   warps 0-1  sum the per-warp partials of panel j, push them to the cluster
 //   all warps  y += S_{panel j-1} x_{j-1} from the still-resident set, release the set
 // S is read from HBM exactly once.
-// CTAs per cluster (row split): 4 up to n = 1232, 8 up to n = 2464 (template parameter CL)
+// CTAs per cluster (row split): 4 up to n = 1144, 8 up to n = 2288, 16 (non-portable) up to 4576
 // 15 consumer warps + 1 producer warp: 4 warps per SM sub-partition, so up to 128 registers per
 // thread (a 17th warp would cap every thread at 96)
 constexpr int kCLCW = 15;                        // consumer warps
 constexpr int kCLCons = kCLCW * kWarp;
 constexpr int kCLThreads = kCLCons + kWarp;
-// 28 rows per chunk (TMA box outer dimension) = 14 row pairs: two per x-group warp and at most
-// two per y-group warp (with 30 rows one x warp carried three pairs and paced the whole pass)
-constexpr int kCLRows = 28;
-constexpr int kCLChunk = kCLRows * 256;          // 7 KB per chunk slot (128-byte aligned)
-constexpr int kCLMaxV = 11;                      // chunks per CTA and panel -> 308 rows per CTA
-constexpr int kCLMaxRows4 = 4 * kCLRows * kCLMaxV;   // n <= 1232 with 4-CTA clusters
-constexpr int kCLMaxRows8 = 8 * kCLRows * kCLMaxV;   // n <= 2464 with 8-CTA clusters
+// 26 rows per chunk (TMA box outer dimension) = 13 row pairs: at most two per x-group and per
+// y-group warp (with 30 rows one x warp carried three pairs and paced the whole pass), and small
+// enough that three 10-chunk slot-sets fit beside the fixed buffers for every cluster size
+constexpr int kCLRows = 26;
+constexpr int kCLChunk = kCLRows * 256;          // 6.5 KB per chunk slot (128-byte aligned)
+constexpr int kCLMaxV = 11;                      // chunks per CTA and panel -> 286 rows per CTA
+constexpr int kCLMaxRows4 = 4 * kCLRows * kCLMaxV;   // n <= 1144 with 4-CTA clusters
+constexpr int kCLMaxRows8 = 8 * kCLRows * kCLMaxV;   // n <= 2288 with 8-CTA clusters
+constexpr int kCLMaxRows16 = 16 * kCLRows * kCLMaxV;  // n <= 4576 with 16-CTA (non-portable) clusters
 constexpr int kCLG = 3;                          // chunks per batch of shared loads (y group)
 constexpr int kCLXW = 7;                         // x-group warps (partial sums, exchange, x)
 constexpr int kCLYW = kCLCW - kCLXW;             // y-group warps (8)
@@ -468,17 +470,17 @@ constexpr int kCLSets = 8;                       // max panel slot-sets in the r
 __host__ __device__ constexpr size_t cl_fixed(int CL) {
   return 2 * kCLXW * 64 * 8 + 2 * (CL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
 }
-// as many 7 KB chunk slots as fit beside the fixed buffers in 227 KB (30 with CL = 4, 29 with 8)
+// as many chunk slots as fit beside the fixed buffers in 227 KB (33 / 32 / 30 for CL = 4 / 8 / 16)
 __host__ __device__ constexpr int cl_slots(int CL) {
-  return (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk) < 30 ? (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk)
-                                                                    : 30;
+  return (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk) < 33 ? (int)((227 * 1024 - 1024 - cl_fixed(CL)) / kCLChunk)
+                                                                    : 33;
 }
 __host__ __device__ constexpr size_t cl_smem(int CL) { return 1024 + (size_t)cl_slots(CL) * kCLChunk + cl_fixed(CL); }
 
-// chunks per CTA: the template instance (3, 6, 10 or 11) covering ceil(n / (CL * 28))
+// chunks per CTA: the template instance (3, 6, 8, 10 or 11) covering ceil(n / (CL * 26))
 inline int cl_nch(int64_t n, int CL) {
   const int c = (int)((n + CL * kCLRows - 1) / (CL * kCLRows));
-  return c <= 3 ? 3 : c <= 6 ? 6 : c <= 10 ? 10 : 11;
+  return c <= 3 ? 3 : c <= 6 ? 6 : c <= 8 ? 8 : c <= 10 ? 10 : 11;
 }
 
 // remote (DSMEM) store that completes 8 transaction bytes on the receiving CTA's mbarrier: the
@@ -720,11 +722,13 @@ cudaError_t launch_cols_solve_y_cl(int nch, unsigned grid, cudaStream_t st, cons
                                    double* ypart, int y_only) {
   auto pick = [&](auto kfn) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL));
+    if (CL > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     kfn<<<grid, kCLThreads, cl_smem(CL), st>>>(smap, n, m, z, v, lam, acc, x, ypart, y_only);
   };
   switch (nch) {
     case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3, CL>); break;
     case 6: pick(cols_solve_y_cl_kernel<TS, TV, 6, CL>); break;
+    case 8: pick(cols_solve_y_cl_kernel<TS, TV, 8, CL>); break;
     case 10: pick(cols_solve_y_cl_kernel<TS, TV, 10, CL>); break;
     default: pick(cols_solve_y_cl_kernel<TS, TV, 11, CL>); break;
   }
@@ -738,6 +742,7 @@ int cl_max_active(int num_sms) {
   if (!max_cl) {
     auto probe = cols_solve_y_cl_kernel<TS, float, 10, CL>;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL));
+    if (CL > 8) cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(CL * 32));
     cfg.blockDim = dim3(kCLThreads);
@@ -752,7 +757,7 @@ int cl_max_active(int num_sms) {
     int mc = 0;
     if (cudaOccupancyMaxActiveClusters(&mc, (void*)probe, &cfg) != cudaSuccess || mc < 1) {
       cudaGetLastError();
-      mc = num_sms / CL;
+      mc = CL > 8 ? -1 : num_sms / CL;              // non-portable size not schedulable: unused
     }
     max_cl = mc;
   }
@@ -944,10 +949,10 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
   // one support rule and one grid size for the fused pass and the y-only pass, so that a
   // recomputed y = S x is bit-identical to the solve's (test_solvers.py:109-114)
   if (!aligned16(S, ldS, sizeof(TS))) return cudaErrorNotSupported;
-  // n <= 2464: the cluster kernel (S read from HBM once, in 256-byte TMA rows); 4-CTA clusters up
-  // to n = 1232, 8-CTA ones above
+  // n <= 4576: the cluster kernel (S read from HBM once, in 256-byte TMA rows); 4-CTA clusters up
+  // to n = 1144, 8-CTA to 2288, 16-CTA (non-portable, when schedulable) above
   static const int cl_env = getenv("FS_CY_CL") ? atoi(getenv("FS_CY_CL")) : 1;
-  if (cl_env && n <= kCLMaxRows8) {
+  if (cl_env && n <= kCLMaxRows16 && (n <= kCLMaxRows8 || cl_max_active<TS, 16>(num_sms) >= 4)) {
     CUtensorMap smap;
     memset(&smap, 0, sizeof smap);
     if (make_tensor_map_2d(&smap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -956,8 +961,11 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
       return n <= kCLMaxRows4
                  ? cols_solve_y_cl_t<TS, 4>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
                                             st, launches, y_only)
-                 : cols_solve_y_cl_t<TS, 8>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
-                                            st, launches, y_only);
+             : n <= kCLMaxRows8
+                 ? cols_solve_y_cl_t<TS, 8>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
+                                            st, launches, y_only)
+                 : cols_solve_y_cl_t<TS, 16>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y,
+                                             num_sms, st, launches, y_only);
   }
   const size_t smem = cy_smem_bytes<TS>(n);
   if (smem > 200 * 1024) return cudaErrorNotSupported;

@@ -853,13 +853,13 @@ def test_large_n_takes_the_direct_and_two_pass_paths(fsb, n, m):
 
 # ---------------------------------------------------------------- cluster x+y pass boundaries
 
-@pytest.mark.parametrize("n", [1, 27, 28, 29, 113, 250, 1100, 1120, 1121, 1232, 1233, 2200, 2464, 2465])
+@pytest.mark.parametrize("n", [1, 25, 26, 27, 105, 250, 1040, 1041, 1144, 1145, 2200, 2288, 2289, 3000, 4576, 4577])
 @pytest.mark.parametrize("m", [1, 65, 4099])
 def test_xy_pass_shapes_match_oracle(fsb, n, m):
     """The fused x = (v - S^T z)/lam, y = S x pass (cols_solve_y_cl: 4-CTA clusters, 30-row chunks,
-    256-byte panels; 4-CTA clusters to n = 1232, 8-CTA to 2464) at chunk/panel/rank boundaries — n
-    below one chunk, ranks with no rows, partial last chunks and panels, the 10/11-chunk instances,
-    both cluster sizes, and n = 2465 on the two-pass fallback — in fp64 mode (exact
+    256-byte panels; 4-CTA clusters to n = 1144, 8-CTA to 2288, 16-CTA to 4576) at chunk/panel/rank
+    boundaries — n below one chunk, ranks with no rows, partial last chunks and panels, the 10/11-
+    chunk instances, every cluster size, and n = 4577 on the two-pass fallback — in fp64 mode (exact
     products), with the stored residual reproduced bit for bit by residual()."""
     rng = np.random.Generator(np.random.PCG64(7 * n + m))
     S = rng.standard_normal((n, m)) / np.sqrt(max(n, 1))
