@@ -154,11 +154,17 @@ def all_finite(t) -> bool:
 
 
 def context_for(device: int, n: int, m: int) -> Context:
-    """Return a cached context on `device` large enough for (n, m); grows geometrically."""
+    """Return a cached context on `device` large enough for (n, m).
+
+    A context that must grow keeps the old bounds only while that costs little: the tiled score
+    copy is sized n_max * m_max, so (8192, 1e6) followed by (1024, 3e6) must become a (1024, 3e6)
+    context, not an (8192, 3e6) one (98 GB)."""
     ctx = _contexts.get(device)
     if ctx is None or ctx.n_max < n or ctx.m_max < m:
         n_max = max(n, ctx.n_max if ctx else 0)
         m_max = max(m, ctx.m_max if ctx else 0)
+        if n_max * m_max > 2 * n * m:
+            n_max, m_max = n, m
         if ctx is not None:
             ctx.close()
         ctx = Context(device, n_max, m_max)

@@ -17,6 +17,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace fs {
 namespace {
@@ -40,6 +41,49 @@ FS_DEVINL void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
+}
+
+// One 32-column stage: 8 k-steps of the warp's 8 x 4 grid of m8n8k4 fp64 MMAs.
+FS_DEVINL void stage_mma(double (&acc)[8][4][2], const double* A, const double* B, int wr, int wc, int fr, int fk) {
+#pragma unroll
+  for (int ks = 0; ks < kK; ks += 4) {
+    double af[8], bf[4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) af[a] = A[(wr + 8 * a + fr) * kLd + ks + fk];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) bf[b] = B[(wc + 8 * b + fr) * kLd + ks + fk];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
+  }
+}
+
+// Tile epilogue: packed lower G (+ lam on the diagonal) when the tile has one split, else the
+// partial tile into the split-K workspace (row-major 128 x 128 per block).
+FS_DEVINL void store_tile(const double (&acc)[8][4][2], int64_t rA, int64_t rB, int64_t n, double lam, double* ws,
+                          double* Gp, int direct, int wr, int wc, int fr, int lane) {
+  // accumulator fragment (m8n8 f64): thread holds rows fr, columns 2*(lane&3) + {0,1}
+  const int cc = 2 * (lane & 3);
+  if (direct) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t gi = rA + wr + 8 * a + fr, gj = rB + wc + 8 * b + cc + e;
+          if (gi < n && gj <= gi) Gp[gi * (gi + 1) / 2 + gj] = acc[a][b][e] + (gi == gj ? lam : 0.0);
+        }
+  } else {
+    double* out = ws + (size_t)blockIdx.x * kT * kT;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        *reinterpret_cast<double2*>(out + (wr + 8 * a + fr) * kT + wc + 8 * b + cc) =
+            make_double2(acc[a][b][0], acc[a][b][1]);
+  }
 }
 
 // Stage loader: rows [r0, r0+128) x cols [k0, k0+32) of S -> 16 doubles per thread in registers.
@@ -115,19 +159,7 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
       if (!diag) lb.load(S, n, kend, ldS, rB, k0 + kK, vec);
     }
     const double* A = dsm + buf * kStageDoubles;
-    const double* B = diag ? A : A + kT * kLd;
-#pragma unroll
-    for (int ks = 0; ks < kK; ks += 4) {
-      double af[8], bf[4];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) af[a] = A[(wr + 8 * a + fr) * kLd + ks + fk];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = B[(wc + 8 * b + fr) * kLd + ks + fk];
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(acc[a][b], af[a], bf[b]);
-    }
+    stage_mma(acc, A, diag ? A : A + kT * kLd, wr, wc, fr, fk);
     if (more) {
       double* nxt = dsm + (buf ^ 1) * kStageDoubles;
       la.store(nxt);
@@ -136,27 +168,75 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
     __syncthreads();
     buf ^= 1;
   }
-  // accumulator fragment (m8n8 f64): thread holds rows fr, columns 2*(lane&3) + {0,1}
-  const int cc = 2 * (lane & 3);
-  if (direct) {
+  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
+}
+
+// fp64 scores with 16-byte aligned rows: global -> shared with cp.async (no register staging,
+// no store pass after the MMAs), three stages in flight (3 x 72 KB).  Thread t copies 8 16-byte
+// pieces of each operand per stage; pieces past the last row or column are zero-filled (src-size).
+constexpr int kAsyncStages = 3;
+constexpr size_t kAsyncSmemBytes = (size_t)kAsyncStages * kStageDoubles * sizeof(double);   // 221 KB
+
+FS_DEVINL void cp16(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+FS_DEVINL void issue_stage(double* dst, const double* __restrict__ S, int64_t n, int64_t kend, int64_t ldS, int64_t r0,
+                           int64_t k0) {
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t gi = rA + wr + 8 * a + fr, gj = rB + wc + 8 * b + cc + e;
-          if (gi < n && gj <= gi) Gp[gi * (gi + 1) / 2 + gj] = acc[a][b][e] + (gi == gj ? lam : 0.0);
-        }
-  } else {
-    double* out = ws + (size_t)blockIdx.x * kT * kT;
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-        *reinterpret_cast<double2*>(out + (wr + 8 * a + fr) * kT + wc + 8 * b + cc) =
-            make_double2(acc[a][b][0], acc[a][b][1]);
+  for (int q = 0; q < 8; ++q) {
+    const int piece = threadIdx.x + q * kThreads;       // 128 rows x 16 pieces
+    const int r = piece >> 4, c = (piece & 15) * 2;
+    const int64_t gr = r0 + r, gc = k0 + c;
+    const int64_t left = kend - gc;
+    const int bytes = gr < n ? (left >= 2 ? 16 : left == 1 ? 8 : 0) : 0;
+    cp16(dst + r * kLd + c, bytes ? S + gr * ldS + gc : S, bytes);
   }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
+                       double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct) {
+  extern __shared__ __align__(16) double dsm[];
+  int I, J;
+  tile_ij(blockIdx.x / P, I, J);
+  const int split = blockIdx.x % P;
+  const bool diag = I == J;
+  const int64_t kbeg = (int64_t)split * kchunk;
+  const int64_t kend = m < kbeg + kchunk ? m : kbeg + kchunk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 2) * 64, wc = (warp & 3) * 32;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int64_t rA = (int64_t)I * kT, rB = (int64_t)J * kT;
+  const int nst = kbeg < kend ? (int)((kend - kbeg + kK - 1) / kK) : 0;
+  auto issue = [&](int st) {
+    if (st < nst) {
+      double* d = dsm + (st % kAsyncStages) * kStageDoubles;
+      issue_stage(d, S, n, kend, ldS, rA, kbeg + (int64_t)st * kK);
+      if (!diag) issue_stage(d + kT * kLd, S, n, kend, ldS, rB, kbeg + (int64_t)st * kK);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");   // empty groups keep the count uniform
+  };
+  issue(0);
+  issue(1);
+  int buf = 0;
+  for (int st = 0; st < nst; ++st) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // stage st landed (this thread's pieces)
+    __syncthreads();                                       // ... everyone's; stage st-1 fully consumed
+    issue(st + 2);                                         // refills the buffer stage st-1 used
+    const double* A = dsm + buf * kStageDoubles;
+    stage_mma(acc, A, diag ? A : A + kT * kLd, wr, wc, fr, fk);
+    buf = buf == kAsyncStages - 1 ? 0 : buf + 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
 }
 
 // Fixed-order sum of the P split-K partials of a tile.  Block (tile, part): kRedParts slices of
@@ -194,6 +274,15 @@ DPlan dplan(int64_t n, int64_t m, int num_sms) {
   return p;
 }
 
+// FS_DMMA_ASYNC=0 selects the register-staged loader for fp64 scores too (A/B switch).
+bool dmma_async() {
+  static const bool on = [] {
+    const char* e = getenv("FS_DMMA_ASYNC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 size_t syrk_dmma_workspace_bytes(int num_sms) { return (size_t)num_sms * kT * kT * sizeof(double); }
@@ -209,7 +298,11 @@ cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
   const int direct = p.P == 1 ? 1 : 0;
   const int vec = ((reinterpret_cast<uintptr_t>(S) | (uintptr_t)(ldS * (s_f64 ? 8 : 4))) & 15) == 0 ? 1 : 0;
   const unsigned grid = (unsigned)(p.tiles * p.P);
-  if (s_f64) {
+  if (s_f64 && vec && dmma_async()) {
+    cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
+    syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam,
+                                                                     ws, Gp, direct);
+  } else if (s_f64) {
     cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
                                                                  Gp, direct, vec);

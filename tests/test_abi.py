@@ -71,3 +71,26 @@ def test_no_oracle_import_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, flags=re.M), f
+
+
+def test_context_growth_does_not_multiply_bounds(monkeypatch):
+    """context_for keeps old bounds only when cheap: (8192, 1e6) then (1024, 3e6) must not become
+    an (8192, 3e6) workspace (the sweep that found it ran out of HBM)."""
+    from paper_2310_17556_b200 import _lib
+
+    class FakeCtx:
+        def __init__(self, device, n_max, m_max):
+            self.device, self.n_max, self.m_max = device, n_max, m_max
+
+        def close(self):
+            pass
+
+    monkeypatch.setattr(_lib, "Context", FakeCtx)
+    monkeypatch.setattr(_lib, "_contexts", {})
+    c = _lib.context_for(0, 8192, 1_000_000)
+    assert (c.n_max, c.m_max) == (8192, 1_000_000)
+    c = _lib.context_for(0, 1024, 3_000_000)
+    assert (c.n_max, c.m_max) == (1024, 3_000_000)
+    c = _lib.context_for(0, 2048, 3_000_000)          # 2x the area of the request: keep growing
+    assert (c.n_max, c.m_max) == (2048, 3_000_000)
+    assert _lib.context_for(0, 1024, 2_000_000) is c  # fits: reused
