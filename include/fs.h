@@ -66,7 +66,9 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max);
 void fs_ctx_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);
 /* Device bytes one solve of (n, m) in (dtype, precision) touches besides S, v, x
- * (feeds WorkspaceMeter, core.py:63-96; a context may own more to serve any smaller problem). */
+ * (feeds WorkspaceMeter, core.py:63-96; a context may own more to serve any smaller problem).
+ * Not counted: the tensor-core modes' re-laid-out copy of S itself (F16X2: 4 n m bytes, TF32X3:
+ * 8 n m bytes; allocated on first use of that mode, sized for the context's n_max x m_max). */
 size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t fs_launch_count(const fs_ctx* ctx);

@@ -161,17 +161,20 @@ int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int6
   return fail(ctx, FS_EINVAL, "unknown precision mode");
 }
 
-// The tiled copy S_t is sized for the context's (n_max, m_max) and allocated on the first
-// TF32X3 use (fp64-only users never pay for it).
-int ensure_tiles(fs_ctx* ctx) {
-  const size_t need = std::max(fs::tiles_bytes(ctx->n_max, ctx->m_max), fs::tiles16_bytes(ctx->n_max, ctx->m_max));
+// The tiled copy S_t is sized for the context's (n_max, m_max) in the layout the mode needs
+// (F16X2: two fp16 planes, 4 bytes per score; TF32X3: two tf32 planes, 8 bytes) and allocated on
+// first use — fp64-only users never pay for it, and an F16X2 user at the per-rank shard of
+// n = 16384, m = 1e7 / 8 (82 GB of scores) is not charged the 164 GB TF32X3 layout.
+int ensure_tiles(fs_ctx* ctx, bool f16) {
+  const size_t need = f16 ? fs::tiles16_bytes(ctx->n_max, ctx->m_max) : fs::tiles_bytes(ctx->n_max, ctx->m_max);
   if (ctx->St_bytes >= need) return FS_OK;
   if (ctx->d_St) cudaFree(ctx->d_St);
   ctx->d_St = nullptr;
   ctx->St_bytes = 0;
   if (cudaMalloc((void**)&ctx->d_St, need) != cudaSuccess) {
     cudaGetLastError();
-    return fail(ctx, FS_ENOMEM, "cannot allocate the tiled copy of S for TF32X3");
+    return fail(ctx, FS_ENOMEM, f16 ? "cannot allocate the fp16 planes of S (F16X2)"
+                                    : "cannot allocate the tf32 planes of S (TF32X3)");
   }
   ctx->St_bytes = need;
   return FS_OK;
@@ -244,7 +247,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
   } else if (use_tc == 2) {
     // F16X2: row scales from a sample, split planes (+ u = S w), kind::f16 SYRK.  The overflow
     // flag is checked by the caller at its next host synchronisation.
-    if ((rc = ensure_tiles(ctx))) return rc;
+    if ((rc = ensure_tiles(ctx, true))) return rc;
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
     if (e == cudaSuccess) e = fs::row_scales((const float*)S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, &l);
     if (e == cudaSuccess)
@@ -255,7 +258,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     if (e == cudaSuccess)
       e = fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
   } else if (use_tc) {
-    if ((rc = ensure_tiles(ctx))) return rc;
+    if ((rc = ensure_tiles(ctx, false))) return rc;
     e = fs::gemv_rows_retile((const float*)S, n, m, ldS, w32, ctx->d_partials, u, ctx->d_St, st, &l);
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
     if (e == cudaSuccess) e = fs::syrk_tc(ctx->d_St, n, m, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
@@ -765,7 +768,7 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     }
   }
   const bool direct = use_tc == 2 && f16_direct() && fs::syrk_tc_supported(ctx->d_Sin, ldd);
-  if (use_tc && !direct && (rc = ensure_tiles(ctx))) return rc;
+  if (use_tc && !direct && (rc = ensure_tiles(ctx, use_tc == 2))) return rc;
   ctx->n_marks = 0;
   prof_mark(ctx, -1, st);
   FS_CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st), "flag reset");
