@@ -263,12 +263,32 @@ struct DPlan {
   int64_t kchunk;
 };
 
+// Fraction of the SM-slots of the last full round that P-way split tiles keep busy.
+double round_fill(int tiles, int P, int num_sms) {
+  const int64_t units = (int64_t)tiles * P, rounds = (units + num_sms - 1) / num_sms;
+  return (double)units / (double)(rounds * num_sms);
+}
+
 DPlan dplan(int64_t n, int64_t m, int num_sms) {
   DPlan p;
   const int nb = (int)((n + kT - 1) / kT);
   p.tiles = nb * (nb + 1) / 2;
   const int64_t kblocks = (m + kK - 1) / kK;
-  p.P = p.tiles >= num_sms ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(num_sms / p.tiles, kblocks / 4));
+  if (p.tiles < num_sms) {
+    p.P = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms / p.tiles, kblocks / 4));
+  } else {
+    // more tiles than SMs: split K when it fills the last round better (n = 4096: 528 tiles are
+    // 3.57 rounds -> 5-way splits fill 17.8 of 18), within the workspace the context holds
+    // (shared with the tcgen05 SYRK) and keeping >= 16 stages per unit
+    const size_t cap = std::max(syrk_dmma_workspace_bytes(num_sms), syrk_tc_workspace_bytes(n, m, num_sms));
+    p.P = 1;
+    double best = round_fill(p.tiles, 1, num_sms);
+    for (int P = 2; P <= 8; ++P) {
+      if (kblocks / P < 16 || (size_t)p.tiles * P * kT * kT * sizeof(double) > cap) break;
+      const double f = round_fill(p.tiles, P, num_sms);
+      if (f > best + 0.03) { best = f; p.P = P; }
+    }
+  }
   p.kchunk = ((kblocks + p.P - 1) / p.P) * kK;
   p.P = (int)((m + p.kchunk - 1) / p.kchunk);
   return p;

@@ -201,6 +201,20 @@ def test_gram_stage(fsb, n, m, precision):
     assert np.array_equal(W, W.T)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_fp64_gram_split_k_with_more_tiles_than_sms(fsb, dtype):
+    """n = 2500: 210 tiles of 128 > 148 SMs -> the fp64 SYRK splits K two ways to fill the last
+    round (syrk_dmma.cu dplan); odd m exercises the cp.async loader's partial 16-byte pieces."""
+    n, m = 2500, 6001
+    rng = np.random.Generator(np.random.PCG64(2500))
+    S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(dtype)
+    W = fsb.gram(fsb.ScoreMatrix(S), 0.25, precision="fp64")
+    ref = O.gram(S.astype(np.float64), 0.25)
+    # exact fp64 products, different summation order than numpy's: a few ulps of the 6001-term sums
+    assert np.abs(W - ref).max() / np.abs(ref).max() <= 5e-14
+    assert np.array_equal(W, W.T)
+
+
 @pytest.mark.parametrize("precision", ["tf32x3", "f16x2"])
 def test_split_gram_error_is_fp32_level(fsb, precision):
     """3xTF32 / F16X2 must be far more accurate than one tf32/fp16 product (2^-11): ~fp32 per entry."""
