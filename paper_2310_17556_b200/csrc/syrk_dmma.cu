@@ -86,6 +86,41 @@ FS_DEVINL void store_tile(const double (&acc)[8][4][2], int64_t rA, int64_t rB, 
   }
 }
 
+// Two-level accumulation.  One fp64 register chain over a 250k-column split accumulates ~sqrt(250k)
+// ulps of rounding (4.8e-14 of the diagonal at 1024 x 1e6, 100x numpy's dgemm — enough to
+// lift the solve's first-pass residual over the 1e-10 refinement threshold).  Every kFlush stages
+// (2048 columns) each thread adds its registers into a private slot of the CTA's 128 x 128
+// workspace tile (L2-resident; the split-K partial's own slot) and restarts them from zero, so
+// the long chain runs over ~120 block sums instead of 250k products (error 8e-16 of the diagonal,
+// numpy's level; Gram +4%, every 32 stages +8.5%).  All warps flush at the same stage (staggering
+// them stalls every stage's barrier instead: 38 -> 52 ms).
+constexpr int kFlush = 64;
+
+FS_DEVINL void flush_acc(double (&acc)[8][4][2], double* buf, bool first, int wr, int wc, int fr, int lane) {
+  const int cc = 2 * (lane & 3);
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double2* p = reinterpret_cast<double2*>(buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc);
+      const double2 o = first ? make_double2(0.0, 0.0) : *p;
+      *p = make_double2(o.x + acc[a][b][0], o.y + acc[a][b][1]);
+      acc[a][b][0] = acc[a][b][1] = 0.0;
+    }
+}
+
+FS_DEVINL void unflush_acc(double (&acc)[8][4][2], const double* buf, int wr, int wc, int fr, int lane) {
+  const int cc = 2 * (lane & 3);
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double2 o = *reinterpret_cast<const double2*>(buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc);
+      acc[a][b][0] = o.x + acc[a][b][0];
+      acc[a][b][1] = o.y + acc[a][b][1];
+    }
+}
+
 // Stage loader: rows [r0, r0+128) x cols [k0, k0+32) of S -> 16 doubles per thread in registers.
 // Thread t covers row (t >> 1) and 16 consecutive columns ((t & 1) * 16 ...).
 template <typename T>
@@ -126,7 +161,7 @@ struct Loader {
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P, double lam,
-                 double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec) {
+                 double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec, int flush) {
   extern __shared__ __align__(16) double dsm[];
   int I, J;
   tile_ij(blockIdx.x / P, I, J);
@@ -152,6 +187,9 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
     if (!diag) lb.store(dsm + kT * kLd);
   }
   __syncthreads();
+  double* fbuf = ws + (size_t)blockIdx.x * kT * kT;
+  int since = 0;
+  bool flushed = false;
   for (int64_t k0 = kbeg; k0 < kend; k0 += kK) {
     const bool more = k0 + kK < kend;
     if (more) {                                           // next stage -> registers
@@ -167,7 +205,13 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
     }
     __syncthreads();
     buf ^= 1;
+    if (flush && ++since == kFlush && more) {
+      flush_acc(acc, fbuf, !flushed, wr, wc, fr, lane);
+      flushed = true;
+      since = 0;
+    }
   }
+  if (flushed) unflush_acc(acc, fbuf, wr, wc, fr, lane);
   store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
 }
 
@@ -198,7 +242,7 @@ FS_DEVINL void issue_stage(double* dst, const double* __restrict__ S, int64_t n,
 
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
-                       double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct) {
+                       double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct, int flush) {
   extern __shared__ __align__(16) double dsm[];
   int I, J;
   tile_ij(blockIdx.x / P, I, J);
@@ -227,6 +271,9 @@ syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64
   issue(0);
   issue(1);
   int buf = 0;
+  double* fbuf = ws + (size_t)blockIdx.x * kT * kT;
+  int since = 0;
+  bool flushed = false;
   for (int st = 0; st < nst; ++st) {
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // stage st landed (this thread's pieces)
     __syncthreads();                                       // ... everyone's; stage st-1 fully consumed
@@ -234,8 +281,14 @@ syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64
     const double* A = dsm + buf * kStageDoubles;
     stage_mma(acc, A, diag ? A : A + kT * kLd, wr, wc, fr, fk);
     buf = buf == kAsyncStages - 1 ? 0 : buf + 1;
+    if (flush && ++since == kFlush && st + 1 < nst) {
+      flush_acc(acc, fbuf, !flushed, wr, wc, fr, lane);
+      flushed = true;
+      since = 0;
+    }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (flushed) unflush_acc(acc, fbuf, wr, wc, fr, lane);
   store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
 }
 
@@ -303,6 +356,15 @@ bool dmma_async() {
   return on;
 }
 
+// FS_DMMA_FLUSH=0 turns the two-level accumulation off (single register chain; A/B switch).
+bool dmma_flush() {
+  static const bool on = [] {
+    const char* e = getenv("FS_DMMA_FLUSH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 size_t syrk_dmma_workspace_bytes(int num_sms) { return (size_t)num_sms * kT * kT * sizeof(double); }
@@ -318,18 +380,21 @@ cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
   const int direct = p.P == 1 ? 1 : 0;
   const int vec = ((reinterpret_cast<uintptr_t>(S) | (uintptr_t)(ldS * (s_f64 ? 8 : 4))) & 15) == 0 ? 1 : 0;
   const unsigned grid = (unsigned)(p.tiles * p.P);
+  // the flush slots are the split-K partial tiles' own: one 128 x 128 fp64 tile per CTA
+  const size_t cap = std::max(syrk_dmma_workspace_bytes(num_sms), syrk_tc_workspace_bytes(n, m, num_sms));
+  const int flush = ws && (size_t)grid * kT * kT * sizeof(double) <= cap && dmma_flush() ? 1 : 0;
   if (s_f64 && vec && dmma_async()) {
     cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
     syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam,
-                                                                     ws, Gp, direct);
+                                                                     ws, Gp, direct, flush);
   } else if (s_f64) {
     cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
-                                                                 Gp, direct, vec);
+                                                                 Gp, direct, vec, flush);
   } else {
     cudaFuncSetAttribute(syrk_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     syrk_dmma_kernel<float><<<grid, kThreads, kSmemBytes, st>>>((const float*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
-                                                                Gp, direct, vec);
+                                                                Gp, direct, vec, flush);
   }
   if (launches) *launches += 1;
   if (!direct) {

@@ -215,6 +215,23 @@ def test_fp64_gram_split_k_with_more_tiles_than_sms(fsb, dtype):
     assert np.array_equal(W, W.T)
 
 
+def test_fp64_gram_is_accurate_over_long_k(fsb):
+    """Exact fp64 products summed over 50k-column splits: the two-level accumulation keeps the
+    error at a few ulps of the diagonal (one register chain gave ~2.5e-14 here, 4.8e-14 at m = 1e6,
+    enough to push the headline fp64 solve over the 1e-10 refinement threshold)."""
+    import math
+    n, m = 1024, 200_000
+    rng = np.random.Generator(np.random.PCG64(11))
+    S = (rng.standard_normal((n, m), dtype=np.float32) / np.float32(32))
+    W = fsb.gram(fsb.ScoreMatrix(S), 1e-300, precision="fp64")
+    A = S.astype(np.float64)
+    errs = []
+    for i, j in [(0, 0), (511, 511), (1023, 1023), (5, 900), (700, 3), (1000, 999)]:
+        exact = math.fsum((A[i] * A[j]).tolist())       # products of fp32 values are exact in fp64
+        errs.append(abs(W[i, j] - exact) / W[i, i])
+    assert max(errs) <= 6e-15, errs
+
+
 @pytest.mark.parametrize("precision", ["tf32x3", "f16x2"])
 def test_split_gram_error_is_fp32_level(fsb, precision):
     """3xTF32 / F16X2 must be far more accurate than one tf32/fp16 product (2^-11): ~fp32 per entry."""
