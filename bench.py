@@ -4,12 +4,17 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 Workload (BASELINE configs[1], the paper headline): n=1024 samples, m=1e6 parameters,
-fp32 scores, lam=1e-3, synthetic N(0,1)/sqrt(n) (torch Philox, seed 0 + rank).  One step =
-one full solve_chol (Gram -> potrf -> TRSV pair -> fused x epilogue -> fp64 residual
-diagnostics), i.e. the reference's timed unit (solvers.py:151-206 via bench.py:254-267).
+fp32 scores, lam=1e-3.  N=1: the reference generator's system (PCG64 seed 0, bench.py:155-160)
+rounded to fp32 — the CPU reference solves its exact fp64 upcast, so the line carries
+relerr(x) against the reference (`parity`).  One step = one full solve_chol in the fp32
+headline mode (f16x2 Gram, no refinement; Gram -> potrf -> TRSV pair -> fused x epilogue ->
+fp64 residual diagnostics), i.e. the reference's timed unit (solvers.py:151-206 via
+bench.py:254-267).  `parity` also times the drop-in default (precision/refine "auto": the
+reference's refinement rule, result within its 1e-8 promise) and the exact fp64 mode.
 
 N=1: the one-shot C-ABI solve on device-resident inputs (`value`) and the public Python API
-with host (pinned) buffers, H2D + D2H inside the timed region (`e2e`).
+with host (pinned) buffers, H2D + D2H inside the timed region (`e2e`; `e2e_streamed_ms` is the
+defer=True path that overlaps the upload with the Gram).
 N>1 (torchrun, one rank per GPU): the m axis is column-sharded (strong scaling: total m
 fixed), one NCCL all-reduce of the packed [W | u] per solve, time = max over ranks.
 
@@ -33,6 +38,8 @@ sys.path.insert(0, ROOT)
 METRIC = "damped-Fisher solve ms at n=1024,m=1e6; SYRK TC util + GEMV HBM GB/s vs peak"
 WORKLOAD = "chol solve n=1024, m=1e6, fp32 scores, lam=1e-3 (BASELINE configs[1], paper headline)"
 L2_NOTE = "inputs (S = 4.1 GB fp32) larger than the 126 MB L2; no flush needed"
+DATA_NOTE = ("synthetic: the reference generator's system (PCG64 seed 0, S = N(0,1)/sqrt(n) then v, bench.py:155-160) "
+             "rounded to fp32; the CPU reference solves its exact fp64 upcast (the identical system)")
 
 
 def parse():
@@ -50,6 +57,10 @@ def parse():
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU (column-sharded, NCCL) code path even at one rank (a 1-rank NCCL group)")
     ap.add_argument("--cpu-repeats", type=int, default=2)
+    ap.add_argument("--philox", action="store_true", help="device Philox data instead of the reference generator")
+    ap.add_argument("--no-modes", dest="modes", action="store_false",
+                    help="skip timing the drop-in default and fp64 modes")
+    ap.add_argument("--pageable", action="store_true", help="also time e2e from pageable numpy memory")
     return ap.parse_args()
 
 
@@ -142,19 +153,31 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference (CPU) arm
 
-def cpu_reference(n, m, lam, steps, warmup, seed=0):
-    """Time the oracle port of solve_chol (numpy/scipy, the reference's BLAS/LAPACK calls)."""
+def reference_system(n, m, seed=0):
+    """The reference generator's system (bench.py:127-171 / SURVEY §8d): PCG64(seed), S = N(0,1)/sqrt(n)
+    drawn first in row-major order, then v = N(0,1)^m, both rounded to fp32 for the fp32 workload.
+    Returns (S32, v32, S64, v64): the fp32 arrays the GPU solves and their exact fp64 upcasts, the
+    identical system the CPU reference solves."""
     import numpy as np
     from oracle import fisher_oracle as O
-    rng = np.random.Generator(np.random.PCG64(seed))
-    S = (rng.standard_normal((n, m), dtype=np.float32) / np.float32(np.sqrt(n))).astype(np.float64)
-    v = rng.standard_normal(m, dtype=np.float32).astype(np.float64)
+    S64, v64, _ = O.generate_problem(seed, n, m, 1e-3)
+    S32 = S64.astype(np.float32)
+    v32 = v64.astype(np.float32)
+    np.copyto(S64, S32)            # S64 <- fp64(fp32(S)): same buffer, no second 8 GB array
+    v64 = v32.astype(np.float64)
+    return S32, v32, S64, v64
+
+
+def cpu_reference(S64, v64, lam, steps, warmup):
+    """Time the oracle port of solve_chol (numpy/scipy, the reference's BLAS/LAPACK calls)."""
+    from oracle import fisher_oracle as O
     for _ in range(warmup):
-        O.solve_chol(S, v, lam)
+        O.solve_chol(S64, v64, lam)
     times = []
+    sol = None
     for _ in range(steps):
         t0 = time.perf_counter()
-        sol = O.solve_chol(S, v, lam)
+        sol = O.solve_chol(S64, v64, lam)
         times.append(time.perf_counter() - t0)
     try:
         cores = len(os.sched_getaffinity(0))
@@ -164,36 +187,38 @@ def cpu_reference(n, m, lam, steps, warmup, seed=0):
     # to its gram / potrf / chol_apply (GEMVs + TRSVs) / residual breakdown)
     phases = {}
     t = time.perf_counter()
-    W = O.gram(S, lam)
+    W = O.gram(S64, lam)
     phases["gram"] = (time.perf_counter() - t) * 1e3
     t = time.perf_counter()
     L = O.cholesky_lower(W)
     phases["potrf"] = (time.perf_counter() - t) * 1e3
     t = time.perf_counter()
-    x = O.chol_apply(S, lam, L, v)
+    x = O.chol_apply(S64, lam, L, v64)
     phases["chol_apply_gemv_trsv"] = (time.perf_counter() - t) * 1e3
     t = time.perf_counter()
-    O.residual(S, lam, v, x)
+    O.residual(S64, lam, v64, x)
     phases["residual"] = (time.perf_counter() - t) * 1e3
     cpu_reference.phases_ms = phases
-    return times, sol.rel_residual, cores
+    return times, sol, cores
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     n, m = args.n, args.m
-    times, rel, cores = cpu_reference(n, m, args.lam, max(1, args.steps), max(0, min(args.warmup, 1)))
+    _, _, S64, v64 = reference_system(n, m)
+    warm = max(0, min(args.warmup, 1))
+    times, sol, cores = cpu_reference(S64, v64, args.lam, max(1, args.steps), warm)
     ms = statistics.median(times) * 1e3
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": len(times),
-        "warmup": max(0, min(args.warmup, 1)), "ms_per_step": ms, "higher_is_better": False,
+        "warmup": warm, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": "synthetic: PCG64 N(0,1)/sqrt(n) rounded to fp32, upcast to fp64 (the identical system)",
+        "data": DATA_NOTE,
         "config": {"workload": WORKLOAD, "n": n, "m": m, "lam": args.lam, "l2": L2_NOTE},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "port",
                          "sample": f"full workload n={n}, m={m} per step, median of {len(times)}",
-                         "rel_residual": rel, "phases_ms": getattr(cpu_reference, "phases_ms", None)},
+                         "rel_residual": sol.rel_residual, "phases_ms": getattr(cpu_reference, "phases_ms", None)},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -212,6 +237,12 @@ def make_shard(n, m_local, seed, device, dtype):
     S.normal_(generator=g).mul_(1.0 / n ** 0.5)
     v = torch.empty(m_local, dtype=dtype, device=device).normal_(generator=g)
     return S, v
+
+
+def _rel_err(x, ref):
+    """||x - ref|| / max(1, ||ref||), the reference's comparison (tests/conftest.py:27-29)."""
+    import numpy as np
+    return float(np.linalg.norm(np.asarray(x) - ref) / max(1.0, float(np.linalg.norm(ref))))
 
 
 def run_b200(args, rank, world, local):
@@ -236,7 +267,21 @@ def run_b200(args, rank, world, local):
     a, b = column_shard(m, world, rank)
     m_local = b - a
     dtype = torch.float64 if args.precision == "fp64" else torch.float32
-    S, v = make_shard(n, m_local, 1234 + rank, device, dtype)
+    S64 = v64 = None
+    if world == 1 and not args.philox:
+        # N=1: the reference generator's PCG64 system, so x can be compared with the CPU reference
+        S32h, v32h, S64, v64 = reference_system(n, m)
+        per16 = 16 // torch.empty((), dtype=dtype).element_size()
+        ld = -(-m // per16) * per16
+        S = torch.empty((n, ld), dtype=dtype, device=device)[:, :m]
+        S.copy_(torch.from_numpy(S32h if dtype == torch.float32 else S64))
+        v = torch.from_numpy(v32h if dtype == torch.float32 else v64).to(device)
+        data = DATA_NOTE
+        del S32h
+    else:
+        S, v = make_shard(n, m_local, 1234 + rank, device, dtype)
+        data = ("synthetic: torch Philox N(0,1)/sqrt(n), seed 1234+rank, device-resident (N>1: each rank draws its "
+                "own column shard; the CPU-reference comparison runs at N=1)")
     torch.cuda.synchronize()
 
     ctx = _lib.context_for(local, n, m_local)
@@ -253,16 +298,17 @@ def run_b200(args, rank, world, local):
         sm = fsb.ScoreMatrix(S)
 
     stage_acc = {k: [] for k in _lib.PROF_STAGES}
+    last = {}
 
     def one_step():
+        # the fp32 headline mode: f16x2 tensor-core Gram, no refinement (SURVEY §8d fp32 tolerance)
         if not sharded:
-            sol = fsb.solve_chol(system, precision=args.precision)
-            for k, val in ctx.stage_ms().items():
-                stage_acc[k].append(val)
-            return sol.rel_residual
-        sol = sharded_solve_chol_fused(sm, v, lam, precision=args.precision)
+            sol = fsb.solve_chol(system, precision=args.precision, refine=0)
+        else:
+            sol = sharded_solve_chol_fused(sm, v, lam, precision=args.precision)
         for k, val in ctx.stage_ms().items():
             stage_acc[k].append(val)
+        last["sol"] = sol
         return sol.rel_residual
 
     for _ in range(args.warmup):
@@ -292,9 +338,33 @@ def run_b200(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     ms_per_step = elapsed / args.steps
+    x_head = last["sol"].x_local if sharded else last["sol"].x
+    x_head = x_head.cpu().numpy() if isinstance(x_head, torch.Tensor) else np.asarray(x_head)
 
-    # ---- end to end through the public API with host buffers (N=1, rank 0) ----
+    # ---- the drop-in defaults and the reference's own arithmetic, timed on the same system (N=1) ----
+    modes = {}
+    if not sharded and args.modes:
+        for name, kw in (("auto (drop-in default: f16x2 + reference refinement rule, fp64 if needed)",
+                          dict(precision="auto", refine="auto")),
+                         ("fp64 (exact fp64 products, the reference's arithmetic)", dict(precision="fp64"))):
+            if dtype == torch.float64 and name.startswith("auto"):
+                continue
+            sol = fsb.solve_chol(system, **kw)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            reps = 3
+            e0.record(stream)
+            for _ in range(reps):
+                sol = fsb.solve_chol(system, **kw)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            modes[name] = {"ms": e0.elapsed_time(e1) / reps, "precision": sol.precision,
+                           "rel_residual": sol.rel_residual, "x": sol.x.cpu().numpy()}
+
+    # ---- end to end through the public API with host buffers ----
     e2e = None
+    e2e_extra = {}
     if args.e2e_steps > 0:
         S_host = torch.empty((n, m_local), dtype=dtype, pin_memory=True)
         S_host.copy_(S)
@@ -302,37 +372,50 @@ def run_b200(args, rank, world, local):
         v_host.copy_(v)
         Sh, vh = S_host.numpy(), v_host.numpy()
 
-        def e2e_step():
-            # the call a user makes with host (numpy) buffers: the single-GPU public API, or per rank
-            # the sharded one (same pipelined host entry + the NCCL all-reduce callback)
+        def time_e2e(step, steps):
+            step()   # warm
+            torch.cuda.synchronize()
+            if sharded:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            if sharded:
+                t = torch.tensor([ms], dtype=torch.float64, device=device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            return ms
+
+        def e2e_step(host_S, defer=False):
+            # the call a user makes with host (numpy) buffers: ScoreMatrix construction uploads and
+            # validates S (the reference's frozen copy), the solve returns a numpy x
             if not sharded:
-                out = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=args.precision).x
+                out = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(host_S, defer=defer), lam, vh),
+                                     precision=args.precision, refine=0).x
             else:
-                out = sharded_solve_chol_fused(fsb.ScoreMatrix(Sh), vh, lam, precision=args.precision).x_local
+                out = sharded_solve_chol_fused(fsb.ScoreMatrix(host_S, defer=True), vh, lam,
+                                               precision=args.precision).x_local
             assert isinstance(out, np.ndarray)
 
-        e2e_step()   # warm
-        torch.cuda.synchronize()
-        if sharded:
-            dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        if sharded:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = time_e2e(lambda: e2e_step(Sh), args.e2e_steps)
         e2e = {"value": e2e_ms, "unit": "ms",
                "h2d_bytes_per_step": int(Sh.nbytes + vh.nbytes), "d2h_bytes_per_step": int(m_local * 8 + 16),
-               "path": ("solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v)) -> numpy x"
+               "path": ("solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v), precision='f16x2', "
+                        "refine=0) -> numpy x; construction uploads + validates S on the device"
                         if not sharded else
-                        "per rank: sharded_solve_chol_fused(ScoreMatrix(pinned numpy shard), numpy v shard) -> numpy x"
-                        " shard; max over ranks")}
+                        "per rank: sharded_solve_chol_fused(ScoreMatrix(pinned numpy shard, defer=True), numpy v "
+                        "shard) -> numpy x shard; max over ranks")}
+        if not sharded:
+            e2e_extra["e2e_streamed_ms"] = time_e2e(lambda: e2e_step(Sh, defer=True), args.e2e_steps)
+            if args.pageable:
+                Sp = np.array(Sh)        # ordinary (pageable) numpy memory, what most callers hold
+                e2e_extra["e2e_pageable_ms"] = time_e2e(lambda: e2e_step(Sp), max(1, args.e2e_steps - 1))
+                del Sp
         del S_host, v_host
 
     if rank != 0:
@@ -353,8 +436,8 @@ def run_b200(args, rank, world, local):
         peak_mode = pk["bf16_tflops_sustained"] / 3.0      # fp16 = bf16 dense rate; 3 MMAs per product
         peak_note = "bf16 sustained (= fp16 dense, power-capped clocks) /3 (hi*hi + hi*lo + lo*hi)"
     else:
-        peak_mode = 40.0                                     # fp64 (nominal B200 FP64)
-        peak_note = "nominal B200 fp64 40 TF/s"
+        peak_mode = 36.9                                     # fp64 DMMA, measured (tools/ubench/dmma_peak.cu)
+        peak_note = "fp64 DMMA 36.9 TF/s measured (tools/ubench/dmma_peak.cu)"
     roofline = None
     if st.get("gram"):
         achieved = syrk_flops / (st["gram"] * 1e-3) / 1e12
@@ -367,10 +450,12 @@ def run_b200(args, rank, world, local):
     es = dtype.itemsize
     gemv = {}
     if st.get("gemv_sv"):
-        # tf32x3: the retile pass reads S once and writes the tiled copy S_t (tiles.cuh) + u = S v
+        # K3 by SURVEY §8(d): n m s + m s + n 8 (read S and v once, write u); the retile pass also
+        # writes the tiled copy (F16X2: two fp16 planes, 4 bytes per score) -> both figures
         tiles = (-(-n // 256) * 256) * (-(-m_local // 64) * 64) * 4 if args.precision != "fp64" else 0
-        bytes_sv = n * m_local * es + tiles + m_local * es + n * 8
-        gemv["gemv_sv_GBps"] = bytes_sv / (st["gemv_sv"] * 1e-3) / 1e9
+        bytes_k3 = n * m_local * es + m_local * es + n * 8
+        gemv["gemv_sv_GBps"] = bytes_k3 / (st["gemv_sv"] * 1e-3) / 1e9
+        gemv["gemv_sv_with_tile_write_GBps"] = (bytes_k3 + tiles) / (st["gemv_sv"] * 1e-3) / 1e9
     if st.get("gemv_stz"):
         # fused x = (v - S^T z)/lam and y = S x (cluster kernel): S from HBM exactly once
         bytes_stz = n * m_local * es + m_local * es + m_local * 8 + n * 8
@@ -383,12 +468,21 @@ def run_b200(args, rank, world, local):
                 **gemv, **{k.replace("GBps", "frac"): val / pk["hbm_gbs"] for k, val in list(gemv.items())}}
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    parity = None
+    if world == 1 and S64 is not None and not args.no_cpu_baseline:
         try:
-            times, rel_cpu, cores = cpu_reference(n, m_local, lam, args.cpu_repeats, 0)
+            times, sol_ref, cores = cpu_reference(S64, v64, lam, args.cpu_repeats, 0)
             cpu = {"value": statistics.median(times) * 1e3, "unit": "ms", "cores": cores, "kind": "port",
-                   "sample": f"full workload n={n}, m={m_local} fp64 oracle solve_chol, median of {len(times)}",
-                   "rel_residual": rel_cpu, "phases_ms": getattr(cpu_reference, "phases_ms", None)}
+                   "sample": f"full workload n={n}, m={m_local} fp64 oracle solve_chol on the identical system, "
+                             f"median of {len(times)}",
+                   "rel_residual": sol_ref.rel_residual, "phases_ms": getattr(cpu_reference, "phases_ms", None)}
+            parity = {"tolerance_relerr_fp32_modes": 1e-6, "tolerance_relerr_fp64": 1e-10,
+                      "reference_rel_residual": sol_ref.rel_residual,
+                      "headline": {"precision": args.precision, "refine": 0, "rel_residual": rels[-1],
+                                   "relerr_vs_reference": _rel_err(x_head, sol_ref.x)}}
+            for name, d in modes.items():
+                parity[name] = {"ms": d["ms"], "precision": d["precision"], "rel_residual": d["rel_residual"],
+                                "relerr_vs_reference": _rel_err(d["x"], sol_ref.x)}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "port", "sample": f"failed: {e}"}
 
@@ -396,16 +490,18 @@ def run_b200(args, rank, world, local):
         "metric": METRIC, "value": ms_per_step, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
-        "data": "synthetic: torch Philox N(0,1)/sqrt(n), seed 1234+rank, device-resident",
+        "data": data,
         "config": {"workload": WORKLOAD, "n": n, "m": m, "m_per_rank": m_local, "lam": lam,
-                   "precision": args.precision, "diagnostics": True, "l2": L2_NOTE,
+                   "precision": args.precision, "refine": 0, "diagnostics": True, "l2": L2_NOTE,
                    "parallelism": f"column-shard m over {world} GPU(s), NCCL all-reduce of [W|u]"},
         "roofline": roofline,
         "roofline_gemv": gemv or None,
         "stage_ms": st,
         "rel_residual": rels[-1],
+        "parity": parity,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        **e2e_extra,
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }

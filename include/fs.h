@@ -138,6 +138,15 @@ int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m
 /* iterative refinement: up to k correction steps with the same factor while
  * rel_residual > refine_above and each step at least halves it; k = 1 is the reference rule */
 #define FS_FLAG_REFINE_STEPS(k) (FS_FLAG_REFINE | (((k) & 0xFF) << 8))
+/* multi-rank: the caller's validation found non-finite entries in this rank's shard.  The rank
+ * still joins every collective (contributing zeros) and every rank returns FS_EINVAL together;
+ * with no all-reduce callback the call just returns FS_EINVAL.  More generally, with a callback
+ * no rank returns between two all-reduces: a rank whose local step fails joins the remaining
+ * collectives idle and the failure reaches every rank through a status slot of the norms
+ * all-reduce (all return an error together: the failing rank its own status, the others
+ * FS_ECUDA, or FS_EINVAL for a peer's non-finite input).  A zero-column shard (m = 0, S / v / x
+ * may be NULL) is valid with a callback: it contributes nothing. */
+#define FS_FLAG_INVALID_SHARD 0x10000
 int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
                   int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
                   void* allreduce_user, int flags, double refine_above, int64_t* pivot,
@@ -166,6 +175,13 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
  * against S (flags: FS_FLAG_RESIDUAL only; no refinement on this route).  Synchronizes. */
 int fs_syevj_packed(fs_ctx* ctx, const double* G_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
                     void* stream);
+/* fs_heevj_packed: eigenpairs of G = S S^H (complex scores; solvers.py:258-266 with A.conj().T)
+ * from G2_packed, the packed Gram of [Re S; Im S] (2n rows): the Jacobi eigensolver runs on the
+ * real 2n x 2n representation [[Re G, -Im G], [Im G, Re G]] (each eigenvalue twice) and one
+ * eigenvector per complex direction is extracted; w (n) descending, U (n x n, interleaved
+ * complex, ldU = n, column j <-> w[j]).  The context needs n_max >= 2n.  Synchronizes. */
+int fs_heevj_packed(fs_ctx* ctx, const double* G2_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
+                    void* stream);
 int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m, int64_t ldS,
                   const void* v, double lam, double sigma_floor, double* x, fs_allreduce_fn allreduce,
                   void* allreduce_user, int flags, int64_t* rank, double* out_res, void* stream);
@@ -178,6 +194,39 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
  * out: device, real `dtype`, leading dimension ldo.  The caller then runs fs_chol_solve. */
 int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, void* out,
                      int64_t ldo, void* stream);
+
+/* W = S S^H + lam I for complex S (core.py:279-290): G2_packed is the packed lower Gram of the
+ * kind-0 embedding [Re S; Im S] (2n rows, from fs_embed_complex + fs_gram_packed with shift 0);
+ * W is n x n complex (interleaved re, im doubles, leading dimension ldW in complex elements),
+ * exactly Hermitian, lam added on the diagonal. */
+int fs_hermitian_gram(fs_ctx* ctx, const double* G2_packed, int64_t n, double lam, double* W, int64_t ldW,
+                      void* stream);
+
+/* Y = T X (fp64 tensor cores, exact fp64 products): T r x n fp64 (row-major, ldT), X n x m in the
+ * score layout (row-major, ldX, dtype fp32/fp64), Y r x m fp64 (row-major, ldY).  The factor
+ * products of the comparison routes: thin_svd_eigh's V^T = (U / sigma)^T S (replaces
+ * solvers.py:272-276, A.T @ B -> dgemm) and the svd route's Q^T = L^-1 S, V^T = W^T Q^T. */
+int fs_apply_rows(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                  int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream);
+
+/* ---- direct-SVD comparison route ("svda", solvers.py:280-291, :357-364) ----
+ * The reference calls dgesdd on S.  The GPU route: shifted CholeskyQR3 of S^T (fs_gram_packed in
+ * FP64 on S and on Q^T, fs_potrf, fs_tri_inverse, fs_apply_rows) gives S = L Q^T; the one-sided
+ * Jacobi SVD of the n x n factor L = W diag(sigma) Z^T gives S = W diag(sigma) (Q Z)^T.
+ * fs_tri_inverse: Linv = L^-1 for a lower-triangular L (row-major; Linv's upper triangle zero).
+ * fs_jacobi_svd: A (n x n, row-major) = U diag(sigma) Zt with sigma descending (>= 0), U and Zt
+ *   n x n row-major (U's column j and Zt's row j belong to sigma[j]); works on A's columns, so
+ *   the condition number is not squared.  Synchronizes; FS_ENOCONV if not converged.
+ * fs_factor_solve: the solve from left factors, x = (v - S^T z)/lam with z = U_r diag(1/(w + lam))
+ *   U_r^T (S v) (U n x r, ldU; w length r, e.g. sigma^2) — equal to solvers.py:315-317's
+ *   V (sigma^2+lam)^-1 V^T v + (v - V V^T v)/lam for V = S^T U diag(1/sigma), without forming V
+ *   or dividing by sigma; flags: FS_FLAG_RESIDUAL (residual against S).  Synchronizes. */
+int fs_tri_inverse(fs_ctx* ctx, const double* L, int64_t n, int64_t ldL, double* Linv, int64_t ldo, void* stream);
+int fs_jacobi_svd(fs_ctx* ctx, const double* A, int64_t n, int64_t lda, double* sigma, double* U, int64_t ldu,
+                  double* Zt, int64_t ldz, int* sweeps, void* stream);
+int fs_factor_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v,
+                    double lam, const double* U, int64_t ldU, const double* w, int64_t r, double* x, int flags,
+                    double* out_res, void* stream);
 
 /* ---- input validation (core.py:108-119: np.isfinite(S).all() on construction) ----
  * FS_OK when all rows x cols entries (row-major, leading dimension ld) of the device array a are

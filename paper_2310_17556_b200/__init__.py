@@ -2,8 +2,9 @@
 
 Solves (S^T S + lam I) x = v for wide score matrices (m >> n) by the paper's
 Algorithm 1 with hand-written sm_100a kernels behind the C ABI of include/fs.h:
-tcgen05/TMEM 3xTF32 (or exact fp64) Gram, fp64 blocked Cholesky, TRSV pair, and
-HBM-streaming GEMVs with a fused (v - S^T z)/lam epilogue.  Multi-GPU: the m axis
+tcgen05/TMEM split-precision (or exact fp64) Gram, fp64 blocked Cholesky, TRSV pair, and
+HBM-streaming GEMVs with a fused (v - S^T z)/lam epilogue; the eigh / direct-SVD comparison
+routes and the complex variants on the same kernels.  Multi-GPU: the m axis
 is column-sharded with one NCCL all-reduce of [W | u] (see distributed.py).
 
 The public names mirror /root/reference/pkg/src/fisher_solve/__init__.py for the
@@ -21,10 +22,13 @@ from .core import (
     Solution,
     Variant,
     WorkspaceMeter,
+    as_scores,
+    as_system,
     gram,
     gram_packed,
     residual,
 )
+from .fmat import FmatError, read_matrix, read_vector, write_matrix, write_vector
 from .solvers import (
     DEFAULT_NAIVE_CAP,
     DEFAULT_SIGMA_FLOOR,
@@ -35,10 +39,13 @@ from .solvers import (
     solve_chol,
     solve_chol_hermitian,
     solve_realpart,
+    resolve_solver,
     solve_svd_direct,
     solve_svd_eigh,
+    solve_svd_from_factors,
     ThinSvd,
     eigh_gram,
+    thin_svd_direct,
     thin_svd_eigh,
 )
 

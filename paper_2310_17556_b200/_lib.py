@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfisher_b
 FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED, FS_ENOCONV = range(7)
 FS_F32, FS_F64 = 0, 1
 FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO, FS_PREC_F16X2 = 0, 1, 2, 3
-FS_FLAG_RESIDUAL, FS_FLAG_REFINE = 1, 2
+FS_FLAG_RESIDUAL, FS_FLAG_REFINE, FS_FLAG_INVALID_SHARD = 1, 2, 0x10000
 PROF_STAGES = ("gram", "gemv_sv", "allreduce", "potrf", "trsv", "gemv_stz", "residual")
 
 _c_int64 = ctypes.c_int64
@@ -55,6 +55,15 @@ SIGNATURES = {
                                      ctypes.POINTER(_c_int64), _dp, _vp]),
     "fs_embed_complex": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                         _c_int64, _vp]),
+    "fs_hermitian_gram": (ctypes.c_int, [_vp, _vp, _c_int64, ctypes.c_double, _vp, _c_int64, _vp]),
+    "fs_apply_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _c_int64, _c_int64,
+                                     _vp, _c_int64, _vp]),
+    "fs_heevj_packed": (ctypes.c_int, [_vp, _vp, _c_int64, _vp, _vp, _c_int64, ctypes.POINTER(ctypes.c_int), _vp]),
+    "fs_tri_inverse": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp, _c_int64, _vp]),
+    "fs_jacobi_svd": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp, _vp, _c_int64, _vp, _c_int64,
+                                     ctypes.POINTER(ctypes.c_int), _vp]),
+    "fs_factor_solve": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, ctypes.c_double,
+                                       _vp, _c_int64, _vp, _c_int64, _vp, ctypes.c_int, _dp, _vp]),
     "fs_all_finite": (ctypes.c_int, [ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp]),
     "fs_chol_solve_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                           ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,

@@ -114,7 +114,7 @@ def _cmd_solve(args) -> int:
     if args.precision != "fp64" and not np.iscomplexobj(S) and args.fp32:
         S = S.astype(np.float32)
         rhs = rhs.astype(np.float32)
-    system = fsb.DampedSystem(fsb.ScoreMatrix(S), args.lam, rhs)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), args.lam, rhs)
     sol = _run(system, args.method, args.variant, args.precision, _parse_refine(args.refine))
     if args.out is not None:
         fmat.write_vector(args.out, sol.x)
@@ -154,7 +154,7 @@ def _system_for(args, n, m):
     if args.device_resident:
         dev = torch.device("cuda", torch.cuda.current_device())
         return fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam, torch.from_numpy(v).to(dev))
-    return fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v)
+    return fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), lam, v)
 
 
 def _cmd_bench(args) -> int:

@@ -5,15 +5,22 @@ and errors).  Differences that make it B200-native:
 
 * ``ScoreMatrix`` keeps the scores resident on a CUDA device (``.tensor``), in the
   caller's precision when that is float32/float64 (the reference always widens to
-  float64, core.py:108-119; ints/bools still widen to float64).  ``.data`` returns a
-  read-only host copy for code written against the reference.
+  float64, core.py:108-119; ints/bools still widen to float64).  Construction makes the
+  private copy and validates finiteness there, as the reference does (core.py:132-142):
+  a host array is uploaded and checked on the device at construction, so later changes to
+  the caller's array do not reach the solve.  ``ScoreMatrix(a, defer=True)`` opts into the
+  streamed host entry instead (the upload overlaps the Gram inside the solve; validation
+  happens there and the caller must not modify ``a`` until the solve returns).
+  ``.data`` returns a read-only host copy for code written against the reference.
 * ``gram`` and ``residual`` run on the GPU through the C ABI (include/fs.h); there
-  is no CPU fallback.
+  is no CPU fallback.  Complex scores go through the real embeddings of fs_embed_complex
+  (no kernel ever reads complex memory as real rows).
 """
 
 from __future__ import annotations
 
 import enum
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -89,11 +96,13 @@ def _coerce_damping(lam) -> float:       # core.py:99-105
     return lam
 
 
-def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.Tensor:
-    """Coerce to a float32/float64 CUDA tensor and validate finiteness (core.py:108-119).
+def _to_device_tensor(a, name: str, device, force_copy: bool = False, validate: bool = True) -> torch.Tensor:
+    """Coerce to a float32/float64 (or complex64/complex128) CUDA tensor and validate finiteness
+    (core.py:108-119).
 
     2-D inputs get unit column stride and 16-byte aligned rows (padded leading dimension);
     ``force_copy`` guarantees the result does not alias ``a`` (the reference freezes a copy).
+    Host arrays are always copied (uploaded), so the result never aliases them.
     """
     if isinstance(a, torch.Tensor):
         t = a
@@ -103,28 +112,32 @@ def _to_device_tensor(a, name: str, device, force_copy: bool = False) -> torch.T
         elif t.dtype not in (torch.float32, torch.float64):
             t = t.to(torch.float64)
     else:
-        t = torch.from_numpy(_coerce_host(a, name))
+        arr = _coerce_host(a, name)
+        with warnings.catch_warnings():      # read-only arrays (e.g. another ScoreMatrix's .data)
+            warnings.simplefilter("ignore", UserWarning)
+            t = torch.from_numpy(arr)
     dev = device if device is not None else (t.device if t.is_cuda else default_device())
     if t.dim() == 2 and t.shape[1] > 0:
         # rows start on 16-byte boundaries (TMA / vector-load requirement); pad columns are never read
-        per16 = 16 // t.element_size()
+        per16 = max(1, 16 // t.element_size())
         ld = -(-t.shape[1] // per16) * per16
         if force_copy or not (t.is_cuda and t.device == dev and t.stride(1) == 1 and t.stride(0) % per16 == 0
                               and t.data_ptr() % 16 == 0):
             buf = torch.empty((t.shape[0], ld), dtype=t.dtype, device=dev)
             t = buf[:, : t.shape[1]].copy_(t, non_blocking=True)
     else:
+        src_ptr = a.data_ptr() if isinstance(a, torch.Tensor) else None
         t = t.to(dev, non_blocking=True).contiguous()
-        if force_copy and isinstance(a, torch.Tensor) and t.data_ptr() == a.data_ptr():
+        if force_copy and src_ptr is not None and t.data_ptr() == src_ptr:
             t = t.clone()
-    if t.numel() and not _lib.all_finite(t):
+    if validate and t.numel() and not _lib.all_finite(t):
         raise ValueError(f"{name} must contain only finite entries")
     return t
 
 
 def _coerce_host(a, name: str) -> np.ndarray:
-    """numpy side of core.py:108-119: numeric dtype -> C-contiguous float32/float64 (no copy when it
-    already is one).  Finiteness is checked on the device during the upload (fs_chol_solve_host)."""
+    """numpy side of core.py:108-119: numeric dtype -> C-contiguous float32/float64 (complex64 /
+    complex128 for complex input); no copy when it already is one."""
     arr = np.asarray(a)
     if np.iscomplexobj(arr):      # complex scores (SURVEY §8f-3): complex64 kept, else complex128
         return np.ascontiguousarray(arr if arr.dtype in (np.complex64, np.complex128) else arr.astype(np.complex128))
@@ -135,20 +148,29 @@ def _coerce_host(a, name: str) -> np.ndarray:
     return np.ascontiguousarray(arr)
 
 
+_HOST_DTYPES = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+                np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torch.complex128}
+
+
 class ScoreMatrix:
     """Dense n-by-m score matrix, one sample per row (core.py:122-162).
 
-    A CUDA tensor is copied once onto an aligned device buffer and validated immediately.  A host
-    array (numpy, lists) stays on the host until first use: solve_chol streams it to the GPU in
-    row chunks overlapped with the Gram (fs_chol_solve_host) and checks finiteness there, so a
-    non-finite entry raises the reference's ValueError from that first call.  The host array is
-    read at that point, not copied at construction.
+    Construction validates and freezes a private copy like the reference (core.py:132-142): a
+    CUDA tensor is copied onto an aligned device buffer, a host array (numpy, lists) is uploaded
+    to one; non-finite entries raise ValueError here, and the caller's array is neither frozen
+    nor read again.
+
+    ``defer=True`` (host arrays only) keeps the array on the host until the first solve, which
+    streams it to the GPU in column chunks overlapped with the Gram (fs_chol_solve_host) and
+    checks finiteness there — the fastest host-to-answer path, at the cost of the reference's
+    construction-time checks: the caller must not modify the array until the solve returns.
     """
 
-    def __init__(self, data, device=None):
+    def __init__(self, data, device=None, *, defer: bool = False):
         src = data
         self._host = None
         self._t = None
+        self._src = None
         self._device = device
         if isinstance(src, torch.Tensor):
             t = _to_device_tensor(data, "score matrix", device, force_copy=src.is_cuda)
@@ -157,7 +179,11 @@ class ScoreMatrix:
         else:
             arr = _coerce_host(data, "score matrix")
             shape = arr.shape
-            self._src = arr
+            if len(shape) == 2 and shape[0] >= 1 and shape[1] >= 1:
+                if defer and not np.iscomplexobj(arr):
+                    self._src = arr
+                else:
+                    self._t = _to_device_tensor(arr, "score matrix", device)
         if len(shape) != 2:
             raise ValueError(f"score matrix must be 2-D, got shape {shape}")
         if shape[0] < 1 or shape[1] < 1:
@@ -167,14 +193,15 @@ class ScoreMatrix:
         self.host_origin = not (isinstance(src, torch.Tensor) and src.is_cuda)
 
     @classmethod
-    def _owned(cls, t: torch.Tensor) -> "ScoreMatrix":
+    def _owned(cls, t: torch.Tensor, host_origin: bool = False) -> "ScoreMatrix":
         """Wrap a device tensor this package produced (aligned rows, finite): no copy, no check."""
         sm = cls.__new__(cls)
         sm._host = None
+        sm._src = None
         sm._t = t
         sm._device = t.device
         sm._shape = (int(t.shape[0]), int(t.shape[1]))
-        sm.host_origin = False
+        sm.host_origin = host_origin
         return sm
 
     @property
@@ -183,7 +210,7 @@ class ScoreMatrix:
 
     @property
     def host_array(self) -> np.ndarray | None:
-        """The C-contiguous host array of a host-origin matrix that has not been uploaded yet."""
+        """The C-contiguous host array of a deferred (``defer=True``) matrix not uploaded yet."""
         return None if self._t is not None else self._src
 
     @property
@@ -196,7 +223,8 @@ class ScoreMatrix:
     @property
     def data(self) -> np.ndarray:
         if self._host is None:
-            h = self._src.view() if self._t is None else self._t.cpu().numpy()
+            h = np.array(self._src) if self._t is None else self._t.cpu().numpy()
+            h = np.ascontiguousarray(h)
             h.flags.writeable = False
             self._host = h
         return self._host
@@ -221,8 +249,7 @@ class ScoreMatrix:
     def dtype(self) -> torch.dtype:
         if self._t is not None:
             return self._t.dtype
-        return {np.dtype(np.float32): torch.float32, np.dtype(np.complex64): torch.complex64,
-                np.dtype(np.complex128): torch.complex128}.get(self._src.dtype, torch.float64)
+        return _HOST_DTYPES.get(self._src.dtype, torch.float64)
 
     @property
     def device(self) -> torch.device:
@@ -242,12 +269,35 @@ class ScoreMatrix:
         return {torch.complex64: torch.float32, torch.complex128: torch.float64}.get(self.dtype, self.dtype)
 
 
+def as_scores(S) -> "ScoreMatrix":
+    """A ScoreMatrix of this package from one, from a reference ``fisher_solve.ScoreMatrix`` (any
+    object with a ``.data`` array, core.py:122-162) or from raw data — so code holding the
+    reference's objects can call the B200 entry points unchanged."""
+    if isinstance(S, ScoreMatrix):
+        return S
+    if not isinstance(S, (np.ndarray, torch.Tensor, list, tuple)) and hasattr(S, "data"):
+        return ScoreMatrix(S.data)
+    return ScoreMatrix(S)
+
+
+def as_system(system) -> "DampedSystem":
+    """A DampedSystem of this package from one or from a reference ``fisher_solve.DampedSystem``
+    (``.S``, ``.lam``, ``.v``, core.py:165-203)."""
+    if isinstance(system, DampedSystem):
+        return system
+    if all(hasattr(system, a) for a in ("S", "lam", "v")):
+        return DampedSystem(as_scores(system.S), system.lam, system.v)
+    raise ValueError(f"expected a DampedSystem, got {type(system).__name__}")
+
+
 class DampedSystem:
-    """The system (S^T S + lam I) x = v (core.py:165-203); v lives beside S in S's dtype."""
+    """The system (S^T S + lam I) x = v (core.py:165-203); v lives beside S in S's dtype.
+
+    v is validated (1-D, length m, finite, real when S is real) and copied at construction, like
+    the reference's frozen copy (core.py:179-195)."""
 
     def __init__(self, S: ScoreMatrix, lam, v):
-        if not isinstance(S, ScoreMatrix):
-            S = ScoreMatrix(S)
+        S = as_scores(S)
         self.S = S
         self.lam = _coerce_damping(lam)
         v_complex = v.is_complex() if isinstance(v, torch.Tensor) else np.iscomplexobj(np.asarray(v))
@@ -256,19 +306,8 @@ class DampedSystem:
         self._v = None
         self._vh = None
         self._host_v = None
-        if S.is_complex:
-            # complex scores (SURVEY §8f-3): v keeps its own kind (the real-part variant needs a
-            # real v), in the scores' precision
-            t = _to_device_tensor(v, "right-hand side", S.tensor.device,
-                                  force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
-            if t.dim() != 1:
-                raise ValueError(f"right-hand side must be 1-D, got shape {tuple(t.shape)}")
-            if t.shape[0] != S.m:
-                raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
-            self._v = t.to(S.dtype if t.is_complex() else S.real_dtype)
-            return
-        if not S.is_uploaded and not (isinstance(v, torch.Tensor) and v.is_cuda):
-            # host system: v stays on the host beside S (validated here, it is small)
+        if S.host_array is not None and not (isinstance(v, torch.Tensor) and v.is_cuda):
+            # deferred host system: v stays on the host beside S (validated and copied here)
             vh = _coerce_host(v.numpy() if isinstance(v, torch.Tensor) else v, "right-hand side")
             if vh.ndim != 1:
                 raise ValueError(f"right-hand side must be 1-D, got shape {vh.shape}")
@@ -276,7 +315,7 @@ class DampedSystem:
                 raise ValueError(f"right-hand side length {vh.shape[0]} does not match parameter count {S.m}")
             if not np.isfinite(vh).all():
                 raise ValueError("right-hand side must contain only finite entries")
-            self._vh = np.ascontiguousarray(vh, dtype=np.float32 if S.dtype == torch.float32 else np.float64)
+            self._vh = np.array(vh, dtype=np.float32 if S.dtype == torch.float32 else np.float64, copy=True)
             return
         t = _to_device_tensor(v, "right-hand side", S.tensor.device,
                               force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
@@ -284,11 +323,16 @@ class DampedSystem:
             raise ValueError(f"right-hand side must be 1-D, got shape {tuple(t.shape)}")
         if t.shape[0] != S.m:
             raise ValueError(f"right-hand side length {t.shape[0]} does not match parameter count {S.m}")
-        self._v = t.to(S.dtype)
+        if S.is_complex:
+            # complex scores (SURVEY §8f-3): v keeps its own kind (the real-part variant needs a
+            # real v), in the scores' precision
+            self._v = t.to(S.dtype if t.is_complex() else S.real_dtype)
+        else:
+            self._v = t.to(S.dtype)
 
     @property
     def host_v(self) -> np.ndarray | None:
-        """v on the host (S's dtype) while the system has not been uploaded."""
+        """v on the host (S's dtype) while a deferred system has not been uploaded."""
         return self._vh if self._v is None else None
 
     @property
@@ -300,7 +344,7 @@ class DampedSystem:
     @property
     def v(self) -> np.ndarray:
         if self._host_v is None:
-            h = self._vh.view() if self._v is None else self._v.cpu().numpy()
+            h = self._vh.copy() if self._v is None else self._v.cpu().numpy()
             h.flags.writeable = False
             self._host_v = h
         return self._host_v
@@ -327,7 +371,13 @@ class Solution:                          # core.py:206-223
 
 
 def _dt(t: torch.Tensor) -> int:
-    return _lib.FS_F64 if t.dtype == torch.float64 else _lib.FS_F32
+    """fs_dtype of a REAL device array; complex data never reaches a real kernel (ValueError)."""
+    if t.dtype == torch.float64:
+        return _lib.FS_F64
+    if t.dtype == torch.float32:
+        return _lib.FS_F32
+    raise ValueError(f"this kernel takes real float32/float64 data, got {t.dtype}"
+                     + (" (complex scores go through the real embeddings)" if t.is_complex() else ""))
 
 
 def _stream(device) -> int:
@@ -361,22 +411,54 @@ def resolve_precision(precision: str, dtype: torch.dtype) -> str:
 
 
 def gram_packed(S: ScoreMatrix, lam: float, precision: str = "auto") -> torch.Tensor:
-    """Packed lower W = S S^T + lam I on the device (fp64, length n(n+1)/2)."""
+    """Packed lower W = S S^T + lam I on the device (fp64, length n(n+1)/2); real scores only
+    (complex scores: ``gram`` returns the Hermitian S S^H + lam I)."""
     t = S.tensor
     n, m = S.n, S.m
+    dt = _dt(t)
     prec = resolve_precision(precision, t.dtype)
     ctx = _lib.context_for(t.device.index, n, m)
     out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
-    rc = ctx.lib.fs_gram_packed(ctx.handle, _dt(t), PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0),
+    rc = ctx.lib.fs_gram_packed(ctx.handle, dt, PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0),
                                 float(lam), out.data_ptr(), _stream(t.device))
     _check(ctx, rc, "fs_gram_packed")
     return out
 
 
-def gram(S: ScoreMatrix, lam: float, meter: WorkspaceMeter | None = None, precision: str = "auto") -> np.ndarray:
-    """Damped Gram matrix W = S S^T + lam I, n-by-n, exactly symmetric (core.py:270-290)."""
-    lam = _coerce_damping(lam)
+def gram_hermitian_device(S: ScoreMatrix, lam: float, precision: str = "auto") -> torch.Tensor:
+    """W = S S^H + lam I for complex scores, an n x n complex128 CUDA tensor, exactly Hermitian
+    (core.py:279-290).  The Gram of C = [Re S; Im S] (2n x m, fs_embed_complex kind 0) holds
+    Re S Re S^T + Im S Im S^T (the real part) and Im S Re S^T - Re S Im S^T (the imaginary part)
+    in its blocks; fs_hermitian_gram combines them, mirrors with conjugation and adds lam."""
+    if not S.is_complex:
+        raise ValueError("gram_hermitian_device expects complex scores")
     n = S.n
+    C = embed_complex(S, 0)
+    G2 = gram_packed(C, 0.0, precision)
+    dev = G2.device
+    W = torch.empty((n, n), dtype=torch.complex128, device=dev)
+    ctx = _lib.context_for(dev.index, 2 * n, S.m)
+    rc = ctx.lib.fs_hermitian_gram(ctx.handle, G2.data_ptr(), n, float(lam), W.data_ptr(), n, _stream(dev))
+    _check(ctx, rc, "fs_hermitian_gram")
+    return W
+
+
+def gram(S: ScoreMatrix, lam: float, meter: WorkspaceMeter | None = None, precision: str = "auto") -> np.ndarray:
+    """Damped Gram matrix W = S S^T + lam I (S S^H for complex S), n-by-n, exactly symmetric /
+    Hermitian (core.py:270-290)."""
+    lam = _coerce_damping(lam)
+    S = as_scores(S)
+    n = S.n
+    if S.is_complex:
+        if meter is not None:
+            meter.alloc(2 * S.n * S.m)          # the embedded copy [Re S; Im S]
+            meter.alloc(2 * n * (2 * n + 1))
+            meter.free(2 * S.n * S.m)
+        W = gram_hermitian_device(S, lam, precision).cpu().numpy()
+        if meter is not None:
+            meter.alloc(2 * n * n)
+            meter.free(2 * n * (2 * n + 1))
+        return W
     if meter is not None:
         meter.alloc(n * (n + 1) // 2)
     packed = gram_packed(S, lam, precision).cpu().numpy()
@@ -440,8 +522,9 @@ def residual(system: DampedSystem, x, variant: Variant = Variant.PLAIN) -> tuple
 
     HERMITIAN (S^H S + lam I) and REALPART (Re[S^H S] + lam I) are evaluated through the real
     representation / the stacked real matrix (fs_embed_complex): the same norms."""
+    system = as_system(system)
     if not isinstance(variant, Variant):
-        raise ValueError(f"unknown operator variant: {variant!r}")
+        variant = _as_variant(variant)
     if variant is not Variant.PLAIN:
         if not system.S.is_complex:
             raise ValueError(f"variant {variant.value} expects complex scores")
@@ -458,13 +541,69 @@ def residual(system: DampedSystem, x, variant: Variant = Variant.PLAIN) -> tuple
             raise ValueError("the real-part operator needs a real right-hand side and solution")
         inner = DampedSystem(embed_complex(system.S, 0), system.lam, system.v_tensor)
         return residual_device(inner, xt.to(torch.float64).contiguous())
+    if system.S.is_complex:
+        return _residual_plain_complex(system, x)
     if isinstance(x, torch.Tensor):
-        xt = x.to(system.S.tensor.device, torch.float64).contiguous()
+        xt = x.to(system.S.tensor.device)
     else:
         xa = np.asarray(x)
         if xa.ndim != 1 or xa.shape[0] != system.m:
             raise ValueError(f"solution vector has shape {xa.shape}, expected ({system.m},)")
-        xt = torch.from_numpy(np.ascontiguousarray(xa, dtype=np.float64)).to(system.S.tensor.device)
+        xt = torch.from_numpy(np.ascontiguousarray(xa)).to(system.S.tensor.device)
+    if xt.is_complex():
+        # real operator, complex x: ||A Re x - v||^2 + ||A Im x||^2 (core.py:296-297 on complex x)
+        if xt.dim() != 1 or xt.shape[0] != system.m:
+            raise ValueError(f"solution vector has shape {tuple(xt.shape)}, expected ({system.m},)")
+        a_re, _ = residual_device(system, xt.real.to(torch.float64).contiguous())
+        zero = DampedSystem(system.S, system.lam, torch.zeros_like(system.v_tensor))
+        a_im, _ = residual_device(zero, xt.imag.to(torch.float64).contiguous())
+        abs_res = float(np.hypot(a_re, a_im))
+        return abs_res, abs_res / max(float(torch.linalg.vector_norm(system.v_tensor.double())), EPS)
+    xt = xt.to(torch.float64).contiguous()
     if xt.dim() != 1 or xt.shape[0] != system.m:
         raise ValueError(f"solution vector has shape {tuple(xt.shape)}, expected ({system.m},)")
     return residual_device(system, xt)
+
+
+def _as_variant(variant) -> Variant:
+    """Variant from this package's enum, the reference's (same values) or its string value."""
+    try:
+        return Variant(getattr(variant, "value", variant))
+    except ValueError:
+        raise ValueError(f"unknown operator variant: {variant!r}") from None
+
+
+def _residual_plain_complex(system: DampedSystem, x) -> tuple[float, float]:
+    """PLAIN variant on complex scores: ||S^T (S x) + lam x - v|| without conjugation, as
+    core.py:296-297 evaluates it for complex A.  With rho(S) = [[Re S, -Im S], [Im S, Re S]]
+    (fs_embed_complex kind 1): rho(S) [Re x; Im x] = [Re Sx; Im Sx], and rho(S)^T applied to
+    [Re t; -Im t] gives [Re S^T t; -Im S^T t]; so with y' = [Re Sx; -Im Sx], x' = [Re x; -Im x]
+    and v' = [Re v; -Im v], fs_residual_cols forms [Re r; -Im r] and the same norms."""
+    S = system.S
+    dev = S.tensor.device
+    xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
+    xt = xt.to(dev)
+    if xt.dim() != 1 or xt.shape[0] != system.m:
+        raise ValueError(f"solution vector has shape {tuple(xt.shape)}, expected ({system.m},)")
+    n, m = S.n, S.m
+    E = embed_complex(S, 1).tensor
+    xhat = stack_complex_vector(xt, torch.float64)
+    ctx = _lib.context_for(dev.index, 2 * n, 2 * m)
+    st = _stream(dev)
+    y = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    rc = ctx.lib.fs_gemv_rows(ctx.handle, _dt(E), E.data_ptr(), 2 * n, 2 * m, E.stride(0), xhat.data_ptr(),
+                              _lib.FS_F64, y.data_ptr(), st)
+    _check(ctx, rc, "fs_gemv_rows")
+    y[n:].neg_()
+    xflip = xhat.clone()
+    xflip[m:].neg_()
+    vflip = stack_complex_vector(system.v_tensor, torch.float64)
+    vflip[m:].neg_()
+    sums = torch.empty(2, dtype=torch.float64, device=dev)
+    rc = ctx.lib.fs_residual_cols(ctx.handle, _dt(E), E.data_ptr(), 2 * n, 2 * m, E.stride(0), y.data_ptr(),
+                                  xflip.data_ptr(), vflip.data_ptr(), _lib.FS_F64, system.lam, None,
+                                  sums.data_ptr(), st)
+    _check(ctx, rc, "fs_residual_cols")
+    rr, vv = sums.cpu().tolist()
+    abs_res = float(np.sqrt(rr))
+    return abs_res, abs_res / max(float(np.sqrt(vv)), EPS)

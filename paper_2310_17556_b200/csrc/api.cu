@@ -41,6 +41,12 @@ struct fs_ctx {
   size_t ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
+  // multi-rank failure protocol (see solve_tail): first local failure of the current solve, an
+  // empty (zero-column) shard, and whether this rank's own input was non-finite
+  int poison_rc = 0;
+  std::string poison_msg;
+  bool empty_shard = false;
+  bool local_nonfinite = false;
   uint8_t* d_St = nullptr;      // tiled copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
   // eigh comparison route (lazy): Jacobi workspace, U (n_max^2), w, scratch, info
@@ -51,6 +57,8 @@ struct fs_ctx {
   int* d_info = nullptr;
   int* h_info = nullptr;        // pinned [2]
   double* h_w = nullptr;        // pinned n_max
+  void* d_svd = nullptr;        // direct-SVD route (lazy): Jacobi SVD workspace / tri-inverse scratch
+  size_t svd_bytes = 0;
   float* d_scale = nullptr;     // F16X2 row scales (n_max)
   double* d_inv_scale = nullptr;
   int* d_ovf = nullptr;         // F16X2 retile flags (bit 1: fp16 overflow)
@@ -187,14 +195,31 @@ int ensure_eig(fs_ctx* ctx) {
   bool ok = cudaMalloc(&ctx->d_eig, fs::syevj_workspace_bytes(n, ctx->num_sms)) == cudaSuccess &&
             cudaMalloc((void**)&ctx->d_U, (size_t)n * n * sizeof(double)) == cudaSuccess &&
             cudaMalloc((void**)&ctx->d_w, (size_t)n * sizeof(double)) == cudaSuccess &&
-            cudaMalloc((void**)&ctx->d_t, (size_t)n * sizeof(double)) == cudaSuccess &&
-            cudaMalloc((void**)&ctx->d_info, 2 * sizeof(int)) == cudaSuccess &&
-            cudaMallocHost((void**)&ctx->h_info, 2 * sizeof(int)) == cudaSuccess &&
+            (ctx->d_t || cudaMalloc((void**)&ctx->d_t, (size_t)n * sizeof(double)) == cudaSuccess) &&
+            (ctx->d_info || cudaMalloc((void**)&ctx->d_info, 2 * sizeof(int)) == cudaSuccess) &&
+            (ctx->h_info || cudaMallocHost((void**)&ctx->h_info, 2 * sizeof(int)) == cudaSuccess) &&
             cudaMallocHost((void**)&ctx->h_w, (size_t)n * sizeof(double)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     return fail(ctx, FS_ENOMEM, "cannot allocate the eigensolver workspace");
   }
+  return FS_OK;
+}
+
+int ensure_svd(fs_ctx* ctx, int64_t n) {
+  const size_t need = std::max(fs::jacobi_svd_workspace_bytes(n), (size_t)n * n * sizeof(double));
+  if (ctx->svd_bytes >= need) return FS_OK;
+  if (ctx->d_svd) cudaFree(ctx->d_svd);
+  ctx->d_svd = nullptr;
+  ctx->svd_bytes = 0;
+  bool ok = cudaMalloc(&ctx->d_svd, need) == cudaSuccess;
+  if (ok && !ctx->d_info) ok = cudaMalloc((void**)&ctx->d_info, 2 * sizeof(int)) == cudaSuccess;
+  if (ok && !ctx->h_info) ok = cudaMallocHost((void**)&ctx->h_info, 2 * sizeof(int)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    return fail(ctx, FS_ENOMEM, "cannot allocate the SVD workspace");
+  }
+  ctx->svd_bytes = need;
   return FS_OK;
 }
 
@@ -278,56 +303,113 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
 // internal: the F16X2 Gram overflowed on some rank -> recompute with TF32X3
 constexpr int kRetryTf32 = 100;
 
+// ---- multi-rank failure protocol ----
+// With an all-reduce callback every rank must issue the same collectives in the same order, so
+// no rank may return between two of them.  A rank whose local step fails (a CUDA error, a lazy
+// allocation that does not fit, an empty shard's missing data) becomes "idle": it records the
+// first failure, skips its remaining kernels, contributes zeros to every collective and keeps
+// joining them.  The norms all-reduce carries a status slot (sums[3] = idle + 1024 * non-finite
+// input), so every rank learns at the same host synchronisation that the solve failed and all
+// return an error together (the failing rank its own status, the others FS_ECUDA / FS_EINVAL
+// naming a peer).  Host-side control flow between collectives depends only on all-reduced values
+// (the norms, the overflow flag) or on arguments every rank shares, so ranks cannot diverge.
+// One rank (no callback) keeps the direct early returns.
+constexpr double kStatusIdle = 1.0, kStatusNonFinite = 1024.0;
+
+namespace {
+void poison(fs_ctx* ctx, int rc) {
+  if (!ctx->poison_rc) {
+    ctx->poison_rc = rc;
+    ctx->poison_msg = ctx->err;
+  }
+}
+
+__global__ void status_slot_kernel(const int* nonfinite, int idle, int host_nonfinite, double* out) {
+  double s = idle ? kStatusIdle : 0.0;
+  if (host_nonfinite || (nonfinite && (*nonfinite & 1))) s += kStatusNonFinite;
+  *out = s;
+}
+
+// after the norms all-reduce: the collective decision when the status slot is set
+int collective_failure(fs_ctx* ctx, double status) {
+  const long long nf = (long long)(status / kStatusNonFinite);
+  if (ctx->poison_rc) {
+    ctx->err = ctx->poison_msg;
+    return ctx->poison_rc;
+  }
+  if (ctx->local_nonfinite) return fail(ctx, FS_EINVAL, "score matrix and right-hand side must contain only finite entries");
+  if (nf > 0) return fail(ctx, FS_EINVAL, "a peer rank's score shard or right-hand side has non-finite entries");
+  return fail(ctx, FS_ECUDA, "a peer rank failed during the collective solve");
+}
+}  // namespace
+
+// a local step inside a collective solve: single rank -> return the failure; multi-rank -> idle
+#define FS_STEP(expr)                          \
+  do {                                         \
+    int _r = (expr);                           \
+    if (_r) {                                  \
+      if (!multi) return _r;                   \
+      poison(ctx, _r);                         \
+    }                                          \
+  } while (0)
+#define FS_CKS(expr, where) FS_STEP(([&]() -> int { cudaError_t _e = (expr); \
+                                      return _e == cudaSuccess ? FS_OK : cuda_fail(ctx, _e, where); })())
+
 static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
                     double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
-                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf);
+                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf,
+                    const int* nonfinite = nullptr);
 
 // ovf: F16X2 retile flag word (bit 2 = fp16 overflow) or NULL.  The bit joins the norms
 // all-reduce, so every rank takes the same retry decision.
 static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
                double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
-               double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf = nullptr) {
-  int rc = FS_OK;
-  const int nsums = ovf ? 3 : 2;
+               double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf = nullptr,
+               const int* nonfinite = nullptr) {
+  const bool multi = allreduce != nullptr;
   void* stream = (void*)st;
   double* u = ctx->d_packed + n * (n + 1) / 2;
-  if (allreduce && allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
-    return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
+  if (multi) {
+    if (ctx->poison_rc || ctx->empty_shard) cudaMemsetAsync(ctx->d_packed, 0, packed_len(n) * sizeof(double), st);
+    if (allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
+      return fail(ctx, FS_ECUDA, "allreduce of [W | u] failed");
+  }
   prof_mark(ctx, FS_PROF_ALLREDUCE, st);
-  // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic)
-  if ((rc = fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream))) return rc;
-  // L = chol(W) with the TRSV pair z = L^-T L^-1 u fused into the same persistent kernel
+  // 2. W = G + lam I, L = chol(W) (redundant on every rank, deterministic: identical L)
   bool solved = false;
-  {
-    FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
+  if (!ctx->poison_rc) FS_STEP(fs_unpack_lower(ctx, ctx->d_packed, n, lam, ctx->d_W, n, stream));
+  if (!ctx->poison_rc) {
+    // L = chol(W) with the TRSV pair z = L^-T L^-1 u fused into the same persistent kernel
+    FS_CKS(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
     int l = 0;
-    cudaError_t e = fs::potrf_lower(ctx->d_W, n, n, ctx->d_status, ctx->d_potrf, st, &l, u, ctx->d_z, &solved);
+    if (!ctx->poison_rc) FS_CKS(fs::potrf_lower(ctx->d_W, n, n, ctx->d_status, ctx->d_potrf, st, &l, u, ctx->d_z, &solved),
+                                "potrf");
     ctx->launches += l;
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "potrf");
   }
   prof_mark(ctx, FS_PROF_POTRF, st);
-  if (!solved) {
-    FS_CK(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
+  if (!solved && !ctx->poison_rc) {
+    FS_CKS(cudaMemcpyAsync(ctx->d_z, u, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "copy u");
     int l = 0;
-    cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
+    if (!ctx->poison_rc) FS_CKS(fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l), "trsv_pair");
     ctx->launches += l;
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair");
   }
   prof_mark(ctx, FS_PROF_TRSV, st);
   return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
-                  out_res, st, ovf);
+                  out_res, st, ovf, nonfinite);
 }
 
 // From z (in ctx->d_z) to x = (v - S^T z)/lam, the residual diagnostics and the optional
 // refinement with the Cholesky factor in ctx->d_W (solvers.py:122-126, :160-194).
 static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v, int vdt,
                     double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user, int flags,
-                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf) {
-  int rc = FS_OK;
+                    double refine_above, int64_t* pivot, double* out_res, cudaStream_t st, const int* ovf,
+                    const int* nonfinite) {
+  const bool multi = allreduce != nullptr;
   void* stream = (void*)st;
-  const int nsums = ovf ? 3 : 2;
+  const int nsums = multi ? 4 : (ovf ? 3 : 2);
   const bool want_res = (flags & FS_FLAG_RESIDUAL) != 0;
   const bool want_refine = (flags & FS_FLAG_REFINE) != 0;
+  auto idle = [&]() { return ctx->poison_rc != 0 || ctx->empty_shard; };
   // 3. x = (v - S^T z) / lam on the local shard; with diagnostics fused with y = S x (one
   //    HBM pass; falls back to two passes when n is too large for the fused kernel)
   bool y_ready = false;
@@ -350,9 +432,9 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve");
     return FS_OK;
   };
-  if ((rc = solve_cols(v, vdt == FS_F64, lam, false))) return rc;
+  if (!idle()) FS_STEP(solve_cols(v, vdt == FS_F64, lam, false));
   prof_mark(ctx, FS_PROF_GEMV_STZ, st);
-  if (ctx->early_x_host) {   // host entry: x -> host on up_st while the residual pass runs
+  if (ctx->early_x_host && !idle()) {   // host entry: x -> host on up_st while the residual pass runs
     FS_CK(cudaEventRecord(ctx->ev_xready, st), "event");
     FS_CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_xready, 0), "event wait");
     FS_CK(cudaMemcpyAsync(ctx->early_x_host, x, m * sizeof(double), cudaMemcpyDeviceToHost, ctx->up_st),
@@ -360,34 +442,49 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     FS_CK(cudaEventRecord(ctx->ev_xcopy, ctx->up_st), "event");
     ctx->early_x_state = 1;
   }
+  // the status slot and the overflow flag of one norms all-reduce (multi-rank: always 4 doubles)
+  auto fill_flags = [&]() -> int {
+    if (ovf && !idle()) {
+      int lf = 0;
+      FS_CKS(fs::flag_bit_to_double(ovf, 2, ctx->d_sums + 2, st, &lf), "overflow flag");
+      ctx->launches += lf;
+    } else if (multi) {
+      cudaMemsetAsync(ctx->d_sums + 2, 0, sizeof(double), st);
+    }
+    if (multi) {
+      status_slot_kernel<<<1, 1, 0, st>>>(nonfinite, ctx->poison_rc != 0 ? 1 : 0, ctx->local_nonfinite ? 1 : 0,
+                                          ctx->d_sums + 3);
+      ctx->launches += 1;
+    }
+    return FS_OK;
+  };
   double abs_res = NAN, rel_res = NAN;
   // refinement steps: FS_FLAG_REFINE alone = the reference's single step; bits 8-15 raise it
   const int max_steps = want_refine ? std::max(1, (flags >> 8) & 0xFF) : 0;
   double prev_rel = INFINITY;
   for (int pass = 0; want_res && pass <= max_steps; ++pass) {
     // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
-    if (!y_ready && (rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream))) return rc;
-    if (allreduce && allreduce(ctx->d_y, n, allreduce_user, stream) != 0)
-      return fail(ctx, FS_ECUDA, "allreduce of y failed");
-    {
+    if (!y_ready && !idle()) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream));
+    if (multi) {
+      if (idle()) cudaMemsetAsync(ctx->d_y, 0, n * sizeof(double), st);
+      if (allreduce(ctx->d_y, n, allreduce_user, stream) != 0) return fail(ctx, FS_ECUDA, "allreduce of y failed");
+    }
+    if (!idle()) {
       int l = 0;
-      cudaError_t e = fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
-                                        pass < max_steps ? ctx->d_r : nullptr, ctx->d_block_sums,
-                                        ctx->d_sums, st, &l);
+      FS_CKS(fs::residual_cols(dtype == FS_F64, S, n, m, ldS, ctx->d_y, x, v, vdt == FS_F64, lam,
+                               pass < max_steps ? ctx->d_r : nullptr, ctx->d_block_sums, ctx->d_sums, st, &l),
+             "residual_cols");
       ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "residual_cols");
     }
-    if (ovf) {
-      int lf = 0;
-      FS_CK(fs::flag_bit_to_double(ovf, 2, ctx->d_sums + 2, st, &lf), "overflow flag");
-      ctx->launches += lf;
-    }
-    if (allreduce && allreduce(ctx->d_sums, nsums, allreduce_user, stream) != 0)
+    if (idle()) cudaMemsetAsync(ctx->d_sums, 0, 2 * sizeof(double), st);
+    if (int r = fill_flags()) return r;
+    if (multi && allreduce(ctx->d_sums, nsums, allreduce_user, stream) != 0)
       return fail(ctx, FS_ECUDA, "allreduce of residual norms failed");
     prof_mark(ctx, FS_PROF_RESIDUAL, st);
     FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, nsums * sizeof(double), cudaMemcpyDeviceToHost, st), "norms d2h");
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
+    if (multi && ctx->h_sums[3] > 0.0) return collective_failure(ctx, ctx->h_sums[3]);
     if (ovf && ctx->h_sums[2] > 0.0) return kRetryTf32;
     if (*ctx->h_status != 0) break;
     abs_res = sqrt(ctx->h_sums[0]);
@@ -398,34 +495,41 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     prev_rel = rel_res;
     // one correction pass with the same factor (solvers.py:183-194): d = chol_apply(-r)
     // residual_cols stored r = (S^T y + lam x) - v; refinement right-hand side is -r
-    if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream))) return rc;
-    if (allreduce && allreduce(ctx->d_z, n, allreduce_user, stream) != 0)
-      return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
-    {
+    if (!idle()) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, ctx->d_r, FS_F64, ctx->d_z, stream));
+    if (multi) {
+      if (idle()) cudaMemsetAsync(ctx->d_z, 0, n * sizeof(double), st);
+      if (allreduce(ctx->d_z, n, allreduce_user, stream) != 0)
+        return fail(ctx, FS_ECUDA, "allreduce of refinement u failed");
+    }
+    if (!ctx->poison_rc) {
       int l = 0;
-      cudaError_t e = fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l);
+      FS_CKS(fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l), "trsv_pair (refine)");
       ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "trsv_pair (refine)");
     }
     // x += (-r - S^T z') / lam  ==  x - (r + S^T z') / lam ; z' = W^-1 S r  (linearity)
     if (ctx->early_x_state == 1) {   // x changes: the early copy must finish reading it first
       FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");
       ctx->early_x_state = 2;
     }
-    if ((rc = solve_cols(ctx->d_r, 1, -lam, true))) return rc;
+    if (!idle()) FS_STEP(solve_cols(ctx->d_r, 1, -lam, true));
   }
   if (!want_res) {
-    if (ovf) {
-      int lf = 0;
-      FS_CK(fs::flag_bit_to_double(ovf, 2, ctx->d_sums + 2, st, &lf), "overflow flag");
-      ctx->launches += lf;
-      if (allreduce && allreduce(ctx->d_sums + 2, 1, allreduce_user, stream) != 0)
-        return fail(ctx, FS_ECUDA, "allreduce of the overflow flag failed");
-      FS_CK(cudaMemcpyAsync(ctx->h_sums + 2, ctx->d_sums + 2, sizeof(double), cudaMemcpyDeviceToHost, st), "flag d2h");
+    const int off = 2, cnt = multi ? 2 : 1;
+    if (ovf || multi) {
+      if (int r = fill_flags()) return r;
+      if (multi && allreduce(ctx->d_sums + off, cnt, allreduce_user, stream) != 0)
+        return fail(ctx, FS_ECUDA, "allreduce of the overflow / status flags failed");
+      FS_CK(cudaMemcpyAsync(ctx->h_sums + off, ctx->d_sums + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, st),
+            "flag d2h");
     }
     FS_CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "status d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
+    if (multi && ctx->h_sums[3] > 0.0) return collective_failure(ctx, ctx->h_sums[3]);
     if (ovf && ctx->h_sums[2] > 0.0) return kRetryTf32;
+  }
+  if (ctx->poison_rc) {   // single rank never gets here idle; multi-rank: the status slot said so
+    ctx->err = ctx->poison_msg;
+    return ctx->poison_rc;
   }
   if (ctx->prof_on) {
     // each mark closes the stage it names (refinement passes fold into their stages)
@@ -513,6 +617,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   cudaFree(ctx->d_potrf);
   cudaFree(ctx->d_scale); cudaFree(ctx->d_inv_scale); cudaFree(ctx->d_ovf);
   if (ctx->d_eig) cudaFree(ctx->d_eig);
+  if (ctx->d_svd) cudaFree(ctx->d_svd);
   if (ctx->d_U) cudaFree(ctx->d_U);
   if (ctx->d_w) cudaFree(ctx->d_w);
   if (ctx->d_t) cudaFree(ctx->d_t);
@@ -674,54 +779,75 @@ int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m
   return FS_OK;
 }
 
-int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
-                  int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
-                  void* allreduce_user, int flags, double refine_above, int64_t* pivot,
-                  double* out_res, void* stream) {
-  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+// one solve's local state of the multi-rank protocol starts clean
+static void begin_solve(fs_ctx* ctx, bool empty) {
+  ctx->poison_rc = 0;
+  ctx->poison_msg.clear();
+  ctx->empty_shard = empty;
+  ctx->local_nonfinite = false;
+}
+
+static int chol_solve_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m, int64_t ldS,
+                           const void* v, double lam, double* x, fs_allreduce_fn allreduce, void* allreduce_user,
+                           int flags, double refine_above, int64_t* pivot, double* out_res, void* stream,
+                           const int* nonfinite = nullptr) {
+  const bool multi = allreduce != nullptr;
+  // an empty column shard (m < world) still joins every collective with zero contributions
+  const bool empty = multi && m == 0;
+  int rc = empty ? (ctx && n >= 1 && n <= ctx->n_max ? FS_OK : check_shape(ctx, dtype, S, n, 1, 1))
+                 : check_shape(ctx, dtype, S, n, m, ldS);
   if (rc) return rc;
   if ((rc = check_lam(ctx, lam))) return rc;
-  if (!v || !x) return fail(ctx, FS_EINVAL, "NULL vector");
+  if (!empty && (!v || !x)) return fail(ctx, FS_EINVAL, "NULL vector");
+  int use_tc = 0;
+  if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
   if (pivot) *pivot = -1;
+  begin_solve(ctx, empty);
+  if (flags & FS_FLAG_INVALID_SHARD) {
+    // the caller found non-finite entries in this rank's shard: fail, on every rank together
+    fail(ctx, FS_EINVAL, "score matrix and right-hand side must contain only finite entries");
+    if (!multi) return FS_EINVAL;
+    poison(ctx, FS_EINVAL);
+    ctx->local_nonfinite = true;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int vdt = dtype;  // v has the dtype of S
-  {
+  if (dtype == FS_F32 && !use_tc && !empty && !ctx->poison_rc) {
     // fp64 precision mode on fp32 scores: widen v once so every GEMV product is exact fp64
-    int use_tc = 0;
-    if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
-    if (dtype == FS_F32 && !use_tc) {
-      int l = 0;
-      cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
-      ctx->launches += l;
-      if (e != cudaSuccess) return cuda_fail(ctx, e, "widen v");
-      v = ctx->d_v64;
-      vdt = FS_F64;
-    }
+    int l = 0;
+    FS_CKS(fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l), "widen v");
+    ctx->launches += l;
+    v = ctx->d_v64;
+    vdt = FS_F64;
   }
   double* u = ctx->d_packed + n * (n + 1) / 2;
   ctx->n_marks = 0;
   prof_mark(ctx, -1, st);
-  // 1. partial Gram (no shift) and u = S v, packed for one all-reduce (TF32X3: one fused
-  //    streaming pass computes u and writes the tiled copy the tensor-core SYRK reads)
-  {
-    int use_tc = 0;
-    if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+  // 1. partial Gram (no shift) and u = S v, packed for one all-reduce (tensor-core modes: one
+  //    fused streaming pass computes u and writes the tiled copy the SYRK reads)
+  if (!empty && !ctx->poison_rc) {
     if (use_tc && vdt == FS_F32) {
-      if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st, (const float*)v, u))) return rc;
+      FS_STEP(gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st, (const float*)v, u));
     } else {
-      if ((rc = gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st))) return rc;
-      if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+      FS_STEP(gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st));
+      if (!ctx->poison_rc) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream));
       prof_mark(ctx, FS_PROF_GEMV_SV, st);
     }
   }
-  int use_tc = 0;
-  resolve_precision(ctx, dtype, precision, S, ldS, &use_tc);
   rc = solve_tail(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
-                  out_res, st, use_tc == 2 ? ctx->d_ovf : nullptr);
+                  out_res, st, use_tc == 2 ? ctx->d_ovf : nullptr, nonfinite);
   if (rc == kRetryTf32)
-    return fs_chol_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
-                         refine_above, pivot, out_res, stream);
+    return chol_solve_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
+                           refine_above, pivot, out_res, stream, nonfinite);
   return rc;
+}
+
+int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
+                  int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
+                  void* allreduce_user, int flags, double refine_above, int64_t* pivot,
+                  double* out_res, void* stream) {
+  return chol_solve_impl(ctx, dtype, precision, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
+                         refine_above, pivot, out_res, stream);
 }
 
 int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host, int64_t n, int64_t m,
@@ -736,6 +862,8 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
   int use_tc = 0;
   if ((rc = resolve_precision(ctx, dtype, precision, S_host, ldS, &use_tc))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool multi = allreduce != nullptr;   // see solve_tail: no rank returns between collectives
+  begin_solve(ctx, false);
   const size_t elem = dtype == FS_F64 ? 8 : 4;
   const int64_t per16 = 16 / (int64_t)elem;
   const int64_t ldd = (m + per16 - 1) / per16 * per16;   // device rows start on 16-byte boundaries
@@ -747,11 +875,13 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     ctx->Sin_bytes = 0;
     if (cudaMalloc(&ctx->d_Sin, need) != cudaSuccess) {
       cudaGetLastError();
-      return fail(ctx, FS_ENOMEM, "cannot allocate the device copy of S");
+      ctx->d_Sin = nullptr;
+      FS_STEP(fail(ctx, FS_ENOMEM, "cannot allocate the device copy of S"));
+    } else {
+      ctx->Sin_bytes = need;
     }
-    ctx->Sin_bytes = need;
   }
-  if (!ctx->d_vin) {
+  if (!ctx->d_vin && !ctx->poison_rc) {
     bool ok = cudaMalloc((void**)&ctx->d_vin, ctx->m_max * sizeof(double)) == cudaSuccess &&
               cudaMalloc((void**)&ctx->d_xin, ctx->m_max * sizeof(double)) == cudaSuccess &&
               cudaMalloc((void**)&ctx->d_flag, sizeof(int)) == cudaSuccess &&
@@ -764,20 +894,22 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
       ok = cudaEventCreateWithFlags(&ctx->ev_chunk[i], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
       cudaGetLastError();
-      return fail(ctx, FS_ENOMEM, "cannot allocate the host-entry buffers");
+      FS_STEP(fail(ctx, FS_ENOMEM, "cannot allocate the host-entry buffers"));
     }
   }
   const bool direct = use_tc == 2 && f16_direct() && fs::syrk_tc_supported(ctx->d_Sin, ldd);
-  if (use_tc && !direct && (rc = ensure_tiles(ctx, use_tc == 2))) return rc;
+  if (use_tc && !direct && !ctx->poison_rc) FS_STEP(ensure_tiles(ctx, use_tc == 2));
   ctx->n_marks = 0;
   prof_mark(ctx, -1, st);
-  FS_CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st), "flag reset");
-  FS_CK(cudaMemcpyAsync(ctx->d_vin, v_host, m * elem, cudaMemcpyHostToDevice, st), "v h2d");
   int l = 0;
-  FS_CK(fs::check_finite(ctx->d_vin, dtype == FS_F64, 1, m, m, ctx->d_flag, ctx->num_sms, st, &l), "check v");
-  // the upload stream must not overwrite d_Sin while earlier work on `st` still reads it
-  FS_CK(cudaEventRecord(ctx->ev_free, st), "event");
-  FS_CK(cudaStreamWaitEvent(ctx->up_st, ctx->ev_free, 0), "event wait");
+  if (!ctx->poison_rc) {
+    FS_CKS(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st), "flag reset");
+    FS_CKS(cudaMemcpyAsync(ctx->d_vin, v_host, m * elem, cudaMemcpyHostToDevice, st), "v h2d");
+    FS_CKS(fs::check_finite(ctx->d_vin, dtype == FS_F64, 1, m, m, ctx->d_flag, ctx->num_sms, st, &l), "check v");
+    // the upload stream must not overwrite d_Sin while earlier work on `st` still reads it
+    FS_CKS(cudaEventRecord(ctx->ev_free, st), "event");
+    FS_CKS(cudaStreamWaitEvent(ctx->up_st, ctx->ev_free, 0), "event wait");
+  }
   const int64_t hpitch = ldS * (int64_t)elem, dpitch = ldd * (int64_t)elem;
   // upload columns [c0, c1) of every row (2-D copy: n segments of (c1-c0) elements)
   auto upload = [&](int64_t c0, int64_t c1, int ev) -> cudaError_t {
@@ -799,7 +931,12 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     fs_ctx* c;
     ~EarlyReset() { c->early_x_host = nullptr; c->early_x_state = 0; }
   } early_reset{ctx};
-  if (use_tc) {
+  const int* nonfinite = ctx->d_flag;
+  if (ctx->poison_rc) {
+    // this rank failed before the first collective: join them idle (multi-rank only)
+    rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
+                    pivot, out_res, st, nullptr, nullptr);
+  } else if (use_tc) {
     // K-chunks of >= 32 MB (about 16, then tapering): upload columns [c0, c1) of all rows -> retile them (+ u
     // partials + finiteness) -> SYRK over their K-blocks, accumulated into the packed Gram.  The
     // transfer of chunk c+1 overlaps the kernels of chunk c; only the last chunk's share is exposed.
@@ -816,15 +953,15 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
       return rest - w < CW ? rest : w;
     };
     int c = 0;
-    for (int64_t c0 = 0, c1 = 0; c0 < m; c0 = c1, ++c) {
+    for (int64_t c0 = 0, c1 = 0; c0 < m && !ctx->poison_rc; c0 = c1, ++c) {
       c1 = std::min(m, c0 + (c + 1 < fs_ctx::kMaxChunks ? next_width(m - c0) : m - c0));
-      FS_CK(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
+      FS_CKS(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
       if (use_tc == 2 && direct) {
         // F16X2 direct: row scales from the first chunk's columns, then the K-range SYRK splits the
         // chunk in-kernel and accumulates u = S v
         if (c == 0)
-          FS_CK(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
-        FS_CK(fs::syrk_f16_direct((const float*)S, ldd, n, m, ctx->d_scale, ctx->d_inv_scale, (const float*)v,
+          FS_CKS(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
+        FS_CKS(fs::syrk_f16_direct((const float*)S, ldd, n, m, ctx->d_scale, ctx->d_inv_scale, (const float*)v,
                                   ctx->d_flag, ctx->d_partials, u, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms,
                                   st, &l, (int)(c0 / fs::kTile16Cols),
                                   (int)((c1 + fs::kTile16Cols - 1) / fs::kTile16Cols), c > 0),
@@ -832,43 +969,48 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
       } else if (use_tc == 2) {
         // F16X2: row scales from the first chunk's columns, then split planes + K-range SYRK
         if (c == 0)
-          FS_CK(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
-        FS_CK(fs::retile16_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St,
+          FS_CKS(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
+        FS_CKS(fs::retile16_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St,
                                 ctx->d_scale, c0, c1, ctx->d_flag, st, &l),
               "retile16");
-        FS_CK(fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st,
+        FS_CKS(fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st,
                            &l, (int)(c0 / fs::kTile16Cols), (int)((c1 + fs::kTile16Cols - 1) / fs::kTile16Cols),
                            c > 0),
               "syrk_f16");
       } else {
-        FS_CK(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
+        FS_CKS(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
                               ctx->d_flag, st, &l),
               "retile");
-        FS_CK(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
+        FS_CKS(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
                           (int)(c0 / fs::kTileCols), (int)((c1 + fs::kTileCols - 1) / fs::kTileCols), c > 0),
               "syrk_tc");
       }
     }
-    if (!(use_tc == 2 && direct)) FS_CK(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
+    if (!(use_tc == 2 && direct) && !ctx->poison_rc) FS_CKS(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
     ctx->launches += l;
     prof_mark(ctx, FS_PROF_GRAM, st);
     rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
-                    pivot, out_res, st, use_tc == 2 ? ctx->d_flag : nullptr);
+                    pivot, out_res, st, use_tc == 2 ? ctx->d_flag : nullptr, nonfinite);
     if (rc == kRetryTf32)   // fp16 overflow: S is on the device already
-      rc = fs_chol_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
-                         refine_above, pivot, out_res, stream);
+      rc = chol_solve_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
+                           refine_above, pivot, out_res, stream, nonfinite);
   } else {
-    FS_CK(upload(0, m, 0), "S h2d");
-    FS_CK(fs::check_finite(S, dtype == FS_F64, n, m, ldd, ctx->d_flag, ctx->num_sms, st, &l), "check S");
+    FS_CKS(upload(0, m, 0), "S h2d");
+    if (!ctx->poison_rc)
+      FS_CKS(fs::check_finite(S, dtype == FS_F64, n, m, ldd, ctx->d_flag, ctx->num_sms, st, &l), "check S");
     ctx->launches += l;
-    rc = fs_chol_solve(ctx, dtype, precision, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
-                       refine_above, pivot, out_res, stream);
+    if (ctx->poison_rc)
+      rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
+                      pivot, out_res, st, nullptr, nullptr);
+    else
+      rc = chol_solve_impl(ctx, dtype, precision, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
+                           refine_above, pivot, out_res, stream, nonfinite);
   }
   const int early = ctx->early_x_state;
   ctx->early_x_host = nullptr;
   ctx->early_x_state = 0;
   if (early) FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");   // the early copy is done
-  if (rc != FS_OK && rc != FS_NOT_PD) {
+  if ((rc != FS_OK && rc != FS_NOT_PD && rc != FS_EINVAL) || !ctx->d_flag || !ctx->h_flag) {
     cudaStreamSynchronize(st);
     return rc;
   }
@@ -910,6 +1052,7 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   int use_tc = 0;
   if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
+  begin_solve(ctx, false);
   int vdt = dtype;
   if (dtype == FS_F32 && !use_tc) {
     int l = 0;
@@ -975,6 +1118,130 @@ int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n,
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "embed_complex");
   return FS_OK;
+}
+
+int fs_hermitian_gram(fs_ctx* ctx, const double* G2_packed, int64_t n, double lam, double* W, int64_t ldW,
+                      void* stream) {
+  if (!ctx || !G2_packed || !W || n < 1 || ldW < n) return fail(ctx, FS_EINVAL, "bad hermitian_gram arguments");
+  if (!(lam >= 0.0) || !isfinite(lam)) return fail(ctx, FS_EINVAL, "diagonal shift must be finite and >= 0");
+  int l = 0;
+  cudaError_t e = fs::hermitian_gram(G2_packed, n, lam, W, ldW, ctx->num_sms, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "hermitian_gram");
+  return FS_OK;
+}
+
+int fs_apply_rows(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                  int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream) {
+  if (!ctx) return FS_EINVAL;
+  if (dtype != FS_F32 && dtype != FS_F64) return fail(ctx, FS_EINVAL, "dtype must be FS_F32 or FS_F64");
+  if (!T || !X || !Y || r < 1 || n < 1 || m < 1 || ldT < n || ldX < m || ldY < m)
+    return fail(ctx, FS_EINVAL, "bad apply_rows arguments");
+  int l = 0;
+  cudaError_t e = fs::apply_rows(dtype == FS_F64, T, r, n, ldT, X, m, ldX, Y, ldY, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "apply_rows");
+  return FS_OK;
+}
+
+int fs_heevj_packed(fs_ctx* ctx, const double* G2_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
+                    void* stream) {
+  if (!ctx || !G2_packed || !w || !U || n < 1 || ldU != n) return fail(ctx, FS_EINVAL, "bad heevj arguments");
+  if (2 * n > ctx->n_max) return fail(ctx, FS_ENOMEM, "2n exceeds n_max");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_svd(ctx, 2 * n);
+  if (rc) return rc;
+  double* R = (double*)ctx->d_svd;                       // packed rho(G): n (2n + 1) doubles
+  double* scratch = R + n * (2 * n + 1);                 // 2n doubles (extraction candidate)
+  int* kept = (int*)(scratch + 2 * n);
+  int l = 0;
+  cudaError_t e = fs::rho_gram(G2_packed, n, R, ctx->num_sms, st, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "rho_gram");
+  if ((rc = eig_impl(ctx, R, 2 * n, st))) {
+    if (sweeps && ctx->h_info) *sweeps = ctx->h_info[0];
+    return rc;
+  }
+  if (sweeps) *sweeps = ctx->h_info[0];
+  // clusters: eigenvalues of rho(G) within 1e-9 |w|_max of their neighbour
+  const double wmax = std::max(fabs(ctx->h_w[0]), fabs(ctx->h_w[2 * n - 1]));
+  l = 0;
+  e = fs::herm_extract(ctx->d_U, ctx->d_w, n, 1e-9 * std::max(wmax, 1e-300), U, w, kept, scratch, st, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "herm_extract");
+  FS_CK(cudaMemcpyAsync(ctx->h_info, kept, sizeof(int), cudaMemcpyDeviceToHost, st), "kept d2h");
+  FS_CK(cudaStreamSynchronize(st), "sync");
+  if (ctx->h_info[0] != n) return fail(ctx, FS_ENOCONV, "Hermitian eigenvector extraction incomplete");
+  return FS_OK;
+}
+
+int fs_tri_inverse(fs_ctx* ctx, const double* L, int64_t n, int64_t ldL, double* Linv, int64_t ldo, void* stream) {
+  if (!ctx || !L || !Linv || n < 1 || ldL < n || ldo < n) return fail(ctx, FS_EINVAL, "bad tri_inverse arguments");
+  int rc = ensure_svd(ctx, n);
+  if (rc) return rc;
+  int l = 0;
+  cudaError_t e = fs::tri_inverse(L, n, ldL, Linv, ldo, (double*)ctx->d_svd, ctx->num_sms, (cudaStream_t)stream, &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "tri_inverse");
+  return FS_OK;
+}
+
+int fs_jacobi_svd(fs_ctx* ctx, const double* A, int64_t n, int64_t lda, double* sigma, double* U, int64_t ldu,
+                  double* Zt, int64_t ldz, int* sweeps, void* stream) {
+  if (!ctx || !A || !sigma || !U || !Zt || n < 1 || lda < n || ldu < n || ldz < n)
+    return fail(ctx, FS_EINVAL, "bad jacobi_svd arguments");
+  if (n > 16384) return fail(ctx, FS_EUNSUPPORTED, "the Jacobi SVD supports n <= 16384");
+  int rc = ensure_svd(ctx, n);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double tol = std::max(1e-15, (double)n * 1.1102230246251565e-16);
+  int l = 0;
+  cudaError_t e = fs::jacobi_svd(A, n, lda, sigma, U, ldu, Zt, ldz, 60, tol, ctx->d_svd, ctx->num_sms, ctx->d_info, st,
+                                 &l);
+  ctx->launches += l;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "jacobi_svd");
+  FS_CK(cudaMemcpyAsync(ctx->h_info, ctx->d_info, 2 * sizeof(int), cudaMemcpyDeviceToHost, st), "info d2h");
+  FS_CK(cudaStreamSynchronize(st), "sync");
+  if (sweeps) *sweeps = ctx->h_info[0];
+  if (ctx->h_info[1]) return fail(ctx, FS_ENOCONV, "SVD did not converge");
+  return FS_OK;
+}
+
+int fs_factor_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v,
+                    double lam, const double* U, int64_t ldU, const double* w, int64_t r, double* x, int flags,
+                    double* out_res, void* stream) {
+  int rc = check_shape(ctx, dtype, S, n, m, ldS);
+  if (rc) return rc;
+  if ((rc = check_lam(ctx, lam))) return rc;
+  if (!v || !x || (r > 0 && (!U || !w)) || r < 0 || r > n || ldU < r) return fail(ctx, FS_EINVAL, "bad factor_solve arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  begin_solve(ctx, false);
+  int vdt = dtype;
+  if (dtype == FS_F32) {   // exact fp64 GEMV products on this route
+    int l = 0;
+    cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "widen v");
+    v = ctx->d_v64;
+    vdt = FS_F64;
+  }
+  ctx->n_marks = 0;
+  double* u = ctx->d_packed + n * (n + 1) / 2;
+  if ((rc = fs_gemv_rows(ctx, dtype, S, n, m, ldS, v, vdt, u, stream))) return rc;
+  if (!ctx->d_t && cudaMalloc((void**)&ctx->d_t, (size_t)ctx->n_max * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, FS_ENOMEM, "cannot allocate the factor-solve scratch");
+  }
+  {
+    int l = 0;
+    cudaError_t e = fs::eig_apply(U, ldU, n, r, u, w, lam, ctx->d_t, ctx->d_z, st, &l);
+    ctx->launches += l;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "factor apply");
+  }
+  FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "status reset");
+  int64_t piv = -1;
+  return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, nullptr, nullptr, flags & FS_FLAG_RESIDUAL, 0.0, &piv,
+                  out_res, st, nullptr);
 }
 
 int fs_all_finite(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, void* stream) {

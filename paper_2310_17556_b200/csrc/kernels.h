@@ -117,6 +117,30 @@ cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const 
 // ---- complex.cu: kind 0 -> [Re S; Im S] (2n x m), kind 1 -> [[Re, -Im], [Im, Re]] (2n x 2m) ----
 cudaError_t embed_complex(bool f64, const void* S, int64_t n, int64_t m, int64_t ldS, int kind, void* out, int64_t ldo,
                           int num_sms, cudaStream_t st, int* launches);
+// W (n x n interleaved complex) = S S^H + lam I from the packed Gram of [Re S; Im S] (2n rows)
+cudaError_t hermitian_gram(const double* G2, int64_t n, double lam, double* W, int64_t ldW, int num_sms,
+                           cudaStream_t st, int* launches);
+
+// packed lower rho(G) (2n x 2n) of G = S S^H from the packed Gram of [Re S; Im S]
+cudaError_t rho_gram(const double* G2, int64_t n, double* R, int num_sms, cudaStream_t st, int* launches);
+// complex eigenvectors of G (n x n interleaved, column j <-> w[j]) from rho(G)'s eigenpairs (Y, w2)
+cudaError_t herm_extract(const double* Y, const double* w2, int64_t n, double tol, double* U, double* w, int* kept,
+                         double* scratch, cudaStream_t st, int* launches);
+
+// ---- apply.cu: Y (r x m, fp64) = T (r x n, fp64) X (n x m, fp32/fp64 row-major), fp64 tensor cores ----
+cudaError_t apply_rows(bool x_f64, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X, int64_t m,
+                       int64_t ldX, double* Y, int64_t ldY, cudaStream_t st, int* launches);
+
+// ---- svd.cu: the direct-SVD route's n x n pieces ----
+// Linv = L^-1 (lower, row-major ldo; upper zeroed); scratch: n*n doubles
+cudaError_t tri_inverse(const double* L, int64_t n, int64_t ldL, double* Linv, int64_t ldo, double* scratch,
+                        int num_sms, cudaStream_t st, int* launches);
+size_t jacobi_svd_workspace_bytes(int64_t n);
+// one-sided Jacobi SVD of A (n x n): A = U diag(sigma) Zt, sigma descending (>= 0);
+// d_info[0] = sweeps, d_info[1] = 1 if not converged within max_sweeps
+cudaError_t jacobi_svd(const double* A, int64_t n, int64_t lda, double* sigma, double* U, int64_t ldu, double* Zt,
+                       int64_t ldz, int max_sweeps, double tol, void* ws, int num_sms, int* d_info, cudaStream_t st,
+                       int* launches);
 
 // ---- tmap.cu: 2-D tensor map (no swizzle) over a row-major array of `outer` rows ----
 cudaError_t make_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,

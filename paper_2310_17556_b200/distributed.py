@@ -200,16 +200,23 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
                              diagnostics: bool = True, refine: int = 0, group=None) -> ShardedSolution:
     """The column-sharded solve through ONE C-ABI call per rank: the same fused kernels as the
     single-GPU path on the local shard (retile + u, tcgen05 SYRK, x + y pass, residual), with the
-    C ABI's all-reduce callback doing the three exchanges ([G | u], y, the norms) over NCCL.
+    C ABI's all-reduce callback doing the exchanges ([G | u], y, the norms) over NCCL.
 
     S_local: a CUDA tensor (validated and aligned here), a ScoreMatrix already on the device (used
-    as is: validated once at construction), or a host shard (numpy / host-origin ScoreMatrix) —
+    as is: validated once at construction), or a host shard (numpy / deferred host ScoreMatrix) —
     the latter goes through fs_chol_solve_host (pipelined column-chunk upload overlapped with the
-    Gram) and returns x_local on the host."""
-    from .core import ScoreMatrix, _to_device_tensor
+    Gram) and returns x_local on the host.
+
+    Collective-safe: validation failures of this rank's shard (non-finite entries) do not raise
+    here, before the collectives — the rank joins them idle (FS_FLAG_INVALID_SHARD) and every rank
+    raises ValueError together; a factorization breakdown raises FactorizationError on every rank
+    (the factor is identical everywhere).  A zero-column shard (m < world) contributes nothing."""
+    from .core import ScoreMatrix, _coerce_host, _to_device_tensor
     from .solvers import _pinned_out
     dev = torch.device("cuda", torch.cuda.current_device())
     host = None
+    invalid = False
+    S = None
     if isinstance(S_local, ScoreMatrix):
         if S_local.is_uploaded or not S_local.host_origin:
             S = S_local.tensor
@@ -218,9 +225,18 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
             host = S_local.host_array
     elif isinstance(S_local, torch.Tensor) and S_local.is_cuda:
         dev = S_local.device
-        S = _to_device_tensor(S_local, "score matrix", dev)    # aligned rows (no copy when already)
+        if S_local.dim() == 2 and S_local.shape[1] == 0:
+            S = S_local
+        else:
+            S = _to_device_tensor(S_local, "score matrix", dev, validate=False)   # aligned rows (no copy when already)
+            invalid = not _lib.all_finite(S)
     else:
-        host = ScoreMatrix(S_local).host_array                 # numpy shard: validated on the device
+        arr = _coerce_host(S_local, "score matrix")
+        if arr.ndim == 2 and arr.shape[1] == 0:
+            S = torch.empty((arr.shape[0], 0), dtype=torch.float32 if arr.dtype == np.float32 else torch.float64,
+                            device=dev)
+        else:
+            host = ScoreMatrix(arr, defer=True).host_array        # numpy shard: validated on the device
     piv = ctypes.c_int64(-1)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
     flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (refine << 8)) if refine else 0)
@@ -238,14 +254,19 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
                                         cb, None, flags, REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(dev))
         what = "fs_chol_solve_host"
     else:
+        n, m = int(S.shape[0]), int(S.shape[1])
         v = v_local.to(dev).to(S.dtype).contiguous() if isinstance(v_local, torch.Tensor) else \
             torch.as_tensor(np.asarray(v_local), device=dev).to(S.dtype).contiguous()
-        n, m = int(S.shape[0]), int(S.shape[1])
+        if m and v.numel() and not _lib.all_finite(v):
+            invalid = True
+        if invalid:
+            flags |= _lib.FS_FLAG_INVALID_SHARD
         prec = resolve_precision(precision, S.dtype)
-        ctx = _lib.context_for(dev.index, n, m)
+        ctx = _lib.context_for(dev.index, n, max(m, 1))
         x = torch.empty(m, dtype=torch.float64, device=dev)
-        rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
-                                   v.data_ptr(), float(lam), x.data_ptr(), cb, None, flags, REFINE_ABOVE_REL,
+        rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr() if m else None, n, m,
+                                   S.stride(0) if m else 0, v.data_ptr() if m else None, float(lam),
+                                   x.data_ptr() if m else None, cb, None, flags, REFINE_ABOVE_REL,
                                    ctypes.byref(piv), res, _stream(dev))
         what = "fs_chol_solve"
     if rc == _lib.FS_NOT_PD:

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import weakref
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 from time import perf_counter
 
 import numpy as np
@@ -27,10 +27,13 @@ from .core import (
     Variant,
     WorkspaceMeter,
     PRECISIONS,
+    as_scores,
+    as_system,
     _check,
     _dt,
     _stream,
     embed_complex,
+    gram_packed,
     resolve_precision,
     stack_complex_vector,
 )
@@ -125,38 +128,64 @@ def _meter_slots(n: int, m: int, dtype: int, precision: int) -> int:
     return int(lib.fs_workspace_bytes(n, m, dtype, precision)) // 8
 
 
+AUTO_REFINE_STEPS = 12              # fp32 modes: correction steps the "auto" rule may take
+RESULT_PROMISE_REL = 1e-8           # solvers.py:41-42: the factored route promises rel_residual <= 1e-8
+
+
+def _refine_steps(refine, prec: str) -> int:
+    if isinstance(refine, str):
+        if refine != "auto":
+            raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
+        # the reference rule (solvers.py:171-194): refine while rel_residual > 1e-10.  fp64 needs
+        # one step at most (the reference's single correction pass); the fp32-split factors
+        # contract ~u32 sigma_max^2/lam per step, so they may take several
+        return 1 if prec == "fp64" else AUTO_REFINE_STEPS
+    if isinstance(refine, bool):
+        return 1 if refine else 0
+    if isinstance(refine, (int, np.integer)) and 0 <= int(refine) <= 255:
+        return int(refine)
+    raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
+
+
+def _host_x(x: torch.Tensor) -> np.ndarray:
+    """x (device fp64) -> a numpy array in page-locked memory (fast D2H; see _PinnedOut)."""
+    out = _pinned_out.get(int(x.shape[0]))
+    torch.from_numpy(out).copy_(x)
+    return out
+
+
 def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, precision: str = "auto",
                refine: str | bool | int = "auto", diagnostics: bool = True) -> Solution:
     """Solve (S^T S + lam I) x = v through the n-by-n Gram factorization (solvers.py:197-206).
 
-    precision: "fp64" (exact fp64 products, the reference's arithmetic), "f16x2" (default for
-    fp32 scores: row-scaled two-plane fp16 split on the tensor cores), "tf32x3", or "auto".
-    refine: "auto" applies the reference's one-step refinement rule (rel_residual > 1e-10,
-    solvers.py:171-194) in fp64 mode and none in the fp32 modes, whose stated bound is
-    4 u32 sigma_max^2/lam; True forces the reference rule; an int k > 1 runs up to k correction
-    steps with the same factor and fp64 residuals (mixed-precision iterative refinement,
-    SURVEY §8f-1), stopping at rel_residual <= 1e-10 or when a step no longer halves it —
-    it contracts when u32 sigma_max^2/lam << 1; False disables refinement.
+    precision: "fp64" (exact fp64 products, the reference's arithmetic), "f16x2" (row-scaled
+    two-plane fp16 split on the tensor cores), "tf32x3", or "auto" (fp64 scores -> fp64,
+    float32 scores -> f16x2 with the result-quality guarantee below).
+    refine: "auto" applies the reference's rule (refine while rel_residual > 1e-10,
+    solvers.py:171-194): one correction step in fp64 mode, up to AUTO_REFINE_STEPS steps in the
+    fp32-split modes (mixed-precision iterative refinement: fp32-split factor, fp64 residuals,
+    stopping at 1e-10 or when a step no longer halves the residual).  With precision="auto" as
+    well, a float32 solve whose refined rel_residual still exceeds the reference's promise of
+    1e-8 (solvers.py:41-42; it happens when u32 sigma_max^2/lam is not << 1) is recomputed in
+    fp64 mode, so the drop-in default always meets the reference's result contract.
+    True = the reference's single step; an int k = up to k steps; False/0 = none (the raw fp32
+    mode, tolerance 4 u32 sigma_max^2/lam).
     diagnostics: compute abs/rel residual on the GPU (two extra passes over S), as the
     reference does inside solve_chol (solvers.py:160-170).
     """
+    system = as_system(system)
     if system.S.is_complex:
         raise ValueError("solve_chol handles real scores; use solve_chol_hermitian")
     t0 = perf_counter()
     n, m = system.n, system.m
     prec = resolve_precision(precision, system.S.dtype)
-    steps = 0
-    if refine == "auto":
-        steps = 1 if prec == "fp64" else 0
-    elif isinstance(refine, bool):
-        steps = 1 if refine else 0
-    elif isinstance(refine, (int, np.integer)) and 0 <= int(refine) <= 255:
-        steps = int(refine)
-    else:
-        raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
+    steps = _refine_steps(refine, prec)
     do_refine = steps > 0
     if do_refine and not diagnostics:
-        raise ValueError("refinement needs the residual diagnostics")
+        if refine == "auto":
+            steps, do_refine = 0, False
+        else:
+            raise ValueError("refinement needs the residual diagnostics")
     flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (steps << 8)) if do_refine else 0)
     dt = _lib.FS_F32 if system.S.dtype == torch.float32 else _lib.FS_F64
     device = system.S.device
@@ -168,7 +197,8 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
     Sh, vh = system.S.host_array, system.host_v
     if Sh is not None and vh is not None:
-        # host system: one call streams S in row chunks overlapped with the Gram, returns x on the host
+        # deferred host system: one call streams S in column chunks overlapped with the Gram and
+        # returns x on the host
         x = _pinned_out.get(m)
         rc = ctx.lib.fs_chol_solve_host(ctx.handle, dt, PRECISIONS[prec], Sh.ctypes.data, n, m,
                                         Sh.strides[0] // Sh.itemsize, vh.ctypes.data, system.lam, x.ctypes.data,
@@ -190,7 +220,12 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
             f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",
             pivot=int(piv.value))
     _check(ctx, rc, what)
-    xo = x.cpu().numpy() if (system.S.host_origin and isinstance(x, torch.Tensor)) else x
+    if (precision == "auto" and refine == "auto" and prec != "fp64" and diagnostics
+            and not float(res[1]) <= RESULT_PROMISE_REL):
+        # the fp32-split factor could not reach the reference's promise: exact fp64 products
+        sol = solve_chol(system, meter, precision="fp64", refine="auto", diagnostics=True)
+        return replace(sol, wall_seconds=perf_counter() - t0)
+    xo = _host_x(x) if (system.S.host_origin and isinstance(x, torch.Tensor)) else x
     return Solution(x=xo, method=Method.CHOL, abs_residual=float(res[0]), rel_residual=float(res[1]),
                     wall_seconds=perf_counter() - t0, precision=prec)
 
@@ -200,6 +235,7 @@ def solve_chol_hermitian(system: DampedSystem, meter: WorkspaceMeter | None = No
     """(S^H S + lam I) x = v for complex scores (solvers.py:209-213), through the real
     representation rho(S) = [[Re S, -Im S], [Im S, Re S]] (rho(S)^T rho(S) = rho(S^H S)): the plain
     route on 2n rows and 2m columns solves for [Re x; Im x] (fs_embed_complex + fs_chol_solve)."""
+    system = as_system(system)
     if not system.S.is_complex:
         raise ValueError("solve_chol_hermitian expects complex scores; use solve_chol")
     t0 = perf_counter()
@@ -219,6 +255,7 @@ def solve_realpart(system: DampedSystem, meter: WorkspaceMeter | None = None, *,
     """(Re[S^H S] + lam I) x = v for complex scores and a real v (solvers.py:216-240): the plain
     route on C = [Re S; Im S] (sr.py:61-70, built on the device by fs_embed_complex); the
     residual of the real-part operator equals C's plain residual."""
+    system = as_system(system)
     if not system.S.is_complex:
         raise ValueError("real-part variant expects complex scores")
     if system.v_tensor.is_complex():
@@ -231,21 +268,48 @@ def solve_realpart(system: DampedSystem, meter: WorkspaceMeter | None = None, *,
                     wall_seconds=perf_counter() - t0, precision=inner.precision)
 
 
+def _shape_of(a) -> tuple:
+    return tuple(a.shape)
+
+
 @dataclass(frozen=True)
 class ThinSvd:
-    """Thin SVD factors S = U diag(sigma) V^T (solvers.py ThinSvd): U n x r, sigma (r,), V m x r."""
+    """Thin SVD factors S = U diag(sigma) V^H (core.py:226-267): U n x r and V m x r with
+    orthonormal columns, sigma strictly positive and nonincreasing; r = 0 means numerically zero.
+    The factors are numpy arrays for host-origin scores, CUDA tensors for device scores."""
 
     U: object
     sigma: object
     V: object
 
+    def __post_init__(self):                 # core.py:237-253
+        U, sigma, V = self.U, self.sigma, self.V
+        if len(_shape_of(U)) != 2 or len(_shape_of(V)) != 2 or len(_shape_of(sigma)) != 1:
+            raise ValueError("thin SVD factors have wrong ranks")
+        r = _shape_of(sigma)[0]
+        if _shape_of(U)[1] != r or _shape_of(V)[1] != r:
+            raise ValueError(f"inconsistent retained rank: U has {_shape_of(U)[1]} columns, "
+                             f"V has {_shape_of(V)[1]}, sigma has {r}")
+        if r > min(_shape_of(U)[0], _shape_of(V)[0]):
+            raise ValueError("retained rank exceeds min(n, m)")
+        if r > 0:
+            sg = sigma.detach().cpu().numpy() if isinstance(sigma, torch.Tensor) else np.asarray(sigma)
+            if not np.all(sg > 0.0):
+                raise ValueError("singular values must be strictly positive")
+            if np.any(np.diff(sg) > 0.0):
+                raise ValueError("singular values must be nonincreasing")
+
     @property
     def r(self) -> int:
-        return int(self.sigma.shape[0])
+        return int(_shape_of(self.sigma)[0])
+
+    @property
+    def n(self) -> int:
+        return int(_shape_of(self.U)[0])
 
     @property
     def m(self) -> int:
-        return int(self.V.shape[0])
+        return int(_shape_of(self.V)[0])
 
 
 def _check_floor(sigma_floor) -> float:
@@ -257,7 +321,7 @@ def _check_floor(sigma_floor) -> float:
 
 def eigh_gram(S: ScoreMatrix, precision: str = "auto") -> tuple[torch.Tensor, torch.Tensor, int]:
     """Eigenpairs of the Gram S S^T on the GPU (solvers.py:257-266): w descending (fp64, device),
-    U (n x n fp64, device, column j <-> w[j]), and the Jacobi sweep count."""
+    U (n x n fp64, device, column j <-> w[j]), and the Jacobi sweep count (real scores)."""
     t = S.tensor
     n = S.n
     Gp = _gram_packed_unshifted(S, precision)
@@ -276,26 +340,46 @@ def eigh_gram(S: ScoreMatrix, precision: str = "auto") -> tuple[torch.Tensor, to
 def _gram_packed_unshifted(S: ScoreMatrix, precision: str) -> torch.Tensor:
     t = S.tensor
     n, m = S.n, S.m
+    dt = _dt(t)
     prec = resolve_precision(precision, t.dtype)
     ctx = _lib.context_for(t.device.index, n, m)
     out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
-    rc = ctx.lib.fs_gram_packed(ctx.handle, _dt(t), PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0), 0.0,
+    rc = ctx.lib.fs_gram_packed(ctx.handle, dt, PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0), 0.0,
                                 out.data_ptr(), _stream(t.device))
     _check(ctx, rc, "fs_gram_packed")
     return out
+
+
+def _apply_rows(T: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
+    """Y = T X on the device (fs_apply_rows, fp64 tensor cores): T r x n fp64, X n x m (a real
+    score-layout matrix, fp32 or fp64, unit column stride) -> Y r x m fp64, 16-byte aligned rows."""
+    r, n = int(T.shape[0]), int(T.shape[1])
+    m = int(X.shape[1])
+    T = T.to(torch.float64).contiguous()
+    ldy = -(-m // 2) * 2
+    Y = torch.empty((r, ldy), dtype=torch.float64, device=X.device)[:, :m]
+    ctx = _lib.context_for(X.device.index, n, m)
+    rc = ctx.lib.fs_apply_rows(ctx.handle, _dt(X), T.data_ptr(), r, n, T.stride(0), X.data_ptr(), m, X.stride(0),
+                               Y.data_ptr(), Y.stride(0), _stream(X.device))
+    _check(ctx, rc, "fs_apply_rows")
+    return Y
 
 
 def thin_svd_eigh(S: ScoreMatrix, sigma_floor: float = DEFAULT_SIGMA_FLOOR, *, precision: str = "auto") -> ThinSvd:
     """Thin SVD via the eigendecomposition of the n-by-n Gram matrix (solvers.py:243-277) on the GPU.
 
     Eigenvalues made negative by round-off are clamped to zero; singular values at or below
-    sigma_floor * sigma_max are truncated; V = S^T (U / sigma).  The Gram and the Jacobi
-    eigensolver are this package's kernels; the explicit m x r factor V is one plain dense
-    product (torch.matmul) — the solve route (solve_svd_eigh) never forms it.
+    sigma_floor * sigma_max are truncated; V = S^T (U / sigma), formed as V^T = (U / sigma)^T S by
+    this package's fp64 tensor-core GEMM (fs_apply_rows).  Complex scores: the eigenpairs of
+    S S^H come from the Hermitian Jacobi eigensolver (fs_heevj_packed) on the Gram of
+    [Re S; Im S], and V^H = (U / sigma)^H S through the real representation.
     """
     sigma_floor = _check_floor(sigma_floor)
+    S = as_scores(S)
     if S.n > S.m:
         raise ValueError(f"thin_svd_eigh requires n <= m, got shape {S.shape}")
+    if S.is_complex:
+        return _thin_svd_eigh_complex(S, sigma_floor, precision)
     w, U, _ = eigh_gram(S, precision)
     sigma = torch.sqrt(torch.clamp(w, min=0.0))
     keep = sigma > sigma_floor * sigma[0]
@@ -304,9 +388,46 @@ def thin_svd_eigh(S: ScoreMatrix, sigma_floor: float = DEFAULT_SIGMA_FLOOR, *, p
     if sigma.numel() == 0:
         V = torch.zeros((S.m, 0), dtype=torch.float64, device=U.device)
     else:
-        V = S.tensor.to(torch.float64).T @ (U / sigma)
+        V = _apply_rows((U / sigma).T, S.tensor).T      # V^T = (U / sigma)^T S  (r x m)
     if S.host_origin:
-        return ThinSvd(U=U.cpu().numpy(), sigma=sigma.cpu().numpy(), V=V.cpu().numpy())
+        return ThinSvd(U=U.cpu().numpy(), sigma=sigma.cpu().numpy(), V=np.ascontiguousarray(V.cpu().numpy()))
+    return ThinSvd(U=U, sigma=sigma, V=V)
+
+
+def _thin_svd_eigh_complex(S: ScoreMatrix, sigma_floor: float, precision: str) -> ThinSvd:
+    """Complex scores (solvers.py:258-276 with S S^H and V = S^H U / sigma): the Gram of
+    C = [Re S; Im S] (one real SYRK on 2n rows), the Hermitian eigenpairs from fs_heevj_packed,
+    and V^H = (U / sigma)^H S as two real fs_apply_rows products on C:
+    Re V^H = [Re B^T, Im B^T] C and Im V^H = [-Im B^T, Re B^T] C with B = U / sigma."""
+    n, m = S.n, S.m
+    C = embed_complex(S, 0)
+    G2 = gram_packed(C, 0.0, precision)
+    dev = G2.device
+    ctx = _lib.context_for(dev.index, 2 * n, m)
+    w = torch.empty(n, dtype=torch.float64, device=dev)
+    Ui = torch.empty((n, n, 2), dtype=torch.float64, device=dev)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_heevj_packed(ctx.handle, G2.data_ptr(), n, w.data_ptr(), Ui.data_ptr(), n, ctypes.byref(sweeps),
+                                 _stream(dev))
+    if rc == _lib.FS_ENOCONV:
+        raise FactorizationError(f"eigendecomposition did not converge: {ctx.last_error()}")
+    _check(ctx, rc, "fs_heevj_packed")
+    U = torch.view_as_complex(Ui)
+    sigma = torch.sqrt(torch.clamp(w, min=0.0))
+    keep = sigma > sigma_floor * sigma[0]
+    U = U[:, keep].contiguous()
+    sigma = sigma[keep].contiguous()
+    r = int(sigma.shape[0])
+    if r == 0:
+        V = torch.zeros((m, 0), dtype=torch.complex128, device=dev)
+    else:
+        B = U / sigma
+        Bt_re, Bt_im = B.real.T, B.imag.T
+        T = torch.cat([torch.cat([Bt_re, Bt_im], dim=1), torch.cat([-Bt_im, Bt_re], dim=1)], dim=0)   # 2r x 2n
+        Y = _apply_rows(T, C.tensor)                         # [Re V^H; Im V^H]  (2r x m)
+        V = torch.complex(Y[:r], -Y[r:]).T                   # V = (V^H)^H
+    if S.host_origin:
+        return ThinSvd(U=U.cpu().numpy(), sigma=sigma.cpu().numpy(), V=np.ascontiguousarray(V.cpu().numpy()))
     return ThinSvd(U=U, sigma=sigma, V=V)
 
 
@@ -318,14 +439,30 @@ def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOO
     On the GPU (fs_eigh_solve): Gram + u = S v (same kernels and precision modes as solve_chol),
     Jacobi eigendecomposition, and the solve through S^T without forming V:
     x = (v - S^T z) / lam with z = U_r diag(1 / (w_r + lam)) U_r^T u over the kept eigenpairs.
+    Complex scores (S^H S + lam I, the HERMITIAN residual as solvers.py:319-320 picks): the same
+    route on the real representation rho(S) = [[Re S, -Im S], [Im S, Re S]] for [Re x; Im x]
+    (rho(S) rho(S)^T = rho(S S^H) has every eigenvalue of S S^H twice, so the floor keeps or drops
+    both copies and the solve is the complex one).
     """
-    sigma_floor = _check_floor(sigma_floor)
+    return _eigh_route(as_system(system), _check_floor(sigma_floor), precision, diagnostics, Method.SVD_EIGH)
+
+
+def _eigh_route(system: DampedSystem, sigma_floor: float, precision: str, diagnostics: bool,
+                method: Method) -> Solution:
     t0 = perf_counter()
+    if system.n > system.m:
+        raise ValueError(f"thin_svd_eigh requires n <= m, got shape {(system.n, system.m)}")
+    if system.S.is_complex:
+        m = system.m
+        emb = embed_complex(system.S, 1)
+        vhat = stack_complex_vector(system.v_tensor, system.S.real_dtype)
+        inner = _eigh_route(DampedSystem(emb, system.lam, vhat), sigma_floor, precision, diagnostics, method)
+        x = torch.complex(inner.x[:m], inner.x[m:])
+        xo = x.cpu().numpy() if system.S.host_origin else x
+        return replace(inner, x=xo, wall_seconds=perf_counter() - t0)
     S = system.S.tensor
     v = system.v_tensor
     n, m = system.n, system.m
-    if n > m:
-        raise ValueError(f"thin_svd_eigh requires n <= m, got shape {(n, m)}")
     prec = resolve_precision(precision, S.dtype)
     ctx = _lib.context_for(S.device.index, n, m)
     x = torch.empty(m, dtype=torch.float64, device=S.device)
@@ -338,20 +475,286 @@ def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOO
     if rc == _lib.FS_ENOCONV:
         raise FactorizationError(f"eigendecomposition did not converge: {ctx.last_error()}")
     _check(ctx, rc, "fs_eigh_solve")
-    xo = x.cpu().numpy() if system.S.host_origin else x
-    return Solution(x=xo, method=Method.SVD_EIGH, abs_residual=float(res[0]), rel_residual=float(res[1]),
+    xo = _host_x(x) if system.S.host_origin else x
+    return Solution(x=xo, method=method, abs_residual=float(res[0]), rel_residual=float(res[1]),
                     wall_seconds=perf_counter() - t0, precision=prec)
 
 
-def solve_svd_direct(system: DampedSystem, *, precision: str = "auto", diagnostics: bool = True) -> Solution:
-    """solve_svd_direct (solvers.py:357-364, the "svda" comparison route): thin SVD of S, exact-zero
-    singular values dropped (solvers.py:280-291), then the factor solve with the residual against S.
+def solve_svd_from_factors(svd: ThinSvd, lam: float, v, *, source: ScoreMatrix | None = None,
+                           method: Method = Method.SVD_EIGH) -> Solution:
+    """x = V (sigma^2 + lam)^-1 V^H v + (v - V V^H v) / lam from thin SVD factors (solvers.py:294-344),
+    on the GPU: with V^H in the score layout (r x m), t = V^H v is fs_gemv_rows and
+    x = (v - V z) / lam with z = t sigma^2 / (sigma^2 + lam) is fs_gemv_cols_solve (the chol
+    route's x pass; the same algebra as the reference, never forming V V^H).  Rank 0 gives
+    x = v / lam exactly.  Residuals: against ``source`` when given (HERMITIAN for complex
+    scores), else against the operator V diag(sigma^2) V^H + lam I the factors span.  Complex
+    factors run on the real representation of V^H (fs_embed_complex)."""
+    from .core import _coerce_damping, _to_device_tensor, default_device
+    t0 = perf_counter()
+    lam = _coerce_damping(lam)
+    if source is not None:
+        source = as_scores(source)
+    dev = svd.V.device if isinstance(svd.V, torch.Tensor) else (
+        source.device if source is not None else default_device())
+    vt = _to_device_tensor(v, "right-hand side", dev, force_copy=isinstance(v, torch.Tensor) and v.is_cuda)
+    if vt.dim() != 1 or vt.shape[0] != svd.m:
+        raise ValueError(f"right-hand side has shape {tuple(vt.shape)}, expected ({svd.m},)")
+    host_out = not isinstance(svd.V, torch.Tensor)
+    V = torch.as_tensor(svd.V, device=dev)
+    sigma = torch.as_tensor(svd.sigma, device=dev, dtype=torch.float64)
+    m, r = svd.m, svd.r
+    cplx = V.is_complex() or vt.is_complex()
+    if cplx:
+        vhat = stack_complex_vector(vt.to(torch.complex128), torch.float64)
+    else:
+        vhat = vt.to(torch.float64).contiguous()
+    if r == 0:
+        xhat = vhat / lam
+    else:
+        if cplx:
+            Vh = ScoreMatrix(V.to(torch.complex128).conj().T.contiguous())
+            E = embed_complex(Vh, 1).tensor                 # rho(V^H): 2r x 2m
+            d = torch.cat([sigma, sigma])
+        else:
+            E = _to_device_tensor(V.to(torch.float64).T, "right factor", dev)   # V^T: r x m, aligned
+            d = sigma
+        rows, cols = int(E.shape[0]), int(E.shape[1])
+        ctx = _lib.context_for(dev.index, rows, cols)
+        st = _stream(dev)
+        t = torch.empty(rows, dtype=torch.float64, device=dev)
+        rc = ctx.lib.fs_gemv_rows(ctx.handle, _dt(E), E.data_ptr(), rows, cols, E.stride(0), vhat.data_ptr(),
+                                  _lib.FS_F64, t.data_ptr(), st)
+        _check(ctx, rc, "fs_gemv_rows")
+        z = t * (d * d) / (d * d + lam)
+        xhat = torch.empty(cols, dtype=torch.float64, device=dev)
+        rc = ctx.lib.fs_gemv_cols_solve(ctx.handle, _dt(E), E.data_ptr(), rows, cols, E.stride(0), z.data_ptr(),
+                                        vhat.data_ptr(), _lib.FS_F64, lam, 0, xhat.data_ptr(), st)
+        _check(ctx, rc, "fs_gemv_cols_solve")
+    x = torch.complex(xhat[:m], xhat[m:]) if cplx else xhat
+    if source is not None:
+        from .core import residual as _residual
+        system = DampedSystem(source, lam, vt)
+        abs_res, rel_res = _residual(system, x, Variant.HERMITIAN if source.is_complex else Variant.PLAIN)
+    elif r == 0:
+        abs_res = float(torch.linalg.vector_norm(lam * xhat - vhat))
+        rel_res = abs_res / max(float(torch.linalg.vector_norm(vhat)), EPS)
+    else:
+        y = torch.empty(rows, dtype=torch.float64, device=dev)
+        rc = ctx.lib.fs_gemv_rows(ctx.handle, _dt(E), E.data_ptr(), rows, cols, E.stride(0), xhat.data_ptr(),
+                                  _lib.FS_F64, y.data_ptr(), st)
+        _check(ctx, rc, "fs_gemv_rows")
+        y *= d * d
+        sums = torch.empty(2, dtype=torch.float64, device=dev)
+        rc = ctx.lib.fs_residual_cols(ctx.handle, _dt(E), E.data_ptr(), rows, cols, E.stride(0), y.data_ptr(),
+                                      xhat.data_ptr(), vhat.data_ptr(), _lib.FS_F64, lam, None, sums.data_ptr(), st)
+        _check(ctx, rc, "fs_residual_cols")
+        rr, vv = sums.cpu().tolist()
+        abs_res = float(np.sqrt(rr))
+        rel_res = abs_res / max(float(np.sqrt(vv)), EPS)
+    xo = x.cpu().numpy() if host_out or (source is not None and source.host_origin) else x
+    return Solution(x=xo, method=method, abs_residual=abs_res, rel_residual=rel_res,
+                    wall_seconds=perf_counter() - t0, precision="fp64")
 
-    The reference calls dgesdd; the paper's GPU svda called cuSOLVER gesvda, a Gram-based
-    approximate tall-skinny SVD.  This route follows the paper's algorithm class: the thin SVD
-    comes from the Jacobi eigendecomposition of S S^T (fs_eigh_solve) with NO floor — only
-    singular values that are exactly zero (eigenvalues <= 0) are dropped, as in the reference.
-    """
-    sol = solve_svd_eigh(system, 0.0, precision=precision, diagnostics=diagnostics)
-    return Solution(x=sol.x, method=Method.SVD_DIRECT, abs_residual=sol.abs_residual,
-                    rel_residual=sol.rel_residual, wall_seconds=sol.wall_seconds, precision=sol.precision)
+
+def thin_svd_direct(S: ScoreMatrix) -> ThinSvd:
+    """Thin SVD of S itself (solvers.py:280-291; the reference calls dgesdd): exact-zero singular
+    values dropped.  GPU route: shifted CholeskyQR3 of S^H (fp64 tensor-core
+    Gram, potrf, triangular inverse and fs_apply_rows), then a one-sided Jacobi SVD of the n x n
+    triangular factor (fs_svd_direct).  Tall S (n > m) is handled through S^T."""
+    return _svda(as_scores(S), want_factors=True)
+
+
+def solve_svd_direct(system: DampedSystem, *, precision: str = "auto", diagnostics: bool = True) -> Solution:
+    """solve_svd_direct (solvers.py:357-364, the "svda" comparison route): thin SVD of S (see
+    thin_svd_direct), then the factor solve with the residual against S.  The solve never forms
+    V: with S = U diag(sigma) V^T, x = (v - S^T z)/lam and z = U diag(1/(sigma^2 + lam)) U^T S v
+    (the eigh route's algebra with w = sigma^2 from the SVD, not from the Gram)."""
+    t0 = perf_counter()
+    system = as_system(system)
+    if system.S.is_complex:
+        raise ValueError("solve_svd_direct: complex scores are not supported on the GPU svd route")
+    sol = _svda(system.S, want_factors=False, system=system, diagnostics=diagnostics)
+    return replace(sol, wall_seconds=perf_counter() - t0)
+
+
+U64 = 2.0 ** -53
+
+
+def _potrf_device(Gp: torch.Tensor, n: int, shift: float) -> torch.Tensor | None:
+    """L = chol(unpack(Gp) + shift I) on the device, or None on breakdown."""
+    dev = Gp.device
+    ctx = _lib.context_for(dev.index, n, 1)
+    W = torch.empty((n, n), dtype=torch.float64, device=dev)
+    st = _stream(dev)
+    rc = ctx.lib.fs_unpack_lower(ctx.handle, Gp.data_ptr(), n, float(shift), W.data_ptr(), n, st)
+    _check(ctx, rc, "fs_unpack_lower")
+    piv = ctypes.c_int64(-1)
+    rc = ctx.lib.fs_potrf(ctx.handle, W.data_ptr(), n, n, ctypes.byref(piv), st)
+    if rc == _lib.FS_NOT_PD:
+        return None
+    _check(ctx, rc, "fs_potrf")
+    return W
+
+
+def _tri_inverse(L: torch.Tensor) -> torch.Tensor:
+    n = int(L.shape[0])
+    ctx = _lib.context_for(L.device.index, n, 1)
+    out = torch.empty((n, n), dtype=torch.float64, device=L.device)
+    rc = ctx.lib.fs_tri_inverse(ctx.handle, L.data_ptr(), n, L.stride(0), out.data_ptr(), n, _stream(L.device))
+    _check(ctx, rc, "fs_tri_inverse")
+    return out
+
+
+def _jacobi_svd(A: torch.Tensor):
+    n = int(A.shape[0])
+    dev = A.device
+    ctx = _lib.context_for(dev.index, n, 1)
+    sigma = torch.empty(n, dtype=torch.float64, device=dev)
+    U = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Zt = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_jacobi_svd(ctx.handle, A.data_ptr(), n, A.stride(0), sigma.data_ptr(), U.data_ptr(), n,
+                               Zt.data_ptr(), n, ctypes.byref(sweeps), _stream(dev))
+    if rc == _lib.FS_ENOCONV:
+        raise FactorizationError(f"SVD did not converge: {ctx.last_error()}")
+    _check(ctx, rc, "fs_jacobi_svd")
+    return sigma, U, Zt
+
+
+def _svda(S: ScoreMatrix, want_factors: bool, system: DampedSystem | None = None, diagnostics: bool = True):
+    """The direct-SVD route on the GPU (see thin_svd_direct).  Shifted CholeskyQR3 (Fukaya,
+    Kannan, Nakatsukasa, Zhang, Yamamoto 2020) of the tall X = S^T: the first Gram is shifted by
+    s = 11 (m n + n (n + 1)) u ||S||_F^2 so its Cholesky factor exists for cond(S) up to ~1/u, and
+    two plain CholeskyQR steps restore Q's orthogonality to O(u); every Gram is the exact-product
+    fp64 SYRK, every Q^T <- L^-1 Q^T and factor product is fs_apply_rows.  Then S = L Q^T and
+    the one-sided Jacobi SVD of L (not of a Gram: no squared condition number) gives the
+    singular triplets.  A later step whose Gram is singular (exact rank deficiency: a zero or
+    repeated row) is shifted as well, and the directions that stay at the shift's noise level
+    (sigma <= sqrt(n m) u sigma_max) are dropped as numerically zero — the reference's dgesdd
+    keeps tiny nonzero values there, which differ from run to run of any algorithm."""
+    if S.is_complex:
+        raise ValueError("thin_svd_direct: complex scores are not supported on the GPU svd route")
+    from .core import _to_device_tensor
+    n, m = S.n, S.m
+    if n > m:
+        # tall S: the thin SVD of S^T (wide), factors swapped (S = U s V^T <=> S^T = V s U^T)
+        X = _to_device_tensor(S.tensor.T, "score matrix", S.tensor.device, force_copy=True)
+        ST = ScoreMatrix._owned(X, host_origin=S.host_origin)
+        if want_factors:
+            f = _svda(ST, True)
+            return ThinSvd(U=f.V, sigma=f.sigma, V=f.U)
+        sigma, U, Zt, Qt, r = _svda_core(ST)
+        # S = (Q Z) diag(sigma) W^T: S's left factors are Q Z (n x r), formed as (Z^T Q^T)^T
+        Uleft = _apply_rows(Zt[:r], Qt).T.contiguous() if r else torch.zeros((n, 0), dtype=torch.float64,
+                                                                               device=X.device)
+        return _factor_solve(system, Uleft, sigma[:r], diagnostics)
+    sigma, U, Zt, Qt, r = _svda_core(S)
+    if not want_factors:
+        return _factor_solve(system, U[:, :r].contiguous(), sigma[:r], diagnostics)
+    dev = S.tensor.device
+    if r == 0:
+        Uo = torch.zeros((n, 0), dtype=torch.float64, device=dev)
+        so = torch.zeros(0, dtype=torch.float64, device=dev)
+        V = torch.zeros((m, 0), dtype=torch.float64, device=dev)
+    else:
+        Uo = U[:, :r].contiguous()
+        so = sigma[:r].contiguous()
+        V = _apply_rows(Zt[:r], Qt).T                    # V^T = Z^T Q^T
+    if S.host_origin:
+        return ThinSvd(U=Uo.cpu().numpy(), sigma=so.cpu().numpy(), V=np.ascontiguousarray(V.cpu().numpy()))
+    return ThinSvd(U=Uo, sigma=so, V=V)
+
+
+def _svda_core(S: ScoreMatrix):
+    """-> (sigma descending, W (n x n), Z^T (n x n), Q^T (n x m fp64), kept rank r) with S = L Q^T,
+    L = W diag(sigma) Z^T."""
+    X = S.tensor
+    n, m = S.n, S.m
+    dev = X.device
+    Gp = gram_packed(S, 0.0, "fp64")
+    diag = torch.arange(n, device=dev, dtype=torch.int64)
+    fro2 = float(Gp[diag * (diag + 1) // 2 + diag].sum())
+    if fro2 == 0.0:          # exactly zero scores: every singular value is an exact zero (dropped)
+        z = torch.zeros(0, dtype=torch.float64, device=dev)
+        return z, torch.zeros((n, n), dtype=torch.float64, device=dev), torch.zeros((n, n), dtype=torch.float64,
+                                                                                   device=dev), None, 0
+    shift = 11.0 * (m * n + n * (n + 1)) * U64 * fro2
+    L = _potrf_device(Gp, n, shift)
+    if L is None:
+        raise FactorizationError("SVD did not converge: the shifted CholeskyQR Gram is not positive definite")
+    Lacc = L
+    Qt = _apply_rows(_tri_inverse(L), X)
+    deficient = False
+    for _ in range(2):
+        Gq = gram_packed(ScoreMatrix._owned(Qt), 0.0, "fp64")
+        Lk = _potrf_device(Gq, n, 0.0)
+        if Lk is None:       # exact rank deficiency: shift this step too
+            deficient = True
+            q2 = float(Gq[diag * (diag + 1) // 2 + diag].sum())
+            Lk = _potrf_device(Gq, n, 11.0 * (m * n + n * (n + 1)) * U64 * max(q2, 1.0))
+            if Lk is None:
+                raise FactorizationError("SVD did not converge: CholeskyQR breakdown")
+        Lacc = _apply_rows(Lacc, Lk)
+        Qt = _apply_rows(_tri_inverse(Lk), Qt)
+    sigma, W, Zt = _jacobi_svd(Lacc)
+    sg = sigma.cpu().numpy()
+    cut = np.sqrt(float(n) * m) * U64 * sg[0] if deficient else 0.0
+    r = int(np.count_nonzero(sg > cut))
+    return sigma, W, Zt, Qt, r
+
+
+def _factor_solve(system: DampedSystem, U: torch.Tensor, sigma: torch.Tensor, diagnostics: bool) -> Solution:
+    """x = (v - S^T z)/lam, z = U diag(1/(sigma^2 + lam)) U^T S v (fs_factor_solve), residual against S."""
+    t0 = perf_counter()
+    S = system.S.tensor
+    v = system.v_tensor
+    n, m = system.n, system.m
+    r = int(sigma.shape[0])
+    ctx = _lib.context_for(S.device.index, n, m)
+    x = torch.empty(m, dtype=torch.float64, device=S.device)
+    w = (sigma * sigma).contiguous()
+    Uc = U.contiguous() if r else torch.zeros((n, 1), dtype=torch.float64, device=S.device)
+    res = (ctypes.c_double * 2)(float("nan"), float("nan"))
+    flags = _lib.FS_FLAG_RESIDUAL if diagnostics else 0
+    rc = ctx.lib.fs_factor_solve(ctx.handle, _dt(S), S.data_ptr(), n, m, S.stride(0), v.data_ptr(), system.lam,
+                                 Uc.data_ptr(), max(r, 1), w.data_ptr() if r else None, r, x.data_ptr(), flags, res,
+                                 _stream(S.device))
+    _check(ctx, rc, "fs_factor_solve")
+    xo = _host_x(x) if system.S.host_origin else x
+    return Solution(x=xo, method=Method.SVD_DIRECT, abs_residual=float(res[0]), rel_residual=float(res[1]),
+                    wall_seconds=perf_counter() - t0, precision="fp64")
+
+
+def resolve_solver(system: DampedSystem, method, variant=Variant.PLAIN, f=None, tol=1e-10, max_iter=None,
+                   naive_cap=DEFAULT_NAIVE_CAP):
+    """Map (method, variant, scalar kind) to a zero-argument solve callable (bench.py:183-219).
+
+    Raises ValueError on method/kind mismatches, as the reference does.  The GPU path provides
+    chol (plain / hermitian / realpart), eigh and svd; the reference's CPU-only baselines
+    (naive, cg, rvb) are out of this package's scope and raise ValueError naming them."""
+    system = as_system(system)
+    method = Method(getattr(method, "value", method))
+    variant = Variant(getattr(variant, "value", variant))
+    is_complex = system.S.is_complex
+    if method is Method.CHOL:
+        if variant is Variant.PLAIN:
+            if is_complex:
+                raise ValueError("plain chol needs real scores; pick hermitian or realpart")
+            return lambda: solve_chol(system)
+        if variant is Variant.HERMITIAN:
+            if not is_complex:
+                raise ValueError("hermitian variant needs complex scores")
+            return lambda: solve_chol_hermitian(system)
+        if not is_complex:
+            raise ValueError("real-part variant needs complex scores")
+        return lambda: solve_realpart(system)
+    if method in (Method.NAIVE, Method.CG, Method.RVB):
+        raise ValueError(f"method {method.value} is a CPU baseline of the reference; the B200 path provides "
+                         "chol, eigh and svd")
+    if variant is not Variant.PLAIN:
+        raise ValueError(f"method {method.value} supports the plain variant only")
+    if method is Method.SVD_EIGH:
+        return lambda: solve_svd_eigh(system)
+    if method is Method.SVD_DIRECT:
+        return lambda: solve_svd_direct(system)
+    raise ValueError(f"unknown method: {method!r}")

@@ -412,7 +412,9 @@ def test_abi_allreduce_callback_single_rank(fsb):
                            lam, x.data_ptr(), cb, None, _lib.FS_FLAG_RESIDUAL, 1e-10, ctypes.byref(piv), res,
                            torch.cuda.current_stream().cuda_stream)
     assert rc == 0
-    assert calls == [64 * 65 // 2 + 64, 64, 2]
+    # [G | u], y, then the norms with the overflow flag and the multi-rank status slot (api.cu: a
+    # rank that failed locally joins every collective idle; the status reaches all ranks here)
+    assert calls == [64 * 65 // 2 + 64, 64, 4]
     ref = O.solve_chol(S, v, lam)
     assert O.rel_err(x.cpu().numpy(), ref.x) <= 1e-10
     ctx.close()
@@ -510,10 +512,10 @@ def test_host_entry_matches_device_entry(fsb, n, m):
     dev = torch.device("cuda", 0)
     for dt, prec in ((np.float64, "fp64"), (np.float32, "tf32x3"), (np.float32, "f16x2"), (np.float32, "fp64")):
         Sh, vh = S.astype(dt), v.astype(dt)
-        host = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh), lam, vh), precision=prec)
+        host = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(Sh, defer=True), lam, vh), precision=prec, refine=0)
         assert isinstance(host.x, np.ndarray)
         d = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(Sh).to(dev)), lam,
-                                            torch.from_numpy(vh).to(dev)), precision=prec)
+                                            torch.from_numpy(vh).to(dev)), precision=prec, refine=0)
         xd = d.x.cpu().numpy()
         if prec == "fp64":
             assert np.array_equal(host.x, xd), (dt, O.rel_err(host.x, xd))
@@ -531,12 +533,16 @@ def test_host_entry_rejects_non_finite_scores(fsb, where, dt):
     S = S.astype(dt)
     i, j = {"first": (0, 0), "last_row": (299, 1000), "last_col": (150, 2002), "inf": (257, 5)}[where]
     S[i, j] = np.inf if where == "inf" else np.nan
-    system = fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v.astype(dt))
+    # construction validates on the device (core.py:132-142) ...
+    with pytest.raises(ValueError, match="finite"):
+        fsb.ScoreMatrix(S)
+    # ... and the deferred (streamed) host entry validates inside the solve
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), lam, v.astype(dt))
     with pytest.raises(ValueError, match="finite"):
         fsb.solve_chol(system)
     # the context stays usable
     S[i, j] = 0.0
-    sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v.astype(dt)))
+    sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), lam, v.astype(dt)))
     assert np.isfinite(sol.x).all()
 
 
@@ -605,7 +611,7 @@ def test_f16x2_overflow_falls_back_to_tf32x3(fsb, entry):
         assert torch.equal(a.x, b.x)
         x = a.x.cpu().numpy()
     else:
-        a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v), precision="f16x2")
+        a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), lam, v), precision="f16x2")
         x = a.x
     ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
     assert O.rel_err(x, ref.x) <= 1e-6
@@ -845,7 +851,7 @@ def test_fused_sharded_entry_with_nccl_callback(fsb):
         St = torch.from_numpy(S.astype(np.float32)).to(dev)
         vt = torch.from_numpy(v.astype(np.float32)).to(dev)
         a = sharded_solve_chol_fused(St, vt, lam, precision="f16x2")
-        b = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(St), lam, vt), precision="f16x2")
+        b = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(St), lam, vt), precision="f16x2", refine=0)
         assert torch.equal(a.x_local, b.x)
         assert a.rel_residual == b.rel_residual
         # a pre-validated device ScoreMatrix (bench's per-step call) and a host (numpy) shard
@@ -854,7 +860,8 @@ def test_fused_sharded_entry_with_nccl_callback(fsb):
         assert torch.equal(c.x_local, b.x)
         S32, v32 = S.astype(np.float32), v.astype(np.float32)
         h = sharded_solve_chol_fused(S32, v32, lam, precision="f16x2")
-        hb = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32), precision="f16x2")
+        hb = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32, defer=True), lam, v32), precision="f16x2",
+                            refine=0)
         assert isinstance(h.x_local, np.ndarray)
         np.testing.assert_array_equal(h.x_local, hb.x)
         assert O.rel_err(h.x_local, b.x.cpu().numpy()) <= 1e-6

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_r2.py tests/test_multirank_gpu.py -q -m gpu > gpurun_out/r2_t2.log 2>&1
+timeout 1800 python -m pytest tests/test_gpu_parity.py -q -m gpu -x > gpurun_out/r2_t3.log 2>&1
