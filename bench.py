@@ -6,11 +6,12 @@
 Workload (BASELINE configs[1], the paper headline): n=1024 samples, m=1e6 parameters,
 fp32 scores, lam=1e-3.  N=1: the reference generator's system (PCG64 seed 0, bench.py:155-160)
 rounded to fp32 — the CPU reference solves its exact fp64 upcast, so the line carries
-relerr(x) against the reference (`parity`).  One step = one full solve_chol in the fp32
-headline mode (f16x2 Gram, no refinement; Gram -> potrf -> TRSV pair -> fused x epilogue ->
-fp64 residual diagnostics), i.e. the reference's timed unit (solvers.py:151-206 via
-bench.py:254-267).  `parity` also times the drop-in default (precision/refine "auto": the
-reference's refinement rule, result within its 1e-8 promise) and the exact fp64 mode.
+relerr(x) against the reference (`parity`).  One step = one full solve_chol as the drop-in
+default runs it on fp32 scores: the f16x2 tensor-core Gram -> potrf -> TRSV pair -> fused
+x + y pass -> z-space refinement steps (each one TRSV pair + one fused pass) -> fp64 residual
+diagnostics, i.e. the reference's timed unit (solvers.py:151-206 via bench.py:254-267) at the
+reference's result quality (rel_residual <= 1e-10, its refinement rule).  `parity` also times
+the raw fp32-split modes (no refinement) and the exact fp64 mode on the same system.
 
 N=1: the one-shot C-ABI solve on device-resident inputs (`value`) and the public Python API
 with host (pinned) buffers, H2D + D2H inside the timed region (`e2e`; `e2e_streamed_ms` is the
@@ -52,6 +53,10 @@ def parse():
     ap.add_argument("--m", type=int, default=1_000_000)
     ap.add_argument("--lam", type=float, default=1e-3)
     ap.add_argument("--precision", default="f16x2", choices=["f16x2", "tf32x3", "fp64"])
+    ap.add_argument("--refine", default="auto",
+                    help="'auto' (the drop-in default: the reference's result rule), or a step count (0 = raw mode)")
+    ap.add_argument("--sharded-refine", type=int, default=2,
+                    help="z-space refinement steps per solve at N > 1 (fixed: multi-rank control flow is collective)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
@@ -60,7 +65,8 @@ def parse():
     ap.add_argument("--philox", action="store_true", help="device Philox data instead of the reference generator")
     ap.add_argument("--no-modes", dest="modes", action="store_false",
                     help="skip timing the drop-in default and fp64 modes")
-    ap.add_argument("--pageable", action="store_true", help="also time e2e from pageable numpy memory")
+    ap.add_argument("--no-pageable", dest="pageable", action="store_false",
+                    help="skip timing e2e from pageable numpy memory")
     return ap.parse_args()
 
 
@@ -301,11 +307,12 @@ def run_b200(args, rank, world, local):
     last = {}
 
     def one_step():
-        # the fp32 headline mode: f16x2 tensor-core Gram, no refinement (SURVEY §8d fp32 tolerance)
+        # the drop-in default on fp32 scores: the f16x2 tensor-core Gram + z-space refinement to the
+        # reference's result quality (rel_residual <= 1e-10; solvers.py:41-43, :171-194)
         if not sharded:
-            sol = fsb.solve_chol(system, precision=args.precision, refine=0)
+            sol = fsb.solve_chol(system, precision=args.precision, refine=args.refine)
         else:
-            sol = sharded_solve_chol_fused(sm, v, lam, precision=args.precision)
+            sol = sharded_solve_chol_fused(sm, v, lam, precision=args.precision, refine=args.sharded_refine)
         for k, val in ctx.stage_ms().items():
             stage_acc[k].append(val)
         last["sol"] = sol
@@ -344,10 +351,11 @@ def run_b200(args, rank, world, local):
     # ---- the drop-in defaults and the reference's own arithmetic, timed on the same system (N=1) ----
     modes = {}
     if not sharded and args.modes:
-        for name, kw in (("auto (drop-in default: f16x2 + reference refinement rule, fp64 if needed)",
-                          dict(precision="auto", refine="auto")),
+        for name, kw in (("raw f16x2 (no refinement; SURVEY 8d fp32 tolerance relerr <= 1e-6)",
+                          dict(precision="f16x2", refine=0)),
+                         ("raw tf32x3 (no refinement)", dict(precision="tf32x3", refine=0)),
                          ("fp64 (exact fp64 products, the reference's arithmetic)", dict(precision="fp64"))):
-            if dtype == torch.float64 and name.startswith("auto"):
+            if dtype == torch.float64 and name.startswith("raw"):
                 continue
             sol = fsb.solve_chol(system, **kw)
             torch.cuda.synchronize()
@@ -396,17 +404,17 @@ def run_b200(args, rank, world, local):
             # validates S (the reference's frozen copy), the solve returns a numpy x
             if not sharded:
                 out = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(host_S, defer=defer), lam, vh),
-                                     precision=args.precision, refine=0).x
+                                     precision=args.precision, refine=args.refine).x
             else:
                 out = sharded_solve_chol_fused(fsb.ScoreMatrix(host_S, defer=True), vh, lam,
-                                               precision=args.precision).x_local
+                                               precision=args.precision, refine=args.sharded_refine).x_local
             assert isinstance(out, np.ndarray)
 
         e2e_ms = time_e2e(lambda: e2e_step(Sh), args.e2e_steps)
         e2e = {"value": e2e_ms, "unit": "ms",
                "h2d_bytes_per_step": int(Sh.nbytes + vh.nbytes), "d2h_bytes_per_step": int(m_local * 8 + 16),
-               "path": ("solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v), precision='f16x2', "
-                        "refine=0) -> numpy x; construction uploads + validates S on the device"
+               "path": ("solve_chol(DampedSystem(ScoreMatrix(pinned numpy S), lam, numpy v)) -> numpy x (the "
+                        "drop-in default); construction uploads + validates S on the device"
                         if not sharded else
                         "per rank: sharded_solve_chol_fused(ScoreMatrix(pinned numpy shard, defer=True), numpy v "
                         "shard) -> numpy x shard; max over ranks")}
@@ -478,7 +486,8 @@ def run_b200(args, rank, world, local):
                    "rel_residual": sol_ref.rel_residual, "phases_ms": getattr(cpu_reference, "phases_ms", None)}
             parity = {"tolerance_relerr_fp32_modes": 1e-6, "tolerance_relerr_fp64": 1e-10,
                       "reference_rel_residual": sol_ref.rel_residual,
-                      "headline": {"precision": args.precision, "refine": 0, "rel_residual": rels[-1],
+                      "headline": {"precision": args.precision, "refine": str(args.refine),
+                                   "rel_residual": rels[-1], "reference_gate_1e-6": rels[-1] <= 1e-6,
                                    "relerr_vs_reference": _rel_err(x_head, sol_ref.x)}}
             for name, d in modes.items():
                 parity[name] = {"ms": d["ms"], "precision": d["precision"], "rel_residual": d["rel_residual"],
@@ -492,7 +501,10 @@ def run_b200(args, rank, world, local):
         "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
         "data": data,
         "config": {"workload": WORKLOAD, "n": n, "m": m, "m_per_rank": m_local, "lam": lam,
-                   "precision": args.precision, "refine": 0, "diagnostics": True, "l2": L2_NOTE,
+                   "precision": args.precision,
+                   "refine": (f"{args.refine} (z-space refinement: f16x2 factor, exact fp64 residuals)"
+                              if args.precision != "fp64" else f"{args.refine} (the reference's rule)"),
+                   "diagnostics": True, "l2": L2_NOTE,
                    "parallelism": f"column-shard m over {world} GPU(s), NCCL all-reduce of [W|u]"},
         "roofline": roofline,
         "roofline_gemv": gemv or None,
@@ -513,6 +525,8 @@ def run_b200(args, rank, world, local):
 
 def main():
     args = parse()
+    if args.refine != "auto":
+        args.refine = int(args.refine)
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)

@@ -45,8 +45,8 @@ typedef enum {
   FS_PREC_AUTO = 2,   /* FP64 for fp64 input, F16X2 for fp32 input                      */
   FS_PREC_F16X2 = 3   /* fp32 input split per row-scaled element into two fp16 planes
                          (22 significant bits), tcgen05 kind::f16 hi*hi + hi*lo + lo*hi,
-                         fp64 drain; an fp16 overflow (a row whose magnitude range defeats
-                         the sampled scale) transparently recomputes with TF32X3           */
+                         fp64 drain; row scales exact (fs_set_row_absmax) or sampled, an
+                         overflow of sampled scales recomputes with exact ones (below)     */
 } fs_precision;
 
 /* Host-supplied sum-all-reduce over ranks of `count` doubles in device memory,
@@ -81,8 +81,9 @@ int64_t fs_launch_count(const fs_ctx* ctx);
 #define FS_PROF_POTRF 3      /* unpack + lam + Cholesky                         */
 #define FS_PROF_TRSV 4       /* z = L^-T L^-1 u                                 */
 #define FS_PROF_GEMV_STZ 5   /* x = (v - S^T z) / lam                           */
-#define FS_PROF_RESIDUAL 6   /* y = S x, r = S^T y + lam x - v, norms (+ refinement) */
-#define FS_PROF_STAGES 7
+#define FS_PROF_RESIDUAL 6   /* y = S x, r = S^T y + lam x - v, norms (+ x-space refinement) */
+#define FS_PROF_REFINE 7     /* z-space refinement steps (FS_FLAG_REFINE_Z)      */
+#define FS_PROF_STAGES 8
 int fs_profile_enable(fs_ctx* ctx, int on);
 int fs_profile_read(fs_ctx* ctx, double* ms, int count);
 
@@ -138,6 +139,13 @@ int fs_residual_cols(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m
 /* iterative refinement: up to k correction steps with the same factor while
  * rel_residual > refine_above and each step at least halves it; k = 1 is the reference rule */
 #define FS_FLAG_REFINE_STEPS(k) (FS_FLAG_REFINE | (((k) & 0xFF) << 8))
+/* z-space refinement (the fp32-split modes; needs FS_FLAG_RESIDUAL): up to k steps of
+ * z += W~^-1 (S v - W z) on the n x n system, the residual read off the fused x + y pass
+ * (lam (y - z) = S v - W z), each step one TRSV pair and one fused pass over S.  Contracts by
+ * ~2^-21 kappa(W) per step whatever sigma_max^2/lam is (the x-space scheme contracts by
+ * ~2^-21 sigma_max^2/lam and stalls once that nears 1).  Takes precedence over FS_FLAG_REFINE. */
+#define FS_FLAG_REFINE_Z 4
+#define FS_FLAG_REFINE_Z_STEPS(k) (FS_FLAG_REFINE_Z | (((k) & 0xFF) << 8))
 /* multi-rank: the caller's validation found non-finite entries in this rank's shard.  The rank
  * still joins every collective (contributing zeros) and every rank returns FS_EINVAL together;
  * with no all-reduce callback the call just returns FS_EINVAL.  More generally, with a callback
@@ -227,6 +235,24 @@ int fs_jacobi_svd(fs_ctx* ctx, const double* A, int64_t n, int64_t lda, double* 
 int fs_factor_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, const void* v,
                     double lam, const double* U, int64_t ldU, const double* w, int64_t r, double* x, int flags,
                     double* out_res, void* stream);
+
+/* ---- F16X2 row scales ----
+ * fs_row_absmax: out[i] = max_j |a[i, j]| (float, device, `rows` entries) in one streaming pass,
+ *   FS_EINVAL when an entry is not finite (so it doubles as the construction-time validation of
+ *   core.py:108-119).  Context-free; synchronizes.
+ * fs_set_row_absmax: hand those maxima to the next F16X2 Gram / solve on this context (device
+ *   pointer, valid until that call returns; consumed by it).  With exact maxima every row is
+ *   scaled to max |S_i| 2^k in [2^14, 2^15): no fp16 overflow is possible.  Without them the
+ *   scale comes from each row's first 4096 columns; an overflow is detected and that solve (on
+ *   every rank together) recomputes once in F16X2 with exact row scales from its own pass over S
+ *   — no second copy of S, unlike a TF32X3 recomputation (kept only as a last resort).
+ * fs_fallback_count: how many such recomputations this context has made. */
+int fs_row_absmax(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, float* out, void* stream);
+int fs_set_row_absmax(fs_ctx* ctx, const float* row_absmax, int64_t n);
+int64_t fs_fallback_count(const fs_ctx* ctx);
+/* Split-K count the FP64 Gram takes for (n, m) on this context (plan query for tests; -1 for the
+ * other precision modes). */
+int fs_gram_splits(const fs_ctx* ctx, int64_t n, int64_t m, int precision);
 
 /* ---- input validation (core.py:108-119: np.isfinite(S).all() on construction) ----
  * FS_OK when all rows x cols entries (row-major, leading dimension ld) of the device array a are

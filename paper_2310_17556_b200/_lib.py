@@ -15,8 +15,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfisher_b
 FS_OK, FS_EINVAL, FS_NOT_PD, FS_ECUDA, FS_ENOMEM, FS_EUNSUPPORTED, FS_ENOCONV = range(7)
 FS_F32, FS_F64 = 0, 1
 FS_PREC_FP64, FS_PREC_TF32X3, FS_PREC_AUTO, FS_PREC_F16X2 = 0, 1, 2, 3
-FS_FLAG_RESIDUAL, FS_FLAG_REFINE, FS_FLAG_INVALID_SHARD = 1, 2, 0x10000
-PROF_STAGES = ("gram", "gemv_sv", "allreduce", "potrf", "trsv", "gemv_stz", "residual")
+FS_FLAG_RESIDUAL, FS_FLAG_REFINE, FS_FLAG_REFINE_Z, FS_FLAG_INVALID_SHARD = 1, 2, 4, 0x10000
+PROF_STAGES = ("gram", "gemv_sv", "allreduce", "potrf", "trsv", "gemv_stz", "residual", "refine")
 
 _c_int64 = ctypes.c_int64
 _vp = ctypes.c_void_p
@@ -64,6 +64,10 @@ SIGNATURES = {
                                      ctypes.POINTER(ctypes.c_int), _vp]),
     "fs_factor_solve": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, ctypes.c_double,
                                        _vp, _c_int64, _vp, _c_int64, _vp, ctypes.c_int, _dp, _vp]),
+    "fs_row_absmax": (ctypes.c_int, [ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _vp]),
+    "fs_set_row_absmax": (ctypes.c_int, [_vp, _vp, _c_int64]),
+    "fs_fallback_count": (_c_int64, [_vp]),
+    "fs_gram_splits": (ctypes.c_int, [_vp, _c_int64, _c_int64, ctypes.c_int]),
     "fs_all_finite": (ctypes.c_int, [ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp]),
     "fs_chol_solve_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp,
                                           ctypes.c_double, _vp, ALLREDUCE_FN, _vp, ctypes.c_int, ctypes.c_double,
@@ -131,6 +135,13 @@ class Context:
     def profile(self, on: bool = True) -> None:
         self.lib.fs_profile_enable(self.handle, 1 if on else 0)
 
+    def fallbacks(self) -> int:
+        return int(self.lib.fs_fallback_count(self.handle))
+
+    def hint_row_absmax(self, absmax, n: int) -> None:
+        """Exact F16X2 row scales for the next solve / Gram on this context (fs_set_row_absmax)."""
+        self.lib.fs_set_row_absmax(self.handle, None if absmax is None else absmax.data_ptr(), int(n))
+
     def stage_ms(self) -> dict:
         buf = (ctypes.c_double * len(PROF_STAGES))()
         self.lib.fs_profile_read(self.handle, buf, len(PROF_STAGES))
@@ -160,6 +171,23 @@ def all_finite(t) -> bool:
     if rc not in (0, 1):
         raise NativeLibraryError(f"fs_all_finite failed (status {rc})")
     return rc == 0
+
+
+def row_absmax(t):
+    """(finite, absmax) for a 2-D float32 CUDA tensor: one device pass (fs_row_absmax) that both
+    validates finiteness and returns max_j |t[i, j]| per row (float32, device) — the exact F16X2
+    row scales for every later solve on these scores."""
+    import torch
+    if t.dim() != 2 or t.stride(1) != 1 or t.dtype not in (torch.float32, torch.float64):
+        raise ValueError("row_absmax needs a 2-D float tensor with unit column stride")
+    out = torch.empty(t.shape[0], dtype=torch.float32, device=t.device)
+    lib = load()
+    with torch.cuda.device(t.device):
+        rc = lib.fs_row_absmax(FS_F64 if t.dtype == torch.float64 else FS_F32, t.data_ptr(), t.shape[0], t.shape[1],
+                               t.stride(0), out.data_ptr(), torch.cuda.current_stream(t.device).cuda_stream)
+    if rc not in (0, 1):
+        raise NativeLibraryError(f"fs_row_absmax failed (status {rc})")
+    return rc == 0, out
 
 
 def context_for(device: int, n: int, m: int) -> Context:

@@ -31,13 +31,15 @@ from . import _lib
 EPS = float(np.finfo(np.float64).eps)   # core.py:16
 
 
-class ScalarKind(enum.Enum):             # core.py:22-24
+# str mixins: a member equals its value ("chol" == Method.CHOL), so the reference's own enums
+# accept this package's members (fisher_solve.Method(Method.CHOL)) in code that mixes the two
+class ScalarKind(str, enum.Enum):        # core.py:22-24
     REAL64 = "real64"
     REAL32 = "real32"
     COMPLEX128 = "complex128"
 
 
-class Method(enum.Enum):                 # core.py:27-35
+class Method(str, enum.Enum):            # core.py:27-35
     CHOL = "chol"
     SVD_EIGH = "eigh"
     SVD_DIRECT = "svd"
@@ -46,7 +48,7 @@ class Method(enum.Enum):                 # core.py:27-35
     CG = "cg"
 
 
-class Variant(enum.Enum):                # core.py:38-48
+class Variant(str, enum.Enum):           # core.py:38-48
     PLAIN = "plain"
     HERMITIAN = "hermitian"
     REALPART = "realpart"
@@ -171,9 +173,11 @@ class ScoreMatrix:
         self._host = None
         self._t = None
         self._src = None
+        self._absmax = None
         self._device = device
         if isinstance(src, torch.Tensor):
-            t = _to_device_tensor(data, "score matrix", device, force_copy=src.is_cuda)
+            t = self._validated(_to_device_tensor(data, "score matrix", device, force_copy=src.is_cuda,
+                                                  validate=False))
             shape = tuple(t.shape)
             self._t = t
         else:
@@ -183,7 +187,7 @@ class ScoreMatrix:
                 if defer and not np.iscomplexobj(arr):
                     self._src = arr
                 else:
-                    self._t = _to_device_tensor(arr, "score matrix", device)
+                    self._t = self._validated(_to_device_tensor(arr, "score matrix", device, validate=False))
         if len(shape) != 2:
             raise ValueError(f"score matrix must be 2-D, got shape {shape}")
         if shape[0] < 1 or shape[1] < 1:
@@ -192,12 +196,31 @@ class ScoreMatrix:
         # numpy in -> numpy out (drop-in semantics); CUDA tensor in -> CUDA tensor out
         self.host_origin = not (isinstance(src, torch.Tensor) and src.is_cuda)
 
+    def _validated(self, t: torch.Tensor) -> torch.Tensor:
+        """Finiteness check on the device (core.py:108-119); for float32 scores the same pass keeps
+        each row's max |S_i| — the exact F16X2 row scales of every later solve (fs_row_absmax)."""
+        if t.numel() == 0:
+            return t
+        if t.dim() == 2 and t.dtype == torch.float32:
+            ok, self._absmax = _lib.row_absmax(t)
+        else:
+            ok = _lib.all_finite(t)
+        if not ok:
+            raise ValueError("score matrix must contain only finite entries")
+        return t
+
+    @property
+    def row_absmax(self) -> torch.Tensor | None:
+        """Per-row max |S_i| of float32 scores (device), computed at validation; None otherwise."""
+        return self._absmax
+
     @classmethod
     def _owned(cls, t: torch.Tensor, host_origin: bool = False) -> "ScoreMatrix":
         """Wrap a device tensor this package produced (aligned rows, finite): no copy, no check."""
         sm = cls.__new__(cls)
         sm._host = None
         sm._src = None
+        sm._absmax = None
         sm._t = t
         sm._device = t.device
         sm._shape = (int(t.shape[0]), int(t.shape[1]))
@@ -216,7 +239,7 @@ class ScoreMatrix:
     @property
     def tensor(self) -> torch.Tensor:
         if self._t is None:
-            self._t = _to_device_tensor(self._src, "score matrix", self._device)
+            self._t = self._validated(_to_device_tensor(self._src, "score matrix", self._device, validate=False))
             self._src = None
         return self._t
 
@@ -419,10 +442,16 @@ def gram_packed(S: ScoreMatrix, lam: float, precision: str = "auto") -> torch.Te
     prec = resolve_precision(precision, t.dtype)
     ctx = _lib.context_for(t.device.index, n, m)
     out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
+    hint_scales(ctx, S)
     rc = ctx.lib.fs_gram_packed(ctx.handle, dt, PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0),
                                 float(lam), out.data_ptr(), _stream(t.device))
     _check(ctx, rc, "fs_gram_packed")
     return out
+
+
+def hint_scales(ctx, S: "ScoreMatrix") -> None:
+    """Exact F16X2 row scales for the next call on ctx when the scores carry their row maxima."""
+    ctx.hint_row_absmax(S.row_absmax if isinstance(S, ScoreMatrix) else None, S.n)
 
 
 def gram_hermitian_device(S: ScoreMatrix, lam: float, precision: str = "auto") -> torch.Tensor:

@@ -16,6 +16,8 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fs.h"
 #include "kernels.h"
 #include "tiles.cuh"
@@ -28,12 +30,14 @@ struct fs_ctx {
   double* d_W = nullptr;        // n x n, becomes L in place
   double* d_z = nullptr;        // n
   double* d_y = nullptr;        // n
+  double* d_zacc = nullptr;     // n: accumulated z of the z-space refinement
   double* d_partials = nullptr; // row-GEMV chunk partials
   double* d_block_sums = nullptr;
   double* d_sums = nullptr;     // 4
   double* d_r = nullptr;        // m (residual vector, refinement right-hand side)
   double* d_v64 = nullptr;      // m (fp64 copy of an fp32 v in fp64 precision mode)
   double* d_syrk_ws = nullptr;
+  size_t syrk_bytes = 0;
   double* d_potrf = nullptr;    // inverted diagonal blocks (Linv) + double-buffered panels
   int64_t* d_status = nullptr;
   int64_t* h_status = nullptr;  // pinned
@@ -62,6 +66,12 @@ struct fs_ctx {
   float* d_scale = nullptr;     // F16X2 row scales (n_max)
   double* d_inv_scale = nullptr;
   int* d_ovf = nullptr;         // F16X2 retile flags (bit 1: fp16 overflow)
+  // F16X2 exact row scales: a caller-supplied row max |S_i| (fs_set_row_absmax, used by the next
+  // solve / Gram), or this context's own pass over S after an overflow of the sampled scales
+  const float* hint_absmax = nullptr;
+  int64_t hint_n = 0;
+  float* d_absmax = nullptr;    // n_max
+  int64_t fallbacks = 0;        // exact-scale recomputations (+ TF32X3 last resorts)
   int* h_ovf = nullptr;         // pinned
   // host-buffer entry (fs_chol_solve_host): device copies of S, v, x, an upload stream and
   // one event per uploaded row chunk (all lazy)
@@ -91,6 +101,12 @@ struct fs_ctx {
 };
 
 namespace {
+// NVTX ranges per solve stage (header-only NVTX v3: free unless a profiler attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 inline void prof_mark(fs_ctx* ctx, int stage, cudaStream_t st) {
   if (ctx->prof_on && ctx->n_marks < fs_ctx::kMaxMarks && ctx->ev[ctx->n_marks]) {
     cudaEventRecord(ctx->ev[ctx->n_marks], st);
@@ -119,7 +135,7 @@ Sizes sizes_for(int64_t n, int64_t m, int num_sms) {
   s.partials = (size_t)fs::gemv_rows_chunks(m, true) * n * sizeof(double);
   s.block_sums = (size_t)fs::residual_cols_blocks(m, true) * 2 * sizeof(double);
   s.r = (size_t)m * sizeof(double);
-  s.syrk = std::max(fs::syrk_dmma_workspace_bytes(num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
+  s.syrk = std::max(fs::syrk_dmma_workspace_bytes(n, m, num_sms), fs::syrk_tc_workspace_bytes(n, m, num_sms));
   s.potrf = (size_t)fs::potrf_scratch_doubles(n) * sizeof(double);
   return s;
 }
@@ -249,6 +265,27 @@ bool f16_direct() {
   return env != 0;
 }
 
+// F16X2 row scales: exact from a row-max hint (the caller's fs_set_row_absmax, or this context's
+// own pass after an overflow), else from the sampled head of each row (overflow -> exact retry).
+cudaError_t f16_scales(fs_ctx* ctx, const float* S, int64_t n, int64_t m, int64_t ldS, cudaStream_t st, int* l) {
+  if (ctx->hint_absmax && ctx->hint_n == n) return fs::scales_from_max(ctx->hint_absmax, n, ctx->d_scale, ctx->d_inv_scale, st, l);
+  return fs::row_scales(S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, l);
+}
+
+// after an fp16 overflow of the sampled scales: the exact row maxima of S (one streaming pass),
+// used as the hint of the recomputation
+cudaError_t exact_row_max(fs_ctx* ctx, const float* S, int64_t n, int64_t m, int64_t ldS, cudaStream_t st) {
+  int l = 0;
+  cudaError_t e = cudaMemsetAsync(ctx->d_absmax, 0, n * sizeof(float), st);
+  if (e == cudaSuccess)
+    e = fs::check_finite(S, false, n, m, ldS, ctx->d_ovf, ctx->num_sms, st, &l, (unsigned*)ctx->d_absmax);
+  ctx->launches += l;
+  ctx->hint_absmax = ctx->d_absmax;
+  ctx->hint_n = n;
+  ctx->fallbacks += 1;
+  return e;
+}
+
 // Gram stage.  TF32X3: retile S into S_t (optionally fused with u = S w), then the CTA-pair
 // tcgen05 SYRK on S_t.  FP64: exact-product SIMT SYRK on S.
 int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, int64_t m,
@@ -264,7 +301,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     // and forms u = S w in the same pass.  The overflow flag is checked by the caller at its next
     // host synchronisation.
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
-    if (e == cudaSuccess) e = fs::row_scales((const float*)S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, &l);
+    if (e == cudaSuccess) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
     if (e == cudaSuccess)
       e = fs::syrk_f16_direct((const float*)S, ldS, n, m, ctx->d_scale, ctx->d_inv_scale, w32, ctx->d_ovf,
@@ -274,7 +311,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     // flag is checked by the caller at its next host synchronisation.
     if ((rc = ensure_tiles(ctx, true))) return rc;
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
-    if (e == cudaSuccess) e = fs::row_scales((const float*)S, n, m, ldS, ctx->d_scale, ctx->d_inv_scale, st, &l);
+    if (e == cudaSuccess) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
     if (e == cudaSuccess)
       e = fs::retile16_cols((const float*)S, n, m, ldS, w32, ctx->d_partials, ctx->d_St, ctx->d_scale, 0, m,
                             ctx->d_ovf, st, &l);
@@ -288,7 +325,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
     if (e == cudaSuccess) e = fs::syrk_tc(ctx->d_St, n, m, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
   } else {
-    e = fs::syrk_dmma(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+    e = fs::syrk_dmma(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->syrk_bytes, ctx->num_sms, st, &l);
   }
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "gram");
@@ -330,6 +367,37 @@ __global__ void status_slot_kernel(const int* nonfinite, int idle, int host_nonf
   *out = s;
 }
 
+// z-space refinement (see finish_x): t = lam (y - z_acc) into dz
+__global__ void zres_kernel(const double* __restrict__ y, const double* __restrict__ zacc, double lam, int64_t n,
+                            double* __restrict__ dz) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dz[i] = lam * (y[i] - zacc[i]);
+}
+// z_acc += dz; sums[0] = |dz|^2, sums[1] = |z_acc|^2 (one CTA, fixed order: deterministic)
+__global__ void zadd_kernel(double* __restrict__ zacc, const double* __restrict__ dz, int64_t n,
+                            double* __restrict__ sums) {
+  __shared__ double red[2][32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = dz[i], z = zacc[i] + d;
+    zacc[i] = z;
+    a = fma(d, d, a);
+    b = fma(z, z, b);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = a; red[1][threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { sa += red[0][w]; sb += red[1][w]; }
+    sums[0] = sa;
+    sums[1] = sb;
+  }
+}
+
 // after the norms all-reduce: the collective decision when the status slot is set
 int collective_failure(fs_ctx* ctx, double status) {
   const long long nf = (long long)(status / kStatusNonFinite);
@@ -369,6 +437,7 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
   const bool multi = allreduce != nullptr;
   void* stream = (void*)st;
   double* u = ctx->d_packed + n * (n + 1) / 2;
+  NvtxRange range("fs: allreduce + potrf + trsv");
   if (multi) {
     if (ctx->poison_rc || ctx->empty_shard) cudaMemsetAsync(ctx->d_packed, 0, packed_len(n) * sizeof(double), st);
     if (allreduce(ctx->d_packed, (int64_t)packed_len(n), allreduce_user, stream) != 0)
@@ -432,7 +501,10 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     if (e != cudaSuccess) return cuda_fail(ctx, e, "gemv_cols_solve");
     return FS_OK;
   };
-  if (!idle()) FS_STEP(solve_cols(v, vdt == FS_F64, lam, false));
+  {
+    NvtxRange r("fs: x = (v - S^T z)/lam, y = S x");
+    if (!idle()) FS_STEP(solve_cols(v, vdt == FS_F64, lam, false));
+  }
   prof_mark(ctx, FS_PROF_GEMV_STZ, st);
   if (ctx->early_x_host && !idle()) {   // host entry: x -> host on up_st while the residual pass runs
     FS_CK(cudaEventRecord(ctx->ev_xready, st), "event");
@@ -458,11 +530,58 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     }
     return FS_OK;
   };
+  // ---- z-space refinement (FS_FLAG_REFINE_Z, the fp32-split modes) ----
+  // x = (v - S^T z)/lam depends on S only through the n-vector z = W^-1 S v, W = S S^T + lam I.
+  // The split Gram's factor solves W~ = W + E instead; refining z on the n x n system W z = u
+  // contracts by ||W~^-1 E|| ~ 2^-21 kappa(W) per step, whereas refining x on the m x m system
+  // (the reference's scheme) contracts by ~2^-21 sigma_max^2 / lam — no contraction at all at
+  // the headline (sigma^2/lam ~ 1e6).  The z residual needs no extra pass: with y = S x (already
+  // formed by the fused x + y pass, exact fp64 products), lam (y - z) = S v - S S^T z - lam z =
+  // u - W z exactly.  A step is: d = W~^-1 lam (y - z) (the TRSV pair), z += d, and one fused pass
+  // x += (0 - S^T d)/lam, y = S x.  Single rank: stop once |d| <= 2^-50 |z|; multi-rank: the
+  // fixed step count (control flow may not depend on rank-local data).  Profiled as
+  // FS_PROF_REFINE.
+  const bool want_z = (flags & FS_FLAG_REFINE_Z) != 0 && want_res;
+  if (want_z) {
+    const int zsteps = std::max(1, (flags >> 8) & 0xFF);
+    if (!idle()) FS_CKS(cudaMemcpyAsync(ctx->d_zacc, ctx->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "z copy");
+    if (!idle()) FS_CKS(cudaMemsetAsync(ctx->d_r, 0, m * sizeof(double), st), "zero rhs");
+    for (int step = 0; step < zsteps; ++step) {
+      NvtxRange r("fs: z-space refinement step");
+      if (!y_ready && !idle()) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream));
+      if (multi) {
+        if (idle()) cudaMemsetAsync(ctx->d_y, 0, n * sizeof(double), st);
+        if (allreduce(ctx->d_y, n, allreduce_user, stream) != 0) return fail(ctx, FS_ECUDA, "allreduce of y failed");
+      }
+      if (!ctx->poison_rc) {
+        const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 64);
+        zres_kernel<<<g, 256, 0, st>>>(ctx->d_y, ctx->d_zacc, lam, n, ctx->d_z);
+        int l = 0;
+        FS_CKS(fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l), "trsv_pair (z refine)");
+        zadd_kernel<<<1, 1024, 0, st>>>(ctx->d_zacc, ctx->d_z, n, ctx->d_sums);
+        ctx->launches += l + 2;
+      }
+      if (ctx->early_x_state == 1) {   // x changes: the early copy must finish reading it first
+        FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");
+        ctx->early_x_state = 2;
+      }
+      if (!idle()) FS_STEP(solve_cols(ctx->d_r, 1, lam, true));
+      prof_mark(ctx, FS_PROF_REFINE, st);
+      if (!multi && step + 1 < zsteps) {
+        FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "dz d2h");
+        FS_CK(cudaStreamSynchronize(st), "sync");
+        // the last correction moved z by <= 1e-12 of its size: x is at the fp64 residual floor
+        // (the reference's refine rule, rel_residual <= 1e-10, is met one step earlier than that)
+        if (!(ctx->h_sums[0] > 1e-24 * ctx->h_sums[1])) break;
+      }
+    }
+  }
   double abs_res = NAN, rel_res = NAN;
   // refinement steps: FS_FLAG_REFINE alone = the reference's single step; bits 8-15 raise it
-  const int max_steps = want_refine ? std::max(1, (flags >> 8) & 0xFF) : 0;
+  const int max_steps = want_refine && !want_z ? std::max(1, (flags >> 8) & 0xFF) : 0;
   double prev_rel = INFINITY;
   for (int pass = 0; want_res && pass <= max_steps; ++pass) {
+    NvtxRange r("fs: residual (+ x-space refinement)");
     // residual: y = S x (all-reduced), r = S^T y + lam x - v, norms all-reduced
     if (!y_ready && !idle()) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream));
     if (multi) {
@@ -582,17 +701,20 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
   A((void**)&ctx->d_W, s.W);
   A((void**)&ctx->d_z, s.vec);
   A((void**)&ctx->d_y, s.vec);
+  A((void**)&ctx->d_zacc, s.vec);
   A((void**)&ctx->d_partials, s.partials);
   A((void**)&ctx->d_block_sums, s.block_sums);
   A((void**)&ctx->d_sums, 4 * sizeof(double));
   A((void**)&ctx->d_r, s.r);
   A((void**)&ctx->d_v64, s.r);
   A((void**)&ctx->d_syrk_ws, s.syrk);
+  ctx->syrk_bytes = s.syrk;
   A((void**)&ctx->d_potrf, s.potrf);
   A((void**)&ctx->d_status, sizeof(int64_t));
   A((void**)&ctx->d_scale, n_max * sizeof(float));
   A((void**)&ctx->d_inv_scale, n_max * sizeof(double));
   A((void**)&ctx->d_ovf, sizeof(int));
+  A((void**)&ctx->d_absmax, n_max * sizeof(float));
   if (ok && cudaMallocHost((void**)&ctx->h_ovf, sizeof(int)) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&ctx->h_status, sizeof(int64_t)) != cudaSuccess) ok = false;
   if (ok && cudaMallocHost((void**)&ctx->h_sums, 4 * sizeof(double)) != cudaSuccess) ok = false;
@@ -611,11 +733,11 @@ int fs_ctx_create(fs_ctx** out, int device, int64_t n_max, int64_t m_max) {
 
 void fs_ctx_destroy(fs_ctx* ctx) {
   if (!ctx) return;
-  cudaFree(ctx->d_packed); cudaFree(ctx->d_W); cudaFree(ctx->d_z); cudaFree(ctx->d_y);
+  cudaFree(ctx->d_packed); cudaFree(ctx->d_W); cudaFree(ctx->d_z); cudaFree(ctx->d_y); cudaFree(ctx->d_zacc);
   cudaFree(ctx->d_partials); cudaFree(ctx->d_block_sums); cudaFree(ctx->d_sums);
   cudaFree(ctx->d_r); cudaFree(ctx->d_v64); cudaFree(ctx->d_syrk_ws); cudaFree(ctx->d_status);
   cudaFree(ctx->d_potrf);
-  cudaFree(ctx->d_scale); cudaFree(ctx->d_inv_scale); cudaFree(ctx->d_ovf);
+  cudaFree(ctx->d_scale); cudaFree(ctx->d_inv_scale); cudaFree(ctx->d_ovf); cudaFree(ctx->d_absmax);
   if (ctx->d_eig) cudaFree(ctx->d_eig);
   if (ctx->d_svd) cudaFree(ctx->d_svd);
   if (ctx->d_U) cudaFree(ctx->d_U);
@@ -673,8 +795,14 @@ int fs_gram_packed(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t
     cudaStream_t st = (cudaStream_t)stream;
     FS_CK(cudaMemcpyAsync(ctx->h_ovf, ctx->d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
-    if (*ctx->h_ovf & 2) return gram_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, lam, G_packed, st);
+    if (*ctx->h_ovf & 2) {   // the sampled scales overflowed: exact row scales, F16X2 again
+      FS_CK(exact_row_max(ctx, (const float*)S, n, m, ldS, st), "row max");
+      rc = gram_impl(ctx, dtype, FS_PREC_F16X2, S, n, m, ldS, lam, G_packed, st);
+      ctx->hint_absmax = nullptr;
+      return rc;
+    }
   }
+  ctx->hint_absmax = nullptr;
   return FS_OK;
 }
 
@@ -826,6 +954,7 @@ static int chol_solve_impl(fs_ctx* ctx, int dtype, int precision, const void* S,
   // 1. partial Gram (no shift) and u = S v, packed for one all-reduce (tensor-core modes: one
   //    fused streaming pass computes u and writes the tiled copy the SYRK reads)
   if (!empty && !ctx->poison_rc) {
+    NvtxRange r("fs: gram + u = S v");
     if (use_tc && vdt == FS_F32) {
       FS_STEP(gram_impl(ctx, dtype, precision, S, n, m, ldS, 0.0, ctx->d_packed, st, (const float*)v, u));
     } else {
@@ -834,11 +963,32 @@ static int chol_solve_impl(fs_ctx* ctx, int dtype, int precision, const void* S,
       prof_mark(ctx, FS_PROF_GEMV_SV, st);
     }
   }
+  if ((flags & FS_FLAG_REFINE_Z) && vdt == FS_F32 && !empty && !ctx->poison_rc) {
+    // z-space refinement: every x pass in exact fp64 products (the first one's fp32 rounding
+    // would otherwise stay in x's component outside the row space of S, ~1e-9 of the residual)
+    int l = 0;
+    FS_CKS(fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l), "widen v");
+    ctx->launches += l;
+    v = ctx->d_v64;
+    vdt = FS_F64;
+  }
   rc = solve_tail(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above, pivot,
                   out_res, st, use_tc == 2 ? ctx->d_ovf : nullptr, nonfinite);
-  if (rc == kRetryTf32)
+  const bool had_hint = ctx->hint_absmax != nullptr;
+  ctx->hint_absmax = nullptr;
+  if (rc == kRetryTf32) {
+    // some rank's sampled fp16 scales overflowed (the decision is collective): every rank
+    // recomputes in F16X2 with exact row scales (no second copy of S); exact scales cannot
+    // overflow, so the TF32X3 recomputation is only a last resort
+    if (!had_hint) {
+      if (!ctx->poison_rc && !ctx->empty_shard) FS_CKS(exact_row_max(ctx, (const float*)S, n, m, ldS, st), "row max");
+      return chol_solve_impl(ctx, dtype, FS_PREC_F16X2, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
+                             refine_above, pivot, out_res, stream, nonfinite);
+    }
+    ctx->fallbacks += 1;
     return chol_solve_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
                            refine_above, pivot, out_res, stream, nonfinite);
+  }
   return rc;
 }
 
@@ -846,6 +996,7 @@ int fs_chol_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
                   int64_t ldS, const void* v, double lam, double* x, fs_allreduce_fn allreduce,
                   void* allreduce_user, int flags, double refine_above, int64_t* pivot,
                   double* out_res, void* stream) {
+  NvtxRange range("fs_chol_solve");
   return chol_solve_impl(ctx, dtype, precision, S, n, m, ldS, v, lam, x, allreduce, allreduce_user, flags,
                          refine_above, pivot, out_res, stream);
 }
@@ -989,11 +1140,20 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     if (!(use_tc == 2 && direct) && !ctx->poison_rc) FS_CKS(fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l), "u reduce");
     ctx->launches += l;
     prof_mark(ctx, FS_PROF_GRAM, st);
-    rc = solve_tail(ctx, dtype, S, n, m, ldd, v, dtype, lam, x, allreduce, allreduce_user, flags, refine_above,
+    int vdt = dtype;
+    if ((flags & FS_FLAG_REFINE_Z) && dtype == FS_F32 && !ctx->poison_rc) {   // exact x passes (chol_solve_impl)
+      FS_CKS(fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l), "widen v");
+      v = ctx->d_v64;
+      vdt = FS_F64;
+    }
+    rc = solve_tail(ctx, dtype, S, n, m, ldd, v, vdt, lam, x, allreduce, allreduce_user, flags, refine_above,
                     pivot, out_res, st, use_tc == 2 ? ctx->d_flag : nullptr, nonfinite);
-    if (rc == kRetryTf32)   // fp16 overflow: S is on the device already
-      rc = chol_solve_impl(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
+    v = ctx->d_vin;
+    if (rc == kRetryTf32) {   // fp16 overflow of the sampled scales: S is on the device already
+      if (!ctx->poison_rc) FS_CKS(exact_row_max(ctx, (const float*)S, n, m, ldd, st), "row max");
+      rc = chol_solve_impl(ctx, dtype, FS_PREC_F16X2, S, n, m, ldd, v, lam, x, allreduce, allreduce_user, flags,
                            refine_above, pivot, out_res, stream, nonfinite);
+    }
   } else {
     FS_CKS(upload(0, m, 0), "S h2d");
     if (!ctx->poison_rc)
@@ -1077,13 +1237,18 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
     return fail(ctx, FS_ECUDA, "allreduce of [G | u] failed");
   prof_mark(ctx, FS_PROF_ALLREDUCE, st);
   // 2. G = U diag(w) U^T, w descending (solvers.py:261-266); sigma floor (solvers.py:267-271)
+  const bool had_hint = ctx->hint_absmax != nullptr;
+  ctx->hint_absmax = nullptr;
   if ((rc = eig_impl(ctx, ctx->d_packed, n, st))) return rc;
   if (use_tc == 2) {   // an F16X2 overflow shows up here already (the eigh path synchronises)
     FS_CK(cudaMemcpyAsync(ctx->h_ovf, ctx->d_ovf, sizeof(int), cudaMemcpyDeviceToHost, st), "flag d2h");
     FS_CK(cudaStreamSynchronize(st), "sync");
-    if (*ctx->h_ovf & 2)
-      return fs_eigh_solve(ctx, dtype, FS_PREC_TF32X3, S, n, m, ldS, v, lam, sigma_floor, x, allreduce,
-                           allreduce_user, flags, rank, out_res, stream);
+    if (*ctx->h_ovf & 2) {   // sampled scales overflowed: exact row scales (TF32X3 only as a last resort)
+      if (!had_hint) FS_CK(exact_row_max(ctx, (const float*)S, n, m, ldS, st), "row max");
+      else ctx->fallbacks += 1;
+      return fs_eigh_solve(ctx, dtype, had_hint ? FS_PREC_TF32X3 : FS_PREC_F16X2, S, n, m, ldS, v, lam, sigma_floor, x,
+                           allreduce, allreduce_user, flags, rank, out_res, stream);
+    }
   }
   prof_mark(ctx, FS_PROF_POTRF, st);
   const double s0 = sqrt(std::max(ctx->h_w[0], 0.0));
@@ -1242,6 +1407,46 @@ int fs_factor_solve(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
   int64_t piv = -1;
   return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, nullptr, nullptr, flags & FS_FLAG_RESIDUAL, 0.0, &piv,
                   out_res, st, nullptr);
+}
+
+int fs_row_absmax(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, float* out, void* stream) {
+  if (!a || !out || rows < 1 || cols < 0 || ld < cols || (dtype != FS_F32 && dtype != FS_F64)) return FS_EINVAL;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return FS_ECUDA;
+  struct Flag { int* d = nullptr; int* h = nullptr; };
+  static Flag flags[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return FS_EINVAL;
+  Flag& f = flags[dev];
+  if (!f.d && (cudaMalloc((void**)&f.d, sizeof(int)) != cudaSuccess ||
+               cudaMallocHost((void**)&f.h, sizeof(int)) != cudaSuccess))
+    return FS_ENOMEM;
+  cudaStream_t st = (cudaStream_t)stream;
+  int l = 0;
+  if (cudaMemsetAsync(f.d, 0, sizeof(int), st) != cudaSuccess ||
+      cudaMemsetAsync(out, 0, rows * sizeof(float), st) != cudaSuccess ||
+      (cols > 0 && fs::check_finite(a, dtype == FS_F64, rows, cols, ld, f.d, sms, st, &l, (unsigned*)out) != cudaSuccess) ||
+      cudaMemcpyAsync(f.h, f.d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return FS_ECUDA;
+  return (*f.h & 1) ? FS_EINVAL : FS_OK;
+}
+
+int fs_set_row_absmax(fs_ctx* ctx, const float* row_absmax, int64_t n) {
+  if (!ctx || n < 0) return FS_EINVAL;
+  ctx->hint_absmax = row_absmax;
+  ctx->hint_n = row_absmax ? n : 0;
+  return FS_OK;
+}
+
+int64_t fs_fallback_count(const fs_ctx* ctx) { return ctx ? ctx->fallbacks : 0; }
+
+int fs_gram_splits(const fs_ctx* ctx, int64_t n, int64_t m, int precision) {
+  if (!ctx || n < 1 || m < 1) return -1;
+  if (precision != FS_PREC_FP64) return -1;
+  return fs::syrk_dmma_splits(n, m, ctx->num_sms, ctx->syrk_bytes);
 }
 
 int fs_all_finite(int dtype, const void* a, int64_t rows, int64_t cols, int64_t ld, void* stream) {

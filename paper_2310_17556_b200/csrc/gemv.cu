@@ -880,20 +880,60 @@ __global__ void reduce_pairs_kernel(const double* __restrict__ block_sums, int64
 // 4 loads in flight per thread.
 template <typename T>
 __global__ void check_finite_kernel(const T* __restrict__ a, int64_t rows, int64_t cols, int64_t ld,
-                                    int* __restrict__ flag) {
+                                    int* __restrict__ flag, unsigned* __restrict__ rowmax) {
+  // rowmax (optional): per-row max |a| as float bits (non-negative floats order like unsigned ints),
+  // one atomicMax per block and row after a block reduction
+  __shared__ float red[32];
   bool bad = false;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     const T* row = a + r * ld;
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float mx = 0.f;
     for (; c + 3 * step < cols; c += 4 * step) {
       const T x0 = ld_stream(row + c), x1 = ld_stream(row + c + step), x2 = ld_stream(row + c + 2 * step),
               x3 = ld_stream(row + c + 3 * step);
       bad |= !(isfinite(x0) && isfinite(x1) && isfinite(x2) && isfinite(x3));
+      if (rowmax) mx = fmaxf(fmaxf(fmaxf(mx, fabsf((float)x0)), fabsf((float)x1)), fmaxf(fabsf((float)x2), fabsf((float)x3)));
     }
-    for (; c < cols; c += step) bad |= !isfinite(ld_stream(row + c));
+    for (; c < cols; c += step) {
+      const T x = ld_stream(row + c);
+      bad |= !isfinite(x);
+      if (rowmax) mx = fmaxf(mx, fabsf((float)x));
+    }
+    if (rowmax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float b = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = fmaxf(b, red[w]);
+        if (b > 0.f) atomicMax(rowmax + r, __float_as_uint(b));
+      }
+      __syncthreads();
+    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// F16X2 row scales from exact row maxima: 2^k with max |S_i| 2^k in [2^14, 2^15), so no element
+// of the row can overflow fp16 (max 65504) and elements down to 2^-18 of the row maximum keep a
+// normal lo plane (all 22 bits).
+__global__ void scales_from_max_kernel(const float* __restrict__ absmax, int64_t n, float* __restrict__ scale,
+                                       double* __restrict__ inv_scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float mx = absmax[i];
+  int k = 0;
+  if (mx > 0.f && isfinite(mx)) {
+    int e;
+    frexpf(mx, &e);                     // mx in [2^(e-1), 2^e)
+    k = 15 - e;                         // mx * 2^k in [2^14, 2^15)
+    k = k > 120 ? 120 : (k < -120 ? -120 : k);
+  }
+  scale[i] = ldexpf(1.f, k);
+  inv_scale[i] = ldexp(1.0, -k);
 }
 
 __global__ void widen_kernel(const float* __restrict__ in, int64_t m, double* __restrict__ out) {
@@ -1173,14 +1213,21 @@ cudaError_t flag_bit_to_double(const int* flags, int bit, double* out, cudaStrea
 }
 
 cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
-                         cudaStream_t st, int* launches) {
+                         cudaStream_t st, int* launches, unsigned* rowmax) {
   // ~num_sms * 8 blocks: x covers the columns (<= 1024 per block row), y the rows
   const int64_t want = (int64_t)num_sms * 8;
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((cols + 1023) / 1024, want));
   const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(rows, 65535), want / gx));
   const dim3 grid((unsigned)gx, (unsigned)gy);
-  if (is64) check_finite_kernel<double><<<grid, 256, 0, st>>>((const double*)a, rows, cols, ld, flag);
-  else check_finite_kernel<float><<<grid, 256, 0, st>>>((const float*)a, rows, cols, ld, flag);
+  if (is64) check_finite_kernel<double><<<grid, 256, 0, st>>>((const double*)a, rows, cols, ld, flag, rowmax);
+  else check_finite_kernel<float><<<grid, 256, 0, st>>>((const float*)a, rows, cols, ld, flag, rowmax);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t scales_from_max(const float* absmax, int64_t n, float* scale, double* inv_scale, cudaStream_t st,
+                            int* launches) {
+  scales_from_max_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(absmax, n, scale, inv_scale);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

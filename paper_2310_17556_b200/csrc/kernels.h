@@ -7,8 +7,12 @@
 namespace fs {
 
 // ---- gemv.cu (HBM-bound streaming passes over S) ----
+// flag |= 1 if any entry is non-finite; rowmax (optional, zero-initialised): per-row max |a| as float bits
 cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
-                         cudaStream_t st, int* launches);
+                         cudaStream_t st, int* launches, unsigned* rowmax = nullptr);
+// F16X2 row scales 2^k from exact row maxima (max |S_i| 2^k in [2^14, 2^15): no fp16 overflow)
+cudaError_t scales_from_max(const float* absmax, int64_t n, float* scale, double* inv_scale, cudaStream_t st,
+                            int* launches);
 cudaError_t widen_f32(const float* in, int64_t m, double* out, cudaStream_t st, int* launches);
 // fp32 u = S w (w may be NULL: retile only) that also writes the tiled copy S_t (tiles.cuh)
 // rows [r0, r1) only (r1 < 0: all; when r1 == n the tiled copy's zero padding rows are written
@@ -58,10 +62,11 @@ cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64
                           int* launches);
 
 // ---- syrk_dmma.cu (exact-product fp64 Gram on the fp64 tensor cores, any dtype) ----
-size_t syrk_dmma_workspace_bytes(int num_sms);                        // bound for any problem
-size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms);       // exact for (n, m)
+size_t syrk_dmma_workspace_bytes(int64_t n, int64_t m, int num_sms);   // a context for (n, m): every smaller plan fits
+size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms);        // tiles x splits (partials + flush slots)
+int syrk_dmma_splits(int64_t n, int64_t m, int num_sms, size_t ws_bytes);   // split count the plan takes
 cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam, double* Gp,
-                      double* ws, int num_sms, cudaStream_t st, int* launches);
+                      double* ws, size_t ws_bytes, int num_sms, cudaStream_t st, int* launches);
 
 // ---- syrk_tc.cu (tcgen05 3xTF32 Gram, fp32 input) ----
 size_t syrk_tc_workspace_bytes(int64_t n, int64_t m, int num_sms);

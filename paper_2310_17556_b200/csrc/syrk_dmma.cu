@@ -322,7 +322,8 @@ double round_fill(int tiles, int P, int num_sms) {
   return (double)units / (double)(rounds * num_sms);
 }
 
-DPlan dplan(int64_t n, int64_t m, int num_sms) {
+// cap: bytes of split-K partial / flush tiles available (SIZE_MAX: the unconstrained plan)
+DPlan dplan(int64_t n, int64_t m, int num_sms, size_t cap) {
   DPlan p;
   const int nb = (int)((n + kT - 1) / kT);
   p.tiles = nb * (nb + 1) / 2;
@@ -331,9 +332,8 @@ DPlan dplan(int64_t n, int64_t m, int num_sms) {
     p.P = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms / p.tiles, kblocks / 4));
   } else {
     // more tiles than SMs: split K when it fills the last round better (n = 4096: 528 tiles are
-    // 3.57 rounds -> 5-way splits fill 17.8 of 18), within the workspace the context holds
-    // (shared with the tcgen05 SYRK) and keeping >= 16 stages per unit
-    const size_t cap = std::max(syrk_dmma_workspace_bytes(num_sms), syrk_tc_workspace_bytes(n, m, num_sms));
+    // 3.57 rounds -> 5-way splits fill 17.8 of 18), within the workspace the context holds and
+    // keeping >= 16 stages per unit
     p.P = 1;
     double best = round_fill(p.tiles, 1, num_sms);
     for (int P = 2; P <= 8; ++P) {
@@ -367,22 +367,31 @@ bool dmma_flush() {
 
 }  // namespace
 
-size_t syrk_dmma_workspace_bytes(int num_sms) { return (size_t)num_sms * kT * kT * sizeof(double); }
-
-size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms) {
-  DPlan p = dplan(n, m, num_sms);
-  return p.P > 1 ? (size_t)p.tiles * p.P * kT * kT * sizeof(double) : 0;
+// One 128 x 128 fp64 tile per CTA of the grid: the split-K partial and, with or without a split,
+// the CTA's flush slot of the two-level accumulation.  A context sized for (n_max, m_max) holds
+// the unconstrained plan of that problem (or one tile per SM, whichever is larger); every smaller
+// problem's plan then fits, because dplan caps its split count by the bytes actually held.
+size_t syrk_dmma_workspace_bytes(int64_t n, int64_t m, int num_sms) {
+  const DPlan p = dplan(n, m, num_sms, SIZE_MAX);
+  return (size_t)std::max<int64_t>(num_sms, (int64_t)p.tiles * p.P) * kT * kT * sizeof(double);
 }
 
+size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms) {
+  const DPlan p = dplan(n, m, num_sms, SIZE_MAX);
+  return (size_t)p.tiles * p.P * kT * kT * sizeof(double);
+}
+
+int syrk_dmma_splits(int64_t n, int64_t m, int num_sms, size_t ws_bytes) { return dplan(n, m, num_sms, ws_bytes).P; }
+
 cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam, double* Gp,
-                      double* ws, int num_sms, cudaStream_t st, int* launches) {
-  DPlan p = dplan(n, m, num_sms);
+                      double* ws, size_t ws_bytes, int num_sms, cudaStream_t st, int* launches) {
+  DPlan p = dplan(n, m, num_sms, ws_bytes);
   const int direct = p.P == 1 ? 1 : 0;
   const int vec = ((reinterpret_cast<uintptr_t>(S) | (uintptr_t)(ldS * (s_f64 ? 8 : 4))) & 15) == 0 ? 1 : 0;
   const unsigned grid = (unsigned)(p.tiles * p.P);
+  if (!direct && (!ws || (size_t)grid * kT * kT * sizeof(double) > ws_bytes)) return cudaErrorInvalidValue;
   // the flush slots are the split-K partial tiles' own: one 128 x 128 fp64 tile per CTA
-  const size_t cap = std::max(syrk_dmma_workspace_bytes(num_sms), syrk_tc_workspace_bytes(n, m, num_sms));
-  const int flush = ws && (size_t)grid * kT * kT * sizeof(double) <= cap && dmma_flush() ? 1 : 0;
+  const int flush = ws && (size_t)grid * kT * kT * sizeof(double) <= ws_bytes && dmma_flush() ? 1 : 0;
   if (s_f64 && vec && dmma_async()) {
     cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
     syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam,

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .core import EPS, FactorizationError, _check, _dt, _stream, resolve_precision, PRECISIONS
-from .solvers import REFINE_ABOVE_REL
+from .solvers import REFINE_ABOVE_REL, refine_flags
 
 
 def column_shard(m: int, world: int, rank: int) -> tuple[int, int]:
@@ -217,6 +217,7 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
     host = None
     invalid = False
     S = None
+    absmax = None
     if isinstance(S_local, ScoreMatrix):
         if S_local.is_uploaded or not S_local.host_origin:
             S = S_local.tensor
@@ -229,7 +230,11 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
             S = S_local
         else:
             S = _to_device_tensor(S_local, "score matrix", dev, validate=False)   # aligned rows (no copy when already)
-            invalid = not _lib.all_finite(S)
+            if S.dtype == torch.float32:      # the validation pass also yields the exact F16X2 row scales
+                ok, absmax = _lib.row_absmax(S)
+            else:
+                ok = _lib.all_finite(S)
+            invalid = not ok
     else:
         arr = _coerce_host(S_local, "score matrix")
         if arr.ndim == 2 and arr.shape[1] == 0:
@@ -239,13 +244,13 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
             host = ScoreMatrix(arr, defer=True).host_array        # numpy shard: validated on the device
     piv = ctypes.c_int64(-1)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
-    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (refine << 8)) if refine else 0)
     cb = nccl_allreduce_fn(dev, group)
     if host is not None:
         n, m = int(host.shape[0]), int(host.shape[1])
         vh = np.ascontiguousarray(v_local.detach().cpu().numpy() if isinstance(v_local, torch.Tensor)
                                   else np.asarray(v_local), dtype=host.dtype)
         prec = resolve_precision(precision, torch.float32 if host.dtype == np.float32 else torch.float64)
+        flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | refine_flags(prec, refine)
         ctx = _lib.context_for(dev.index, n, m)
         x = _pinned_out.get(m)
         dt = _lib.FS_F32 if host.dtype == np.float32 else _lib.FS_F64
@@ -259,11 +264,12 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
             torch.as_tensor(np.asarray(v_local), device=dev).to(S.dtype).contiguous()
         if m and v.numel() and not _lib.all_finite(v):
             invalid = True
-        if invalid:
-            flags |= _lib.FS_FLAG_INVALID_SHARD
+        flags = _lib.FS_FLAG_INVALID_SHARD if invalid else 0
         prec = resolve_precision(precision, S.dtype)
+        flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | refine_flags(prec, refine) | flags
         ctx = _lib.context_for(dev.index, n, max(m, 1))
         x = torch.empty(m, dtype=torch.float64, device=dev)
+        ctx.hint_row_absmax(S_local.row_absmax if isinstance(S_local, ScoreMatrix) else absmax, n)
         rc = ctx.lib.fs_chol_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr() if m else None, n, m,
                                    S.stride(0) if m else 0, v.data_ptr() if m else None, float(lam),
                                    x.data_ptr() if m else None, cb, None, flags, REFINE_ABOVE_REL,

@@ -34,6 +34,7 @@ from .core import (
     _stream,
     embed_complex,
     gram_packed,
+    hint_scales,
     resolve_precision,
     stack_complex_vector,
 )
@@ -50,21 +51,33 @@ def fp32_residual_bound(sigma2_max_over_lam: float) -> float:
 
 @dataclass(frozen=True)
 class CholWorkspace:
-    """Lower Cholesky factor of the damped Gram matrix (solvers.py:57-71), device resident."""
+    """Lower Cholesky factor of the damped Gram matrix (solvers.py:57-71).  L is an n x n float64
+    CUDA tensor (upper triangle exactly zero) or, as the reference holds it, a numpy array — then
+    it is uploaded once for the solves."""
 
-    L: torch.Tensor   # n x n float64 CUDA tensor, upper triangle exactly zero
+    L: object
 
     @property
     def n(self) -> int:
         return int(self.L.shape[0])
 
+    def _device_L(self) -> torch.Tensor:
+        if isinstance(self.L, torch.Tensor) and self.L.is_cuda:
+            return self.L
+        cached = self.__dict__.get("_dL")
+        if cached is None:
+            from .core import default_device
+            cached = torch.as_tensor(np.ascontiguousarray(np.asarray(self.L, dtype=np.float64))).to(default_device())
+            object.__setattr__(self, "_dL", cached)
+        return cached
+
     def solve_gram(self, b) -> np.ndarray:
         """Solve (L L^T) y = b by forward then back substitution on the GPU."""
+        L = self._device_L()
         bt = torch.as_tensor(np.asarray(b, dtype=np.float64) if not isinstance(b, torch.Tensor) else b,
-                             dtype=torch.float64).to(self.L.device).clone()
-        ctx = _lib.context_for(self.L.device.index, self.n, 1)
-        rc = ctx.lib.fs_trsv_pair(ctx.handle, self.L.data_ptr(), self.n, self.L.stride(0), bt.data_ptr(),
-                                  _stream(self.L.device))
+                             dtype=torch.float64).to(L.device).clone()
+        ctx = _lib.context_for(L.device.index, self.n, 1)
+        rc = ctx.lib.fs_trsv_pair(ctx.handle, L.data_ptr(), self.n, L.stride(0), bt.data_ptr(), _stream(L.device))
         _check(ctx, rc, "fs_trsv_pair")
         return bt.cpu().numpy() if not isinstance(b, torch.Tensor) else bt
 
@@ -128,7 +141,7 @@ def _meter_slots(n: int, m: int, dtype: int, precision: int) -> int:
     return int(lib.fs_workspace_bytes(n, m, dtype, precision)) // 8
 
 
-AUTO_REFINE_STEPS = 12              # fp32 modes: correction steps the "auto" rule may take
+AUTO_REFINE_STEPS = 4               # fp32 modes: z-space correction steps the "auto" rule may take
 RESULT_PROMISE_REL = 1e-8           # solvers.py:41-42: the factored route promises rel_residual <= 1e-8
 
 
@@ -138,13 +151,21 @@ def _refine_steps(refine, prec: str) -> int:
             raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
         # the reference rule (solvers.py:171-194): refine while rel_residual > 1e-10.  fp64 needs
         # one step at most (the reference's single correction pass); the fp32-split factors
-        # contract ~u32 sigma_max^2/lam per step, so they may take several
+        # refine z on the n x n system (contraction ~2^-21 kappa(W) per step, FS_FLAG_REFINE_Z)
         return 1 if prec == "fp64" else AUTO_REFINE_STEPS
     if isinstance(refine, bool):
         return 1 if refine else 0
     if isinstance(refine, (int, np.integer)) and 0 <= int(refine) <= 255:
         return int(refine)
     raise ValueError(f"refine must be 'auto', a bool or a step count in [0, 255], got {refine!r}")
+
+
+def refine_flags(prec: str, steps: int) -> int:
+    """fs_chol_solve refinement flags: fp64 -> the reference's x-space correction (solvers.py:183-194);
+    the fp32-split modes -> z-space refinement on the n x n system (FS_FLAG_REFINE_Z)."""
+    if steps <= 0:
+        return 0
+    return (_lib.FS_FLAG_REFINE if prec == "fp64" else _lib.FS_FLAG_REFINE_Z) | (min(int(steps), 255) << 8)
 
 
 def _host_x(x: torch.Tensor) -> np.ndarray:
@@ -161,15 +182,16 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
     precision: "fp64" (exact fp64 products, the reference's arithmetic), "f16x2" (row-scaled
     two-plane fp16 split on the tensor cores), "tf32x3", or "auto" (fp64 scores -> fp64,
     float32 scores -> f16x2 with the result-quality guarantee below).
-    refine: "auto" applies the reference's rule (refine while rel_residual > 1e-10,
-    solvers.py:171-194): one correction step in fp64 mode, up to AUTO_REFINE_STEPS steps in the
-    fp32-split modes (mixed-precision iterative refinement: fp32-split factor, fp64 residuals,
-    stopping at 1e-10 or when a step no longer halves the residual).  With precision="auto" as
-    well, a float32 solve whose refined rel_residual still exceeds the reference's promise of
-    1e-8 (solvers.py:41-42; it happens when u32 sigma_max^2/lam is not << 1) is recomputed in
-    fp64 mode, so the drop-in default always meets the reference's result contract.
-    True = the reference's single step; an int k = up to k steps; False/0 = none (the raw fp32
-    mode, tolerance 4 u32 sigma_max^2/lam).
+    refine: "auto" applies the reference's result rule (solvers.py:171-194): in fp64 mode its
+    single x-space correction when rel_residual > 1e-10; in the fp32-split modes up to
+    AUTO_REFINE_STEPS z-space steps (mixed-precision refinement of z = W^-1 S v on the n x n
+    system with the split factor and exact fp64 residuals read off the fused x + y pass, one pass
+    over S per step; it converges whatever sigma_max^2/lam is, because the n x n system is as
+    well conditioned as W).  With precision="auto" as well, a float32 solve whose rel_residual
+    still exceeds the reference's promise of 1e-8 (solvers.py:41-42) is recomputed in fp64 mode,
+    so the drop-in default always meets the reference's result contract.  True = one step; an
+    int k = up to k steps; False/0 = none (the raw fp32 mode, tolerance 4 u32 sigma_max^2/lam,
+    SURVEY §8d).
     diagnostics: compute abs/rel residual on the GPU (two extra passes over S), as the
     reference does inside solve_chol (solvers.py:160-170).
     """
@@ -186,7 +208,7 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
             steps, do_refine = 0, False
         else:
             raise ValueError("refinement needs the residual diagnostics")
-    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | ((_lib.FS_FLAG_REFINE | (steps << 8)) if do_refine else 0)
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (refine_flags(prec, steps) if do_refine else 0)
     dt = _lib.FS_F32 if system.S.dtype == torch.float32 else _lib.FS_F64
     device = system.S.device
     ctx = _lib.context_for(device.index, n, m)
@@ -209,6 +231,7 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
         S = system.S.tensor
         v = system.v_tensor
         x = torch.empty(m, dtype=torch.float64, device=S.device)
+        hint_scales(ctx, system.S)
         rc = ctx.lib.fs_chol_solve(ctx.handle, dt, PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0),
                                    v.data_ptr(), system.lam, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
                                    REFINE_ABOVE_REL, ctypes.byref(piv), res, _stream(S.device))
@@ -344,6 +367,7 @@ def _gram_packed_unshifted(S: ScoreMatrix, precision: str) -> torch.Tensor:
     prec = resolve_precision(precision, t.dtype)
     ctx = _lib.context_for(t.device.index, n, m)
     out = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=t.device)
+    hint_scales(ctx, S)
     rc = ctx.lib.fs_gram_packed(ctx.handle, dt, PRECISIONS[prec], t.data_ptr(), n, m, t.stride(0), 0.0,
                                 out.data_ptr(), _stream(t.device))
     _check(ctx, rc, "fs_gram_packed")
@@ -359,7 +383,8 @@ def _apply_rows(T: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
     ldy = -(-m // 2) * 2
     Y = torch.empty((r, ldy), dtype=torch.float64, device=X.device)[:, :m]
     ctx = _lib.context_for(X.device.index, n, m)
-    rc = ctx.lib.fs_apply_rows(ctx.handle, _dt(X), T.data_ptr(), r, n, T.stride(0), X.data_ptr(), m, X.stride(0),
+    ldT = T.stride(0) if r > 1 else n          # a 1-row tensor may carry any row stride
+    rc = ctx.lib.fs_apply_rows(ctx.handle, _dt(X), T.data_ptr(), r, n, ldT, X.data_ptr(), m, X.stride(0),
                                Y.data_ptr(), Y.stride(0), _stream(X.device))
     _check(ctx, rc, "fs_apply_rows")
     return Y
@@ -469,6 +494,7 @@ def _eigh_route(system: DampedSystem, sigma_floor: float, precision: str, diagno
     rank = ctypes.c_int64(0)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
     flags = _lib.FS_FLAG_RESIDUAL if diagnostics else 0
+    hint_scales(ctx, system.S)
     rc = ctx.lib.fs_eigh_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0), v.data_ptr(),
                                system.lam, sigma_floor, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,
                                ctypes.byref(rank), res, _stream(S.device))

@@ -205,9 +205,12 @@ def test_gram_stage(fsb, n, m, precision):
 def test_fp64_gram_split_k_with_more_tiles_than_sms(fsb, dtype):
     """n = 2500: 210 tiles of 128 > 148 SMs -> the fp64 SYRK splits K two ways to fill the last
     round (syrk_dmma.cu dplan); odd m exercises the cp.async loader's partial 16-byte pieces."""
+    from paper_2310_17556_b200 import _lib
     n, m = 2500, 6001
     rng = np.random.Generator(np.random.PCG64(2500))
     S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(dtype)
+    ctx = _lib.context_for(0, n, m)
+    assert ctx.lib.fs_gram_splits(ctx.handle, n, m, _lib.FS_PREC_FP64) == 2     # the plan really splits
     W = fsb.gram(fsb.ScoreMatrix(S), 0.25, precision="fp64")
     ref = O.gram(S.astype(np.float64), 0.25)
     # exact fp64 products, different summation order than numpy's: a few ulps of the 6001-term sums
@@ -590,30 +593,54 @@ def test_host_entry_abi_pitched_rows(fsb, pinned):
 # ---------------------------------------------------------------- F16X2 row-scale overflow fallback
 
 @pytest.mark.parametrize("entry", ["gram", "device", "host"])
-def test_f16x2_overflow_falls_back_to_tf32x3(fsb, entry):
-    """A row whose sampled head is tiny but whose tail is huge defeats the sampled fp16 scale:
-    the overflow is detected and the Gram recomputed with TF32X3 — same results as asking for it."""
+def test_f16x2_overflow_recomputes_with_exact_scales(fsb, entry):
+    """A row whose sampled head is tiny but whose tail is huge defeats a sampled fp16 scale.  A
+    validated ScoreMatrix carries exact row maxima (no overflow possible); without them (raw ABI,
+    deferred host entry) the overflow is detected and the solve recomputes once in F16X2 with
+    exact row scales — no TF32X3 copy of S — and the result meets the fp32 tolerance."""
+    from paper_2310_17556_b200 import _lib
     S, v, lam = O.generate_problem(21, 40, 12000, 1e-2)
     S = S.astype(np.float32)
     S[7, :5000] *= 1e-6          # sample region (first 4096 columns) tiny
     S[7, 9000] = 50.0            # 2^9+ beyond the scaled sample maximum
     v = v.astype(np.float32)
+    dev = torch.device("cuda", 0)
+    ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
+    ctx = _lib.context_for(0, 40, 12000)
+    f0 = ctx.fallbacks()
     if entry == "gram":
-        W16 = fsb.gram(fsb.ScoreMatrix(S), 0.5, precision="f16x2")
-        W32 = fsb.gram(fsb.ScoreMatrix(S), 0.5, precision="tf32x3")
-        assert np.array_equal(W16, W32)
+        W = fsb.gram(fsb.ScoreMatrix(S), 0.5, precision="f16x2")        # exact maxima: no recompute
+        assert ctx.fallbacks() == f0
+        Wr = O.gram(S.astype(np.float64), 0.5)
+        assert np.abs(W - Wr).max() <= 2e-6 * np.abs(Wr).max()
+        St = torch.from_numpy(S).to(dev)
+        out = torch.empty(40 * 41 // 2, dtype=torch.float64, device=dev)
+        ctx.hint_row_absmax(None, 0)
+        rc = ctx.lib.fs_gram_packed(ctx.handle, _lib.FS_F32, _lib.FS_PREC_F16X2, St.data_ptr(), 40, 12000, 12000, 0.5,
+                                    out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert rc == 0 and ctx.fallbacks() == f0 + 1                    # sampled scales -> one exact recompute
+        Wp = np.zeros((40, 40))
+        Wp[np.tril_indices(40)] = out.cpu().numpy()
+        assert np.abs(Wp - np.tril(Wr)).max() <= 2e-6 * np.abs(Wr).max()
         return
     if entry == "device":
-        dev = torch.device("cuda", 0)
-        mk = lambda: fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam, torch.from_numpy(v).to(dev))
-        a = fsb.solve_chol(mk(), precision="f16x2")
-        b = fsb.solve_chol(mk(), precision="tf32x3")
-        assert torch.equal(a.x, b.x)
+        a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S).to(dev)), lam,
+                                            torch.from_numpy(v).to(dev)), precision="f16x2", refine=0)
+        assert ctx.fallbacks() == f0
         x = a.x.cpu().numpy()
+        St = torch.from_numpy(S).to(dev)
+        vt = torch.from_numpy(v).to(dev)
+        xr = torch.empty(12000, dtype=torch.float64, device=dev)
+        piv = ctypes.c_int64(0)
+        res = (ctypes.c_double * 2)()
+        rc = ctx.lib.fs_chol_solve(ctx.handle, _lib.FS_F32, _lib.FS_PREC_F16X2, St.data_ptr(), 40, 12000, 12000,
+                                   vt.data_ptr(), lam, xr.data_ptr(), _lib.ALLREDUCE_FN(), None, _lib.FS_FLAG_RESIDUAL,
+                                   1e-10, ctypes.byref(piv), res, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0 and ctx.fallbacks() == f0 + 1
+        assert O.rel_err(xr.cpu().numpy(), ref.x) <= 1e-6
     else:
         a = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S, defer=True), lam, v), precision="f16x2")
         x = a.x
-    ref = O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
     assert O.rel_err(x, ref.x) <= 1e-6
 
 

@@ -72,8 +72,21 @@ def test_headline_drop_in_default_meets_reference_promise(fsb, headline):
     S32, v32, lam, ref = headline
     sol = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32))
     assert isinstance(sol.x, np.ndarray)
-    assert sol.rel_residual <= 1e-8, (sol.precision, sol.rel_residual)
-    assert O.rel_err(sol.x, ref.x) <= 1e-9, O.rel_err(sol.x, ref.x)
+    # z-space refinement on the f16x2 factor reaches the reference's own level (6e-11) without the
+    # fp64 Gram: sigma_max^2/lam ~ 1e6 does not slow it (the x-space scheme stalls here)
+    assert sol.precision == "f16x2"
+    assert sol.rel_residual <= 1e-10, (sol.precision, sol.rel_residual)
+    assert O.rel_err(sol.x, ref.x) <= 1e-13, O.rel_err(sol.x, ref.x)
+
+
+def test_z_refinement_contracts_per_step(fsb, headline):
+    """Each z-space step (TRSV pair + one fused pass) cuts rel_residual by >= 1e5 until the fp64
+    floor: 1.9e-2 -> ~1e-8 -> ~6e-11 at the headline."""
+    S32, v32, lam, ref = headline
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    rels = [fsb.solve_chol(system, precision="f16x2", refine=k).rel_residual for k in (0, 1, 2)]
+    assert rels[1] <= 1e-5 * rels[0] and rels[2] <= 1e-10, rels
 
 
 @pytest.mark.parametrize("n,m,precisions", [(8192, 100_000, ("f16x2",)), (1024, 3_000_000, ("f16x2", "tf32x3"))])
@@ -351,3 +364,29 @@ def test_solve_svd_direct_matches_oracle_and_tall(fsb):
     sol = fsb.solve_svd_direct(fsb.DampedSystem(fsb.ScoreMatrix(St), 0.1, vt))
     assert O.rel_err(sol.x, O.dense_solve(St, 0.1, vt)) <= 1e-10
     assert sol.rel_residual <= 1e-12
+
+
+# ---------------------------------------------------------------- exact F16X2 row scales (verdict r1 #7)
+
+def test_layer_structured_heavy_tailed_scores_need_no_recompute(fsb):
+    """Column blocks at scales 2^-10 ... 2^10 with Student-t(3) entries (real score matrices are
+    layer-structured with per-layer scales): the exact row maxima taken at validation leave no
+    fp16 overflow, so no solve is recomputed, and x meets the fp32 tolerance."""
+    from paper_2310_17556_b200 import _lib
+    rng = np.random.Generator(np.random.PCG64(77))
+    n, m, blocks = 256, 60000, 21
+    S = rng.standard_t(3, size=(n, m))
+    edges = np.linspace(0, m, blocks + 1).astype(int)
+    for b, e in enumerate(np.arange(-10, 11)):
+        S[:, edges[b]:edges[b + 1]] *= 2.0 ** e
+    S32 = (S / np.sqrt(n)).astype(np.float32)
+    v32 = rng.standard_normal(m).astype(np.float32)
+    lam = 1e-1
+    ref = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
+    ctx = _lib.context_for(0, n, m)
+    f0 = ctx.fallbacks()
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    sol = fsb.solve_chol(system, precision="f16x2", refine=0)
+    assert ctx.fallbacks() == f0
+    assert O.rel_err(sol.x.cpu().numpy(), ref.x) <= 1e-6, O.rel_err(sol.x.cpu().numpy(), ref.x)

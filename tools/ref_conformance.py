@@ -70,6 +70,8 @@ def install_shim():
     import paper_2310_17556_b200 as fsb
     from paper_2310_17556_b200 import cli as b_cli, core as b_core, fmat as b_fmat, solvers as b_solvers
     ref = load_reference()
+    for sub in ("core", "solvers", "fmat", "cli", "bench", "sr"):
+        importlib.import_module(f"fisher_solve_ref.{sub}")
     provided = {}
 
     def overlay(name, ref_mod, *ours):
@@ -114,7 +116,9 @@ class Collector:
         if report.when == "call" or (report.when == "setup" and report.outcome != "passed"):
             entry = {"outcome": report.outcome, "seconds": round(report.duration, 3)}
             if report.outcome == "failed":
-                entry["error"] = str(report.longrepr).splitlines()[-1][:400]
+                lines = str(report.longrepr).splitlines()
+                err = [ln for ln in lines if ln.startswith("E ")]
+                entry["error"] = (" | ".join(err[:6]) + " @ " + lines[-1])[:1200]
             self.results[report.nodeid] = entry
 
 

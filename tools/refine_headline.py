@@ -18,7 +18,7 @@ dev = torch.device("cuda", 0)
 system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
 for prec in ("f16x2", "tf32x3", "fp64"):
     out = []
-    for k in ((0, 1, 2, 3, 4, 6, 8, 12) if prec != "fp64" else (0, 1)):
+    for k in ((0, 1, 2, 3, 4) if prec != "fp64" else (0, 1)):
         fsb.solve_chol(system, precision=prec, refine=k)
         torch.cuda.synchronize()
         t = time.perf_counter()
