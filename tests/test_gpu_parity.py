@@ -203,14 +203,15 @@ def test_gram_stage(fsb, n, m, precision):
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_fp64_gram_split_k_with_more_tiles_than_sms(fsb, dtype):
-    """n = 2500: 210 tiles of 128 > 148 SMs -> the fp64 SYRK splits K two ways to fill the last
-    round (syrk_dmma.cu dplan); odd m exercises the cp.async loader's partial 16-byte pieces."""
+    """n = 2500: 210 tiles of 128 > 148 SMs -> the fp64 SYRK splits K to fill the last round
+    (syrk_dmma.cu dplan: 7 ways fill 1470 of 1480 SM slots); odd m exercises the cp.async
+    loader's partial 16-byte pieces."""
     from paper_2310_17556_b200 import _lib
     n, m = 2500, 6001
     rng = np.random.Generator(np.random.PCG64(2500))
     S = (rng.standard_normal((n, m)) / np.sqrt(n)).astype(dtype)
     ctx = _lib.context_for(0, n, m)
-    assert ctx.lib.fs_gram_splits(ctx.handle, n, m, _lib.FS_PREC_FP64) == 2     # the plan really splits
+    assert ctx.lib.fs_gram_splits(ctx.handle, n, m, _lib.FS_PREC_FP64) > 1     # the plan really splits
     W = fsb.gram(fsb.ScoreMatrix(S), 0.25, precision="fp64")
     ref = O.gram(S.astype(np.float64), 0.25)
     # exact fp64 products, different summation order than numpy's: a few ulps of the 6001-term sums
@@ -680,8 +681,8 @@ def test_host_solutions_stay_independent(fsb):
 @pytest.mark.parametrize("precision", ["f16x2", "tf32x3"])
 def test_iterative_refinement_contracts_in_fp32_modes(fsb, precision):
     """u32 sigma^2/lam ~ 0.02: each correction step (fp32-split factor, fp64 residual) contracts the
-    residual ~5x (tools/refine_probe.py: 1.4e-2 -> 1.5e-10 in 12 steps); x converges to the fp64
-    solve of the identical system."""
+    residual (z-space refinement with exact fp64 residuals: 1.4e-2 -> 1.2e-8 -> 8.5e-12, then the
+    1e-10 stop rule ends it); x converges to the fp64 solve of the identical system."""
     S, v, lam = O.generate_problem(41, 256, 65536, 1e-3)
     S32, v32 = S.astype(np.float32), v.astype(np.float32)
     system = fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)
@@ -691,7 +692,8 @@ def test_iterative_refinement_contracts_in_fp32_modes(fsb, precision):
         sol = fsb.solve_chol(system, precision=precision, refine=k)
         rels.append(sol.rel_residual)
         errs.append(O.rel_err(sol.x, ref.x))
-    assert rels[1] < 0.5 * rels[0] and rels[2] < 0.5 * rels[1] and rels[3] < rels[2], rels
+    assert rels[1] < 0.5 * rels[0] and rels[2] < 0.5 * rels[1] and rels[3] <= rels[2], rels
+    assert rels[2] <= 1e-10 or rels[3] < rels[2], rels     # converged, or still contracting
     assert rels[3] <= 1e-6, rels
     assert errs[3] <= 1e-11 and errs[3] < errs[0], errs
 
