@@ -53,6 +53,10 @@ struct fs_ctx {
   bool local_nonfinite = false;
   uint8_t* d_St = nullptr;      // tiled copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
+  // F16X2 ring SYRK (lazy): the L2-resident tile ring, its ready/freed counters, u partials
+  uint8_t* d_ring = nullptr;
+  int* d_ring_cnt = nullptr;
+  double* d_ring_upart = nullptr;
   // eigh comparison route (lazy): Jacobi workspace, U (n_max^2), w, scratch, info
   void* d_eig = nullptr;
   double* d_U = nullptr;
@@ -204,6 +208,26 @@ int ensure_tiles(fs_ctx* ctx, bool f16) {
   return FS_OK;
 }
 
+int ensure_ring(fs_ctx* ctx) {
+  if (ctx->d_ring) return FS_OK;
+  bool ok = cudaMalloc((void**)&ctx->d_ring, fs::syrk_ring_bytes()) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_ring_cnt, 2 * 74 * 16 * sizeof(int)) == cudaSuccess &&
+            cudaMalloc((void**)&ctx->d_ring_upart, fs::syrk_ring_upart_doubles(ctx->n_max) * sizeof(double)) ==
+                cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cudaFree(ctx->d_ring); cudaFree(ctx->d_ring_cnt); cudaFree(ctx->d_ring_upart);
+    ctx->d_ring = nullptr; ctx->d_ring_cnt = nullptr; ctx->d_ring_upart = nullptr;
+    return fail(ctx, FS_ENOMEM, "cannot allocate the F16X2 tile ring");
+  }
+  return FS_OK;
+}
+
+// F16X2 ring SYRK for this shape (FS_F16_RING=0 turns it off; FS_F16_DIRECT wins when set)
+bool use_ring(fs_ctx* ctx, const void* S, int64_t n, int64_t m, int64_t ldS) {
+  return fs::syrk_tc_supported(S, ldS) && fs::syrk_ring_ok(n, m, ctx->num_sms);
+}
+
 int ensure_eig(fs_ctx* ctx) {
   if (ctx->d_eig) return FS_OK;
   if (ctx->n_max > fs::syevj_max_n()) return fail(ctx, FS_EUNSUPPORTED, "eigh route supports n <= 8192");
@@ -306,9 +330,20 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     if (e == cudaSuccess)
       e = fs::syrk_f16_direct((const float*)S, ldS, n, m, ctx->d_scale, ctx->d_inv_scale, w32, ctx->d_ovf,
                               ctx->d_partials, u, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  } else if (use_tc == 2 && use_ring(ctx, S, n, m, ldS) && (rc = ensure_ring(ctx)) == FS_OK) {
+    // F16X2 ring: row scales, then ONE kernel splits S into the L2-resident tile ring, forms
+    // u = S w and the Gram from it (no S_t16 round trip through HBM)
+    e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
+    if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
+    if (e == cudaSuccess)
+      e = fs::syrk_f16_ring((const float*)S, ldS, n, m, ctx->d_scale, ctx->d_inv_scale, w32, ctx->d_ovf,
+                            ctx->d_ring_upart, u, lam, Gp, ctx->d_syrk_ws, ctx->d_ring, ctx->d_ring_cnt,
+                            ctx->num_sms, st, &l);
   } else if (use_tc == 2) {
     // F16X2: row scales from a sample, split planes (+ u = S w), kind::f16 SYRK.  The overflow
     // flag is checked by the caller at its next host synchronisation.
+    rc = FS_OK;   // (a failed ring allocation falls back to the pre-tiled planes)
     if ((rc = ensure_tiles(ctx, true))) return rc;
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
     if (e == cudaSuccess) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
@@ -752,6 +787,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   for (int i = 0; i < fs_ctx::kMaxMarks; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->d_St) cudaFree(ctx->d_St);
+  cudaFree(ctx->d_ring); cudaFree(ctx->d_ring_cnt); cudaFree(ctx->d_ring_upart);
   if (ctx->d_Sin) cudaFree(ctx->d_Sin);
   if (ctx->d_vin) cudaFree(ctx->d_vin);
   if (ctx->d_xin) cudaFree(ctx->d_xin);

@@ -33,6 +33,21 @@ template <> struct VecOf<double> { using V = double2; static constexpr int N = 2
 template <typename T> FS_DEVINL void vec_to_array(const float4& v, T* a) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
 template <typename T> FS_DEVINL void vec_to_array(const double2& v, T* a) { a[0] = v.x; a[1] = v.y; }
 
+// fp32 -> fp64, exact, on the integer + fp64 pipes instead of the XU pipe (F2F.F64.F32 paced the
+// fused x + y pass: ncu XU 63% busy).  Arithmetic shift right by 3 puts sign | exponent | mantissa
+// where an fp64 with exponent field e (bias 1023) wants them, the mask clears the sign copies, the
+// low word takes the last 3 mantissa bits; the double read is x * 2^-896 (denormal x included),
+// the multiply by 2^896 is exact.  fp32 inf/NaN (rejected by input validation) map to finite values.
+FS_DEVINL double f2d_alu(float x) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t hi = ((uint32_t)((int32_t)u >> 3)) & 0x8FFFFFFFu;
+  return __hiloint2double((int)hi, (int)(u << 29)) * 0x1p896;
+}
+// element e of a 4-float vector: 3 of 4 through the integer pipe, 1 through the XU pipe (balances
+// the two; the fp64 pipe takes the extra DMULs)
+template <typename T> FS_DEVINL double to_f64_mix(T x, int e) { return (double)x; }
+template <> FS_DEVINL double to_f64_mix<float>(float x, int e) { return (e & 3) == 3 ? (double)x : f2d_alu(x); }
+
 template <typename TS>
 constexpr int row_chunk_cols() { return kWarp * VecOf<TS>::N * kRowUnroll; }
 
@@ -441,7 +456,7 @@ cols_solve_y_kernel(const TS* __restrict__ S, int64_t n, int64_t m, int64_t ldS,
 // exchange buffer with st.async (the data and the peer's mbarrier complete_tx travel together);
 // every CTA adds the CL partials in rank order, so x is identical everywhere.  Software
 // pipeline, one CTA barrier per panel: iteration j
-//   warps 2-3  x of panel j-1 from the exchange (pushed an iteration ago, latency hidden)
+//   warps 2-3  (after the push below) x of panel j-1 from the exchange, pushed an iteration ago
 //   all warps  x-phase of panel j: partial column sums
 //   -- barrier --
 //   warps 0-1  sum the per-warp partials of panel j, push them to the cluster
@@ -464,11 +479,18 @@ constexpr int kCLMaxRows8 = 8 * kCLRows * kCLMaxV;   // n <= 2288 with 8-CTA clu
 constexpr int kCLMaxRows16 = 16 * kCLRows * kCLMaxV;  // n <= 4576 with 16-CTA (non-portable) clusters
 constexpr int kCLG = 3;                          // chunks per batch of shared loads (y group)
 constexpr int kCLXW = 7;                         // x-group warps (partial sums, exchange, x)
+// exchange buffers: x of panel j-1 is formed after panel j's push, so a peer may push panels
+// j+1 and j+2 before this CTA consumes j-1 (it cannot push j+3: that needs this CTA's push j+1)
+// exchange buffers: a peer's push of panel q needs its slot-set of q - R free, i.e. this CTA's push
+// of q - R, which needs this CTA's own y group past q - 2R — so the x partials of panel p (read
+// when this CTA's y group forms x of p) are safe from a peer's push of p + K for K >= 2R.  K per
+// cluster size; the slot-set count R is capped at (K - 1) / 2.
+__host__ __device__ constexpr int cl_xb(int CL) { return CL >= 16 ? 5 : 9; }
 constexpr int kCLYW = kCLCW - kCLXW;             // y-group warps (8)
 constexpr int kCLXThreads = kCLXW * kWarp;
 constexpr int kCLSets = 8;                       // max panel slot-sets in the ring
 __host__ __device__ constexpr size_t cl_fixed(int CL) {
-  return 2 * kCLXW * 64 * 8 + 2 * (CL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + 2) * 8;
+  return 2 * kCLXW * 64 * 8 + cl_xb(CL) * (CL + 1) * 64 * 8 + 2 * 64 * 8 + (2 * kCLSets + cl_xb(CL)) * 8;
 }
 // as many chunk slots as fit beside the fixed buffers in 227 KB (33 / 32 / 30 for CL = 4 / 8 / 16)
 __host__ __device__ constexpr int cl_slots(int CL) {
@@ -500,7 +522,9 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   constexpr int VN1 = 16 / (int)sizeof(TS);       // columns per 16-byte vector
   constexpr int CW = 16 * VN1;                    // columns per panel (256 bytes)
   constexpr int kSlots = cl_slots(CL);
-  constexpr int R = kSlots / NCH < kCLSets ? kSlots / NCH : kCLSets;   // slot-sets
+  constexpr int kCLXB = cl_xb(CL);                // exchange buffers
+  constexpr int R0 = kSlots / NCH < kCLSets ? kSlots / NCH : kCLSets;
+  constexpr int R = R0 < (kCLXB - 1) / 2 ? R0 : (kCLXB - 1) / 2;   // slot-sets
   constexpr int RPC = NCH * kCLRows;              // rows per CTA
   constexpr int RP = kCLRows / 2;                 // row pairs per chunk (one warp-wide load each)
   constexpr uint32_t kSetBytes = NCH * kCLChunk;
@@ -512,12 +536,12 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   extern __shared__ __align__(1024) unsigned char cl_raw[];
   unsigned char* ring = cl_raw + ((1024u - (ptx::smem_u32(cl_raw) & 1023u)) & 1023u);   // [R][NCH][7.5 KB]
   double* red = (double*)(ring + (size_t)kSlots * kCLChunk);       // [2][x warps][64]
-  double* xch = red + 2 * kCLXW * 64;                              // [2][CL][64] partial column sums
-  double* xo = xch + 2 * CL * 64;                                  // [2][64] old x (accumulate; from rank 0)
-  double* xs = xo + 2 * 64;                                        // [2][64]
+  double* xch = red + 2 * kCLXW * 64;                              // [kCLXB][CL][64] partial column sums
+  double* xo = xch + kCLXB * CL * 64;                              // [kCLXB][64] old x (accumulate; from rank 0)
+  double* xs = xo + kCLXB * 64;                                    // [2][64]
   uint64_t* full = (uint64_t*)(xs + 2 * 64);                       // [sets]
   uint64_t* empty = full + kCLSets;                                // [sets]
-  uint64_t* xbar = empty + kCLSets;                                // [2]
+  uint64_t* xbar = empty + kCLSets;                                // [kCLXB]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)ptx::cluster_ctarank();
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
@@ -526,8 +550,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   const int64_t np = panels > cid ? (panels - 1 - cid) / ncl + 1 : 0;
   if (tid == 0) {
     for (int s = 0; s < R; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], kCLYW); }
-    ptx::mbar_init(&xbar[0], 1);
-    ptx::mbar_init(&xbar[1], 1);
+    for (int b = 0; b < kCLXB; ++b) ptx::mbar_init(&xbar[b], 1);
     ptx::fence_mbar_init();
   }
   ptx::cluster_sync();                             // peers' exchange barriers exist before use
@@ -552,7 +575,9 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
     }
     __syncwarp();
   } else if (warp < kCLXW) {
-    // ---------------- x group: partial column sums, the cluster exchange, x ----------------
+    // ---------------- x group: partial column sums of panel j, pushed to the cluster ----------------
+    // (never waits on the exchange: the y group forms x, so the exchange latency overlaps the
+    // next panels' partial sums)
     // warp a owns row pairs a, a + 7, a + 14 of every chunk
     Zt zr[NCH][PA];
 #pragma unroll
@@ -563,102 +588,74 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         const int64_t row = row0 + k * kCLRows + 2 * rp + half;
         zr[k][p] = (!y_only && rp < RP && row < n) ? (Zt)z[row] : (Zt)0;
       }
-    // warps 2-3 form x of panel j-1 and load v (or x, y-only) one iteration ahead
-    const bool xw = tid >= 64 && tid < 64 + CW;
-    const int t = tid - 64;
-    double vnext = 0.0;
-    if (xw && np > 0) {
-      const int64_t c = cid * CW + t;
-      vnext = c < m ? (y_only ? x[c] : (double)v[c]) : 0.0;
-    }
     int setx = 0;
     uint32_t phx = 0;
-    for (int64_t j = 0; j <= np; ++j) {
+    for (int64_t j = 0; j < np && !y_only; ++j) {
       const int rb = (int)(j & 1);
-      if (j >= 1 && xw) {
-        const int64_t p = j - 1;                   // panel whose x is formed now
-        const int b = (int)(p & 1);
-        const int64_t c = (cid + p * ncl) * CW + t;
-        const double vc = vnext;
-        if (j < np) {
-          const int64_t cn = c + ncl * CW;
-          vnext = cn < m ? (y_only ? x[cn] : (double)v[cn]) : 0.0;
-        }
-        double xv = 0.0;
-        if (y_only) {
-          xv = vc;
-        } else {
-          ptx::mbar_wait(&xbar[b], (uint32_t)((p >> 1) & 1));
-          double sum = 0.0;
+      Zt acc[VN1];
 #pragma unroll
-          for (int r = 0; r < CL; ++r) sum += xch[(b * CL + r) * 64 + t];
-          if (c < m) {
-            xv = (vc - sum) / lam;     // true division: x = v / lam exactly when S = 0 (solvers.py:124-126)
-            // accumulate: the old x travels with rank 0's partials (read there before the push,
-            // so no rank can see rank 0's overwrite of x[c])
-            if (accumulate) xv = xo[b * 64 + t] + xv;
-            if (rank == 0) x[c] = xv;
-          }
-        }
-        if (p >= 2) ptx::named_bar_sync(4 + b, CW + kCLYW * kWarp);   // y group done with xs[b]
-        xs[b * 64 + t] = xv;
-        bar_arrive_n(2 + b, CW + kCLYW * kWarp);                   // xs[b] ready
-      }
-      if (j < np && !y_only) {
-        Zt acc[VN1];
+      for (int e = 0; e < VN1; ++e) acc[e] = 0;
+      ptx::mbar_wait(&full[setx], phx);
+      const unsigned char* src = ring + (size_t)setx * kSetBytes + off;
 #pragma unroll
-        for (int e = 0; e < VN1; ++e) acc[e] = 0;
-        ptx::mbar_wait(&full[setx], phx);
-        const unsigned char* src = ring + (size_t)setx * kSetBytes + off;
+      for (int k = 0; k < NCH; ++k) {
+        VT bv[PA];
 #pragma unroll
-        for (int k = 0; k < NCH; ++k) {
-          VT bv[PA];
+        for (int p = 0; p < PA; ++p)
+          if (warp + p * kCLXW < RP) bv[p] = *reinterpret_cast<const VT*>(src + k * kCLChunk + (warp + p * kCLXW) * 512);
 #pragma unroll
-          for (int p = 0; p < PA; ++p)
-            if (warp + p * kCLXW < RP) bv[p] = *reinterpret_cast<const VT*>(src + k * kCLChunk + (warp + p * kCLXW) * 512);
+        for (int p = 0; p < PA; ++p) {
+          if (warp + p * kCLXW < RP) {
+            TS a[VN1];
+            vec_to_array(bv[p], a);
 #pragma unroll
-          for (int p = 0; p < PA; ++p) {
-            if (warp + p * kCLXW < RP) {
-              TS a[VN1];
-              vec_to_array(bv[p], a);
-#pragma unroll
-              for (int e = 0; e < VN1; ++e) acc[e] = fma((Zt)a[e], zr[k][p], acc[e]);
+            for (int e = 0; e < VN1; ++e) {
+              if constexpr (sizeof(Zt) == 8) acc[e] = fma(to_f64_mix(a[e], e), zr[k][p], acc[e]);
+              else acc[e] = fma((Zt)a[e], zr[k][p], acc[e]);
             }
           }
         }
-        double* rw = red + rb * kCLXW * 64 + warp * 64;
-#pragma unroll
-        for (int e = 0; e < VN1; ++e) {
-          double d = (double)acc[e];
-          d += __shfl_xor_sync(0xffffffffu, d, 16);
-          if (lane < 16) rw[vq * VN1 + e] = d;
-        }
-        ptx::named_bar_sync(1, kCLXThreads);       // red[rb] holds panel j's per-warp partials
-        if (tid < CW) {                            // warps 0-1 push them to every CTA
-          double part = 0.0;
-#pragma unroll
-          for (int w = 0; w < kCLXW; ++w) part += red[(rb * kCLXW + w) * 64 + tid];
-          // the local barrier expects all CL partial vectors (a peer's complete_tx may land
-          // before this expect_tx: the phase cannot complete until this one arrival is made)
-          if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[rb], (CL + (accumulate ? 1 : 0)) * CW * 8);
-          const uint32_t mine = ptx::smem_u32(xch + (rb * CL + rank) * 64 + tid);
-          const uint32_t bar = ptx::smem_u32(&xbar[rb]);
-#pragma unroll
-          for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
-          if (accumulate && rank == 0) {
-            const int64_t c = (cid + j * ncl) * CW + tid;
-            const double xold = c < m ? x[c] : 0.0;
-            const uint32_t xa = ptx::smem_u32(xo + rb * 64 + tid);
-#pragma unroll
-            for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
-          }
-        }
-        if (++setx == R) { setx = 0; phx ^= 1; }
       }
+      double* rw = red + rb * kCLXW * 64 + warp * 64;
+#pragma unroll
+      for (int e = 0; e < VN1; ++e) {
+        double d = (double)acc[e];
+        d += __shfl_xor_sync(0xffffffffu, d, 16);
+        if (lane < 16) rw[vq * VN1 + e] = d;
+      }
+      ptx::named_bar_sync(1, kCLXThreads);         // red[rb] holds panel j's per-warp partials
+      if (tid < CW) {                              // warps 0-1 push them to every CTA
+        double part = 0.0;
+#pragma unroll
+        for (int w = 0; w < kCLXW; ++w) part += red[(rb * kCLXW + w) * 64 + tid];
+        // the local barrier expects all CL partial vectors (a peer's complete_tx may land
+        // before this expect_tx: the phase cannot complete until this one arrival is made)
+        const int xb = (int)(j % kCLXB);
+        if (tid == 0) ptx::mbar_arrive_expect_tx(&xbar[xb], (CL + (accumulate ? 1 : 0)) * CW * 8);
+        const uint32_t mine = ptx::smem_u32(xch + (xb * CL + rank) * 64 + tid);
+        const uint32_t bar = ptx::smem_u32(&xbar[xb]);
+#pragma unroll
+        for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
+        if (accumulate && rank == 0) {
+          const int64_t c = (cid + j * ncl) * CW + tid;
+          const double xold = c < m ? x[c] : 0.0;
+          const uint32_t xa = ptx::smem_u32(xo + xb * 64 + tid);
+#pragma unroll
+          for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
+        }
+      }
+      if (++setx == R) { setx = 0; phx ^= 1; }
     }
   } else {
-    // ---------------- y group: y += S_panel x_panel, releases the slot-set ----------------
+    // ---------------- y group: x of panel p from the exchange, then y += S_panel x_panel ----------------
     const int wb = warp - kCLXW;                   // warp b owns row pairs b, b + 8 of every chunk
+    const int ty = tid - kCLXThreads;              // 0 .. 255; ty < 64 forms x of column ty
+    const bool xw = ty < CW;
+    double vnext = 0.0;                            // v (or x, y-only) one panel ahead
+    if (xw && np > 0) {
+      const int64_t c = cid * CW + ty;
+      vnext = c < m ? (y_only ? x[c] : (double)v[c]) : 0.0;
+    }
     double yreg[NCH][PB];
 #pragma unroll
     for (int k = 0; k < NCH; ++k)
@@ -668,11 +665,36 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
     uint32_t phy = 0;
     for (int64_t p = 0; p < np; ++p) {
       const int b = (int)(p & 1);
-      ptx::named_bar_sync(2 + b, CW + kCLYW * kWarp);             // xs[b] holds x of panel p
+      if (xw) {
+        const int64_t c = (cid + p * ncl) * CW + ty;
+        const double vc = vnext;
+        if (p + 1 < np) {
+          const int64_t cn = c + ncl * CW;
+          vnext = cn < m ? (y_only ? x[cn] : (double)v[cn]) : 0.0;
+        }
+        double xv = 0.0;
+        if (y_only) {
+          xv = vc;
+        } else {
+          const int xb = (int)(p % kCLXB);
+          ptx::mbar_wait(&xbar[xb], (uint32_t)((p / kCLXB) & 1));
+          double sum = 0.0;
+#pragma unroll
+          for (int r = 0; r < CL; ++r) sum += xch[(xb * CL + r) * 64 + ty];
+          if (c < m) {
+            xv = (vc - sum) / lam;     // true division: x = v / lam exactly when S = 0 (solvers.py:124-126)
+            // accumulate: the old x travels with rank 0's partials (read there before the push,
+            // so no rank can see rank 0's overwrite of x[c])
+            if (accumulate) xv = xo[xb * 64 + ty] + xv;
+            if (rank == 0) x[c] = xv;
+          }
+        }
+        xs[b * 64 + ty] = xv;
+      }
+      ptx::named_bar_sync(2, kCLYW * kWarp);       // xs[b] holds x of panel p (xs[b] of p-2 fully read)
       double xv[VN1];
 #pragma unroll
       for (int e = 0; e < VN1; ++e) xv[e] = xs[b * 64 + vq * VN1 + e];
-      if (p + 2 < np) bar_arrive_n(4 + b, CW + kCLYW * kWarp);     // xs[b] may be rewritten
       ptx::mbar_wait(&full[sety], phy);            // (already complete: makes the TMA data visible here)
       const unsigned char* src = ring + (size_t)sety * kSetBytes + off;
 #pragma unroll
@@ -692,7 +714,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
               TS a[VN1];
               vec_to_array(bv[k][q], a);
 #pragma unroll
-              for (int e = 0; e < VN1; ++e) yreg[k0 + k][q] = fma((double)a[e], xv[e], yreg[k0 + k][q]);
+              for (int e = 0; e < VN1; ++e) yreg[k0 + k][q] = fma(to_f64_mix(a[e], e), xv[e], yreg[k0 + k][q]);
             }
       }
       __syncwarp();                                // the whole warp has consumed the slot-set
@@ -992,16 +1014,17 @@ cudaError_t cols_solve_y_t(const TS* S, int64_t n, int64_t m, int64_t ldS, const
   // n <= 4576: the cluster kernel (S read from HBM once, in 256-byte TMA rows); 4-CTA clusters up
   // to n = 1144, 8-CTA to 2288, 16-CTA (non-portable, when schedulable) above
   static const int cl_env = getenv("FS_CY_CL") ? atoi(getenv("FS_CY_CL")) : 1;
+  static const int cl_min = getenv("FS_CY_CLMIN") ? atoi(getenv("FS_CY_CLMIN")) : 4;   // experiments: force 8 / 16
   if (cl_env && n <= kCLMaxRows16 && (n <= kCLMaxRows8 || cl_max_active<TS, 16>(num_sms) >= 4)) {
     CUtensorMap smap;
     memset(&smap, 0, sizeof smap);
     if (make_tensor_map_2d(&smap, sizeof(TS) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                            S, (uint64_t)m, (uint64_t)n, (uint64_t)ldS * sizeof(TS), 256 / sizeof(TS), kCLRows) ==
         cudaSuccess)
-      return n <= kCLMaxRows4
+      return n <= kCLMaxRows4 && cl_min <= 4
                  ? cols_solve_y_cl_t<TS, 4>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
                                             st, launches, y_only)
-             : n <= kCLMaxRows8
+             : n <= kCLMaxRows8 && cl_min <= 8
                  ? cols_solve_y_cl_t<TS, 8>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y, num_sms,
                                             st, launches, y_only)
                  : cols_solve_y_cl_t<TS, 16>(smap, n, m, z, v, v_f64, lam, accumulate, x, ypart, ypart_rows, y,

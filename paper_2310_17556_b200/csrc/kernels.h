@@ -91,6 +91,19 @@ cudaError_t syrk_f16_direct(const float* S, int64_t ldS, int64_t n, int64_t m, c
                             const double* inv_scale, const float* v, int* flags, double* upart, double* u, double lam,
                             double* G_packed, double* ws, int num_sms, cudaStream_t st, int* launches,
                             int kb_begin = 0, int kb_end = -1, int accum = 0);
+// F16X2 "ring": fp32 S is split ONCE per element by the SYRK's own converter warps (each
+// (K-block, row block) tile by one CTA of its split group) into an L2-resident ring of
+// pre-swizzled hi/lo tiles (ring: syrk_ring_bytes(); counters: 2 * 74 * 16 ints), from which every
+// consumer bulk-copies as in the pre-tiled mode — no S_t16 copy in HBM and no separate retile
+// pass.  u (+)= S v (v may be null) through upart (syrk_ring_upart_doubles(n)).
+// cudaErrorNotSupported when the shape does not qualify (syrk_ring_ok).
+size_t syrk_ring_bytes();
+size_t syrk_ring_upart_doubles(int64_t n);
+bool syrk_ring_ok(int64_t n, int64_t m, int num_sms);
+cudaError_t syrk_f16_ring(const float* S, int64_t ldS, int64_t n, int64_t m, const float* scale,
+                          const double* inv_scale, const float* v, int* flags, double* upart, double* u, double lam,
+                          double* G_packed, double* ws, uint8_t* ring, int* counters, int num_sms, cudaStream_t st,
+                          int* launches, int kb_begin = 0, int kb_end = -1, int accum = 0);
 
 // ---- potrf.cu / trsv.cu (fp64 small dense factor + solves) ----
 cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W, int64_t ldW,
@@ -98,6 +111,7 @@ cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W
 // scratch = potrf_scratch_doubles(n) doubles; on return it starts with the inverted 64x64
 // diagonal blocks of L (Linv), which trsv_pair consumes
 int64_t potrf_scratch_doubles(int64_t n);
+int64_t potrf_trsv_flags_offset(int64_t n);   // doubles before trsv_pair's block flags in that scratch
 // u / z (optional): the TRSV pair z = L^-T L^-1 u fused into the factorisation's persistent
 // kernel (*solved = true when it ran; otherwise call trsv_pair)
 cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch,

@@ -1040,6 +1040,11 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 
 int64_t potrf_scratch_doubles(int64_t n) {
   const int64_t nb = (n + kNB - 1) / kNB;
+  return potrf_trsv_flags_offset(n) + nb /* trsv_pair's 2 nb block flags */;
+}
+
+int64_t potrf_trsv_flags_offset(int64_t n) {
+  const int64_t nb = (n + kNB - 1) / kNB;
   return nb * kNB * kNB /* Linv */ + 2 * n * kNB /* panels */ + 1 /* grid barrier words */ + 2 * n /* solve */ +
          (nb + 1) / 2 /* backward-solve block flags */;
 }

@@ -62,6 +62,7 @@ constexpr int kDrainBlocks = 2;           // 2 x 32 columns = 24 MMAs per draine
 constexpr int kFlushChunks = 64;
 constexpr int kPfDist = 8;                // K-blocks between an L2 prefetch and its bulk load
 constexpr int kRegsProducer = 56, kRegsConverter = 80, kRegsEpilogue = 184;
+constexpr int kRegsProducerRing = 48, kRegsConverterRing = 88;   // ring: the converters load 8 float4 per batch
 constexpr uint32_t kIdesc = ptx::idesc_tf32(2 * kBlk, kN);
 // F16X2 (tiles.cuh): a stage holds the hi+lo tiles of the A and B row blocks (4 x 16 KB), no
 // converter ring; kind::f16 MMAs (K = 16) on 64-column K-blocks
@@ -74,10 +75,31 @@ constexpr int kXBytes = kBlk * kTile16Cols * 4; // one 128 x 64 fp32 box: 32 KB
 template <bool kF16, bool kDirect = false> constexpr int raw_stages() { return kDirect ? 2 : kF16 ? 3 : kRaw; }
 template <bool kF16> constexpr int lo_stages() { return kF16 ? 0 : kLo; }
 template <bool kF16> constexpr int stage_bytes() { return kF16 ? 4 * kBoxBytes : kStageBytes; }
-template <bool kF16, bool kDirect = false> constexpr size_t smem_bytes() {
+// F16X2 ring (kRing): the SYRK's converter warps split fp32 S themselves, but each (K-block, row
+// block) tile ONCE for the whole grid, into an L2-resident ring of pre-swizzled hi/lo tiles that
+// every consuming CTA then bulk-copies exactly as in the pre-tiled mode (see syrk_f16_ring).
+constexpr int kRingMaxNb = 24;                  // row blocks (n <= 3072): the per-CTA u partials
+constexpr int kRingRowsPerBatch = 4;           // converter rows per load batch (8 spills at 88 registers)
+constexpr int kRingMaxDepth = 16;               // K-blocks per group's ring
+constexpr int kRingMaxSlots = 74 * kRingMaxDepth;   // P * R counters (P <= clusters <= 74)
+constexpr size_t kRingBytes = (size_t)48 << 20; // ring budget (L2 is 126 MB)
+template <bool kF16, bool kDirect = false, bool kRing = false> constexpr size_t smem_bytes() {
   return (size_t)(raw_stages<kF16, kDirect>() * stage_bytes<kF16>() + lo_stages<kF16>() * kStageBytes) +
-         (kDirect ? (size_t)kXS * kXBytes + 128 * 8 : 0) + 1024 + (kDirect ? 256 : 512);
+         (kDirect ? (size_t)kXS * kXBytes + 128 * 8 : 0) + (kRing ? (size_t)kRingMaxNb * kBlk * 8 : 0) + 1024 +
+         (kDirect ? 256 : 512);
 }
+struct RingArgs {          // F16X2 ring mode inputs
+  const float* S;          // fp32 scores (row-major, ldS)
+  int64_t ldS, m;
+  const float* v;          // u = S v partials (or null)
+  const float* scale;      // per-row power-of-two scales
+  int* flags;              // |= 1 non-finite input, |= 2 fp16 overflow
+  uint8_t* ring;           // [P][R][nbt] hi+lo tile pairs (32 KB each)
+  int* ready;              // [P][R] tiles converted into the slot (monotonic over rounds)
+  int* freed;              // [P][R] CTAs whose copy of the slot landed (monotonic)
+  double* upart;           // [P][2 tiles][n] per-CTA u partials
+  int R;                   // ring depth in K-blocks
+};
 struct DirectArgs {        // F16X2 direct mode inputs
   const float* v;          // u = S v partials for the diagonal pair tiles' units (or null)
   const float* scale;      // per-row power-of-two scales
@@ -162,12 +184,12 @@ struct Ring {  // stage index + mbarrier phase of a circular buffer
   FS_DEVINL void next(int depth) { if (++s == depth) { s = 0; ph ^= 1; } }
 };
 
-template <bool kF16, bool kDirect = false>
+template <bool kF16, bool kDirect = false, bool kRing = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, int tiles, int P, int KB, int KC, int D,
                double* __restrict__ accbuf, double* __restrict__ Gp, double lam, int direct, int dbg, int kb_base,
                int accum, const double* __restrict__ inv_scale, const __grid_constant__ CUtensorMap tmap, int sym,
-               const __grid_constant__ UnitMap um, int units, const DirectArgs da) {
+               const __grid_constant__ UnitMap um, int units, const DirectArgs da, const RingArgs ra) {
   constexpr int kRawS = raw_stages<kF16, kDirect>();
   constexpr int kLoS = lo_stages<kF16>();
   constexpr int kSB = stage_bytes<kF16>();
@@ -179,7 +201,8 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
   uint8_t* lo = smem + (size_t)kRawS * kSB;
   uint8_t* xraw = smem + (size_t)kRawS * kSB + (size_t)kLoS * kStageBytes;   // direct: fp32 box slots
   double* xu = reinterpret_cast<double*>(xraw + (kDirect ? (size_t)kXS * kXBytes : 0));   // [128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xu) + (kDirect ? 128 * 8 : 0));
+  double* xur = xu + (kDirect ? 128 : 0);                                                 // ring: [nbt][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xur + (kRing ? kRingMaxNb * kBlk : 0));
   uint64_t* full = bars;                 // local TMA -> local converters / relay   [kRawS]
   uint64_t* conv = full + kRawS;         // both CTAs' converters -> leader MMA     [kRawS]
   uint64_t* empty = conv + kRawS;        // MMA (multicast) -> each producer        [kRawS]
@@ -219,8 +242,56 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
   const int wg = warp >> 2;
 
   if (wg == 0) {
-    ptx::setmaxnreg_dec<kRegsProducer>();
-    if (kDirect && warp == 0 && lane == 0) {
+    if constexpr (kRing) ptx::setmaxnreg_dec<kRegsProducerRing>();
+    else ptx::setmaxnreg_dec<kRegsProducer>();
+    if (kRing && warp == 0 && lane == 0) {
+      // ====== ring producer: wait until the group's converters filled the slot, then the same
+      //        1-D bulk copies of pre-swizzled tiles as the pre-tiled mode ======
+      Ring rr;
+      const int u = cluster;                      // ring mode: one unit per cluster
+      if (u < units) {
+        int t, kb0, nk;
+        unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
+        const int q = unit_split(um, u, P, tiles, t);
+        int pp, qq; pair_of(tile0 + t, pp, qq);
+        const int blkA = 2 * pp + (int)crank, blkB = 2 * qq + (int)crank;
+        const bool diag = pp == qq;
+        const uint32_t bytes = (diag ? 1 : 2) * kBlkBytes;
+        const uint8_t* ringq = ra.ring + (size_t)q * ra.R * nbt * kBlkBytes;
+        const int* rdy = ra.ready + q * ra.R;
+        int slot = 0, round = 0;
+        for (int k = 0; k < nk; ++k) {
+          ptx::mbar_wait(&empty[rr.s], rr.ph ^ 1);
+          ptx::wait_ge(rdy + slot, nbt * (round + 1));
+          ptx::fence_proxy_async_global();
+          uint8_t* st = raw + (size_t)rr.s * kSB;
+          ptx::mbar_arrive_expect_tx(&full[rr.s], bytes);
+          ptx::bulk_load(st, ringq + ((size_t)slot * nbt + blkA) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          if (!diag) ptx::bulk_load(st + kBlkBytes, ringq + ((size_t)slot * nbt + blkB) * kBlkBytes, kBlkBytes, &full[rr.s]);
+          rr.next(kRawS);
+          if (++slot == ra.R) { slot = 0; ++round; }
+        }
+      }
+    } else if (kRing && warp == 2 && lane == 0) {
+      // ====== ring relay: own copy landed -> leader's conv barrier, and the slot is free for the
+      //        group's converters as far as this CTA is concerned ======
+      Ring rr;
+      const uint32_t conv0 = ptx::mapa(ptx::smem_u32(conv), 0);
+      const int u = cluster;
+      if (u < units) {
+        int t, kb0, nk;
+        unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
+        int* fre = ra.freed + unit_split(um, u, P, tiles, t) * ra.R;
+        int slot = 0;
+        for (int k = 0; k < nk; ++k) {
+          ptx::mbar_wait(&full[rr.s], rr.ph);
+          ptx::mbar_arrive_cluster(conv0 + rr.s * 8);
+          ptx::red_release_gpu_add(fre + slot, 1);
+          rr.next(kRawS);
+          if (++slot == ra.R) slot = 0;
+        }
+      }
+    } else if (kDirect && warp == 0 && lane == 0) {
       // ============ direct producer: fp32 boxes of S (own row blocks) -> raw slots ============
       ptx::tma_prefetch_desc(&tmap);
       Ring xr;
@@ -240,7 +311,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           }
         }
       }
-    } else if (!kDirect && warp == 0 && lane == 0) {
+    } else if (!kDirect && !kRing && warp == 0 && lane == 0) {
       // ============ bulk-copy producer (each CTA: its own pre-swizzled S_t tiles) ============
       Ring rr;
       for (int u = cluster; u < units; u += nclusters) {
@@ -497,6 +568,141 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
     const bool bad = !isfinite(xmax), ovf = !bad && amax >= 65520.f;
     const unsigned bb = __ballot_sync(0xffffffffu, bad), bo = __ballot_sync(0xffffffffu, ovf);
     if (lane == 0 && (bb | bo)) atomicOr(da.flags, (bb ? 1 : 0) | (bo ? 2 : 0));
+  } else if (wg == 1 && kRing) {
+    // ====== ring converters: the group's CTAs split its (K-block, row block) tiles round-robin
+    //        (item k * nbt + rb -> CTA (2 t + crank) of the 2 * tiles in the group) and write the
+    //        hi/lo planes (the retile16 arithmetic) into slot k % R of the group's L2-resident
+    //        ring; u = S v partials per row in shared memory (fp64, fixed order) ======
+    ptx::setmaxnreg_dec<kRegsConverterRing>();
+    const int ct = threadIdx.x - 128, cw = ct >> 5;
+    const int j = lane & 7, rl = lane >> 3;       // 16-byte chunk of the tile row, row in a 4-row group
+    for (int e = ct; e < nbt * kBlk; e += 128) xur[e] = 0.0;
+    bool bad = false, ovf = false;
+    const int u = cluster;
+    int q = 0, g = 0;
+    const int G = 2 * tiles;
+    ptx::named_bar_sync(1, 128);
+    if (u < units) {
+      int t, kb0, nk;
+      unit_decode(um, u, P, KC, KB, tiles, t, kb0, nk);
+      q = unit_split(um, u, P, tiles, t);
+      g = 2 * t + (int)crank;
+      uint8_t* ringq = ra.ring + (size_t)q * ra.R * nbt * kBlkBytes;
+      int* rdy = ra.ready + q * ra.R;
+      const int* fre = ra.freed + q * ra.R;
+      const uint64_t pol_first = ptx::policy_evict_first(), pol_last = ptx::policy_evict_last();
+      const bool vec = ((reinterpret_cast<uintptr_t>(ra.S) | (uintptr_t)(ra.ldS * 4)) & 15) == 0;
+      const int64_t total = (int64_t)nk * nbt;
+      // this thread's L2 prefetch of one 256-byte row piece of an upcoming tile
+      auto prefetch = [&](int64_t idx) {
+        if (idx >= total) return;
+        const int k = (int)(idx / nbt), rb = (int)(idx % nbt);
+        const int64_t row = (int64_t)rb * kBlk + ct, col = (int64_t)(kb_base + kb0 + k) * kTile16Cols;
+        if (row < n && vec && col + kTile16Cols <= ra.m)
+          ptx::bulk_prefetch_l2_hint(ra.S + row * ra.ldS + col, kTile16Cols * 4, pol_first);
+      };
+      int64_t it = (int64_t)g;
+      prefetch(it);
+      prefetch(it + G);
+      long long c_wait = 0, c_conv = 0, c_pub = 0;
+      const long long c_t0 = clock64();
+      for (; it < total; it += G) {
+        prefetch(it + 2 * G);
+        const int k = (int)(it / nbt), rb = (int)(it % nbt);
+        const int slot = k % ra.R, round = k / ra.R;
+        long long c0 = (dbg & 512) ? clock64() : 0;
+        if (round > 0 && ct == 0) ptx::wait_ge(fre + slot, G * round);   // every CTA copied round - 1 out
+        ptx::named_bar_sync(1, 128);
+        if (dbg & 512) { const long long c1 = clock64(); c_wait += c1 - c0; c0 = c1; }
+        uint8_t* tile = ringq + ((size_t)slot * nbt + rb) * kBlkBytes;
+        const int64_t c = (int64_t)(kb_base + kb0 + k) * kTile16Cols + j * 8;   // this lane's 8 columns
+        const bool fullc = vec && c + 8 <= ra.m;
+        float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f), w1 = w0;
+        if (ra.v) {
+          if (fullc) {
+            w0 = __ldg(reinterpret_cast<const float4*>(ra.v + c));
+            w1 = __ldg(reinterpret_cast<const float4*>(ra.v + c) + 1);
+          } else {
+            float a[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) a[e] = (c + e < ra.m) ? __ldg(ra.v + c + e) : 0.f;
+            w0 = make_float4(a[0], a[1], a[2], a[3]);
+            w1 = make_float4(a[4], a[5], a[6], a[7]);
+          }
+        }
+        constexpr int kRB = kRingRowsPerBatch;           // rows per thread per batch (all loads first)
+#pragma unroll 1
+        for (int h = 0; h < 8 / kRB; ++h) {
+          float4 buf[kRB][2];
+#pragma unroll
+          for (int b = 0; b < kRB; ++b) {
+            const int r = ((h * kRB + b) * 4 + cw) * 4 + rl;
+            const int64_t i = (int64_t)rb * kBlk + r;
+            const float* row = ra.S + i * ra.ldS + c;
+            if (i < n && fullc) {
+              buf[b][0] = ptx::ld_hint_f4(reinterpret_cast<const float4*>(row), pol_first);
+              buf[b][1] = ptx::ld_hint_f4(reinterpret_cast<const float4*>(row) + 1, pol_first);
+            } else {
+              float a[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) a[e] = (i < n && c + e < ra.m) ? __ldg(row + e) : 0.f;
+              buf[b][0] = make_float4(a[0], a[1], a[2], a[3]);
+              buf[b][1] = make_float4(a[4], a[5], a[6], a[7]);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < kRB; ++b) {
+            const int r = ((h * kRB + b) * 4 + cw) * 4 + rl;
+            const int64_t i = (int64_t)rb * kBlk + r;
+            const float sc = i < n ? __ldg(ra.scale + i) : 1.f;
+            const float xs[8] = {buf[b][0].x, buf[b][0].y, buf[b][0].z, buf[b][0].w,
+                                 buf[b][1].x, buf[b][1].y, buf[b][1].z, buf[b][1].w};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              bad |= !isfinite(xs[e]) || !isfinite(xs[e + 1]);
+              const float y0 = xs[e] * sc, y1 = xs[e + 1] * sc;
+              const __half2 h = __floats2half2_rn(y0, y1);
+              const float2 hf = __half22float2(h);
+              ovf |= isinf(hf.x) || isinf(hf.y);
+              const __half2 l = __floats2half2_rn(y0 - hf.x, y1 - hf.y);
+              hw[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const int off = r * 128 + ((j ^ (r & 7)) << 4);
+            ptx::st_evict_last(tile + off, make_uint4(hw[0], hw[1], hw[2], hw[3]), pol_last);
+            ptx::st_evict_last(tile + kBoxBytes + off, make_uint4(lw[0], lw[1], lw[2], lw[3]), pol_last);
+            if (ra.v) {
+              float p = 0.f;
+              p = fmaf(xs[0], w0.x, p); p = fmaf(xs[1], w0.y, p); p = fmaf(xs[2], w0.z, p); p = fmaf(xs[3], w0.w, p);
+              p = fmaf(xs[4], w1.x, p); p = fmaf(xs[5], w1.y, p); p = fmaf(xs[6], w1.z, p); p = fmaf(xs[7], w1.w, p);
+              p += __shfl_xor_sync(0xffffffffu, p, 1);   // the row's 8 lanes (64 columns)
+              p += __shfl_xor_sync(0xffffffffu, p, 2);
+              p += __shfl_xor_sync(0xffffffffu, p, 4);
+              if (j == 0) xur[rb * kBlk + r] += (double)p;
+            }
+          }
+        }
+        if (dbg & 512) { const long long c1 = clock64(); c_conv += c1 - c0; c0 = c1; }
+        if (!(dbg & 1024)) ptx::fence_proxy_async_global();   // generic writes -> the consumers' bulk copies
+        ptx::named_bar_sync(1, 128);
+        if (ct == 0) ptx::red_release_gpu_add(rdy + slot, 1);
+        if (dbg & 512) { const long long c1 = clock64(); c_pub += c1 - c0; }
+      }
+      if ((dbg & 512) && ct == 0 && cluster < 74 && crank == 0) {
+        g_conv_wait[cluster * 4 + 0] = c_wait;
+        g_conv_wait[cluster * 4 + 1] = c_conv;
+        g_conv_wait[cluster * 4 + 2] = c_pub;
+        g_conv_wait[cluster * 4 + 3] = clock64() - c_t0;
+      }
+    }
+    const unsigned bb = __ballot_sync(0xffffffffu, bad), bo = __ballot_sync(0xffffffffu, ovf);
+    if (lane == 0 && (bb | bo)) atomicOr(ra.flags, (bb ? 1 : 0) | (bo ? 2 : 0));
+    if (ra.v && u < units) {
+      ptx::named_bar_sync(1, 128);
+      double* up = ra.upart + ((size_t)q * G + g) * n;
+      for (int e = ct; e < n; e += 128) up[e] = xur[e];
+    }
   } else if (wg == 1 && kF16) {
     // ====== F16X2 relay: own TMA completion -> leader's conv barrier; on diagonal pair tiles
     //        (symmetric mode) the hi/2 plane is written into the stage's free half first ======
@@ -835,7 +1041,7 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
   }
   syrk_tc_kernel<kF16, kDirect><<<2 * clusters, kThreads, smem_bytes<kF16, kDirect>(), st>>>(
       St, n, (int)tiles_nb(n), p.tile0, p.tiles, p_arg, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
-      p.kb_base, accum, inv_scale, tmap, sym, um, units, da);
+      p.kb_base, accum, inv_scale, tmap, sym, um, units, da, RingArgs{});
   if (launches) *launches += 1;
   if (dbg & 256) {
     unsigned long long h[74 * 4] = {};
@@ -870,7 +1076,133 @@ cudaError_t syrk_launch(const uint8_t* St, int64_t n, int64_t m, double lam, dou
   }
   return cudaGetLastError();
 }
+// Clusters of the ring kernel that can be resident at once (its CTAs wait on one another's
+// conversions, so the whole grid must be co-resident); 0 on failure.
+int ring_max_clusters() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes<true, false, true>());
+  int nc = 0;
+  if (e == cudaSuccess) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(2 * 74);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_bytes<true, false, true>();
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    e = cudaOccupancyMaxActiveClusters(&nc, syrk_tc_kernel<true, false, true>, &cfg);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    nc = 0;
+  }
+  cached = nc;
+  return nc;
+}
+
+// Ring geometry for (n, m, K-range): plan with clusters capped at the co-resident count, one unit
+// per cluster (tile-major), ring depth R from the bytes available.  R = 0: the shape does not
+// qualify (too many pair tiles or row blocks, or too little ring memory).
+struct RingPlan {
+  Plan p;
+  int R;
+};
+RingPlan ring_plan(int64_t n, int64_t m, int num_sms, int kb_begin, int kb_end, size_t ring_bytes) {
+  RingPlan rp;
+  rp.R = 0;
+  const int mc = std::min(ring_max_clusters(), num_sms / 2);
+  rp.p = make_plan(n, m, 2 * std::max(mc, 1), 0, -1, kb_begin, kb_end, kTile16Cols);
+  const Plan& p = rp.p;
+  const int nbt = (int)tiles_nb(n);
+  if (mc < 1 || p.tiles > mc || p.tiles * p.P > mc || nbt > kRingMaxNb || p.KB <= 0) return rp;
+  const size_t per_round = (size_t)p.P * nbt * 2 * kBoxBytes;   // one K-block of every group
+  rp.R = (int)std::min<size_t>(kRingMaxDepth, ring_bytes / per_round);
+  if (rp.R < 4) rp.R = 0;
+  return rp;
+}
 }  // namespace
+
+size_t syrk_ring_bytes() { return kRingBytes; }
+size_t syrk_ring_upart_doubles(int64_t n) { return (size_t)148 * (size_t)std::min<int64_t>(n, kRingMaxNb * kBlk); }
+
+bool syrk_ring_ok(int64_t n, int64_t m, int num_sms) {
+  static const int env = getenv("FS_F16_RING") ? atoi(getenv("FS_F16_RING")) : 0;   // off: converter-bound (DESIGN K1)
+  if (!env) return false;
+  return ring_plan(n, m, num_sms, 0, -1, kRingBytes).R > 0;
+}
+
+cudaError_t syrk_f16_ring(const float* S, int64_t ldS, int64_t n, int64_t m, const float* scale,
+                          const double* inv_scale, const float* v, int* flags, double* upart, double* u, double lam,
+                          double* G_packed, double* ws, uint8_t* ring, int* counters, int num_sms, cudaStream_t st,
+                          int* launches, int kb_begin, int kb_end, int accum) {
+  if (!syrk_tc_supported(S, ldS)) return cudaErrorNotSupported;
+  RingPlan rp = ring_plan(n, m, num_sms, kb_begin, kb_end, kRingBytes);
+  if (rp.R == 0) return cudaErrorNotSupported;
+  const Plan& p = rp.p;
+  if (p.tiles <= 0 || p.KB <= 0) return cudaSuccess;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(syrk_tc_kernel<true, false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<true, false, true>());
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  static const int dbg = getenv("FS_SYRK_DBG") ? atoi(getenv("FS_SYRK_DBG")) : 0;
+  int* ready = counters;
+  int* freed = counters + kRingMaxSlots;
+  cudaError_t e = cudaMemsetAsync(counters, 0, 2 * kRingMaxSlots * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  UnitMap um;
+  memset(&um, 0, sizeof um);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  RingArgs ra{S, ldS, m, v, scale, flags, ring, ready, freed, upart, rp.R};
+  const int units = p.tiles * p.P;   // one per cluster, tile-major (P > 0)
+  syrk_tc_kernel<true, false, true><<<2 * units, kThreads, smem_bytes<true, false, true>(), st>>>(
+      nullptr, n, (int)tiles_nb(n), p.tile0, p.tiles, p.P, p.KB, p.KC, p.D, ws, G_packed, lam, p.direct ? 1 : 0, dbg,
+      p.kb_base, accum, inv_scale, tmap, 0, um, units, DirectArgs{}, ra);
+  if (launches) *launches += 1;
+  if (dbg & 256) {
+    unsigned long long h[74 * 4] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_syrk_wait, sizeof h);
+    double wd = 0, wt = 0, tot = 0, ns = 0;
+    int c = 0;
+    for (int i = 0; i < 74; ++i)
+      if (h[i * 4 + 3]) { wd += h[i * 4]; wt += h[i * 4 + 1]; tot += h[i * 4 + 2]; ns += h[i * 4 + 3]; ++c; }
+    if (c) fprintf(stderr, "ring syrk mma thread: wait operands %.0f%%, wait tmem %.0f%%, %.0f kcycles in %.3f ms -> %.0f MHz (%d clusters, R=%d)\n",
+                   100 * wd / tot, 100 * wt / tot, tot / c / 1e3, ns / c / 1e6, tot / ns * 1e3, c, rp.R);
+  }
+  if (dbg & 512) {
+    unsigned long long h[74 * 4] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_conv_wait, sizeof h);
+    double w = 0, c = 0, pb = 0, tot = 0;
+    for (int i = 0; i < 74; ++i)
+      if (h[i * 4 + 3]) { w += h[i * 4]; c += h[i * 4 + 1]; pb += h[i * 4 + 2]; tot += h[i * 4 + 3]; }
+    if (tot > 0)
+      fprintf(stderr, "ring converters (thread 0 of each leader): wait freed %.0f%%, load+convert+store %.0f%%, fence+publish %.0f%%, rest %.0f%%\n",
+              100 * w / tot, 100 * c / tot, 100 * pb / tot, 100 * (tot - w - c - pb) / tot);
+  }
+  if (!p.direct) {
+    syrk_tc_reduce<<<2 * p.tiles * kRedSplit, 256, 0, st>>>(ws, p.tile0, p.tiles, p.P, n, lam, G_packed, accum,
+                                                            inv_scale, 0, um);
+    if (launches) *launches += 1;
+  }
+  if (v && u) {
+    reduce_upart_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(upart, p.P * 2 * p.tiles, n, u, accum);
+    if (launches) *launches += 1;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t syrk_tc(const uint8_t* St, int64_t n, int64_t m, double lam, double* G_packed, double* ws, int num_sms,
                     cudaStream_t st, int* launches, int prow0, int prow1, int kb_begin, int kb_end, int accum) {

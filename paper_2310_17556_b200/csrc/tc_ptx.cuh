@@ -99,6 +99,64 @@ FS_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
                : "memory");
 }
 
+// ---------------- global-memory flags between CTAs (the F16X2 ring SYRK) ----------------
+FS_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FS_DEV void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// generic-proxy global writes <-> async-proxy (bulk copy) global reads
+FS_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+FS_DEV uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *p >= target (acquire); traps after ~20 s so a broken protocol fails loudly
+// instead of hanging the device
+FS_DEV void wait_ge(const int* p, int target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t ns = 32;
+  while (ld_acquire_gpu(p) < target) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if (globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
+// 16-byte store with an L2 evict_last hint (data re-read from L2 by other SMs soon)
+FS_DEV void st_evict_last(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(policy)
+               : "memory");
+}
+FS_DEV uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+FS_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// L2 prefetch of `bytes` (multiple of 16, 16-B aligned) with a cache policy
+FS_DEV void bulk_prefetch_l2_hint(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(reinterpret_cast<uint64_t>(src)),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
+FS_DEV float4 ld_hint_f4(const float4* p, uint64_t policy) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(policy));
+  return r;
+}
+
 // L2-only prefetch of a 2-D tile (no shared memory, no completion tracking).
 FS_DEV void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),

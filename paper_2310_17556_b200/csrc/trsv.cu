@@ -6,6 +6,8 @@
 // potrf already produced: each block step is an off-diagonal GEMV (coalesced row reads of L,
 // L2-resident) followed by a 64x64 GEMV with Linv_BB — no dependent global-load chains.
 // One CTA of 1024 threads; deterministic (fixed reduction order).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -84,11 +86,176 @@ trsv_pair_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const doub
   }
 }
 
+// Flag-chained variant: CTA B owns 64-row block B.  Forward: t_B = z_B - sum_{C<B} L_BC z'_C,
+// each term applied as soon as CTA C publishes z'_C (release/acquire flag), then
+// z'_B = Linv_BB t_B.  Backward: t_B = z'_B - sum_{C>B} L_CB^T z_C as the z_C are published,
+// z_B = Linv_BB^T t_B.  The off-diagonal products of all blocks run in parallel; the critical
+// path is one 64 x 64 GEMV + a flag hop per block and direction (the single-CTA kernel above
+// streams all of L through one SM twice: 258 us at n = 1024).  Fixed accumulation order
+// (C ascending / descending per thread): deterministic, identical z on every call.
+constexpr int kFT = 256;                       // threads per CTA (8 warps)
+constexpr int kFW = kFT / 32;
+
+FS_DEVINL int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FS_DEVINL void st_rel(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+FS_DEVINL void wait_flag(const int* p) {
+  if (threadIdx.x == 0)
+    while (ld_acq(p) == 0) __nanosleep(20);
+  __syncthreads();
+}
+
+constexpr int kSP = kNB + 1;                   // smem pitch (doubles) of the preloaded 64 x 64 blocks
+constexpr size_t kFlagSmem = 3 * (size_t)kNB * kSP * sizeof(double);
+
+__global__ void __launch_bounds__(kFT, 1)
+trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
+                      double* __restrict__ z, const int64_t* status, int* __restrict__ fflag, int* __restrict__ bflag) {
+  extern __shared__ double fsm[];
+  double* LI = fsm;                            // Linv_BB
+  double* LP = LI + kNB * kSP;                 // L_{B,B-1}: the forward step on the critical path
+  double* LN = LP + kNB * kSP;                 // L_{B+1,B}: the backward step on the critical path
+  __shared__ double t[kNB], zin[kNB];
+  __shared__ double part[kFW][kNB];
+  if (status && *(volatile const int64_t*)status != 0) return;   // uniform: every CTA returns
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (int)((n + kNB - 1) / kNB);
+  const int B = blockIdx.x;
+  const int64_t r0 = (int64_t)B * kNB;
+  const int b = (int)(n - r0 < kNB ? n - r0 : kNB);
+  const int bn = B + 1 < nb ? (int)(n - r0 - kNB < kNB ? n - r0 - kNB : kNB) : 0;   // rows of block B + 1
+  // the blocks the two critical-path steps need do not depend on z: load them before any wait
+  for (int e = threadIdx.x; e < kNB * kNB; e += kFT) {
+    const int r = e >> 6, c = e & 63;
+    LI[r * kSP + c] = Linv[(size_t)B * kNB * kNB + e];
+    LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
+    LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
+  }
+  __syncthreads();
+  // ---------------- forward: rows r = warp + 8 i of block B, columns lane, lane + 32 ----------------
+  double acc[kNB / kFW];
+#pragma unroll
+  for (int i = 0; i < kNB / kFW; ++i) acc[i] = 0.0;
+  for (int C = 0; C < B - 1; ++C) {            // off the critical path: streamed from L2 as published
+    wait_flag(fflag + C);
+    const int64_t c0 = (int64_t)C * kNB;
+    const double z0 = z[c0 + lane], z1 = z[c0 + lane + 32];
+#pragma unroll
+    for (int i = 0; i < kNB / kFW; ++i) {
+      const int r = warp + kFW * i;
+      if (r < b) {
+        const double* row = L + (r0 + r) * ld + c0;
+        acc[i] = fma(row[lane], z0, acc[i]);
+        acc[i] = fma(row[lane + 32], z1, acc[i]);
+      }
+    }
+  }
+  if (B > 0) {                                 // C = B - 1 from shared memory
+    wait_flag(fflag + B - 1);
+    if (threadIdx.x < kNB) zin[threadIdx.x] = z[r0 - kNB + threadIdx.x];
+    __syncthreads();
+    const double z0 = zin[lane], z1 = zin[lane + 32];
+#pragma unroll
+    for (int i = 0; i < kNB / kFW; ++i) {
+      const int r = warp + kFW * i;
+      acc[i] = fma(LP[r * kSP + lane], z0, acc[i]);
+      acc[i] = fma(LP[r * kSP + lane + 32], z1, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kNB / kFW; ++i) {
+    const double sum = warp_sum(acc[i]);
+    const int r = warp + kFW * i;
+    if (lane == 0) t[r] = (r < b) ? z[r0 + r] - sum : 0.0;
+  }
+  __syncthreads();
+  {                                            // z'_B = Linv_BB t  (4 threads per row)
+    const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
+    double sum = 0.0;
+    for (int c = q; c <= r; c += 4) sum = fma(LI[r * kSP + c], t[c], sum);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (q == 0 && r < b) z[r0 + r] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_rel(fflag + B, 1);
+  }
+  // ---------------- backward: columns lane, lane + 32 of block B, rows of block C by warp ----------------
+  double a0 = 0.0, a1 = 0.0;
+  for (int C = nb - 1; C > B + 1; --C) {
+    wait_flag(bflag + C);
+    const int64_t c0 = (int64_t)C * kNB;
+    const int bc = (int)(n - c0 < kNB ? n - c0 : kNB);
+    for (int r = warp; r < bc; r += kFW) {
+      const double zi = z[c0 + r];
+      const double* row = L + (c0 + r) * ld + r0;
+      if (lane < b) a0 = fma(row[lane], zi, a0);
+      if (lane + 32 < b) a1 = fma(row[lane + 32], zi, a1);
+    }
+  }
+  if (B + 1 < nb) {                            // C = B + 1 from shared memory
+    wait_flag(bflag + B + 1);
+    if (threadIdx.x < kNB) zin[threadIdx.x] = threadIdx.x < bn ? z[r0 + kNB + threadIdx.x] : 0.0;
+    __syncthreads();
+    for (int r = warp; r < bn; r += kFW) {
+      const double zi = zin[r];
+      a0 = fma(LN[r * kSP + lane], zi, a0);
+      a1 = fma(LN[r * kSP + lane + 32], zi, a1);
+    }
+  }
+  part[warp][lane] = a0;
+  part[warp][lane + 32] = a1;
+  __syncthreads();
+  if (threadIdx.x < kNB) {
+    const int c = threadIdx.x;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kFW; ++w) sum += part[w][c];
+    t[c] = (c < b) ? z[r0 + c] - sum : 0.0;
+  }
+  __syncthreads();
+  {                                            // z_B = Linv_BB^T t
+    const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+    double sum = 0.0;
+    for (int r = c + q; r < kNB; r += 4) sum = fma(LI[r * kSP + c], t[r], sum);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (q == 0 && c < b) z[r0 + c] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_rel(bflag + B, 1);
+  }
+}
+
 }  // namespace
 
 cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
                       const int64_t* d_status, cudaStream_t st, int* launches) {
-  trsv_pair_kernel<<<1, kThreads, 0, st>>>(L, n, ldL, Linv, z, d_status);
+  const int64_t nb = (n + kNB - 1) / kNB;
+  static const int env = getenv("FS_TRSV_FLAGS") ? atoi(getenv("FS_TRSV_FLAGS")) : 1;
+  // every block's CTA must be resident while earlier ones spin on its flags: nb <= 148 CTAs of
+  // 256 threads always fit beside each other (Linv is the potrf scratch, flags sit at its end)
+  if (env && nb >= 2 && nb <= 148) {
+    int* flags = reinterpret_cast<int*>(const_cast<double*>(Linv) + potrf_trsv_flags_offset(n));
+    cudaError_t e = cudaMemsetAsync(flags, 0, 2 * nb * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(trsv_pair_flag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlagSmem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    trsv_pair_flag_kernel<<<(unsigned)nb, kFT, kFlagSmem, st>>>(L, n, ldL, Linv, z, d_status, flags, flags + nb);
+  } else {
+    trsv_pair_kernel<<<1, kThreads, 0, st>>>(L, n, ldL, Linv, z, d_status);
+  }
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
