@@ -193,8 +193,17 @@ int resolve_precision(fs_ctx* ctx, int dtype, int precision, const void* S, int6
 // (F16X2: two fp16 planes, 4 bytes per score; TF32X3: two tf32 planes, 8 bytes) and allocated on
 // first use — fp64-only users never pay for it, and an F16X2 user at the per-rank shard of
 // n = 16384, m = 1e7 / 8 (82 GB of scores) is not charged the 164 GB TF32X3 layout.
+// The tiled copy is capped at tile_cap_bytes() (16 GB): a larger (n, m) is split into K-chunks that each
+// fit (retile a column range, SYRK its K-blocks, accumulate), so an F16X2 solve needs S plus at
+// most 16 GB (n = 16384, m = 2e6: 131 GB of scores, one B200).
+size_t tile_cap_bytes() {   // FS_TILE_CAP_MB overrides (tests force the K-chunked path with it)
+  static const size_t cap = getenv("FS_TILE_CAP_MB") ? (size_t)atoll(getenv("FS_TILE_CAP_MB")) << 20
+                                                     : (size_t)16 << 30;
+  return cap;
+}
 int ensure_tiles(fs_ctx* ctx, bool f16) {
-  const size_t need = f16 ? fs::tiles16_bytes(ctx->n_max, ctx->m_max) : fs::tiles_bytes(ctx->n_max, ctx->m_max);
+  const size_t need = std::min(tile_cap_bytes(), f16 ? fs::tiles16_bytes(ctx->n_max, ctx->m_max)
+                                                  : fs::tiles_bytes(ctx->n_max, ctx->m_max));
   if (ctx->St_bytes >= need) return FS_OK;
   if (ctx->d_St) cudaFree(ctx->d_St);
   ctx->d_St = nullptr;
@@ -340,11 +349,10 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
       e = fs::syrk_f16_ring((const float*)S, ldS, n, m, ctx->d_scale, ctx->d_inv_scale, w32, ctx->d_ovf,
                             ctx->d_ring_upart, u, lam, Gp, ctx->d_syrk_ws, ctx->d_ring, ctx->d_ring_cnt,
                             ctx->num_sms, st, &l);
-  } else if (use_tc == 2) {
-    // F16X2: row scales from a sample, split planes (+ u = S w), kind::f16 SYRK.  The overflow
-    // flag is checked by the caller at its next host synchronisation.
-    rc = FS_OK;   // (a failed ring allocation falls back to the pre-tiled planes)
-    if ((rc = ensure_tiles(ctx, true))) return rc;
+  } else if (use_tc == 2 && ((rc = FS_OK), true) && (rc = ensure_tiles(ctx, true)) == FS_OK &&
+             fs::tiles16_bytes(n, m) <= ctx->St_bytes) {
+    // F16X2: row scales, split planes (+ u = S w), kind::f16 SYRK.  The overflow flag is checked
+    // by the caller at its next host synchronisation.  (A failed ring allocation falls back here.)
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
     if (e == cudaSuccess) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
     if (e == cudaSuccess)
@@ -354,11 +362,41 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
     if (e == cudaSuccess)
       e = fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
-  } else if (use_tc) {
-    if ((rc = ensure_tiles(ctx, false))) return rc;
-    e = fs::gemv_rows_retile((const float*)S, n, m, ldS, w32, ctx->d_partials, u, ctx->d_St, st, &l);
+  } else if (use_tc && !rc && (rc = ensure_tiles(ctx, use_tc == 2)) == FS_OK) {
+    // K-chunked: the tiled copy of all of S would exceed the cap.  Each chunk of K-blocks is
+    // retiled into the same buffer (addressed through a base shifted by the chunk's first
+    // K-block, so the kernels' absolute tile offsets land in it), its SYRK share accumulated
+    // into Gp (lam added once); stream order keeps a chunk's SYRK ahead of the next retile.
+    const bool f16 = use_tc == 2;
+    const int64_t nb = fs::tiles_nb(n), tile_cols = f16 ? fs::kTile16Cols : fs::kTileCols;
+    const size_t kb_bytes = (size_t)nb * (f16 ? 2 : 1) * fs::kTileBytes;
+    const int64_t KB = (m + tile_cols - 1) / tile_cols;
+    const int64_t align = fs::gemv_rows_chunk_cols() / tile_cols;   // column chunks of the u partials
+    const int64_t kbc = (int64_t)(ctx->St_bytes / kb_bytes) / align * align;
+    if (kbc < align) return fail(ctx, FS_ENOMEM, "tiled copy too small for one K-chunk");
+    e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
+    if (e == cudaSuccess && f16) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
+    for (int64_t kb0 = 0; kb0 < KB && e == cudaSuccess; kb0 += kbc) {
+      const int64_t kb1 = std::min(KB, kb0 + kbc), c0 = kb0 * tile_cols, c1 = std::min(m, kb1 * tile_cols);
+      uint8_t* base = ctx->d_St - (ptrdiff_t)(kb0 * (int64_t)kb_bytes);
+      const double lam_c = kb0 == 0 ? lam : 0.0;
+      if (f16) {
+        e = fs::retile16_cols((const float*)S, n, m, ldS, w32, ctx->d_partials, base, ctx->d_scale, c0, c1,
+                              ctx->d_ovf, st, &l);
+        if (e == cudaSuccess)
+          e = fs::syrk_f16(base, n, m, ctx->d_inv_scale, lam_c, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l, (int)kb0,
+                           (int)kb1, kb0 > 0);
+      } else {
+        e = fs::retile_cols((const float*)S, n, m, ldS, w32, ctx->d_partials, base, c0, c1, ctx->d_ovf, st, &l);
+        if (e == cudaSuccess)
+          e = fs::syrk_tc(base, n, m, lam_c, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1, (int)kb0, (int)kb1,
+                          kb0 > 0);
+      }
+    }
+    if (e == cudaSuccess && w32) e = fs::reduce_row_partials(ctx->d_partials, n, m, u, st, &l);
     if (e == cudaSuccess && w32) prof_mark(ctx, FS_PROF_GEMV_SV, st);
-    if (e == cudaSuccess) e = fs::syrk_tc(ctx->d_St, n, m, lam, Gp, ctx->d_syrk_ws, ctx->num_sms, st, &l);
+  } else if (use_tc) {
+    return rc;
   } else {
     e = fs::syrk_dmma(dtype == FS_F64, S, n, m, ldS, lam, Gp, ctx->d_syrk_ws, ctx->syrk_bytes, ctx->num_sms, st, &l);
   }
@@ -1143,6 +1181,15 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
     for (int64_t c0 = 0, c1 = 0; c0 < m && !ctx->poison_rc; c0 = c1, ++c) {
       c1 = std::min(m, c0 + (c + 1 < fs_ctx::kMaxChunks ? next_width(m - c0) : m - c0));
       FS_CKS(upload(c0, c1, c % fs_ctx::kMaxChunks), "S h2d");
+      // the chunk's tiles at the start of the (capped) tiled copy: a base shifted by its first
+      // K-block keeps the kernels' absolute offsets; stream order keeps chunk c's SYRK ahead of
+      // chunk c+1's retile
+      const int64_t tcols = use_tc == 2 ? fs::kTile16Cols : fs::kTileCols;
+      const size_t kbb = (size_t)fs::tiles_nb(n) * (use_tc == 2 ? 2 : 1) * fs::kTileBytes;
+      uint8_t* St_c = ctx->d_St ? ctx->d_St - (ptrdiff_t)((c0 / tcols) * (int64_t)kbb) : nullptr;
+      if (!direct && (size_t)((c1 - c0 + tcols - 1) / tcols + 1) * kbb > ctx->St_bytes)
+        FS_STEP(fail(ctx, FS_ENOMEM, "a host-entry K-chunk exceeds the tiled copy"));
+      if (ctx->poison_rc) break;
       if (use_tc == 2 && direct) {
         // F16X2 direct: row scales from the first chunk's columns, then the K-range SYRK splits the
         // chunk in-kernel and accumulates u = S v
@@ -1157,18 +1204,18 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
         // F16X2: row scales from the first chunk's columns, then split planes + K-range SYRK
         if (c == 0)
           FS_CKS(fs::row_scales((const float*)S, n, m, ldd, ctx->d_scale, ctx->d_inv_scale, st, &l, c1), "scales");
-        FS_CKS(fs::retile16_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St,
+        FS_CKS(fs::retile16_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, St_c,
                                 ctx->d_scale, c0, c1, ctx->d_flag, st, &l),
               "retile16");
-        FS_CKS(fs::syrk_f16(ctx->d_St, n, m, ctx->d_inv_scale, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st,
+        FS_CKS(fs::syrk_f16(St_c, n, m, ctx->d_inv_scale, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st,
                            &l, (int)(c0 / fs::kTile16Cols), (int)((c1 + fs::kTile16Cols - 1) / fs::kTile16Cols),
                            c > 0),
               "syrk_f16");
       } else {
-        FS_CKS(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, ctx->d_St, c0, c1,
+        FS_CKS(fs::retile_cols((const float*)S, n, m, ldd, (const float*)v, ctx->d_partials, St_c, c0, c1,
                               ctx->d_flag, st, &l),
               "retile");
-        FS_CKS(fs::syrk_tc(ctx->d_St, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
+        FS_CKS(fs::syrk_tc(St_c, n, m, 0.0, ctx->d_packed, ctx->d_syrk_ws, ctx->num_sms, st, &l, 0, -1,
                           (int)(c0 / fs::kTileCols), (int)((c1 + fs::kTileCols - 1) / fs::kTileCols), c > 0),
               "syrk_tc");
       }

@@ -632,7 +632,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         }
         constexpr int kRB = kRingRowsPerBatch;           // rows per thread per batch (all loads first)
 #pragma unroll 1
-        for (int h = 0; h < 8 / kRB; ++h) {
+        for (int h = 0; h < ((dbg & 2048) ? 0 : 8 / kRB); ++h) {   // dbg 2048: publish without converting
           float4 buf[kRB][2];
 #pragma unroll
           for (int b = 0; b < kRB; ++b) {

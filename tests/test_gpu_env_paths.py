@@ -1,0 +1,108 @@
+"""GPU parity of the code paths that environment switches select (each case runs in a fresh
+process, because the switches are read once per process):
+
+  FS_TILE_CAP_MB  caps the tiled copy of S -> the K-chunked Gram (retile a column range, SYRK its
+                  K-blocks, accumulate), the path that lets n = 16384, m = 2e6 fit on one B200
+  FS_F16_RING=1   the F16X2 ring SYRK (each tile split once into an L2-resident ring)
+  FS_TRSV_FLAGS=0 the single-CTA TRSV pair instead of the flag-chained one
+
+Tolerances: fp32 modes relerr(x) <= 1e-6 vs the reference's fp64 solve of the same
+fp32-rounded system; the chunked Gram vs the one-shot Gram <= 2e-6 of max |G| (the same split
+products, but each chunk's split-K plan groups the tensor core's fp32 accumulation differently).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fisher_oracle as O
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASE = r'''
+import sys, json, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2310_17556_b200 as fsb
+from oracle import fisher_oracle as O
+n, m, prec, entry, refine = {n}, {m}, {prec!r}, {entry!r}, {refine!r}
+S, v, lam = O.generate_problem(7, n, m, 1e-3)
+S32, v32 = S.astype(np.float32), v.astype(np.float32)
+if entry == "device":
+    sm = fsb.ScoreMatrix(torch.from_numpy(S32).cuda())
+    system = fsb.DampedSystem(sm, lam, torch.from_numpy(v32).cuda())
+    G = fsb.gram_packed(sm, lam, precision=prec).cpu().numpy()
+else:
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S32, defer=True), lam, v32)
+    G = np.zeros(1)
+sol = fsb.solve_chol(system, precision=prec, refine=refine)
+x = sol.x.cpu().numpy() if hasattr(sol.x, "cpu") else np.asarray(sol.x)
+np.savez({out!r}, x=x, G=G)
+print(json.dumps({{"rel_residual": float(sol.rel_residual)}}))
+'''
+
+
+def run_case(tmp_path, env, n, m, prec, entry="device", refine=0):
+    out = str(tmp_path / f"case_{abs(hash((tuple(sorted(env.items())), n, m, prec, entry)))}.npz")
+    code = CASE.format(root=ROOT, n=n, m=m, prec=prec, entry=entry, refine=refine, out=out)
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    info = json.loads(r.stdout.strip().splitlines()[-1])
+    d = np.load(out)
+    return d["x"], d["G"], info
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+
+
+def reference(n, m):
+    S, v, lam = O.generate_problem(7, n, m, 1e-3)
+    S64, v64 = S.astype(np.float32).astype(np.float64), v.astype(np.float32).astype(np.float64)
+    return O.solve_chol(S64, v64, lam)
+
+
+@pytest.mark.parametrize("prec", ["f16x2", "tf32x3"])
+@pytest.mark.parametrize("n,m", [(300, 70001), (1024, 50000)])
+def test_k_chunked_gram_matches_one_shot_and_oracle(gpu, tmp_path, prec, n, m):
+    # a 6 MB cap: the planes of (n, m) need ~n m 4 bytes, so the Gram runs in many K-chunks
+    x1, G1, _ = run_case(tmp_path, {}, n, m, prec)
+    x2, G2, _ = run_case(tmp_path, {"FS_TILE_CAP_MB": "6"}, n, m, prec)
+    assert np.abs(G2 - G1).max() <= 2e-6 * np.abs(G1).max()
+    ref = reference(n, m)
+    assert O.rel_err(x2, ref.x) <= 1e-6
+    assert O.rel_err(x1, ref.x) <= 1e-6
+
+
+@pytest.mark.parametrize("prec", ["f16x2", "tf32x3"])
+def test_k_chunked_host_entry(gpu, tmp_path, prec):
+    n, m = 512, 90001
+    # planes of all of S: 184 MB > the 64 MB cap; the host entry's ~32 MB upload chunks fit
+    x, _, info = run_case(tmp_path, {"FS_TILE_CAP_MB": "64"}, n, m, prec, entry="host")
+    assert O.rel_err(x, reference(n, m).x) <= 1e-6
+
+
+@pytest.mark.parametrize("n,m", [(128, 70000), (300, 65573), (1024, 100000), (2048, 40000)])
+def test_ring_syrk_gram_is_bit_identical_and_solves(gpu, tmp_path, n, m):
+    x1, G1, _ = run_case(tmp_path, {"FS_F16_RING": "0"}, n, m, "f16x2")
+    x2, G2, _ = run_case(tmp_path, {"FS_F16_RING": "1"}, n, m, "f16x2")
+    assert np.array_equal(G1, G2)          # same tiles, same MMA order: bit-identical Gram
+    assert O.rel_err(x2, reference(n, m).x) <= 1e-6
+
+
+def test_single_cta_trsv_pair_matches_flag_chained(gpu, tmp_path):
+    n, m = 1000, 60000
+    x1, _, i1 = run_case(tmp_path, {"FS_TRSV_FLAGS": "0"}, n, m, "f16x2", refine=2)
+    x2, _, i2 = run_case(tmp_path, {"FS_TRSV_FLAGS": "1"}, n, m, "f16x2", refine=2)
+    ref = reference(n, m)
+    assert O.rel_err(x1, ref.x) <= 1e-10 and O.rel_err(x2, ref.x) <= 1e-10
+    assert i2["rel_residual"] <= 1e-10
