@@ -524,7 +524,11 @@ static int solve_tail(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t 
     // L = chol(W) with the TRSV pair z = L^-T L^-1 u fused into the same persistent kernel
     FS_CKS(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "potrf status reset");
     int l = 0;
-    if (!ctx->poison_rc) FS_CKS(fs::potrf_lower(ctx->d_W, n, n, ctx->d_status, ctx->d_potrf, st, &l, u, ctx->d_z, &solved),
+    // the TRSV pair rides along inside the factorisation kernel up to FS_POTRF_FUSE_MAXN; above
+    // it the flag-chained TRSV kernel is faster than the fused grid-barrier steps
+    static const int64_t fuse_maxn = getenv("FS_POTRF_FUSE_MAXN") ? atoll(getenv("FS_POTRF_FUSE_MAXN")) : 4096;
+    const double* u_fused = n <= fuse_maxn ? u : nullptr;
+    if (!ctx->poison_rc) FS_CKS(fs::potrf_lower(ctx->d_W, n, n, ctx->d_status, ctx->d_potrf, st, &l, u_fused, ctx->d_z, &solved),
                                 "potrf");
     ctx->launches += l;
   }

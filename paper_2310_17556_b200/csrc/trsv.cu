@@ -240,9 +240,21 @@ cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Lin
                       const int64_t* d_status, cudaStream_t st, int* launches) {
   const int64_t nb = (n + kNB - 1) / kNB;
   static const int env = getenv("FS_TRSV_FLAGS") ? atoi(getenv("FS_TRSV_FLAGS")) : 1;
-  // every block's CTA must be resident while earlier ones spin on its flags: nb <= 148 CTAs of
-  // 256 threads always fit beside each other (Linv is the potrf scratch, flags sit at its end)
-  if (env && nb >= 2 && nb <= 148) {
+  // every block's CTA must be resident while earlier ones spin on its flags: nb <= (CTAs per SM)
+  // x SMs (2 per SM: ~100 KB of shared memory each; n <= 18944 on 148 SMs).  Linv is the potrf
+  // scratch, the flags sit at its end.
+  static int resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(trsv_pair_flag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlagSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsv_pair_flag_kernel, kFT, kFlagSmem) != cudaSuccess)
+      per_sm = 0;
+    cudaGetLastError();
+    resident = per_sm * sms;
+  }
+  if (env && nb >= 2 && nb <= resident) {
     int* flags = reinterpret_cast<int*>(const_cast<double*>(Linv) + potrf_trsv_flags_offset(n));
     cudaError_t e = cudaMemsetAsync(flags, 0, 2 * nb * sizeof(int), st);
     if (e != cudaSuccess) return e;
