@@ -372,7 +372,8 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     const size_t kb_bytes = (size_t)nb * (f16 ? 2 : 1) * fs::kTileBytes;
     const int64_t KB = (m + tile_cols - 1) / tile_cols;
     const int64_t align = fs::gemv_rows_chunk_cols() / tile_cols;   // column chunks of the u partials
-    const int64_t kbc = (int64_t)(ctx->St_bytes / kb_bytes) / align * align;
+    const int64_t fit = (int64_t)(ctx->St_bytes / kb_bytes);
+    const int64_t kbc = fit >= KB ? KB : fit / align * align;   // one chunk when everything fits
     if (kbc < align) return fail(ctx, FS_ENOMEM, "tiled copy too small for one K-chunk");
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
     if (e == cudaSuccess && f16) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
@@ -1191,7 +1192,7 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
       const int64_t tcols = use_tc == 2 ? fs::kTile16Cols : fs::kTileCols;
       const size_t kbb = (size_t)fs::tiles_nb(n) * (use_tc == 2 ? 2 : 1) * fs::kTileBytes;
       uint8_t* St_c = ctx->d_St ? ctx->d_St - (ptrdiff_t)((c0 / tcols) * (int64_t)kbb) : nullptr;
-      if (!direct && (size_t)((c1 - c0 + tcols - 1) / tcols + 1) * kbb > ctx->St_bytes)
+      if (!direct && (size_t)((c1 - c0 + tcols - 1) / tcols) * kbb > ctx->St_bytes)   // (c0 % tcols == 0)
         FS_STEP(fail(ctx, FS_ENOMEM, "a host-entry K-chunk exceeds the tiled copy"));
       if (ctx->poison_rc) break;
       if (use_tc == 2 && direct) {

@@ -19,6 +19,8 @@
 // no shared-memory round trips; the off-diagonal pieces are 32^3 GEMMs by the whole CTA.
 // Every kernel first checks the status word, so a breakdown stops the remaining work.
 // Deterministic: fixed operation order, no atomics.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -1040,7 +1042,7 @@ cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* 
 
 int64_t potrf_scratch_doubles(int64_t n) {
   const int64_t nb = (n + kNB - 1) / kNB;
-  return potrf_trsv_flags_offset(n) + nb /* trsv_pair's 2 nb block flags */;
+  return potrf_trsv_flags_offset(n) + nb /* trsv_pair's 2 nb block flags */ + 1 /* blocked: sub status */;
 }
 
 int64_t potrf_trsv_flags_offset(int64_t n) {
@@ -1057,9 +1059,117 @@ cudaError_t unpack_lower(const double* Gp, int64_t n, double add_diag, double* W
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- blocked path (large n)
+// Right-looking with 256-wide block columns: the diagonal block by the persistent kernel above
+// (its four 64-block inverses land in Linv at their global positions), the panel below as a
+// GEMM-form TRSM (potrf_panel_kernel), the trailing matrix by the 128 x 128 DMMA tiles of the
+// Gram (syrk_dmma_trail, K = 256): the n^3/3 flops run in large tensor-core tiles instead of the
+// persistent kernel's 64^3 tile updates with a grid barrier per 64 columns.
+constexpr int kNB2 = 256;
+constexpr size_t kPanelSmem = 5 * kTileSmem;
+
+// rows [r0, r0 + 64) of the panel below diagonal block [k0, k0 + 64 nbk):
+//   X_b = (A_b - sum_{c<b} X_c L_bc^T) Linv_bb^T,  b = 0 .. nbk-1 (4 threads x 4 x 4 DMMA results)
+__global__ void __launch_bounds__(kThreads)
+potrf_panel_kernel(double* W, int64_t n, int64_t ld, int64_t k0, int nbk, const double* __restrict__ Linv,
+                   const int64_t* status) {
+  if (*(volatile const int64_t*)status != 0) return;
+  extern __shared__ double psm[];
+  double (*X[3])[kLd];
+  for (int c = 0; c < 3; ++c) X[c] = reinterpret_cast<double (*)[kLd]>(psm + c * kNB * kLd);
+  double (*T)[kLd] = reinterpret_cast<double (*)[kLd]>(psm + 3 * kNB * kLd);
+  double (*B)[kLd] = reinterpret_cast<double (*)[kLd]>(psm + 4 * kNB * kLd);
+  const int64_t r0 = k0 + (int64_t)nbk * kNB + (int64_t)blockIdx.x * kNB;
+  for (int b = 0; b < nbk; ++b) {
+    const int64_t cb = k0 + (int64_t)b * kNB;
+    load_tile(W, n, ld, r0, cb, T);
+    double sub[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sub[i][j] = 0.0;
+    for (int c = 0; c < b; ++c) {
+      __syncthreads();                          // B free (previous product done)
+      load_tile(W, n, ld, cb, k0 + (int64_t)c * kNB, B);   // L_bc
+      __syncthreads();
+      double acc[4][4];
+      gemm_nt(X[c], B, acc);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sub[i][j] += acc[i][j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) T[frag_row(i)][frag_col(i, j)] -= sub[i][j];
+    load_block64(Linv + (size_t)(k0 / kNB + b) * kNB * kNB, B);
+    __syncthreads();
+    double acc[4][4];
+    gemm_nt(T, B, acc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = frag_row(i), c = frag_col(i, j);
+        if (b < 3) X[b][r][c] = acc[i][j];
+        if (r0 + r < n) W[(r0 + r) * ld + cb + c] = acc[i][j];
+      }
+  }
+}
+
+// the diagonal block's local status (1-based column) -> the global word, first failure only
+__global__ void potrf_status_fixup_kernel(int64_t* status, const int64_t* sub, int64_t k0) {
+  const int64_t sv = *(volatile const int64_t*)sub;
+  if (*status == 0 && sv != 0) *status = sv + k0;
+}
+
+int64_t potrf_blocked_min_n() {
+  // measured (tools/large_fit.py): n = 4096 persistent 3.10 vs blocked 3.44 ms; n = 8192 15.7 vs
+  // 13.7; n = 16384 107 vs 81
+  static const int64_t v = getenv("FS_POTRF_BLOCKED_MINN") ? atoll(getenv("FS_POTRF_BLOCKED_MINN")) : 6144;
+  return v;
+}
+
+cudaError_t potrf_blocked(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch, cudaStream_t st,
+                          int* launches) {
+  const int64_t nb = (n + kNB - 1) / kNB;
+  double* Linv = scratch;
+  int64_t* sub = reinterpret_cast<int64_t*>(scratch + potrf_trsv_flags_offset(n) + nb);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(potrf_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kPanelSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaError_t e = cudaMemsetAsync(sub, 0, sizeof(int64_t), st);
+  for (int64_t k0 = 0; k0 < n && e == cudaSuccess; k0 += kNB2) {
+    const int64_t w = std::min<int64_t>(kNB2, n - k0);
+    // the diagonal block's working space follows its Linv blocks: it overwrites only Linv
+    // blocks of later diagonal blocks (written when those are factored) and the unused panels
+    e = potrf_lower(W + k0 * ldW + k0, w, ldW, sub, Linv + (k0 / kNB) * kNB * kNB, st, launches, nullptr, nullptr,
+                    nullptr);
+    if (e != cudaSuccess) break;
+    potrf_status_fixup_kernel<<<1, 1, 0, st>>>(d_status, sub, k0);
+    if (launches) *launches += 1;
+    const int64_t nt = n - k0 - w;
+    if (nt <= 0) break;
+    potrf_panel_kernel<<<(unsigned)((nt + kNB - 1) / kNB), kThreads, kPanelSmem, st>>>(W, n, ldW, k0, (int)(w / kNB),
+                                                                                       Linv, d_status);
+    if (launches) *launches += 1;
+    e = syrk_dmma_trail(W + (k0 + w) * ldW + k0, nt, w, ldW, W + (k0 + w) * ldW + k0 + w, ldW, d_status, st,
+                        launches);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
 cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch,
                         cudaStream_t st, int* launches, const double* u, double* z, bool* solved) {
   if (solved) *solved = false;
+  if (n >= potrf_blocked_min_n() && n > kNB2) return potrf_blocked(W, n, ldW, d_status, scratch, st, launches);
   const int nb = (int)((n + kNB - 1) / kNB);
   double* Linv = scratch;
   double* panel0 = Linv + (int64_t)nb * kNB * kNB;

@@ -62,10 +62,21 @@ FS_DEVINL void stage_mma(double (&acc)[8][4][2], const double* A, const double* 
 // Tile epilogue: packed lower G (+ lam on the diagonal) when the tile has one split, else the
 // partial tile into the split-K workspace (row-major 128 x 128 per block).
 FS_DEVINL void store_tile(const double (&acc)[8][4][2], int64_t rA, int64_t rB, int64_t n, double lam, double* ws,
-                          double* Gp, int direct, int wr, int wc, int fr, int lane) {
+                          double* Gp, int direct, int wr, int wc, int fr, int lane, int64_t ldc = 0) {
   // accumulator fragment (m8n8 f64): thread holds rows fr, columns 2*(lane&3) + {0,1}
   const int cc = 2 * (lane & 3);
-  if (direct) {
+  if (ldc > 0) {
+    // trailing update of a blocked Cholesky: C (row-major, pitch ldc, lower) -= the tile
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t gi = rA + wr + 8 * a + fr, gj = rB + wc + 8 * b + cc + e;
+          if (gi < n && gj <= gi) Gp[gi * ldc + gj] -= acc[a][b][e];
+        }
+  } else if (direct) {
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -161,7 +172,9 @@ struct Loader {
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P, double lam,
-                 double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec, int flush) {
+                 double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec, int flush, int64_t ldc = 0,
+                 const int64_t* status = nullptr) {
+  if (status && *(volatile const int64_t*)status != 0) return;
   extern __shared__ __align__(16) double dsm[];
   int I, J;
   tile_ij(blockIdx.x / P, I, J);
@@ -212,7 +225,7 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
     }
   }
   if (flushed) unflush_acc(acc, fbuf, wr, wc, fr, lane);
-  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
+  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane, ldc);
 }
 
 // fp64 scores with 16-byte aligned rows: global -> shared with cp.async (no register staging,
@@ -242,7 +255,9 @@ FS_DEVINL void issue_stage(double* dst, const double* __restrict__ S, int64_t n,
 
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
-                       double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct, int flush) {
+                       double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct, int flush,
+                       int64_t ldc = 0, const int64_t* status = nullptr) {
+  if (status && *(volatile const int64_t*)status != 0) return;
   extern __shared__ __align__(16) double dsm[];
   int I, J;
   tile_ij(blockIdx.x / P, I, J);
@@ -259,6 +274,17 @@ syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int64_t rA = (int64_t)I * kT, rB = (int64_t)J * kT;
+  if (ldc > 0 && threadIdx.x < kT && rA + threadIdx.x < n) {
+    // trailing update: pull this tile's rows of C into L2 while the MMAs run, so the closing
+    // read-modify-write hits L2 (C is far larger than L2 at the sizes this path serves)
+    const double* crow = Gp + (rA + threadIdx.x) * ldc + rB;
+    const int64_t cols = std::min<int64_t>(kT, rA + threadIdx.x - rB + 1);
+    if (cols > 0) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(crow) & ~(uintptr_t)15;
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(crow + cols) + 15) & ~(uintptr_t)15;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+    }
+  }
   const int nst = kbeg < kend ? (int)((kend - kbeg + kK - 1) / kK) : 0;
   auto issue = [&](int st) {
     if (st < nst) {
@@ -289,7 +315,7 @@ syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (flushed) unflush_acc(acc, fbuf, wr, wc, fr, lane);
-  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane);
+  store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane, ldc);
 }
 
 // Fixed-order sum of the P split-K partials of a tile.  Block (tile, part): kRedParts slices of
@@ -410,6 +436,31 @@ cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
     syrk_dmma_reduce<<<p.tiles * kRedParts, 256, 0, st>>>(ws, p.P, n, lam, Gp);
     if (launches) *launches += 1;
   }
+  return cudaGetLastError();
+}
+
+// Trailing update of a blocked Cholesky: C (nt x nt lower, row-major pitch ldc) -= P P^T with P
+// the nt x K panel (row-major, pitch ldP) — the same 128 x 128 DMMA tiles as the Gram, no split,
+// subtracted in place.  Skipped entirely once *status is set.
+cudaError_t syrk_dmma_trail(const double* P, int64_t nt, int64_t K, int64_t ldP, double* C, int64_t ldc,
+                            const int64_t* status, cudaStream_t st, int* launches) {
+  if (nt <= 0 || K <= 0) return cudaSuccess;
+  const int64_t T = (nt + kT - 1) / kT;
+  const unsigned grid = (unsigned)(T * (T + 1) / 2);
+  const bool vec = ((reinterpret_cast<uintptr_t>(P) | (uintptr_t)(ldP * 8)) & 15) == 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
+    cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    attr = true;
+  }
+  if (vec)
+    syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, ldc,
+                                                                     status);
+  else
+    syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, 0, ldc,
+                                                                 status);
+  if (launches) *launches += 1;
   return cudaGetLastError();
 }
 

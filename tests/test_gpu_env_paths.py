@@ -106,3 +106,59 @@ def test_single_cta_trsv_pair_matches_flag_chained(gpu, tmp_path):
     ref = reference(n, m)
     assert O.rel_err(x1, ref.x) <= 1e-10 and O.rel_err(x2, ref.x) <= 1e-10
     assert i2["rel_residual"] <= 1e-10
+
+
+POTRF_CASE = r'''
+import sys, json, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2310_17556_b200 as fsb
+from paper_2310_17556_b200.solvers import _cholesky_lower
+from oracle import fisher_oracle as O
+n, bad = {n}, {bad}
+rng = np.random.Generator(np.random.PCG64(n + 7))
+A = rng.standard_normal((n, n + 64))
+W = A @ A.T / n + 0.1 * np.eye(n)
+if bad >= 0:
+    W[bad, :bad] = W[bad - 1, :bad]
+    W[:bad, bad] = W[bad, :bad]
+    W[bad, bad] = W[bad - 1, bad - 1] - 1.0
+    try:
+        O.cholesky_lower(W)
+        ref_piv = None
+    except O.OracleFactorizationError as e:
+        ref_piv = e.pivot
+    try:
+        _cholesky_lower(W)
+        piv = None
+    except fsb.FactorizationError as e:
+        piv = e.pivot
+    print(json.dumps({{"piv": piv, "ref_piv": ref_piv}}))
+else:
+    L = _cholesky_lower(W)
+    ref = O.cholesky_lower(W)
+    print(json.dumps({{"err": float(np.abs(L - ref).max() / np.abs(ref).max()),
+                      "upper_zero": bool(np.array_equal(np.triu(L, 1), np.zeros((n, n))))}}))
+'''
+
+
+def run_potrf(env, n, bad=-1):
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", POTRF_CASE.format(root=ROOT, n=n, bad=bad)], env=e, capture_output=True,
+                       text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("n,minn", [(700, "300"), (1100, "300"), (4500, "4096")])
+def test_blocked_potrf_matches_lapack(gpu, n, minn):
+    """256-wide block columns: diagonal blocks by the persistent kernel, GEMM-form panel TRSM, DMMA
+    trailing tiles (FS_POTRF_BLOCKED_MINN lowers the size where it takes over)."""
+    info = run_potrf({"FS_POTRF_BLOCKED_MINN": minn}, n)
+    assert info["err"] <= 1e-10 and info["upper_zero"], info
+
+
+@pytest.mark.parametrize("n,bad", [(700, 5), (700, 300), (700, 699), (1100, 513)])
+def test_blocked_potrf_pivot_index(gpu, n, bad):
+    info = run_potrf({"FS_POTRF_BLOCKED_MINN": "300"}, n, bad)
+    assert info["ref_piv"] == bad and info["piv"] == bad, info
