@@ -374,7 +374,7 @@ int gram_impl(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t n, i
     const int64_t align = fs::gemv_rows_chunk_cols() / tile_cols;   // column chunks of the u partials
     const int64_t fit = (int64_t)(ctx->St_bytes / kb_bytes);
     const int64_t kbc = fit >= KB ? KB : fit / align * align;   // one chunk when everything fits
-    if (kbc < align) return fail(ctx, FS_ENOMEM, "tiled copy too small for one K-chunk");
+    if (kbc < 1) return fail(ctx, FS_ENOMEM, "tiled copy too small for one K-chunk");
     e = cudaMemsetAsync(ctx->d_ovf, 0, sizeof(int), st);
     if (e == cudaSuccess && f16) e = f16_scales(ctx, (const float*)S, n, m, ldS, st, &l);
     for (int64_t kb0 = 0; kb0 < KB && e == cudaSuccess; kb0 += kbc) {

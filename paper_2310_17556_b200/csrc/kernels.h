@@ -65,8 +65,9 @@ cudaError_t residual_cols(bool s_f64, const void* S, int64_t n, int64_t m, int64
 size_t syrk_dmma_workspace_bytes(int64_t n, int64_t m, int num_sms);   // a context for (n, m): every smaller plan fits
 size_t syrk_dmma_plan_bytes(int64_t n, int64_t m, int num_sms);        // tiles x splits (partials + flush slots)
 int syrk_dmma_splits(int64_t n, int64_t m, int num_sms, size_t ws_bytes);   // split count the plan takes
+// cols > 0: update only C's first `cols` columns (all nt rows; a whole number of 128-col tiles)
 cudaError_t syrk_dmma_trail(const double* P, int64_t nt, int64_t K, int64_t ldP, double* C, int64_t ldc,
-                            const int64_t* status, cudaStream_t st, int* launches);
+                            const int64_t* status, cudaStream_t st, int* launches, int64_t cols = 0);
 cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t ldS, double lam, double* Gp,
                       double* ws, size_t ws_bytes, int num_sms, cudaStream_t st, int* launches);
 

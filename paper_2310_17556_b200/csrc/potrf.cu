@@ -25,6 +25,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <mutex>
 
 namespace fs {
 namespace {
@@ -1132,11 +1133,45 @@ int64_t potrf_blocked_min_n() {
   return v;
 }
 
+// One-step look-ahead on two streams forked from the caller's: a high-priority stream runs the
+// critical path — strip k+1 -= P_k P_k(strip)^T, then the diagonal factor and panel of block
+// column k+1 — while a low-priority stream applies the rest of step k's update (columns beyond
+// strip k+1), so the latency-bound diagonal/panel kernels hide under the big trailing update.
+// The next strip update waits for that rest (it touches the same columns).  Enqueue is
+// serialised by a mutex (the streams and events are shared per process).
+struct BlockedStreams {
+  cudaStream_t hp = nullptr, lp = nullptr;
+  static constexpr int kEv = 2 * 160;            // n <= 40960
+  cudaEvent_t ev[kEv] = {};
+  cudaEvent_t fork = nullptr;
+  bool ok = false;
+};
+
+BlockedStreams& blocked_streams() {
+  static BlockedStreams b;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    int lo = 0, hi = 0;
+    bool ok = cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess &&
+              cudaStreamCreateWithPriority(&b.hp, cudaStreamNonBlocking, hi) == cudaSuccess &&
+              cudaStreamCreateWithPriority(&b.lp, cudaStreamNonBlocking, lo) == cudaSuccess &&
+              cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < BlockedStreams::kEv; ++i)
+      ok = cudaEventCreateWithFlags(&b.ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) cudaGetLastError();
+    b.ok = ok;
+  }
+  return b;
+}
+
 cudaError_t potrf_blocked(double* W, int64_t n, int64_t ldW, int64_t* d_status, double* scratch, cudaStream_t st,
                           int* launches) {
   const int64_t nb = (n + kNB - 1) / kNB;
   double* Linv = scratch;
   int64_t* sub = reinterpret_cast<int64_t*>(scratch + potrf_trsv_flags_offset(n) + nb);
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(potrf_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1144,23 +1179,64 @@ cudaError_t potrf_blocked(double* W, int64_t n, int64_t ldW, int64_t* d_status, 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  cudaError_t e = cudaMemsetAsync(sub, 0, sizeof(int64_t), st);
-  for (int64_t k0 = 0; k0 < n && e == cudaSuccess; k0 += kNB2) {
+  BlockedStreams& bs = blocked_streams();
+  const int64_t steps = (n + kNB2 - 1) / kNB2;
+  const bool ahead = bs.ok && 2 * steps <= BlockedStreams::kEv && getenv("FS_POTRF_LOOKAHEAD") == nullptr;
+  cudaStream_t hp = ahead ? bs.hp : st, lp = ahead ? bs.lp : st;
+  cudaError_t e = cudaSuccess;
+  if (ahead) {
+    e = cudaEventRecord(bs.fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hp, bs.fork, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(lp, bs.fork, 0);
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(sub, 0, sizeof(int64_t), hp);
+  // diagonal block + panel of block column k (on hp)
+  auto diag_panel = [&](int64_t k0) -> cudaError_t {
     const int64_t w = std::min<int64_t>(kNB2, n - k0);
     // the diagonal block's working space follows its Linv blocks: it overwrites only Linv
     // blocks of later diagonal blocks (written when those are factored) and the unused panels
-    e = potrf_lower(W + k0 * ldW + k0, w, ldW, sub, Linv + (k0 / kNB) * kNB * kNB, st, launches, nullptr, nullptr,
-                    nullptr);
-    if (e != cudaSuccess) break;
-    potrf_status_fixup_kernel<<<1, 1, 0, st>>>(d_status, sub, k0);
-    if (launches) *launches += 1;
+    cudaError_t r = potrf_lower(W + k0 * ldW + k0, w, ldW, sub, Linv + (k0 / kNB) * kNB * kNB, hp, launches, nullptr,
+                                nullptr, nullptr);
+    if (r != cudaSuccess) return r;
+    potrf_status_fixup_kernel<<<1, 1, 0, hp>>>(d_status, sub, k0);
     const int64_t nt = n - k0 - w;
-    if (nt <= 0) break;
-    potrf_panel_kernel<<<(unsigned)((nt + kNB - 1) / kNB), kThreads, kPanelSmem, st>>>(W, n, ldW, k0, (int)(w / kNB),
-                                                                                       Linv, d_status);
-    if (launches) *launches += 1;
-    e = syrk_dmma_trail(W + (k0 + w) * ldW + k0, nt, w, ldW, W + (k0 + w) * ldW + k0 + w, ldW, d_status, st,
-                        launches);
+    if (nt > 0)
+      potrf_panel_kernel<<<(unsigned)((nt + kNB - 1) / kNB), kThreads, kPanelSmem, hp>>>(W, n, ldW, k0, (int)(w / kNB),
+                                                                                         Linv, d_status);
+    if (launches) *launches += nt > 0 ? 2 : 1;
+    return cudaGetLastError();
+  };
+  if (e == cudaSuccess) e = diag_panel(0);
+  for (int64_t s = 0; e == cudaSuccess && (s + 1) * kNB2 < n; ++s) {
+    const int64_t k0 = s * kNB2, w = kNB2, r0 = k0 + w, nt = n - r0;   // panel s: rows [r0, n)
+    const double* P = W + r0 * ldW + k0;
+    const int64_t ws = std::min<int64_t>(kNB2, nt);                     // strip s+1 width
+    if (ahead) {
+      cudaEvent_t ev_p = bs.ev[2 * s], ev_r = bs.ev[2 * s + 1];
+      if ((e = cudaEventRecord(ev_p, hp)) != cudaSuccess) break;        // panel s done
+      // rest of step s (columns beyond strip s+1) on lp
+      if ((e = cudaStreamWaitEvent(lp, ev_p, 0)) != cudaSuccess) break;
+      if (nt > ws && (e = syrk_dmma_trail(P + ws * ldW, nt - ws, w, ldW, W + (r0 + ws) * ldW + r0 + ws, ldW, d_status,
+                                          lp, launches)) != cudaSuccess)
+        break;
+      // strip s+1 on hp, after the previous step's rest (same columns)
+      if (s > 0 && (e = cudaStreamWaitEvent(hp, bs.ev[2 * s - 1], 0)) != cudaSuccess) break;
+      if ((e = syrk_dmma_trail(P, nt, w, ldW, W + r0 * ldW + r0, ldW, d_status, hp, launches, ws)) != cudaSuccess)
+        break;
+      if ((e = cudaEventRecord(ev_r, lp)) != cudaSuccess) break;
+    } else {
+      e = syrk_dmma_trail(P, nt, w, ldW, W + r0 * ldW + r0, ldW, d_status, st, launches);
+      if (e != cudaSuccess) break;
+    }
+    e = diag_panel(r0);
+  }
+  if (ahead) {                                   // join: the caller's stream waits for both
+    cudaError_t e2 = cudaEventRecord(bs.fork, hp);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, bs.fork, 0);
+    cudaEvent_t last_lp = bs.ev[BlockedStreams::kEv - 1];
+    if (e2 == cudaSuccess) e2 = cudaEventRecord(last_lp, lp);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(st, last_lp, 0);
+    if (e == cudaSuccess) e = e2;
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   return e;

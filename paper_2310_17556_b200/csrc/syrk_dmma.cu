@@ -173,11 +173,17 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P, double lam,
                  double* __restrict__ ws, double* __restrict__ Gp, int direct, int vec, int flush, int64_t ldc = 0,
-                 const int64_t* status = nullptr) {
+                 const int64_t* status = nullptr, int jmax = 0) {
   if (status && *(volatile const int64_t*)status != 0) return;
   extern __shared__ __align__(16) double dsm[];
   int I, J;
-  tile_ij(blockIdx.x / P, I, J);
+  if (jmax > 0) {
+    I = blockIdx.x / jmax;
+    J = blockIdx.x % jmax;
+    if (J > I) return;
+  } else {
+    tile_ij(blockIdx.x / P, I, J);
+  }
   const int split = blockIdx.x % P;
   const bool diag = I == J;
   const int64_t kbeg = (int64_t)split * kchunk;
@@ -256,11 +262,17 @@ FS_DEVINL void issue_stage(double* dst, const double* __restrict__ S, int64_t n,
 __global__ void __launch_bounds__(kThreads, 1)
 syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
                        double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct, int flush,
-                       int64_t ldc = 0, const int64_t* status = nullptr) {
+                       int64_t ldc = 0, const int64_t* status = nullptr, int jmax = 0) {
   if (status && *(volatile const int64_t*)status != 0) return;
   extern __shared__ __align__(16) double dsm[];
   int I, J;
-  tile_ij(blockIdx.x / P, I, J);
+  if (jmax > 0) {            // column strip: tiles (I, J) with J < jmax, grid jmax x row tiles
+    I = blockIdx.x / jmax;
+    J = blockIdx.x % jmax;
+    if (J > I) return;
+  } else {
+    tile_ij(blockIdx.x / P, I, J);
+  }
   const int split = blockIdx.x % P;
   const bool diag = I == J;
   const int64_t kbeg = (int64_t)split * kchunk;
@@ -443,10 +455,12 @@ cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
 // the nt x K panel (row-major, pitch ldP) — the same 128 x 128 DMMA tiles as the Gram, no split,
 // subtracted in place.  Skipped entirely once *status is set.
 cudaError_t syrk_dmma_trail(const double* P, int64_t nt, int64_t K, int64_t ldP, double* C, int64_t ldc,
-                            const int64_t* status, cudaStream_t st, int* launches) {
+                            const int64_t* status, cudaStream_t st, int* launches, int64_t cols) {
   if (nt <= 0 || K <= 0) return cudaSuccess;
   const int64_t T = (nt + kT - 1) / kT;
-  const unsigned grid = (unsigned)(T * (T + 1) / 2);
+  // cols > 0: only the first `cols` columns of C (a strip of whole 128-column tiles)
+  const int jmax = cols > 0 ? (int)std::min<int64_t>(T, (cols + kT - 1) / kT) : 0;
+  const unsigned grid = jmax > 0 ? (unsigned)(T * jmax) : (unsigned)(T * (T + 1) / 2);
   const bool vec = ((reinterpret_cast<uintptr_t>(P) | (uintptr_t)(ldP * 8)) & 15) == 0;
   static bool attr = false;
   if (!attr) {
@@ -456,10 +470,10 @@ cudaError_t syrk_dmma_trail(const double* P, int64_t nt, int64_t K, int64_t ldP,
   }
   if (vec)
     syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, ldc,
-                                                                     status);
+                                                                     status, jmax);
   else
     syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, 0, ldc,
-                                                                 status);
+                                                                 status, jmax);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
