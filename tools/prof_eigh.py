@@ -10,8 +10,8 @@ S = torch.randn(n, m, device=dev) / n ** 0.5
 v = torch.randn(m, device=dev)
 system = fsb.DampedSystem(fsb.ScoreMatrix(S), 1e-3, v)
 for prec in ("f16x2", "fp64"):
-    for route in ("chol", "eigh"):
-        f = fsb.solve_chol if route == "chol" else fsb.solve_svd_eigh
+    for route in ("chol", "eigh", "svd"):
+        f = {"chol": fsb.solve_chol, "eigh": fsb.solve_svd_eigh, "svd": fsb.solve_svd_direct}[route]
         f(system, precision=prec)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
