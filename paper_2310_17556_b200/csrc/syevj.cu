@@ -14,6 +14,8 @@
 // the off-diagonal Frobenius norm falls below tol * ||A||_F (fixed-order reduction:
 // deterministic).  Rotations follow Golub & Van Loan sym.schur2 (|t| <= 1, the stable root).
 // A single-CTA bitonic sort orders the eigenpairs.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -150,6 +152,270 @@ jacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restri
   }
 }
 
+// ---------------------------------------------------------------- block Jacobi (n >= 128)
+// The scalar kernel above is latency-bound: n-1 rounds per sweep, each a full pass over A plus a
+// grid barrier (~10 us at n = 1024: 11 sweeps = 110 ms).  The block version pairs 32-row blocks
+// (round-robin over 2q = np/32 blocks, q pairs per round, 2q-1 rounds per sweep):
+//   phase A  one CTA per pair: the 64 x 64 super-block [I J] x [I J] gets one inner cyclic Jacobi
+//            sweep in shared memory (63 rounds of 32 disjoint rotations), accumulating V (64 x 64,
+//            orthogonal); V^T goes to global memory
+//   phase B  every 64 x 64 block (P1, P2 >= ... lower) of A: A'_{P1P2} = V1^T A_{P1P2} V2 (two DMMA
+//            64^3 products, written to both triangles of the other buffer: exactly symmetric), and
+//            every 64 x 64 block of U: U_{c,P2} <- U_{c,P2} V2 (in place)
+// with a grid barrier after each phase.  Same rotations as scalar cyclic Jacobi, applied as
+// tensor-core block products: the n^3 work per sweep runs on DMMA and a sweep costs 2q-1 rounds of
+// (one inner sweep + two barriers) instead of np-1 fully serialised rounds.
+constexpr int kBB = 32;                 // block rows
+constexpr int kSB = 2 * kBB;            // super-block (pair) size
+constexpr int kBP = kSB + 4;            // smem pitch of the DMMA tiles (conflict-free fragments, as potrf)
+constexpr int kMP = kSB + 1;            // smem pitch of the inner-sweep matrices
+constexpr int kBThreads = 256;
+constexpr size_t kBSmemA = (size_t)3 * kSB * kMP * sizeof(double);           // M, M', V
+constexpr size_t kBSmemB = (size_t)6 * kSB * kBP * sizeof(double);           // X, Vt1, Vt2, T + U's X, V
+constexpr size_t kBSmem = kBSmemA > kBSmemB ? kBSmemA : kBSmemB;
+
+// super-block row r (0..63) of pair (I, J) -> matrix row
+FS_DEVINL int sb_row(int I, int J, int r) { return r < kBB ? I * kBB + r : J * kBB + r - kBB; }
+
+// C (64 x 64, 4 x 4 per thread) = A B^T, both 64 x 64 row-major in smem (pitch kBP), fp64 tensor
+// cores (mma.sync m8n8k4): warp w owns rows [16 (w/2), +16) x cols [32 (w%2), +32)
+FS_DEVINL int bfrag_row(int i) { return ((threadIdx.x >> 5) >> 1) * 16 + 8 * (i >> 1) + ((threadIdx.x & 31) >> 2); }
+FS_DEVINL int bfrag_col(int i, int j) { return ((threadIdx.x >> 5) & 1) * 32 + 8 * j + 2 * (threadIdx.x & 3) + (i & 1); }
+FS_DEVINL void bgemm_nt(const double* A, const double* B, double acc[4][4]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32, fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < kSB; k0 += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) a[t] = A[(wr + 8 * t + fr) * kBP + k0 + fk];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) b[t] = B[(wc + 8 * t + fr) * kBP + k0 + fk];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+            : "+d"(acc[2 * t][u]), "+d"(acc[2 * t + 1][u])
+            : "d"(a[t]), "d"(b[u]));
+  }
+}
+
+// rows of pair P1 x columns of pair P2 of an np x np matrix -> smem (pitch kBP); transposed: the
+// element (r, c) is stored at [c][r]
+FS_DEVINL void load_pair_block(const double* __restrict__ M, int np, int I1, int J1, int I2, int J2, double* dst,
+                               bool transposed) {
+  for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) {
+    const int r = e >> 6, c = e & 63;
+    const double val = M[(int64_t)sb_row(I1, J1, r) * np + sb_row(I2, J2, c)];
+    if (transposed) dst[c * kBP + r] = val;
+    else dst[r * kBP + c] = val;
+  }
+}
+
+__global__ void __launch_bounds__(kBThreads, 1)
+bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restrict__ U, double* __restrict__ Vt,
+               int np, int max_sweeps, double tol, double* __restrict__ partial, unsigned* ctl, int* info,
+               double* __restrict__ wraw) {
+  extern __shared__ double bsm[];
+  __shared__ double red[kBThreads / 32];
+  const int nblk = np / kBB, q = nblk / 2, rounds = nblk - 1;
+  double* Aold = A0;
+  double* Anew = A1;
+  auto frob = [&](const double* A, bool off_only) -> double {
+    double s = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * kBThreads + threadIdx.x; e < (int64_t)np * np;
+         e += (int64_t)gridDim.x * kBThreads) {
+      const int i = (int)(e / np), j = (int)(e % np);
+      if (!off_only || i != j) s += A[e] * A[e];
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kBThreads / 32; ++w) t += red[w];
+      partial[blockIdx.x] = t;
+    }
+    grid_barrier(ctl, ctl + 1);
+    double tot = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) tot += partial[b];
+    grid_barrier(ctl, ctl + 1);
+    return tot;
+  };
+  // U <- U V for every (64-row chunk c, pair P2) block of a round's rotations Vp (in place:
+  // each block by one CTA), tasks spread over CTAs first, first + stride, ...
+  auto u_update = [&](const double* Vp, int rr, int t0, int t1, int first, int stride) {
+    if (first < 0) return;
+    double* X = bsm + 4 * kSB * kBP;                 // past phase A's buffers (kBSmem holds both)
+    double* V2t = X + kSB * kBP;
+    for (int ut = t0 + first; ut < t1; ut += stride) {
+      const int c = ut / q, P2 = ut % q;
+      int I2, J2;
+      pair_of_round(rr, P2, rounds, I2, J2);
+      for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) {
+        const int a = e >> 6, b = e & 63;
+        X[a * kBP + b] = U[(int64_t)(c * kSB + a) * np + sb_row(I2, J2, b)];
+        V2t[a * kBP + b] = Vp[(size_t)P2 * kSB * kSB + e];
+      }
+      __syncthreads();
+      double acc[4][4];
+      bgemm_nt(X, V2t, acc);                         // U' = U V2
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          U[(int64_t)(c * kSB + bfrag_row(i)) * np + sb_row(I2, J2, bfrag_col(i, j))] = acc[i][j];
+      __syncthreads();
+    }
+  };
+  int nround = 0, prev_r = 0;                        // rounds done (all sweeps), the last one's index
+  // a round's U blocks [0, ndefer) are applied during the NEXT round's phase A by the CTAs the
+  // inner sweeps leave idle (ten each at most: about one inner sweep's time), the rest in its phase B
+  const int spare = (int)gridDim.x - q;
+  const int ndefer = spare > 0 ? min(q * q, 10 * spare) : q * q;
+  const double fro2 = frob(Aold, false);
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    const double off2 = frob(Aold, true);
+    if (!(off2 > tol * tol * fro2)) break;
+    for (int r = 0; r < rounds; ++r) {
+      // ---------------- phase A: inner sweep of each pair's super-block; meanwhile the other
+      // CTAs apply the PREVIOUS round's rotations to U (U feeds nothing inside the iteration) ----
+      double* Vr = Vt + (size_t)(nround & 1) * q * kSB * kSB;             // this round's V^T
+      const double* Vp = Vt + (size_t)((nround & 1) ^ 1) * q * kSB * kSB; // the previous round's
+      if (nround > 0 && (int)gridDim.x > q) u_update(Vp, prev_r, 0, ndefer, (int)blockIdx.x - q, (int)gridDim.x - q);
+      for (int P = blockIdx.x; P < q; P += gridDim.x) {
+        int I, J;
+        pair_of_round(r, P, rounds, I, J);
+        double* M = bsm;
+        double* M2 = bsm + kSB * kMP;
+        double* V = bsm + 2 * kSB * kMP;
+        for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) {
+          const int a = e >> 6, b = e & 63;
+          M[a * kMP + b] = Aold[(int64_t)sb_row(I, J, a) * np + sb_row(I, J, b)];
+          V[a * kMP + b] = a == b ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        // every warp computes all 32 rotations of an inner round (lane k: pair k) and takes the
+        // ones it needs by shuffle: one CTA barrier per inner round
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int ir = 0; ir < kSB - 1; ++ir) {
+          int pk, qk;
+          pair_of_round(ir, lane, kSB - 1, pk, qk);
+          const Rot Rk = schur2(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
+          // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane)
+#pragma unroll
+          for (int i = 0; i < kBB / (kBThreads / 32); ++i) {
+            const int k1 = warp + (kBThreads / 32) * i;
+            int p1, q1;
+            pair_of_round(ir, k1, kSB - 1, p1, q1);
+            const Rot R1{__shfl_sync(0xffffffffu, Rk.c, k1), __shfl_sync(0xffffffffu, Rk.s, k1)};
+            const double bpp = M[p1 * kMP + pk], bpq = M[p1 * kMP + qk], bqp = M[q1 * kMP + pk],
+                         bqq = M[q1 * kMP + qk];
+            const double rpp = R1.c * bpp - R1.s * bqp, rpq = R1.c * bpq - R1.s * bqq;
+            const double rqp = R1.s * bpp + R1.c * bqp, rqq = R1.s * bpq + R1.c * bqq;
+            M2[p1 * kMP + pk] = Rk.c * rpp - Rk.s * rpq;
+            M2[p1 * kMP + qk] = Rk.s * rpp + Rk.c * rpq;
+            M2[q1 * kMP + pk] = Rk.c * rqp - Rk.s * rqq;
+            M2[q1 * kMP + qk] = Rk.s * rqp + Rk.c * rqq;
+          }
+          // V <- V J: columns pk, qk of rows warp + 8 i (in place: each (row, pair) by one thread)
+#pragma unroll
+          for (int i = 0; i < kSB / (kBThreads / 32); ++i) {
+            const int row = warp + (kBThreads / 32) * i;
+            const double a = V[row * kMP + pk], b = V[row * kMP + qk];
+            V[row * kMP + pk] = Rk.c * a - Rk.s * b;
+            V[row * kMP + qk] = Rk.s * a + Rk.c * b;
+          }
+          __syncthreads();
+          double* tmp = M; M = M2; M2 = tmp;
+        }
+        // V^T to global: Vt[P][i][j] = V[j][i]
+        double* vt = Vr + (size_t)P * kSB * kSB;
+        for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) vt[e] = V[(e & 63) * kMP + (e >> 6)];
+        __syncthreads();
+      }
+      if (nround > 0 && (int)gridDim.x <= q) u_update(Vp, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
+      grid_barrier(ctl, ctl + 1);
+      // ---------------- phase B: A' = J^T A J (lower pair blocks, mirrored) ----------------
+      const int atasks = q * (q + 1) / 2;
+      for (int task = blockIdx.x; task < atasks; task += gridDim.x) {
+        double* X = bsm;
+        double* V1t = bsm + kSB * kBP;
+        double* V2t = bsm + 2 * kSB * kBP;
+        double* T = bsm + 3 * kSB * kBP;
+        double acc[4][4];
+        if (task < atasks) {
+          int P1 = (int)((sqrt(8.0 * (double)task + 1.0) - 1.0) * 0.5);
+          while ((P1 + 1) * (P1 + 2) / 2 <= task) ++P1;
+          while (P1 * (P1 + 1) / 2 > task) --P1;
+          const int P2 = task - P1 * (P1 + 1) / 2;
+          int I1, J1, I2, J2;
+          pair_of_round(r, P1, rounds, I1, J1);
+          pair_of_round(r, P2, rounds, I2, J2);
+          // X^T (columns of P2 as rows) so that T = V1^T X is one A B^T product: T[i][j] =
+          // sum_k V1t[i][k] Xt[j][k]
+          load_pair_block(Aold, np, I1, J1, I2, J2, X, true);
+          const double* v1 = Vr + (size_t)P1 * kSB * kSB;
+          const double* v2 = Vr + (size_t)P2 * kSB * kSB;
+          for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) {
+            V1t[(e >> 6) * kBP + (e & 63)] = v1[e];
+            // V2 itself (rows [k][j] = V2t[j][k]): stored so that T V2 = A B^T with B[j][k] = V2[k][j]
+            V2t[(e >> 6) * kBP + (e & 63)] = v2[e];
+          }
+          __syncthreads();
+          bgemm_nt(V1t, X, acc);                    // T = V1^T X
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) T[bfrag_row(i) * kBP + bfrag_col(i, j)] = acc[i][j];
+          __syncthreads();
+          bgemm_nt(T, V2t, acc);                    // A' = T V2
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int gr = sb_row(I1, J1, bfrag_row(i)), gc = sb_row(I2, J2, bfrag_col(i, j));
+              Anew[(int64_t)gr * np + gc] = acc[i][j];
+              if (P1 != P2) Anew[(int64_t)gc * np + gr] = acc[i][j];
+            }
+        }
+        __syncthreads();
+      }
+      // the rest of this round's U blocks (after the A tasks: same CTAs, next free slots)
+      u_update(Vr, r, ndefer, q * q, ((int)blockIdx.x + atasks) % (int)gridDim.x, (int)gridDim.x);
+      grid_barrier(ctl, ctl + 1);
+      double* t = Aold; Aold = Anew; Anew = t;
+      prev_r = r;
+      ++nround;
+    }
+  }
+  if (nround > 0) {                                   // the last round's rotations
+    u_update(Vt + (size_t)((nround & 1) ^ 1) * q * kSB * kSB, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
+    grid_barrier(ctl, ctl + 1);
+  }
+  for (int i = blockIdx.x * kBThreads + threadIdx.x; i < np; i += gridDim.x * kBThreads)
+    wraw[i] = Aold[(int64_t)i * np + i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[0] = sweep;
+    info[1] = sweep < max_sweeps ? 0 : 1;
+  }
+}
+
+// U (n_real x n_real) from the block kernel's U (columns = eigenvectors) in sorted order
+__global__ void gather_ucol_kernel(const double* __restrict__ Ub, int np, int n_real, const int* __restrict__ idx,
+                                   double* __restrict__ U, int64_t ldu) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n_real * n_real) return;
+  const int i = (int)(e / n_real), j = (int)(e % n_real);
+  U[i * ldu + j] = Ub[(int64_t)i * np + idx[j]];
+}
+
 // eigenvalues (diag of the converged A), sorted descending with their indices; n_sort = pow2 >= n
 __global__ void sort_desc_kernel(const double* __restrict__ wraw, int n_real, int n_sort, double* __restrict__ w,
                                  int* __restrict__ idx) {
@@ -232,9 +498,14 @@ __global__ void eig_apply_z_kernel(const double* __restrict__ U, int64_t ldu, in
 }  // namespace
 
 size_t syevj_workspace_bytes(int64_t n, int num_sms) {
-  const int64_t np = (n + 1) & ~(int64_t)1;
-  return (size_t)3 * np * np * sizeof(double) + (size_t)num_sms * sizeof(double) + (size_t)np * (sizeof(double) + 4) +
-         64;
+  const int64_t np = (n + kSB - 1) / kSB * kSB;   // covers the scalar kernel's even padding too
+  return (size_t)3 * np * np * sizeof(double) + (size_t)2 * np * kSB * sizeof(double) /* Vt x 2 */ +
+         (size_t)num_sms * sizeof(double) + (size_t)np * (sizeof(double) + 4) + 64;
+}
+
+bool syevj_block(int64_t n) {
+  static const int env = getenv("FS_SYEVJ_BLOCK") ? atoi(getenv("FS_SYEVJ_BLOCK")) : 1;
+  return env != 0 && n >= 2 * kSB;
 }
 
 int64_t syevj_max_n() { return 8192; }
@@ -250,6 +521,40 @@ cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const 
 cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu, int max_sweeps, double tol,
                   void* ws, int num_sms, int* d_info, cudaStream_t st, int* launches) {
   if (n < 1 || n > syevj_max_n()) return cudaErrorInvalidValue;
+  if (syevj_block(n)) {
+    const int np = (int)((n + kSB - 1) / kSB * kSB);
+    double* A0 = reinterpret_cast<double*>(ws);
+    double* A1 = A0 + (size_t)np * np;
+    double* Ub = A1 + (size_t)np * np;
+    double* Vt = Ub + (size_t)np * np;
+    double* partial = Vt + (size_t)2 * np * kSB;
+    double* wraw = partial + num_sms;
+    int* idx = reinterpret_cast<int*>(wraw + np);
+    unsigned* ctl = reinterpret_cast<unsigned*>(idx + np);
+    cudaError_t e = cudaMemsetAsync(ctl, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    const int64_t tot = (int64_t)np * np;
+    init_eig_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Gp, (int)n, np, A0, Ub);   // U = I
+    static bool battr = false;
+    if (!battr) {
+      cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
+      cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 8192);
+      battr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bjacobi_kernel, kBThreads, kBSmem);
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int npi = np;
+    void* args[] = {&A0, &A1, &Ub, &Vt, &npi, &max_sweeps, &tol, &partial, &ctl, &d_info, &wraw};
+    e = cudaLaunchCooperativeKernel((const void*)bjacobi_kernel, dim3(num_sms), dim3(kBThreads), args, kBSmem, st);
+    if (e != cudaSuccess) return e;
+    int n_sort = 1;
+    while (n_sort < np) n_sort <<= 1;
+    sort_desc_kernel<<<1, 1024, (size_t)n_sort * 12, st>>>(wraw, (int)n, n_sort, w, idx);
+    gather_ucol_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, st>>>(Ub, np, (int)n, idx, U, ldu);
+    if (launches) *launches += 4;
+    return cudaGetLastError();
+  }
   const int np = (int)((n + 1) & ~(int64_t)1);
   double* A0 = reinterpret_cast<double*>(ws);
   double* A1 = A0 + (size_t)np * np;
