@@ -14,6 +14,7 @@
 // the off-diagonal Frobenius norm falls below tol * ||A||_F (fixed-order reduction:
 // deterministic).  Rotations follow Golub & Van Loan sym.schur2 (|t| <= 1, the stable root).
 // A single-CTA bitonic sort orders the eigenpairs.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -24,14 +25,23 @@ namespace {
 
 constexpr int kJThreads = 512;
 
+FS_DEVINL unsigned long long ptx_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct Rot {
   double c, s;
 };
 
 FS_DEVINL void pair_of_round(int r, int k, int np1, int& p, int& q) {
-  // players 0..np1 (np1 = n-1); position 0 of the top row is fixed at player np1
-  p = (k == 0) ? np1 : (r + k) % np1;
-  q = (r - k + np1) % np1;
+  // players 0..np1 (np1 = n-1); position 0 of the top row is fixed at player np1.  0 <= r, k <
+  // np1, so both sums wrap at most once: compare-and-subtract instead of an integer modulo (the
+  // block kernel's inner sweep evaluates this five times per thread and round)
+  const int a = r + k, b = r - k + np1;
+  p = (k == 0) ? np1 : (a >= np1 ? a - np1 : a);
+  q = b >= np1 ? b - np1 : b;
 }
 
 FS_DEVINL Rot schur2(double app, double aqq, double apq) {
@@ -217,12 +227,17 @@ FS_DEVINL void load_pair_block(const double* __restrict__ M, int np, int I1, int
   }
 }
 
+// FS_SYEVJ_DBG: CTA 0's %globaltimer split of the rounds (phase A, barrier, phase B, barrier), ns
+__device__ unsigned long long g_bj_time[4];
+
 __global__ void __launch_bounds__(kBThreads, 1)
 bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restrict__ U, double* __restrict__ Vt,
                int np, int max_sweeps, double tol, double* __restrict__ partial, unsigned* ctl, int* info,
-               double* __restrict__ wraw) {
+               double* __restrict__ wraw, int dbg) {
   extern __shared__ double bsm[];
   __shared__ double red[kBThreads / 32];
+  unsigned long long tA = 0, tB1 = 0, tB = 0, tB2 = 0, t0 = 0, t1 = 0;
+  auto now = [&]() -> unsigned long long { return dbg ? ptx_globaltimer() : 0ull; };
   const int nblk = np / kBB, q = nblk / 2, rounds = nblk - 1;
   double* Aold = A0;
   double* Anew = A1;
@@ -284,6 +299,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
     const double off2 = frob(Aold, true);
     if (!(off2 > tol * tol * fro2)) break;
     for (int r = 0; r < rounds; ++r) {
+      t0 = now();
       // ---------------- phase A: inner sweep of each pair's super-block; meanwhile the other
       // CTAs apply the PREVIOUS round's rotations to U (U feeds nothing inside the iteration) ----
       double* Vr = Vt + (size_t)(nround & 1) * q * kSB * kSB;             // this round's V^T
@@ -302,18 +318,27 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
         }
         __syncthreads();
         // every warp computes all 32 rotations of an inner round (lane k: pair k) and takes the
-        // ones it needs by shuffle: one CTA barrier per inner round
+        // ones it needs by shuffle: one CTA barrier per inner round.  The first round of a sweep
+        // runs the full cyclic sweep of the super-block (63 rounds: pairs inside I, inside J and
+        // across); later rounds only the 1024 cross pairs (I_k, J_{(k+t) mod 32}), 32 rounds —
+        // every index pair is still rotated at least once per outer sweep, as in cyclic Jacobi,
+        // and the inner sweeps (the latency-bound phase) take half the rounds
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        for (int ir = 0; ir < kSB - 1; ++ir) {
+        const bool full = r == 0;
+        auto inner_pair = [&](int ir, int k, int& p, int& qq) {
+          if (full) pair_of_round(ir, k, kSB - 1, p, qq);
+          else { p = k; qq = kBB + ((k + ir) & (kBB - 1)); }
+        };
+        for (int ir = 0; ir < (full ? kSB - 1 : kBB); ++ir) {
           int pk, qk;
-          pair_of_round(ir, lane, kSB - 1, pk, qk);
+          inner_pair(ir, lane, pk, qk);
           const Rot Rk = schur2(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
           // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane)
 #pragma unroll
           for (int i = 0; i < kBB / (kBThreads / 32); ++i) {
             const int k1 = warp + (kBThreads / 32) * i;
             int p1, q1;
-            pair_of_round(ir, k1, kSB - 1, p1, q1);
+            inner_pair(ir, k1, p1, q1);
             const Rot R1{__shfl_sync(0xffffffffu, Rk.c, k1), __shfl_sync(0xffffffffu, Rk.s, k1)};
             const double bpp = M[p1 * kMP + pk], bpq = M[p1 * kMP + qk], bqp = M[q1 * kMP + pk],
                          bqq = M[q1 * kMP + qk];
@@ -341,7 +366,9 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
         __syncthreads();
       }
       if (nround > 0 && (int)gridDim.x <= q) u_update(Vp, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
+      t1 = now(); tA += t1 - t0; t0 = t1;
       grid_barrier(ctl, ctl + 1);
+      t1 = now(); tB1 += t1 - t0; t0 = t1;
       // ---------------- phase B: A' = J^T A J (lower pair blocks, mirrored) ----------------
       const int atasks = q * (q + 1) / 2;
       for (int task = blockIdx.x; task < atasks; task += gridDim.x) {
@@ -389,7 +416,9 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       }
       // the rest of this round's U blocks (after the A tasks: same CTAs, next free slots)
       u_update(Vr, r, ndefer, q * q, ((int)blockIdx.x + atasks) % (int)gridDim.x, (int)gridDim.x);
+      t1 = now(); tB += t1 - t0; t0 = t1;
       grid_barrier(ctl, ctl + 1);
+      t1 = now(); tB2 += t1 - t0;
       double* t = Aold; Aold = Anew; Anew = t;
       prev_r = r;
       ++nround;
@@ -398,6 +427,11 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
   if (nround > 0) {                                   // the last round's rotations
     u_update(Vt + (size_t)((nround & 1) ^ 1) * q * kSB * kSB, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
     grid_barrier(ctl, ctl + 1);
+  }
+  if (dbg && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == (unsigned)q)) {
+    const int o = blockIdx.x == 0 ? 0 : 2;
+    if (o == 0) { g_bj_time[0] = tA; g_bj_time[1] = tB1 + tB2; g_bj_time[2] = tB; }
+    else g_bj_time[3] = tA;
   }
   for (int i = blockIdx.x * kBThreads + threadIdx.x; i < np; i += gridDim.x * kBThreads)
     wraw[i] = Aold[(int64_t)i * np + i];
@@ -545,7 +579,9 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bjacobi_kernel, kBThreads, kBSmem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int npi = np;
-    void* args[] = {&A0, &A1, &Ub, &Vt, &npi, &max_sweeps, &tol, &partial, &ctl, &d_info, &wraw};
+    static const int dbg = getenv("FS_SYEVJ_DBG") ? atoi(getenv("FS_SYEVJ_DBG")) : 0;
+    int dbgi = dbg;
+    void* args[] = {&A0, &A1, &Ub, &Vt, &npi, &max_sweeps, &tol, &partial, &ctl, &d_info, &wraw, &dbgi};
     e = cudaLaunchCooperativeKernel((const void*)bjacobi_kernel, dim3(num_sms), dim3(kBThreads), args, kBSmem, st);
     if (e != cudaSuccess) return e;
     int n_sort = 1;
@@ -553,6 +589,13 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
     sort_desc_kernel<<<1, 1024, (size_t)n_sort * 12, st>>>(wraw, (int)n, n_sort, w, idx);
     gather_ucol_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, st>>>(Ub, np, (int)n, idx, U, ldu);
     if (launches) *launches += 4;
+    if (dbg) {
+      unsigned long long h[4] = {};
+      cudaStreamSynchronize(st);
+      cudaMemcpyFromSymbol(h, g_bj_time, sizeof h);
+      fprintf(stderr, "bjacobi CTA 0: phase A %.2f ms, barriers %.2f ms, phase B %.2f ms; CTA q (U work) %.2f ms\n",
+              h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6);
+    }
     return cudaGetLastError();
   }
   const int np = (int)((n + 1) & ~(int64_t)1);
