@@ -983,3 +983,37 @@ def test_ill_conditioned_geometric_spectrum(fsb, lam):
         sol32 = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32), precision=prec)
         bound = 64 * 2.0 ** -24 * 1.0 / lam          # u32 sigma_max^2 / lam (sigma_max = 1), widened
         assert O.rel_err(sol32.x, ref32.x) <= max(1e-6, bound), (prec, O.rel_err(sol32.x, ref32.x))
+
+
+@pytest.mark.parametrize("case", ["rank_deficient", "geometric", "clustered"])
+def test_block_jacobi_hard_spectra(fsb, case):
+    """The block Jacobi path (n >= 128) on spectra that stress it: 156 zero eigenvalues (rank 100),
+    a geometric decay over 12 decades, and tight clusters; same contract as LAPACK eigh."""
+    from paper_2310_17556_b200 import _lib
+    n = 256 if case != "geometric" else 200
+    rng = np.random.Generator(np.random.PCG64(7))
+    if case == "rank_deficient":
+        A = rng.standard_normal((n, 100))
+        G = A @ A.T
+    else:
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = (np.logspace(0, -12, n) if case == "geometric"
+               else np.repeat([3.0, 2.0, 1.0, 0.5], n // 4) * (1 + 1e-10 * rng.standard_normal(n)))
+        G = (Q * lam) @ Q.T
+        G = 0.5 * (G + G.T)
+    dev = torch.device("cuda", 0)
+    Gp = torch.from_numpy(G[np.tril_indices(n)].copy()).to(dev)
+    ctx = _lib.context_for(0, n, 8)
+    w = torch.empty(n, dtype=torch.float64, device=dev)
+    U = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_syevj_packed(ctx.handle, Gp.data_ptr(), n, w.data_ptr(), U.data_ptr(), n, ctypes.byref(sweeps),
+                                 torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, ctx.last_error()
+    w, U = w.cpu().numpy(), U.cpu().numpy()
+    ref = np.linalg.eigvalsh(G)[::-1]
+    scale = np.abs(ref).max()
+    assert np.all(np.diff(w) <= 0)
+    assert np.abs(w - ref).max() <= 1e-12 * scale
+    assert np.abs(U.T @ U - np.eye(n)).max() <= 1e-12
+    assert np.abs(U @ np.diag(w) @ U.T - G).max() <= 1e-12 * scale
