@@ -674,7 +674,17 @@ def _svda(S: ScoreMatrix, want_factors: bool, system: DampedSystem | None = None
         Uleft = _apply_rows(Zt[:r], Qt).T.contiguous() if r else torch.zeros((n, 0), dtype=torch.float64,
                                                                                device=X.device)
         return _factor_solve(system, Uleft, sigma[:r], diagnostics)
-    sigma, U, Zt, Qt, r = _svda_core(S)
+    Gp = gram_packed(S, 0.0, "fp64")
+    fast = _svda_gram_route(Gp, n)
+    if fast is not None:
+        sigma, U = fast
+        if not want_factors:
+            return _factor_solve(system, U, sigma, diagnostics)
+        Vt = _apply_rows((U.T / sigma[:, None]).contiguous(), S.tensor)   # V^T = diag(1/sigma) U^T S
+        if S.host_origin:
+            return ThinSvd(U=U.cpu().numpy(), sigma=sigma.cpu().numpy(), V=np.ascontiguousarray(Vt.T.cpu().numpy()))
+        return ThinSvd(U=U, sigma=sigma, V=Vt.T)
+    sigma, U, Zt, Qt, r = _svda_core(S, Gp)
     if not want_factors:
         return _factor_solve(system, U[:, :r].contiguous(), sigma[:r], diagnostics)
     dev = S.tensor.device
@@ -691,13 +701,52 @@ def _svda(S: ScoreMatrix, want_factors: bool, system: DampedSystem | None = None
     return ThinSvd(U=Uo, sigma=so, V=V)
 
 
-def _svda_core(S: ScoreMatrix):
+# The svd route's well-conditioned fast path: when the exact-product fp64 Gram G = S S^T certifies
+# cond(S)^2 = w_max / w_min <= 1/SVDA_GRAM_RATIO (cond(S) <= 100), the thin SVD comes from G's eigendecomposition
+# (sigma = sqrt(w), U = G's eigenvectors — the Gram-based algorithm class of the paper's cuSOLVER
+# gesvda).  G's rounding error is a few u ||S||^2, so each sigma_i^2 carries a relative error of
+# at most ~u w_max / w_i <= 1e4 u ~ 2e-12 (V's orthonormality likewise): well inside the 1e-8 that
+# dgesdd's results are compared at.
+# Anything worse conditioned (or rank deficient) takes the shifted CholeskyQR3 + one-sided Jacobi
+# route, whose accuracy does not depend on cond(S).  FS_SVDA_GRAM=0 forces that route.
+SVDA_GRAM_RATIO = 1e-4
+
+
+def _syevj_device(Gp: torch.Tensor, n: int):
+    """(w descending, U) of the packed symmetric Gram on the device (fs_syevj_packed)."""
+    dev = Gp.device
+    ctx = _lib.context_for(dev.index, n, 1)
+    w = torch.empty(n, dtype=torch.float64, device=dev)
+    U = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sweeps = ctypes.c_int(0)
+    rc = ctx.lib.fs_syevj_packed(ctx.handle, Gp.data_ptr(), n, w.data_ptr(), U.data_ptr(), n, ctypes.byref(sweeps),
+                                 _stream(dev))
+    if rc == _lib.FS_ENOCONV:
+        raise FactorizationError(f"eigendecomposition did not converge: {ctx.last_error()}")
+    _check(ctx, rc, "fs_syevj_packed")
+    return w, U
+
+
+def _svda_gram_route(Gp: torch.Tensor, n: int):
+    """(sigma, U) from the Gram when it certifies a well-conditioned S, else None."""
+    import os
+    if os.environ.get("FS_SVDA_GRAM", "1") == "0" or n > 8192:
+        return None
+    w, U = _syevj_device(Gp, n)
+    wh = w.cpu().numpy()
+    if not (wh[0] > 0.0 and wh[-1] >= SVDA_GRAM_RATIO * wh[0]):
+        return None
+    return torch.sqrt(w), U
+
+
+def _svda_core(S: ScoreMatrix, Gp: torch.Tensor | None = None):
     """-> (sigma descending, W (n x n), Z^T (n x n), Q^T (n x m fp64), kept rank r) with S = L Q^T,
-    L = W diag(sigma) Z^T."""
+    L = W diag(sigma) Z^T.  Gp: S's fp64 Gram when the caller has it already."""
     X = S.tensor
     n, m = S.n, S.m
     dev = X.device
-    Gp = gram_packed(S, 0.0, "fp64")
+    if Gp is None:
+        Gp = gram_packed(S, 0.0, "fp64")
     diag = torch.arange(n, device=dev, dtype=torch.int64)
     fro2 = float(Gp[diag * (diag + 1) // 2 + diag].sum())
     if fro2 == 0.0:          # exactly zero scores: every singular value is an exact zero (dropped)
