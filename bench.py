@@ -369,6 +369,25 @@ def run_b200(args, rank, world, local):
             torch.cuda.synchronize()
             modes[name] = {"ms": e0.elapsed_time(e1) / reps, "precision": sol.precision,
                            "rel_residual": sol.rel_residual, "x": sol.x.cpu().numpy()}
+    # ---- the paper's comparison on the same system: chol vs the eigh and svd routes (all GPU) ----
+    routes = None
+    if not sharded and args.modes:
+        routes = {"chol_ms": None}
+        for name, fn in (("eigh", fsb.solve_svd_eigh), ("svd", fsb.solve_svd_direct)):
+            sol = fn(system)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            reps = 2
+            e0.record(stream)
+            for _ in range(reps):
+                sol = fn(system)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            routes[f"{name}_ms"] = e0.elapsed_time(e1) / reps
+            routes[f"{name}_rel_residual"] = sol.rel_residual
+            modes[f"route {name}"] = {"ms": routes[f"{name}_ms"], "precision": sol.precision,
+                                      "rel_residual": sol.rel_residual, "x": sol.x.cpu().numpy()}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -509,6 +528,9 @@ def run_b200(args, rank, world, local):
         "roofline": roofline,
         "roofline_gemv": gemv or None,
         "stage_ms": st,
+        "routes": routes if routes is None else {**routes, "chol_ms": ms_per_step,
+                                                 "note": "solve_svd_eigh / solve_svd_direct with their defaults on "
+                                                         "the same device-resident system (paper: chol vs eigh/svda)"},
         "rel_residual": rels[-1],
         "parity": parity,
         "cpu_baseline": cpu,
