@@ -8,8 +8,11 @@
 // One CTA of 1024 threads; deterministic (fixed reduction order).
 #include <stdlib.h>
 
+#include <string.h>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace fs {
 namespace {
@@ -234,12 +237,196 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   }
 }
 
+// Cluster variant (nb <= 16 blocks, one CTA per block, one thread-block cluster): the same
+// substitution order, but every published block of z travels CTA-to-CTA through distributed
+// shared memory — st.async of the 64 values into each consumer's buffer with that consumer's
+// mbarrier completing on the bytes — instead of a global store, a release flag and an acquire
+// poll on the other side.  A hop (receive, two 64 x 64 smem GEMVs, push) drops to ~1 us.
+constexpr int kCMaxNb = 16;
+constexpr size_t kClusterSmem = 3 * (size_t)kNB * kSP * sizeof(double) + 2 * (size_t)kCMaxNb * kNB * sizeof(double);
+
+FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
+               "r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(kFT, 1)
+trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
+                         double* __restrict__ z, const int64_t* status) {
+  extern __shared__ double csm[];
+  double* LI = csm;
+  double* LP = LI + kNB * kSP;
+  double* LN = LP + kNB * kSP;
+  double* zf = LN + kNB * kSP;                 // [kCMaxNb][64] published z' blocks (forward)
+  double* zb = zf + kCMaxNb * kNB;             // [kCMaxNb][64] published z blocks (backward)
+  __shared__ __align__(8) uint64_t fbar[kCMaxNb], bbar[kCMaxNb];
+  __shared__ double t[kNB];
+  __shared__ double part[kFW][kNB];
+  const bool stop = status && *(volatile const int64_t*)status != 0;   // uniform over the cluster
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (int)((n + kNB - 1) / kNB);
+  const int B = (int)fs::ptx::cluster_ctarank();
+  const int64_t r0 = (int64_t)B * kNB;
+  const int b = (int)(n - r0 < kNB ? n - r0 : kNB);
+  const int bn = B + 1 < nb ? (int)(n - r0 - kNB < kNB ? n - r0 - kNB : kNB) : 0;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < nb; ++c) {
+      fs::ptx::mbar_init(&fbar[c], 1);
+      fs::ptx::mbar_init(&bbar[c], 1);
+    }
+    fs::ptx::fence_mbar_init();
+    // each barrier completes once: on the 64 values of the block it names (one local arrival
+    // carries the expected bytes, so a peer's bytes may land before it)
+    for (int c = 0; c < B; ++c) fs::ptx::mbar_arrive_expect_tx(&fbar[c], kNB * 8);
+    for (int c = B + 1; c < nb; ++c) fs::ptx::mbar_arrive_expect_tx(&bbar[c], kNB * 8);
+  }
+  for (int e = threadIdx.x; e < kNB * kNB; e += kFT) {
+    const int r = e >> 6, c = e & 63;
+    LI[r * kSP + c] = Linv[(size_t)B * kNB * kNB + e];
+    LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
+    LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
+  }
+  fs::ptx::cluster_sync();                      // barriers armed everywhere before any push
+  auto push = [&](double* buf, uint64_t* bars, int slot, int dst, double val, int c) {
+    const uint32_t a = fs::ptx::mapa(fs::ptx::smem_u32(buf + slot * kNB + c), (uint32_t)dst);
+    const uint32_t br = fs::ptx::mapa(fs::ptx::smem_u32(&bars[slot]), (uint32_t)dst);
+    st_async_f64(a, val, br);
+  };
+  if (!stop) {
+    // ---------------- forward ----------------
+    double acc[kNB / kFW];
+#pragma unroll
+    for (int i = 0; i < kNB / kFW; ++i) acc[i] = 0.0;
+    for (int C = 0; C < B; ++C) {
+      fs::ptx::mbar_wait(&fbar[C], 0);
+      const double z0 = zf[C * kNB + lane], z1 = zf[C * kNB + lane + 32];
+      const bool crit = C == B - 1;
+#pragma unroll
+      for (int i = 0; i < kNB / kFW; ++i) {
+        const int r = warp + kFW * i;
+        if (crit) {
+          acc[i] = fma(LP[r * kSP + lane], z0, acc[i]);
+          acc[i] = fma(LP[r * kSP + lane + 32], z1, acc[i]);
+        } else if (r < b) {
+          const double* row = L + (r0 + r) * ld + (int64_t)C * kNB;
+          acc[i] = fma(row[lane], z0, acc[i]);
+          acc[i] = fma(row[lane + 32], z1, acc[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kNB / kFW; ++i) {
+      const double sum = warp_sum(acc[i]);
+      const int r = warp + kFW * i;
+      if (lane == 0) t[r] = (r < b) ? z[r0 + r] - sum : 0.0;
+    }
+    __syncthreads();
+    {                                           // z'_B = Linv_BB t, kept locally and pushed to B+1..
+      const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
+      double sum = 0.0;
+      for (int c = q; c <= r; c += 4) sum = fma(LI[r * kSP + c], t[c], sum);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (q == 0) {
+        const double zr = r < b ? sum : 0.0;
+        zf[B * kNB + r] = zr;
+        for (int d = B + 1; d < nb; ++d) push(zf, fbar, B, d, zr, r);
+      }
+    }
+    __syncthreads();
+    // ---------------- backward ----------------
+    double a0 = 0.0, a1 = 0.0;
+    for (int C = nb - 1; C > B; --C) {
+      fs::ptx::mbar_wait(&bbar[C], 0);
+      const int64_t c0 = (int64_t)C * kNB;
+      const int bc = (int)(n - c0 < kNB ? n - c0 : kNB);
+      if (C == B + 1) {
+        for (int r = warp; r < bn; r += kFW) {
+          const double zi = zb[C * kNB + r];
+          a0 = fma(LN[r * kSP + lane], zi, a0);
+          a1 = fma(LN[r * kSP + lane + 32], zi, a1);
+        }
+      } else {
+        for (int r = warp; r < bc; r += kFW) {
+          const double zi = zb[C * kNB + r];
+          const double* row = L + (c0 + r) * ld + r0;
+          if (lane < b) a0 = fma(row[lane], zi, a0);
+          if (lane + 32 < b) a1 = fma(row[lane + 32], zi, a1);
+        }
+      }
+    }
+    part[warp][lane] = a0;
+    part[warp][lane + 32] = a1;
+    __syncthreads();
+    if (threadIdx.x < kNB) {
+      const int c = threadIdx.x;
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kFW; ++w) sum += part[w][c];
+      t[c] = (c < b) ? zf[B * kNB + c] - sum : 0.0;
+    }
+    __syncthreads();
+    {                                           // z_B = Linv_BB^T t -> z, pushed to 0..B-1
+      const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
+      double sum = 0.0;
+      for (int r = c + q; r < kNB; r += 4) sum = fma(LI[r * kSP + c], t[r], sum);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if (q == 0) {
+        if (c < b) z[r0 + c] = sum;
+        const double zc = c < b ? sum : 0.0;
+        for (int d = 0; d < B; ++d) push(zb, bbar, B, d, zc, c);
+      }
+    }
+  }
+  fs::ptx::cluster_sync();                      // no CTA leaves while a peer may still push to it
+}
+
 }  // namespace
 
 cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
                       const int64_t* d_status, cudaStream_t st, int* launches) {
   const int64_t nb = (n + kNB - 1) / kNB;
   static const int env = getenv("FS_TRSV_FLAGS") ? atoi(getenv("FS_TRSV_FLAGS")) : 1;
+  static const int cl_env = getenv("FS_TRSV_CLUSTER") ? atoi(getenv("FS_TRSV_CLUSTER")) : 1;
+  if (env && cl_env && nb >= 2 && nb <= kCMaxNb) {
+    // one cluster of nb CTAs (non-portable above 8); the launch reports when the GPU cannot
+    // schedule that cluster size, and the flag-chained kernel below takes over
+    static int attr = -1;
+    if (attr < 0) {
+      attr = cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kClusterSmem) == cudaSuccess &&
+                     cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                          1) == cudaSuccess
+                 ? 1 : 0;
+      cudaGetLastError();
+    }
+    if (attr == 1) {
+      cudaLaunchConfig_t cfg;
+      memset(&cfg, 0, sizeof cfg);
+      cfg.gridDim = dim3((unsigned)nb);
+      cfg.blockDim = dim3(kFT);
+      cfg.dynamicSmemBytes = kClusterSmem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)nb;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ok_clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&ok_clusters, trsv_pair_cluster_kernel, &cfg) == cudaSuccess &&
+          ok_clusters >= 1) {
+        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status);
+        if (e == cudaSuccess) {
+          if (launches) *launches += 1;
+          return cudaGetLastError();
+        }
+      }
+      cudaGetLastError();
+    }
+  }
   // every block's CTA must be resident while earlier ones spin on its flags: nb <= (CTAs per SM)
   // x SMs (2 per SM: ~100 KB of shared memory each; n <= 18944 on 148 SMs).  Linv is the potrf
   // scratch, the flags sit at its end.

@@ -99,13 +99,16 @@ def test_ring_syrk_gram_is_bit_identical_and_solves(gpu, tmp_path, n, m):
     assert O.rel_err(x2, reference(n, m).x) <= 1e-6
 
 
-def test_single_cta_trsv_pair_matches_flag_chained(gpu, tmp_path):
-    n, m = 1000, 60000
-    x1, _, i1 = run_case(tmp_path, {"FS_TRSV_FLAGS": "0"}, n, m, "f16x2", refine=2)
-    x2, _, i2 = run_case(tmp_path, {"FS_TRSV_FLAGS": "1"}, n, m, "f16x2", refine=2)
+@pytest.mark.parametrize("n", [130, 1000])
+def test_trsv_pair_variants_agree(gpu, tmp_path, n):
+    """single-CTA, flag-chained multi-CTA and cluster (DSMEM) TRSV pairs in the refinement steps:
+    the same z up to rounding order (x to the fp64 solve's 1e-10)."""
+    m = 60000
     ref = reference(n, m)
-    assert O.rel_err(x1, ref.x) <= 1e-10 and O.rel_err(x2, ref.x) <= 1e-10
-    assert i2["rel_residual"] <= 1e-10
+    for env in ({"FS_TRSV_FLAGS": "0"}, {"FS_TRSV_CLUSTER": "0"}, {}):
+        x, _, info = run_case(tmp_path, env, n, m, "f16x2", refine=2)
+        assert O.rel_err(x, ref.x) <= 1e-10, (env, O.rel_err(x, ref.x))
+        assert info["rel_residual"] <= 1e-10
 
 
 POTRF_CASE = r'''
