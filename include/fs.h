@@ -7,8 +7,13 @@
  *
  * Every pointer argument named S, v, x, W, L, u, z, y, r is a DEVICE pointer;
  * every call is ordered on the given CUDA stream (cudaStream_t passed as void*,
- * NULL = legacy default stream).  No call allocates device memory except
- * fs_ctx_create.  Plain C types only: no torch, no C++ in the signatures.
+ * NULL = legacy default stream).  Device memory: fs_ctx_create allocates every
+ * workspace of the fp64 chol path; a mode's larger workspaces are allocated by the
+ * context on the FIRST call that needs them and kept for later calls (the tensor-core
+ * modes' tiled copy of S, capped at 16 GB; the eigh route's Jacobi buffers; the svd
+ * route's scratch; the host entry's device copy of S) — a caller that must not
+ * allocate inside a timed or captured region warms the context up with one call
+ * first.  Plain C types only: no torch, no C++ in the signatures.
  *
  * This ABI replaces the numpy/scipy calls of the reference package
  * (/root/reference/pkg/src/fisher_solve/, cited per entry point below).  The
@@ -67,8 +72,9 @@ void fs_ctx_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);
 /* Device bytes one solve of (n, m) in (dtype, precision) touches besides S, v, x
  * (feeds WorkspaceMeter, core.py:63-96; a context may own more to serve any smaller problem).
- * Not counted: the tensor-core modes' re-laid-out copy of S itself (F16X2: 4 n m bytes, TF32X3:
- * 8 n m bytes; allocated on first use of that mode, sized for the context's n_max x m_max). */
+ * Not counted: the tensor-core modes' re-laid-out copy of S itself (F16X2 and TF32X3: 4 n m
+ * bytes, capped at 16 GB with a K-chunked Gram beyond; allocated on first use of that mode,
+ * sized for the context's n_max x m_max). */
 size_t fs_workspace_bytes(int64_t n, int64_t m, int dtype, int precision);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t fs_launch_count(const fs_ctx* ctx);
