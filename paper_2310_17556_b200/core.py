@@ -98,6 +98,67 @@ def _coerce_damping(lam) -> float:       # core.py:99-105
     return lam
 
 
+# Pageable host arrays: the driver's own pageable copy runs at ~11 GB/s (measured, 4.1 GB in
+# 374 ms).  Large ones are staged instead: worker threads copy row chunks into a ring of pinned
+# buffers (numpy copyto releases the GIL, so the threads copy in parallel) while the previous
+# chunk's DMA to the device runs.
+_STAGE_MIN_BYTES = 64 << 20
+_STAGE_CHUNK_BYTES = 64 << 20
+_STAGE_BUFFERS = 3
+_stage_state: dict = {}
+
+
+def _stage_pool():
+    if "pool" not in _stage_state:
+        import concurrent.futures
+        import os
+        workers = max(1, min(8, (os.cpu_count() or 2) - 1))
+        _stage_state["pool"] = concurrent.futures.ThreadPoolExecutor(max_workers=workers)
+        _stage_state["workers"] = workers
+        _stage_state["bufs"] = [torch.empty(_STAGE_CHUNK_BYTES, dtype=torch.uint8, pin_memory=True)
+                                for _ in range(_STAGE_BUFFERS)]
+        _stage_state["events"] = [None] * _STAGE_BUFFERS    # last DMA reading each buffer (any call)
+        import threading
+        _stage_state["lock"] = threading.Lock()
+    return _stage_state["pool"], _stage_state["workers"], _stage_state["bufs"]
+
+
+def _upload_staged(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """dst (CUDA, rows of a 2-D view) <- src (pageable CPU, C-contiguous 2-D), row chunks through
+    pinned staging buffers; ordered on the current stream, returns once the last chunk is queued."""
+    pool, workers, bufs = _stage_pool()
+    rows, cols = int(src.shape[0]), int(src.shape[1])
+    row_bytes = cols * src.element_size()
+    per = max(1, _STAGE_CHUNK_BYTES // row_bytes)
+    if per * row_bytes > _STAGE_CHUNK_BYTES:        # one row larger than a buffer: plain copy
+        dst.copy_(src)
+        return
+    stream = torch.cuda.current_stream(dst.device)
+    src_np = src.numpy()
+    with _stage_state["lock"]:
+        _staged_chunks(pool, workers, bufs, _stage_state["events"], src, src_np, dst, rows, cols, row_bytes, per,
+                       stream)
+
+
+def _staged_chunks(pool, workers, bufs, events, src, src_np, dst, rows, cols, row_bytes, per, stream):
+    for i, r0 in enumerate(range(0, rows, per)):
+        r1 = min(rows, r0 + per)
+        k = i % len(bufs)
+        if events[k] is not None:
+            events[k].synchronize()                 # the DMA that last read this buffer is done
+        view = bufs[k][: (r1 - r0) * row_bytes].view(src.dtype).view(r1 - r0, cols)
+        vnp = view.numpy()
+        step = -(-(r1 - r0) // workers)
+        futs = [pool.submit(np.copyto, vnp[a:a + step], src_np[r0 + a:min(r1, r0 + a + step)])
+                for a in range(0, r1 - r0, step)]
+        for f in futs:
+            f.result()
+        dst[r0:r1].copy_(view, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        events[k] = ev
+
+
 def _to_device_tensor(a, name: str, device, force_copy: bool = False, validate: bool = True) -> torch.Tensor:
     """Coerce to a float32/float64 (or complex64/complex128) CUDA tensor and validate finiteness
     (core.py:108-119).
@@ -126,7 +187,12 @@ def _to_device_tensor(a, name: str, device, force_copy: bool = False, validate: 
         if force_copy or not (t.is_cuda and t.device == dev and t.stride(1) == 1 and t.stride(0) % per16 == 0
                               and t.data_ptr() % 16 == 0):
             buf = torch.empty((t.shape[0], ld), dtype=t.dtype, device=dev)
-            t = buf[:, : t.shape[1]].copy_(t, non_blocking=True)
+            if (not t.is_cuda and not t.is_pinned() and t.is_contiguous() and not t.is_complex()
+                    and t.numel() * t.element_size() >= _STAGE_MIN_BYTES):
+                _upload_staged(t, buf[:, : t.shape[1]])
+                t = buf[:, : t.shape[1]]
+            else:
+                t = buf[:, : t.shape[1]].copy_(t, non_blocking=True)
     else:
         src_ptr = a.data_ptr() if isinstance(a, torch.Tensor) else None
         t = t.to(dev, non_blocking=True).contiguous()

@@ -390,3 +390,18 @@ def test_layer_structured_heavy_tailed_scores_need_no_recompute(fsb):
     sol = fsb.solve_chol(system, precision="f16x2", refine=0)
     assert ctx.fallbacks() == f0
     assert O.rel_err(sol.x.cpu().numpy(), ref.x) <= 1e-6, O.rel_err(sol.x.cpu().numpy(), ref.x)
+
+
+@pytest.mark.parametrize("dt,m", [(np.float32, 600001), (np.float64, 160003)])
+def test_staged_pageable_upload_is_exact(fsb, dt, m):
+    """Pageable host arrays >= 64 MB go through the pinned staging ring (parallel host copies
+    overlapped with the DMA); the device copy must be bit-exact, pitch padding included, and the
+    caller's array is free to change right after construction."""
+    rng = np.random.Generator(np.random.PCG64(m))
+    S = rng.standard_normal((60, m)).astype(dt)
+    assert S.nbytes >= 64 << 20
+    sm = fsb.ScoreMatrix(S)
+    S[:] = 0.0                                        # the frozen copy must not see this
+    got = sm.tensor.cpu().numpy()
+    ref = rng.__class__(np.random.PCG64(m)).standard_normal((60, m)).astype(dt)
+    assert np.array_equal(got, ref)
