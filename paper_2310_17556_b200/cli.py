@@ -17,6 +17,7 @@ m x m system (small m) and against each other.
 from __future__ import annotations
 
 import argparse
+import os
 import enum
 import math
 import statistics
@@ -328,6 +329,18 @@ def build_parser() -> argparse.ArgumentParser:
     return p
 
 
+def _thread_limit():
+    """FISHER_SOLVE_THREADS (cli.py:259-266): host-thread cap, 0 or unset = automatic; a negative
+    value is an error.  Here it caps the host-side threads (torch's CPU pool), the GPU is unaffected."""
+    raw = os.environ.get("FISHER_SOLVE_THREADS", "").strip()
+    if not raw:
+        return None
+    limit = int(raw)
+    if limit < 0:
+        raise ValueError(f"FISHER_SOLVE_THREADS must be >= 0, got {limit}")
+    return limit or None
+
+
 def run_cli(argv=None) -> int:
     parser = build_parser()
     try:
@@ -336,6 +349,10 @@ def run_cli(argv=None) -> int:
         return exc.code if isinstance(exc.code, int) else 2
     from .core import FactorizationError
     try:
+        limit = _thread_limit()
+        if limit is not None:
+            import torch
+            torch.set_num_threads(limit)
         return args.func(args)
     except (ValueError, OSError, FactorizationError) as exc:
         print(f"fisher-solve-b200: error: {exc}", file=sys.stderr)
