@@ -106,8 +106,14 @@ FS_DEVINL int ld_acq(const int* p) {
 }
 FS_DEVINL void st_rel(int* p, int v) { asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
 FS_DEVINL void wait_flag(const int* p) {
-  if (threadIdx.x == 0)
-    while (ld_acq(p) == 0) __nanosleep(20);
+  if (threadIdx.x == 0 && ld_acq(p) == 0) {
+    // a peer that never publishes is a bug: trap after ~20 s instead of hanging the device
+    const uint64_t t0 = fs::ptx::globaltimer();
+    while (ld_acq(p) == 0) {
+      __nanosleep(20);
+      if (fs::ptx::globaltimer() - t0 > 20000000000ull) __trap();
+    }
+  }
   __syncthreads();
 }
 
