@@ -153,7 +153,7 @@ def run_potrf(env, n, bad=-1):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("n,minn", [(700, "300"), (1100, "300"), (4500, "4096")])
+@pytest.mark.parametrize("n,minn", [(700, "300"), (1100, "300"), (4500, "4096"), (6145, "6144")])
 def test_blocked_potrf_matches_lapack(gpu, n, minn):
     """256-wide block columns: diagonal blocks by the persistent kernel, GEMM-form panel TRSM, DMMA
     trailing tiles (FS_POTRF_BLOCKED_MINN lowers the size where it takes over)."""
