@@ -112,7 +112,7 @@ def _stage_pool():
     if "pool" not in _stage_state:
         import concurrent.futures
         import os
-        workers = max(1, min(8, (os.cpu_count() or 2) - 1))
+        workers = int(os.environ.get("FS_STAGE_WORKERS", "0")) or max(1, min(8, (os.cpu_count() or 2) - 1))
         _stage_state["pool"] = concurrent.futures.ThreadPoolExecutor(max_workers=workers)
         _stage_state["workers"] = workers
         _stage_state["bufs"] = [torch.empty(_STAGE_CHUNK_BYTES, dtype=torch.uint8, pin_memory=True)
