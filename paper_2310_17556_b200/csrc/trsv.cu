@@ -6,6 +6,7 @@
 // potrf already produced: each block step is an off-diagonal GEMV (coalesced row reads of L,
 // L2-resident) followed by a 64x64 GEMV with Linv_BB — no dependent global-load chains.
 // One CTA of 1024 threads; deterministic (fixed reduction order).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <string.h>
@@ -127,7 +128,7 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   double* LI = fsm;                            // Linv_BB
   double* LP = LI + kNB * kSP;                 // L_{B,B-1}: the forward step on the critical path
   double* LN = LP + kNB * kSP;                 // L_{B+1,B}: the backward step on the critical path
-  __shared__ double t[kNB], zin[kNB];
+  __shared__ double t[kNB], zin[kNB], ub[kNB];
   __shared__ double part[kFW][kNB];
   if (status && *(volatile const int64_t*)status != 0) return;   // uniform: every CTA returns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -143,23 +144,39 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
     LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
     LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
   }
+  if (threadIdx.x < kNB) ub[threadIdx.x] = threadIdx.x < b ? z[r0 + threadIdx.x] : 0.0;   // u_B, off the chain
   __syncthreads();
   // ---------------- forward: rows r = warp + 8 i of block B, columns lane, lane + 32 ----------------
   double acc[kNB / kFW];
 #pragma unroll
   for (int i = 0; i < kNB / kFW; ++i) acc[i] = 0.0;
-  for (int C = 0; C < B - 1; ++C) {            // off the critical path: streamed from L2 as published
+  // off the critical path: the L_BC rows of the next published block are loaded (registers)
+  // before waiting for its flag, so the L2 latency overlaps the wait
+  double lrow[kNB / kFW][2];
+  auto load_rows = [&](int C, double (&dst)[kNB / kFW][2]) {
+#pragma unroll
+    for (int i = 0; i < kNB / kFW; ++i) {
+      const int r = warp + kFW * i;
+      const double* row = L + (r0 + r) * ld + (int64_t)C * kNB;
+      dst[i][0] = r < b ? row[lane] : 0.0;
+      dst[i][1] = r < b ? row[lane + 32] : 0.0;
+    }
+  };
+  if (B >= 2) load_rows(0, lrow);
+  for (int C = 0; C < B - 1; ++C) {
+    double nrow[kNB / kFW][2];
+    if (C + 1 < B - 1) load_rows(C + 1, nrow);
     wait_flag(fflag + C);
     const int64_t c0 = (int64_t)C * kNB;
     const double z0 = z[c0 + lane], z1 = z[c0 + lane + 32];
 #pragma unroll
     for (int i = 0; i < kNB / kFW; ++i) {
-      const int r = warp + kFW * i;
-      if (r < b) {
-        const double* row = L + (r0 + r) * ld + c0;
-        acc[i] = fma(row[lane], z0, acc[i]);
-        acc[i] = fma(row[lane + 32], z1, acc[i]);
-      }
+      acc[i] = fma(lrow[i][0], z0, acc[i]);
+      acc[i] = fma(lrow[i][1], z1, acc[i]);
+    }
+    if (C + 1 < B - 1) {
+#pragma unroll
+      for (int i = 0; i < kNB / kFW; ++i) { lrow[i][0] = nrow[i][0]; lrow[i][1] = nrow[i][1]; }
     }
   }
   if (B > 0) {                                 // C = B - 1 from shared memory
@@ -178,7 +195,7 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   for (int i = 0; i < kNB / kFW; ++i) {
     const double sum = warp_sum(acc[i]);
     const int r = warp + kFW * i;
-    if (lane == 0) t[r] = (r < b) ? z[r0 + r] - sum : 0.0;
+    if (lane == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
   }
   __syncthreads();
   {                                            // z'_B = Linv_BB t  (4 threads per row)
@@ -256,9 +273,11 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
                "r"(bar) : "memory");
 }
 
+__device__ unsigned long long g_trsv_t[kCMaxNb][4];   // FS_TRSV_DBG: per block fwd arrive/push, bwd arrive/push
+
 __global__ void __launch_bounds__(kFT, 1)
 trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
-                         double* __restrict__ z, const int64_t* status) {
+                         double* __restrict__ z, const int64_t* status, int dbg) {
   extern __shared__ double csm[];
   double* LI = csm;
   double* LP = LI + kNB * kSP;
@@ -266,7 +285,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
   double* zf = LN + kNB * kSP;                 // [kCMaxNb][64] published z' blocks (forward)
   double* zb = zf + kCMaxNb * kNB;             // [kCMaxNb][64] published z blocks (backward)
   __shared__ __align__(8) uint64_t fbar[kCMaxNb], bbar[kCMaxNb];
-  __shared__ double t[kNB];
+  __shared__ double t[kNB], ub[kNB];
   __shared__ double part[kFW][kNB];
   const bool stop = status && *(volatile const int64_t*)status != 0;   // uniform over the cluster
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -292,6 +311,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
     LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
     LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
   }
+  if (threadIdx.x < kNB) ub[threadIdx.x] = threadIdx.x < b ? z[r0 + threadIdx.x] : 0.0;   // u_B, off the chain
   fs::ptx::cluster_sync();                      // barriers armed everywhere before any push
   auto push = [&](double* buf, uint64_t* bars, int slot, int dst, double val, int c) {
     const uint32_t a = fs::ptx::mapa(fs::ptx::smem_u32(buf + slot * kNB + c), (uint32_t)dst);
@@ -303,28 +323,50 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
     double acc[kNB / kFW];
 #pragma unroll
     for (int i = 0; i < kNB / kFW; ++i) acc[i] = 0.0;
-    for (int C = 0; C < B; ++C) {
-      fs::ptx::mbar_wait(&fbar[C], 0);
-      const double z0 = zf[C * kNB + lane], z1 = zf[C * kNB + lane + 32];
-      const bool crit = C == B - 1;
+    // off the critical path: the L_BC rows of the next block C are loaded (registers) before
+    // waiting for z'_C, so the L2 latency overlaps the wait; C = B-1 comes from shared memory
+    double lrow[kNB / kFW][2];
+    auto load_rows = [&](int C, double (&dst)[kNB / kFW][2]) {
 #pragma unroll
       for (int i = 0; i < kNB / kFW; ++i) {
         const int r = warp + kFW * i;
-        if (crit) {
-          acc[i] = fma(LP[r * kSP + lane], z0, acc[i]);
-          acc[i] = fma(LP[r * kSP + lane + 32], z1, acc[i]);
-        } else if (r < b) {
-          const double* row = L + (r0 + r) * ld + (int64_t)C * kNB;
-          acc[i] = fma(row[lane], z0, acc[i]);
-          acc[i] = fma(row[lane + 32], z1, acc[i]);
-        }
+        const double* row = L + (r0 + r) * ld + (int64_t)C * kNB;
+        dst[i][0] = r < b ? row[lane] : 0.0;
+        dst[i][1] = r < b ? row[lane + 32] : 0.0;
+      }
+    };
+    if (B >= 2) load_rows(0, lrow);
+    for (int C = 0; C < B - 1; ++C) {
+      double nrow[kNB / kFW][2];
+      if (C + 1 < B - 1) load_rows(C + 1, nrow);
+      fs::ptx::mbar_wait(&fbar[C], 0);
+      const double z0 = zf[C * kNB + lane], z1 = zf[C * kNB + lane + 32];
+#pragma unroll
+      for (int i = 0; i < kNB / kFW; ++i) {
+        acc[i] = fma(lrow[i][0], z0, acc[i]);
+        acc[i] = fma(lrow[i][1], z1, acc[i]);
+      }
+      if (C + 1 < B - 1) {
+#pragma unroll
+        for (int i = 0; i < kNB / kFW; ++i) { lrow[i][0] = nrow[i][0]; lrow[i][1] = nrow[i][1]; }
       }
     }
+    if (B > 0) {                                // C = B - 1: the critical block, from shared memory
+      fs::ptx::mbar_wait(&fbar[B - 1], 0);
+      const double z0 = zf[(B - 1) * kNB + lane], z1 = zf[(B - 1) * kNB + lane + 32];
+#pragma unroll
+      for (int i = 0; i < kNB / kFW; ++i) {
+        const int r = warp + kFW * i;
+        acc[i] = fma(LP[r * kSP + lane], z0, acc[i]);
+        acc[i] = fma(LP[r * kSP + lane + 32], z1, acc[i]);
+      }
+    }
+    if (dbg && threadIdx.x == 0) g_trsv_t[B][0] = fs::ptx::globaltimer();
 #pragma unroll
     for (int i = 0; i < kNB / kFW; ++i) {
       const double sum = warp_sum(acc[i]);
       const int r = warp + kFW * i;
-      if (lane == 0) t[r] = (r < b) ? z[r0 + r] - sum : 0.0;
+      if (lane == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
     }
     __syncthreads();
     {                                           // z'_B = Linv_BB t, kept locally and pushed to B+1..
@@ -340,6 +382,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
       }
     }
     __syncthreads();
+    if (dbg && threadIdx.x == 0) g_trsv_t[B][1] = fs::ptx::globaltimer();
     // ---------------- backward ----------------
     double a0 = 0.0, a1 = 0.0;
     for (int C = nb - 1; C > B; --C) {
@@ -361,6 +404,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
         }
       }
     }
+    if (dbg && threadIdx.x == 0) g_trsv_t[B][2] = fs::ptx::globaltimer();
     part[warp][lane] = a0;
     part[warp][lane + 32] = a1;
     __syncthreads();
@@ -384,6 +428,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
         for (int d = 0; d < B; ++d) push(zb, bbar, B, d, zc, c);
       }
     }
+    if (dbg && threadIdx.x == 0) g_trsv_t[B][3] = fs::ptx::globaltimer();
   }
   fs::ptx::cluster_sync();                      // no CTA leaves while a peer may still push to it
 }
@@ -424,9 +469,19 @@ cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Lin
       int ok_clusters = 0;
       if (cudaOccupancyMaxActiveClusters(&ok_clusters, trsv_pair_cluster_kernel, &cfg) == cudaSuccess &&
           ok_clusters >= 1) {
-        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status);
+        static const int dbg = getenv("FS_TRSV_DBG") ? atoi(getenv("FS_TRSV_DBG")) : 0;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status, dbg);
         if (e == cudaSuccess) {
           if (launches) *launches += 1;
+          if (dbg) {
+            unsigned long long h[kCMaxNb][4] = {};
+            cudaStreamSynchronize(st);
+            cudaMemcpyFromSymbol(h, g_trsv_t, sizeof h);
+            const unsigned long long t0 = h[0][0];
+            for (int B = 0; B < (int)nb; ++B)
+              fprintf(stderr, "trsv block %2d: fwd ready %6.2f pushed %6.2f | bwd ready %6.2f pushed %6.2f us\n", B,
+                      (h[B][0] - t0) * 1e-3, (h[B][1] - t0) * 1e-3, (h[B][2] - t0) * 1e-3, (h[B][3] - t0) * 1e-3);
+          }
           return cudaGetLastError();
         }
       }
