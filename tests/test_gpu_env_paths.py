@@ -165,3 +165,22 @@ def test_blocked_potrf_matches_lapack(gpu, n, minn):
 def test_blocked_potrf_pivot_index(gpu, n, bad):
     info = run_potrf({"FS_POTRF_BLOCKED_MINN": "300"}, n, bad)
     assert info["ref_piv"] == bad and info["piv"] == bad, info
+
+
+def test_repeated_solves_are_bit_identical(gpu):
+    """Race check by repetition (compute-sanitizer is closed on this pool): every cross-CTA protocol
+    on the path — the SYRK's CTA-pair barriers, the split-K reduce, the persistent potrf's grid
+    barriers and flags, the cluster TRSV's DSMEM pushes, the x + y pass's exchange, the block
+    Jacobi's phases — runs in a fixed order, so repeated solves must agree bit for bit."""
+    import paper_2310_17556_b200 as fsb
+    S, v, lam = O.generate_problem(99, 1000, 60000, 1e-3)
+    S32, v32 = S.astype(np.float32), v.astype(np.float32)
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    for fn, kw in ((fsb.solve_chol, {}), (fsb.solve_chol, {"precision": "fp64"}), (fsb.solve_svd_eigh, {})):
+        ref = fn(system, **kw)
+        x0 = ref.x.cpu().numpy()
+        for _ in range(6):
+            sol = fn(system, **kw)
+            assert np.array_equal(sol.x.cpu().numpy(), x0), (fn.__name__, kw)
+            assert sol.rel_residual == ref.rel_residual
