@@ -808,15 +808,23 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
         if (threadIdx.x == 256) ptx::mbar_arrive_cluster(tempty0 + b * 8);
         ++chunk;
         if (!(dbg & 8) && ((j + 1) % kFlushChunks == 0 || j == nch - 1)) {
+          // the fp64 partial tiles (36 MB at the headline) are re-read and rewritten every 64
+          // drains: kept in L2 (evict_last) so the flushes stop costing DRAM traffic
+          const uint64_t pol = (dbg & 4096) ? 0ull : ptx::policy_evict_last();
 #pragma unroll
           for (int g = 0; g < kN / 2; g += 16) {
             double old[16];
             if (!first_flush) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) old[e] = sc[(size_t)(g + e) * kBlk];
+              for (int e = 0; e < 16; ++e)
+                old[e] = pol ? ptx::ld_hint_f64(sc + (size_t)(g + e) * kBlk, pol) : sc[(size_t)(g + e) * kBlk];
             }
 #pragma unroll
-            for (int e = 0; e < 16; ++e) sc[(size_t)(g + e) * kBlk] = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
+            for (int e = 0; e < 16; ++e) {
+              const double val = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
+              if (pol) ptx::st_hint_f64(sc + (size_t)(g + e) * kBlk, val, pol);
+              else sc[(size_t)(g + e) * kBlk] = val;
+            }
           }
           first_flush = false;
         }

@@ -149,6 +149,14 @@ FS_DEV void bulk_prefetch_l2_hint(const void* src, uint32_t bytes, uint64_t poli
                "r"(bytes), "l"(policy)
                : "memory");
 }
+FS_DEV double ld_hint_f64(const double* p, uint64_t policy) {
+  double r;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(policy));
+  return r;
+}
+FS_DEV void st_hint_f64(double* p, double v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
+}
 FS_DEV float4 ld_hint_f4(const float4* p, uint64_t policy) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
