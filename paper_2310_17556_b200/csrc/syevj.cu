@@ -55,6 +55,45 @@ FS_DEVINL Rot schur2(double app, double aqq, double apq) {
   return R;
 }
 
+// The same rotation with the hardware reciprocal / reciprocal-sqrt approximations + Newton
+// steps (~1 ulp) instead of the library's IEEE division and square root, whose special-case
+// paths made the rotation the longest link of the block kernel's inner round.  Off-diagonals in
+// the denormal range count as converged; a huge tau takes the asymptote t = 1 / (2 tau).
+FS_DEVINL double rcp_fast(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+FS_DEVINL double rsqrt_fast(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double h = 0.5 * d * y * y;
+  y = y * (1.5 - h);
+  h = 0.5 * d * y * y;
+  return y * (1.5 - h);
+}
+FS_DEVINL Rot schur2_fast(double app, double aqq, double apq) {
+  Rot R{1.0, 0.0};
+  if (fabs(apq) > 1e-290) {
+    const double tau = (aqq - app) * rcp_fast(2.0 * apq);
+    const double at = fabs(tau);
+    double t;
+    if (at > 1e150) {
+      t = 0.5 * rcp_fast(at);
+    } else {
+      const double x = fma(tau, tau, 1.0);
+      t = rcp_fast(at + x * rsqrt_fast(x));    // x rsqrt(x) = sqrt(1 + tau^2)
+    }
+    if (!(tau >= 0.0)) t = -t;
+    R.c = rsqrt_fast(fma(t, t, 1.0));
+    R.s = t * R.c;
+  }
+  return R;
+}
+
 // sense-reversing grid barrier (the launch is cooperative: all CTAs are co-resident)
 FS_DEVINL void grid_barrier(unsigned* count, volatile unsigned* gen) {
   __syncthreads();
@@ -332,7 +371,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
         for (int ir = 0; ir < (full ? kSB - 1 : kBB); ++ir) {
           int pk, qk;
           inner_pair(ir, lane, pk, qk);
-          const Rot Rk = schur2(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
+          const Rot Rk = schur2_fast(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
           // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane)
 #pragma unroll
           for (int i = 0; i < kBB / (kBThreads / 32); ++i) {
