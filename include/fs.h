@@ -186,7 +186,10 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
  * np.linalg.eigh -> dsyevd).  n <= 8192.  *sweeps = Jacobi sweeps run.  Synchronizes.
  * fs_eigh_solve: solve_svd_eigh — Gram (precision as fs_chol_solve), eigh, singular values
  * floored at sigma_floor * sigma_max (*rank = kept count), x from the kept eigenpairs, residual
- * against S (flags: FS_FLAG_RESIDUAL only; no refinement on this route).  Synchronizes. */
+ * against S (flags: FS_FLAG_RESIDUAL; with it, FS_FLAG_REFINE_Z_STEPS(k) in the fp32-split
+ * precisions refines z with the kept-eigenpair apply as the correction solve — the reference's
+ * route has no refinement, the refined x converges to its fp64 result; FS_FLAG_REFINE is
+ * ignored).  Synchronizes. */
 int fs_syevj_packed(fs_ctx* ctx, const double* G_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,
                     void* stream);
 /* fs_heevj_packed: eigenpairs of G = S S^H (complex scores; solvers.py:258-266 with A.conj().T)

@@ -54,6 +54,10 @@ struct fs_ctx {
   uint8_t* d_St = nullptr;      // tiled copy of S for the tensor-core Gram (lazy, tiles.cuh)
   size_t St_bytes = 0;
   // F16X2 ring SYRK (lazy): the L2-resident tile ring, its ready/freed counters, u partials
+  // z-space refinement's correction solve: 0 = the Cholesky factor in d_W (TRSV pair), 1 = the
+  // eigh route's kept eigenpairs (d_U, d_w, eig_rank)
+  int z_solver = 0;
+  int64_t eig_rank = 0;
   uint8_t* d_ring = nullptr;
   int* d_ring_cnt = nullptr;
   double* d_ring_upart = nullptr;
@@ -634,7 +638,11 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
       const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 64);
       zres_kernel<<<g, 256, 0, st>>>(ctx->d_y, ctx->d_zacc, lam, n, ctx->d_z);
       int l = 0;
-      FS_CKS(fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l), "trsv_pair (z refine)");
+      if (ctx->z_solver == 1)   // eigh route: d = U_r diag(1 / (w_r + lam)) U_r^T e (in place)
+        FS_CKS(fs::eig_apply(ctx->d_U, n, n, ctx->eig_rank, ctx->d_z, ctx->d_w, lam, ctx->d_t, ctx->d_z, st, &l),
+               "eig_apply (z refine)");
+      else
+        FS_CKS(fs::trsv_pair(ctx->d_W, n, n, ctx->d_potrf, ctx->d_z, ctx->d_status, st, &l), "trsv_pair (z refine)");
       zadd_kernel<<<1, 1024, 0, st>>>(ctx->d_zacc, ctx->d_z, n, ctx->d_sums);
       ctx->launches += l + 2;
     }
@@ -1321,6 +1329,7 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   if ((rc = resolve_precision(ctx, dtype, precision, S, ldS, &use_tc))) return rc;
   begin_solve(ctx, false);
   int vdt = dtype;
+  const bool refine_z = (flags & FS_FLAG_REFINE_Z) != 0 && (flags & FS_FLAG_RESIDUAL) != 0 && use_tc;
   if (dtype == FS_F32 && !use_tc) {
     int l = 0;
     cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
@@ -1373,10 +1382,28 @@ int fs_eigh_solve(fs_ctx* ctx, int dtype, int precision, const void* S, int64_t 
   }
   prof_mark(ctx, FS_PROF_TRSV, st);
   FS_CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int64_t), st), "status reset");
-  // 4. x and the residual against S (solvers.py:318-322 -> _finish); no refinement on this route
+  // 4. x and the residual against S (solvers.py:318-322 -> _finish).  The fp32-split modes may
+  //    refine z on the kept eigen-subspace like the chol route (the reference's eigh route has
+  //    no refinement; its fp64 result is what the refined one converges to): exact fp64 x passes
+  int fl = flags & FS_FLAG_RESIDUAL;
+  if (refine_z) {
+    fl |= flags & (FS_FLAG_REFINE_Z | (0xFF << 8));
+    if (vdt == FS_F32) {
+      int l = 0;
+      cudaError_t e = fs::widen_f32((const float*)v, m, ctx->d_v64, st, &l);
+      ctx->launches += l;
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "widen v");
+      v = ctx->d_v64;
+      vdt = FS_F64;
+    }
+  }
   int64_t piv = -1;
-  return finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, flags & FS_FLAG_RESIDUAL, 0.0,
-                  &piv, out_res, st, nullptr);
+  ctx->z_solver = 1;
+  ctx->eig_rank = r;
+  rc = finish_x(ctx, dtype, S, n, m, ldS, v, vdt, lam, x, allreduce, allreduce_user, fl, 1e-10 /* solvers.py:43 */, &piv,
+                out_res, st, nullptr);
+  ctx->z_solver = 0;
+  return rc;
 }
 
 int fs_embed_complex(fs_ctx* ctx, int kind, int dtype, const void* S, int64_t n, int64_t m, int64_t ldS, void* out,

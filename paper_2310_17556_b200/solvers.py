@@ -457,7 +457,7 @@ def _thin_svd_eigh_complex(S: ScoreMatrix, sigma_floor: float, precision: str) -
 
 
 def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOOR, *, precision: str = "auto",
-                   diagnostics: bool = True) -> Solution:
+                   diagnostics: bool = True, refine: str | bool | int = "auto") -> Solution:
     """solve_svd_eigh (solvers.py:347-354): thin SVD through the Gram eigendecomposition, then
     x = V (sigma^2 + lam)^-1 V^T v + (v - V V^T v) / lam (solvers.py:315-317), residual against S.
 
@@ -468,12 +468,18 @@ def solve_svd_eigh(system: DampedSystem, sigma_floor: float = DEFAULT_SIGMA_FLOO
     route on the real representation rho(S) = [[Re S, -Im S], [Im S, Re S]] for [Re x; Im x]
     (rho(S) rho(S)^T = rho(S S^H) has every eigenvalue of S S^H twice, so the floor keeps or drops
     both copies and the solve is the complex one).
+    refine: the reference's eigh route has no correction step, so fp64 mode never refines; in the
+    fp32-split modes "auto" (with diagnostics) takes up to AUTO_REFINE_STEPS z-space steps as in
+    solve_chol, the correction solve being the same kept-eigenpair apply: z converges to the fp64
+    route's z = U_r diag(1 / (w_r + lam)) U_r^T u, i.e. the float32 default reaches the result the
+    reference computes in fp64.  An int k = up to k steps; False/0 = the raw fp32 route.
     """
-    return _eigh_route(as_system(system), _check_floor(sigma_floor), precision, diagnostics, Method.SVD_EIGH)
+    return _eigh_route(as_system(system), _check_floor(sigma_floor), precision, diagnostics, Method.SVD_EIGH,
+                       refine)
 
 
 def _eigh_route(system: DampedSystem, sigma_floor: float, precision: str, diagnostics: bool,
-                method: Method) -> Solution:
+                method: Method, refine: str | bool | int = "auto") -> Solution:
     t0 = perf_counter()
     if system.n > system.m:
         raise ValueError(f"thin_svd_eigh requires n <= m, got shape {(system.n, system.m)}")
@@ -481,7 +487,8 @@ def _eigh_route(system: DampedSystem, sigma_floor: float, precision: str, diagno
         m = system.m
         emb = embed_complex(system.S, 1)
         vhat = stack_complex_vector(system.v_tensor, system.S.real_dtype)
-        inner = _eigh_route(DampedSystem(emb, system.lam, vhat), sigma_floor, precision, diagnostics, method)
+        inner = _eigh_route(DampedSystem(emb, system.lam, vhat), sigma_floor, precision, diagnostics, method,
+                            refine)
         x = torch.complex(inner.x[:m], inner.x[m:])
         xo = x.cpu().numpy() if system.S.host_origin else x
         return replace(inner, x=xo, wall_seconds=perf_counter() - t0)
@@ -493,7 +500,14 @@ def _eigh_route(system: DampedSystem, sigma_floor: float, precision: str, diagno
     x = torch.empty(m, dtype=torch.float64, device=S.device)
     rank = ctypes.c_int64(0)
     res = (ctypes.c_double * 2)(float("nan"), float("nan"))
-    flags = _lib.FS_FLAG_RESIDUAL if diagnostics else 0
+    steps = _refine_steps(refine, prec)
+    if prec == "fp64":
+        steps = 0
+    if steps > 0 and not diagnostics:
+        if refine != "auto":
+            raise ValueError("refinement needs the residual diagnostics")
+        steps = 0
+    flags = (_lib.FS_FLAG_RESIDUAL if diagnostics else 0) | (refine_flags(prec, steps) if steps > 0 else 0)
     hint_scales(ctx, system.S)
     rc = ctx.lib.fs_eigh_solve(ctx.handle, _dt(S), PRECISIONS[prec], S.data_ptr(), n, m, S.stride(0), v.data_ptr(),
                                system.lam, sigma_floor, x.data_ptr(), _lib.ALLREDUCE_FN(), None, flags,

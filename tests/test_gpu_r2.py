@@ -89,6 +89,40 @@ def test_z_refinement_contracts_per_step(fsb, headline):
     assert rels[1] <= 1e-5 * rels[0] and rels[2] <= 1e-10, rels
 
 
+def test_eigh_route_fp32_default_reaches_fp64_result(fsb, headline):
+    """solve_svd_eigh on float32 scores: the f16x2 Gram's eigenpairs alone leave rel_residual at
+    the fp32 level (~1e-2 at sigma_max^2/lam ~ 1e6); z-space steps with the kept-eigenpair apply
+    as the correction solve bring x to the fp64 result (the reference computes this route in
+    fp64; at full rank its x is the chol x to ~1e-12)."""
+    S32, v32, lam, ref = headline
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    raw = fsb.solve_svd_eigh(system, precision="f16x2", refine=0)
+    sol = fsb.solve_svd_eigh(system)
+    assert sol.precision == "f16x2"
+    assert raw.rel_residual > 1e-6 and sol.rel_residual <= 1e-10, (raw.rel_residual, sol.rel_residual)
+    assert O.rel_err(sol.x.cpu().numpy(), ref.x) <= 1e-10, O.rel_err(sol.x.cpu().numpy(), ref.x)
+    assert O.rel_err(raw.x.cpu().numpy(), ref.x) <= 1e-5
+
+
+@pytest.mark.parametrize("prec", ["f16x2", "tf32x3"])
+def test_eigh_refinement_with_floored_spectrum(fsb, prec):
+    """Rank-deficient scores (k < n) with a floor that drops the null directions: the refined z
+    stays in the kept subspace, so x matches the reference's truncated fp64 route."""
+    rng = np.random.Generator(np.random.PCG64(21))
+    n, k, m, lam = 160, 100, 30000, 1e-3
+    S32 = (rng.standard_normal((n, k)) @ rng.standard_normal((k, m)) / k).astype(np.float32)
+    v32 = rng.standard_normal(m).astype(np.float32)
+    floor = 1e-2   # the nonzero sigmas sit within ~1/9 of sigma_max; the fp32 null ones near 1e-7
+    ref = O.solve_svd_eigh(S32.astype(np.float64), v32.astype(np.float64), lam, floor)
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    sol = fsb.solve_svd_eigh(system, floor, precision=prec)
+    assert O.rel_err(sol.x.cpu().numpy(), ref.x) <= 1e-8, O.rel_err(sol.x.cpu().numpy(), ref.x)
+    with pytest.raises(ValueError):
+        fsb.solve_svd_eigh(system, precision=prec, refine=2, diagnostics=False)
+
+
 @pytest.mark.parametrize("n,m,precisions", [(8192, 100_000, ("f16x2",)), (1024, 3_000_000, ("f16x2", "tf32x3"))])
 def test_configs_2_and_3_vs_cpu_reference(fsb, n, m, precisions):
     """BASELINE configs[2] (n sweep top, n=8192 at m=1e5) and configs[3] (m sweep, m=3e6):
