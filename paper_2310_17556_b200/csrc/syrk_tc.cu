@@ -811,19 +811,31 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
           // the fp64 partial tiles (36 MB at the headline) are re-read and rewritten every 64
           // drains: kept in L2 (evict_last) so the flushes stop costing DRAM traffic
           const uint64_t pol = (dbg & 4096) ? 0ull : ptx::policy_evict_last();
+          if (first_flush || (dbg & 8192)) {
+            // dbg 8192: the earlier read-modify-write flush (load latency on this thread)
 #pragma unroll
-          for (int g = 0; g < kN / 2; g += 16) {
-            double old[16];
-            if (!first_flush) {
+            for (int g = 0; g < kN / 2; g += 16) {
+              double old[16];
+              if (!first_flush) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e)
-                old[e] = pol ? ptx::ld_hint_f64(sc + (size_t)(g + e) * kBlk, pol) : sc[(size_t)(g + e) * kBlk];
+                for (int e = 0; e < 16; ++e)
+                  old[e] = pol ? ptx::ld_hint_f64(sc + (size_t)(g + e) * kBlk, pol) : sc[(size_t)(g + e) * kBlk];
+              }
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const double val = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
+                if (pol) ptx::st_hint_f64(sc + (size_t)(g + e) * kBlk, val, pol);
+                else sc[(size_t)(g + e) * kBlk] = val;
+              }
             }
+          } else {
+            // later flushes: fp64 adds performed at L2 (red, no return value), so the epilogue
+            // goes straight back to draining TMEM; each slot element has this one writer, whose
+            // adds land in program order: the same fl(old + acc) sequence as a read-modify-write
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const double val = (first_flush ? 0.0 : old[e]) + (double)acc[g + e];
-              if (pol) ptx::st_hint_f64(sc + (size_t)(g + e) * kBlk, val, pol);
-              else sc[(size_t)(g + e) * kBlk] = val;
+            for (int e = 0; e < kN / 2; ++e) {   // fully unrolled: acc stays in registers
+              if (pol) ptx::red_add_hint_f64(sc + (size_t)e * kBlk, (double)acc[e], pol);
+              else ptx::red_add_f64(sc + (size_t)e * kBlk, (double)acc[e]);
             }
           }
           first_flush = false;
@@ -837,7 +849,7 @@ syrk_tc_kernel(const uint8_t* __restrict__ St, int64_t n, int nbt, int tile0, in
             const int64_t gj = (int64_t)(2 * qq) * kBlk + c;
             if (gj > gi) break;
             double* g = Gp + gi * (gi + 1) / 2 + gj;
-            double val = sc[(size_t)e * kBlk];
+            double val = __ldcg(sc + (size_t)e * kBlk);   // L2: where the flush's adds were performed
             if (kF16) val *= inv_scale[gi] * inv_scale[gj];       // exact: powers of two
             *g = (accum ? *g : 0.0) + val + (gi == gj ? lam : 0.0);
           }

@@ -157,6 +157,14 @@ FS_DEV double ld_hint_f64(const double* p, uint64_t policy) {
 FS_DEV void st_hint_f64(double* p, double v, uint64_t policy) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
 }
+// fire-and-forget fp64 add at L2 (no value returned, so no load latency on the issuing thread);
+// a thread's own operations on one address stay in program order
+FS_DEV void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+FS_DEV void red_add_hint_f64(double* p, double v, uint64_t policy) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(policy) : "memory");
+}
 FS_DEV float4 ld_hint_f4(const float4* p, uint64_t policy) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"

@@ -67,6 +67,10 @@ def test_float32_default_meets_promise(fsb, n, m, lam, seed):
     system, S, v = random_system(fsb, seed, n, m, lam, np.float32)
     sol = fsb.solve_chol(system)
     assert sol.rel_residual <= 1e-8, (sol.precision, sol.rel_residual)
+    # the stored residual is that of the returned x (an exact recompute: y = S x, fp64 products; at the rounding floor
+    # the summation order moves it by a few percent at most)
+    _, rel = fsb.residual(system, sol.x, fsb.Variant.PLAIN)
+    assert abs(sol.rel_residual - rel) <= 0.05 * rel + 1e-15, (sol.rel_residual, rel)
 
 
 @given(n=st.integers(1, 32), m=st.integers(1, 48), lam_exp=st.integers(-6, 1), seed=st.integers(0, 2**32 - 1))

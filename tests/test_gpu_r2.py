@@ -77,6 +77,10 @@ def test_headline_drop_in_default_meets_reference_promise(fsb, headline):
     assert sol.precision == "f16x2"
     assert sol.rel_residual <= 1e-10, (sol.precision, sol.rel_residual)
     assert O.rel_err(sol.x, ref.x) <= 1e-13, O.rel_err(sol.x, ref.x)
+    # the stored residual is the returned x's own (exact recompute; summation order moves it at most a few percent): no
+    # step may report the residual of an algebraic update instead of S x
+    _, rel = fsb.residual(fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32), sol.x, fsb.Variant.PLAIN)
+    assert abs(sol.rel_residual - rel) <= 0.05 * rel, (sol.rel_residual, rel)
 
 
 def test_z_refinement_contracts_per_step(fsb, headline):
