@@ -107,15 +107,25 @@ FS_DEVINL void store_tile(const double (&acc)[8][4][2], int64_t rA, int64_t rB, 
 // them stalls every stage's barrier instead: 38 -> 52 ms).
 constexpr int kFlush = 64;
 
+FS_DEVINL void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 FS_DEVINL void flush_acc(double (&acc)[8][4][2], double* buf, bool first, int wr, int wc, int fr, int lane) {
   const int cc = 2 * (lane & 3);
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      double2* p = reinterpret_cast<double2*>(buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc);
-      const double2 o = first ? make_double2(0.0, 0.0) : *p;
-      *p = make_double2(o.x + acc[a][b][0], o.y + acc[a][b][1]);
+      double* q = buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc;
+      if (first) {
+        *reinterpret_cast<double2*>(q) = make_double2(0.0 + acc[a][b][0], 0.0 + acc[a][b][1]);
+      } else {
+        // the add happens at L2 (no load round trip on the critical stage); one writer per
+        // element, program order: the same fl(old + acc) as a read-modify-write
+        red_add_f64(q, acc[a][b][0]);
+        red_add_f64(q + 1, acc[a][b][1]);
+      }
       acc[a][b][0] = acc[a][b][1] = 0.0;
     }
 }
@@ -126,7 +136,7 @@ FS_DEVINL void unflush_acc(double (&acc)[8][4][2], const double* buf, int wr, in
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const double2 o = *reinterpret_cast<const double2*>(buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc);
+      const double2 o = __ldcg(reinterpret_cast<const double2*>(buf + (wr + 8 * a + fr) * kT + wc + 8 * b + cc));
       acc[a][b][0] = o.x + acc[a][b][0];
       acc[a][b][1] = o.y + acc[a][b][1];
     }
