@@ -147,10 +147,13 @@ def _staged_chunks(pool, workers, bufs, events, src, src_np, dst, rows, cols, ro
         if events[k] is not None:
             events[k].synchronize()                 # the DMA that last read this buffer is done
         view = bufs[k][: (r1 - r0) * row_bytes].view(src.dtype).view(r1 - r0, cols)
-        vnp = view.numpy()
-        step = -(-(r1 - r0) // workers)
-        futs = [pool.submit(np.copyto, vnp[a:a + step], src_np[r0 + a:min(r1, r0 + a + step)])
-                for a in range(0, r1 - r0, step)]
+        # split the chunk's bytes (contiguous rows) evenly over the workers, not whole rows: a 64 MB
+        # chunk of 4 MB rows has only 16 rows
+        vflat = view.numpy().reshape(-1)
+        sflat = src_np[r0:r1].reshape(-1)
+        step = -(-vflat.size // workers)
+        step = -(-step // 1024) * 1024            # 4-8 KB aligned pieces
+        futs = [pool.submit(np.copyto, vflat[a:a + step], sflat[a:a + step]) for a in range(0, vflat.size, step)]
         for f in futs:
             f.result()
         dst[r0:r1].copy_(view, non_blocking=True)
