@@ -372,29 +372,49 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
           int pk, qk;
           inner_pair(ir, lane, pk, qk);
           const Rot Rk = schur2_fast(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
-          // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane)
+          // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane), and V <- V J (columns pk,
+          // qk of rows warp + 8 i; each (row, pair) by one thread).  All shared loads of the round
+          // are issued before any store: M / M2 swap every round and V is updated in place, so the
+          // compiler cannot move a load above a store itself (each load -> FMA -> store chain
+          // otherwise waits out the shared-memory latency in turn)
+          constexpr int kNI = kBB / (kBThreads / 32), kNV = kSB / (kBThreads / 32);
+          int p1[kNI], q1[kNI];
+          double bpp[kNI], bpq[kNI], bqp[kNI], bqq[kNI], r1c[kNI], r1s[kNI], va[kNV], vb[kNV];
 #pragma unroll
-          for (int i = 0; i < kBB / (kBThreads / 32); ++i) {
+          for (int i = 0; i < kNI; ++i) {
             const int k1 = warp + (kBThreads / 32) * i;
-            int p1, q1;
-            inner_pair(ir, k1, p1, q1);
-            const Rot R1{__shfl_sync(0xffffffffu, Rk.c, k1), __shfl_sync(0xffffffffu, Rk.s, k1)};
-            const double bpp = M[p1 * kMP + pk], bpq = M[p1 * kMP + qk], bqp = M[q1 * kMP + pk],
-                         bqq = M[q1 * kMP + qk];
-            const double rpp = R1.c * bpp - R1.s * bqp, rpq = R1.c * bpq - R1.s * bqq;
-            const double rqp = R1.s * bpp + R1.c * bqp, rqq = R1.s * bpq + R1.c * bqq;
-            M2[p1 * kMP + pk] = Rk.c * rpp - Rk.s * rpq;
-            M2[p1 * kMP + qk] = Rk.s * rpp + Rk.c * rpq;
-            M2[q1 * kMP + pk] = Rk.c * rqp - Rk.s * rqq;
-            M2[q1 * kMP + qk] = Rk.s * rqp + Rk.c * rqq;
+            inner_pair(ir, k1, p1[i], q1[i]);
+            bpp[i] = M[p1[i] * kMP + pk];
+            bpq[i] = M[p1[i] * kMP + qk];
+            bqp[i] = M[q1[i] * kMP + pk];
+            bqq[i] = M[q1[i] * kMP + qk];
           }
-          // V <- V J: columns pk, qk of rows warp + 8 i (in place: each (row, pair) by one thread)
 #pragma unroll
-          for (int i = 0; i < kSB / (kBThreads / 32); ++i) {
+          for (int i = 0; i < kNV; ++i) {
             const int row = warp + (kBThreads / 32) * i;
-            const double a = V[row * kMP + pk], b = V[row * kMP + qk];
-            V[row * kMP + pk] = Rk.c * a - Rk.s * b;
-            V[row * kMP + qk] = Rk.s * a + Rk.c * b;
+            va[i] = V[row * kMP + pk];
+            vb[i] = V[row * kMP + qk];
+          }
+#pragma unroll
+          for (int i = 0; i < kNI; ++i) {
+            const int k1 = warp + (kBThreads / 32) * i;
+            r1c[i] = __shfl_sync(0xffffffffu, Rk.c, k1);
+            r1s[i] = __shfl_sync(0xffffffffu, Rk.s, k1);
+          }
+#pragma unroll
+          for (int i = 0; i < kNI; ++i) {
+            const double rpp = r1c[i] * bpp[i] - r1s[i] * bqp[i], rpq = r1c[i] * bpq[i] - r1s[i] * bqq[i];
+            const double rqp = r1s[i] * bpp[i] + r1c[i] * bqp[i], rqq = r1s[i] * bpq[i] + r1c[i] * bqq[i];
+            M2[p1[i] * kMP + pk] = Rk.c * rpp - Rk.s * rpq;
+            M2[p1[i] * kMP + qk] = Rk.s * rpp + Rk.c * rpq;
+            M2[q1[i] * kMP + pk] = Rk.c * rqp - Rk.s * rqq;
+            M2[q1[i] * kMP + qk] = Rk.s * rqp + Rk.c * rqq;
+          }
+#pragma unroll
+          for (int i = 0; i < kNV; ++i) {
+            const int row = warp + (kBThreads / 32) * i;
+            V[row * kMP + pk] = Rk.c * va[i] - Rk.s * vb[i];
+            V[row * kMP + qk] = Rk.s * va[i] + Rk.c * vb[i];
           }
           __syncthreads();
           double* tmp = M; M = M2; M2 = tmp;
