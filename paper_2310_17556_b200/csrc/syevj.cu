@@ -268,6 +268,9 @@ FS_DEVINL void load_pair_block(const double* __restrict__ M, int np, int I1, int
 
 // FS_SYEVJ_DBG: CTA 0's %globaltimer split of the rounds (phase A, barrier, phase B, barrier), ns
 __device__ unsigned long long g_bj_time[4];
+// FS_SYEVJ_DBG bit 2: CTA 0 warp 0's clock64 split of the inner rounds (loads + rotation, shuffles
+// + updates + stores, barrier), cycles, and the inner-round count
+__device__ unsigned long long g_bj_ir[4];
 
 __global__ void __launch_bounds__(kBThreads, 1)
 bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restrict__ U, double* __restrict__ Vt,
@@ -327,6 +330,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       __syncthreads();
     }
   };
+  long long ir_t[4] = {0, 0, 0, 0};
   int nround = 0, prev_r = 0;                        // rounds done (all sweeps), the last one's index
   // a round's U blocks [0, ndefer) are applied during the NEXT round's phase A by the CTAs the
   // inner sweeps leave idle (ten each at most: about one inner sweep's time), the rest in its phase B
@@ -350,10 +354,11 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
         double* M = bsm;
         double* M2 = bsm + kSB * kMP;
         double* V = bsm + 2 * kSB * kMP;
+        const bool full = r == 0;
         for (int e = threadIdx.x; e < kSB * kSB; e += kBThreads) {
           const int a = e >> 6, b = e & 63;
           M[a * kMP + b] = Aold[(int64_t)sb_row(I, J, a) * np + sb_row(I, J, b)];
-          V[a * kMP + b] = a == b ? 1.0 : 0.0;
+          if (full) V[a * kMP + b] = a == b ? 1.0 : 0.0;
         }
         __syncthreads();
         // every warp computes all 32 rotations of an inner round (lane k: pair k) and takes the
@@ -363,21 +368,38 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
         // every index pair is still rotated at least once per outer sweep, as in cyclic Jacobi,
         // and the inner sweeps (the latency-bound phase) take half the rounds
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const bool full = r == 0;
         auto inner_pair = [&](int ir, int k, int& p, int& qq) {
           if (full) pair_of_round(ir, k, kSB - 1, p, qq);
           else { p = k; qq = kBB + ((k + ir) & (kBB - 1)); }
         };
+        const bool tir = (dbg & 2) && blockIdx.x == 0 && warp == 0;
+        // cross rounds: V in registers.  Lane k holds, for rows warp + 8 i, column k (the I half,
+        // fixed) and column 32 + ((k + ir) mod 32) (the J half: its pair partner this round); after
+        // the round the J column moves one lane down (shuffle), so V never touches shared memory
+        // until the 32 rounds bring every J column back to lane k
+        constexpr int kNV = kSB / (kBThreads / 32);
+        double vI[kNV], vJ[kNV];
+#pragma unroll
+        for (int i = 0; i < kNV; ++i) {
+          const int row = warp + (kBThreads / 32) * i;
+          vI[i] = row == lane ? 1.0 : 0.0;
+          vJ[i] = row == kBB + lane ? 1.0 : 0.0;
+        }
         for (int ir = 0; ir < (full ? kSB - 1 : kBB); ++ir) {
+          long long c0 = tir ? clock64() : 0;
           int pk, qk;
           inner_pair(ir, lane, pk, qk);
           const Rot Rk = schur2_fast(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
+          if (tir) {   // make the rotation's completion visible to the clock
+            const long long c1 = clock64() + (Rk.c + Rk.s == 12345.0 ? 1 : 0);
+            ir_t[0] += c1 - c0; c0 = c1;
+          }
           // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane), and V <- V J (columns pk,
           // qk of rows warp + 8 i; each (row, pair) by one thread).  All shared loads of the round
           // are issued before any store: M / M2 swap every round and V is updated in place, so the
           // compiler cannot move a load above a store itself (each load -> FMA -> store chain
           // otherwise waits out the shared-memory latency in turn)
-          constexpr int kNI = kBB / (kBThreads / 32), kNV = kSB / (kBThreads / 32);
+          constexpr int kNI = kBB / (kBThreads / 32);
           int p1[kNI], q1[kNI];
           double bpp[kNI], bpq[kNI], bqp[kNI], bqq[kNI], r1c[kNI], r1s[kNI], va[kNV], vb[kNV];
 #pragma unroll
@@ -389,11 +411,13 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
             bqp[i] = M[q1[i] * kMP + pk];
             bqq[i] = M[q1[i] * kMP + qk];
           }
+          if (full) {
 #pragma unroll
-          for (int i = 0; i < kNV; ++i) {
-            const int row = warp + (kBThreads / 32) * i;
-            va[i] = V[row * kMP + pk];
-            vb[i] = V[row * kMP + qk];
+            for (int i = 0; i < kNV; ++i) {
+              const int row = warp + (kBThreads / 32) * i;
+              va[i] = V[row * kMP + pk];
+              vb[i] = V[row * kMP + qk];
+            }
           }
 #pragma unroll
           for (int i = 0; i < kNI; ++i) {
@@ -410,14 +434,34 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
             M2[q1[i] * kMP + pk] = Rk.c * rqp - Rk.s * rqq;
             M2[q1[i] * kMP + qk] = Rk.s * rqp + Rk.c * rqq;
           }
+          if (full) {
+#pragma unroll
+            for (int i = 0; i < kNV; ++i) {
+              const int row = warp + (kBThreads / 32) * i;
+              V[row * kMP + pk] = Rk.c * va[i] - Rk.s * vb[i];
+              V[row * kMP + qk] = Rk.s * va[i] + Rk.c * vb[i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < kNV; ++i) {
+              const double a = vI[i], b = vJ[i];
+              vI[i] = Rk.c * a - Rk.s * b;
+              vJ[i] = __shfl_sync(0xffffffffu, Rk.s * a + Rk.c * b, (lane + 1) & 31);
+            }
+          }
+          if (tir) { const long long c1 = clock64(); ir_t[1] += c1 - c0; c0 = c1; }
+          __syncthreads();
+          if (tir) { ir_t[2] += clock64() - c0; ir_t[3] += 1; }
+          double* tmp = M; M = M2; M2 = tmp;
+        }
+        if (!full) {   // the register V (every J column back at lane k) -> shared
 #pragma unroll
           for (int i = 0; i < kNV; ++i) {
             const int row = warp + (kBThreads / 32) * i;
-            V[row * kMP + pk] = Rk.c * va[i] - Rk.s * vb[i];
-            V[row * kMP + qk] = Rk.s * va[i] + Rk.c * vb[i];
+            V[row * kMP + lane] = vI[i];
+            V[row * kMP + kBB + lane] = vJ[i];
           }
           __syncthreads();
-          double* tmp = M; M = M2; M2 = tmp;
         }
         // V^T to global: Vt[P][i][j] = V[j][i]
         double* vt = Vr + (size_t)P * kSB * kSB;
@@ -489,7 +533,10 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
   }
   if (dbg && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == (unsigned)q)) {
     const int o = blockIdx.x == 0 ? 0 : 2;
-    if (o == 0) { g_bj_time[0] = tA; g_bj_time[1] = tB1 + tB2; g_bj_time[2] = tB; }
+    if (o == 0) {
+      g_bj_time[0] = tA; g_bj_time[1] = tB1 + tB2; g_bj_time[2] = tB;
+      for (int k = 0; k < 4; ++k) g_bj_ir[k] = (unsigned long long)ir_t[k];
+    }
     else g_bj_time[3] = tA;
   }
   for (int i = blockIdx.x * kBThreads + threadIdx.x; i < np; i += gridDim.x * kBThreads)
@@ -654,6 +701,12 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
       cudaMemcpyFromSymbol(h, g_bj_time, sizeof h);
       fprintf(stderr, "bjacobi CTA 0: phase A %.2f ms, barriers %.2f ms, phase B %.2f ms; CTA q (U work) %.2f ms\n",
               h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6);
+      if (dbg & 2) {
+        cudaMemcpyFromSymbol(h, g_bj_ir, sizeof h);
+        const double k = h[3] ? (double)h[3] : 1.0;
+        fprintf(stderr, "bjacobi inner rounds %llu: rotation %.0f, updates %.0f, barrier %.0f cycles each\n", h[3],
+                h[0] / k, h[1] / k, h[2] / k);
+      }
     }
     return cudaGetLastError();
   }
