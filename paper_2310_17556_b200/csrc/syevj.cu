@@ -94,21 +94,20 @@ FS_DEVINL Rot schur2_fast(double app, double aqq, double apq) {
   return R;
 }
 
-// sense-reversing grid barrier (the launch is cooperative: all CTAs are co-resident)
-FS_DEVINL void grid_barrier(unsigned* count, volatile unsigned* gen) {
+// grid barrier on a monotonic arrival counter (the launch is cooperative: all CTAs are
+// co-resident): each CTA's thread 0 adds 1 with release semantics and waits, with acquire loads,
+// for the count of this barrier's generation (target += gridDim.x per call; ctl is zeroed before
+// the launch).  One L2 round trip per CTA instead of the sense-reversing barrier's atomic +
+// generation flip + re-read (~3.2 -> ~2 us per barrier with 148 CTAs).
+FS_DEVINL void grid_barrier(unsigned* count, unsigned& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0;
-      __threadfence();
-      atomicAdd((unsigned*)gen, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    target += gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while ((int)(v - target) < 0);
   }
   __syncthreads();
 }
@@ -120,6 +119,7 @@ jacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restri
               double tol, double* __restrict__ partial, unsigned* ctl, int* info, double* __restrict__ wraw) {
   extern __shared__ Rot rot[];           // n/2 rotations of the current round
   __shared__ double red[kJThreads / 32];
+  unsigned bar_target = 0;
   const int half = n / 2, np1 = n - 1;
   double* Aold = A0;
   double* Anew = A1;
@@ -139,10 +139,10 @@ jacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restri
       for (int w = 0; w < kJThreads / 32; ++w) t += red[w];
       partial[blockIdx.x] = t;
     }
-    grid_barrier(ctl, ctl + 1);
+    grid_barrier(ctl, bar_target);
     double tot = 0.0;
     for (int b = 0; b < (int)gridDim.x; ++b) tot += partial[b];
-    grid_barrier(ctl, ctl + 1);          // partial[] may be overwritten afterwards
+    grid_barrier(ctl, bar_target);          // partial[] may be overwritten afterwards
     return tot;
   };
   const double fro2 = frob_off(Aold, false);
@@ -190,7 +190,7 @@ jacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restri
           uq[j] = R1.s * a + R1.c * b;
         }
       }
-      grid_barrier(ctl, ctl + 1);
+      grid_barrier(ctl, bar_target);
       double* t = Aold; Aold = Anew; Anew = t;
     }
   }
@@ -278,6 +278,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
                double* __restrict__ wraw, int dbg) {
   extern __shared__ double bsm[];
   __shared__ double red[kBThreads / 32];
+  unsigned bar_target = 0;
   unsigned long long tA = 0, tB1 = 0, tB = 0, tB2 = 0, t0 = 0, t1 = 0;
   auto now = [&]() -> unsigned long long { return dbg ? ptx_globaltimer() : 0ull; };
   const int nblk = np / kBB, q = nblk / 2, rounds = nblk - 1;
@@ -298,10 +299,10 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       for (int w = 0; w < kBThreads / 32; ++w) t += red[w];
       partial[blockIdx.x] = t;
     }
-    grid_barrier(ctl, ctl + 1);
+    grid_barrier(ctl, bar_target);
     double tot = 0.0;
     for (int b = 0; b < (int)gridDim.x; ++b) tot += partial[b];
-    grid_barrier(ctl, ctl + 1);
+    grid_barrier(ctl, bar_target);
     return tot;
   };
   // U <- U V for every (64-row chunk c, pair P2) block of a round's rotations Vp (in place:
@@ -470,7 +471,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       }
       if (nround > 0 && (int)gridDim.x <= q) u_update(Vp, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
       t1 = now(); tA += t1 - t0; t0 = t1;
-      grid_barrier(ctl, ctl + 1);
+      grid_barrier(ctl, bar_target);
       t1 = now(); tB1 += t1 - t0; t0 = t1;
       // ---------------- phase B: A' = J^T A J (lower pair blocks, mirrored) ----------------
       const int atasks = q * (q + 1) / 2;
@@ -520,7 +521,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       // the rest of this round's U blocks (after the A tasks: same CTAs, next free slots)
       u_update(Vr, r, ndefer, q * q, ((int)blockIdx.x + atasks) % (int)gridDim.x, (int)gridDim.x);
       t1 = now(); tB += t1 - t0; t0 = t1;
-      grid_barrier(ctl, ctl + 1);
+      grid_barrier(ctl, bar_target);
       t1 = now(); tB2 += t1 - t0;
       double* t = Aold; Aold = Anew; Anew = t;
       prev_r = r;
@@ -529,7 +530,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
   }
   if (nround > 0) {                                   // the last round's rotations
     u_update(Vt + (size_t)((nround & 1) ^ 1) * q * kSB * kSB, prev_r, 0, ndefer, (int)blockIdx.x, (int)gridDim.x);
-    grid_barrier(ctl, ctl + 1);
+    grid_barrier(ctl, bar_target);
   }
   if (dbg && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == (unsigned)q)) {
     const int o = blockIdx.x == 0 ? 0 : 2;
