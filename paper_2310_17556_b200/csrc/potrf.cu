@@ -803,21 +803,18 @@ __device__ void aux_tile(double* W, int64_t n, int64_t ld, int k, const double* 
   }
 }
 
-// sense-reversing grid barrier (cooperative launch: all CTAs co-resident)
-__device__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
+// grid barrier on a monotonic arrival counter (cooperative launch: all CTAs co-resident; ctl is
+// zeroed before the launch): thread 0 adds 1 with release semantics and polls with acquire loads
+// until this generation's count (target += gridDim.x per call) — one L2 round trip per CTA
+__device__ void grid_barrier(unsigned* count, unsigned& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0;
-      __threadfence();
-      atomicAdd((unsigned*)gen, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    target += gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while ((int)(v - target) < 0);
   }
   __syncthreads();
 }
@@ -831,6 +828,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
                         int64_t* status, unsigned* ctl, const double* __restrict__ u, double* ut, double* tb,
                         double* __restrict__ z) {
   extern __shared__ double dsm[];
+  unsigned bar_target = 0;
   double (*P)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 3 * kNB * kLd);   // CTA 0: Linv_kk
   const int nb = (int)((n + kNB - 1) / kNB);
   if (u)                                                  // working right-hand side of L t = u
@@ -843,7 +841,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
     factor_diag(W, n, ld, 0, status, Linv, A, P, T, false);   // Linv_00 stays in P
   }
   POTRF_MARK(1);
-  grid_barrier(ctl, ctl + 1);
+  grid_barrier(ctl, bar_target);
   POTRF_MARK(2);
   int k = 0;
   const int G = gridDim.x;
@@ -875,7 +873,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
         const int o = threadIdx.x >> 2;
         if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = a;
       }
-      grid_barrier(ctl, ctl + 1);
+      grid_barrier(ctl, bar_target);
       // phase B: every trailing tile but the factored diagonal, one product each; the forward
       // substitution of row block k+1 (its panel rows came from CTA 0)
       for (int tile = 1 + (int)blockIdx.x; tile < tiles; tile += G) {
@@ -895,7 +893,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
         const int o = threadIdx.x >> 2;
         if ((threadIdx.x & 3) == 0 && o < valid) ut[r1 + o] -= a;
       }
-      grid_barrier(ctl, ctl + 1);
+      grid_barrier(ctl, bar_target);
       continue;
     }
     if (blockIdx.x == 0) {
@@ -914,7 +912,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
         step_tile(W, n, ld, k, Linv, panel0, panel1, status, tile, dsm, u ? ut : nullptr, tb);
       }
     if (k < 30) POTRF_MARK(3 + 2 * k);
-    grid_barrier(ctl, ctl + 1);
+    grid_barrier(ctl, bar_target);
     if (k < 30) POTRF_MARK(4 + 2 * k);
   }
   POTRF_MARK(70);
@@ -941,7 +939,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
     if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = acc;
   }
   POTRF_MARK(71);
-  grid_barrier(ctl, ctl + 1);                             // tb = t complete, W holds all of L
+  grid_barrier(ctl, bar_target);                             // tb = t complete, W holds all of L
   POTRF_MARK(72);
   // backward solve L^T z = t, left-looking per block with release/acquire flags instead of a grid
   // barrier per block: CTA c owns block c (c = blockIdx.x + i*G, taken in decreasing order) and
