@@ -1497,7 +1497,10 @@ int fs_jacobi_svd(fs_ctx* ctx, const double* A, int64_t n, int64_t lda, double* 
   int rc = ensure_svd(ctx, n);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  const double tol = std::max(1e-15, (double)n * 1.1102230246251565e-16);
+  // rows orthogonal to sqrt(n) u (LAPACK dgesvj's default): the factor solve amplifies the
+  // singular vectors' error by sigma^2/lam (n u left the headline's full route at rel_residual
+  // 4.5e-8; sqrt(n) u: 8.6e-9, +7 ms of 570)
+  const double tol = std::max(1e-15, std::sqrt((double)n) * 1.1102230246251565e-16);
   int l = 0;
   cudaError_t e = fs::jacobi_svd(A, n, lda, sigma, U, ldu, Zt, ldz, 60, tol, ctx->d_svd, ctx->num_sms, ctx->d_info, st,
                                  &l);

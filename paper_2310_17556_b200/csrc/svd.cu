@@ -61,20 +61,17 @@ FS_DEVINL void round_pair(int r, int k, int np1, int& p, int& q) {
   q = (r - k + np1) % np1;
 }
 
-FS_DEVINL void grid_sync(unsigned* count, volatile unsigned* gen) {
+// grid barrier on a monotonic arrival counter (cooperative launch; ctl zeroed before it): thread
+// 0 adds 1 with release semantics and polls with acquire loads for this generation's count
+FS_DEVINL void grid_sync(unsigned* count, unsigned& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0;
-      __threadfence();
-      atomicAdd((unsigned*)gen, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
+    target += gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while ((int)(v - target) < 0);
   }
   __syncthreads();
 }
@@ -93,6 +90,7 @@ jacobi_svd_kernel(double* __restrict__ B, double* __restrict__ Vt, int np, int m
   const int warps_total = gridDim.x * (kSThreads / 32);
   const int gw = blockIdx.x * (kSThreads / 32) + (threadIdx.x >> 5);
   unsigned* rotations = ctl + 2;
+  unsigned bar_target = 0;
   int sweep = 0;
   bool converged = false;
   for (; sweep < max_sweeps && !converged; ++sweep) {
@@ -133,10 +131,10 @@ jacobi_svd_kernel(double* __restrict__ B, double* __restrict__ Vt, int np, int m
           if (lane == 0) atomicAdd(cnt, 1u);
         }
       }
-      grid_sync(ctl, ctl + 1);
+      grid_sync(ctl, bar_target);
     }
     converged = *(volatile unsigned*)cnt == 0u;
-    grid_sync(ctl, ctl + 1);   // everyone read the counter before it is reset two sweeps on
+    grid_sync(ctl, bar_target);   // everyone read the counter before it is reset two sweeps on
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     info[0] = sweep;
