@@ -276,6 +276,11 @@ def sharded_solve_chol_fused(S_local, v_local, lam: float, *, precision: str = "
                                    ctypes.byref(piv), res, _stream(dev))
         what = "fs_chol_solve"
     if rc == _lib.FS_NOT_PD:
+        if precision == "auto" and prec != "fp64":
+            # the split Gram lost definiteness (its ~2^-22 ||G|| error): every rank saw the same
+            # all-reduced Gram, so every rank retries in the reference's fp64 arithmetic together
+            return sharded_solve_chol_fused(S_local, v_local, lam, precision="fp64", diagnostics=diagnostics,
+                                            refine=refine, group=group)
         raise FactorizationError(f"Gram matrix is not positive definite at pivot {piv.value}", pivot=int(piv.value))
     _check(ctx, rc, what)
     return ShardedSolution(x_local=x, abs_residual=float(res[0]), rel_residual=float(res[1]), refined=refine > 0)

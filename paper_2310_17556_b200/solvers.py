@@ -239,6 +239,12 @@ def solve_chol(system: DampedSystem, meter: WorkspaceMeter | None = None, *, pre
     if meter is not None:
         meter.free(slots)
     if rc == _lib.FS_NOT_PD:
+        if precision == "auto" and prec != "fp64":
+            # the split Gram carries ~2^-22 ||G|| of error, so W~ can lose definiteness where the
+            # reference's fp64 W keeps it (near-dependent rows, lam below that error): decide in the
+            # reference's arithmetic — its success, or its failure with its own pivot
+            sol = solve_chol(system, meter, precision="fp64", refine=refine, diagnostics=diagnostics)
+            return replace(sol, wall_seconds=perf_counter() - t0)
         raise FactorizationError(
             f"Gram matrix is not positive definite at pivot {piv.value}; retry with a larger damping",
             pivot=int(piv.value))

@@ -443,3 +443,52 @@ def test_staged_pageable_upload_is_exact(fsb, dt, m):
     got = sm.tensor.cpu().numpy()
     ref = rng.__class__(np.random.PCG64(m)).standard_normal((60, m)).astype(dt)
     assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------- definiteness in the split Gram
+
+def test_auto_falls_back_to_fp64_when_the_split_gram_is_indefinite(fsb):
+    """Near-dependent rows with lam far below the F16X2 Gram's ~2^-22 ||G|| error: W~ can lose
+    definiteness where the reference's fp64 W keeps it.  precision="auto" must then decide in the
+    reference's arithmetic (succeed as it does), never raise on the split factor's behalf."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    n, m = 64, 4096
+    S = rng.standard_normal((n, m))
+    for k in range(0, 16, 2):                    # 8 near-duplicate row pairs
+        S[k + 1] = S[k] + 1e-6 * rng.standard_normal(m)
+    S32 = S.astype(np.float32)
+    v32 = rng.standard_normal(m).astype(np.float32)
+    lam = 1e-5          # ~2^-22 ||G|| ~ 1e-3 >> lam: the F16X2 factor breaks down (pivot 7 on a B200)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(S32), lam, v32)
+    try:
+        fsb.solve_chol(system, precision="f16x2", refine=0)
+        split_failed = False
+    except fsb.FactorizationError:
+        split_failed = True
+    assert split_failed
+    sol = fsb.solve_chol(system)
+    assert sol.precision == "fp64"
+    ref = O.solve_chol(S32.astype(np.float64), v32.astype(np.float64), lam)
+    # cond(W) ~ 4e8: the reference's own fp64 solve ends at rel_residual 4.6e-8 (ours: 1.8e-8)
+    assert sol.rel_residual <= 10 * ref.rel_residual, (sol.rel_residual, ref.rel_residual)
+    assert O.rel_err(sol.x, ref.x) <= 1e-5, O.rel_err(sol.x, ref.x)
+
+
+def test_auto_reports_the_reference_pivot_when_fp64_also_fails(fsb):
+    """Rows 0 and 1 identical with an exactly representable pivot (G_00 = 4, lam = 1e-30 rounds
+    away): W_11 - L_10^2 = 4 - 2 * 2 = 0 in any order of fp64 operations, so the reference's dpotrf
+    fails at pivot 1; the drop-in's split factor fails too, its fp64 retry as well, and it raises
+    the reference's pivot."""
+    rng = np.random.Generator(np.random.PCG64(7))
+    n, m = 32, 2048
+    S = rng.choice(np.array([-1.0, 1.0], dtype=np.float32), size=(n, m))
+    S[0] = 0.0
+    S[0, :4] = 1.0
+    S[1] = S[0]
+    v = rng.standard_normal(m).astype(np.float32)
+    lam = 1e-30
+    with pytest.raises(O.OracleFactorizationError) as eo:
+        O.solve_chol(S.astype(np.float64), v.astype(np.float64), lam)
+    with pytest.raises(fsb.FactorizationError) as eg:
+        fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v))
+    assert eg.value.pivot == eo.value.pivot == 1
