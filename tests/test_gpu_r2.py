@@ -492,3 +492,23 @@ def test_auto_reports_the_reference_pivot_when_fp64_also_fails(fsb):
     with pytest.raises(fsb.FactorizationError) as eg:
         fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S), lam, v))
     assert eg.value.pivot == eo.value.pivot == 1
+
+
+def test_complex64_solve_svd_eigh_refines_to_the_dense_solution(fsb):
+    """complex64 scores: the Hermitian route runs on the real representation in F16X2 and its
+    z-space refinement (kept-eigenpair apply) takes x to the fp64 dense solution."""
+    rng = np.random.Generator(np.random.PCG64(31))
+    n, m = 48, 3000
+    A = (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))).astype(np.complex64)
+    v = (rng.standard_normal(m) + 1j * rng.standard_normal(m)).astype(np.complex64)
+    lam = 1e-2
+    system = fsb.DampedSystem(fsb.ScoreMatrix(A), lam, v)
+    sol = fsb.solve_svd_eigh(system)
+    raw = fsb.solve_svd_eigh(system, refine=0)
+    A64, v64 = A.astype(np.complex128), v.astype(np.complex128)
+    # (A^H A + lam I)^-1 v = (v - A^H (A A^H + lam I)^-1 A v) / lam  (Woodbury; n x n in fp64)
+    z = np.linalg.solve(A64 @ A64.conj().T + lam * np.eye(n), A64 @ v64)
+    ref = (v64 - A64.conj().T @ z) / lam
+    err = np.linalg.norm(sol.x - ref) / np.linalg.norm(ref)
+    assert err <= 1e-9, err
+    assert sol.rel_residual <= 1e-10 < raw.rel_residual, (sol.rel_residual, raw.rel_residual)
