@@ -98,6 +98,11 @@ struct fs_ctx {
   double* early_x_host = nullptr;
   int early_x_state = 0;
   cudaEvent_t ev_xready = nullptr, ev_xcopy = nullptr;
+  // z-space refinement: |d|, |z| of a correction fetched on a side stream, so the host decides on
+  // the next step while the current x + y pass still runs (no idle gap between the steps)
+  cudaStream_t dz_st = nullptr;
+  cudaEvent_t ev_dz = nullptr, ev_dz_done = nullptr;
+  double* h_dz = nullptr;       // pinned, 2 doubles
   // stage timing (fs_profile_enable): events recorded on the solve stream after each stage,
   // in chronological order; stage time = gap to the previous mark
   static constexpr int kMaxMarks = 24;
@@ -627,8 +632,25 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
   const bool want_z = (flags & FS_FLAG_REFINE_Z) != 0 && want_res;
   const int zsteps = want_z ? std::max(1, (flags >> 8) & 0xFF) : 0;
   int zdone = 0;
+  // single rank: fetch (|d|^2, |z|^2) of the step on the side stream (created on first use;
+  // false -> the caller synchronises the stream instead)
+  auto fetch_dz = [&]() -> bool {
+    if (!ctx->dz_st) {
+      if (cudaStreamCreateWithFlags(&ctx->dz_st, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_dz, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_dz_done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaMallocHost((void**)&ctx->h_dz, 2 * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+    }
+    return cudaEventRecord(ctx->ev_dz, st) == cudaSuccess && cudaStreamWaitEvent(ctx->dz_st, ctx->ev_dz, 0) == cudaSuccess &&
+           cudaMemcpyAsync(ctx->h_dz, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->dz_st) == cudaSuccess &&
+           cudaEventRecord(ctx->ev_dz_done, ctx->dz_st) == cudaSuccess;
+  };
+  bool dz_async = false;
   // one z-space step: d = W~^-1 lam (y - z_acc), z_acc += d, x += -S^T d / lam, y = S x
-  auto z_step = [&]() -> int {
+  auto z_step = [&](bool fetch) -> int {
     NvtxRange r("fs: z-space refinement step");
     if (!y_ready && !idle()) FS_STEP(fs_gemv_rows(ctx, dtype, S, n, m, ldS, x, FS_F64, ctx->d_y, stream));
     if (multi) {
@@ -647,6 +669,8 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
       zadd_kernel<<<1, 1024, 0, st>>>(ctx->d_zacc, ctx->d_z, n, ctx->d_sums);
       ctx->launches += l + 2;
     }
+    static const bool dz_env = getenv("FS_DZ_ASYNC") ? atoi(getenv("FS_DZ_ASYNC")) != 0 : true;
+    dz_async = fetch && !multi && dz_env && fetch_dz();
     if (ctx->early_x_state == 1) {   // x changes: the early copy must finish reading it first
       FS_CK(cudaStreamWaitEvent(st, ctx->ev_xcopy, 0), "event wait");
       ctx->early_x_state = 2;
@@ -660,13 +684,20 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
     if (!idle()) FS_CKS(cudaMemcpyAsync(ctx->d_zacc, ctx->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, st), "z copy");
     if (!idle()) FS_CKS(cudaMemsetAsync(ctx->d_r, 0, m * sizeof(double), st), "zero rhs");
     for (int step = 0; step < zsteps; ++step) {
-      if (int rc = z_step()) return rc;
-      if (!multi && step + 1 < zsteps) {
-        FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "dz d2h");
-        FS_CK(cudaStreamSynchronize(st), "sync");
+      const bool check = !multi && step + 1 < zsteps;
+      if (int rc = z_step(check)) return rc;
+      if (check) {
+        const double* hs = ctx->h_sums;
+        if (dz_async) {
+          FS_CK(cudaEventSynchronize(ctx->ev_dz_done), "dz wait");
+          hs = ctx->h_dz;
+        } else {
+          FS_CK(cudaMemcpyAsync(ctx->h_sums, ctx->d_sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "dz d2h");
+          FS_CK(cudaStreamSynchronize(st), "sync");
+        }
         // the last correction moved z by <= 1e-12 of its size: x is at (or next to) the fp64
         // residual floor; the residual below decides whether one more step is needed
-        if (!(ctx->h_sums[0] > 1e-24 * ctx->h_sums[1])) break;
+        if (!(hs[0] > 1e-24 * hs[1])) break;
       }
     }
   }
@@ -679,7 +710,7 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
   // at the fp64 floor of z, which at large m can leave x's residual slightly above 1e-10)
   for (int zround = 0;; ++zround) {
     if (zround > 0) {
-      if (int rc = z_step()) return rc;
+      if (int rc = z_step(false)) return rc;
     }
     for (int pass = 0; want_res && pass <= max_steps; ++pass) {
       NvtxRange r("fs: residual (+ x-space refinement)");
@@ -867,6 +898,10 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   for (int i = 0; i < fs_ctx::kMaxChunks; ++i)
     if (ctx->ev_chunk[i]) cudaEventDestroy(ctx->ev_chunk[i]);
   if (ctx->ev_free) cudaEventDestroy(ctx->ev_free);
+  if (ctx->dz_st) cudaStreamDestroy(ctx->dz_st);
+  if (ctx->ev_dz) cudaEventDestroy(ctx->ev_dz);
+  if (ctx->ev_dz_done) cudaEventDestroy(ctx->ev_dz_done);
+  if (ctx->h_dz) cudaFreeHost(ctx->h_dz);
   if (ctx->ev_xready) cudaEventDestroy(ctx->ev_xready);
   if (ctx->ev_xcopy) cudaEventDestroy(ctx->ev_xcopy);
   if (ctx->up_st) cudaStreamDestroy(ctx->up_st);
