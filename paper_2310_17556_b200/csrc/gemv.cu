@@ -590,6 +590,14 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
       }
     int setx = 0;
     uint32_t phx = 0;
+    // accumulate: the old x of the panel is pushed with rank 0's partials; it is loaded one panel
+    // ahead so the global-load latency stays off the exchange (the y group waits for that push)
+    const bool xo_push = accumulate && rank == 0 && tid < CW && !y_only;
+    double xold_next = 0.0;
+    if (xo_push && np > 0) {
+      const int64_t c = cid * CW + tid;
+      xold_next = c < m ? x[c] : 0.0;
+    }
     for (int64_t j = 0; j < np && !y_only; ++j) {
       const int rb = (int)(j & 1);
       Zt acc[VN1];
@@ -636,9 +644,12 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         const uint32_t bar = ptx::smem_u32(&xbar[xb]);
 #pragma unroll
         for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(mine, r), part, ptx::mapa(bar, r));
-        if (accumulate && rank == 0) {
-          const int64_t c = (cid + j * ncl) * CW + tid;
-          const double xold = c < m ? x[c] : 0.0;
+        if (xo_push) {
+          const double xold = xold_next;
+          if (j + 1 < np) {
+            const int64_t cn = (cid + (j + 1) * ncl) * CW + tid;
+            xold_next = cn < m ? x[cn] : 0.0;
+          }
           const uint32_t xa = ptx::smem_u32(xo + xb * 64 + tid);
 #pragma unroll
           for (int r = 0; r < CL; ++r) st_async_f64(ptx::mapa(xa, r), xold, ptx::mapa(bar, r));
