@@ -183,7 +183,7 @@ int fs_chol_solve_host(fs_ctx* ctx, int dtype, int precision, const void* S_host
 /* ---- eigh comparison route (solvers.py:243-277, :294-354) ----
  * fs_syevj_packed: eigenpairs of a packed lower symmetric fp64 matrix (device): w (n) descending,
  * U (n x n, leading dimension ldU, column j <-> w[j]); parallel Jacobi on the GPU (replaces
- * np.linalg.eigh -> dsyevd).  n <= 8192.  *sweeps = Jacobi sweeps run.  Synchronizes.
+ * np.linalg.eigh -> dsyevd).  n <= 16384.  *sweeps = Jacobi sweeps run.  Synchronizes.
  * fs_eigh_solve: solve_svd_eigh — Gram (precision as fs_chol_solve), eigh, singular values
  * floored at sigma_floor * sigma_max (*rank = kept count), x from the kept eigenpairs, residual
  * against S (flags: FS_FLAG_RESIDUAL; with it, FS_FLAG_REFINE_Z_STEPS(k) in the fp32-split

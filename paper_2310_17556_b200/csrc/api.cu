@@ -248,7 +248,7 @@ bool use_ring(fs_ctx* ctx, const void* S, int64_t n, int64_t m, int64_t ldS) {
 
 int ensure_eig(fs_ctx* ctx) {
   if (ctx->d_eig) return FS_OK;
-  if (ctx->n_max > fs::syevj_max_n()) return fail(ctx, FS_EUNSUPPORTED, "eigh route supports n <= 8192");
+  if (ctx->n_max > fs::syevj_max_n()) return fail(ctx, FS_EUNSUPPORTED, "eigh route supports n <= 16384");
   const int64_t n = ctx->n_max;
   bool ok = cudaMalloc(&ctx->d_eig, fs::syevj_workspace_bytes(n, ctx->num_sms)) == cudaSuccess &&
             cudaMalloc((void**)&ctx->d_U, (size_t)n * n * sizeof(double)) == cudaSuccess &&

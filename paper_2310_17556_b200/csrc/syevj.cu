@@ -649,7 +649,7 @@ bool syevj_block(int64_t n) {
   return env != 0 && n >= 2 * kSB;
 }
 
-int64_t syevj_max_n() { return 8192; }
+int64_t syevj_max_n() { return 16384; }   // the one-CTA sort: 12 B x 16384 of shared memory
 
 cudaError_t eig_apply(const double* U, int64_t ldu, int64_t n, int64_t r, const double* u, const double* w, double lam,
                       double* t, double* z, cudaStream_t st, int* launches) {
@@ -679,7 +679,7 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
     static bool battr = false;
     if (!battr) {
       cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
-      cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 8192);
+      cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384);
       battr = true;
     }
     int per_sm = 0;
@@ -727,7 +727,7 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 8192);
+    cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384);
     attr = true;
   }
   int per_sm = 0;

@@ -750,7 +750,7 @@ def _syevj_device(Gp: torch.Tensor, n: int):
 def _svda_gram_route(Gp: torch.Tensor, n: int):
     """(sigma, U) from the Gram when it certifies a well-conditioned S, else None."""
     import os
-    if os.environ.get("FS_SVDA_GRAM", "1") == "0" or n > 8192:
+    if os.environ.get("FS_SVDA_GRAM", "1") == "0" or n > 16384:
         return None
     w, U = _syevj_device(Gp, n)
     wh = w.cpu().numpy()

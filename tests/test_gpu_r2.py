@@ -512,3 +512,19 @@ def test_complex64_solve_svd_eigh_refines_to_the_dense_solution(fsb):
     err = np.linalg.norm(sol.x - ref) / np.linalg.norm(ref)
     assert err <= 1e-9, err
     assert sol.rel_residual <= 1e-10 < raw.rel_residual, (sol.rel_residual, raw.rel_residual)
+
+
+def test_eigh_gram_above_8192(fsb):
+    """n = 8200 (padded to 8224: the descending sort runs on 16384 keys in one CTA): the Jacobi
+    eigendecomposition's invariants on the GPU — U orthonormal, G U = U diag(w), w descending,
+    sum(w) = trace(G) — to fp64 accuracy."""
+    n, m = 8200, 9000
+    g = torch.Generator(device="cuda").manual_seed(8200)
+    S = torch.randn(n, m, device="cuda", dtype=torch.float64, generator=g) / np.sqrt(m)
+    w, U, sweeps = fsb.eigh_gram(fsb.ScoreMatrix(S), "fp64")
+    G = S @ S.T
+    assert bool((w[:-1] >= w[1:]).all())
+    scale = G.norm().item()
+    assert (G @ U - U * w).norm().item() <= 1e-11 * scale * np.sqrt(n)
+    assert (U.T @ U - torch.eye(n, device="cuda", dtype=torch.float64)).norm().item() <= 1e-10 * np.sqrt(n)
+    assert abs(w.sum().item() - torch.trace(G).item()) <= 1e-11 * abs(torch.trace(G).item())
