@@ -626,7 +626,7 @@ static int finish_x(fs_ctx* ctx, int dtype, const void* S, int64_t n, int64_t m,
   // the headline (sigma^2/lam ~ 1e6).  The z residual needs no extra pass: with y = S x (already
   // formed by the fused x + y pass, exact fp64 products), lam (y - z) = S v - S S^T z - lam z =
   // u - W z exactly.  A step is: d = W~^-1 lam (y - z) (the TRSV pair), z += d, and one fused pass
-  // x += (0 - S^T d)/lam, y = S x.  Single rank: stop once |d| <= 2^-50 |z|; multi-rank: the
+  // x += (0 - S^T d)/lam, y = S x.  Single rank: stop once |d| <= 1e-12 |z|; multi-rank: the
   // fixed step count (control flow may not depend on rank-local data).  Profiled as
   // FS_PROF_REFINE.
   const bool want_z = (flags & FS_FLAG_REFINE_Z) != 0 && want_res;
