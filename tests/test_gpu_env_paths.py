@@ -5,6 +5,7 @@ process, because the switches are read once per process):
                   K-blocks, accumulate), the path that lets n = 16384, m = 2e6 fit on one B200
   FS_F16_RING=1   the F16X2 ring SYRK (each tile split once into an L2-resident ring)
   FS_TRSV_FLAGS=0 the single-CTA TRSV pair instead of the flag-chained one
+  FS_DZ_ASYNC=0   the refinement's convergence test through a stream sync instead of a side stream
 
 Tolerances: fp32 modes relerr(x) <= 1e-6 vs the reference's fp64 solve of the same
 fp32-rounded system; the chunked Gram vs the one-shot Gram <= 2e-6 of max |G| (the same split
@@ -97,6 +98,15 @@ def test_ring_syrk_gram_is_bit_identical_and_solves(gpu, tmp_path, n, m):
     x2, G2, _ = run_case(tmp_path, {"FS_F16_RING": "1"}, n, m, "f16x2")
     assert np.array_equal(G1, G2)          # same tiles, same MMA order: bit-identical Gram
     assert O.rel_err(x2, reference(n, m).x) <= 1e-6
+
+
+def test_refinement_step_decisions_sync_or_side_stream_bit_identical(gpu, tmp_path):
+    """The z-space steps' convergence numbers come back on a side stream while the x + y pass runs
+    (default) or through a stream sync (FS_DZ_ASYNC=0): the same decisions, the same bits."""
+    n, m = 1024, 200000
+    x1, _, i1 = run_case(tmp_path, {}, n, m, "f16x2", refine=4)
+    x2, _, i2 = run_case(tmp_path, {"FS_DZ_ASYNC": "0"}, n, m, "f16x2", refine=4)
+    assert np.array_equal(x1, x2) and i1["rel_residual"] == i2["rel_residual"] <= 1e-10
 
 
 @pytest.mark.parametrize("n", [130, 1000])
