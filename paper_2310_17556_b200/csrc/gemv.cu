@@ -950,6 +950,64 @@ __global__ void check_finite_kernel(const T* __restrict__ a, int64_t rows, int64
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// The same check (and row maxima) for wide rows: one block per (row, 8192-element column chunk),
+// every thread's 32 elements loaded as independent 16-byte vectors before any use (128 bytes in
+// flight per thread), one block reduction and atomicMax per (row, chunk).  The strided kernel
+// above walks all rows inside each block with 16 bytes in flight and two barriers per row: 2.9 ms
+// for a 1024 x 1e6 fp32 matrix, against ~0.65 ms at the copy bandwidth here.
+constexpr int kCFChunk = 8192;
+template <typename T>
+__global__ void __launch_bounds__(256)
+check_finite_rows_kernel(const T* __restrict__ a, int64_t rows, int64_t cols, int64_t ld, int* __restrict__ flag,
+                         unsigned* __restrict__ rowmax) {
+  using VT = typename VecOf<T>::V;
+  constexpr int VN = VecOf<T>::N;
+  constexpr int kPer = kCFChunk / 256 / VN;      // vectors per thread
+  __shared__ float red[8];
+  bool bad = false;
+  const int64_t c0 = (int64_t)blockIdx.x * kCFChunk;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const T* row = a + r * ld;
+    float mx = 0.f;
+    if (c0 + kCFChunk <= cols && (reinterpret_cast<uintptr_t>(row + c0) & 15) == 0) {
+      VT v[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) v[k] = ld_stream(reinterpret_cast<const VT*>(row + c0) + k * 256 + threadIdx.x);
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        T e[VN];
+        vec_to_array(v[k], e);
+#pragma unroll
+        for (int i = 0; i < VN; ++i) {
+          bad |= !isfinite(e[i]);
+          mx = fmaxf(mx, fabsf((float)e[i]));
+        }
+      }
+    } else {
+      const int64_t c1 = c0 + kCFChunk < cols ? c0 + kCFChunk : cols;
+      for (int64_t c = c0 + threadIdx.x; c < c1; c += 256) {
+        const T x = ld_stream(row + c);
+        bad |= !isfinite(x);
+        mx = fmaxf(mx, fabsf((float)x));
+      }
+    }
+    if (rowmax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float b = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) b = fmaxf(b, red[w]);
+        if (b > 0.f) atomicMax(rowmax + r, __float_as_uint(b));
+      }
+      __syncthreads();
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // F16X2 row scales from exact row maxima: 2^k with max |S_i| 2^k in [2^14, 2^15), so no element
 // of the row can overflow fp16 (max 65504) and elements down to 2^-18 of the row maximum keep a
 // normal lo plane (all 22 bits).
@@ -1248,6 +1306,14 @@ cudaError_t flag_bit_to_double(const int* flags, int bit, double* out, cudaStrea
 
 cudaError_t check_finite(const void* a, bool is64, int64_t rows, int64_t cols, int64_t ld, int* flag, int num_sms,
                          cudaStream_t st, int* launches, unsigned* rowmax) {
+  if (cols >= kCFChunk) {   // wide rows: one block per (row, column chunk)
+    const int64_t gx = (cols + kCFChunk - 1) / kCFChunk;
+    const dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(rows, 65535));
+    if (is64) check_finite_rows_kernel<double><<<grid, 256, 0, st>>>((const double*)a, rows, cols, ld, flag, rowmax);
+    else check_finite_rows_kernel<float><<<grid, 256, 0, st>>>((const float*)a, rows, cols, ld, flag, rowmax);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   // ~num_sms * 8 blocks: x covers the columns (<= 1024 per block row), y the rows
   const int64_t want = (int64_t)num_sms * 8;
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((cols + 1023) / 1024, want));
