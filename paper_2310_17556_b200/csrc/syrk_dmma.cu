@@ -43,15 +43,19 @@ FS_DEVINL void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// One 32-column stage: 8 k-steps of the warp's 8 x 4 grid of m8n8k4 fp64 MMAs.
-FS_DEVINL void stage_mma(double (&acc)[8][4][2], const double* A, const double* B, int wr, int wc, int fr, int fk) {
+// One 32-column stage: 8 k-steps of the warp's 8 x 4 grid of m8n8k4 fp64 MMAs.  T = float: the
+// stage holds the fp32 scores as they are and each fragment is widened on its way to the
+// registers (exact) — half the shared-memory bytes of an fp64 stage.  Row pitch LD elements (36:
+// the eight fragment rows of a load hit distinct banks in both widths).
+template <typename T = double, int LD = kLd>
+FS_DEVINL void stage_mma(double (&acc)[8][4][2], const T* A, const T* B, int wr, int wc, int fr, int fk) {
 #pragma unroll
   for (int ks = 0; ks < kK; ks += 4) {
     double af[8], bf[4];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) af[a] = A[(wr + 8 * a + fr) * kLd + ks + fk];
+    for (int a = 0; a < 8; ++a) af[a] = (double)A[(wr + 8 * a + fr) * LD + ks + fk];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) bf[b] = B[(wc + 8 * b + fr) * kLd + ks + fk];
+    for (int b = 0; b < 4; ++b) bf[b] = (double)B[(wc + 8 * b + fr) * LD + ks + fk];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -244,37 +248,51 @@ syrk_dmma_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int
   store_tile(acc, rA, rB, n, lam, ws, Gp, direct, wr, wc, fr, lane, ldc);
 }
 
-// fp64 scores with 16-byte aligned rows: global -> shared with cp.async (no register staging,
-// no store pass after the MMAs), three stages in flight (3 x 72 KB).  Thread t copies 8 16-byte
-// pieces of each operand per stage; pieces past the last row or column are zero-filled (src-size).
-constexpr int kAsyncStages = 3;
-constexpr size_t kAsyncSmemBytes = (size_t)kAsyncStages * kStageDoubles * sizeof(double);   // 221 KB
+// Scores with 16-byte aligned rows: global -> shared with cp.async (no register staging, no
+// store pass after the MMAs).  fp64: three stages in flight (3 x 72 KB); fp32: four (4 x 36 KB),
+// the fp32 values staged as they are and widened per fragment.  Thread t copies the 16-byte pieces
+// of its rows (8 per operand and stage in fp64, 4 in fp32); pieces past the last row or column
+// are zero-filled (src-size).
+template <typename T> struct Async;
+template <> struct Async<double> { static constexpr int kStages = 3, kPieces = 16, kPerPiece = 2; };
+template <> struct Async<float> { static constexpr int kStages = 4, kPieces = 8, kPerPiece = 4; };
+template <typename T> constexpr int async_stage_elems() { return 2 * kT * kLd; }
+template <typename T> constexpr size_t async_smem_bytes() {
+  return (size_t)Async<T>::kStages * async_stage_elems<T>() * sizeof(T);   // 221 KB fp64, 147 KB fp32
+}
+constexpr size_t kAsyncSmemBytes = async_smem_bytes<double>();
 
-FS_DEVINL void cp16(double* dst, const double* src, int bytes) {
+FS_DEVINL void cp16(void* dst, const void* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(bytes)
                : "memory");
 }
 
-FS_DEVINL void issue_stage(double* dst, const double* __restrict__ S, int64_t n, int64_t kend, int64_t ldS, int64_t r0,
+template <typename T>
+FS_DEVINL void issue_stage(T* dst, const T* __restrict__ S, int64_t n, int64_t kend, int64_t ldS, int64_t r0,
                            int64_t k0) {
+  constexpr int kPieces = Async<T>::kPieces, kPer = Async<T>::kPerPiece;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int piece = threadIdx.x + q * kThreads;       // 128 rows x 16 pieces
-    const int r = piece >> 4, c = (piece & 15) * 2;
+  for (int q = 0; q < kT * kPieces / kThreads; ++q) {
+    const int piece = threadIdx.x + q * kThreads;       // 128 rows x kPieces pieces
+    const int r = piece / kPieces, c = (piece % kPieces) * kPer;
     const int64_t gr = r0 + r, gc = k0 + c;
     const int64_t left = kend - gc;
-    const int bytes = gr < n ? (left >= 2 ? 16 : left == 1 ? 8 : 0) : 0;
+    const int bytes = gr < n ? (int)(left >= kPer ? 16 : left > 0 ? left * (int64_t)sizeof(T) : 0) : 0;
     cp16(dst + r * kLd + c, bytes ? S + gr * ldS + gc : S, bytes);
   }
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
+syrk_dmma_async_kernel(const T* __restrict__ S, int64_t n, int64_t m, int64_t ldS, int64_t kchunk, int P,
                        double lam, double* __restrict__ ws, double* __restrict__ Gp, int direct, int flush,
                        int64_t ldc = 0, const int64_t* status = nullptr, int jmax = 0) {
   if (status && *(volatile const int64_t*)status != 0) return;
-  extern __shared__ __align__(16) double dsm[];
+  constexpr int kAsyncStages = Async<T>::kStages;
+  constexpr int kStageElems = async_stage_elems<T>();
+  extern __shared__ __align__(16) unsigned char dsm_raw[];
+  T* dsm = reinterpret_cast<T*>(dsm_raw);
   int I, J;
   if (jmax > 0) {            // column strip: tiles (I, J) with J < jmax, grid jmax x row tiles
     I = blockIdx.x / jmax;
@@ -310,24 +328,25 @@ syrk_dmma_async_kernel(const double* __restrict__ S, int64_t n, int64_t m, int64
   const int nst = kbeg < kend ? (int)((kend - kbeg + kK - 1) / kK) : 0;
   auto issue = [&](int st) {
     if (st < nst) {
-      double* d = dsm + (st % kAsyncStages) * kStageDoubles;
-      issue_stage(d, S, n, kend, ldS, rA, kbeg + (int64_t)st * kK);
-      if (!diag) issue_stage(d + kT * kLd, S, n, kend, ldS, rB, kbeg + (int64_t)st * kK);
+      T* d = dsm + (st % kAsyncStages) * kStageElems;
+      issue_stage<T>(d, S, n, kend, ldS, rA, kbeg + (int64_t)st * kK);
+      if (!diag) issue_stage<T>(d + kT * kLd, S, n, kend, ldS, rB, kbeg + (int64_t)st * kK);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");   // empty groups keep the count uniform
   };
-  issue(0);
-  issue(1);
+#pragma unroll
+  for (int q = 0; q < kAsyncStages - 1; ++q) issue(q);
   int buf = 0;
   double* fbuf = ws + (size_t)blockIdx.x * kT * kT;
   int since = 0;
   bool flushed = false;
   for (int st = 0; st < nst; ++st) {
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // stage st landed (this thread's pieces)
+    // stage st landed (this thread's pieces): kAsyncStages - 2 younger groups may stay in flight
+    asm volatile("cp.async.wait_group %0;" ::"n"(kAsyncStages - 2) : "memory");
     __syncthreads();                                       // ... everyone's; stage st-1 fully consumed
-    issue(st + 2);                                         // refills the buffer stage st-1 used
-    const double* A = dsm + buf * kStageDoubles;
-    stage_mma(acc, A, diag ? A : A + kT * kLd, wr, wc, fr, fk);
+    issue(st + kAsyncStages - 1);                          // refills the buffer stage st-1 used
+    const T* A = dsm + buf * kStageElems;
+    stage_mma<T>(acc, A, diag ? A : A + kT * kLd, wr, wc, fr, fk);
     buf = buf == kAsyncStages - 1 ? 0 : buf + 1;
     if (flush && ++since == kFlush && st + 1 < nst) {
       flush_acc(acc, fbuf, !flushed, wr, wc, fr, lane);
@@ -441,9 +460,15 @@ cudaError_t syrk_dmma(bool s_f64, const void* S, int64_t n, int64_t m, int64_t l
   // the flush slots are the split-K partial tiles' own: one 128 x 128 fp64 tile per CTA
   const int flush = ws && (size_t)grid * kT * kT * sizeof(double) <= ws_bytes && dmma_flush() ? 1 : 0;
   if (s_f64 && vec && dmma_async()) {
-    cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
-    syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam,
-                                                                     ws, Gp, direct, flush);
+    cudaFuncSetAttribute(syrk_dmma_async_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAsyncSmemBytes);
+    syrk_dmma_async_kernel<double><<<grid, kThreads, kAsyncSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk,
+                                                                             p.P, lam, ws, Gp, direct, flush);
+  } else if (!s_f64 && vec && dmma_async()) {
+    constexpr size_t smem32 = async_smem_bytes<float>();
+    cudaFuncSetAttribute(syrk_dmma_async_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32);
+    syrk_dmma_async_kernel<float><<<grid, kThreads, smem32, st>>>((const float*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
+                                                                  Gp, direct, flush);
   } else if (s_f64) {
     cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>((const double*)S, n, m, ldS, p.kchunk, p.P, lam, ws,
@@ -474,13 +499,14 @@ cudaError_t syrk_dmma_trail(const double* P, int64_t nt, int64_t K, int64_t ldP,
   const bool vec = ((reinterpret_cast<uintptr_t>(P) | (uintptr_t)(ldP * 8)) & 15) == 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(syrk_dmma_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmemBytes);
+    cudaFuncSetAttribute(syrk_dmma_async_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kAsyncSmemBytes);
     cudaFuncSetAttribute(syrk_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     attr = true;
   }
   if (vec)
-    syrk_dmma_async_kernel<<<grid, kThreads, kAsyncSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, ldc,
-                                                                     status, jmax);
+    syrk_dmma_async_kernel<double><<<grid, kThreads, kAsyncSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0,
+                                                                             ldc, status, jmax);
   else
     syrk_dmma_kernel<double><<<grid, kThreads, kSmemBytes, st>>>(P, nt, K, ldP, K, 1, 0.0, nullptr, C, 1, 0, 0, ldc,
                                                                  status, jmax);
