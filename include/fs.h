@@ -225,6 +225,11 @@ int fs_hermitian_gram(fs_ctx* ctx, const double* G2_packed, int64_t n, double la
  * solvers.py:272-276, A.T @ B -> dgemm) and the svd route's Q^T = L^-1 S, V^T = W^T Q^T. */
 int fs_apply_rows(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
                   int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream);
+/* The same with T lower triangular (its strictly upper part is never read: every row tile stops
+ * its contraction at its last row, ~half the products): the CholeskyQR steps' Q^T = L^-1 X and
+ * the triangular factor products. */
+int fs_apply_rows_lower(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                        int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream);
 
 /* ---- direct-SVD comparison route ("svda", solvers.py:280-291, :357-364) ----
  * The reference calls dgesdd on S.  The GPU route: shifted CholeskyQR3 of S^T (fs_gram_packed in

@@ -58,6 +58,8 @@ SIGNATURES = {
     "fs_hermitian_gram": (ctypes.c_int, [_vp, _vp, _c_int64, ctypes.c_double, _vp, _c_int64, _vp]),
     "fs_apply_rows": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _c_int64, _c_int64,
                                      _vp, _c_int64, _vp]),
+    "fs_apply_rows_lower": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _c_int64, _c_int64, _c_int64, _vp, _c_int64,
+                                           _c_int64, _vp, _c_int64, _vp]),
     "fs_heevj_packed": (ctypes.c_int, [_vp, _vp, _c_int64, _vp, _vp, _c_int64, ctypes.POINTER(ctypes.c_int), _vp]),
     "fs_tri_inverse": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp, _c_int64, _vp]),
     "fs_jacobi_svd": (ctypes.c_int, [_vp, _vp, _c_int64, _c_int64, _vp, _vp, _c_int64, _vp, _c_int64,

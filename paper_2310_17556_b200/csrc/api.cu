@@ -1469,17 +1469,27 @@ int fs_hermitian_gram(fs_ctx* ctx, const double* G2_packed, int64_t n, double la
   return FS_OK;
 }
 
-int fs_apply_rows(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
-                  int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream) {
+static int apply_rows_impl(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                           int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream, bool lower) {
   if (!ctx) return FS_EINVAL;
   if (dtype != FS_F32 && dtype != FS_F64) return fail(ctx, FS_EINVAL, "dtype must be FS_F32 or FS_F64");
   if (!T || !X || !Y || r < 1 || n < 1 || m < 1 || ldT < n || ldX < m || ldY < m)
     return fail(ctx, FS_EINVAL, "bad apply_rows arguments");
   int l = 0;
-  cudaError_t e = fs::apply_rows(dtype == FS_F64, T, r, n, ldT, X, m, ldX, Y, ldY, (cudaStream_t)stream, &l);
+  cudaError_t e = fs::apply_rows(dtype == FS_F64, T, r, n, ldT, X, m, ldX, Y, ldY, (cudaStream_t)stream, &l, lower);
   ctx->launches += l;
   if (e != cudaSuccess) return cuda_fail(ctx, e, "apply_rows");
   return FS_OK;
+}
+
+int fs_apply_rows(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                  int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream) {
+  return apply_rows_impl(ctx, dtype, T, r, n, ldT, X, m, ldX, Y, ldY, stream, false);
+}
+
+int fs_apply_rows_lower(fs_ctx* ctx, int dtype, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X,
+                        int64_t m, int64_t ldX, double* Y, int64_t ldY, void* stream) {
+  return apply_rows_impl(ctx, dtype, T, r, n, ldT, X, m, ldX, Y, ldY, stream, true);
 }
 
 int fs_heevj_packed(fs_ctx* ctx, const double* G2_packed, int64_t n, double* w, double* U, int64_t ldU, int* sweeps,

@@ -11,7 +11,8 @@
 // accumulators per thread), K (= n, the contraction runs over the ROWS of X) in 32-deep stages,
 // double-buffered through shared memory with register staging.  The X stage is stored transposed
 // ([column][k], pitch 36 doubles) so the .col B fragments read it like the SYRK's B rows; a warp
-// stores 32 consecutive k of one column per instruction (conflict-free).  Tiles sharing a column
+// stores 32 consecutive k of one column per instruction (conflict-free).  A lower-triangular T
+// (the CholeskyQR steps' L^-1) stops each row tile's K loop at its last row: ~half the products.  Tiles sharing a column
 // panel of X are adjacent in the launch order, so X streams from HBM about once and T (r x n
 // doubles) stays in L2.  The bound is the fp64 tensor rate (2 r n m flops).
 #include "common.cuh"
@@ -115,7 +116,7 @@ struct LoadX {
 template <typename TX>
 __global__ void __launch_bounds__(kThreads, 1)
 apply_rows_kernel(const double* __restrict__ T, int64_t r, int64_t n, int64_t ldT, const TX* __restrict__ X, int64_t m,
-                  int64_t ldX, double* __restrict__ Y, int64_t ldY, int tiles_r, int vecT, int vecX) {
+                  int64_t ldX, double* __restrict__ Y, int64_t ldY, int tiles_r, int vecT, int vecX, int lower) {
   extern __shared__ __align__(16) double dsm[];
   const int64_t r0 = (int64_t)(blockIdx.x % tiles_r) * kT;
   const int64_t c0 = (int64_t)(blockIdx.x / tiles_r) * kT;
@@ -135,8 +136,10 @@ apply_rows_kernel(const double* __restrict__ T, int64_t r, int64_t n, int64_t ld
   lx.store(dsm + kT * kLd);
   __syncthreads();
   int buf = 0;
-  for (int64_t k0 = 0; k0 < n; k0 += kK) {
-    const bool more = k0 + kK < n;
+  // lower-triangular T: rows [r0, r0 + 128) have no entries past column r0 + 127
+  const int64_t kend = lower ? (r0 + kT < n ? r0 + kT : n) : n;
+  for (int64_t k0 = 0; k0 < kend; k0 += kK) {
+    const bool more = k0 + kK < kend;
     if (more) {
       lt.load(T, r, n, ldT, r0, k0 + kK, vecT);
       lx.load(X, n, m, ldX, k0 + kK, c0, vecX);
@@ -173,7 +176,7 @@ apply_rows_kernel(const double* __restrict__ T, int64_t r, int64_t n, int64_t ld
 }  // namespace
 
 cudaError_t apply_rows(bool x_f64, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X, int64_t m,
-                       int64_t ldX, double* Y, int64_t ldY, cudaStream_t st, int* launches) {
+                       int64_t ldX, double* Y, int64_t ldY, cudaStream_t st, int* launches, bool lower) {
   if (r < 1 || n < 1 || m < 1) return cudaErrorInvalidValue;
   const int64_t tiles_r = (r + kT - 1) / kT, tiles_c = (m + kT - 1) / kT;
   if (tiles_r * tiles_c > INT32_MAX) return cudaErrorInvalidValue;
@@ -183,11 +186,11 @@ cudaError_t apply_rows(bool x_f64, const double* T, int64_t r, int64_t n, int64_
   if (x_f64) {
     cudaFuncSetAttribute(apply_rows_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     apply_rows_kernel<double><<<grid, kThreads, kSmemBytes, st>>>(T, r, n, ldT, (const double*)X, m, ldX, Y, ldY,
-                                                                  (int)tiles_r, vecT, vecX);
+                                                                  (int)tiles_r, vecT, vecX, lower ? 1 : 0);
   } else {
     cudaFuncSetAttribute(apply_rows_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     apply_rows_kernel<float><<<grid, kThreads, kSmemBytes, st>>>(T, r, n, ldT, (const float*)X, m, ldX, Y, ldY,
-                                                                 (int)tiles_r, vecT, vecX);
+                                                                 (int)tiles_r, vecT, vecX, lower ? 1 : 0);
   }
   if (launches) *launches += 1;
   return cudaGetLastError();

@@ -151,7 +151,7 @@ cudaError_t herm_extract(const double* Y, const double* w2, int64_t n, double to
 
 // ---- apply.cu: Y (r x m, fp64) = T (r x n, fp64) X (n x m, fp32/fp64 row-major), fp64 tensor cores ----
 cudaError_t apply_rows(bool x_f64, const double* T, int64_t r, int64_t n, int64_t ldT, const void* X, int64_t m,
-                       int64_t ldX, double* Y, int64_t ldY, cudaStream_t st, int* launches);
+                       int64_t ldX, double* Y, int64_t ldY, cudaStream_t st, int* launches, bool lower = false);
 
 // ---- svd.cu: the direct-SVD route's n x n pieces ----
 // Linv = L^-1 (lower, row-major ldo; upper zeroed); scratch: n*n doubles

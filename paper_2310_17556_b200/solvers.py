@@ -380,9 +380,10 @@ def _gram_packed_unshifted(S: ScoreMatrix, precision: str) -> torch.Tensor:
     return out
 
 
-def _apply_rows(T: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
+def _apply_rows(T: torch.Tensor, X: torch.Tensor, lower: bool = False) -> torch.Tensor:
     """Y = T X on the device (fs_apply_rows, fp64 tensor cores): T r x n fp64, X n x m (a real
-    score-layout matrix, fp32 or fp64, unit column stride) -> Y r x m fp64, 16-byte aligned rows."""
+    score-layout matrix, fp32 or fp64, unit column stride) -> Y r x m fp64, 16-byte aligned rows.
+    lower: T is lower triangular (fs_apply_rows_lower skips its zero upper part)."""
     r, n = int(T.shape[0]), int(T.shape[1])
     m = int(X.shape[1])
     T = T.to(torch.float64).contiguous()
@@ -390,8 +391,9 @@ def _apply_rows(T: torch.Tensor, X: torch.Tensor) -> torch.Tensor:
     Y = torch.empty((r, ldy), dtype=torch.float64, device=X.device)[:, :m]
     ctx = _lib.context_for(X.device.index, n, m)
     ldT = T.stride(0) if r > 1 else n          # a 1-row tensor may carry any row stride
-    rc = ctx.lib.fs_apply_rows(ctx.handle, _dt(X), T.data_ptr(), r, n, ldT, X.data_ptr(), m, X.stride(0),
-                               Y.data_ptr(), Y.stride(0), _stream(X.device))
+    fn = ctx.lib.fs_apply_rows_lower if lower else ctx.lib.fs_apply_rows
+    rc = fn(ctx.handle, _dt(X), T.data_ptr(), r, n, ldT, X.data_ptr(), m, X.stride(0), Y.data_ptr(), Y.stride(0),
+            _stream(X.device))
     _check(ctx, rc, "fs_apply_rows")
     return Y
 
@@ -778,7 +780,7 @@ def _svda_core(S: ScoreMatrix, Gp: torch.Tensor | None = None):
     if L is None:
         raise FactorizationError("SVD did not converge: the shifted CholeskyQR Gram is not positive definite")
     Lacc = L
-    Qt = _apply_rows(_tri_inverse(L), X)
+    Qt = _apply_rows(_tri_inverse(L), X, lower=True)
     deficient = False
     for _ in range(2):
         Gq = gram_packed(ScoreMatrix._owned(Qt), 0.0, "fp64")
@@ -789,8 +791,8 @@ def _svda_core(S: ScoreMatrix, Gp: torch.Tensor | None = None):
             Lk = _potrf_device(Gq, n, 11.0 * (m * n + n * (n + 1)) * U64 * max(q2, 1.0))
             if Lk is None:
                 raise FactorizationError("SVD did not converge: CholeskyQR breakdown")
-        Lacc = _apply_rows(Lacc, Lk)
-        Qt = _apply_rows(_tri_inverse(Lk), Qt)
+        Lacc = _apply_rows(Lacc, Lk, lower=True)   # a product of lower triangular factors
+        Qt = _apply_rows(_tri_inverse(Lk), Qt, lower=True)
     sigma, W, Zt = _jacobi_svd(Lacc)
     sg = sigma.cpu().numpy()
     cut = np.sqrt(float(n) * m) * U64 * sg[0] if deficient else 0.0

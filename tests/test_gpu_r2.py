@@ -317,6 +317,21 @@ def test_apply_rows_matches_numpy(fsb, r, n, m, dt):
     assert np.abs(Y - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()) * np.sqrt(n)
 
 
+@pytest.mark.parametrize("n,m", [(1, 5), (100, 1000), (129, 4097), (300, 20000), (1024, 3000)])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_apply_rows_lower_skips_only_zeros(fsb, n, m, dt):
+    """fs_apply_rows_lower (each row tile stops its contraction at its last row) equals the dense
+    product with the same lower-triangular T, up to the sign of zero."""
+    from paper_2310_17556_b200.solvers import _apply_rows
+    rng = np.random.Generator(np.random.PCG64(n * 3 + m))
+    T = np.tril(rng.standard_normal((n, n)))
+    sm = fsb.ScoreMatrix(rng.standard_normal((n, m)).astype(dt))
+    Tt = torch.from_numpy(T).cuda()
+    Yl = _apply_rows(Tt, sm.tensor, lower=True).cpu().numpy()
+    Yd = _apply_rows(Tt, sm.tensor).cpu().numpy()
+    assert np.array_equal(Yl, Yd)
+
+
 @pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 300, 1024])
 def test_tri_inverse_and_jacobi_svd(fsb, n):
     from paper_2310_17556_b200.solvers import _jacobi_svd, _tri_inverse
