@@ -78,32 +78,38 @@ FS_DEVINL void grid_sync(unsigned* count, unsigned& target) {
 
 // B: np x np (rows = columns of the input A; padding rows zero), Vt: np x np (identity at the
 // start).  Each round rotates the np/2 disjoint row pairs (p, q) of the round-robin schedule, one
-// warp per pair: alpha = |b_p|^2, beta = |b_q|^2, gamma = b_p . b_q; when |gamma| > tol
-// sqrt(alpha beta) the Rutishauser rotation orthogonalises them (rows p, q of Vt get the same
-// rotation).  A sweep with no rotation ends the iteration.  ctl: [count, gen, rotations(sweep
-// parity 0/1)]; info: [sweeps, not converged].
+// TEAM of tw warps per pair (tw = 1, 2, 4 or 8 so that the teams cover the pairs): each warp
+// forms its segment's alpha = |b_p|^2, beta = |b_q|^2, gamma = b_p . b_q, the team adds the
+// segments in fixed order through shared memory (one named barrier), and when |gamma| > tol
+// sqrt(alpha beta) every warp applies the Rutishauser rotation to its segment of rows p, q of B
+// and of Vt.  (One warp per pair left a round L2-latency bound: 32 dependent load steps per lane;
+// four warps per pair at n = 1024 give 8, with 128 instead of 32 CTAs.)  A sweep with no rotation
+// ends the iteration.  ctl: [count, gen, rotations(sweep parity 0/1)]; info: [sweeps, not
+// converged].
 __global__ void __launch_bounds__(kSThreads, 1)
 jacobi_svd_kernel(double* __restrict__ B, double* __restrict__ Vt, int np, int max_sweeps, double tol, unsigned* ctl,
-                  int* info) {
+                  int* info, int tw) {
+  __shared__ double part[2][kSThreads / 32][3];          // [round parity][warp][a, b, g]
   const int half = np / 2, np1 = np - 1;
-  const int lane = threadIdx.x & 31;
-  const int warps_total = gridDim.x * (kSThreads / 32);
-  const int gw = blockIdx.x * (kSThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int teams_total = gridDim.x * (kSThreads / 32) / tw;
+  const int team = (blockIdx.x * (kSThreads / 32) + warp) / tw, w_in = warp % tw;
+  const int team0 = warp - w_in;                         // the team's first warp in this CTA
   unsigned* rotations = ctl + 2;
   unsigned bar_target = 0;
-  int sweep = 0;
+  int sweep = 0, par = 0;
   bool converged = false;
   for (; sweep < max_sweeps && !converged; ++sweep) {
     unsigned* cnt = rotations + (sweep & 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) rotations[(sweep + 1) & 1] = 0u;   // next sweep's counter
     for (int r = 0; r < np1; ++r) {
-      for (int k = gw; k < half; k += warps_total) {
+      for (int k = team; k < half; k += teams_total) {
         int p, q;
         round_pair(r, k, np1, p, q);
         double* bp = B + (int64_t)p * np;
         double* bq = B + (int64_t)q * np;
         double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < np; i += 32) {
+        for (int i = w_in * 32 + lane; i < np; i += 32 * tw) {
           const double x = bp[i], y = bq[i];
           a = fma(x, x, a);
           b = fma(y, y, b);
@@ -112,23 +118,34 @@ jacobi_svd_kernel(double* __restrict__ B, double* __restrict__ Vt, int np, int m
         a = warp_sum(a);
         b = warp_sum(b);
         g = warp_sum(g);
+        if (tw > 1) {
+          if (lane == 0) { part[par][warp][0] = a; part[par][warp][1] = b; part[par][warp][2] = g; }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + team0 / tw), "r"(32 * tw) : "memory");
+          a = b = g = 0.0;
+          for (int w = 0; w < tw; ++w) {                 // fixed order: identical in every warp
+            a += part[par][team0 + w][0];
+            b += part[par][team0 + w][1];
+            g += part[par][team0 + w][2];
+          }
+          par ^= 1;   // the next pair's partials go to the other buffer (no second barrier)
+        }
         if (fabs(g) > tol * sqrt(a * b) && g != 0.0) {
           const double zeta = (b - a) / (2.0 * g);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = lane; i < np; i += 32) {
+          for (int i = w_in * 32 + lane; i < np; i += 32 * tw) {
             const double x = bp[i], y = bq[i];
             bp[i] = c * x - s * y;
             bq[i] = s * x + c * y;
           }
           double* vp = Vt + (int64_t)p * np;
           double* vq = Vt + (int64_t)q * np;
-          for (int i = lane; i < np; i += 32) {
+          for (int i = w_in * 32 + lane; i < np; i += 32 * tw) {
             const double x = vp[i], y = vq[i];
             vp[i] = c * x - s * y;
             vq[i] = s * x + c * y;
           }
-          if (lane == 0) atomicAdd(cnt, 1u);
+          if (lane == 0 && w_in == 0) atomicAdd(cnt, 1u);
         }
       }
       grid_sync(ctl, bar_target);
@@ -243,10 +260,14 @@ cudaError_t jacobi_svd(const double* A, int64_t n, int64_t lda, double* sigma, d
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_svd_kernel, kSThreads, 0);
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  // a handful of CTAs for small n (every pair gets a warp; fewer CTAs make the barrier cheaper)
-  const int want = std::max(1, std::min(num_sms, (np / 2 + kSThreads / 32 - 1) / (kSThreads / 32)));
+  // warps per pair: the largest of 8, 4, 2, 1 whose teams still fit on the SMs (each pair gets a
+  // team; a small n keeps few CTAs, which makes the grid barrier cheaper)
+  const int wpc = kSThreads / 32;
+  int tw = 8;
+  while (tw > 1 && (int64_t)(np / 2) * tw > (int64_t)num_sms * wpc) tw >>= 1;
+  const int want = std::max(1, std::min(num_sms, (int)(((int64_t)(np / 2) * tw + wpc - 1) / wpc)));
   int npi = np;
-  void* args[] = {&B, &Vt, &npi, &max_sweeps, &tol, &ctl, &d_info};
+  void* args[] = {&B, &Vt, &npi, &max_sweeps, &tol, &ctl, &d_info, &tw};
   e = cudaLaunchCooperativeKernel((const void*)jacobi_svd_kernel, dim3(want), dim3(kSThreads), args, 0, st);
   if (e != cudaSuccess) return e;
   row_norms_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(B, np, (int)n, sraw);
