@@ -543,3 +543,33 @@ def test_eigh_gram_above_8192(fsb):
     assert (G @ U - U * w).norm().item() <= 1e-11 * scale * np.sqrt(n)
     assert (U.T @ U - torch.eye(n, device="cuda", dtype=torch.float64)).norm().item() <= 1e-10 * np.sqrt(n)
     assert abs(w.sum().item() - torch.trace(G).item()) <= 1e-11 * abs(torch.trace(G).item())
+
+
+def test_deferred_host_system_refines_like_the_device_path(fsb):
+    """The host entry (ScoreMatrix(..., defer=True): column chunks streamed and overlapped with
+    the Gram) runs the same z-space refinement as the device path: rel_residual at the
+    reference's level and x equal to the device solve's to 1e-12."""
+    S32, v32, lam = fp32_system(12, 768, 300000)
+    dev = torch.device("cuda", 0)
+    host = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(S32, defer=True), lam, v32))
+    devs = fsb.solve_chol(fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam,
+                                           torch.from_numpy(v32).to(dev)))
+    assert host.rel_residual <= 1e-10 and devs.rel_residual <= 1e-10, (host.rel_residual, devs.rel_residual)
+    assert O.rel_err(np.asarray(host.x), devs.x.cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", ["f16x2", "tf32x3"])
+def test_eigh_refinement_small_lambda_floored(fsb, prec):
+    """Small damping with a floor that drops part of the spectrum: the refined split route agrees
+    with the reference's fp64 truncated route."""
+    rng = np.random.Generator(np.random.PCG64(44))
+    n, m = 96, 20000
+    scales = np.logspace(0, -6, n)[:, None]
+    S32 = (rng.standard_normal((n, m)) * scales).astype(np.float32)
+    v32 = rng.standard_normal(m).astype(np.float32)
+    lam, floor = 1e-6, 1e-4
+    ref = O.solve_svd_eigh(S32.astype(np.float64), v32.astype(np.float64), lam, floor)
+    dev = torch.device("cuda", 0)
+    system = fsb.DampedSystem(fsb.ScoreMatrix(torch.from_numpy(S32).to(dev)), lam, torch.from_numpy(v32).to(dev))
+    sol = fsb.solve_svd_eigh(system, floor, precision=prec)
+    assert O.rel_err(sol.x.cpu().numpy(), ref.x) <= 1e-6, O.rel_err(sol.x.cpu().numpy(), ref.x)
