@@ -19,6 +19,17 @@ FS_DEVINL double warp_sum(double v) {
   return v;
 }
 
+// N independent warp sums, interleaved: five rounds of N independent shuffles instead of N
+// dependent five-shuffle chains (the same xor order per value: bit-identical to warp_sum).  On
+// the TRSV's critical path 8 chained sums cost ~1 us per block.
+template <int N>
+FS_DEVINL void warp_sum_n(double (&v)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
+
 // Streaming (read-once) loads: keep S out of L1, (L2 evict hints need 256-bit vectors).
 FS_DEVINL float4 ld_stream(const float4* p) {
   float4 r;

@@ -100,6 +100,31 @@ trsv_pair_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const doub
 constexpr int kFT = 256;                       // threads per CTA (8 warps)
 constexpr int kFW = kFT / 32;
 
+// The 8 rows' warp sums as a reduce-scatter butterfly: xor 16 / 8 / 4 each halve the values a
+// lane carries (it keeps the half its partner sends), xor 2 / 1 finish the single value.  9
+// fp64 shuffles per warp instead of 40 (the shuffle unit, not the latency, bounded the
+// interleaved sums: ~0.7 us per block on the TRSV's critical path).  Lane l ends with the sum of
+// row 4 ((l >> 4) & 1) + 2 ((l >> 3) & 1) + ((l >> 2) & 1).
+FS_DEVINL double reduce_scatter8(const double (&v)[8], int lane) {
+  const bool b4 = lane & 16, b2 = lane & 8, b1 = lane & 4;
+  double h[4], q[2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double send = b4 ? v[j] : v[j + 4], keep = b4 ? v[j + 4] : v[j];
+    h[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double send = b2 ? h[j] : h[j + 2], keep = b2 ? h[j + 2] : h[j];
+    q[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double r = (b1 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, b1 ? q[0] : q[1], 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+
+
 FS_DEVINL int ld_acq(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -119,6 +144,26 @@ FS_DEVINL void wait_flag(const int* p) {
 }
 
 constexpr int kSP = kNB + 1;                   // smem pitch (doubles) of the preloaded 64 x 64 blocks
+
+// z = Linv^T t (column c, rows c+q, c+q+4, ...): all 16 shared loads issued before the FMA chain
+// (a data-dependent trip count kept each FMA waiting on its own loads; backward link 0.7 -> 0.5
+// us).  The FMA order is the loop's: bit-identical.  (The forward z' = Linv t keeps its loop:
+// unrolled, its 16 row loads per thread doubled the conflicting shared-memory traffic.)
+FS_DEVINL double lcol_dot(const double* LI, const double* t, int c, int q) {
+  double lv[16], tv[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int r = min(c + q + 4 * k, kNB - 1);
+    lv[k] = LI[r * kSP + c];
+    tv[k] = t[r];
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (c + q + 4 * k < kNB) sum = fma(lv[k], tv[k], sum);
+  return sum;
+}
+
 constexpr size_t kFlagSmem = 3 * (size_t)kNB * kSP * sizeof(double);
 
 __global__ void __launch_bounds__(kFT, 1)
@@ -191,11 +236,11 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
       acc[i] = fma(LP[r * kSP + lane + 32], z1, acc[i]);
     }
   }
-#pragma unroll
-  for (int i = 0; i < kNB / kFW; ++i) {
-    const double sum = warp_sum(acc[i]);
-    const int r = warp + kFW * i;
-    if (lane == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
+  static_assert(kNB / kFW == 8, "the butterfly reduces 8 rows per warp");
+  {
+    const double sum = reduce_scatter8(acc, lane);
+    const int r = warp + kFW * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
+    if ((lane & 3) == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
   }
   __syncthreads();
   {                                            // z'_B = Linv_BB t  (4 threads per row)
@@ -247,8 +292,7 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   __syncthreads();
   {                                            // z_B = Linv_BB^T t
     const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
-    double sum = 0.0;
-    for (int r = c + q; r < kNB; r += 4) sum = fma(LI[r * kSP + c], t[r], sum);
+    double sum = lcol_dot(LI, t, c, q);
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     if (q == 0 && c < b) z[r0 + c] = sum;
@@ -274,6 +318,8 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
 }
 
 __device__ unsigned long long g_trsv_t[kCMaxNb][4];   // FS_TRSV_DBG: per block fwd arrive/push, bwd arrive/push
+__device__ unsigned long long g_trsv_t2[kCMaxNb][3];  // FS_TRSV_DBG=2: t formed, z' formed, first push issued
+__device__ unsigned long long g_trsv_w[kCMaxNb][16];  // FS_TRSV_DBG=2: per-warp ready / sums done
 
 __global__ void __launch_bounds__(kFT, 1)
 trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
@@ -362,23 +408,29 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
       }
     }
     if (dbg && threadIdx.x == 0) g_trsv_t[B][0] = fs::ptx::globaltimer();
-#pragma unroll
-    for (int i = 0; i < kNB / kFW; ++i) {
-      const double sum = warp_sum(acc[i]);
-      const int r = warp + kFW * i;
-      if (lane == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
+    if ((dbg & 2) && lane == 0) g_trsv_w[B][warp] = fs::ptx::globaltimer() + (acc[0] == 1.2345 ? 1 : 0);
+    {
+      const double sum = reduce_scatter8(acc, lane);
+      const int r = warp + kFW * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
+      if ((lane & 3) == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
     }
+    if ((dbg & 2) && lane == 0) g_trsv_w[B][8 + warp] = fs::ptx::globaltimer();
     __syncthreads();
+    if ((dbg & 2) && threadIdx.x == 0) g_trsv_t2[B][0] = fs::ptx::globaltimer();
     {                                           // z'_B = Linv_BB t, kept locally and pushed to B+1..
       const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
       double sum = 0.0;
       for (int c = q; c <= r; c += 4) sum = fma(LI[r * kSP + c], t[c], sum);
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      if ((dbg & 2) && threadIdx.x == 0) g_trsv_t2[B][1] = fs::ptx::globaltimer() + (sum == 1.2345 ? 1 : 0);
       if (q == 0) {
         const double zr = r < b ? sum : 0.0;
         zf[B * kNB + r] = zr;
-        for (int d = B + 1; d < nb; ++d) push(zf, fbar, B, d, zr, r);
+        for (int d = B + 1; d < nb; ++d) {
+          push(zf, fbar, B, d, zr, r);
+          if ((dbg & 2) && threadIdx.x == 0 && d == B + 1) g_trsv_t2[B][2] = fs::ptx::globaltimer();
+        }
       }
     }
     __syncthreads();
@@ -418,8 +470,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
     __syncthreads();
     {                                           // z_B = Linv_BB^T t -> z, pushed to 0..B-1
       const int c = threadIdx.x >> 2, q = threadIdx.x & 3;
-      double sum = 0.0;
-      for (int r = c + q; r < kNB; r += 4) sum = fma(LI[r * kSP + c], t[r], sum);
+      double sum = lcol_dot(LI, t, c, q);
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
       if (q == 0) {
@@ -478,9 +529,20 @@ cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Lin
             cudaStreamSynchronize(st);
             cudaMemcpyFromSymbol(h, g_trsv_t, sizeof h);
             const unsigned long long t0 = h[0][0];
-            for (int B = 0; B < (int)nb; ++B)
+            unsigned long long h2[kCMaxNb][3] = {};
+            if (dbg & 2) cudaMemcpyFromSymbol(h2, g_trsv_t2, sizeof h2);
+            for (int B = 0; B < (int)nb; ++B) {
               fprintf(stderr, "trsv block %2d: fwd ready %6.2f pushed %6.2f | bwd ready %6.2f pushed %6.2f us\n", B,
                       (h[B][0] - t0) * 1e-3, (h[B][1] - t0) * 1e-3, (h[B][2] - t0) * 1e-3, (h[B][3] - t0) * 1e-3);
+              if (dbg & 2) {
+                unsigned long long hw[kCMaxNb][16] = {};
+                cudaMemcpyFromSymbol(hw, g_trsv_w, sizeof hw);
+                fprintf(stderr, "   t formed %6.2f, z' formed %6.2f, first push %6.2f us; warps ready/summed:", (h2[B][0] - t0) * 1e-3,
+                        (h2[B][1] - t0) * 1e-3, h2[B][2] ? (h2[B][2] - t0) * 1e-3 : 0.0);
+                for (int w = 0; w < 8; ++w) fprintf(stderr, " %.2f/%.2f", (hw[B][w] - t0) * 1e-3, (hw[B][8 + w] - t0) * 1e-3);
+                fprintf(stderr, "\n");
+              }
+            }
           }
           return cudaGetLastError();
         }
