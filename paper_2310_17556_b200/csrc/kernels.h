@@ -122,6 +122,10 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
                         bool* solved = nullptr);
 cudaError_t invert_diag_blocks(const double* L, int64_t n, int64_t ldL, double* scratch, cudaStream_t st,
                                int* launches);
+// potrf's fused TRSVs: the backward half on the TRSV cluster (from potrf's forward result t)
+bool trsv_cluster_ok(int64_t n);
+cudaError_t trsv_backward_cluster(const double* L, int64_t n, int64_t ldL, const double* Linv, const double* t,
+                                  double* z, const int64_t* d_status, cudaStream_t st, int* launches);
 cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
                       const int64_t* d_status, cudaStream_t st, int* launches);
 

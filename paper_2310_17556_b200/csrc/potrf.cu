@@ -826,7 +826,7 @@ __device__ void grid_barrier(unsigned* count, unsigned& target) {
 __global__ void __launch_bounds__(kThreads, 1)
 potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* panel0, double* panel1,
                         int64_t* status, unsigned* ctl, const double* __restrict__ u, double* ut, double* tb,
-                        double* __restrict__ z) {
+                        double* __restrict__ z, int skip_bwd) {
   extern __shared__ double dsm[];
   unsigned bar_target = 0;
   double (*P)[kLd] = reinterpret_cast<double (*)[kLd]>(dsm + 3 * kNB * kLd);   // CTA 0: Linv_kk
@@ -939,6 +939,7 @@ potrf_persistent_kernel(double* W, int64_t n, int64_t ld, double* Linv, double* 
     if ((threadIdx.x & 3) == 0 && kc + o < n) tb[kc + o] = acc;
   }
   POTRF_MARK(71);
+  if (skip_bwd) return;   // the backward half runs on the TRSV cluster from tb (trsv_backward_cluster)
   grid_barrier(ctl, bar_target);                             // tb = t complete, W holds all of L
   POTRF_MARK(72);
   // backward solve L^T z = t, left-looking per block with release/acquire flags instead of a grid
@@ -1281,10 +1282,15 @@ cudaError_t potrf_lower(double* W, int64_t n, int64_t ldW, int64_t* d_status, do
       int64_t nn = n, ldd = ldW;
       double* ut = panel1 + n * kNB + 1;                 // after the barrier words
       double* tb = ut + n;
-      void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl, &u, &ut, &tb, &z};
+      // the backward solve: inside the kernel (flag-chained over CTAs, ~48 us at n = 1024) or,
+      // when the TRSV cluster fits (n <= 1024), as its backward half (~15 us over DSMEM)
+      static const int bwd_env = getenv("FS_POTRF_CLUSTER_BWD") ? atoi(getenv("FS_POTRF_CLUSTER_BWD")) : 1;
+      int skip_bwd = (u && bwd_env && trsv_cluster_ok(n)) ? 1 : 0;
+      void* args[] = {&W, &nn, &ldd, &Linv, &panel0, &panel1, &d_status, &ctl, &u, &ut, &tb, &z, &skip_bwd};
       e = cudaLaunchCooperativeKernel((const void*)potrf_persistent_kernel, dim3(g), dim3(kThreads), args,
                                       4 * kTileSmem, st);
       if (launches) *launches += 1;
+      if (e == cudaSuccess && skip_bwd) e = trsv_backward_cluster(W, n, ldW, Linv, tb, z, d_status, st, launches);
       if (solved && u && e == cudaSuccess) *solved = true;
       return e;
     }

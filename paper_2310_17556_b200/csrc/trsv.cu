@@ -186,7 +186,7 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   for (int e = threadIdx.x; e < kNB * kNB; e += kFT) {
     const int r = e >> 6, c = e & 63;
     LI[r * kSP + c] = Linv[(size_t)B * kNB * kNB + e];
-    LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
+    LP[r * kSP + c] = (B > 0 && r < b && !tfwd) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;   // forward only
     LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
   }
   if (threadIdx.x < kNB) ub[threadIdx.x] = threadIdx.x < b ? z[r0 + threadIdx.x] : 0.0;   // u_B, off the chain
@@ -323,7 +323,8 @@ __device__ unsigned long long g_trsv_w[kCMaxNb][16];  // FS_TRSV_DBG=2: per-warp
 
 __global__ void __launch_bounds__(kFT, 1)
 trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
-                         double* __restrict__ z, const int64_t* status, int dbg) {
+                         double* __restrict__ z, const int64_t* status, int dbg, const double* __restrict__ tfwd) {
+  // tfwd != nullptr: backward solve only, L^T z = tfwd (the forward half already ran inside potrf)
   extern __shared__ double csm[];
   double* LI = csm;
   double* LP = LI + kNB * kSP;
@@ -364,7 +365,11 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
     const uint32_t br = fs::ptx::mapa(fs::ptx::smem_u32(&bars[slot]), (uint32_t)dst);
     st_async_f64(a, val, br);
   };
-  if (!stop) {
+  if (!stop && tfwd) {
+    if (threadIdx.x < kNB) zf[B * kNB + threadIdx.x] = threadIdx.x < b ? tfwd[r0 + threadIdx.x] : 0.0;
+    __syncthreads();
+  }
+  if (!stop && !tfwd) {
     // ---------------- forward ----------------
     double acc[kNB / kFW];
 #pragma unroll
@@ -435,6 +440,8 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
     }
     __syncthreads();
     if (dbg && threadIdx.x == 0) g_trsv_t[B][1] = fs::ptx::globaltimer();
+  }
+  if (!stop) {
     // ---------------- backward ----------------
     double a0 = 0.0, a1 = 0.0;
     for (int C = nb - 1; C > B; --C) {
@@ -484,14 +491,14 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
   fs::ptx::cluster_sync();                      // no CTA leaves while a peer may still push to it
 }
 
-}  // namespace
 
-cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
-                      const int64_t* d_status, cudaStream_t st, int* launches) {
+// The pair on one thread-block cluster of nb CTAs (nb <= 16; non-portable above 8), or
+// cudaErrorNotSupported when that cluster cannot be used (the caller falls back).  tfwd: the
+// backward half only, from the forward result tfwd.
+cudaError_t launch_cluster(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
+                           const int64_t* d_status, cudaStream_t st, int* launches, const double* tfwd) {
   const int64_t nb = (n + kNB - 1) / kNB;
-  static const int env = getenv("FS_TRSV_FLAGS") ? atoi(getenv("FS_TRSV_FLAGS")) : 1;
-  static const int cl_env = getenv("FS_TRSV_CLUSTER") ? atoi(getenv("FS_TRSV_CLUSTER")) : 1;
-  if (env && cl_env && nb >= 2 && nb <= kCMaxNb) {
+  if (nb >= 2 && nb <= kCMaxNb) {
     // one cluster of nb CTAs (non-portable above 8); the launch reports when the GPU cannot
     // schedule that cluster size, and the flag-chained kernel below takes over
     static int attr = -1;
@@ -521,7 +528,7 @@ cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Lin
       if (cudaOccupancyMaxActiveClusters(&ok_clusters, trsv_pair_cluster_kernel, &cfg) == cudaSuccess &&
           ok_clusters >= 1) {
         static const int dbg = getenv("FS_TRSV_DBG") ? atoi(getenv("FS_TRSV_DBG")) : 0;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status, dbg);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status, dbg, tfwd);
         if (e == cudaSuccess) {
           if (launches) *launches += 1;
           if (dbg) {
@@ -549,6 +556,62 @@ cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Lin
       }
       cudaGetLastError();
     }
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// Whether the cluster kernel can run the pair (or its backward half) for this n: nb in [2, 16],
+// the attributes set and a cluster of nb CTAs schedulable.  Cached per nb.
+bool trsv_cluster_ok(int64_t n) {
+  static const int cl_env = getenv("FS_TRSV_CLUSTER") ? atoi(getenv("FS_TRSV_CLUSTER")) : 1;
+  static int ok[kCMaxNb + 1] = {};                 // 0 unknown, 1 yes, -1 no
+  const int64_t nb = (n + kNB - 1) / kNB;
+  if (!cl_env || nb < 2 || nb > kCMaxNb) return false;
+  if (ok[nb] == 0) {
+    bool good = cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kClusterSmem) == cudaSuccess &&
+                cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                    cudaSuccess;
+    if (good) {
+      cudaLaunchConfig_t cfg;
+      memset(&cfg, 0, sizeof cfg);
+      cfg.gridDim = dim3((unsigned)nb);
+      cfg.blockDim = dim3(kFT);
+      cfg.dynamicSmemBytes = kClusterSmem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)nb;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      good = cudaOccupancyMaxActiveClusters(&clusters, trsv_pair_cluster_kernel, &cfg) == cudaSuccess && clusters >= 1;
+    }
+    cudaGetLastError();
+    ok[nb] = good ? 1 : -1;
+  }
+  return ok[nb] == 1;
+}
+
+// The backward half on the cluster from the forward result t (potrf's fused forward solve):
+// z = L^-T t.  Call only when trsv_cluster_ok(n).
+cudaError_t trsv_backward_cluster(const double* L, int64_t n, int64_t ldL, const double* Linv, const double* t,
+                                  double* z, const int64_t* d_status, cudaStream_t st, int* launches) {
+  if (!trsv_cluster_ok(n)) return cudaErrorNotSupported;
+  return launch_cluster(L, n, ldL, Linv, z, d_status, st, launches, t);
+}
+
+cudaError_t trsv_pair(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
+                      const int64_t* d_status, cudaStream_t st, int* launches) {
+  const int64_t nb = (n + kNB - 1) / kNB;
+  static const int env = getenv("FS_TRSV_FLAGS") ? atoi(getenv("FS_TRSV_FLAGS")) : 1;
+  static const int cl_env = getenv("FS_TRSV_CLUSTER") ? atoi(getenv("FS_TRSV_CLUSTER")) : 1;
+  if (env && cl_env) {
+    const cudaError_t e = launch_cluster(L, n, ldL, Linv, z, d_status, st, launches, nullptr);
+    if (e != cudaErrorNotSupported) return e;
   }
   // every block's CTA must be resident while earlier ones spin on its flags: nb <= (CTAs per SM)
   // x SMs (2 per SM: ~100 KB of shared memory each; n <= 18944 on 148 SMs).  Linv is the potrf

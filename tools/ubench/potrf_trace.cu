@@ -2,7 +2,8 @@
 // the time CTA 0 spends on its tiles (tile 0 = next diagonal block + its factorisation, the critical
 // path) and waiting in the grid barrier, then the forward/backward TRSV barriers.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -Iinclude \
-//        -o potrf_trace tools/ubench/potrf_trace.cu paper_2310_17556_b200/csrc/syrk_dmma.cu
+//        -o potrf_trace tools/ubench/potrf_trace.cu paper_2310_17556_b200/csrc/syrk_dmma.cu \
+//        paper_2310_17556_b200/csrc/trsv.cu
 // Round-2 final build, n = 1024: 16.4 us per block step (panel loads 1.6, two 64^3 DMMA GEMMs
 // 4.5, chol_inv64 8.2, L / Linv stores 1.7), grid barrier ~1.1 us, backward solve 48 us.
 #define FS_POTRF_TRACE 1
