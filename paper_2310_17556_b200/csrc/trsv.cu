@@ -186,7 +186,7 @@ trsv_pair_flag_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const
   for (int e = threadIdx.x; e < kNB * kNB; e += kFT) {
     const int r = e >> 6, c = e & 63;
     LI[r * kSP + c] = Linv[(size_t)B * kNB * kNB + e];
-    LP[r * kSP + c] = (B > 0 && r < b && !tfwd) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;   // forward only
+    LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
     LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
   }
   if (threadIdx.x < kNB) ub[threadIdx.x] = threadIdx.x < b ? z[r0 + threadIdx.x] : 0.0;   // u_B, off the chain
@@ -355,7 +355,7 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
   for (int e = threadIdx.x; e < kNB * kNB; e += kFT) {
     const int r = e >> 6, c = e & 63;
     LI[r * kSP + c] = Linv[(size_t)B * kNB * kNB + e];
-    LP[r * kSP + c] = (B > 0 && r < b) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;
+    LP[r * kSP + c] = (B > 0 && r < b && !tfwd) ? L[(r0 + r) * ld + r0 - kNB + c] : 0.0;   // forward only
     LN[r * kSP + c] = (r < bn && c < b) ? L[(r0 + kNB + r) * ld + r0 + c] : 0.0;
   }
   if (threadIdx.x < kNB) ub[threadIdx.x] = threadIdx.x < b ? z[r0 + threadIdx.x] : 0.0;   // u_B, off the chain
