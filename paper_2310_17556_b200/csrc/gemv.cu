@@ -16,7 +16,6 @@
 #include "tiles.cuh"
 
 #include <algorithm>
-#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -515,12 +514,6 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
 }
 FS_DEVINL void bar_arrive_n(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 
-// FS_CY_DBG=1: per-CTA clock64 split of the pass (x group warp 0: waiting for data / computing /
-// at its barrier; y group first warp: waiting for the exchange / for data / computing; the
-// producer: waiting for a free slot-set)
-__device__ int g_cy_dbg;
-__device__ unsigned long long g_cy_t[296][8];
-
 template <typename TS, typename TV, int NCH, int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCLThreads, 1)
 cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int64_t m, const double* __restrict__ z,
@@ -551,8 +544,6 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
   uint64_t* xbar = empty + kCLSets;                                // [kCLXB]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)ptx::cluster_ctarank();
-  const int dbg = g_cy_dbg;
-  long long tp_wait = 0, tx_wait = 0, tx_work = 0, tx_bar = 0, ty_xwait = 0, ty_dwait = 0, ty_work = 0;
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int64_t row0 = (int64_t)rank * RPC;
   const int64_t panels = (m + CW - 1) / CW;
@@ -572,11 +563,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
       int set = 0;
       uint32_t use = 0;                            // completed passes over the ring
       for (int64_t j = 0; j < np; ++j) {
-        if (use > 0) {
-          const long long c0 = dbg ? clock64() : 0;
-          ptx::mbar_wait(&empty[set], (use - 1) & 1);
-          if (dbg) tp_wait += clock64() - c0;
-        }
+        if (use > 0) ptx::mbar_wait(&empty[set], (use - 1) & 1);
         const int32_t col = (int32_t)((cid + j * ncl) * CW);
         ptx::mbar_arrive_expect_tx(&full[set], kSetBytes);
 #pragma unroll
@@ -616,9 +603,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
       Zt acc[VN1];
 #pragma unroll
       for (int e = 0; e < VN1; ++e) acc[e] = 0;
-      long long c0 = (dbg && warp == 0) ? clock64() : 0;
       ptx::mbar_wait(&full[setx], phx);
-      if (dbg && warp == 0) { const long long c1 = clock64(); tx_wait += c1 - c0; c0 = c1; }
       const unsigned char* src = ring + (size_t)setx * kSetBytes + off;
 #pragma unroll
       for (int k = 0; k < NCH; ++k) {
@@ -646,9 +631,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         d += __shfl_xor_sync(0xffffffffu, d, 16);
         if (lane < 16) rw[vq * VN1 + e] = d;
       }
-      if (dbg && warp == 0) { const long long c1 = clock64(); tx_work += c1 - c0; c0 = c1; }
       ptx::named_bar_sync(1, kCLXThreads);         // red[rb] holds panel j's per-warp partials
-      if (dbg && warp == 0) { const long long c1 = clock64(); tx_bar += c1 - c0; }
       if (tid < CW) {                              // warps 0-1 push them to every CTA
         double part = 0.0;
 #pragma unroll
@@ -705,9 +688,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
           xv = vc;
         } else {
           const int xb = (int)(p % kCLXB);
-          const long long c0 = (dbg && ty == 0) ? clock64() : 0;
           ptx::mbar_wait(&xbar[xb], (uint32_t)((p / kCLXB) & 1));
-          if (dbg && ty == 0) ty_xwait += clock64() - c0;
           double sum = 0.0;
 #pragma unroll
           for (int r = 0; r < CL; ++r) sum += xch[(xb * CL + r) * 64 + ty];
@@ -725,9 +706,7 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
       double xv[VN1];
 #pragma unroll
       for (int e = 0; e < VN1; ++e) xv[e] = xs[b * 64 + vq * VN1 + e];
-      long long cy0 = (dbg && ty == 0) ? clock64() : 0;
       ptx::mbar_wait(&full[sety], phy);            // (already complete: makes the TMA data visible here)
-      if (dbg && ty == 0) { const long long c1 = clock64(); ty_dwait += c1 - cy0; cy0 = c1; }
       const unsigned char* src = ring + (size_t)sety * kSetBytes + off;
 #pragma unroll
       for (int k0 = 0; k0 < NCH; k0 += kCLG) {
@@ -750,7 +729,6 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
             }
       }
       __syncwarp();                                // the whole warp has consumed the slot-set
-      if (dbg && ty == 0) ty_work += clock64() - cy0;
       if (lane == 0) ptx::mbar_arrive(&empty[sety]);
       if (++sety == R) { sety = 0; phy ^= 1; }
     }
@@ -768,14 +746,6 @@ cols_solve_y_cl_kernel(const __grid_constant__ CUtensorMap smap, int64_t n, int6
         if (rp < RP && vq == 0 && row < n) ypart[cid * n + row] = t;
       }
   }
-  if (dbg && blockIdx.x < 296) {
-    if (warp == kCLCW && lane == 0) g_cy_t[blockIdx.x][0] = tp_wait;
-    if (warp == 0 && lane == 0) { g_cy_t[blockIdx.x][1] = tx_wait; g_cy_t[blockIdx.x][2] = tx_work; g_cy_t[blockIdx.x][3] = tx_bar; }
-    if (tid == kCLXThreads) {
-      g_cy_t[blockIdx.x][4] = ty_xwait; g_cy_t[blockIdx.x][5] = ty_dwait; g_cy_t[blockIdx.x][6] = ty_work;
-      g_cy_t[blockIdx.x][7] = (unsigned long long)np;
-    }
-  }
   ptx::cluster_sync();                             // no CTA leaves while a peer may still signal it
 }
 
@@ -783,26 +753,10 @@ template <typename TS, typename TV, int CL>
 cudaError_t launch_cols_solve_y_cl(int nch, unsigned grid, cudaStream_t st, const CUtensorMap& smap, int64_t n,
                                    int64_t m, const double* z, const TV* v, double lam, int acc, double* x,
                                    double* ypart, int y_only) {
-  static const int dbg = getenv("FS_CY_DBG") ? atoi(getenv("FS_CY_DBG")) : 0;
-  static bool dbg_set = false;
-  if (!dbg_set) { cudaMemcpyToSymbol(g_cy_dbg, &dbg, sizeof dbg); dbg_set = true; }
   auto pick = [&](auto kfn) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL));
     if (CL > 8) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     kfn<<<grid, kCLThreads, cl_smem(CL), st>>>(smap, n, m, z, v, lam, acc, x, ypart, y_only);
-    if (dbg) {
-      unsigned long long h[296][8] = {};
-      cudaStreamSynchronize(st);
-      cudaMemcpyFromSymbol(h, g_cy_t, sizeof h);
-      double a[8] = {};
-      int c = 0;
-      for (unsigned i = 0; i < grid && i < 296; ++i) { for (int k = 0; k < 8; ++k) a[k] += (double)h[i][k]; ++c; }
-      if (c) {
-        for (int k = 0; k < 8; ++k) a[k] /= c;
-        fprintf(stderr, "x+y pass (per CTA, %.0f panels, cycles/panel): producer waits slot %.0f | x: data %.0f work %.0f barrier %.0f | y: exchange %.0f data %.0f work %.0f\n",
-                a[7], a[0] / a[7], a[1] / a[7], a[2] / a[7], a[3] / a[7], a[4] / a[7], a[5] / a[7], a[6] / a[7]);
-      }
-    }
   };
   switch (nch) {
     case 3: pick(cols_solve_y_cl_kernel<TS, TV, 3, CL>); break;
