@@ -268,9 +268,7 @@ FS_DEVINL void load_pair_block(const double* __restrict__ M, int np, int I1, int
 
 // FS_SYEVJ_DBG: CTA 0's %globaltimer split of the rounds (phase A, barrier, phase B, barrier), ns
 __device__ unsigned long long g_bj_time[4];
-// FS_SYEVJ_DBG bit 2: CTA 0 warp 0's clock64 split of the inner rounds (loads + rotation, shuffles
-// + updates + stores, barrier), cycles, and the inner-round count
-__device__ unsigned long long g_bj_ir[4];
+
 
 __global__ void __launch_bounds__(kBThreads, 1)
 bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restrict__ U, double* __restrict__ Vt,
@@ -331,7 +329,6 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
       __syncthreads();
     }
   };
-  long long ir_t[4] = {0, 0, 0, 0};
   int nround = 0, prev_r = 0;                        // rounds done (all sweeps), the last one's index
   // a round's U blocks [0, ndefer) are applied during the NEXT round's phase A by the CTAs the
   // inner sweeps leave idle (ten each at most: about one inner sweep's time), the rest in its phase B
@@ -373,7 +370,6 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
           if (full) pair_of_round(ir, k, kSB - 1, p, qq);
           else { p = k; qq = kBB + ((k + ir) & (kBB - 1)); }
         };
-        const bool tir = (dbg & 2) && blockIdx.x == 0 && warp == 0;
         // cross rounds: V in registers.  Lane k holds, for rows warp + 8 i, column k (the I half,
         // fixed) and column 32 + ((k + ir) mod 32) (the J half: its pair partner this round); after
         // the round the J column moves one lane down (shuffle), so V never touches shared memory
@@ -387,14 +383,9 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
           vJ[i] = row == kBB + lane ? 1.0 : 0.0;
         }
         for (int ir = 0; ir < (full ? kSB - 1 : kBB); ++ir) {
-          long long c0 = tir ? clock64() : 0;
           int pk, qk;
           inner_pair(ir, lane, pk, qk);
           const Rot Rk = schur2_fast(M[pk * kMP + pk], M[qk * kMP + qk], M[pk * kMP + qk]);
-          if (tir) {   // make the rotation's completion visible to the clock
-            const long long c1 = clock64() + (Rk.c + Rk.s == 12345.0 ? 1 : 0);
-            ir_t[0] += c1 - c0; c0 = c1;
-          }
           // M' = J^T M J by 2 x 2 blocks (k1 = warp + 8 i, k2 = lane), and V <- V J (columns pk,
           // qk of rows warp + 8 i; each (row, pair) by one thread).  All shared loads of the round
           // are issued before any store: M / M2 swap every round and V is updated in place, so the
@@ -450,9 +441,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
               vJ[i] = __shfl_sync(0xffffffffu, Rk.s * a + Rk.c * b, (lane + 1) & 31);
             }
           }
-          if (tir) { const long long c1 = clock64(); ir_t[1] += c1 - c0; c0 = c1; }
           __syncthreads();
-          if (tir) { ir_t[2] += clock64() - c0; ir_t[3] += 1; }
           double* tmp = M; M = M2; M2 = tmp;
         }
         if (!full) {   // the register V (every J column back at lane k) -> shared
@@ -534,10 +523,7 @@ bjacobi_kernel(double* __restrict__ A0, double* __restrict__ A1, double* __restr
   }
   if (dbg && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == (unsigned)q)) {
     const int o = blockIdx.x == 0 ? 0 : 2;
-    if (o == 0) {
-      g_bj_time[0] = tA; g_bj_time[1] = tB1 + tB2; g_bj_time[2] = tB;
-      for (int k = 0; k < 4; ++k) g_bj_ir[k] = (unsigned long long)ir_t[k];
-    }
+    if (o == 0) { g_bj_time[0] = tA; g_bj_time[1] = tB1 + tB2; g_bj_time[2] = tB; }
     else g_bj_time[3] = tA;
   }
   for (int i = blockIdx.x * kBThreads + threadIdx.x; i < np; i += gridDim.x * kBThreads)
@@ -702,12 +688,6 @@ cudaError_t syevj(const double* Gp, int64_t n, double* w, double* U, int64_t ldu
       cudaMemcpyFromSymbol(h, g_bj_time, sizeof h);
       fprintf(stderr, "bjacobi CTA 0: phase A %.2f ms, barriers %.2f ms, phase B %.2f ms; CTA q (U work) %.2f ms\n",
               h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6);
-      if (dbg & 2) {
-        cudaMemcpyFromSymbol(h, g_bj_ir, sizeof h);
-        const double k = h[3] ? (double)h[3] : 1.0;
-        fprintf(stderr, "bjacobi inner rounds %llu: rotation %.0f, updates %.0f, barrier %.0f cycles each\n", h[3],
-                h[0] / k, h[1] / k, h[2] / k);
-      }
     }
     return cudaGetLastError();
   }

@@ -318,8 +318,6 @@ FS_DEVINL void st_async_f64(uint32_t addr, double v, uint32_t bar) {
 }
 
 __device__ unsigned long long g_trsv_t[kCMaxNb][4];   // FS_TRSV_DBG: per block fwd arrive/push, bwd arrive/push
-__device__ unsigned long long g_trsv_t2[kCMaxNb][3];  // FS_TRSV_DBG=2: t formed, z' formed, first push issued
-__device__ unsigned long long g_trsv_w[kCMaxNb][16];  // FS_TRSV_DBG=2: per-warp ready / sums done
 
 __global__ void __launch_bounds__(kFT, 1)
 trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, const double* __restrict__ Linv,
@@ -413,29 +411,22 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
       }
     }
     if (dbg && threadIdx.x == 0) g_trsv_t[B][0] = fs::ptx::globaltimer();
-    if ((dbg & 2) && lane == 0) g_trsv_w[B][warp] = fs::ptx::globaltimer() + (acc[0] == 1.2345 ? 1 : 0);
     {
       const double sum = reduce_scatter8(acc, lane);
       const int r = warp + kFW * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
       if ((lane & 3) == 0) t[r] = (r < b) ? ub[r] - sum : 0.0;
     }
-    if ((dbg & 2) && lane == 0) g_trsv_w[B][8 + warp] = fs::ptx::globaltimer();
     __syncthreads();
-    if ((dbg & 2) && threadIdx.x == 0) g_trsv_t2[B][0] = fs::ptx::globaltimer();
     {                                           // z'_B = Linv_BB t, kept locally and pushed to B+1..
       const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
       double sum = 0.0;
       for (int c = q; c <= r; c += 4) sum = fma(LI[r * kSP + c], t[c], sum);
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      if ((dbg & 2) && threadIdx.x == 0) g_trsv_t2[B][1] = fs::ptx::globaltimer() + (sum == 1.2345 ? 1 : 0);
       if (q == 0) {
         const double zr = r < b ? sum : 0.0;
         zf[B * kNB + r] = zr;
-        for (int d = B + 1; d < nb; ++d) {
-          push(zf, fbar, B, d, zr, r);
-          if ((dbg & 2) && threadIdx.x == 0 && d == B + 1) g_trsv_t2[B][2] = fs::ptx::globaltimer();
-        }
+        for (int d = B + 1; d < nb; ++d) push(zf, fbar, B, d, zr, r);
       }
     }
     __syncthreads();
@@ -536,20 +527,9 @@ cudaError_t launch_cluster(const double* L, int64_t n, int64_t ldL, const double
             cudaStreamSynchronize(st);
             cudaMemcpyFromSymbol(h, g_trsv_t, sizeof h);
             const unsigned long long t0 = h[0][0];
-            unsigned long long h2[kCMaxNb][3] = {};
-            if (dbg & 2) cudaMemcpyFromSymbol(h2, g_trsv_t2, sizeof h2);
-            for (int B = 0; B < (int)nb; ++B) {
+            for (int B = 0; B < (int)nb; ++B)
               fprintf(stderr, "trsv block %2d: fwd ready %6.2f pushed %6.2f | bwd ready %6.2f pushed %6.2f us\n", B,
                       (h[B][0] - t0) * 1e-3, (h[B][1] - t0) * 1e-3, (h[B][2] - t0) * 1e-3, (h[B][3] - t0) * 1e-3);
-              if (dbg & 2) {
-                unsigned long long hw[kCMaxNb][16] = {};
-                cudaMemcpyFromSymbol(hw, g_trsv_w, sizeof hw);
-                fprintf(stderr, "   t formed %6.2f, z' formed %6.2f, first push %6.2f us; warps ready/summed:", (h2[B][0] - t0) * 1e-3,
-                        (h2[B][1] - t0) * 1e-3, h2[B][2] ? (h2[B][2] - t0) * 1e-3 : 0.0);
-                for (int w = 0; w < 8; ++w) fprintf(stderr, " %.2f/%.2f", (hw[B][w] - t0) * 1e-3, (hw[B][8 + w] - t0) * 1e-3);
-                fprintf(stderr, "\n");
-              }
-            }
           }
           return cudaGetLastError();
         }
