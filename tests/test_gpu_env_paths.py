@@ -6,6 +6,7 @@ process, because the switches are read once per process):
   FS_F16_RING=1   the F16X2 ring SYRK (each tile split once into an L2-resident ring)
   FS_TRSV_FLAGS=0 the single-CTA TRSV pair instead of the flag-chained one
   FS_DZ_ASYNC=0   the refinement's convergence test through a stream sync instead of a side stream
+  FS_POTRF_CLUSTER_BWD=0  potrf's own backward solve instead of the TRSV cluster's backward half
 
 Tolerances: fp32 modes relerr(x) <= 1e-6 vs the reference's fp64 solve of the same
 fp32-rounded system; the chunked Gram vs the one-shot Gram <= 2e-6 of max |G| (the same split
@@ -107,6 +108,19 @@ def test_refinement_step_decisions_sync_or_side_stream_bit_identical(gpu, tmp_pa
     x1, _, i1 = run_case(tmp_path, {}, n, m, "f16x2", refine=4)
     x2, _, i2 = run_case(tmp_path, {"FS_DZ_ASYNC": "0"}, n, m, "f16x2", refine=4)
     assert np.array_equal(x1, x2) and i1["rel_residual"] == i2["rel_residual"] <= 1e-10
+
+
+@pytest.mark.parametrize("n", [130, 700, 1024, 1100])
+def test_potrf_backward_on_the_trsv_cluster(gpu, tmp_path, n):
+    """n <= 1024: potrf's fused backward solve runs as the TRSV cluster's backward half
+    (FS_POTRF_CLUSTER_BWD=0: inside the persistent kernel); n = 1100 keeps the in-kernel solve.
+    The same z up to rounding order: x to the fp64 solve's 1e-10 either way."""
+    m = 40000
+    ref = reference(n, m)
+    for env in ({}, {"FS_POTRF_CLUSTER_BWD": "0"}):
+        x, _, info = run_case(tmp_path, env, n, m, "f16x2", refine=2)
+        assert O.rel_err(x, ref.x) <= 1e-10, (env, O.rel_err(x, ref.x))
+        assert info["rel_residual"] <= 1e-10
 
 
 @pytest.mark.parametrize("n", [130, 1000])
