@@ -483,61 +483,47 @@ trsv_pair_cluster_kernel(const double* __restrict__ L, int64_t n, int64_t ld, co
 }
 
 
+}  // namespace
+bool trsv_cluster_ok(int64_t n);
+namespace {
+
 // The pair on one thread-block cluster of nb CTAs (nb <= 16; non-portable above 8), or
 // cudaErrorNotSupported when that cluster cannot be used (the caller falls back).  tfwd: the
 // backward half only, from the forward result tfwd.
 cudaError_t launch_cluster(const double* L, int64_t n, int64_t ldL, const double* Linv, double* z,
                            const int64_t* d_status, cudaStream_t st, int* launches, const double* tfwd) {
+  if (!trsv_cluster_ok(n)) return cudaErrorNotSupported;   // attributes + schedulability, cached per nb
   const int64_t nb = (n + kNB - 1) / kNB;
-  if (nb >= 2 && nb <= kCMaxNb) {
-    // one cluster of nb CTAs (non-portable above 8); the launch reports when the GPU cannot
-    // schedule that cluster size, and the flag-chained kernel below takes over
-    static int attr = -1;
-    if (attr < 0) {
-      attr = cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kClusterSmem) == cudaSuccess &&
-                     cudaFuncSetAttribute(trsv_pair_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                          1) == cudaSuccess
-                 ? 1 : 0;
-      cudaGetLastError();
-    }
-    if (attr == 1) {
-      cudaLaunchConfig_t cfg;
-      memset(&cfg, 0, sizeof cfg);
-      cfg.gridDim = dim3((unsigned)nb);
-      cfg.blockDim = dim3(kFT);
-      cfg.dynamicSmemBytes = kClusterSmem;
-      cfg.stream = st;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = (unsigned)nb;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int ok_clusters = 0;
-      if (cudaOccupancyMaxActiveClusters(&ok_clusters, trsv_pair_cluster_kernel, &cfg) == cudaSuccess &&
-          ok_clusters >= 1) {
-        static const int dbg = getenv("FS_TRSV_DBG") ? atoi(getenv("FS_TRSV_DBG")) : 0;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status, dbg, tfwd);
-        if (e == cudaSuccess) {
-          if (launches) *launches += 1;
-          if (dbg) {
-            unsigned long long h[kCMaxNb][4] = {};
-            cudaStreamSynchronize(st);
-            cudaMemcpyFromSymbol(h, g_trsv_t, sizeof h);
-            const unsigned long long t0 = h[0][0];
-            for (int B = 0; B < (int)nb; ++B)
-              fprintf(stderr, "trsv block %2d: fwd ready %6.2f pushed %6.2f | bwd ready %6.2f pushed %6.2f us\n", B,
-                      (h[B][0] - t0) * 1e-3, (h[B][1] - t0) * 1e-3, (h[B][2] - t0) * 1e-3, (h[B][3] - t0) * 1e-3);
-          }
-          return cudaGetLastError();
-        }
-      }
-      cudaGetLastError();
-    }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3(kFT);
+  cfg.dynamicSmemBytes = kClusterSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)nb;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static const int dbg = getenv("FS_TRSV_DBG") ? atoi(getenv("FS_TRSV_DBG")) : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, trsv_pair_cluster_kernel, L, n, ldL, Linv, z, d_status, dbg, tfwd);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cudaErrorNotSupported;
   }
-  return cudaErrorNotSupported;
+  if (launches) *launches += 1;
+  if (dbg) {
+    unsigned long long h[kCMaxNb][4] = {};
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_trsv_t, sizeof h);
+    const unsigned long long t0 = h[0][0];
+    for (int B = 0; B < (int)nb; ++B)
+      fprintf(stderr, "trsv block %2d: fwd ready %6.2f pushed %6.2f | bwd ready %6.2f pushed %6.2f us\n", B,
+              (h[B][0] - t0) * 1e-3, (h[B][1] - t0) * 1e-3, (h[B][2] - t0) * 1e-3, (h[B][3] - t0) * 1e-3);
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace
